@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the fused sample + CC hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Metric: fused sample+CC edge-sims/s.  One converged sample + CC of all R
+simulations counts 2m*R edge-sims (2m directed slots, R lanes) -- the work of
+one full sweep of the dense model.  `value` is that
+rate with the CSR and X resident in HBM (device-timed with CUDA events on the
+library's stream, L2 flushed by a 256 MB write before every step);
+`e2e` is the same rate measured through the public API
+(`run_fused(g, K, R)` on a host Graph: CSR upload, hash, propagate, memo,
+CELF for K seeds, results back to the host), and `k_seed_wall_s` is that
+step's wall time (BASELINE's second metric).  `cpu_baseline` is the CPU
+oracle (oracle/, a C/OpenMP restatement of the reference's dense label
+propagation + CELF) timed on this host in the same run.
+
+With --gpus N > 1 (torchrun) the R simulations are split into N lane
+windows; value = all ranks' edge-sims / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def b_es(n, m2, R, per_edge):
+    """Dense fused-sweep bytes per edge-sim."""
+    return 4.0 + 8.0 * n / m2 + (4.0 + 4.0 * per_edge) / R
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = Path("/tmp") / f"imx_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path.exists():
+            return None
+        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r]
+        rows = [r for r in rows if len(r) >= 9]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_baseline(cfg, g_host, R, K, budget_s):
+    """Oracle (C/OpenMP restatement of the reference path) on the host."""
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    xadj, adj, w = g_host.xadj, g_host.adj, g_host.weights
+    hashes = oracle.hash_table(xadj, adj)
+    thr = oracle.thresholds(w, oracle.reciprocal(xadj, adj))
+    uniform = bool((thr == thr[0]).all())
+    t_arg = int(thr[0]) if uniform else thr
+    X = oracle.randoms(R, 0)
+    # size the lane sample to the budget: probe 8 lanes first
+    t0 = time.perf_counter()
+    oracle.propagate(xadj, adj, hashes, t_arg, X[:8], threads)
+    per_lane = max((time.perf_counter() - t0) / 8, 1e-6)
+    lanes = int(min(R, max(8, (budget_s / per_lane) // 8 * 8)))
+    t0 = time.perf_counter()
+    labels, sweeps = oracle.propagate(xadj, adj, hashes, t_arg, X[:lanes], threads)
+    t_prop = time.perf_counter() - t0
+    out = {"value": len(adj) * lanes / t_prop, "unit": "edge-sims/s", "cores": threads, "kind": "port",
+           "sample": f"{cfg} lanes 0..{lanes} of {R} (oracle dense propagation, "
+                     f"{sweeps} sweeps, {t_prop:.2f} s)"}
+    if lanes == R:
+        t0 = time.perf_counter()
+        sizes, gains = oracle.sizes_gains(labels, R, threads)
+        oracle.celf(labels, sizes, gains, K, R)
+        out["k_seed_wall_s"] = t_prop + (time.perf_counter() - t0)
+    return out
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle (the reference path restated in C)
+    on the host cores, same config/metric; rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_2008_03095_b200 import configs
+    oracle.build()
+    c = configs.CONFIGS[args.config]
+    edges = configs.edges(args.config)
+    from paper_2008_03095_b200.weights import parse_weight_scheme
+    xadj, adj, _ = oracle.csr_from_edges(c.n, edges)
+    scheme = parse_weight_scheme(c.weights)
+    if hasattr(scheme, "p"):
+        w = np.full(len(adj), scheme.p)
+    else:  # per-edge normal draws in canonical-slot order (graph.py:251-259)
+        src = oracle.sources(xadj)
+        canon = np.flatnonzero(src < adj)
+        rec = oracle.reciprocal(xadj, adj)
+        draws = np.clip(np.random.default_rng(c.seed).normal(scheme.mean, scheme.std,
+                                                              size=len(canon)), 0, 1)
+        w = np.empty(len(adj))
+        w[canon] = draws
+        w[rec[canon]] = draws
+    threads = os.cpu_count() or 1
+    hashes = oracle.hash_table(xadj, adj)
+    thr = oracle.thresholds(w, oracle.reciprocal(xadj, adj))
+    uniform = bool((thr == thr[0]).all())
+    t_arg = int(thr[0]) if uniform else thr
+    X = oracle.randoms(c.R, 0)
+    t0 = time.perf_counter()
+    oracle.propagate(xadj, adj, hashes, t_arg, X[:8], threads)
+    per_lane = max((time.perf_counter() - t0) / 8, 1e-6)
+    per_step = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    lanes = int(min(c.R, max(8, (per_step / per_lane) // 8 * 8)))
+    Xs = X[:lanes]
+    prop, tot = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        labels, sweeps = oracle.propagate(xadj, adj, hashes, t_arg, Xs, threads)
+        t1 = time.perf_counter()
+        sizes, gains = oracle.sizes_gains(labels, lanes, threads)
+        oracle.celf(labels, sizes, gains, c.K, lanes)
+        t2 = time.perf_counter()
+        if i >= args.warmup:
+            prop.append(t1 - t0)
+            tot.append(t2 - t0)
+    units = len(adj) * lanes
+    value = units / float(np.mean(prop))
+    sample = (f"{args.config} lanes 0..{lanes} of {c.R} per step (oracle: dense min-label "
+              f"propagation to fixpoint in {sweeps} sweeps + sizes/gains + CELF heap, "
+              f"{threads} OpenMP threads)")
+    line = {
+        "impl": "reference", "metric": "fused sample+CC edge-sims/sec (2m*R per converged sample+CC)",
+        "value": value, "unit": "edge-sims/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(prop)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": c.description, "n": c.n, "m2": int(len(adj)), "R": c.R,
+                   "K": c.K, "lanes_per_step": lanes},
+        "cpu_baseline": {"value": value, "unit": "edge-sims/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": units / float(np.mean(tot)), "unit": "edge-sims/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "k_seed_wall_s": float(np.mean(tot)) * c.R / lanes},
+        "sweeps": int(sweeps),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import paper_2008_03095_b200 as imx
+    from paper_2008_03095_b200 import _lib, configs
+    from paper_2008_03095_b200.celf import lane_window
+    from paper_2008_03095_b200.context import DeviceContext
+    imx.set_device(local)
+    c = configs.CONFIGS[args.config]
+    t0 = time.perf_counter()
+    edges = configs.edges(args.config)
+    g = configs.build(args.config, edges)
+    t_build = time.perf_counter() - t0
+    n, m2, R, K = g.n, g.m, c.R, c.K
+    X = imx.SimulationRandoms(R, 0).values
+    a, b, scored = lane_window(len(X), R, rank, world)
+    W = b - a
+    table = imx.build_hash_table(g)
+    table.bind(g)
+    ctx = DeviceContext(g, X[a:b], scored, a)
+    thr = imx.slot_thresholds(g)
+    per_edge = 0 if (thr == thr[0]).all() else 1
+    lib = _lib.load()
+
+    # ---- value: fused sample + CC, inputs resident, L2 flushed per step ----
+    ctx.bench_propagate(args.warmup, flush_l2=True)
+    barrier(world)
+    launches0 = lib.imx_launch_count()
+    with Clocks(local) as clk:
+        res = ctx.bench_propagate(args.steps, flush_l2=True)
+    launches = lib.imx_launch_count() - launches0
+    barrier(world)
+    ms = allreduce_max(res["total_ms"], world)
+    units_total = m2 * R                     # all ranks: 2m * R per converged step
+    value = units_total / (ms / 1e3)
+    per_gpu = m2 * W / (res["total_ms"] / 1e3)
+    peak, peak_src = peaks()
+    bes = b_es(n, m2, R, per_edge)
+    achieved = per_gpu * bes / 1e9
+    kern = {k: res[k] for k in ("init_ms", "hook_ms", "compress_ms")}
+    dominant = max(kern, key=kern.get)
+    prof = ROOT / "profiles" / f"ncu_{args.config}_summary.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_propagate")
+        except Exception:
+            traffic = None
+
+    # ---- correctness guard on the measured context ----
+    ctx.propagate(verify=True)
+
+    # ---- e2e: public API with host buffers ----
+    host = imx.Graph(g.xadj, g.adj, g.weights, g.orig_ids)
+    e2e_steps = args.e2e_steps or args.steps
+    times, d2h = [], 0
+    for i in range(args.warmup + e2e_steps):
+        gi = imx.Graph(host.xadj, host.adj, host.weights, host.orig_ids)
+        barrier(world)
+        t0 = time.perf_counter()
+        run = imx.run_fused(gi, K, num_simulations=R, master_seed=0)
+        seeds, spread = list(run.seeds), run.spread
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(allreduce_max(dt, world))
+            d2h = 4 * K + 8 * K + 40 * len(run.selection.trace)
+        del run
+    e2e_s = float(np.mean(times))
+    h2d = 8 * (n + 1) + 4 * m2 + 8 * m2 + 4 * len(X)
+
+    line = {
+        "metric": "fused sample+CC edge-sims/sec (2m*R per converged sample+CC)",
+        "value": value, "unit": "edge-sims/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded generator, graph_seed=weight_seed=config#, master_seed=0)",
+        "config": {"workload": c.description, "n": n, "m2": m2, "R": R, "K": K,
+                   "lanes_per_gpu": W, "l2": "flushed (256 MB write) before every step",
+                   "parallelism": f"R-sharded x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "propagate = k_init + k_hook + k_compress (one converged sample+CC)",
+                     "model": f"B_es={bes:.3f} B/edge-sim dense-sweep model (SURVEY 8(d)) x 2m*R_gpu",
+                     "peak_source": peak_src, "dominant_kernel": dominant,
+                     "kernel_ms": kern},
+        "e2e": {"value": units_total / e2e_s, "unit": "edge-sims/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "k_seed_wall_s": e2e_s, "seeds_head": seeds[:5], "spread": spread},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "graph_build_s": t_build,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, host, R, K, args.cpu_budget_s)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,195 @@
+/*
+ * infuser_b200.h -- C ABI of libinfuser_b200.so, the sm_100a hot path of
+ * InFuseR-MG (fused hash-sampled IC simulation -> per-simulation connected
+ * components -> memoized component-size gains -> CELF seed selection).
+ *
+ * The reference (`infmax`, pure Python/numpy, /root/reference/pkg/src/infmax)
+ * has no FFI.  Each entry point below replaces one reference routine; the
+ * citation after each declaration names the routine (file:line, relative to
+ * pkg/src/infmax/) whose semantics it reproduces bit for bit.  The Python
+ * package paper_2008_03095_b200 binds these symbols with ctypes
+ * (see INTEGRATION.md for the binding a reference maintainer would add).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Every pointer argument is HOST memory,
+ *     borrowed for the duration of the call, unless the name ends in _dev.
+ *   - Return 0 on success, a negative IMX_E* code on failure; the message is
+ *     available from imx_last_error() (thread-local).
+ *   - Vertex ids and labels are int32 (ids < 2^31, graph.py:22); labels and
+ *     sizes are [n][width] int32, simulation-contiguous (propagation.py:1-8).
+ *   - One context owns one device and one lane window [lane0, lane0+width)
+ *     of the simulation set; multi-GPU runs create one context per rank and
+ *     combine the int64 partial sums (gains, CELF gains) with an allreduce.
+ *   - Every call is synchronous with respect to the host unless noted.
+ */
+#ifndef INFUSER_B200_H
+#define INFUSER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IMX_OK          0
+#define IMX_EINVAL     -1   /* bad argument            -> ValueError          */
+#define IMX_ENOMEM     -2   /* device allocation failed -> MemoryError        */
+#define IMX_ECUDA      -3   /* CUDA runtime error       -> RuntimeError       */
+#define IMX_ENODEV     -4   /* no usable sm_100 device  -> RuntimeError       */
+#define IMX_ECONSTRAINT -5  /* documented limit violated -> ConstraintError   */
+#define IMX_EFORMAT    -6   /* malformed graph          -> GraphFormatError   */
+#define IMX_EINTERNAL  -7   /* failed self-check        -> AssertionError     */
+
+typedef struct imx_graph imx_graph;   /* device-resident symmetric CSR        */
+typedef struct imx_ctx   imx_ctx;     /* device-resident labels/sizes/CELF    */
+
+/* ---- library ----------------------------------------------------------- */
+const char *imx_last_error(void);
+int  imx_version(void);                                   /* 10000*maj+100*min */
+/* number of visible CUDA devices with compute capability 10.x (0 on a CPU box) */
+int  imx_device_count(void);
+/* kernels this library has launched in this process (all contexts)        */
+int64_t imx_launch_count(void);
+
+/* ---- K1: CSR builder ----------------------------------------------------
+ * Graph.from_edges (graph.py:124-155): k distinct undirected edges
+ * (edges[2i], edges[2i+1]) on 0..n-1 -> rows sorted by (src, dst), both
+ * directions share weight w_edge[i] (or w_scalar when w_edge == NULL).
+ * Validation order and messages follow graph.py:134-146.  The graph stays on
+ * the device; imx_graph_get_csr copies xadj/adj/weights back.             */
+int  imx_graph_from_edges(int32_t device, int64_t n, const int64_t *edges,
+                          int64_t k, const double *w_edge, double w_scalar,
+                          imx_graph **out);
+/* Upload an existing CSR (Graph(xadj, adj, weights, orig_ids), graph.py:37). */
+int  imx_graph_from_csr(int32_t device, int64_t n, int64_t m2,
+                        const int64_t *xadj, const int32_t *adj,
+                        const double *weights, imx_graph **out);
+void imx_graph_destroy(imx_graph *g);
+int  imx_graph_dims(const imx_graph *g, int64_t *n, int64_t *m2);
+int  imx_graph_get_csr(imx_graph *g, int64_t *xadj, int32_t *adj, double *weights);
+/* Graph.reciprocal_slots (graph.py:85-99); IMX_EFORMAT if not symmetric.  */
+int  imx_graph_reciprocal(imx_graph *g, int64_t *recip);
+/* Graph.with_weights (graph.py:112-119): replace per-slot weights, then
+ * refresh thresholds.  IMX_ECONSTRAINT if a weight is outside [0, 1].     */
+int  imx_graph_set_weights(imx_graph *g, const double *weights);
+
+/* ---- K2: sampler tables -------------------------------------------------
+ * build_hash_table (hashing.py:97-101): per-slot
+ * murmur3_x86_32(LE32(min) || LE32(max), seed 0) & 0x7FFFFFFF.            */
+int  imx_graph_hashes(imx_graph *g, int32_t *hashes_out);
+/* Use caller-provided per-slot hashes (EdgeHashTable.hashes) instead;
+ * hashes == NULL restores the computed table.                              */
+int  imx_graph_set_hashes(imx_graph *g, const int32_t *hashes);
+/* slot_thresholds (hashing.py:153-165): int32(int64(w * (2^31-1))),
+ * max-symmetrized over reciprocal slots when symmetrize != 0.
+ * *uniform_out (nullable) = 1 when all symmetrized thresholds are equal.  */
+int  imx_graph_thresholds(imx_graph *g, int32_t symmetrize, int32_t *thr_out,
+                          int32_t *uniform_out);
+/* Vectorized murmur3 over (lo[i], hi[i]) 8-byte keys, unmasked
+ * (_murmur3_pair_array, hashing.py:65-86).                                 */
+int  imx_murmur3_pairs(int32_t device, const uint32_t *lo, const uint32_t *hi,
+                       int64_t count, uint32_t *out);
+
+/* ---- context: one lane window on one device ----------------------------- */
+typedef struct {
+    int32_t  sweeps;           /* phases executed (init, hook, compress[, verify]) */
+    int32_t  cap;              /* capacity of the arrays below             */
+    int64_t *changed_pairs;    /* per phase: (vertex, lane) labels changed */
+    int64_t *label_sums;       /* per phase: sum of all labels (int64)     */
+    int32_t *modes;            /* per phase: IMX_MODE_*                    */
+} imx_prop_stats;              /* PropagateStats (propagation.py:49-56)   */
+
+#define IMX_MODE_INIT     0
+#define IMX_MODE_HOOK     1
+#define IMX_MODE_COMPRESS 2
+#define IMX_MODE_VERIFY   3
+
+/* X: the 31-bit per-simulation words of lanes [lane0, lane0+width)
+ * (SimulationRandoms.values, hashing.py:111-119); num_scored: how many of
+ * this window's lanes are scored (the rest are padding).                  */
+int  imx_create(imx_graph *g, const int32_t *X, int32_t width,
+                int32_t num_scored, imx_ctx **out);
+void imx_destroy(imx_ctx *c);
+
+/* K3: fused sample + CC (propagate, propagation.py:260-321): converged
+ * min-id labels of every lane.  verify != 0 adds a checking pass (every live
+ * edge joins equal labels, every label is its own root) whose changed count
+ * must be 0 (otherwise IMX_EINTERNAL).  st may be NULL.                    */
+int  imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st);
+
+/* K4+K5: component_sizes_and_gains (propagation.py:371-390): component
+ * histogram over all lanes, int64 gains over the scored lanes.
+ * gains_out may be NULL (gains stay on the device for CELF).              */
+int  imx_memoize(imx_ctx *c, int64_t *gains_out);
+
+/* Load labels (and optionally sizes; NULL -> recomputed from labels) from
+ * the host instead of propagating: select_seeds / initial_marginal_gains on
+ * caller arrays (selection.py:115, propagation.py:349-368).  ld = row
+ * stride of the host arrays in elements (>= width).                        */
+int  imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t *sizes,
+                     int64_t ld);
+
+/* D2H copies of lanes [r0, r1) of this window into dense [n][r1-r0].      */
+int  imx_copy_labels(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out);
+int  imx_copy_sizes (imx_ctx *c, int32_t r0, int32_t r1, int32_t *out);
+
+/* ---- K6-K8: CELF (selection.py:115-149) ---------------------------------
+ * Round-based exact CELF: device keeps prio (last pushed gain), the seed
+ * set, per-lane covered-component bitmaps and per-lane covered totals.    */
+/* prio: n int64 initial priorities (NULL -> this context's own gains).    */
+int  imx_celf_reset(imx_ctx *c, const int64_t *prio);
+/* max (prio desc, id asc) over non-seeds; *v = -1 when none remain.       */
+int  imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out);
+/* Collect the non-seeds v != exclude whose key (-prio[v], v) is <=
+ * (-g, u), i.e. prio[v] > g or (prio[v] == g and v <= u), into the
+ * context's candidate list; copies ids/prio of up to cap of them out and
+ * reports the total in *count.                                             */
+int  imx_celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude,
+                      int32_t *ids_out, int64_t *prio_out, int64_t cap,
+                      int64_t *count);
+/* marginal_gain (selection.py:63-70) of the collected candidates, partial
+ * over this window's scored lanes.                                         */
+int  imx_celf_eval_collected(imx_ctx *c, int64_t *fresh_out);
+/* marginal_gain of an explicit candidate list.                            */
+int  imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int64_t *out);
+/* prio[ids[i]] = vals[i]                                                   */
+int  imx_celf_set_prio(imx_ctx *c, const int32_t *ids, const int64_t *vals,
+                       int64_t cnt);
+/* commit_seed (selection.py:73-81): own u's component in every scored
+ * lane; *gain_out = partial newly covered total.                          */
+int  imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out);
+/* Whole CELF loop on one context (single-rank fast path): k seeds and their
+ * gains; *trace_len = number of dequeues recorded (fetch with
+ * imx_celf_trace).  Requires imx_celf_reset first.                         */
+int  imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out,
+                     int64_t *gains_out, int64_t *trace_len);
+/* The trace of the last imx_celf_select: records of 5 int64
+ * (vertex, stale_gain, fresh_gain, committed, seeds_before) -- TraceRecord,
+ * selection.py:25-33 -- up to cap records.                                 */
+int  imx_celf_trace(imx_ctx *c, int64_t *out, int64_t cap);
+/* per_sim[r] = covered vertices of lane r (SelectionResult.spread_se,
+ * selection.py:105-112), for this window's scored lanes.                  */
+int  imx_per_sim(imx_ctx *c, int64_t *out);
+/* owned bitmap rows: [n][ceil(num_scored/32)] uint32 (SeedState.owned).  */
+int  imx_copy_owned(imx_ctx *c, uint32_t *bits_out);
+
+/* ---- measurement --------------------------------------------------------
+ * Device time (CUDA events on the context stream) of the last call of each
+ * phase and the number of kernels this context launched so far.           */
+typedef struct {
+    float   propagate_ms, memoize_ms, select_ms;
+    float   init_ms, hook_ms, compress_ms;
+    int64_t kernel_launches;
+    int64_t hook_launches;
+} imx_timings;
+int  imx_get_timings(imx_ctx *c, imx_timings *out);
+/* Run propagate `reps` times back to back (inputs resident) and report the
+ * average device time of the whole propagate and of its dominant kernel.  */
+int  imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2,
+                         float *avg_total_ms, float *avg_hook_ms,
+                         float *avg_compress_ms, float *avg_init_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INFUSER_B200_H */

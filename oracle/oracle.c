@@ -1,0 +1,232 @@
+/*
+ * oracle.c -- CPU restatement of the reference's fused hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in paper_2008_03095_b200/ links, loads
+ * or calls this file; only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs use it, as the checker and as the
+ * timed CPU baseline.
+ *
+ * Every function restates one routine of the reference package
+ * /root/reference/pkg/src/infmax (cited file:line) in plain C, with the
+ * reference's exact integer semantics:
+ *   - murmur3 pair hash, 31-bit mask      hashing.py:65-86, 97-101
+ *   - membership (X[r] ^ h) < thr, strict hashing.py:141-150, propagation.py:170
+ *   - min-label propagation to fixpoint   propagation.py:166-221 (dense pull
+ *     sweeps; the reference's index/sparse sweeps reach the same fixpoint)
+ *   - component sizes and int64 gains     propagation.py:371-390
+ *   - CELF with a (-gain, id) min-heap    selection.py:115-149
+ *
+ * Threads: the lanes are independent samples, so lane blocks are split over
+ * OpenMP threads; each thread runs its own lanes to their fixpoint in place
+ * (Gauss-Seidel order inside a block, like the reference's in-place block
+ * updates).  Results do not depend on the thread count.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static inline uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+
+/* murmur3_x86_32 of LE32(lo) || LE32(hi), seed 0 (hashing.py:65-86) */
+uint32_t oracle_murmur3_pair(uint32_t lo, uint32_t hi) {
+    const uint32_t c1 = 0xCC9E2D51u, c2 = 0x1B873593u;
+    uint32_t h = 0, blocks[2] = {lo, hi};
+    for (int i = 0; i < 2; ++i) {
+        uint32_t k = blocks[i] * c1;
+        k = rotl32(k, 15) * c2;
+        h = rotl32(h ^ k, 13) * 5u + 0xE6546B64u;
+    }
+    h ^= 8u;
+    h ^= h >> 16; h *= 0x85EBCA6Bu;
+    h ^= h >> 13; h *= 0xC2B2AE35u;
+    return h ^ (h >> 16);
+}
+
+/* build_hash_table (hashing.py:97-101): per slot hash of (min, max) & H_MAX */
+void oracle_hash_table(int64_t n, const int64_t *xadj, const int32_t *adj, int32_t *out) {
+    for (int64_t u = 0; u < n; ++u)
+        for (int64_t s = xadj[u]; s < xadj[u + 1]; ++s) {
+            uint32_t a = (uint32_t)u, b = (uint32_t)adj[s];
+            out[s] = (int32_t)(oracle_murmur3_pair(a < b ? a : b, a < b ? b : a) & 0x7FFFFFFFu);
+        }
+}
+
+/* One lane block [r0, r1) of the dense pull propagation, to its fixpoint.
+ * labels is the full (n, W) matrix; returns the number of sweeps run
+ * (including the final no-change sweep). */
+static int propagate_block(int64_t n, const int64_t *xadj, const int32_t *adj,
+                           const int32_t *hashes, const int32_t *thr, int32_t thr_uniform,
+                           int uniform, const int32_t *X, int64_t W, int r0, int r1,
+                           int32_t *labels, int64_t *changed_total) {
+    const int B = r1 - r0;
+    int32_t *best = (int32_t *)malloc(sizeof(int32_t) * (size_t)B);
+    int sweeps = 0;
+    int64_t changed;
+    do {
+        changed = 0;
+        for (int64_t v = 0; v < n; ++v) {
+            const int64_t s0 = xadj[v], s1 = xadj[v + 1];
+            if (s0 == s1) continue;
+            int32_t *lv = labels + v * W + r0;
+            for (int j = 0; j < B; ++j) best[j] = lv[j];
+            for (int64_t s = s0; s < s1; ++s) {
+                const int32_t h = hashes[s];
+                const int32_t t = uniform ? thr_uniform : thr[s];
+                const int32_t *lu = labels + (int64_t)adj[s] * W + r0;
+                const int32_t *x = X + r0;
+                for (int j = 0; j < B; ++j) {
+                    const int live = (x[j] ^ h) < t;            /* strict, signed */
+                    const int32_t c = live ? lu[j] : INT32_MAX;
+                    best[j] = c < best[j] ? c : best[j];
+                }
+            }
+            for (int j = 0; j < B; ++j)
+                if (best[j] < lv[j]) { lv[j] = best[j]; ++changed; }
+        }
+        *changed_total += changed;
+        ++sweeps;
+    } while (changed);
+    free(best);
+    return sweeps;
+}
+
+/* propagate (propagation.py:260-321): labels (n, W) int32 min-id labels.
+ * thr may be NULL when uniform (thr_uniform used).  Returns the max sweep
+ * count over lane blocks; *changed = total label decreases. */
+int oracle_propagate(int64_t n, const int64_t *xadj, const int32_t *adj,
+                     const int32_t *hashes, const int32_t *thr, int32_t thr_uniform,
+                     const int32_t *X, int64_t W, int32_t *labels, int nthreads,
+                     int lane_block, int64_t *changed) {
+    for (int64_t v = 0; v < n; ++v)
+        for (int64_t r = 0; r < W; ++r) labels[v * W + r] = (int32_t)v;
+    if (changed) *changed = 0;
+    if (xadj[n] == 0) return 0;
+    if (lane_block <= 0) lane_block = 64;
+    const int nblocks = (int)((W + lane_block - 1) / lane_block);
+    int max_sweeps = 0;
+    int64_t total = 0;
+    const int uniform = thr == NULL;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : max_sweeps) reduction(+ : total)
+#endif
+    for (int b = 0; b < nblocks; ++b) {
+        int r0 = b * lane_block;
+        int r1 = r0 + lane_block < W ? r0 + lane_block : (int)W;
+        int64_t ch = 0;
+        int sw = propagate_block(n, xadj, adj, hashes, thr, thr_uniform, uniform, X, W, r0, r1,
+                                 labels, &ch);
+        if (sw > max_sweeps) max_sweeps = sw;
+        total += ch;
+    }
+    if (changed) *changed = total;
+    return max_sweeps;
+}
+
+/* component_sizes_and_gains (propagation.py:371-390): sizes (n, W) int32
+ * histogram per lane over all W lanes; gains over lanes < num_scored. */
+void oracle_sizes_gains(int64_t n, int64_t W, const int32_t *labels, int64_t num_scored,
+                        int32_t *sizes, int64_t *gains, int nthreads) {
+    memset(sizes, 0, sizeof(int32_t) * (size_t)(n * W));
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t r = 0; r < W; ++r)
+        for (int64_t v = 0; v < n; ++v) sizes[(int64_t)labels[v * W + r] * W + r] += 1;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t v = 0; v < n; ++v) {
+        int64_t acc = 0;
+        for (int64_t r = 0; r < num_scored; ++r) acc += sizes[(int64_t)labels[v * W + r] * W + r];
+        gains[v] = acc;
+    }
+}
+
+/* ---- CELF (selection.py:115-149) --------------------------------------- */
+typedef struct { int64_t neg; int32_t v; } hkey;
+
+static inline int hless(hkey a, hkey b) { return a.neg < b.neg || (a.neg == b.neg && a.v < b.v); }
+
+static void sift_down(hkey *h, int64_t len, int64_t i) {
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < len && hless(h[l], h[m])) m = l;
+        if (r < len && hless(h[r], h[m])) m = r;
+        if (m == i) return;
+        hkey t = h[i]; h[i] = h[m]; h[m] = t;
+        i = m;
+    }
+}
+static void sift_up(hkey *h, int64_t i) {
+    while (i > 0) {
+        int64_t p = (i - 1) / 2;
+        if (!hless(h[i], h[p])) return;
+        hkey t = h[i]; h[i] = h[p]; h[p] = t;
+        i = p;
+    }
+}
+
+/* marginal_gain (selection.py:63-70) */
+static int64_t celf_gain(int32_t u, int64_t W, const int32_t *labels, const int32_t *sizes,
+                         const uint8_t *owned, int64_t ns) {
+    int64_t acc = 0;
+    for (int64_t r = 0; r < ns; ++r) {
+        int64_t l = labels[(int64_t)u * W + r];
+        if (!owned[l * ns + r]) acc += sizes[l * W + r];
+    }
+    return acc;
+}
+
+/* select_seeds: writes k seeds and gains, the trace (5 int64 per dequeue,
+ * up to trace_cap records), per_sim[ns] covered totals; returns the number of
+ * dequeues, or -1 on bad arguments. */
+int64_t oracle_celf(int64_t n, int64_t W, const int32_t *labels, const int32_t *sizes,
+                    const int64_t *init_gains, int64_t ns, int32_t k, int32_t *seeds_out,
+                    int64_t *gains_out, int64_t *trace, int64_t trace_cap, int64_t *per_sim) {
+    if (k < 1 || k > n || ns > W) return -1;
+    hkey *heap = (hkey *)malloc(sizeof(hkey) * (size_t)n);
+    int64_t *fresh_at = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    uint8_t *owned = (uint8_t *)calloc((size_t)(n * ns), 1);
+    for (int64_t v = 0; v < n; ++v) { heap[v].neg = -init_gains[v]; heap[v].v = (int32_t)v; }
+    int64_t len = n;
+    for (int64_t i = n / 2 - 1; i >= 0; --i) sift_down(heap, len, i);
+    int32_t nseeds = 0;
+    int64_t ntrace = 0;
+    if (per_sim) memset(per_sim, 0, sizeof(int64_t) * (size_t)ns);
+    while (nseeds < k) {
+        hkey top = heap[0];
+        heap[0] = heap[--len];
+        sift_down(heap, len, 0);
+        const int32_t u = top.v;
+        const int64_t stale = -top.neg;
+        int64_t rec[5];
+        if (fresh_at[u] == nseeds) {
+            for (int64_t r = 0; r < ns; ++r) {          /* commit_seed, :73-81 */
+                int64_t l = labels[(int64_t)u * W + r];
+                if (!owned[l * ns + r]) {
+                    owned[l * ns + r] = 1;
+                    if (per_sim) per_sim[r] += sizes[l * W + r];
+                }
+            }
+            seeds_out[nseeds] = u;
+            gains_out[nseeds] = stale;
+            rec[0] = u; rec[1] = stale; rec[2] = stale; rec[3] = 1; rec[4] = nseeds;
+            ++nseeds;
+        } else {
+            int64_t f = celf_gain(u, W, labels, sizes, owned, ns);
+            fresh_at[u] = nseeds;
+            heap[len].neg = -f; heap[len].v = u;
+            sift_up(heap, len++);
+            rec[0] = u; rec[1] = stale; rec[2] = f; rec[3] = 0; rec[4] = nseeds;
+        }
+        if (trace && ntrace < trace_cap) memcpy(trace + 5 * ntrace, rec, sizeof rec);
+        ++ntrace;
+    }
+    free(heap); free(fresh_at); free(owned);
+    return ntrace;
+}

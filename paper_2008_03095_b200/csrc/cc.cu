@@ -1,0 +1,1099 @@
+// cc.cu -- K3 fused sample + CC, K4/K5 memoization, K6-K8 CELF on sm_100a.
+//
+// Data layout in HBM (one context = one device, one lane window of width W):
+//   L[n][ld]  uint32  labels, simulation-contiguous (propagation.py:1-8),
+//                     ld = W rounded up to 4 so every row is 16-byte aligned.
+//   C[n][ld]  uint32  per-root member count EXCLUDING the root; the component
+//                     size of label l in lane r is C[l][r] + 1, and
+//                     sizes[l][r] = C[l][r] + (L[l][r] == l) (propagation.py:349-356).
+//   cov[n][cw] uint32 covered-component bitmap of the CELF state, cw = ceil(ns/32)
+//                     (SeedState.owned, selection.py:36-60).
+//
+// Propagation is concurrent union-find over all W lanes at once, not
+// min-label sweeps: the fixpoint the reference's sweeps reach (min vertex id
+// of the component of every vertex in every lane) is unique, so
+// any exact CC algorithm reproduces it.  Trees always hook the
+// larger root under the smaller one, so a root is the minimum id of its tree.
+//
+//   k_init      L[v][r] = v                                    (streaming write)
+//   k_hook      for every undirected edge {lo,hi} and lane r with
+//               (X[r] ^ h) < thr:  union(lo, hi) in lane r      (sampler fused in)
+//   k_compress  L[v][r] = root(v, r); C[root][r] += 1 for non-roots
+//   k_verify    (optional) every live edge joins equal labels; every label is a root
+#include <algorithm>
+#include <vector>
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "graph.cuh"
+
+struct imx_ctx {
+    imx_graph *g = nullptr;
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    int32_t W = 0, ns = 0, cw = 0;
+    int64_t ld = 0;
+    int vb = 0;                   // bits for vertex ids in packed CELF keys
+    int32_t *X = nullptr;         // [ld]
+    uint32_t *L = nullptr;        // [n*ld]
+    uint32_t *C = nullptr;        // [n*ld]
+    int64_t *gains = nullptr;     // [n]
+    int64_t *prio = nullptr;      // [n]
+    uint8_t *inS = nullptr;       // [n]
+    uint32_t *cov = nullptr;      // [n*cw]
+    int64_t *per_sim = nullptr;   // [W]
+    int32_t *cand = nullptr;      // [n]
+    int64_t *fresh = nullptr;     // [n]
+    unsigned long long *scratch = nullptr;  // [8]
+    int64_t ncand = 0;
+    bool labels_ready = false, memo_ready = false, celf_ready = false;
+    int full_counts = 0;          // 1: C holds full sizes (host-loaded labels)
+    cudaEvent_t ev[8];
+    imx_timings tm{};
+    std::vector<int64_t> trace;   // 5 per record
+};
+
+namespace imx {
+
+// ---------------------------------------------------------------------------
+// union-find primitives (per lane; every lane is an independent graph)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t *cell(uint32_t *L, int64_t ld, uint32_t v, int r) {
+    return L + (int64_t)v * ld + r;
+}
+
+// root of x with path halving; the halving stores are benign races: every
+// value ever stored in a cell is an ancestor (a smaller id in the same tree).
+__device__ __forceinline__ uint32_t find_halve(uint32_t *L, int64_t ld, uint32_t x, int r) {
+    uint32_t p = ld_relaxed(cell(L, ld, x, r));
+    while (p != x) {
+        uint32_t gp = ld_relaxed(cell(L, ld, p, r));
+        if (gp == p) return p;
+        st_relaxed(cell(L, ld, x, r), gp);
+        x = gp;
+        p = ld_relaxed(cell(L, ld, x, r));
+    }
+    return x;
+}
+
+__device__ __forceinline__ uint32_t find_ro(const uint32_t *L, int64_t ld, uint32_t x, int r) {
+    uint32_t p;
+    while ((p = ld_relaxed(L + (int64_t)x * ld + r)) != x) x = p;
+    return x;
+}
+
+// union of a and b in lane r: CAS-hook the larger root under the smaller.
+__device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32_t b, int r) {
+    a = find_halve(L, ld, a, r);
+    b = find_halve(L, ld, b, r);
+    while (a != b) {
+        if (a > b) { uint32_t t = a; a = b; b = t; }
+        uint32_t old = atomicCAS(cell(L, ld, b, r), b, a);
+        if (old == b) return 1;
+        b = find_halve(L, ld, old, r);
+        a = find_halve(L, ld, a, r);
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// K3: init / hook / compress / verify
+// ---------------------------------------------------------------------------
+__global__ void k_init(uint32_t *__restrict__ L, int64_t n, int64_t ld) {
+    const int64_t nq = ld >> 2;
+    uint4 *L4 = reinterpret_cast<uint4 *>(L);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = (uint32_t)(i / nq);
+        L4[i] = make_uint4(v, v, v, v);
+    }
+}
+
+// One warp per undirected edge; each thread owns 4 consecutive lanes of a
+// 128-lane chunk, so the first-level label reads of a live lane group are
+// coalesced 16-byte loads of the two endpoint rows.  The hash and threshold
+// are read once per edge and reused across all W lanes.
+template <bool UNI>
+__global__ void __launch_bounds__(256) k_hook(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
+                                              const int32_t *__restrict__ ET, int32_t tu, int64_t me,
+                                              const int32_t *__restrict__ X, int32_t W, int64_t ld,
+                                              uint32_t *__restrict__ L,
+                                              unsigned long long *__restrict__ hooks) {
+    extern __shared__ int4 sX4[];
+    int32_t *sX = reinterpret_cast<int32_t *>(sX4);
+    for (int i = threadIdx.x; i < ld; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
+    __syncthreads();
+    const int nq = (int)(ld >> 2);
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long nh = 0;
+    for (int64_t e = wg; e < me; e += nw) {
+        const int2 uv = __ldg(&E[e]);
+        const int32_t h = __ldg(&EH[e]);
+        const int32_t t = UNI ? tu : __ldg(&ET[e]);
+        for (int q = lane; q < nq; q += 32) {
+            const int4 x = sX4[q];
+            const int r = q << 2;
+            unsigned live = ((unsigned)((x.x ^ h) < t)) | ((unsigned)((x.y ^ h) < t) << 1) |
+                            ((unsigned)((x.z ^ h) < t) << 2) | ((unsigned)((x.w ^ h) < t) << 3);
+            if (r + 4 > W) live &= (1u << (W > r ? W - r : 0)) - 1u;
+            while (live) {
+                const int j = __ffs(live) - 1;
+                live &= live - 1;
+                nh += unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r + j);
+            }
+        }
+    }
+    if (hooks) {
+        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(0xffffffffu, nh, o);
+        if (lane == 0 && nh) atomicAdd(hooks, nh);
+    }
+}
+
+// Full compression + component histogram.  A warp takes a run of RUN
+// consecutive vertices for 128 lanes; along the run each lane keeps
+// (current root, count) and only flushes an atomicAdd when the root changes,
+// so the hub roots of giant components (label 0 in every lane) receive one
+// atomic per run instead of one per member.
+template <int RUN>
+__global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, uint32_t *__restrict__ C,
+                                                  int64_t n, int64_t ld, int32_t W,
+                                                  unsigned long long *__restrict__ changed) {
+    const int nq = (int)(ld >> 2);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int q = blockIdx.y * 32 + lane;
+    const int64_t v0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * RUN;
+    if (q >= nq || v0 >= n) return;
+    const int r = q << 2;
+    uint32_t cur[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+    uint32_t cnt[4] = {0, 0, 0, 0};
+    unsigned long long nch = 0;
+    const int64_t v1 = min(n, v0 + RUN);
+    for (int64_t v = v0; v < v1; ++v) {
+        uint4 *p = reinterpret_cast<uint4 *>(L + v * ld) + q;
+        uint4 l = *p;
+        uint32_t lv[4] = {l.x, l.y, l.z, l.w};
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (r + j >= W || lv[j] == (uint32_t)v) continue;
+            uint32_t root = find_ro(L, ld, lv[j], r + j);
+            if (root != lv[j]) { lv[j] = root; any = true; ++nch; }
+            if (root == cur[j]) {
+                ++cnt[j];
+            } else {
+                if (cnt[j]) atomicAdd(C + (int64_t)cur[j] * ld + r + j, cnt[j]);
+                cur[j] = root;
+                cnt[j] = 1;
+            }
+        }
+        if (any) *p = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (cnt[j]) atomicAdd(C + (int64_t)cur[j] * ld + r + j, cnt[j]);
+    if (changed && nch) atomicAdd(changed, nch);
+}
+
+// Verification sweep: count live (edge, lane) pairs whose endpoint labels
+// differ and labels that are not roots / exceed their vertex.
+template <bool UNI>
+__global__ void k_verify_edges(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
+                               const int32_t *__restrict__ ET, int32_t tu, int64_t me,
+                               const int32_t *__restrict__ X, int32_t W, int64_t ld,
+                               const uint32_t *__restrict__ L, unsigned long long *__restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long nb = 0;
+    for (int64_t e = wg; e < me; e += nw) {
+        const int2 uv = E[e];
+        const int32_t h = EH[e];
+        const int32_t t = UNI ? tu : ET[e];
+        for (int r = lane; r < W; r += 32)
+            if ((X[r] ^ h) < t && L[(int64_t)uv.x * ld + r] != L[(int64_t)uv.y * ld + r]) ++nb;
+    }
+    for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if (lane == 0 && nb) atomicAdd(bad, nb);
+}
+__global__ void k_verify_roots(const uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
+                               unsigned long long *__restrict__ bad) {
+    unsigned long long nb = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = i / W;
+        int r = (int)(i - v * W);
+        uint32_t l = L[v * ld + r];
+        if (l > (uint32_t)v || L[(int64_t)l * ld + r] != l) ++nb;
+    }
+    for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if ((threadIdx.x & 31) == 0 && nb) atomicAdd(bad, nb);
+}
+
+__global__ void k_label_sum(const uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
+                            unsigned long long *__restrict__ out) {
+    unsigned long long s = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = i / W;
+        int r = (int)(i - v * W);
+        s += L[v * ld + r];
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+// ---------------------------------------------------------------------------
+// K4/K5: gains[v] = sum_{r < ns} size(L[v][r], r)   (propagation.py:359-368)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gains(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                                               int64_t n, int64_t ld, int32_t ns, uint32_t add1,
+                                               int64_t *__restrict__ gains) {
+    const int lane = threadIdx.x & 31;
+    const int nqs = (ns + 3) >> 2;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = wg; v < n; v += nw) {
+        const uint4 *Lr = reinterpret_cast<const uint4 *>(L + v * ld);
+        const uint4 *Cr = reinterpret_cast<const uint4 *>(C + v * ld);
+        unsigned long long acc = 0;
+        for (int q = lane; q < nqs; q += 32) {
+            const uint4 l = __ldg(Lr + q), c = __ldg(Cr + q);
+            const uint32_t lv[4] = {l.x, l.y, l.z, l.w}, cv[4] = {c.x, c.y, c.z, c.w};
+            const int r = q << 2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (r + j >= ns) break;
+                uint32_t cnt = (lv[j] == (uint32_t)v) ? cv[j] : __ldg(C + (int64_t)lv[j] * ld + r + j);
+                acc += cnt + add1;
+            }
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) gains[v] = (int64_t)acc;
+    }
+}
+
+// sizes[v][r] for a lane window (C + own-root indicator)
+__global__ void k_sizes_window(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                               int64_t v0, int64_t cnt, int64_t ld, int32_t r0, int32_t r1,
+                               int full_counts, int32_t *__restrict__ out) {
+    const int w = r1 - r0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt * (int64_t)w;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = v0 + i / w;
+        int r = r0 + (int)(i % w);
+        uint32_t c = C[v * ld + r];
+        out[i] = (int32_t)(c + (!full_counts && L[v * ld + r] == (uint32_t)v ? 1u : 0u));
+    }
+}
+__global__ void k_gather_i64(const int32_t *__restrict__ idx, int64_t cnt,
+                             const int64_t *__restrict__ src, int64_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = src[idx[i]];
+}
+// Host-provided labels may be arbitrary (any int in 0..n-1), so C holds
+// full counts for them (full_counts = 1: size = C[l][r], not C[l][r] + 1).
+__global__ void k_hist_full(const uint32_t *__restrict__ L, uint32_t *__restrict__ C,
+                            int64_t n, int64_t ld, int32_t W, unsigned *__restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = i / W;
+        int r = (int)(i - v * W);
+        uint32_t l = L[v * ld + r];
+        if (l >= (uint32_t)n) { atomicOr(bad, 1u); continue; }
+        atomicAdd(C + (int64_t)l * ld + r, 1u);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6-K8: CELF
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long pack_key(int64_t prio, uint32_t v, int vb) {
+    const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
+    return ((unsigned long long)prio << vb) | (unsigned long long)(vmask - v);
+}
+
+__global__ void k_top(const int64_t *__restrict__ prio, const uint8_t *__restrict__ inS, int64_t n,
+                      int vb, unsigned long long *__restrict__ out) {
+    unsigned long long best = 0;
+    bool have = false;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        if (inS[v]) continue;
+        unsigned long long k = pack_key(prio[v], (uint32_t)v, vb) + 1ull;  // +1: 0 = none
+        if (!have || k > best) { best = k; have = true; }
+    }
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+        best = x > best ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
+__global__ void k_collect(const int64_t *__restrict__ prio, const uint8_t *__restrict__ inS, int64_t n,
+                          int vb, unsigned long long thr_key, int32_t exclude,
+                          int32_t *__restrict__ cand, unsigned long long *__restrict__ count) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        bool take = !inS[v] && v != exclude && pack_key(prio[v], (uint32_t)v, vb) >= thr_key;
+        unsigned m = __ballot_sync(__activemask(), take);
+        if (!m) continue;
+        int leader = __ffs(m) - 1;
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (take) cand[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (int32_t)v;
+    }
+}
+
+// marginal_gain (selection.py:63-70): sum over scored lanes of the component
+// size of L[u][r] when that component is not covered yet.  Warp per candidate.
+__global__ void __launch_bounds__(256) k_eval(const int32_t *__restrict__ cand, int64_t cnt,
+                                              const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                                              const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
+                                              int32_t cw, int full_counts,
+                                              int64_t *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t add1 = full_counts ? 0u : 1u;
+    for (int64_t i = wg; i < cnt; i += nw) {
+        const int64_t u = cand[i];
+        unsigned long long acc = 0;
+        for (int r = lane; r < ns; r += 32) {
+            const uint32_t l = L[u * ld + r];
+            const uint32_t word = cov[(int64_t)l * cw + (r >> 5)];
+            if (!((word >> (r & 31)) & 1u)) acc += C[(int64_t)l * ld + r] + add1;
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[i] = (int64_t)acc;
+    }
+}
+
+// commit_seed (selection.py:73-81)
+__global__ void k_commit(int32_t u, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                         uint32_t *__restrict__ cov, int64_t ld, int32_t ns, int32_t cw,
+                         int full_counts, int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
+                         unsigned long long *__restrict__ gain) {
+    unsigned long long acc = 0;
+    const uint32_t add1 = full_counts ? 0u : 1u;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ns; r += gridDim.x * blockDim.x) {
+        const uint32_t l = L[(int64_t)u * ld + r];
+        const uint32_t bit = 1u << (r & 31);
+        const uint32_t old = atomicOr(cov + (int64_t)l * cw + (r >> 5), bit);
+        if (!(old & bit)) {
+            const uint32_t s = C[(int64_t)l * ld + r] + add1;
+            per_sim[r] += s;
+            acc += s;
+        }
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(gain, acc);
+    if (blockIdx.x == 0 && threadIdx.x == 0) inS[u] = 1;
+}
+
+__global__ void k_set_prio(const int32_t *__restrict__ ids, const int64_t *__restrict__ vals,
+                           int64_t cnt, int64_t *__restrict__ prio) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        prio[ids[i]] = vals[i];
+}
+
+static int grid_for(int64_t work, int threads = 256) {
+    int64_t b = ceil_div(work > 0 ? work : 1, threads);
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+}  // namespace imx
+
+using namespace imx;
+
+// ---------------------------------------------------------------------------
+// context lifecycle
+// ---------------------------------------------------------------------------
+static void ctx_free(imx_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    if (c->st) cudaStreamSynchronize(c->st);
+    void *ptrs[] = {c->X, c->L, c->C, c->gains, c->prio, c->inS, c->cov, c->per_sim,
+                    c->cand, c->fresh, c->scratch};
+    for (void *p : ptrs) if (p) cudaFree(p);
+    for (auto &e : c->ev) if (e) cudaEventDestroy(e);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+#define CTX_CHECK(c)                                                       \
+    do {                                                                   \
+        if (!(c)) { set_error("context is NULL"); return IMX_EINVAL; }     \
+        IMX_CUDA(cudaSetDevice((c)->dev));                                 \
+    } while (0)
+
+extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t num_scored,
+                          imx_ctx **out) {
+    if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
+    *out = nullptr;
+    if (!g) { set_error("graph is NULL"); return IMX_EINVAL; }
+    if (width < 1) { set_error("simulation width %d must be positive", width); return IMX_EINVAL; }
+    if (num_scored < 0 || num_scored > width) {
+        set_error("num_scored %d outside [0, %d]", num_scored, width);
+        return IMX_EINVAL;
+    }
+    if (!X) { set_error("X is NULL"); return IMX_EINVAL; }
+    for (int32_t r = 0; r < width; ++r)
+        if (X[r] < 0) { set_error("simulation word %d is negative (must be 31-bit)", r); return IMX_EINVAL; }
+    if (!g->symmetric) { set_error("adjacency is not symmetric"); return IMX_EFORMAT; }
+    IMX_CUDA(cudaSetDevice(g->dev));
+    imx_ctx *c = new imx_ctx();
+    c->g = g;
+    c->dev = g->dev;
+    c->W = width;
+    c->ns = num_scored;
+    c->ld = (width + 3) & ~3;
+    c->cw = (num_scored + 31) / 32;
+    if (c->cw == 0) c->cw = 1;
+    int vb = 1;
+    while ((int64_t(1) << vb) < g->n + 1) ++vb;
+    c->vb = vb;
+    for (auto &e : c->ev) e = nullptr;
+    const int64_t n = g->n;
+    auto fail = [&](int code) { ctx_free(c); return code; };
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return fail(IMX_ECUDA);
+    for (auto &e : c->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return fail(IMX_ECUDA);
+    const size_t cells = (size_t)(n > 0 ? n : 1) * (size_t)c->ld;
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMalloc((void **)&c->X, sizeof(int32_t) * c->ld)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->L, sizeof(uint32_t) * cells)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->C, sizeof(uint32_t) * cells)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->gains, sizeof(int64_t) * (n + 1))) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->scratch, sizeof(unsigned long long) * 8)) != cudaSuccess) {
+        return fail(cuda_fail(e, "cudaMalloc(context)", __FILE__, __LINE__));
+    }
+    std::vector<int32_t> xpad(c->ld, 0);
+    std::copy(X, X + width, xpad.begin());
+    if ((e = cudaMemcpy(c->X, xpad.data(), sizeof(int32_t) * c->ld, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_fail(e, "upload X", __FILE__, __LINE__));
+    *out = c;
+    return IMX_OK;
+}
+
+extern "C" void imx_destroy(imx_ctx *c) { ctx_free(c); }
+
+static int ensure_celf_buffers(imx_ctx *c) {
+    if (c->prio) return IMX_OK;
+    const int64_t n = c->g->n > 0 ? c->g->n : 1;
+    IMX_CUDA(cudaMalloc((void **)&c->prio, sizeof(int64_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->inS, n));
+    IMX_CUDA(cudaMalloc((void **)&c->cov, sizeof(uint32_t) * (size_t)n * c->cw));
+    IMX_CUDA(cudaMalloc((void **)&c->per_sim, sizeof(int64_t) * (c->W + 1)));
+    IMX_CUDA(cudaMalloc((void **)&c->cand, sizeof(int32_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->fresh, sizeof(int64_t) * n));
+    return IMX_OK;
+}
+
+static inline void count_launch(imx_ctx *c, int k = 1) { c->tm.kernel_launches += k; note_launch(k); }
+
+// phases -----------------------------------------------------------------
+static int run_init(imx_ctx *c) {
+    const int64_t n = c->g->n;
+    if (n == 0) return IMX_OK;
+    k_init<<<grid_for(n * (c->ld >> 2)), 256, 0, c->st>>>(c->L, n, c->ld);
+    IMX_CHECK_LAUNCH();
+    IMX_CUDA(cudaMemsetAsync(c->C, 0, sizeof(uint32_t) * (size_t)n * c->ld, c->st));
+    count_launch(c, 1);
+    return IMX_OK;
+}
+
+static int run_hook(imx_ctx *c, unsigned long long *hooks) {
+    imx_graph *g = c->g;
+    if (g->me == 0) return IMX_OK;
+    const size_t smem = sizeof(int32_t) * c->ld;
+    if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
+    const int64_t warps = g->me;
+    int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), 148 * 8);
+    if (g->uniform) {
+        if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(k_hook<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_hook<true><<<blocks, 256, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
+                                                   c->ld, c->L, hooks);
+    } else {
+        if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(k_hook<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_hook<false><<<blocks, 256, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
+                                                    c->ld, c->L, hooks);
+    }
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    c->tm.hook_launches++;
+    return IMX_OK;
+}
+
+static constexpr int kRun = 16;
+static int run_compress(imx_ctx *c, unsigned long long *changed) {
+    const int64_t n = c->g->n;
+    if (n == 0) return IMX_OK;
+    const int nq = (int)(c->ld >> 2);
+    dim3 grid((unsigned)ceil_div(ceil_div(n, kRun), 8), (unsigned)ceil_div(nq, 32));
+    k_compress<kRun><<<grid, 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, changed);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    return IMX_OK;
+}
+
+static int label_sum(imx_ctx *c, int64_t *out) {
+    const int64_t n = c->g->n;
+    IMX_CUDA(cudaMemsetAsync(c->scratch + 4, 0, sizeof(unsigned long long), c->st));
+    if (n) {
+        k_label_sum<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->ld, c->W, c->scratch + 4);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    unsigned long long s = 0;
+    IMX_CUDA(cudaMemcpyAsync(&s, c->scratch + 4, sizeof s, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    *out = (int64_t)s;
+    return IMX_OK;
+}
+
+static void push_stat(imx_prop_stats *st, int mode, int64_t changed, int64_t lsum) {
+    if (!st) return;
+    int i = st->sweeps++;
+    if (i < st->cap) {
+        if (st->changed_pairs) st->changed_pairs[i] = changed;
+        if (st->label_sums) st->label_sums[i] = lsum;
+        if (st->modes) st->modes[i] = mode;
+    }
+}
+
+extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
+    CTX_CHECK(c);
+    imx_graph *g = c->g;
+    const int64_t n = g->n;
+    if (st) st->sweeps = 0;
+    unsigned long long *sc = c->scratch;
+    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long) * 4, c->st));
+    IMX_CUDA(cudaEventRecord(c->ev[0], c->st));
+    IMX_TRY(run_init(c));
+    IMX_CUDA(cudaEventRecord(c->ev[1], c->st));
+    if (g->m2 > 0) {
+        IMX_TRY(run_hook(c, st ? sc : nullptr));
+        IMX_CUDA(cudaEventRecord(c->ev[2], c->st));
+        IMX_TRY(run_compress(c, st ? sc + 1 : nullptr));
+        IMX_CUDA(cudaEventRecord(c->ev[3], c->st));
+    } else {
+        IMX_CUDA(cudaEventRecord(c->ev[2], c->st));
+        IMX_CUDA(cudaEventRecord(c->ev[3], c->st));
+    }
+    IMX_CUDA(cudaEventSynchronize(c->ev[3]));
+    cudaEventElapsedTime(&c->tm.init_ms, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&c->tm.hook_ms, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&c->tm.compress_ms, c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&c->tm.propagate_ms, c->ev[0], c->ev[3]);
+    c->labels_ready = true;
+    c->memo_ready = false;
+    c->celf_ready = false;
+    c->full_counts = 0;
+    if (g->m2 == 0) return IMX_OK;  // propagation.py:276-278: edgeless -> identity, no sweeps
+    // One union-find pass reaches the fixpoint: it is reported as one sweep
+    // whose changed count is the number of (vertex, lane) labels that moved
+    // off the identity, followed (when asked) by the no-change sweep that
+    // proves convergence, as the reference's loop does (propagation.py:304-320).
+    int64_t changed = 0, lsum = 0;
+    if (st) {
+        // labels that differ from identity == hooks (each hook moves exactly
+        // one root) + compressions are not additive; count directly.
+        unsigned long long hc[2];
+        IMX_CUDA(cudaMemcpyAsync(hc, sc, sizeof hc, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        IMX_TRY(label_sum(c, &lsum));
+        // non-identity labels = n*(n-1)/2*W - ... ; count exactly instead:
+        changed = (int64_t)hc[0];  // every non-root (v, r) was hooked exactly once
+        push_stat(st, IMX_MODE_HOOK, changed, lsum);
+    }
+    if (verify || (st && changed > 0)) {
+        IMX_CUDA(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->st));
+        if (g->me) {
+            if (g->uniform)
+                k_verify_edges<true><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->ld, c->L, sc + 2);
+            else
+                k_verify_edges<false><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->ld, c->L, sc + 2);
+            IMX_CHECK_LAUNCH();
+        }
+        k_verify_roots<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->ld, c->W, sc + 2);
+        IMX_CHECK_LAUNCH();
+        count_launch(c, 2);
+        unsigned long long bad = 0;
+        IMX_CUDA(cudaMemcpyAsync(&bad, sc + 2, sizeof bad, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        if (bad) {
+            set_error("propagation self-check failed: %llu violations", bad);
+            return IMX_EINTERNAL;
+        }
+        if (st && changed > 0) push_stat(st, IMX_MODE_VERIFY, 0, lsum);
+    }
+    return IMX_OK;
+}
+
+extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
+    CTX_CHECK(c);
+    if (!c->labels_ready) { set_error("labels not computed (call imx_propagate first)"); return IMX_EINVAL; }
+    const int64_t n = c->g->n;
+    IMX_CUDA(cudaEventRecord(c->ev[4], c->st));
+    if (n) {
+        k_gains<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->ns,
+                                                     c->full_counts ? 0u : 1u, c->gains);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    IMX_CUDA(cudaEventRecord(c->ev[5], c->st));
+    if (gains_out && n)
+        IMX_CUDA(cudaMemcpyAsync(gains_out, c->gains, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    cudaEventElapsedTime(&c->tm.memoize_ms, c->ev[4], c->ev[5]);
+    c->memo_ready = true;
+    return IMX_OK;
+}
+
+extern "C" int imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t *sizes, int64_t ldh) {
+    CTX_CHECK(c);
+    const int64_t n = c->g->n;
+    if (!labels && n) { set_error("labels is NULL"); return IMX_EINVAL; }
+    if (ldh < c->W) { set_error("row stride %lld < width %d", (long long)ldh, c->W); return IMX_EINVAL; }
+    if (n) {
+        IMX_CUDA(cudaMemsetAsync(c->L, 0, sizeof(uint32_t) * (size_t)n * c->ld, c->st));
+        IMX_CUDA(cudaMemcpy2DAsync(c->L, sizeof(uint32_t) * c->ld, labels, sizeof(int32_t) * ldh,
+                                   sizeof(int32_t) * c->W, n, cudaMemcpyHostToDevice, c->st));
+        unsigned *bad = reinterpret_cast<unsigned *>(c->scratch + 6);
+        IMX_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), c->st));
+        if (sizes) {
+            IMX_CUDA(cudaMemsetAsync(c->C, 0, sizeof(uint32_t) * (size_t)n * c->ld, c->st));
+            IMX_CUDA(cudaMemcpy2DAsync(c->C, sizeof(uint32_t) * c->ld, sizes, sizeof(int32_t) * ldh,
+                                       sizeof(int32_t) * c->W, n, cudaMemcpyHostToDevice, c->st));
+        } else {
+            IMX_CUDA(cudaMemsetAsync(c->C, 0, sizeof(uint32_t) * (size_t)n * c->ld, c->st));
+            k_hist_full<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, bad);
+            IMX_CHECK_LAUNCH();
+            count_launch(c);
+        }
+        unsigned hb = 0;
+        IMX_CUDA(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        if (hb) { set_error("label outside 0..n-1"); return IMX_EINVAL; }
+    }
+    c->labels_ready = true;
+    c->memo_ready = false;
+    c->celf_ready = false;
+    c->full_counts = 1;
+    return IMX_OK;
+}
+
+extern "C" int imx_copy_labels(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out) {
+    CTX_CHECK(c);
+    if (r0 < 0 || r1 > c->W || r0 > r1) { set_error("lane window [%d, %d) invalid", r0, r1); return IMX_EINVAL; }
+    if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
+    const int64_t n = c->g->n;
+    if (n == 0 || r1 == r0) return IMX_OK;
+    IMX_CUDA(cudaMemcpy2DAsync(out, sizeof(int32_t) * (r1 - r0), c->L + r0, sizeof(uint32_t) * c->ld,
+                               sizeof(int32_t) * (r1 - r0), n, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    return IMX_OK;
+}
+
+extern "C" int imx_copy_sizes(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out) {
+    CTX_CHECK(c);
+    if (r0 < 0 || r1 > c->W || r0 > r1) { set_error("lane window [%d, %d) invalid", r0, r1); return IMX_EINVAL; }
+    if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
+    const int64_t n = c->g->n;
+    if (n == 0 || r1 == r0) return IMX_OK;
+    const int w = r1 - r0;
+    int64_t rows = std::max<int64_t>(1, (int64_t(256) << 20) / (4 * (int64_t)w));
+    rows = std::min(rows, n);
+    int32_t *tmp;
+    IMX_CUDA(cudaMalloc((void **)&tmp, sizeof(int32_t) * rows * w));
+    int rc = IMX_OK;
+    for (int64_t v0 = 0; v0 < n && rc == IMX_OK; v0 += rows) {
+        int64_t cnt = std::min(rows, n - v0);
+        k_sizes_window<<<grid_for(cnt * w), 256, 0, c->st>>>(c->L, c->C, v0, cnt, c->ld, r0, r1,
+                                                              c->full_counts, tmp);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out + v0 * w, tmp, sizeof(int32_t) * cnt * w, cudaMemcpyDeviceToHost, c->st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "copy sizes", __FILE__, __LINE__);
+        count_launch(c);
+    }
+    cudaFree(tmp);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
+// CELF (selection.py:115-149) -- round-based exact formulation
+// ---------------------------------------------------------------------------
+extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
+    CTX_CHECK(c);
+    if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
+    IMX_TRY(ensure_celf_buffers(c));
+    const int64_t n = c->g->n;
+    if (n) {
+        if (prio) {
+            IMX_CUDA(cudaMemcpyAsync(c->prio, prio, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->st));
+        } else {
+            if (!c->memo_ready) { set_error("gains not computed (call imx_memoize first)"); return IMX_EINVAL; }
+            IMX_CUDA(cudaMemcpyAsync(c->prio, c->gains, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->st));
+        }
+        IMX_CUDA(cudaMemsetAsync(c->inS, 0, n, c->st));
+        IMX_CUDA(cudaMemsetAsync(c->cov, 0, sizeof(uint32_t) * (size_t)n * c->cw, c->st));
+    }
+    IMX_CUDA(cudaMemsetAsync(c->per_sim, 0, sizeof(int64_t) * (c->W + 1), c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    c->celf_ready = true;
+    c->ncand = 0;
+    c->trace.clear();
+    return IMX_OK;
+}
+
+#define CELF_CHECK(c)                                                             \
+    do {                                                                          \
+        CTX_CHECK(c);                                                             \
+        if (!(c)->celf_ready) { set_error("CELF state not initialised (imx_celf_reset)"); return IMX_EINVAL; } \
+    } while (0)
+
+static int celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
+    const int64_t n = c->g->n;
+    unsigned long long *sc = c->scratch + 5;
+    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
+    if (n) {
+        k_top<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, sc);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    unsigned long long key = 0;
+    IMX_CUDA(cudaMemcpyAsync(&key, sc, sizeof key, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (!key) { *v_out = -1; *prio_out = 0; return IMX_OK; }
+    key -= 1;
+    const uint64_t vmask = (c->vb >= 32) ? 0xffffffffull : ((1ull << c->vb) - 1);
+    *v_out = (int32_t)(vmask - (key & vmask));
+    *prio_out = (int64_t)(key >> c->vb);
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
+    CELF_CHECK(c);
+    if (!prio_out || !v_out) { set_error("NULL argument"); return IMX_EINVAL; }
+    return celf_top(c, prio_out, v_out);
+}
+
+// collect candidates, sorted by id on the device list (deterministic order)
+static int celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude, std::vector<int32_t> *ids,
+                        std::vector<int64_t> *pr) {
+    const int64_t n = c->g->n;
+    unsigned long long *sc = c->scratch + 6;
+    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
+    const uint32_t vmask = (c->vb >= 32) ? 0xffffffffu : ((1u << c->vb) - 1u);
+    const unsigned long long thr = ((unsigned long long)g << c->vb) | (unsigned long long)(vmask - (uint32_t)u);
+    if (n) {
+        k_collect<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, thr, exclude, c->cand, sc);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    unsigned long long cnt = 0;
+    IMX_CUDA(cudaMemcpyAsync(&cnt, sc, sizeof cnt, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    c->ncand = (int64_t)cnt;
+    ids->resize(cnt);
+    pr->resize(cnt);
+    if (cnt) {
+        IMX_CUDA(cudaMemcpyAsync(ids->data(), c->cand, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        std::sort(ids->begin(), ids->end());
+        IMX_CUDA(cudaMemcpyAsync(c->cand, ids->data(), sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
+        k_gather_i64<<<grid_for((int64_t)cnt), 256, 0, c->st>>>(c->cand, (int64_t)cnt, c->prio, c->fresh);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+        IMX_CUDA(cudaMemcpyAsync(pr->data(), c->fresh, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+    }
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude, int32_t *ids_out,
+                                int64_t *prio_out, int64_t cap, int64_t *count) {
+    CELF_CHECK(c);
+    if (!count) { set_error("count is NULL"); return IMX_EINVAL; }
+    if (g < 0) { set_error("gain bound must be non-negative"); return IMX_EINVAL; }
+    std::vector<int32_t> ids;
+    std::vector<int64_t> pr;
+    IMX_TRY(celf_collect(c, g, u, exclude, &ids, &pr));
+    *count = (int64_t)ids.size();
+    const int64_t k = std::min<int64_t>(cap, *count);
+    if (k > 0 && ids_out) std::copy(ids.begin(), ids.begin() + k, ids_out);
+    if (k > 0 && prio_out) std::copy(pr.begin(), pr.begin() + k, prio_out);
+    return IMX_OK;
+}
+
+static int celf_eval_dev(imx_ctx *c, const int32_t *dcand, int64_t cnt, int64_t *dout) {
+    if (cnt <= 0) return IMX_OK;
+    k_eval<<<grid_for(cnt * 32), 256, 0, c->st>>>(dcand, cnt, c->L, c->C, c->cov, c->ld, c->ns, c->cw,
+                                                   c->full_counts, dout);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_eval_collected(imx_ctx *c, int64_t *fresh_out) {
+    CELF_CHECK(c);
+    if (c->ncand <= 0) return IMX_OK;
+    IMX_TRY(celf_eval_dev(c, c->cand, c->ncand, c->fresh));
+    if (fresh_out)
+        IMX_CUDA(cudaMemcpyAsync(fresh_out, c->fresh, sizeof(int64_t) * c->ncand, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    return IMX_OK;
+}
+
+extern "C" int imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int64_t *out) {
+    CELF_CHECK(c);
+    if (cnt < 0 || (cnt && (!cand || !out))) { set_error("bad arguments"); return IMX_EINVAL; }
+    if (!cnt) return IMX_OK;
+    for (int64_t i = 0; i < cnt; ++i)
+        if (cand[i] < 0 || cand[i] >= c->g->n) { set_error("vertex %d outside vertex range", cand[i]); return IMX_EINVAL; }
+    int32_t *dc;
+    int64_t *dout;
+    IMX_CUDA(cudaMallocAsync((void **)&dc, sizeof(int32_t) * cnt, c->st));
+    IMX_CUDA(cudaMallocAsync((void **)&dout, sizeof(int64_t) * cnt, c->st));
+    IMX_CUDA(cudaMemcpyAsync(dc, cand, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
+    int rc = celf_eval_dev(c, dc, cnt, dout);
+    if (rc == IMX_OK)
+        IMX_CUDA(cudaMemcpyAsync(out, dout, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, c->st));
+    cudaFreeAsync(dc, c->st);
+    cudaFreeAsync(dout, c->st);
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    return rc;
+}
+
+extern "C" int imx_celf_set_prio(imx_ctx *c, const int32_t *ids, const int64_t *vals, int64_t cnt) {
+    CELF_CHECK(c);
+    if (cnt <= 0) return IMX_OK;
+    int32_t *di;
+    int64_t *dv;
+    IMX_CUDA(cudaMallocAsync((void **)&di, sizeof(int32_t) * cnt, c->st));
+    IMX_CUDA(cudaMallocAsync((void **)&dv, sizeof(int64_t) * cnt, c->st));
+    IMX_CUDA(cudaMemcpyAsync(di, ids, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
+    IMX_CUDA(cudaMemcpyAsync(dv, vals, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, c->st));
+    k_set_prio<<<grid_for(cnt), 256, 0, c->st>>>(di, dv, cnt, c->prio);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    cudaFreeAsync(di, c->st);
+    cudaFreeAsync(dv, c->st);
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    return IMX_OK;
+}
+
+static int celf_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
+    unsigned long long *sc = c->scratch + 7;
+    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
+    k_commit<<<grid_for(std::max(c->ns, 1)), 256, 0, c->st>>>(u, c->L, c->C, c->cov, c->ld, c->ns, c->cw,
+                                                             c->full_counts, c->per_sim, c->inS, sc);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    unsigned long long gsum = 0;
+    IMX_CUDA(cudaMemcpyAsync(&gsum, sc, sizeof gsum, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (gain_out) *gain_out = (int64_t)gsum;
+    return IMX_OK;
+}
+
+extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
+    CELF_CHECK(c);
+    if (u < 0 || u >= c->g->n) { set_error("vertex %d outside vertex range", u); return IMX_EINVAL; }
+    uint8_t in = 0;
+    IMX_CUDA(cudaMemcpyAsync(&in, c->inS + u, 1, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (in) { set_error("vertex %d committed twice", u); return IMX_EINTERNAL; }
+    return celf_commit(c, u, gain_out);
+}
+
+static inline bool key_le(int64_t pa, int32_t va, int64_t pb, int32_t vb) {
+    // (-pa, va) <= (-pb, vb)
+    return pa > pb || (pa == pb && va <= vb);
+}
+
+// Whole CELF loop on one context.  Exactness argument: on a
+// fixed sample set marginal gains are submodular, so the reference's lazy
+// heap commits, at every round t, u* = argmin over V\S of (-fresh, id), after
+// refreshing exactly R_t = {v : (-prio_v, v) <= (-fresh_u*, u*)} in
+// (-prio, id) order.  Round t evaluates the top-priority vertex first and
+// then every vertex whose stale key is at most that vertex's fresh key -- a
+// superset of R_t -- so no unevaluated vertex can beat the winner.
+extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_t *gains_out,
+                               int64_t *trace_len) {
+    CELF_CHECK(c);
+    const int64_t n = c->g->n;
+    if (k < 1 || k > n) { set_error("k=%d invalid for n=%lld", k, (long long)n); return IMX_ECONSTRAINT; }
+    cudaEventRecord(c->ev[6], c->st);
+    c->trace.clear();
+    auto rec = [&](int64_t v, int64_t s, int64_t f, int64_t com, int64_t t) {
+        c->trace.push_back(v); c->trace.push_back(s); c->trace.push_back(f);
+        c->trace.push_back(com); c->trace.push_back(t);
+    };
+    std::vector<int32_t> ids;
+    std::vector<int64_t> pr, fr;
+    for (int32_t t = 0; t < k; ++t) {
+        int64_t gt;
+        int32_t vt;
+        IMX_TRY(celf_top(c, &gt, &vt));
+        if (vt < 0) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
+        int64_t best_f;
+        int32_t best_v;
+        if (t == 0) {
+            // fresh_at starts at 0 == len(S): the first pop commits (selection.py:136-141)
+            best_v = vt; best_f = gt;
+        } else {
+            int64_t f1 = 0;
+            IMX_CUDA(cudaMemcpyAsync(c->cand, &vt, sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+            IMX_TRY(celf_eval_dev(c, c->cand, 1, c->fresh));
+            IMX_CUDA(cudaMemcpyAsync(&f1, c->fresh, sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaStreamSynchronize(c->st));
+            best_v = vt; best_f = f1;
+            ids.assign(1, vt); pr.assign(1, gt); fr.assign(1, f1);
+            if (f1 != gt) {
+                std::vector<int32_t> cids;
+                std::vector<int64_t> cpr;
+                IMX_TRY(celf_collect(c, f1, vt, vt, &cids, &cpr));
+                if (!cids.empty()) {
+                    std::vector<int64_t> cfr(cids.size());
+                    IMX_TRY(celf_eval_dev(c, c->cand, (int64_t)cids.size(), c->fresh));
+                    IMX_CUDA(cudaMemcpyAsync(cfr.data(), c->fresh, sizeof(int64_t) * cids.size(),
+                                             cudaMemcpyDeviceToHost, c->st));
+                    IMX_CUDA(cudaStreamSynchronize(c->st));
+                    for (size_t i = 0; i < cids.size(); ++i) {
+                        ids.push_back(cids[i]); pr.push_back(cpr[i]); fr.push_back(cfr[i]);
+                        if (key_le(cfr[i], cids[i], best_f, best_v) && cids[i] != best_v) {
+                            best_v = cids[i]; best_f = cfr[i];
+                        }
+                    }
+                }
+            }
+            // R_t in (-prio, id) order: refresh records, then prio <- fresh
+            std::vector<size_t> rt;
+            for (size_t i = 0; i < ids.size(); ++i)
+                if (key_le(pr[i], ids[i], best_f, best_v)) rt.push_back(i);
+            std::sort(rt.begin(), rt.end(), [&](size_t a, size_t b) {
+                return pr[a] != pr[b] ? pr[a] > pr[b] : ids[a] < ids[b];
+            });
+            std::vector<int32_t> uid;
+            std::vector<int64_t> uval;
+            for (size_t i : rt) {
+                rec(ids[i], pr[i], fr[i], 0, t);
+                uid.push_back(ids[i]);
+                uval.push_back(fr[i]);
+            }
+            IMX_TRY(imx_celf_set_prio(c, uid.data(), uval.data(), (int64_t)uid.size()));
+        }
+        int64_t got = 0;
+        IMX_TRY(celf_commit(c, best_v, &got));
+        if (got != best_f) {
+            set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                      (long long)got, (long long)best_f, best_v);
+            return IMX_EINTERNAL;
+        }
+        rec(best_v, best_f, best_f, 1, t);
+        if (seeds_out) seeds_out[t] = best_v;
+        if (gains_out) gains_out[t] = best_f;
+    }
+    cudaEventRecord(c->ev[7], c->st);
+    cudaEventSynchronize(c->ev[7]);
+    cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
+    if (trace_len) *trace_len = (int64_t)(c->trace.size() / 5);
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_trace(imx_ctx *c, int64_t *out, int64_t cap) {
+    CTX_CHECK(c);
+    const int64_t len = (int64_t)(c->trace.size() / 5);
+    const int64_t k = std::min(cap, len);
+    if (k > 0 && out) std::copy(c->trace.begin(), c->trace.begin() + 5 * k, out);
+    return IMX_OK;
+}
+
+extern "C" int imx_per_sim(imx_ctx *c, int64_t *out) {
+    CELF_CHECK(c);
+    if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
+    if (c->ns) {
+        IMX_CUDA(cudaMemcpyAsync(out, c->per_sim, sizeof(int64_t) * c->ns, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+    }
+    return IMX_OK;
+}
+
+extern "C" int imx_copy_owned(imx_ctx *c, uint32_t *bits_out) {
+    CELF_CHECK(c);
+    if (!bits_out) { set_error("out is NULL"); return IMX_EINVAL; }
+    const int64_t n = c->g->n;
+    if (n) {
+        IMX_CUDA(cudaMemcpyAsync(bits_out, c->cov, sizeof(uint32_t) * (size_t)n * c->cw, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+    }
+    return IMX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// measurement
+// ---------------------------------------------------------------------------
+extern "C" int imx_get_timings(imx_ctx *c, imx_timings *out) {
+    CTX_CHECK(c);
+    if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
+    *out = c->tm;
+    return IMX_OK;
+}
+
+__global__ void k_flush(uint4 *buf, int64_t cnt, uint32_t salt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = make_uint4(salt, (uint32_t)i, salt, (uint32_t)i);
+}
+
+extern "C" int imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2, float *avg_total_ms,
+                                   float *avg_hook_ms, float *avg_compress_ms, float *avg_init_ms) {
+    CTX_CHECK(c);
+    if (reps < 1) { set_error("reps must be >= 1"); return IMX_EINVAL; }
+    uint4 *fb = nullptr;
+    const int64_t fcnt = (int64_t(256) << 20) / 16;  // 256 MB > 126 MB L2
+    if (flush_l2) IMX_CUDA(cudaMalloc((void **)&fb, fcnt * 16));
+    std::vector<cudaEvent_t> ev(4 * reps);
+    for (auto &e : ev) IMX_CUDA(cudaEventCreate(&e));
+    for (int i = 0; i < reps; ++i) {
+        if (fb) k_flush<<<148 * 8, 256, 0, c->st>>>(fb, fcnt, (uint32_t)i);
+        IMX_CUDA(cudaEventRecord(ev[4 * i], c->st));
+        IMX_TRY(run_init(c));
+        IMX_CUDA(cudaEventRecord(ev[4 * i + 1], c->st));
+        if (c->g->m2) IMX_TRY(run_hook(c, nullptr));
+        IMX_CUDA(cudaEventRecord(ev[4 * i + 2], c->st));
+        if (c->g->m2) IMX_TRY(run_compress(c, nullptr));
+        IMX_CUDA(cudaEventRecord(ev[4 * i + 3], c->st));
+    }
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    double tot = 0, hk = 0, cp = 0, in = 0;
+    for (int i = 0; i < reps; ++i) {
+        float a, b, d, e;
+        cudaEventElapsedTime(&a, ev[4 * i], ev[4 * i + 3]);
+        cudaEventElapsedTime(&b, ev[4 * i + 1], ev[4 * i + 2]);
+        cudaEventElapsedTime(&d, ev[4 * i + 2], ev[4 * i + 3]);
+        cudaEventElapsedTime(&e, ev[4 * i], ev[4 * i + 1]);
+        tot += a; hk += b; cp += d; in += e;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    if (fb) cudaFree(fb);
+    if (avg_total_ms) *avg_total_ms = (float)(tot / reps);
+    if (avg_hook_ms) *avg_hook_ms = (float)(hk / reps);
+    if (avg_compress_ms) *avg_compress_ms = (float)(cp / reps);
+    if (avg_init_ms) *avg_init_ms = (float)(in / reps);
+    c->labels_ready = true;
+    c->memo_ready = false;
+    c->celf_ready = false;
+    c->full_counts = 0;
+    return IMX_OK;
+}

@@ -1,0 +1,30 @@
+// graph.cuh -- device-resident CSR shared by the CC / memo / CELF kernels.
+#pragma once
+#include "common.cuh"
+
+struct imx_graph {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n = 0;           // vertices
+    int64_t m2 = 0;          // directed slots (Graph.m in the reference)
+    int64_t me = 0;          // canonical (lo < hi) slots = undirected edges
+    int64_t *xadj = nullptr; // [n+1]
+    int32_t *adj = nullptr;  // [m2]  rows sorted ascending
+    double *w = nullptr;     // [m2]  per-slot weight
+    int32_t *src = nullptr;  // [m2]  row of each slot
+    int32_t *hash = nullptr; // [m2]  31-bit edge hash (hashing.py:97-101)
+    int32_t *thr = nullptr;  // [m2]  symmetrized threshold (hashing.py:153-165)
+    int64_t *recip = nullptr;// [m2]  reciprocal slot
+    int64_t *cslot = nullptr;// [me]  canonical slot ids in slot order
+    int2 *E = nullptr;       // [me]  (lo, hi) of each undirected edge
+    int32_t *EH = nullptr;   // [me]  its hash
+    int32_t *ET = nullptr;   // [me]  its threshold
+    int32_t thr_u = 0;       // the threshold when uniform
+    int uniform = 1;         // all thresholds equal
+    int symmetric = 1;
+};
+
+namespace imx {
+int select_device(int32_t device);
+void graph_free(imx_graph *g);
+}

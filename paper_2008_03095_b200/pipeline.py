@@ -1,0 +1,133 @@
+"""End-to-end fused pipeline: hash, propagate, memoize, select (reference
+pipeline.py:1-66), with every phase on the GPU.
+
+``run_fused`` keeps the reference signature and ``FusedRun`` surface
+(seeds, spread, spread_se, original_seed_ids, timings keys).  Labels and
+sizes stay in device memory and are copied to the host only when
+``FusedRun.labels`` / ``.sizes`` are read.  Under ``torch.distributed`` with
+world size G > 1 the simulations are split into G contiguous lane windows,
+one per rank; gains and CELF partial sums are combined with int64
+allreduces (celf.py).
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from .celf import LocalComm, TorchComm, lane_window, select_rounds
+from .context import DeviceContext
+from .graph import Graph
+from .hashing import EdgeHashTable, SimulationRandoms, build_hash_table
+from .propagation import propagated_context
+from .selection import SelectionResult, _check_k, result_from_context
+
+__all__ = ["FusedRun", "run_fused", "default_comm"]
+
+
+class FusedRun:
+    """Everything a caller might want back from one fused selection run."""
+
+    def __init__(self, graph: Graph, selection: SelectionResult, ctx: DeviceContext,
+                 table: EdgeHashTable, randoms: SimulationRandoms, timings: dict, comm=None):
+        self.graph = graph
+        self.selection = selection
+        self.table = table
+        self.randoms = randoms
+        self.timings = timings
+        self._ctx = ctx
+        self._comm = comm or LocalComm()
+        self._labels = None
+        self._sizes = None
+
+    def _gather(self, local: np.ndarray) -> np.ndarray:
+        if self._comm.size == 1:
+            return local
+        parts = self._comm.allgather(local.reshape(-1).astype(np.int64))
+        n = self.graph.n
+        return np.concatenate([p.reshape(n, -1) for p in parts], axis=1).astype(np.int32)
+
+    @property
+    def labels(self) -> np.ndarray:
+        """(n, padded R) int32 min-id labels (copied from the device once)."""
+        if self._labels is None:
+            self._labels = self._gather(self._ctx.labels())
+        return self._labels
+
+    @property
+    def sizes(self) -> np.ndarray:
+        """(n, padded R) int32 component sizes indexed by label."""
+        if self._sizes is None:
+            self._sizes = self._gather(self._ctx.sizes())
+        return self._sizes
+
+    @property
+    def seeds(self) -> list:
+        return self.selection.seeds
+
+    @property
+    def spread(self) -> float:
+        return self.selection.spread
+
+    @property
+    def spread_se(self) -> float:
+        return self.selection.spread_se()
+
+    def original_seed_ids(self) -> list:
+        return [int(self.graph.orig_ids[s]) for s in self.selection.seeds]
+
+
+def default_comm():
+    """TorchComm when torch.distributed is initialised with >1 rank."""
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            return TorchComm()
+    except ImportError:
+        pass
+    return LocalComm()
+
+
+def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0,
+              n_threads: int = 1, comm=None) -> FusedRun:
+    """Select k seeds over ``num_simulations`` memoized implicit samples
+    (reference pipeline.py:44-66).  ``n_threads`` is accepted for signature
+    compatibility; ``comm`` (default: torch.distributed if initialised)
+    splits the simulations across ranks."""
+    comm = comm or default_comm()
+    _check_k(k, g.n)
+    timings: dict[str, float] = {}
+    t = time.perf_counter()
+    table = build_hash_table(g)
+    randoms = SimulationRandoms(num_simulations, master_seed)
+    timings["hash"] = time.perf_counter() - t
+
+    t = time.perf_counter()
+    a, b, scored = lane_window(randoms.padded, randoms.num_scored, comm.rank, comm.size)
+    ctx, _ = propagated_context(g, table, randoms.values[a:b], scored, lane0=a)
+    timings["propagate"] = time.perf_counter() - t
+
+    t = time.perf_counter()
+    if comm.size == 1:
+        ctx.memoize(want_gains=False)
+    else:
+        gains = comm.allreduce(ctx.memoize(want_gains=True))
+    timings["memoize"] = time.perf_counter() - t
+
+    t = time.perf_counter()
+    if comm.size == 1:
+        ctx.celf_reset(None)
+        seeds, gains_k, trace = ctx.celf_select(k)
+    else:
+        ctx.celf_reset(gains)
+        seeds, gains_k, trace = select_rounds(ctx, comm, k)
+    selection = result_from_context(ctx, seeds, gains_k, trace, randoms.num_scored)
+    if comm.size > 1:
+        per_sim = np.concatenate(comm.allgather(ctx.per_sim()))
+        selection.state._per_sim = per_sim
+        selection.state._ctx = None
+        selection.state._owned_ctx = ctx
+    timings["select"] = time.perf_counter() - t
+    timings["total"] = sum(timings.values())
+    return FusedRun(g, selection, ctx, table, randoms, timings, comm)

@@ -286,6 +286,7 @@ def run_ours(args, world, rank, local):
 
     # ---- correctness guard on the measured context ----
     ctx.propagate(verify=True)
+    ctx.close()
 
     # ---- e2e: public API with host buffers ----
     host = imx.Graph(g.xadj, g.adj, g.weights, g.orig_ids)
@@ -331,7 +332,6 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = cpu_baseline(args.config, host, R, K, args.cpu_budget_s)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
 
 
 def main():

@@ -142,14 +142,14 @@ int  imx_celf_reset(imx_ctx *c, const int64_t *prio);
 int  imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out);
 /* Collect the non-seeds v != exclude whose key (-prio[v], v) is <=
  * (-g, u), i.e. prio[v] > g or (prio[v] == g and v <= u), into the
- * context's candidate list; copies ids/prio of up to cap of them out and
- * reports the total in *count.                                             */
+ * context's candidate list sorted by that key; copies ids/prio of up to cap
+ * of them out and reports the total in *count.                            */
 int  imx_celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude,
                       int32_t *ids_out, int64_t *prio_out, int64_t cap,
                       int64_t *count);
-/* marginal_gain (selection.py:63-70) of the collected candidates, partial
- * over this window's scored lanes.                                         */
-int  imx_celf_eval_collected(imx_ctx *c, int64_t *fresh_out);
+/* marginal_gain (selection.py:63-70) of collected candidates [lo, hi),
+ * partial over this window's scored lanes.                                 */
+int  imx_celf_eval_collected(imx_ctx *c, int64_t lo, int64_t hi, int64_t *fresh_out);
 /* marginal_gain of an explicit candidate list.                            */
 int  imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int64_t *out);
 /* prio[ids[i]] = vals[i]                                                   */
@@ -181,6 +181,7 @@ typedef struct {
     float   init_ms, hook_ms, compress_ms;
     int64_t kernel_launches;
     int64_t hook_launches;
+    int64_t celf_evaluations;  /* marginal-gain evaluations of the last select */
 } imx_timings;
 int  imx_get_timings(imx_ctx *c, imx_timings *out);
 /* Run propagate `reps` times back to back (inputs resident) and report the

@@ -45,7 +45,8 @@ class PropStats(ctypes.Structure):
 class Timings(ctypes.Structure):
     _fields_ = [("propagate_ms", c_f32), ("memoize_ms", c_f32), ("select_ms", c_f32),
                 ("init_ms", c_f32), ("hook_ms", c_f32), ("compress_ms", c_f32),
-                ("kernel_launches", c_i64), ("hook_launches", c_i64)]
+                ("kernel_launches", c_i64), ("hook_launches", c_i64),
+                ("celf_evaluations", c_i64)]
 
 
 # name -> (restype, argtypes)
@@ -75,7 +76,7 @@ _SIGNATURES = {
     "imx_celf_reset": (c_i32, [c_void_p, c_void_p]),
     "imx_celf_top": (c_i32, [c_void_p, P(c_i64), P(c_i32)]),
     "imx_celf_collect": (c_i32, [c_void_p, c_i64, c_i32, c_i32, c_void_p, c_void_p, c_i64, P(c_i64)]),
-    "imx_celf_eval_collected": (c_i32, [c_void_p, c_void_p]),
+    "imx_celf_eval_collected": (c_i32, [c_void_p, c_i64, c_i64, c_void_p]),
     "imx_eval_gains": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p]),
     "imx_celf_set_prio": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64]),
     "imx_commit": (c_i32, [c_void_p, c_i32, P(c_i64)]),
@@ -168,8 +169,13 @@ def set_device(device: int) -> None:
     _device = int(device)
 
 
+_have_device = None
+
+
 def require_device() -> None:
-    lib = load()
-    if lib.imx_device_count() < 1:
+    global _have_device
+    if _have_device is None:
+        _have_device = load().imx_device_count() > 0
+    if not _have_device:
         raise RuntimeError("no sm_100 CUDA device visible: libinfuser_b200 has no "
                            "CPU fallback")

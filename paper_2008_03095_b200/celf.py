@@ -80,42 +80,50 @@ def lane_window(padded: int, num_scored: int, rank: int, size: int):
     return a, b, scored
 
 
-def select_rounds(shard, comm, k: int):
+def _key_le(pa, va, pb, vb) -> bool:
+    """(-pa, va) <= (-pb, vb)"""
+    return pa > pb or (pa == pb and va <= vb)
+
+
+def select_rounds(shard, comm, k: int, batch0: int = 64):
     """k seeds, their gains and the dequeue trace (T, 5) over a sharded
     CELF state.  ``shard`` offers celf_top / eval_gains / celf_collect /
-    celf_eval_collected / celf_set_prio / commit (see context.DeviceContext)."""
+    celf_eval_collected / celf_set_prio / commit (context.DeviceContext).
+
+    Round t: evaluate the top-priority vertex; collect every vertex whose
+    stale key is at most that fresh key (sorted by stale key, identical on
+    every rank); evaluate it in doubling batches until the best fresh key is
+    below the next stale key.  Each partial evaluation is allreduced."""
     seeds, gains, trace = [], [], []
     for t in range(k):
         g_top, v_top = shard.celf_top()
         if v_top < 0:
             raise AssertionError(f"no candidate left at round {t}")
-        if t == 0:
-            best_v, best_f = v_top, g_top
-        else:
+        best_v, best_f = v_top, g_top
+        if t > 0:
             f1 = int(comm.allreduce(shard.eval_gains(np.array([v_top], np.int32)))[0])
-            ids = [np.array([v_top], np.int64)]
-            prio = [np.array([g_top], np.int64)]
-            fresh = [np.array([f1], np.int64)]
+            best_f = f1
+            ev_ids, ev_prio, ev_fresh = [v_top], [g_top], [f1]
             if f1 != g_top:
-                cids, cpr = shard.celf_collect(f1, v_top, v_top)
-                if len(cids):
-                    cfr = comm.allreduce(shard.celf_eval_collected(len(cids)))
-                    ids.append(cids.astype(np.int64))
-                    prio.append(cpr.astype(np.int64))
-                    fresh.append(cfr)
-            ids = np.concatenate(ids)
-            prio = np.concatenate(prio)
-            fresh = np.concatenate(fresh)
-            # u* = argmin (-fresh, id)
-            w = np.lexsort((ids, -fresh))[0]
-            best_v, best_f = int(ids[w]), int(fresh[w])
-            # R_t in (-prio, id) order
-            in_rt = (prio > best_f) | ((prio == best_f) & (ids <= best_v))
-            order = np.lexsort((ids[in_rt], -prio[in_rt]))
-            rt_ids, rt_prio, rt_fresh = ids[in_rt][order], prio[in_rt][order], fresh[in_rt][order]
-            for v, s, f in zip(rt_ids.tolist(), rt_prio.tolist(), rt_fresh.tolist()):
-                trace.append((v, s, f, 0, t))
-            shard.celf_set_prio(rt_ids.astype(np.int32), rt_fresh)
+                ids, prio = shard.celf_collect(f1, v_top, v_top)
+                lo, b = 0, batch0
+                while lo < len(ids) and not _key_le(best_f, best_v, int(prio[lo]), int(ids[lo])):
+                    hi = min(len(ids), lo + b)
+                    fr = comm.allreduce(shard.celf_eval_collected(lo, hi))
+                    for v, f in zip(ids[lo:hi].tolist(), fr.tolist()):
+                        if _key_le(f, v, best_f, best_v):
+                            best_v, best_f = v, f
+                    ev_ids += ids[lo:hi].tolist()
+                    ev_prio += prio[lo:hi].tolist()
+                    ev_fresh += fr.tolist()
+                    lo, b = hi, 2 * b
+            ev = sorted((-p, v, f) for v, p, f in zip(ev_ids, ev_prio, ev_fresh)
+                        if _key_le(p, v, best_f, best_v))
+            for negp, v, f in ev:
+                trace.append((v, -negp, f, 0, t))
+            batch0 = max(64, len(ev))
+            shard.celf_set_prio(np.array([v for _, v, _ in ev], np.int32),
+                                np.array([f for _, _, f in ev], np.int64))
         got = int(comm.allreduce(np.array([shard.commit(best_v)], np.int64))[0])
         if got != best_f:
             raise AssertionError(f"committed gain {got} != evaluated {best_f} for vertex {best_v}")

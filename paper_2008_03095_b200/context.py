@@ -45,6 +45,7 @@ class DeviceContext:
         check(_lib.load().imx_create(self.dg.handle, ptr(X), self.width, self.num_scored,
                                      ctypes.byref(h)))
         self.handle = h
+        self._collect_cap = 1024
 
     def close(self):
         h, self.handle = getattr(self, "handle", None), None
@@ -113,25 +114,25 @@ class DeviceContext:
         return int(g.value), int(v.value)
 
     def celf_collect(self, g: int, u: int, exclude: int):
-        """Ids (ascending) and stale priorities of non-seeds v != exclude with
-        (-prio[v], v) <= (-g, u); they become the pending evaluation list."""
+        """Ids and stale priorities of the non-seeds v != exclude with
+        (-prio[v], v) <= (-g, u), sorted by that key; they become the pending
+        evaluation list (celf_eval_collected)."""
         lib = _lib.load()
-        cnt = ctypes.c_int64()
-        check(lib.imx_celf_collect(self.handle, int(g), int(u), int(exclude), None, None, 0,
-                                   ctypes.byref(cnt)))
-        k = cnt.value
-        ids = np.empty(k, np.int32)
-        pr = np.empty(k, np.int64)
-        if k:
-            # the device list is already sorted; re-collecting is idempotent
+        cap = max(1024, self._collect_cap)
+        while True:
+            ids = np.empty(cap, np.int32)
+            pr = np.empty(cap, np.int64)
+            cnt = ctypes.c_int64()
             check(lib.imx_celf_collect(self.handle, int(g), int(u), int(exclude), ptr(ids),
-                                       ptr(pr), k, ctypes.byref(cnt)))
-        return ids, pr
+                                       ptr(pr), cap, ctypes.byref(cnt)))
+            if cnt.value <= cap:
+                return ids[: cnt.value], pr[: cnt.value]
+            cap = self._collect_cap = int(cnt.value)
 
-    def celf_eval_collected(self, count: int) -> np.ndarray:
-        out = np.empty(count, np.int64)
-        if count:
-            check(_lib.load().imx_celf_eval_collected(self.handle, ptr(out)))
+    def celf_eval_collected(self, lo: int, hi: int) -> np.ndarray:
+        out = np.empty(hi - lo, np.int64)
+        if hi > lo:
+            check(_lib.load().imx_celf_eval_collected(self.handle, int(lo), int(hi), ptr(out)))
         return out
 
     def eval_gains(self, cand) -> np.ndarray:

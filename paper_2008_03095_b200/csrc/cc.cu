@@ -44,8 +44,18 @@ struct imx_ctx {
     int64_t *per_sim = nullptr;   // [W]
     int32_t *cand = nullptr;      // [n]
     int64_t *fresh = nullptr;     // [n]
-    unsigned long long *scratch = nullptr;  // [8]
+    unsigned long long *scratch = nullptr;  // [16]; [8..12] = CELF round header
     int64_t ncand = 0;
+    int32_t *cand2 = nullptr;     // [n] sort output
+    unsigned long long *keys2 = nullptr;  // [n] sorted keys
+    int64_t *eval_out = nullptr;  // [n]
+    int32_t *d_one = nullptr;     // [1]
+    void *sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    int32_t *h_ids = nullptr, *d_ids = nullptr;   // pinned staging for prio updates
+    int64_t *h_vals = nullptr, *d_vals = nullptr;
+    int64_t stage_cap = 0;
+    int64_t evaluated = 0;
     bool labels_ready = false, memo_ready = false, celf_ready = false;
     int full_counts = 0;          // 1: C holds full sizes (host-loaded labels)
     cudaEvent_t ev[8];
@@ -62,36 +72,47 @@ __device__ __forceinline__ uint32_t *cell(uint32_t *L, int64_t ld, uint32_t v, i
     return L + (int64_t)v * ld + r;
 }
 
-// root of x with path halving; the halving stores are benign races: every
-// value ever stored in a cell is an ancestor (a smaller id in the same tree).
-__device__ __forceinline__ uint32_t find_halve(uint32_t *L, int64_t ld, uint32_t x, int r) {
-    uint32_t p = ld_relaxed(cell(L, ld, x, r));
-    while (p != x) {
-        uint32_t gp = ld_relaxed(cell(L, ld, p, r));
-        if (gp == p) return p;
-        st_relaxed(cell(L, ld, x, r), gp);
-        x = gp;
-        p = ld_relaxed(cell(L, ld, x, r));
-    }
-    return x;
-}
-
 __device__ __forceinline__ uint32_t find_ro(const uint32_t *L, int64_t ld, uint32_t x, int r) {
     uint32_t p;
     while ((p = ld_relaxed(L + (int64_t)x * ld + r)) != x) x = p;
     return x;
 }
 
+// Two root searches advanced in lock step so their loads overlap.  Path
+// splitting: every visited node is re-pointed at its grandparent (a benign
+// race -- any value ever stored in a cell is an ancestor in the same tree).
+// On entry pa = L[xa], pb = L[xb]; on exit xa, xb are roots.
+__device__ __forceinline__ void find2(uint32_t *L, int64_t ld, int r, uint32_t &xa, uint32_t pa,
+                                      uint32_t &xb, uint32_t pb) {
+    for (;;) {
+        const bool da = pa == xa, db = pb == xb;
+        if (da && db) return;
+        uint32_t ga = pa, gb = pb;
+        if (!da) ga = ld_relaxed(cell(L, ld, pa, r));
+        if (!db) gb = ld_relaxed(cell(L, ld, pb, r));
+        if (!da) {
+            if (ga == pa) xa = pa;
+            else { st_relaxed(cell(L, ld, xa, r), ga); xa = pa; pa = ga; }
+        }
+        if (!db) {
+            if (gb == pb) xb = pb;
+            else { st_relaxed(cell(L, ld, xb, r), gb); xb = pb; pb = gb; }
+        }
+    }
+}
+
 // union of a and b in lane r: CAS-hook the larger root under the smaller.
 __device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32_t b, int r) {
-    a = find_halve(L, ld, a, r);
-    b = find_halve(L, ld, b, r);
+    uint32_t pa = ld_relaxed(cell(L, ld, a, r));
+    uint32_t pb = ld_relaxed(cell(L, ld, b, r));
+    find2(L, ld, r, a, pa, b, pb);
     while (a != b) {
-        if (a > b) { uint32_t t = a; a = b; b = t; }
-        uint32_t old = atomicCAS(cell(L, ld, b, r), b, a);
-        if (old == b) return 1;
-        b = find_halve(L, ld, old, r);
-        a = find_halve(L, ld, a, r);
+        const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+        const uint32_t old = atomicCAS(cell(L, ld, hi, r), hi, lo);
+        if (old == hi) return 1;
+        a = lo;
+        b = hi;
+        find2(L, ld, r, a, ld_relaxed(cell(L, ld, lo, r)), b, old);
     }
     return 0;
 }
@@ -109,55 +130,107 @@ __global__ void k_init(uint32_t *__restrict__ L, int64_t n, int64_t ld) {
     }
 }
 
-// One warp per undirected edge; each thread owns 4 consecutive lanes of a
-// 128-lane chunk, so the first-level label reads of a live lane group are
-// coalesced 16-byte loads of the two endpoint rows.  The hash and threshold
-// are read once per edge and reused across all W lanes.
+// Sampler + hooking.  A warp takes tiles of 32 undirected edges (one edge per
+// thread, coalesced loads of (lo, hi), hash and threshold), then walks the
+// tile edge by edge: each thread tests 4 consecutive lanes of a 128-lane
+// chunk against the edge ((X[r] ^ h) < t, X staged in shared memory once per
+// CTA), and the live (edge, lane) pairs are appended to a per-warp queue in
+// shared memory.  Whenever the queue holds 32 pairs the warp drains 32 at
+// once -- one union per thread -- so the latency-bound root searches always
+// run 32-wide instead of at the ~1% density of live lanes.  The adjacency and
+// hash are read once per edge and reused across all W lanes.
+constexpr int kHookWarps = 8;
+constexpr int kQ = 32 + 128;  // drain threshold + one chunk's worth of appends
+
 template <bool UNI>
-__global__ void __launch_bounds__(256) k_hook(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
-                                              const int32_t *__restrict__ ET, int32_t tu, int64_t me,
-                                              const int32_t *__restrict__ X, int32_t W, int64_t ld,
-                                              uint32_t *__restrict__ L,
-                                              unsigned long long *__restrict__ hooks) {
-    extern __shared__ int4 sX4[];
-    int32_t *sX = reinterpret_cast<int32_t *>(sX4);
+__global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
+                                                          const int32_t *__restrict__ ET, int32_t tu, int64_t me,
+                                                          const int32_t *__restrict__ X, int32_t W, int64_t ld,
+                                                          uint32_t *__restrict__ L,
+                                                          unsigned long long *__restrict__ hooks) {
+    extern __shared__ int4 smem4[];
+    int32_t *sX = reinterpret_cast<int32_t *>(smem4);
     for (int i = threadIdx.x; i < ld; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *qlo = reinterpret_cast<uint32_t *>(sX + ld) + warp * 3 * kQ;
+    uint32_t *qhi = qlo + kQ;
+    uint32_t *qr = qhi + kQ;
     __syncthreads();
     const int nq = (int)(ld >> 2);
-    const int lane = threadIdx.x & 31;
-    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned FULL = 0xffffffffu;
+    int qn = 0;  // warp-uniform queue length
     unsigned long long nh = 0;
-    for (int64_t e = wg; e < me; e += nw) {
-        const int2 uv = __ldg(&E[e]);
-        const int32_t h = __ldg(&EH[e]);
-        const int32_t t = UNI ? tu : __ldg(&ET[e]);
-        for (int q = lane; q < nq; q += 32) {
-            const int4 x = sX4[q];
-            const int r = q << 2;
-            unsigned live = ((unsigned)((x.x ^ h) < t)) | ((unsigned)((x.y ^ h) < t) << 1) |
-                            ((unsigned)((x.z ^ h) < t) << 2) | ((unsigned)((x.w ^ h) < t) << 3);
-            if (r + 4 > W) live &= (1u << (W > r ? W - r : 0)) - 1u;
-            while (live) {
-                const int j = __ffs(live) - 1;
-                live &= live - 1;
-                nh += unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r + j);
+    for (int64_t base = ((int64_t)blockIdx.x * kHookWarps + warp) * 32; base < me;
+         base += (int64_t)gridDim.x * kHookWarps * 32) {
+        const int64_t e = base + lane;
+        int2 uv = make_int2(0, 0);
+        int32_t h = 0, t = 0;  // t = 0: nothing is live
+        if (e < me) {
+            uv = __ldg(&E[e]);
+            h = __ldg(&EH[e]);
+            t = UNI ? tu : __ldg(&ET[e]);
+        }
+        const int cnt = (int)(me - base < 32 ? me - base : 32);
+        for (int j = 0; j < cnt; ++j) {
+            const int32_t hj = __shfl_sync(FULL, h, j), tj = __shfl_sync(FULL, t, j);
+            const uint32_t lo = (uint32_t)__shfl_sync(FULL, uv.x, j);
+            const uint32_t hi = (uint32_t)__shfl_sync(FULL, uv.y, j);
+            for (int c0 = 0; c0 < nq; c0 += 32) {
+                const int qd = c0 + lane;
+                unsigned live = 0;
+                if (qd < nq) {
+                    const int4 x = smem4[qd];
+                    live = ((unsigned)((x.x ^ hj) < tj)) | ((unsigned)((x.y ^ hj) < tj) << 1) |
+                           ((unsigned)((x.z ^ hj) < tj) << 2) | ((unsigned)((x.w ^ hj) < tj) << 3);
+                    const int r = qd << 2;
+                    if (r + 4 > W) live &= (1u << (W > r ? W - r : 0)) - 1u;
+                }
+                if (!__any_sync(FULL, live != 0)) continue;
+                const int k = __popc(live);
+                int inc = k;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                int pos = qn + inc - k;
+                while (live) {
+                    const int b = __ffs(live) - 1;
+                    live &= live - 1;
+                    qlo[pos] = lo;
+                    qhi[pos] = hi;
+                    qr[pos] = (uint32_t)((qd << 2) + b);
+                    ++pos;
+                }
+                qn += __shfl_sync(FULL, inc, 31);
+                __syncwarp();
+                while (qn >= 32) {
+                    qn -= 32;
+                    const uint32_t a = qlo[qn + lane], bb = qhi[qn + lane];
+                    const int r = (int)qr[qn + lane];
+                    __syncwarp();
+                    nh += unite(L, ld, a, bb, r);
+                }
             }
         }
     }
+    __syncwarp();
+    if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
     if (hooks) {
-        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(0xffffffffu, nh, o);
+        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
         if (lane == 0 && nh) atomicAdd(hooks, nh);
     }
 }
 
 // Full compression + component histogram.  A warp takes a run of RUN
-// consecutive vertices for 128 lanes; along the run each lane keeps
-// (current root, count) and only flushes an atomicAdd when the root changes,
-// so the hub roots of giant components (label 0 in every lane) receive one
-// atomic per run instead of one per member.
+// consecutive vertices for 128 lanes (one 16-byte quad per thread).  All RUN
+// rows are loaded first, then all first-level parents, so a thread has up to
+// 4*RUN independent loads in flight instead of a dependent chain per vertex.
+// Along the run each lane keeps (current root, count) and flushes one
+// atomicAdd when the root changes, so the hub roots of large components
+// receive one atomic per run instead of one per member.
 template <int RUN>
-__global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, uint32_t *__restrict__ C,
+__global__ void __launch_bounds__(256, 4) k_compress(uint32_t *__restrict__ L, uint32_t *__restrict__ C,
                                                   int64_t n, int64_t ld, int32_t W,
                                                   unsigned long long *__restrict__ changed) {
     const int nq = (int)(ld >> 2);
@@ -167,20 +240,37 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, uint
     const int64_t v0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * RUN;
     if (q >= nq || v0 >= n) return;
     const int r = q << 2;
+    const int nv = (int)(n - v0 < RUN ? n - v0 : RUN);
+    uint32_t lab[RUN][4], par[RUN][4];
+#pragma unroll
+    for (int i = 0; i < RUN; ++i) {
+        uint4 l = make_uint4(0, 0, 0, 0);
+        if (i < nv) l = *(reinterpret_cast<const uint4 *>(L + (v0 + i) * ld) + q);
+        lab[i][0] = l.x; lab[i][1] = l.y; lab[i][2] = l.z; lab[i][3] = l.w;
+    }
+#pragma unroll
+    for (int i = 0; i < RUN; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t x = lab[i][j];
+            par[i][j] = (i < nv && r + j < W && x != (uint32_t)(v0 + i))
+                            ? ld_relaxed(L + (int64_t)x * ld + r + j) : x;
+        }
     uint32_t cur[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
     uint32_t cnt[4] = {0, 0, 0, 0};
     unsigned long long nch = 0;
-    const int64_t v1 = min(n, v0 + RUN);
-    for (int64_t v = v0; v < v1; ++v) {
-        uint4 *p = reinterpret_cast<uint4 *>(L + v * ld) + q;
-        uint4 l = *p;
-        uint32_t lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+    for (int i = 0; i < RUN; ++i) {
+        if (i >= nv) break;
+        const uint32_t v = (uint32_t)(v0 + i);
         bool any = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (r + j >= W || lv[j] == (uint32_t)v) continue;
-            uint32_t root = find_ro(L, ld, lv[j], r + j);
-            if (root != lv[j]) { lv[j] = root; any = true; ++nch; }
+            const uint32_t x = lab[i][j];
+            if (r + j >= W || x == v) continue;
+            const uint32_t p = par[i][j];
+            const uint32_t root = (p == x) ? x : find_ro(L, ld, p, r + j);
+            if (root != x) { lab[i][j] = root; any = true; ++nch; }
             if (root == cur[j]) {
                 ++cnt[j];
             } else {
@@ -189,7 +279,9 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, uint
                 cnt[j] = 1;
             }
         }
-        if (any) *p = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+        if (any)
+            *(reinterpret_cast<uint4 *>(L + (int64_t)v * ld) + q) =
+                make_uint4(lab[i][0], lab[i][1], lab[i][2], lab[i][3]);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -350,26 +442,48 @@ __global__ void k_collect(const int64_t *__restrict__ prio, const uint8_t *__res
 }
 
 // marginal_gain (selection.py:63-70): sum over scored lanes of the component
-// size of L[u][r] when that component is not covered yet.  Warp per candidate.
-__global__ void __launch_bounds__(256) k_eval(const int32_t *__restrict__ cand, int64_t cnt,
-                                              const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
-                                              const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
-                                              int32_t cw, int full_counts,
-                                              int64_t *__restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// size of L[u][r] when that component is not covered yet.  One CTA per
+// candidate; each thread takes 16-byte quads of the label row so the label
+// loads are coalesced and the dependent cov/size gathers of 4 lanes are in
+// flight together.
+constexpr int kEvalThreads = 128;
+__global__ void __launch_bounds__(kEvalThreads) k_eval(const int32_t *__restrict__ cand, int64_t cnt,
+                                                       const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                                                       const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
+                                                       int32_t cw, int full_counts,
+                                                       int64_t *__restrict__ out) {
+    __shared__ unsigned long long part[kEvalThreads / 32];
     const uint32_t add1 = full_counts ? 0u : 1u;
-    for (int64_t i = wg; i < cnt; i += nw) {
+    const int nqs = (ns + 3) >> 2;
+    for (int64_t i = blockIdx.x; i < cnt; i += gridDim.x) {
         const int64_t u = cand[i];
+        if (u < 0) { if (threadIdx.x == 0) out[i] = 0; continue; }
+        const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
         unsigned long long acc = 0;
-        for (int r = lane; r < ns; r += 32) {
-            const uint32_t l = L[u * ld + r];
-            const uint32_t word = cov[(int64_t)l * cw + (r >> 5)];
-            if (!((word >> (r & 31)) & 1u)) acc += C[(int64_t)l * ld + r] + add1;
+        for (int q = threadIdx.x; q < nqs; q += kEvalThreads) {
+            const uint4 l4 = row[q];
+            const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            uint32_t w[4], s[4];
+            const int r = q << 2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool in = r + j < ns;
+                w[j] = in ? cov[(int64_t)lv[j] * cw + ((r + j) >> 5)] : 0xffffffffu;
+                s[j] = in ? C[(int64_t)lv[j] * ld + r + j] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (!((w[j] >> ((r + j) & 31)) & 1u)) acc += s[j] + add1;
         }
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) out[i] = (int64_t)acc;
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int k = 0; k < kEvalThreads / 32; ++k) t += part[k];
+            out[i] = (int64_t)t;
+        }
+        __syncthreads();
     }
 }
 
@@ -395,6 +509,50 @@ __global__ void k_commit(int32_t u, const uint32_t *__restrict__ L, const uint32
     if (blockIdx.x == 0 && threadIdx.x == 0) inS[u] = 1;
 }
 
+// CELF round header (scratch[8..12]): 0 top key+1, 1 fresh gain of the top,
+// 2 collected count, 3 gain of the last commit, 4 collect threshold key.
+enum { H_TOP = 0, H_F1 = 1, H_COUNT = 2, H_GAIN = 3, H_THR = 4 };
+
+__global__ void k_round_decode(const unsigned long long *__restrict__ hdr, int vb, int32_t *__restrict__ one) {
+    unsigned long long key = hdr[H_TOP];
+    const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
+    one[0] = key ? (int32_t)(vmask - (uint32_t)((key - 1) & vmask)) : -1;
+}
+
+__global__ void k_make_thr(unsigned long long *__restrict__ hdr, const int64_t *__restrict__ f1,
+                           const int32_t *__restrict__ one, int vb) {
+    const int32_t v = one[0];
+    hdr[H_F1] = (unsigned long long)f1[0];
+    hdr[H_THR] = v < 0 ? ~0ull : pack_key(f1[0], (uint32_t)v, vb);
+}
+
+// k_collect with the threshold key and the excluded vertex read from device memory
+__global__ void k_collect_dev(const int64_t *__restrict__ prio, const uint8_t *__restrict__ inS, int64_t n,
+                              int vb, const unsigned long long *__restrict__ hdr,
+                              const int32_t *__restrict__ one, int32_t *__restrict__ cand,
+                              unsigned long long *__restrict__ count) {
+    const unsigned long long thr_key = hdr[H_THR];
+    const int32_t exclude = one[0];
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        bool take = !inS[v] && v != exclude && pack_key(prio[v], (uint32_t)v, vb) >= thr_key;
+        unsigned m = __ballot_sync(__activemask(), take);
+        if (!m) continue;
+        int leader = __ffs(m) - 1;
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (take) cand[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (int32_t)v;
+    }
+}
+
+__global__ void k_keys_of(const int32_t *__restrict__ ids, int64_t cnt, const int64_t *__restrict__ prio,
+                          int vb, unsigned long long *__restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = pack_key(prio[ids[i]], (uint32_t)ids[i], vb);
+}
+
 __global__ void k_set_prio(const int32_t *__restrict__ ids, const int64_t *__restrict__ vals,
                            int64_t cnt, int64_t *__restrict__ prio) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
@@ -415,13 +573,38 @@ using namespace imx;
 // ---------------------------------------------------------------------------
 // context lifecycle
 // ---------------------------------------------------------------------------
+// The label/count matrices come from the device's stream-ordered pool with an
+// unbounded release threshold, so back-to-back runs on the same graph reuse
+// the memory instead of paying cudaMalloc/cudaFree every time.
+static cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st) {
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !configured[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured[dev] = true;
+    }
+    return cudaMallocAsync(p, bytes, st);
+}
+
 static void ctx_free(imx_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->dev);
     if (c->st) cudaStreamSynchronize(c->st);
+    if (c->L) cudaFreeAsync(c->L, c->st);
+    if (c->C) cudaFreeAsync(c->C, c->st);
+    c->L = c->C = nullptr;
+    if (c->st) cudaStreamSynchronize(c->st);
     void *ptrs[] = {c->X, c->L, c->C, c->gains, c->prio, c->inS, c->cov, c->per_sim,
-                    c->cand, c->fresh, c->scratch};
+                    c->cand, c->fresh, c->scratch, c->cand2, c->keys2, c->eval_out, c->d_one,
+                    c->sort_tmp, c->d_ids, c->d_vals};
     for (void *p : ptrs) if (p) cudaFree(p);
+    if (c->h_ids) cudaFreeHost(c->h_ids);
+    if (c->h_vals) cudaFreeHost(c->h_vals);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
@@ -468,10 +651,10 @@ extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t
     const size_t cells = (size_t)(n > 0 ? n : 1) * (size_t)c->ld;
     cudaError_t e = cudaSuccess;
     if ((e = cudaMalloc((void **)&c->X, sizeof(int32_t) * c->ld)) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->L, sizeof(uint32_t) * cells)) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->C, sizeof(uint32_t) * cells)) != cudaSuccess ||
+        (e = pool_alloc((void **)&c->L, sizeof(uint32_t) * cells, c->st)) != cudaSuccess ||
+        (e = pool_alloc((void **)&c->C, sizeof(uint32_t) * cells, c->st)) != cudaSuccess ||
         (e = cudaMalloc((void **)&c->gains, sizeof(int64_t) * (n + 1))) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->scratch, sizeof(unsigned long long) * 8)) != cudaSuccess) {
+        (e = cudaMalloc((void **)&c->scratch, sizeof(unsigned long long) * 16)) != cudaSuccess) {
         return fail(cuda_fail(e, "cudaMalloc(context)", __FILE__, __LINE__));
     }
     std::vector<int32_t> xpad(c->ld, 0);
@@ -493,6 +676,28 @@ static int ensure_celf_buffers(imx_ctx *c) {
     IMX_CUDA(cudaMalloc((void **)&c->per_sim, sizeof(int64_t) * (c->W + 1)));
     IMX_CUDA(cudaMalloc((void **)&c->cand, sizeof(int32_t) * n));
     IMX_CUDA(cudaMalloc((void **)&c->fresh, sizeof(int64_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->cand2, sizeof(int32_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->keys2, sizeof(unsigned long long) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->eval_out, sizeof(int64_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->d_one, sizeof(int32_t) * 4));
+    return IMX_OK;
+}
+
+static int ensure_pinned(imx_ctx *c, int64_t cnt) {
+    if (cnt <= c->stage_cap) return IMX_OK;
+    int64_t cap = std::max<int64_t>(cnt, 4096);
+    if (c->h_ids) cudaFreeHost(c->h_ids);
+    if (c->h_vals) cudaFreeHost(c->h_vals);
+    if (c->d_ids) cudaFree(c->d_ids);
+    if (c->d_vals) cudaFree(c->d_vals);
+    c->h_ids = nullptr; c->h_vals = nullptr; c->d_ids = nullptr; c->d_vals = nullptr;
+    c->stage_cap = 0;
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    IMX_CUDA(cudaMallocHost((void **)&c->h_ids, sizeof(int32_t) * cap));
+    IMX_CUDA(cudaMallocHost((void **)&c->h_vals, sizeof(int64_t) * cap));
+    IMX_CUDA(cudaMalloc((void **)&c->d_ids, sizeof(int32_t) * cap));
+    IMX_CUDA(cudaMalloc((void **)&c->d_vals, sizeof(int64_t) * cap));
+    c->stage_cap = cap;
     return IMX_OK;
 }
 
@@ -512,26 +717,21 @@ static int run_init(imx_ctx *c) {
 static int run_hook(imx_ctx *c, unsigned long long *hooks) {
     imx_graph *g = c->g;
     if (g->me == 0) return IMX_OK;
-    const size_t smem = sizeof(int32_t) * c->ld;
+    const size_t smem = sizeof(int32_t) * c->ld + sizeof(uint32_t) * 3 * kQ * kHookWarps;
     if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
-    const int64_t warps = g->me;
-    int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), 148 * 8);
-    if (g->uniform) {
-        if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(k_hook<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_hook<true><<<blocks, 256, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
-                                                   c->ld, c->L, hooks);
-    } else {
-        if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(k_hook<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_hook<false><<<blocks, 256, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
+    const int64_t tiles = ceil_div(g->me, 32);
+    int blocks = (int)std::min<int64_t>(ceil_div(tiles, kHookWarps), 148 * 8);
+    auto kern = g->uniform ? k_hook<true> : k_hook<false>;
+    if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<blocks, kHookWarps * 32, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
                                                     c->ld, c->L, hooks);
-    }
     IMX_CHECK_LAUNCH();
     count_launch(c);
     c->tm.hook_launches++;
     return IMX_OK;
 }
 
-static constexpr int kRun = 16;
+static constexpr int kRun = 4;
 static int run_compress(imx_ctx *c, unsigned long long *changed) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
@@ -787,7 +987,9 @@ extern "C" int imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
     return celf_top(c, prio_out, v_out);
 }
 
-// collect candidates, sorted by id on the device list (deterministic order)
+// Collect the non-seeds whose stale key (-prio, id) is <= (-g, u), sorted by
+// that key on the device (descending packed key == ascending (-prio, id)).
+// The sorted ids stay in c->cand for batch evaluation; ids/prio come back.
 static int celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude, std::vector<int32_t> *ids,
                         std::vector<int64_t> *pr) {
     const int64_t n = c->g->n;
@@ -806,17 +1008,31 @@ static int celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude, std::
     c->ncand = (int64_t)cnt;
     ids->resize(cnt);
     pr->resize(cnt);
-    if (cnt) {
-        IMX_CUDA(cudaMemcpyAsync(ids->data(), c->cand, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, c->st));
-        IMX_CUDA(cudaStreamSynchronize(c->st));
-        std::sort(ids->begin(), ids->end());
-        IMX_CUDA(cudaMemcpyAsync(c->cand, ids->data(), sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
-        k_gather_i64<<<grid_for((int64_t)cnt), 256, 0, c->st>>>(c->cand, (int64_t)cnt, c->prio, c->fresh);
-        IMX_CHECK_LAUNCH();
-        count_launch(c);
-        IMX_CUDA(cudaMemcpyAsync(pr->data(), c->fresh, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, c->st));
-        IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (!cnt) return IMX_OK;
+    // keys of the collected ids, then a device radix sort by key
+    unsigned long long *keys = reinterpret_cast<unsigned long long *>(c->fresh);
+    k_keys_of<<<grid_for((int64_t)cnt), 256, 0, c->st>>>(c->cand, (int64_t)cnt, c->prio, c->vb, keys);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    const int end_bit = 64;
+    size_t tmp_bytes = 0;
+    IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, keys, c->keys2, c->cand,
+                                                       c->cand2, (int64_t)cnt, 0, end_bit, c->st));
+    if (tmp_bytes > c->sort_tmp_bytes) {
+        if (c->sort_tmp) cudaFree(c->sort_tmp);
+        c->sort_tmp = nullptr;
+        c->sort_tmp_bytes = 0;
+        IMX_CUDA(cudaMalloc(&c->sort_tmp, tmp_bytes));
+        c->sort_tmp_bytes = tmp_bytes;
     }
+    IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, tmp_bytes, keys, c->keys2, c->cand,
+                                                       c->cand2, (int64_t)cnt, 0, end_bit, c->st));
+    std::swap(c->cand, c->cand2);
+    std::vector<unsigned long long> hk(cnt);
+    IMX_CUDA(cudaMemcpyAsync(ids->data(), c->cand, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaMemcpyAsync(hk.data(), c->keys2, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    for (size_t i = 0; i < cnt; ++i) (*pr)[i] = (int64_t)(hk[i] >> c->vb);
     return IMX_OK;
 }
 
@@ -837,19 +1053,26 @@ extern "C" int imx_celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclud
 
 static int celf_eval_dev(imx_ctx *c, const int32_t *dcand, int64_t cnt, int64_t *dout) {
     if (cnt <= 0) return IMX_OK;
-    k_eval<<<grid_for(cnt * 32), 256, 0, c->st>>>(dcand, cnt, c->L, c->C, c->cov, c->ld, c->ns, c->cw,
-                                                   c->full_counts, dout);
+    const int blocks = (int)std::min<int64_t>(cnt, 148 * 16);
+    k_eval<<<blocks, kEvalThreads, 0, c->st>>>(dcand, cnt, c->L, c->C, c->cov, c->ld, c->ns, c->cw,
+                                               c->full_counts, dout);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;
 }
 
-extern "C" int imx_celf_eval_collected(imx_ctx *c, int64_t *fresh_out) {
+// evaluate collected[lo, hi) -> fresh_out[hi - lo]
+extern "C" int imx_celf_eval_collected(imx_ctx *c, int64_t lo, int64_t hi, int64_t *fresh_out) {
     CELF_CHECK(c);
-    if (c->ncand <= 0) return IMX_OK;
-    IMX_TRY(celf_eval_dev(c, c->cand, c->ncand, c->fresh));
+    if (lo < 0 || hi > c->ncand || lo > hi) {
+        set_error("collected range [%lld, %lld) outside [0, %lld)", (long long)lo, (long long)hi,
+                  (long long)c->ncand);
+        return IMX_EINVAL;
+    }
+    if (hi == lo) return IMX_OK;
+    IMX_TRY(celf_eval_dev(c, c->cand + lo, hi - lo, c->eval_out));
     if (fresh_out)
-        IMX_CUDA(cudaMemcpyAsync(fresh_out, c->fresh, sizeof(int64_t) * c->ncand, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaMemcpyAsync(fresh_out, c->eval_out, sizeof(int64_t) * (hi - lo), cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
     return IMX_OK;
 }
@@ -874,20 +1097,23 @@ extern "C" int imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int6
     return rc;
 }
 
-extern "C" int imx_celf_set_prio(imx_ctx *c, const int32_t *ids, const int64_t *vals, int64_t cnt) {
-    CELF_CHECK(c);
+static int celf_set_prio_async(imx_ctx *c, const int32_t *ids, const int64_t *vals, int64_t cnt) {
     if (cnt <= 0) return IMX_OK;
-    int32_t *di;
-    int64_t *dv;
-    IMX_CUDA(cudaMallocAsync((void **)&di, sizeof(int32_t) * cnt, c->st));
-    IMX_CUDA(cudaMallocAsync((void **)&dv, sizeof(int64_t) * cnt, c->st));
-    IMX_CUDA(cudaMemcpyAsync(di, ids, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
-    IMX_CUDA(cudaMemcpyAsync(dv, vals, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, c->st));
-    k_set_prio<<<grid_for(cnt), 256, 0, c->st>>>(di, dv, cnt, c->prio);
+    // staged through the pinned host buffer
+    IMX_TRY(ensure_pinned(c, cnt));
+    std::copy(ids, ids + cnt, c->h_ids);
+    std::copy(vals, vals + cnt, c->h_vals);
+    IMX_CUDA(cudaMemcpyAsync(c->d_ids, c->h_ids, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
+    IMX_CUDA(cudaMemcpyAsync(c->d_vals, c->h_vals, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, c->st));
+    k_set_prio<<<grid_for(cnt), 256, 0, c->st>>>(c->d_ids, c->d_vals, cnt, c->prio);
     IMX_CHECK_LAUNCH();
     count_launch(c);
-    cudaFreeAsync(di, c->st);
-    cudaFreeAsync(dv, c->st);
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_set_prio(imx_ctx *c, const int32_t *ids, const int64_t *vals, int64_t cnt) {
+    CELF_CHECK(c);
+    IMX_TRY(celf_set_prio_async(c, ids, vals, cnt));
     IMX_CUDA(cudaStreamSynchronize(c->st));
     return IMX_OK;
 }
@@ -924,10 +1150,18 @@ static inline bool key_le(int64_t pa, int32_t va, int64_t pb, int32_t vb) {
 // Whole CELF loop on one context.  Exactness argument: on a
 // fixed sample set marginal gains are submodular, so the reference's lazy
 // heap commits, at every round t, u* = argmin over V\S of (-fresh, id), after
-// refreshing exactly R_t = {v : (-prio_v, v) <= (-fresh_u*, u*)} in
-// (-prio, id) order.  Round t evaluates the top-priority vertex first and
-// then every vertex whose stale key is at most that vertex's fresh key -- a
-// superset of R_t -- so no unevaluated vertex can beat the winner.
+// refreshing exactly R_t = {v : (-stale_v, v) <= (-fresh_u*, u*)} in
+// (-stale, id) order.  Round t evaluates the top-priority vertex, collects
+// the vertices whose stale key is at most that vertex's fresh key (nothing
+// else can win), sorts them by stale key and evaluates them in doubling
+// batches until the best fresh key found is below the next stale key -- so
+// the evaluated set is R_t plus at most one batch.
+//
+// Launch pattern per round: top -> decode -> eval(top) -> threshold ->
+// collect run back to back on the stream and end in ONE host sync that reads
+// the round header (top key, its fresh gain, collected count, last commit's
+// gain); the sort and the first batch end in a second sync; the priority
+// update and the commit are left in flight for the next round.
 extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_t *gains_out,
                                int64_t *trace_len) {
     CELF_CHECK(c);
@@ -935,78 +1169,153 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     if (k < 1 || k > n) { set_error("k=%d invalid for n=%lld", k, (long long)n); return IMX_ECONSTRAINT; }
     cudaEventRecord(c->ev[6], c->st);
     c->trace.clear();
+    c->evaluated = 0;
     auto rec = [&](int64_t v, int64_t s, int64_t f, int64_t com, int64_t t) {
         c->trace.push_back(v); c->trace.push_back(s); c->trace.push_back(f);
         c->trace.push_back(com); c->trace.push_back(t);
     };
-    std::vector<int32_t> ids;
-    std::vector<int64_t> pr, fr;
-    for (int32_t t = 0; t < k; ++t) {
-        int64_t gt;
-        int32_t vt;
-        IMX_TRY(celf_top(c, &gt, &vt));
-        if (vt < 0) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
-        int64_t best_f;
-        int32_t best_v;
-        if (t == 0) {
-            // fresh_at starts at 0 == len(S): the first pop commits (selection.py:136-141)
-            best_v = vt; best_f = gt;
-        } else {
-            int64_t f1 = 0;
-            IMX_CUDA(cudaMemcpyAsync(c->cand, &vt, sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
-            IMX_TRY(celf_eval_dev(c, c->cand, 1, c->fresh));
-            IMX_CUDA(cudaMemcpyAsync(&f1, c->fresh, sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
-            IMX_CUDA(cudaStreamSynchronize(c->st));
-            best_v = vt; best_f = f1;
-            ids.assign(1, vt); pr.assign(1, gt); fr.assign(1, f1);
-            if (f1 != gt) {
-                std::vector<int32_t> cids;
-                std::vector<int64_t> cpr;
-                IMX_TRY(celf_collect(c, f1, vt, vt, &cids, &cpr));
-                if (!cids.empty()) {
-                    std::vector<int64_t> cfr(cids.size());
-                    IMX_TRY(celf_eval_dev(c, c->cand, (int64_t)cids.size(), c->fresh));
-                    IMX_CUDA(cudaMemcpyAsync(cfr.data(), c->fresh, sizeof(int64_t) * cids.size(),
-                                             cudaMemcpyDeviceToHost, c->st));
-                    IMX_CUDA(cudaStreamSynchronize(c->st));
-                    for (size_t i = 0; i < cids.size(); ++i) {
-                        ids.push_back(cids[i]); pr.push_back(cpr[i]); fr.push_back(cfr[i]);
-                        if (key_le(cfr[i], cids[i], best_f, best_v) && cids[i] != best_v) {
-                            best_v = cids[i]; best_f = cfr[i];
-                        }
-                    }
-                }
-            }
-            // R_t in (-prio, id) order: refresh records, then prio <- fresh
-            std::vector<size_t> rt;
-            for (size_t i = 0; i < ids.size(); ++i)
-                if (key_le(pr[i], ids[i], best_f, best_v)) rt.push_back(i);
-            std::sort(rt.begin(), rt.end(), [&](size_t a, size_t b) {
-                return pr[a] != pr[b] ? pr[a] > pr[b] : ids[a] < ids[b];
-            });
-            std::vector<int32_t> uid;
-            std::vector<int64_t> uval;
-            for (size_t i : rt) {
-                rec(ids[i], pr[i], fr[i], 0, t);
-                uid.push_back(ids[i]);
-                uval.push_back(fr[i]);
-            }
-            IMX_TRY(imx_celf_set_prio(c, uid.data(), uval.data(), (int64_t)uid.size()));
-        }
-        int64_t got = 0;
-        IMX_TRY(celf_commit(c, best_v, &got));
-        if (got != best_f) {
+    unsigned long long *hdr = c->scratch + 8;
+    const uint64_t vmask = (c->vb >= 32) ? 0xffffffffull : ((1ull << c->vb) - 1);
+    IMX_TRY(ensure_pinned(c, 4096));
+    unsigned long long *hh = reinterpret_cast<unsigned long long *>(c->h_vals);  // pinned header copy
+    std::vector<int32_t> eids, ids;
+    std::vector<int64_t> epr, efr, pr, fr;
+    std::vector<unsigned long long> keys;
+    int64_t batch0 = 64;
+    int64_t pending_gain = -1;   // expected gain of the commit still in flight
+    int32_t pending_v = -1;
+    auto check_gain = [&](int64_t got) -> int {
+        if (pending_gain >= 0 && got != pending_gain) {
             set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
-                      (long long)got, (long long)best_f, best_v);
+                      (long long)got, (long long)pending_gain, pending_v);
             return IMX_EINTERNAL;
         }
+        return IMX_OK;
+    };
+    for (int32_t t = 0; t < k; ++t) {
+        // ---- phase 1: top, its fresh gain, the collected candidates ----
+        IMX_CUDA(cudaMemsetAsync(hdr + H_TOP, 0, sizeof(unsigned long long), c->st));
+        IMX_CUDA(cudaMemsetAsync(hdr + H_COUNT, 0, sizeof(unsigned long long), c->st));
+        k_top<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, hdr + H_TOP);
+        k_round_decode<<<1, 1, 0, c->st>>>(hdr, c->vb, c->d_one);
+        count_launch(c, 2);
+        if (t > 0) {
+            IMX_TRY(celf_eval_dev(c, c->d_one, 1, c->eval_out));
+            k_make_thr<<<1, 1, 0, c->st>>>(hdr, c->eval_out, c->d_one, c->vb);
+            k_collect_dev<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, hdr, c->d_one,
+                                                               c->cand, hdr + H_COUNT);
+            count_launch(c, 2);
+        }
+        IMX_CHECK_LAUNCH();
+        IMX_CUDA(cudaMemcpyAsync(hh, hdr, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        IMX_TRY(check_gain((int64_t)hh[H_GAIN]));
+        if (!hh[H_TOP]) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
+        const unsigned long long tk = hh[H_TOP] - 1;
+        const int32_t vt = (int32_t)(vmask - (tk & vmask));
+        const int64_t gt = (int64_t)(tk >> c->vb);
+        int64_t best_f = gt;
+        int32_t best_v = vt;
+        if (t > 0) {
+            const int64_t f1 = (int64_t)hh[H_F1];
+            const int64_t cnt = (int64_t)hh[H_COUNT];
+            c->evaluated += 1;
+            best_f = f1;
+            eids.assign(1, vt); epr.assign(1, gt); efr.assign(1, f1);
+            c->ncand = cnt;
+            if (cnt > 0) {
+                // ---- phase 2: sort by stale key, first batch ----
+                unsigned long long *dkeys = reinterpret_cast<unsigned long long *>(c->fresh);
+                k_keys_of<<<grid_for(cnt), 256, 0, c->st>>>(c->cand, cnt, c->prio, c->vb, dkeys);
+                IMX_CHECK_LAUNCH();
+                count_launch(c);
+                size_t tmp_bytes = 0;
+                IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, dkeys, c->keys2, c->cand,
+                                                                   c->cand2, cnt, 0, 64, c->st));
+                if (tmp_bytes > c->sort_tmp_bytes) {
+                    IMX_CUDA(cudaStreamSynchronize(c->st));
+                    if (c->sort_tmp) cudaFree(c->sort_tmp);
+                    c->sort_tmp = nullptr;
+                    c->sort_tmp_bytes = 0;
+                    IMX_CUDA(cudaMalloc(&c->sort_tmp, tmp_bytes * 2));
+                    c->sort_tmp_bytes = tmp_bytes * 2;
+                }
+                IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, tmp_bytes, dkeys, c->keys2, c->cand,
+                                                                   c->cand2, cnt, 0, 64, c->st));
+                std::swap(c->cand, c->cand2);
+                ids.resize(cnt); pr.resize(cnt); fr.resize(cnt); keys.resize(cnt);
+                int64_t lo = 0, b = batch0, fetched = 0;
+                for (;;) {
+                    const int64_t hi = std::min(cnt, lo + b);
+                    const int64_t fetch_to = std::min(cnt, hi + 1);   // +1: next stale key
+                    IMX_TRY(celf_eval_dev(c, c->cand + lo, hi - lo, c->eval_out));
+                    if (fetch_to > fetched) {
+                        IMX_CUDA(cudaMemcpyAsync(ids.data() + fetched, c->cand + fetched,
+                                                 sizeof(int32_t) * (fetch_to - fetched), cudaMemcpyDeviceToHost, c->st));
+                        IMX_CUDA(cudaMemcpyAsync(keys.data() + fetched, c->keys2 + fetched,
+                                                 sizeof(unsigned long long) * (fetch_to - fetched),
+                                                 cudaMemcpyDeviceToHost, c->st));
+                    }
+                    IMX_CUDA(cudaMemcpyAsync(fr.data() + lo, c->eval_out, sizeof(int64_t) * (hi - lo),
+                                             cudaMemcpyDeviceToHost, c->st));
+                    IMX_CUDA(cudaStreamSynchronize(c->st));
+                    for (int64_t i = fetched; i < fetch_to; ++i) pr[i] = (int64_t)(keys[i] >> c->vb);
+                    fetched = std::max(fetched, fetch_to);
+                    for (int64_t i = lo; i < hi; ++i) {
+                        if (key_le(fr[i], ids[i], best_f, best_v)) { best_f = fr[i]; best_v = ids[i]; }
+                        eids.push_back(ids[i]); epr.push_back(pr[i]); efr.push_back(fr[i]);
+                    }
+                    c->evaluated += hi - lo;
+                    lo = hi;
+                    b *= 2;
+                    if (lo >= cnt || key_le(best_f, best_v, pr[lo], ids[lo])) break;
+                }
+            }
+            // ---- R_t in (-stale, id) order: refresh records, prio <- fresh ----
+            std::vector<size_t> rt;
+            for (size_t i = 0; i < eids.size(); ++i)
+                if (key_le(epr[i], eids[i], best_f, best_v)) rt.push_back(i);
+            std::sort(rt.begin(), rt.end(), [&](size_t a, size_t b2) {
+                return epr[a] != epr[b2] ? epr[a] > epr[b2] : eids[a] < eids[b2];
+            });
+            IMX_TRY(ensure_pinned(c, (int64_t)rt.size() + 8));
+            hh = reinterpret_cast<unsigned long long *>(c->h_vals);
+            int64_t m = 0;
+            for (size_t i : rt) {
+                rec(eids[i], epr[i], efr[i], 0, t);
+                c->h_ids[m] = eids[i];
+                c->h_vals[8 + m] = efr[i];   // h_vals[0..7] hold the header copy
+                ++m;
+            }
+            batch0 = std::max<int64_t>(64, m);
+            if (m) {
+                IMX_CUDA(cudaMemcpyAsync(c->d_ids, c->h_ids, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
+                IMX_CUDA(cudaMemcpyAsync(c->d_vals, c->h_vals + 8, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->st));
+                k_set_prio<<<grid_for(m), 256, 0, c->st>>>(c->d_ids, c->d_vals, m, c->prio);
+                IMX_CHECK_LAUNCH();
+                count_launch(c);
+            }
+        }
+        // ---- commit (in flight; its gain is checked at the next header read) ----
+        IMX_CUDA(cudaMemsetAsync(hdr + H_GAIN, 0, sizeof(unsigned long long), c->st));
+        k_commit<<<grid_for(std::max(c->ns, 1)), 256, 0, c->st>>>(best_v, c->L, c->C, c->cov, c->ld, c->ns, c->cw,
+                                                                 c->full_counts, c->per_sim, c->inS, hdr + H_GAIN);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+        pending_gain = best_f;
+        pending_v = best_v;
         rec(best_v, best_f, best_f, 1, t);
         if (seeds_out) seeds_out[t] = best_v;
         if (gains_out) gains_out[t] = best_f;
     }
+    IMX_CUDA(cudaMemcpyAsync(hh, hdr, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    IMX_TRY(check_gain((int64_t)hh[H_GAIN]));
     cudaEventRecord(c->ev[7], c->st);
     cudaEventSynchronize(c->ev[7]);
     cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
+    c->tm.celf_evaluations = c->evaluated;
+    c->ncand = 0;
     if (trace_len) *trace_len = (int64_t)(c->trace.size() / 5);
     return IMX_OK;
 }

@@ -16,6 +16,7 @@ bitmaps, attached on first use.
 from __future__ import annotations
 
 import csv
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -173,8 +174,38 @@ def _check_k(k: int, n: int) -> int:
     return int(k)
 
 
-def trace_records(trace: np.ndarray) -> list:
-    return [TraceRecord(int(v), int(s), int(f), bool(c), int(t)) for v, s, f, c, t in trace.tolist()]
+class TraceList(Sequence):
+    """The CELF dequeue trace as a read-only list of TraceRecord, built from
+    the (T, 5) int64 array the device returns; records are created on
+    access, so a caller that never reads the trace never pays for it."""
+
+    def __init__(self, arr: np.ndarray):
+        self.array = np.asarray(arr, dtype=np.int64).reshape(-1, 5)
+        self._cache = None
+
+    def _records(self) -> list:
+        if self._cache is None:
+            self._cache = [TraceRecord(v, s, f, bool(c), t) for v, s, f, c, t in self.array.tolist()]
+        return self._cache
+
+    def __len__(self) -> int:
+        return len(self.array)
+
+    def __getitem__(self, i):
+        return self._records()[i]
+
+    def __iter__(self):
+        return iter(self._records())
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+    def __repr__(self):
+        return f"TraceList({len(self)} records)"
+
+
+def trace_records(trace: np.ndarray) -> TraceList:
+    return TraceList(trace)
 
 
 def result_from_context(ctx: DeviceContext, seeds, gains, trace, num_scored: int) -> SelectionResult:

@@ -21,6 +21,8 @@
 //   k_compress  L[v][r] = root(v, r); C[root][r] += 1 for non-roots
 //   k_verify    (optional) every live edge joins equal labels; every label is a root
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 #include <cub/cub.cuh>
 
@@ -56,6 +58,10 @@ struct imx_ctx {
     int64_t *h_vals = nullptr, *d_vals = nullptr;
     int64_t stage_cap = 0;
     int64_t evaluated = 0;
+    int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;  // enumeration segments
+    int64_t nseg_cap = 0;
+    void *scan_tmp = nullptr;
+    size_t scan_tmp_bytes = 0;
     bool labels_ready = false, memo_ready = false, celf_ready = false;
     int full_counts = 0;          // 1: C holds full sizes (host-loaded labels)
     cudaEvent_t ev[8];
@@ -222,71 +228,144 @@ __global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict
     }
 }
 
-// Full compression + component histogram.  A warp takes a run of RUN
-// consecutive vertices for 128 lanes (one 16-byte quad per thread).  All RUN
-// rows are loaded first, then all first-level parents, so a thread has up to
-// 4*RUN independent loads in flight instead of a dependent chain per vertex.
-// Along the run each lane keeps (current root, count) and flushes one
-// atomicAdd when the root changes, so the hub roots of large components
-// receive one atomic per run instead of one per member.
-template <int RUN>
-__global__ void __launch_bounds__(256, 4) k_compress(uint32_t *__restrict__ L, uint32_t *__restrict__ C,
+// ---------------------------------------------------------------------------
+// Sampler by interval enumeration (default).  For a threshold t and a lane
+// word x, {h : (x ^ h) < t} is the union over the set bits i of t of the
+// aligned hash interval [((t ^ x) >> (i+1) << (i+1)) | (x & 2^i), +2^i)
+// (the reference's _xor_below, propagation.py:104-118).  The undirected
+// edges are sorted by (threshold bucket, hash) on the device (graph.cu), so a
+// (lane, bucket, bit) segment is a contiguous range of edges found by two
+// binary searches, and the live (edge, lane) pairs of all lanes form one
+// flattened index space: no dead (edge, lane) pair is ever visited.  With
+// per-edge thresholds a bucket's interval uses the bucket's max threshold
+// and each enumerated edge is re-tested exactly ((x ^ h) < thr, strict).
+// ---------------------------------------------------------------------------
+__global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
+                            const int32_t *__restrict__ btmax, const int64_t *__restrict__ boff,
+                            const int32_t *__restrict__ EH, int64_t *__restrict__ seg_a,
+                            int64_t *__restrict__ seg_n) {
+    const int64_t nseg = (int64_t)W * nb * 31;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(s / (nb * 31));
+        const int rem = (int)(s - (int64_t)r * nb * 31);
+        const int b = rem / 31, i = rem - b * 31;
+        const uint32_t t = (uint32_t)btmax[b];
+        int64_t a = boff[b], cnt = 0;
+        if ((t >> i) & 1u) {
+            const uint32_t x = (uint32_t)X[r];
+            const uint64_t start = ((uint64_t)((t ^ x) >> (i + 1)) << (i + 1)) | (uint64_t)(x & (1u << i));
+            const uint64_t end = start + (1ull << i);
+            int64_t lo = boff[b], hi = boff[b + 1];
+            while (lo < hi) {  // lower_bound(start)
+                const int64_t mid = (lo + hi) >> 1;
+                if ((uint64_t)(uint32_t)EH[mid] < start) lo = mid + 1; else hi = mid;
+            }
+            a = lo;
+            hi = boff[b + 1];
+            while (lo < hi) {  // lower_bound(end)
+                const int64_t mid = (lo + hi) >> 1;
+                if ((uint64_t)(uint32_t)EH[mid] < end) lo = mid + 1; else hi = mid;
+            }
+            cnt = lo - a;
+        }
+        seg_a[s] = a;
+        seg_n[s] = cnt;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) seg_n[nseg] = 0;
+}
+
+// Every thread takes flattened live pairs j; a warp owns chunks of kEnumChunk
+// consecutive j (one binary search over the segment offsets per chunk, then
+// a forward walk), so consecutive threads read consecutive edges of the same
+// hash interval (coalesced) and every thread runs one union per pair.
+constexpr int kEnumChunk = 1024;
+template <bool UNI>
+__global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ off, const int64_t *__restrict__ seg_a,
+                                                   int64_t nseg, int segs_per_lane,
+                                                   const int2 *__restrict__ E, const int32_t *__restrict__ EH,
+                                                   const int32_t *__restrict__ ET, const int32_t *__restrict__ X,
+                                                   int64_t ld, uint32_t *__restrict__ L,
+                                                   unsigned long long *__restrict__ hooks) {
+    const int64_t total = off[nseg];
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long nh = 0;
+    for (int64_t j0 = wg * kEnumChunk; j0 < total; j0 += nw * kEnumChunk) {
+        int64_t s = 0;
+        if (lane == 0) {
+            int64_t lo = 0, hi = nseg;       // largest s with off[s] <= j0
+            while (hi - lo > 1) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (off[mid] <= j0) lo = mid; else hi = mid;
+            }
+            s = lo;
+        }
+        s = __shfl_sync(0xffffffffu, s, 0);
+        const int64_t jend = (total - j0 < kEnumChunk) ? total : j0 + kEnumChunk;
+        for (int64_t j = j0 + lane; j < jend; j += 32) {
+            while (off[s + 1] <= j) ++s;
+            const int64_t e = seg_a[s] + (j - off[s]);
+            const int r = (int)(s / segs_per_lane);
+            if (!UNI && !((X[r] ^ EH[e]) < ET[e])) continue;
+            const int2 uv = E[e];
+            nh += unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r);
+        }
+    }
+    if (hooks) {
+        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(0xffffffffu, nh, o);
+        if (lane == 0 && nh) atomicAdd(hooks, nh);
+    }
+}
+
+// Full compression + component histogram, one thread per 16-byte quad of a
+// label row (full occupancy; the latency of the root searches is hidden by
+// thread-level parallelism).  The searches re-point every visited node at its
+// grandparent with atomicMin (path splitting): concurrent owners store the
+// final root, the smallest id of the tree, so min-updates can never undo a
+// finished label.  Non-root cells add 1 to C[root][r].
+__device__ __forceinline__ uint32_t find_split(uint32_t *L, int64_t ld, uint32_t x, uint32_t p, int r) {
+    for (;;) {
+        const uint32_t gp = ld_relaxed(cell(L, ld, p, r));
+        if (gp == p) return p;
+        atomicMin(cell(L, ld, x, r), gp);
+        x = p;
+        p = gp;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, uint32_t *__restrict__ C,
                                                   int64_t n, int64_t ld, int32_t W,
                                                   unsigned long long *__restrict__ changed) {
-    const int nq = (int)(ld >> 2);
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int q = blockIdx.y * 32 + lane;
-    const int64_t v0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * RUN;
-    if (q >= nq || v0 >= n) return;
-    const int r = q << 2;
-    const int nv = (int)(n - v0 < RUN ? n - v0 : RUN);
-    uint32_t lab[RUN][4], par[RUN][4];
-#pragma unroll
-    for (int i = 0; i < RUN; ++i) {
-        uint4 l = make_uint4(0, 0, 0, 0);
-        if (i < nv) l = *(reinterpret_cast<const uint4 *>(L + (v0 + i) * ld) + q);
-        lab[i][0] = l.x; lab[i][1] = l.y; lab[i][2] = l.z; lab[i][3] = l.w;
-    }
-#pragma unroll
-    for (int i = 0; i < RUN; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t x = lab[i][j];
-            par[i][j] = (i < nv && r + j < W && x != (uint32_t)(v0 + i))
-                            ? ld_relaxed(L + (int64_t)x * ld + r + j) : x;
-        }
-    uint32_t cur[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-    uint32_t cnt[4] = {0, 0, 0, 0};
+    const int64_t nq = ld >> 2;
     unsigned long long nch = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / nq;
+        const int r = (int)(i - v * nq) << 2;
+        uint4 *p4 = reinterpret_cast<uint4 *>(L) + i;
+        const uint4 l = *p4;
+        uint32_t lv[4] = {l.x, l.y, l.z, l.w};
+        uint32_t par[4];
 #pragma unroll
-    for (int i = 0; i < RUN; ++i) {
-        if (i >= nv) break;
-        const uint32_t v = (uint32_t)(v0 + i);
+        for (int j = 0; j < 4; ++j)
+            par[j] = (r + j < W && lv[j] != (uint32_t)v) ? ld_relaxed(cell(L, ld, lv[j], r + j)) : lv[j];
         bool any = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const uint32_t x = lab[i][j];
-            if (r + j >= W || x == v) continue;
-            const uint32_t p = par[i][j];
-            const uint32_t root = (p == x) ? x : find_ro(L, ld, p, r + j);
-            if (root != x) { lab[i][j] = root; any = true; ++nch; }
-            if (root == cur[j]) {
-                ++cnt[j];
-            } else {
-                if (cnt[j]) atomicAdd(C + (int64_t)cur[j] * ld + r + j, cnt[j]);
-                cur[j] = root;
-                cnt[j] = 1;
-            }
+            const uint32_t x = lv[j];
+            if (r + j >= W || x == (uint32_t)v) continue;
+            const uint32_t root = (par[j] == x) ? x : find_split(L, ld, x, par[j], r + j);
+            if (root != x) { lv[j] = root; any = true; ++nch; }
+            atomicAdd(C + (int64_t)root * ld + r + j, 1u);
         }
-        if (any)
-            *(reinterpret_cast<uint4 *>(L + (int64_t)v * ld) + q) =
-                make_uint4(lab[i][0], lab[i][1], lab[i][2], lab[i][3]);
+        if (any) *p4 = make_uint4(lv[0], lv[1], lv[2], lv[3]);
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (cnt[j]) atomicAdd(C + (int64_t)cur[j] * ld + r + j, cnt[j]);
-    if (changed && nch) atomicAdd(changed, nch);
+    if (changed) {
+        for (int o = 16; o; o >>= 1) nch += __shfl_xor_sync(0xffffffffu, nch, o);
+        if ((threadIdx.x & 31) == 0 && nch) atomicAdd(changed, nch);
+    }
 }
 
 // Verification sweep: count live (edge, lane) pairs whose endpoint labels
@@ -601,7 +680,7 @@ static void ctx_free(imx_ctx *c) {
     if (c->st) cudaStreamSynchronize(c->st);
     void *ptrs[] = {c->X, c->L, c->C, c->gains, c->prio, c->inS, c->cov, c->per_sim,
                     c->cand, c->fresh, c->scratch, c->cand2, c->keys2, c->eval_out, c->d_one,
-                    c->sort_tmp, c->d_ids, c->d_vals};
+                    c->sort_tmp, c->d_ids, c->d_vals, c->seg_a, c->seg_n, c->seg_off, c->scan_tmp};
     for (void *p : ptrs) if (p) cudaFree(p);
     if (c->h_ids) cudaFreeHost(c->h_ids);
     if (c->h_vals) cudaFreeHost(c->h_vals);
@@ -714,9 +793,8 @@ static int run_init(imx_ctx *c) {
     return IMX_OK;
 }
 
-static int run_hook(imx_ctx *c, unsigned long long *hooks) {
+static int run_hook_dense(imx_ctx *c, unsigned long long *hooks) {
     imx_graph *g = c->g;
-    if (g->me == 0) return IMX_OK;
     const size_t smem = sizeof(int32_t) * c->ld + sizeof(uint32_t) * 3 * kQ * kHookWarps;
     if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
     const int64_t tiles = ceil_div(g->me, 32);
@@ -727,17 +805,57 @@ static int run_hook(imx_ctx *c, unsigned long long *hooks) {
                                                     c->ld, c->L, hooks);
     IMX_CHECK_LAUNCH();
     count_launch(c);
+    return IMX_OK;
+}
+
+static int run_hook_enum(imx_ctx *c, unsigned long long *hooks) {
+    imx_graph *g = c->g;
+    const int64_t nseg = (int64_t)c->W * g->nb * 31;
+    if (nseg + 1 > c->nseg_cap) {
+        for (int64_t **p : {&c->seg_a, &c->seg_n, &c->seg_off}) { if (*p) cudaFree(*p); *p = nullptr; }
+        c->nseg_cap = 0;
+        IMX_CUDA(cudaMalloc((void **)&c->seg_a, sizeof(int64_t) * (nseg + 1)));
+        IMX_CUDA(cudaMalloc((void **)&c->seg_n, sizeof(int64_t) * (nseg + 1)));
+        IMX_CUDA(cudaMalloc((void **)&c->seg_off, sizeof(int64_t) * (nseg + 1)));
+        c->nseg_cap = nseg + 1;
+        size_t tb = 0;
+        IMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
+        if (tb > c->scan_tmp_bytes) {
+            if (c->scan_tmp) cudaFree(c->scan_tmp);
+            IMX_CUDA(cudaMalloc(&c->scan_tmp, tb));
+            c->scan_tmp_bytes = tb;
+        }
+    }
+    k_seg_count<<<grid_for(nseg), 256, 0, c->st>>>(c->X, c->W, g->nb, g->btmax, g->boff, g->EH,
+                                                   c->seg_a, c->seg_n);
+    IMX_CHECK_LAUNCH();
+    size_t tb = c->scan_tmp_bytes;
+    IMX_CUDA(cub::DeviceScan::ExclusiveSum(c->scan_tmp, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
+    const int blocks = 148 * 8;
+    if (g->uniform)
+        k_hook_enum<true><<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH,
+                                                     g->ET, c->X, c->ld, c->L, hooks);
+    else
+        k_hook_enum<false><<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH,
+                                                      g->ET, c->X, c->ld, c->L, hooks);
+    IMX_CHECK_LAUNCH();
+    count_launch(c, 3);
+    return IMX_OK;
+}
+
+static int run_hook(imx_ctx *c, unsigned long long *hooks) {
+    if (c->g->me == 0) return IMX_OK;
+    static const char *mode = getenv("IMX_HOOK");
+    const bool dense = mode && !strcmp(mode, "dense");
+    IMX_TRY(dense ? run_hook_dense(c, hooks) : run_hook_enum(c, hooks));
     c->tm.hook_launches++;
     return IMX_OK;
 }
 
-static constexpr int kRun = 4;
 static int run_compress(imx_ctx *c, unsigned long long *changed) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
-    const int nq = (int)(c->ld >> 2);
-    dim3 grid((unsigned)ceil_div(ceil_div(n, kRun), 8), (unsigned)ceil_div(nq, 32));
-    k_compress<kRun><<<grid, 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, changed);
+    k_compress<<<grid_for(n * (c->ld >> 2)), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, changed);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;

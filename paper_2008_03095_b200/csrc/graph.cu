@@ -12,6 +12,7 @@
 // The CSR lives on the device for the whole pipeline: the per-slot hash and
 // symmetrized threshold are computed here once, and the canonical
 // (lo < hi) edge list in slot order is the work list of the hook kernel.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstring>
@@ -203,6 +204,54 @@ __global__ void k_fill_edges(const int64_t *__restrict__ cslot, int64_t me,
     }
 }
 
+// sorted-index construction --------------------------------------------------
+__global__ void k_iota_thr_keys(const int32_t *__restrict__ ET, int64_t me, uint32_t *__restrict__ keys,
+                                uint32_t *__restrict__ vals) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < me;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        keys[e] = (uint32_t)ET[e];
+        vals[e] = (uint32_t)e;
+    }
+}
+// position p of the threshold-sorted order -> bucket p*nb/me; key = bucket<<32 | hash
+__global__ void k_bucket_hash_keys(const uint32_t *__restrict__ by_thr, int64_t me, int nb,
+                                   const int32_t *__restrict__ EH, uint64_t *__restrict__ keys,
+                                   uint32_t *__restrict__ vals) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < me;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = by_thr ? by_thr[p] : (uint32_t)p;
+        const uint64_t b = (uint64_t)((p * nb) / me);
+        keys[p] = (b << 32) | (uint32_t)EH[e];
+        vals[p] = e;
+    }
+}
+__global__ void k_permute_edges(const uint32_t *__restrict__ perm, int64_t me,
+                                const int2 *__restrict__ E0, const int32_t *__restrict__ EH0,
+                                const int32_t *__restrict__ ET0, int2 *__restrict__ E,
+                                int32_t *__restrict__ EH, int32_t *__restrict__ ET) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < me;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = perm[j];
+        E[j] = E0[e];
+        EH[j] = EH0[e];
+        ET[j] = ET0[e];
+    }
+}
+// bucket offsets from the sorted keys; per-bucket max threshold
+__global__ void k_bucket_meta(const uint64_t *__restrict__ keys, int64_t me, int nb,
+                              const int32_t *__restrict__ ET, int64_t *__restrict__ boff,
+                              int32_t *__restrict__ btmax) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < me;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(keys[j] >> 32);
+        const int bp = j ? (int)(keys[j - 1] >> 32) : -1;
+        for (int q = bp + 1; q <= b; ++q) boff[q] = j;
+        if (j == me - 1)
+            for (int q = b + 1; q <= nb; ++q) boff[q] = me;
+        atomicMax(btmax + b, ET[j]);
+    }
+}
+
 __global__ void k_murmur_pairs(const uint32_t *__restrict__ lo, const uint32_t *__restrict__ hi,
                                int64_t cnt, uint32_t *__restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
@@ -231,7 +280,7 @@ void graph_free(imx_graph *g) {
     if (!g) return;
     cudaSetDevice(g->dev);
     void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
-                    g->cslot, g->E, g->EH, g->ET};
+                    g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff};
     for (void *p : ptrs) if (p) cudaFree(p);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
@@ -299,6 +348,69 @@ static int graph_finish(imx_graph *g) {
     return IMX_OK;
 }
 
+// Sort the undirected edges by (threshold bucket, hash) so the sampler can
+// enumerate the edges live in a lane as at most 31 hash intervals per bucket
+// (the reference's index sweep, propagation.py:104-163, on the device).
+static int graph_build_index(imx_graph *g) {
+    cudaStream_t st = g->stream;
+    const int64_t me = g->me;
+    const int nb = g->uniform ? 1 : (int)std::min<int64_t>(64, std::max<int64_t>(1, me));
+    if (g->btmax) { cudaFree(g->btmax); g->btmax = nullptr; }
+    if (g->boff) { cudaFree(g->boff); g->boff = nullptr; }
+    g->nb = nb;
+    IMX_CUDA(cudaMalloc((void **)&g->btmax, sizeof(int32_t) * nb));
+    IMX_CUDA(cudaMalloc((void **)&g->boff, sizeof(int64_t) * (nb + 1)));
+    IMX_CUDA(cudaMemsetAsync(g->btmax, 0, sizeof(int32_t) * nb, st));
+    IMX_CUDA(cudaMemsetAsync(g->boff, 0, sizeof(int64_t) * (nb + 1), st));
+    if (me == 0) return IMX_OK;
+    uint32_t *k32 = nullptr, *k32b = nullptr, *v32 = nullptr, *v32b = nullptr;
+    uint64_t *k64 = nullptr, *k64b = nullptr;
+    int2 *E0 = nullptr;
+    int32_t *EH0 = nullptr, *ET0 = nullptr;
+    void *tmp = nullptr;
+    size_t tb = 0, tb2 = 0;
+    int rc = IMX_OK;
+#define GI(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { rc = cuda_fail(_e, #call, __FILE__, __LINE__); goto done; } } while (0)
+    GI(cudaMallocAsync((void **)&v32, sizeof(uint32_t) * me, st));
+    GI(cudaMallocAsync((void **)&v32b, sizeof(uint32_t) * me, st));
+    GI(cudaMallocAsync((void **)&k64, sizeof(uint64_t) * me, st));
+    GI(cudaMallocAsync((void **)&k64b, sizeof(uint64_t) * me, st));
+    GI(cub::DeviceRadixSort::SortPairs(nullptr, tb, k64, k64b, v32, v32b, me, 0, 64, st));
+    if (nb > 1) {
+        GI(cudaMallocAsync((void **)&k32, sizeof(uint32_t) * me, st));
+        GI(cudaMallocAsync((void **)&k32b, sizeof(uint32_t) * me, st));
+        GI(cub::DeviceRadixSort::SortPairs(nullptr, tb2, k32, k32b, v32, v32b, me, 0, 32, st));
+    }
+    GI(cudaMallocAsync(&tmp, std::max(tb, tb2), st));
+    if (nb > 1) {
+        k_iota_thr_keys<<<grid_for(me), 256, 0, st>>>(g->ET, me, k32, v32); note_launch();
+        GI(cudaGetLastError());
+        GI(cub::DeviceRadixSort::SortPairs(tmp, tb2, k32, k32b, v32, v32b, me, 0, 32, st));
+        k_bucket_hash_keys<<<grid_for(me), 256, 0, st>>>(v32b, me, nb, g->EH, k64, v32); note_launch();
+    } else {
+        k_bucket_hash_keys<<<grid_for(me), 256, 0, st>>>(nullptr, me, 1, g->EH, k64, v32); note_launch();
+    }
+    GI(cudaGetLastError());
+    GI(cub::DeviceRadixSort::SortPairs(tmp, tb, k64, k64b, v32, v32b, me, 0, 40, st));
+    GI(cudaMallocAsync((void **)&E0, sizeof(int2) * me, st));
+    GI(cudaMallocAsync((void **)&EH0, sizeof(int32_t) * me, st));
+    GI(cudaMallocAsync((void **)&ET0, sizeof(int32_t) * me, st));
+    GI(cudaMemcpyAsync(E0, g->E, sizeof(int2) * me, cudaMemcpyDeviceToDevice, st));
+    GI(cudaMemcpyAsync(EH0, g->EH, sizeof(int32_t) * me, cudaMemcpyDeviceToDevice, st));
+    GI(cudaMemcpyAsync(ET0, g->ET, sizeof(int32_t) * me, cudaMemcpyDeviceToDevice, st));
+    k_permute_edges<<<grid_for(me), 256, 0, st>>>(v32b, me, E0, EH0, ET0, g->E, g->EH, g->ET); note_launch();
+    GI(cudaGetLastError());
+    k_bucket_meta<<<grid_for(me), 256, 0, st>>>(k64b, me, nb, g->ET, g->boff, g->btmax); note_launch();
+    GI(cudaGetLastError());
+    GI(cudaStreamSynchronize(st));
+done:
+    for (void *p : {(void *)k32, (void *)k32b, (void *)v32, (void *)v32b, (void *)k64, (void *)k64b,
+                    (void *)E0, (void *)EH0, (void *)ET0, tmp})
+        if (p) cudaFreeAsync(p, st);
+#undef GI
+    return rc;
+}
+
 // thresholds from current weights (symmetrized over reciprocal slots when the
 // graph is symmetric) and refresh the edge list's hash/thr columns
 static int graph_refresh_thresholds(imx_graph *g) {
@@ -326,6 +438,7 @@ static int graph_refresh_thresholds(imx_graph *g) {
                                                       g->thr, g->E, g->EH, g->ET); note_launch();
         IMX_CHECK_LAUNCH();
     }
+    IMX_TRY(graph_build_index(g));
     IMX_CUDA(cudaStreamSynchronize(st));
     return IMX_OK;
 }

@@ -16,9 +16,16 @@ struct imx_graph {
     int32_t *thr = nullptr;  // [m2]  symmetrized threshold (hashing.py:153-165)
     int64_t *recip = nullptr;// [m2]  reciprocal slot
     int64_t *cslot = nullptr;// [me]  canonical slot ids in slot order
+    // Undirected edges (lo < hi) sorted by (threshold bucket, hash): the
+    // sampler enumerates the live edges of a lane as hash intervals of a
+    // bucket (see cc.cu, k_hook_enum).  With a uniform threshold there is one
+    // bucket; otherwise nb quantile buckets of the threshold.
     int2 *E = nullptr;       // [me]  (lo, hi) of each undirected edge
-    int32_t *EH = nullptr;   // [me]  its hash
+    int32_t *EH = nullptr;   // [me]  its hash (ascending within a bucket)
     int32_t *ET = nullptr;   // [me]  its threshold
+    int nb = 1;              // threshold buckets
+    int32_t *btmax = nullptr;// [nb]  max threshold of each bucket
+    int64_t *boff = nullptr; // [nb+1] bucket offsets into E/EH/ET
     int32_t thr_u = 0;       // the threshold when uniform
     int uniform = 1;         // all thresholds equal
     int symmetric = 1;

@@ -252,6 +252,15 @@ __global__ void k_bucket_meta(const uint64_t *__restrict__ keys, int64_t me, int
     }
 }
 
+__global__ void k_sum_thr(const int32_t *__restrict__ ET, int64_t me, unsigned long long *__restrict__ out) {
+    unsigned long long acc = 0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < me;
+         e += (int64_t)gridDim.x * blockDim.x)
+        acc += (unsigned long long)(uint32_t)ET[e];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 __global__ void k_murmur_pairs(const uint32_t *__restrict__ lo, const uint32_t *__restrict__ hi,
                                int64_t cnt, uint32_t *__restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
@@ -402,7 +411,15 @@ static int graph_build_index(imx_graph *g) {
     GI(cudaGetLastError());
     k_bucket_meta<<<grid_for(me), 256, 0, st>>>(k64b, me, nb, g->ET, g->boff, g->btmax); note_launch();
     GI(cudaGetLastError());
-    GI(cudaStreamSynchronize(st));
+    {
+        unsigned long long *dsum = reinterpret_cast<unsigned long long *>(k64);   // reuse scratch
+        GI(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long), st));
+        k_sum_thr<<<grid_for(me), 256, 0, st>>>(g->ET, me, dsum); note_launch();
+        unsigned long long hs = 0;
+        GI(cudaMemcpyAsync(&hs, dsum, sizeof hs, cudaMemcpyDeviceToHost, st));
+        GI(cudaStreamSynchronize(st));
+        g->thr_mean = (double)hs / (double)me / 2147483647.0;
+    }
 done:
     for (void *p : {(void *)k32, (void *)k32b, (void *)v32, (void *)v32b, (void *)k64, (void *)k64b,
                     (void *)E0, (void *)EH0, (void *)ET0, tmp})

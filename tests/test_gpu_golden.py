@@ -110,3 +110,22 @@ def test_select_seeds_on_host_arrays_matches_oracle(gpu, orc, name):
     assert np.array_equal(got, trace)
     assert np.array_equal(res.state.per_sim, per_sim)
     assert gpu.recompute_sigma(labels, res.state) == res.sigma
+
+
+@pytest.mark.parametrize("mode", ["enum", "pull", "dense"])
+@pytest.mark.parametrize("name", ["er_big_1000", "er_uniform_r24", "er_wc_r40", "er_const1_r16",
+                                  "er_const0_r16", "er_pad20", "kat_dead_middle", "cfg_c1"])
+def test_every_sampler_strategy_reaches_the_reference_fixpoint(gpu, name, mode, monkeypatch):
+    """The three sampler/hook strategies (interval enumeration, pull
+    first-hop forest + rest unions, dense edge-major scan) give the
+    reference's labels, sizes and gains."""
+    monkeypatch.setenv("IMX_HOOK", mode)
+    z = load_golden(name)
+    g = build_graph(gpu, z)
+    randoms = gpu.SimulationRandoms(int(z["R"]), int(z["master_seed"]))
+    labels, stats = gpu.propagate(g, gpu.build_hash_table(g), randoms, return_stats=True)
+    assert sha(labels) == str(z["labels_sha"])
+    assert stats.changed_pairs[-1] == 0
+    assert stats.changed_pairs[0] == int((labels != np.arange(g.n)[:, None]).sum())
+    sizes, gains = gpu.component_sizes_and_gains(labels, randoms.num_scored)
+    assert np.array_equal(gains, z["gains"])

@@ -1,0 +1,142 @@
+// ctx.cu -- context lifecycle (imx_create / imx_destroy / imx_get_timings)
+// and buffer management shared by propagate.cu, memo.cu and celf.cu.
+#include <algorithm>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace imx {
+
+// The label/count matrices come from the device's stream-ordered pool with an
+// unbounded release threshold, so back-to-back runs on the same graph reuse
+// the memory instead of paying cudaMalloc/cudaFree every time.
+cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st) {
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !configured[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured[dev] = true;
+    }
+    return cudaMallocAsync(p, bytes, st);
+}
+
+void ctx_free(imx_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    if (c->st) cudaStreamSynchronize(c->st);
+    if (c->L) cudaFreeAsync(c->L, c->st);
+    if (c->C) cudaFreeAsync(c->C, c->st);
+    c->L = c->C = nullptr;
+    if (c->st) cudaStreamSynchronize(c->st);
+    void *ptrs[] = {c->X, c->L, c->C, c->gains, c->prio, c->inS, c->cov, c->per_sim,
+                    c->cand, c->fresh, c->scratch, c->cand2, c->keys2, c->eval_out, c->d_one,
+                    c->sort_tmp, c->d_ids, c->d_vals, c->seg_a, c->seg_n, c->seg_off, c->scan_tmp};
+    for (void *p : ptrs) if (p) cudaFree(p);
+    if (c->h_ids) cudaFreeHost(c->h_ids);
+    if (c->h_vals) cudaFreeHost(c->h_vals);
+    for (auto &e : c->ev) if (e) cudaEventDestroy(e);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+int ensure_celf_buffers(imx_ctx *c) {
+    if (c->prio) return IMX_OK;
+    const int64_t n = c->g->n > 0 ? c->g->n : 1;
+    IMX_CUDA(cudaMalloc((void **)&c->prio, sizeof(int64_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->inS, n));
+    IMX_CUDA(cudaMalloc((void **)&c->cov, sizeof(uint32_t) * (size_t)n * c->cw));
+    IMX_CUDA(cudaMalloc((void **)&c->per_sim, sizeof(int64_t) * (c->W + 1)));
+    IMX_CUDA(cudaMalloc((void **)&c->cand, sizeof(int32_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->fresh, sizeof(int64_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->cand2, sizeof(int32_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->keys2, sizeof(unsigned long long) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->eval_out, sizeof(int64_t) * n));
+    IMX_CUDA(cudaMalloc((void **)&c->d_one, sizeof(int32_t) * 4));
+    return IMX_OK;
+}
+
+int ensure_pinned(imx_ctx *c, int64_t cnt) {
+    if (cnt <= c->stage_cap) return IMX_OK;
+    int64_t cap = std::max<int64_t>(cnt, 4096);
+    if (c->h_ids) cudaFreeHost(c->h_ids);
+    if (c->h_vals) cudaFreeHost(c->h_vals);
+    if (c->d_ids) cudaFree(c->d_ids);
+    if (c->d_vals) cudaFree(c->d_vals);
+    c->h_ids = nullptr; c->h_vals = nullptr; c->d_ids = nullptr; c->d_vals = nullptr;
+    c->stage_cap = 0;
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    IMX_CUDA(cudaMallocHost((void **)&c->h_ids, sizeof(int32_t) * cap));
+    IMX_CUDA(cudaMallocHost((void **)&c->h_vals, sizeof(int64_t) * cap));
+    IMX_CUDA(cudaMalloc((void **)&c->d_ids, sizeof(int32_t) * cap));
+    IMX_CUDA(cudaMalloc((void **)&c->d_vals, sizeof(int64_t) * cap));
+    c->stage_cap = cap;
+    return IMX_OK;
+}
+
+
+}  // namespace imx
+
+using namespace imx;
+
+extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t num_scored,
+                          imx_ctx **out) {
+    if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
+    *out = nullptr;
+    if (!g) { set_error("graph is NULL"); return IMX_EINVAL; }
+    if (width < 1) { set_error("simulation width %d must be positive", width); return IMX_EINVAL; }
+    if (num_scored < 0 || num_scored > width) {
+        set_error("num_scored %d outside [0, %d]", num_scored, width);
+        return IMX_EINVAL;
+    }
+    if (!X) { set_error("X is NULL"); return IMX_EINVAL; }
+    for (int32_t r = 0; r < width; ++r)
+        if (X[r] < 0) { set_error("simulation word %d is negative (must be 31-bit)", r); return IMX_EINVAL; }
+    if (!g->symmetric) { set_error("adjacency is not symmetric"); return IMX_EFORMAT; }
+    IMX_CUDA(cudaSetDevice(g->dev));
+    imx_ctx *c = new imx_ctx();
+    c->g = g;
+    c->dev = g->dev;
+    c->W = width;
+    c->ns = num_scored;
+    c->ld = (width + 3) & ~3;
+    c->cw = (num_scored + 31) / 32;
+    if (c->cw == 0) c->cw = 1;
+    int vb = 1;
+    while ((int64_t(1) << vb) < g->n + 1) ++vb;
+    c->vb = vb;
+    for (auto &e : c->ev) e = nullptr;
+    const int64_t n = g->n;
+    auto fail = [&](int code) { ctx_free(c); return code; };
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return fail(IMX_ECUDA);
+    for (auto &e : c->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return fail(IMX_ECUDA);
+    const size_t cells = (size_t)(n > 0 ? n : 1) * (size_t)c->ld;
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMalloc((void **)&c->X, sizeof(int32_t) * c->ld)) != cudaSuccess ||
+        (e = pool_alloc((void **)&c->L, sizeof(uint32_t) * cells, c->st)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->gains, sizeof(int64_t) * (n + 1))) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->scratch, sizeof(unsigned long long) * 16)) != cudaSuccess) {
+        return fail(cuda_fail(e, "cudaMalloc(context)", __FILE__, __LINE__));
+    }
+    std::vector<int32_t> xpad(c->ld, 0);
+    std::copy(X, X + width, xpad.begin());
+    if ((e = cudaMemcpy(c->X, xpad.data(), sizeof(int32_t) * c->ld, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_fail(e, "upload X", __FILE__, __LINE__));
+    *out = c;
+    return IMX_OK;
+}
+
+extern "C" void imx_destroy(imx_ctx *c) { ctx_free(c); }
+
+
+extern "C" int imx_get_timings(imx_ctx *c, imx_timings *out) {
+    CTX_CHECK(c);
+    if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
+    *out = c->tm;
+    return IMX_OK;
+}

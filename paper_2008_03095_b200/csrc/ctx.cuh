@@ -1,0 +1,97 @@
+// ctx.cuh -- the per-device, per-lane-window context shared by the K3-K8
+// translation units (propagate.cu, memo.cu, celf.cu, ctx.cu).
+//
+// Data layout in HBM (one context = one device, one lane window of width W):
+//   L[n][ld] uint32  the label matrix, simulation-contiguous (propagation.py:1-8),
+//                    ld = W rounded up to 4 so every row is 16-byte aligned.
+//                    Cell encoding (see uf.cuh):
+//                      bit 31 set   -> v is the root (= min id) of its component
+//                                      in lane r; bits 0-30 = number of OTHER
+//                                      members (filled by the compress pass)
+//                      bit 31 clear -> parent pointer; after compress, the root
+//                    so label(v, r) = root ? v : cell, and the component size of
+//                    a root cell is (cell & 0x7FFFFFFF) + 1: labels and sizes
+//                    (propagation.py:349-390) live in ONE n*W*4-byte array.
+//   C[n][ld] uint32  only for contexts fed with caller labels (imx_load_labels):
+//                    L then holds plain labels and C their full component sizes.
+//   cov[n][cw]       covered-component bitmap of the CELF state, cw = ceil(ns/32)
+//                    (SeedState.owned, selection.py:36-60).
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+#include "graph.cuh"
+
+struct imx_ctx {
+    imx_graph *g = nullptr;
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    int32_t W = 0, ns = 0, cw = 0;
+    int64_t ld = 0;
+    int vb = 0;                   // bits for vertex ids in packed CELF keys
+    int32_t *X = nullptr;         // [ld]
+    uint32_t *L = nullptr;        // [n*ld]
+    uint32_t *C = nullptr;        // [n*ld] caller-label mode only
+    int64_t *gains = nullptr;     // [n]
+    // CELF state
+    int64_t *prio = nullptr;      // [n]
+    uint8_t *inS = nullptr;       // [n]
+    uint32_t *cov = nullptr;      // [n*cw]
+    int64_t *per_sim = nullptr;   // [W]
+    int32_t *cand = nullptr;      // [n]
+    int32_t *cand2 = nullptr;     // [n] sort output
+    int64_t *fresh = nullptr;     // [n] (also sort keys scratch)
+    unsigned long long *keys2 = nullptr;  // [n] sorted keys
+    int64_t *eval_out = nullptr;  // [n]
+    int32_t *d_one = nullptr;     // [4]
+    int64_t ncand = 0;
+    void *sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    int32_t *h_ids = nullptr, *d_ids = nullptr;   // pinned staging for prio updates
+    int64_t *h_vals = nullptr, *d_vals = nullptr;
+    int64_t stage_cap = 0;
+    int64_t evaluated = 0;
+    std::vector<int64_t> trace;   // 5 per record
+    // interval-enumeration sampler
+    int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;
+    int64_t nseg_cap = 0;
+    void *scan_tmp = nullptr;
+    size_t scan_tmp_bytes = 0;
+    // misc
+    unsigned long long *scratch = nullptr;  // [16]; [8..12] = CELF round header
+    bool labels_ready = false, memo_ready = false, celf_ready = false;
+    cudaEvent_t ev[8];
+    imx_timings tm{};
+};
+
+namespace imx {
+
+inline int grid_for(int64_t work, int threads = 256) {
+    int64_t b = ceil_div(work > 0 ? work : 1, threads);
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+inline void count_launch(imx_ctx *c, int k = 1) {
+    c->tm.kernel_launches += k;
+    note_launch(k);
+}
+
+cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
+int ensure_celf_buffers(imx_ctx *c);
+int ensure_pinned(imx_ctx *c, int64_t cnt);
+int run_init(imx_ctx *c);
+
+}  // namespace imx
+
+#define CTX_CHECK(c)                                                       \
+    do {                                                                   \
+        if (!(c)) { ::imx::set_error("context is NULL"); return IMX_EINVAL; } \
+        IMX_CUDA(cudaSetDevice((c)->dev));                                 \
+    } while (0)
+
+#define CELF_CHECK(c)                                                             \
+    do {                                                                          \
+        CTX_CHECK(c);                                                             \
+        if (!(c)->celf_ready) { ::imx::set_error("CELF state not initialised (imx_celf_reset)"); return IMX_EINVAL; } \
+    } while (0)

@@ -252,6 +252,28 @@ __global__ void k_bucket_meta(const uint64_t *__restrict__ keys, int64_t me, int
     }
 }
 
+// number of neighbours smaller than v = lower_bound(row v, v) - xadj[v]
+__global__ void k_max_prefix(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, int64_t n,
+                             unsigned long long *__restrict__ out) {
+    unsigned long long best = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = xadj[v], hi = xadj[v + 1];
+        const int64_t s0 = lo;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (adj[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        const unsigned long long k = (unsigned long long)(lo - s0);
+        best = k > best ? k : best;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y > best ? y : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
 __global__ void k_sum_thr(const int32_t *__restrict__ ET, int64_t me, unsigned long long *__restrict__ out) {
     unsigned long long acc = 0;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < me;
@@ -326,6 +348,17 @@ static int graph_finish(imx_graph *g) {
     IMX_TRY(read_flags(g, dflags, &flags));
     g->symmetric = (flags & 8u) == 0 && (m2 % 2 == 0);
     cudaFreeAsync(dflags, st);
+    if (m2) {
+        unsigned long long *dmax, hmax = 0;
+        IMX_CUDA(cudaMallocAsync((void **)&dmax, sizeof(unsigned long long), st));
+        IMX_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+        k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, dmax); note_launch();
+        IMX_CHECK_LAUNCH();
+        IMX_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof hmax, cudaMemcpyDeviceToHost, st));
+        IMX_CUDA(cudaStreamSynchronize(st));
+        cudaFreeAsync(dmax, st);
+        g->max_prefix = (int64_t)hmax;
+    }
     // canonical edge list
     g->me = 0;
     if (m2) {

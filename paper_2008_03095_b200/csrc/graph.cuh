@@ -27,6 +27,7 @@ struct imx_graph {
     int32_t *btmax = nullptr;// [nb]  max threshold of each bucket
     int64_t *boff = nullptr; // [nb+1] bucket offsets into E/EH/ET
     int32_t thr_u = 0;       // the threshold when uniform
+    int64_t max_prefix = 0;  // max over v of #neighbours smaller than v
     double thr_mean = 0;     // mean canonical-edge threshold / H_MAX = mean live fraction
     int uniform = 1;         // all thresholds equal
     int symmetric = 1;

@@ -1,0 +1,206 @@
+// memo.cu -- K4/K5 memoization: component sizes and int64 gains
+// (reference component_sizes_and_gains, propagation.py:349-390), plus label /
+// size copies to the host and caller-provided label matrices.
+//
+// After propagate a root cell already holds its component's member count
+// (uf.cuh), so the histogram is free: sizes[l][r] = (cell & COUNT) + 1 for a
+// root cell, 0 otherwise, and the gain of v is the sum over the scored lanes
+// of the size of v's root -- one coalesced row read plus one gather per
+// non-root cell.  Caller labels (imx_load_labels) are arbitrary ids, so they
+// get an explicit size array C[n][ld] (template ENC = false).
+#include <algorithm>
+#include <vector>
+
+#include "ctx.cuh"
+#include "uf.cuh"
+
+namespace imx {
+
+// size of the component of cell (v, r): encoded labels (ENC) or caller labels + C
+template <bool ENC>
+__device__ __forceinline__ uint32_t comp_size(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                                              int64_t ld, uint32_t v, uint32_t w, int r, uint32_t *label) {
+    if (ENC) {
+        if (is_root(w)) { *label = v; return (w & COUNT) + 1u; }
+        *label = w;
+        return (__ldg(L + (int64_t)w * ld + r) & COUNT) + 1u;
+    }
+    *label = w;
+    return __ldg(C + (int64_t)w * ld + r);
+}
+
+// gains[v] = sum_{r < ns} size(comp(v, r))   (propagation.py:359-368)
+template <bool ENC>
+__global__ void __launch_bounds__(256) k_gains(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                                               int64_t n, int64_t ld, int32_t ns, int64_t *__restrict__ gains) {
+    const int lane = threadIdx.x & 31;
+    const int nqs = (ns + 3) >> 2;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = wg; v < n; v += nw) {
+        const uint4 *Lr = reinterpret_cast<const uint4 *>(L + v * ld);
+        unsigned long long acc = 0;
+        for (int q = lane; q < nqs; q += 32) {
+            const uint4 l = __ldg(Lr + q);
+            const uint32_t w[4] = {l.x, l.y, l.z, l.w};
+            const int r = q << 2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (r + j >= ns) break;
+                uint32_t lab;
+                acc += comp_size<ENC>(L, C, ld, (uint32_t)v, w[j], r + j, &lab);
+            }
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) gains[v] = (int64_t)acc;
+    }
+}
+
+// decoded labels / sizes of rows [v0, v0+cnt), lanes [r0, r1) -> dense out
+template <bool ENC>
+__global__ void k_labels_window(const uint32_t *__restrict__ L, int64_t v0, int64_t cnt, int64_t ld,
+                                int32_t r0, int32_t r1, int32_t *__restrict__ out) {
+    const int w = r1 - r0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt * (int64_t)w;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = v0 + i / w;
+        const int r = r0 + (int)(i % w);
+        const uint32_t x = L[v * ld + r];
+        out[i] = (int32_t)(ENC ? label_of((uint32_t)v, x) : x);
+    }
+}
+template <bool ENC>
+__global__ void k_sizes_window(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                               int64_t v0, int64_t cnt, int64_t ld, int32_t r0, int32_t r1,
+                               int32_t *__restrict__ out) {
+    const int w = r1 - r0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt * (int64_t)w;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = v0 + i / w;
+        const int r = r0 + (int)(i % w);
+        if (ENC) {
+            const uint32_t x = L[v * ld + r];
+            out[i] = is_root(x) ? (int32_t)((x & COUNT) + 1u) : 0;
+        } else {
+            out[i] = (int32_t)C[v * ld + r];
+        }
+    }
+}
+
+// full histogram of caller labels (component_sizes, propagation.py:349-356)
+__global__ void k_hist_full(const uint32_t *__restrict__ L, uint32_t *__restrict__ C, int64_t n, int64_t ld,
+                            int32_t W, unsigned *__restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / W;
+        const int r = (int)(i - v * W);
+        const uint32_t l = L[v * ld + r];
+        if (l >= (uint32_t)n) { atomicOr(bad, 1u); continue; }
+        atomicAdd(C + (int64_t)l * ld + r, 1u);
+    }
+}
+
+// copy rows of a decoded window out through a device staging buffer
+template <class Launch>
+static int copy_window(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out, Launch launch) {
+    const int64_t n = c->g->n;
+    const int w = r1 - r0;
+    int64_t rows = std::max<int64_t>(1, (int64_t(256) << 20) / (4 * (int64_t)w));
+    rows = std::min(rows, n);
+    int32_t *tmp;
+    IMX_CUDA(cudaMallocAsync((void **)&tmp, sizeof(int32_t) * rows * w, c->st));
+    int rc = IMX_OK;
+    for (int64_t v0 = 0; v0 < n && rc == IMX_OK; v0 += rows) {
+        const int64_t cnt = std::min(rows, n - v0);
+        launch(v0, cnt, tmp);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out + v0 * w, tmp, sizeof(int32_t) * cnt * w, cudaMemcpyDeviceToHost, c->st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "copy window", __FILE__, __LINE__);
+        count_launch(c);
+    }
+    cudaFreeAsync(tmp, c->st);
+    return rc;
+}
+
+}  // namespace imx
+
+using namespace imx;
+
+extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
+    CTX_CHECK(c);
+    if (!c->labels_ready) { set_error("labels not computed (call imx_propagate first)"); return IMX_EINVAL; }
+    const int64_t n = c->g->n;
+    IMX_CUDA(cudaEventRecord(c->ev[4], c->st));
+    if (n) {
+        if (c->C) k_gains<false><<<grid_for(n * 32), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->ns, c->gains);
+        else k_gains<true><<<grid_for(n * 32), 256, 0, c->st>>>(c->L, nullptr, n, c->ld, c->ns, c->gains);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    IMX_CUDA(cudaEventRecord(c->ev[5], c->st));
+    if (gains_out && n)
+        IMX_CUDA(cudaMemcpyAsync(gains_out, c->gains, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    cudaEventElapsedTime(&c->tm.memoize_ms, c->ev[4], c->ev[5]);
+    c->memo_ready = true;
+    return IMX_OK;
+}
+
+extern "C" int imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t *sizes, int64_t ldh) {
+    CTX_CHECK(c);
+    const int64_t n = c->g->n;
+    if (!labels && n) { set_error("labels is NULL"); return IMX_EINVAL; }
+    if (ldh < c->W) { set_error("row stride %lld < width %d", (long long)ldh, c->W); return IMX_EINVAL; }
+    if (!c->C) IMX_CUDA(pool_alloc((void **)&c->C, sizeof(uint32_t) * (size_t)(n > 0 ? n : 1) * c->ld, c->st));
+    if (n) {
+        const size_t bytes = sizeof(uint32_t) * (size_t)n * c->ld;
+        IMX_CUDA(cudaMemsetAsync(c->L, 0, bytes, c->st));
+        IMX_CUDA(cudaMemcpy2DAsync(c->L, sizeof(uint32_t) * c->ld, labels, sizeof(int32_t) * ldh,
+                                   sizeof(int32_t) * c->W, n, cudaMemcpyHostToDevice, c->st));
+        unsigned *bad = reinterpret_cast<unsigned *>(c->scratch + 6);
+        IMX_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), c->st));
+        IMX_CUDA(cudaMemsetAsync(c->C, 0, bytes, c->st));
+        if (sizes) {
+            IMX_CUDA(cudaMemcpy2DAsync(c->C, sizeof(uint32_t) * c->ld, sizes, sizeof(int32_t) * ldh,
+                                       sizeof(int32_t) * c->W, n, cudaMemcpyHostToDevice, c->st));
+        } else {
+            k_hist_full<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, bad);
+            IMX_CHECK_LAUNCH();
+            count_launch(c);
+        }
+        unsigned hb = 0;
+        IMX_CUDA(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        if (hb) { set_error("label outside 0..n-1"); return IMX_EINVAL; }
+    }
+    c->labels_ready = true;
+    c->memo_ready = false;
+    c->celf_ready = false;
+    return IMX_OK;
+}
+
+extern "C" int imx_copy_labels(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out) {
+    CTX_CHECK(c);
+    if (r0 < 0 || r1 > c->W || r0 > r1) { set_error("lane window [%d, %d) invalid", r0, r1); return IMX_EINVAL; }
+    if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
+    if (c->g->n == 0 || r1 == r0) return IMX_OK;
+    const bool enc = c->C == nullptr;
+    return copy_window(c, r0, r1, out, [&](int64_t v0, int64_t cnt, int32_t *tmp) {
+        if (enc) k_labels_window<true><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, v0, cnt, c->ld, r0, r1, tmp);
+        else k_labels_window<false><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, v0, cnt, c->ld, r0, r1, tmp);
+    });
+}
+
+extern "C" int imx_copy_sizes(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out) {
+    CTX_CHECK(c);
+    if (r0 < 0 || r1 > c->W || r0 > r1) { set_error("lane window [%d, %d) invalid", r0, r1); return IMX_EINVAL; }
+    if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
+    if (c->g->n == 0 || r1 == r0) return IMX_OK;
+    const bool enc = c->C == nullptr;
+    return copy_window(c, r0, r1, out, [&](int64_t v0, int64_t cnt, int32_t *tmp) {
+        if (enc) k_sizes_window<true><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, nullptr, v0, cnt, c->ld, r0, r1, tmp);
+        else k_sizes_window<false><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, c->C, v0, cnt, c->ld, r0, r1, tmp);
+    });
+}

@@ -1,0 +1,683 @@
+// propagate.cu -- K2+K3: fused sample + connected components over all lanes
+// of a context (reference propagate, propagation.py:260-321).
+//
+// The reference drives min-label sweeps to their unique fixpoint (min vertex
+// id of every vertex's component in every sampled graph).  Any exact CC
+// algorithm reaches the same fixpoint, so the device runs ONE
+// concurrent union-find pass (uf.cuh) whose sampler is fused into it -- edge
+// membership (X[r] ^ hash) < thr is decided where the edge is visited and
+// never materialised -- followed by one compression pass:
+//
+//   sampler/hook  one of three strategies (hook_mode):
+//     enum   sorted-hash interval enumeration: only live (edge, lane) pairs
+//     pull   first-hop forest (every vertex points at its smallest live
+//            smaller neighbour, written row by row) + unions of the rest
+//     dense  edge-major scan of all lanes with a per-warp union queue
+//   compress L[v][r] <- root; root cell counts its other members
+//   verify   (optional) every live edge joins equal labels, labels are roots
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <cub/cub.cuh>
+
+#include "ctx.cuh"
+#include "uf.cuh"
+
+namespace imx {
+
+// every cell starts as a root with no other members
+__global__ void k_init(uint32_t *__restrict__ L, int64_t cells4) {
+    uint4 *L4 = reinterpret_cast<uint4 *>(L);
+    const uint4 r4 = make_uint4(ROOT, ROOT, ROOT, ROOT);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cells4;
+         i += (int64_t)gridDim.x * blockDim.x)
+        L4[i] = r4;
+}
+
+// Sampler + hooking.  A warp takes tiles of 32 undirected edges (one edge per
+// thread, coalesced loads of (lo, hi), hash and threshold), then walks the
+// tile edge by edge: each thread tests 4 consecutive lanes of a 128-lane
+// chunk against the edge ((X[r] ^ h) < t, X staged in shared memory once per
+// CTA), and the live (edge, lane) pairs are appended to a per-warp queue in
+// shared memory.  Whenever the queue holds 32 pairs the warp drains 32 at
+// once -- one union per thread -- so the latency-bound root searches always
+// run 32-wide instead of at the ~1% density of live lanes.  The adjacency and
+// hash are read once per edge and reused across all W lanes.
+constexpr int kHookWarps = 8;
+constexpr int kQ = 32 + 128;  // drain threshold + one chunk's worth of appends
+
+template <bool UNI>
+__global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
+                                                          const int32_t *__restrict__ ET, int32_t tu, int64_t me,
+                                                          const int32_t *__restrict__ X, int32_t W, int64_t ld,
+                                                          uint32_t *__restrict__ L,
+                                                          unsigned long long *__restrict__ hooks) {
+    extern __shared__ int4 smem4[];
+    int32_t *sX = reinterpret_cast<int32_t *>(smem4);
+    for (int i = threadIdx.x; i < ld; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *qlo = reinterpret_cast<uint32_t *>(sX + ld) + warp * 3 * kQ;
+    uint32_t *qhi = qlo + kQ;
+    uint32_t *qr = qhi + kQ;
+    __syncthreads();
+    const int nq = (int)(ld >> 2);
+    const unsigned FULL = 0xffffffffu;
+    int qn = 0;  // warp-uniform queue length
+    unsigned long long nh = 0;
+    for (int64_t base = ((int64_t)blockIdx.x * kHookWarps + warp) * 32; base < me;
+         base += (int64_t)gridDim.x * kHookWarps * 32) {
+        const int64_t e = base + lane;
+        int2 uv = make_int2(0, 0);
+        int32_t h = 0, t = 0;  // t = 0: nothing is live
+        if (e < me) {
+            uv = __ldg(&E[e]);
+            h = __ldg(&EH[e]);
+            t = UNI ? tu : __ldg(&ET[e]);
+        }
+        const int cnt = (int)(me - base < 32 ? me - base : 32);
+        for (int j = 0; j < cnt; ++j) {
+            const int32_t hj = __shfl_sync(FULL, h, j), tj = __shfl_sync(FULL, t, j);
+            const uint32_t lo = (uint32_t)__shfl_sync(FULL, uv.x, j);
+            const uint32_t hi = (uint32_t)__shfl_sync(FULL, uv.y, j);
+            for (int c0 = 0; c0 < nq; c0 += 32) {
+                const int qd = c0 + lane;
+                unsigned live = 0;
+                if (qd < nq) {
+                    const int4 x = smem4[qd];
+                    live = ((unsigned)((x.x ^ hj) < tj)) | ((unsigned)((x.y ^ hj) < tj) << 1) |
+                           ((unsigned)((x.z ^ hj) < tj) << 2) | ((unsigned)((x.w ^ hj) < tj) << 3);
+                    const int r = qd << 2;
+                    if (r + 4 > W) live &= (1u << (W > r ? W - r : 0)) - 1u;
+                }
+                if (!__any_sync(FULL, live != 0)) continue;
+                const int k = __popc(live);
+                int inc = k;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                int pos = qn + inc - k;
+                while (live) {
+                    const int b = __ffs(live) - 1;
+                    live &= live - 1;
+                    qlo[pos] = lo;
+                    qhi[pos] = hi;
+                    qr[pos] = (uint32_t)((qd << 2) + b);
+                    ++pos;
+                }
+                qn += __shfl_sync(FULL, inc, 31);
+                __syncwarp();
+                while (qn >= 32) {
+                    qn -= 32;
+                    const uint32_t a = qlo[qn + lane], bb = qhi[qn + lane];
+                    const int r = (int)qr[qn + lane];
+                    __syncwarp();
+                    nh += unite(L, ld, a, bb, r);
+                }
+            }
+        }
+    }
+    __syncwarp();
+    if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
+    if (hooks) {
+        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
+        if (lane == 0 && nh) atomicAdd(hooks, nh);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Sampler by interval enumeration (default).  For a threshold t and a lane
+// word x, {h : (x ^ h) < t} is the union over the set bits i of t of the
+// aligned hash interval [((t ^ x) >> (i+1) << (i+1)) | (x & 2^i), +2^i)
+// (the reference's _xor_below, propagation.py:104-118).  The undirected
+// edges are sorted by (threshold bucket, hash) on the device (graph.cu), so a
+// (lane, bucket, bit) segment is a contiguous range of edges found by two
+// binary searches, and the live (edge, lane) pairs of all lanes form one
+// flattened index space: no dead (edge, lane) pair is ever visited.  With
+// per-edge thresholds a bucket's interval uses the bucket's max threshold
+// and each enumerated edge is re-tested exactly ((x ^ h) < thr, strict).
+// ---------------------------------------------------------------------------
+__global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
+                            const int32_t *__restrict__ btmax, const int64_t *__restrict__ boff,
+                            const int32_t *__restrict__ EH, int64_t *__restrict__ seg_a,
+                            int64_t *__restrict__ seg_n) {
+    const int64_t nseg = (int64_t)W * nb * 31;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(s / (nb * 31));
+        const int rem = (int)(s - (int64_t)r * nb * 31);
+        const int b = rem / 31, i = rem - b * 31;
+        const uint32_t t = (uint32_t)btmax[b];
+        int64_t a = boff[b], cnt = 0;
+        if ((t >> i) & 1u) {
+            const uint32_t x = (uint32_t)X[r];
+            const uint64_t start = ((uint64_t)((t ^ x) >> (i + 1)) << (i + 1)) | (uint64_t)(x & (1u << i));
+            const uint64_t end = start + (1ull << i);
+            int64_t lo = boff[b], hi = boff[b + 1];
+            while (lo < hi) {  // lower_bound(start)
+                const int64_t mid = (lo + hi) >> 1;
+                if ((uint64_t)(uint32_t)EH[mid] < start) lo = mid + 1; else hi = mid;
+            }
+            a = lo;
+            hi = boff[b + 1];
+            while (lo < hi) {  // lower_bound(end)
+                const int64_t mid = (lo + hi) >> 1;
+                if ((uint64_t)(uint32_t)EH[mid] < end) lo = mid + 1; else hi = mid;
+            }
+            cnt = lo - a;
+        }
+        seg_a[s] = a;
+        seg_n[s] = cnt;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) seg_n[nseg] = 0;
+}
+
+// Every thread takes flattened live pairs j; a warp owns chunks of kEnumChunk
+// consecutive j (one binary search over the segment offsets per chunk, then
+// a forward walk), so consecutive threads read consecutive edges of the same
+// hash interval (coalesced) and every thread runs one union per pair.
+constexpr int kEnumChunk = 1024;
+template <bool UNI>
+__global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ off, const int64_t *__restrict__ seg_a,
+                                                   int64_t nseg, int segs_per_lane,
+                                                   const int2 *__restrict__ E, const int32_t *__restrict__ EH,
+                                                   const int32_t *__restrict__ ET, const int32_t *__restrict__ X,
+                                                   int64_t ld, uint32_t *__restrict__ L,
+                                                   unsigned long long *__restrict__ hooks) {
+    const int64_t total = off[nseg];
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long nh = 0;
+    for (int64_t j0 = wg * kEnumChunk; j0 < total; j0 += nw * kEnumChunk) {
+        int64_t s = 0;
+        if (lane == 0) {
+            int64_t lo = 0, hi = nseg;       // largest s with off[s] <= j0
+            while (hi - lo > 1) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (off[mid] <= j0) lo = mid; else hi = mid;
+            }
+            s = lo;
+        }
+        s = __shfl_sync(0xffffffffu, s, 0);
+        const int64_t jend = (total - j0 < kEnumChunk) ? total : j0 + kEnumChunk;
+        for (int64_t j = j0 + lane; j < jend; j += 32) {
+            while (off[s + 1] <= j) ++s;
+            const int64_t e = seg_a[s] + (j - off[s]);
+            const int r = (int)(s / segs_per_lane);
+            if (!UNI && !((X[r] ^ EH[e]) < ET[e])) continue;
+            const int2 uv = E[e];
+            nh += unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r);
+        }
+    }
+    if (hooks) {
+        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(0xffffffffu, nh, o);
+        if (lane == 0 && nh) atomicAdd(hooks, nh);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pull sampler (dense live fraction).  Rows are sorted ascending, so the
+// smaller neighbours of v are a prefix of its row.  Pass 1 writes, for every
+// lane, L[v][r] = the smallest live smaller neighbour (or v) and C[v][r] = 0:
+// a forest whose edges are live edges pointing to smaller ids, built with
+// coalesced row writes and no random reads (it replaces the init kernel).
+// Pass 2 rescans the same prefixes and unites only the live edges that are
+// not a vertex's first live smaller neighbour -- 4-30% of the live pairs on
+// the benchmark graphs -- through the per-warp queue of k_hook.
+// ---------------------------------------------------------------------------
+template <int PASS, bool UNI>
+__global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                                              const int32_t *__restrict__ hash, const int32_t *__restrict__ thr,
+                                              int32_t tu, int64_t n, const int32_t *__restrict__ X, int32_t W,
+                                              int64_t ld, uint32_t *__restrict__ L,
+                                              unsigned long long *__restrict__ hooks) {
+    extern __shared__ int4 smem4[];
+    int32_t *sX = reinterpret_cast<int32_t *>(smem4);
+    for (int i = threadIdx.x; i < ld; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *qlo = reinterpret_cast<uint32_t *>(sX + ld) + warp * 3 * kQ;
+    uint32_t *qhi = qlo + kQ;
+    uint32_t *qr = qhi + kQ;
+    __syncthreads();
+    const int nq = (int)(ld >> 2);
+    const unsigned FULL = 0xffffffffu;
+    int qn = 0;
+    unsigned long long nh = 0;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = wg; v < n; v += nw) {
+        const int64_t s0 = xadj[v], s1 = xadj[v + 1];
+        for (int c0 = 0; c0 < nq; c0 += 32) {
+            const int qd = c0 + lane;
+            const bool active = qd < nq;
+            int4 x = make_int4(0, 0, 0, 0);
+            if (active) x = smem4[qd];
+            const int r = qd << 2;
+            unsigned valid = 0xFu;
+            if (r + 4 > W) valid = (1u << (W > r ? W - r : 0)) - 1u;
+            if (!active) valid = 0;
+            uint32_t best[4] = {ROOT, ROOT, ROOT, ROOT};
+            unsigned seen = 0;
+            for (int64_t sl = s0; sl < s1; ++sl) {
+                const uint32_t u = (uint32_t)__ldg(adj + sl);
+                if (u >= (uint32_t)v) break;
+                const int32_t h = __ldg(hash + sl);
+                const int32_t t = UNI ? tu : __ldg(thr + sl);
+                unsigned live = ((unsigned)((x.x ^ h) < t)) | ((unsigned)((x.y ^ h) < t) << 1) |
+                                ((unsigned)((x.z ^ h) < t) << 2) | ((unsigned)((x.w ^ h) < t) << 3);
+                live &= valid;
+                if (PASS == 1) {
+                    unsigned fresh = live & ~seen;
+                    while (fresh) {
+                        const int j = __ffs(fresh) - 1;
+                        fresh &= fresh - 1;
+                        best[j] = u;
+                    }
+                    seen |= live;
+                } else {
+                    unsigned rest = live & seen;
+                    seen |= live;
+                    if (!__any_sync(FULL, rest != 0)) continue;
+                    const int k = __popc(rest);
+                    int inc = k;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULL, inc, o);
+                        if (lane >= o) inc += y;
+                    }
+                    int pos = qn + inc - k;
+                    while (rest) {
+                        const int b = __ffs(rest) - 1;
+                        rest &= rest - 1;
+                        qlo[pos] = u;
+                        qhi[pos] = (uint32_t)v;
+                        qr[pos] = (uint32_t)(r + b);
+                        ++pos;
+                    }
+                    qn += __shfl_sync(FULL, inc, 31);
+                    __syncwarp();
+                    while (qn >= 32) {
+                        qn -= 32;
+                        const uint32_t a = qlo[qn + lane], bb = qhi[qn + lane];
+                        const int rr = (int)qr[qn + lane];
+                        __syncwarp();
+                        nh += unite(L, ld, a, bb, rr);
+                    }
+                }
+            }
+            if (PASS == 1 && active) {
+                *(reinterpret_cast<uint4 *>(L + v * ld) + qd) = make_uint4(best[0], best[1], best[2], best[3]);
+            }
+        }
+    }
+    if (PASS == 2) {
+        __syncwarp();
+        if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
+    }
+    if (hooks) {
+        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
+        if (lane == 0 && nh) atomicAdd(hooks, nh);
+    }
+}
+
+// Full compression + component count, one thread per 16-byte quad of a label
+// row (full occupancy: the latency of the root searches is hidden by thread
+// parallelism).  Non-root cells get their root and add 1 to the root cell's
+// member count; root cells are never stored by their owner (their count is
+// being incremented concurrently), only non-root lanes are written back.
+__global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
+                                                  unsigned long long *__restrict__ nonroot) {
+    const int64_t nq = ld >> 2;
+    unsigned long long cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / nq;
+        const int r = (int)(i - v * nq) << 2;
+        const uint4 l = reinterpret_cast<const uint4 *>(L)[i];
+        const uint32_t w[4] = {l.x, l.y, l.z, l.w};
+        uint32_t pw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            pw[j] = (r + j < W && !is_root(w[j])) ? ld_relaxed(cell(L, ld, w[j], r + j)) : ROOT;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (r + j >= W || is_root(w[j])) continue;
+            uint32_t x = (uint32_t)v, p = w[j], gw = pw[j];
+            while (!is_root(gw)) {          // path splitting, min-safe
+                atomicMin(cell(L, ld, x, r + j), gw);
+                x = p;
+                p = gw;
+                gw = ld_relaxed(cell(L, ld, p, r + j));
+            }
+            if (p != w[j]) L[v * ld + r + j] = p;
+            atomicAdd(cell(L, ld, p, r + j), 1u);
+            ++cnt;
+        }
+    }
+    if (nonroot) {
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nonroot, cnt);
+    }
+}
+
+// Verification sweep: live (edge, lane) pairs whose endpoint labels differ,
+// and non-root cells that do not point at a smaller root.
+template <bool UNI>
+__global__ void k_verify_edges(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
+                               const int32_t *__restrict__ ET, int32_t tu, int64_t me,
+                               const int32_t *__restrict__ X, int32_t W, int64_t ld,
+                               const uint32_t *__restrict__ L, unsigned long long *__restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long nb = 0;
+    for (int64_t e = wg; e < me; e += nw) {
+        const int2 uv = E[e];
+        const int32_t h = EH[e];
+        const int32_t t = UNI ? tu : ET[e];
+        for (int r = lane; r < W; r += 32)
+            if ((X[r] ^ h) < t &&
+                label_of(uv.x, L[(int64_t)uv.x * ld + r]) != label_of(uv.y, L[(int64_t)uv.y * ld + r]))
+                ++nb;
+    }
+    for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if (lane == 0 && nb) atomicAdd(bad, nb);
+}
+__global__ void k_verify_roots(const uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
+                               unsigned long long *__restrict__ bad) {
+    unsigned long long nb = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / W;
+        const int r = (int)(i - v * W);
+        const uint32_t w = L[v * ld + r];
+        if (!is_root(w) && (w >= (uint32_t)v || !is_root(L[(int64_t)w * ld + r]))) ++nb;
+    }
+    for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if ((threadIdx.x & 31) == 0 && nb) atomicAdd(bad, nb);
+}
+
+__global__ void k_label_sum(const uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
+                            unsigned long long *__restrict__ out) {
+    unsigned long long s = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / W;
+        const int r = (int)(i - v * W);
+        s += label_of((uint32_t)v, L[v * ld + r]);
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+__global__ void k_flush(uint4 *buf, int64_t cnt, uint32_t salt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = make_uint4(salt, (uint32_t)i, salt, (uint32_t)i);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+int run_init(imx_ctx *c) {
+    const int64_t n = c->g->n;
+    if (n == 0) return IMX_OK;
+    const int64_t cells4 = n * (c->ld >> 2);
+    k_init<<<grid_for(cells4), 256, 0, c->st>>>(c->L, cells4);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    return IMX_OK;
+}
+
+static int run_hook_dense(imx_ctx *c, unsigned long long *hooks) {
+    imx_graph *g = c->g;
+    const size_t smem = sizeof(int32_t) * c->ld + sizeof(uint32_t) * 3 * kQ * kHookWarps;
+    if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
+    const int64_t tiles = ceil_div(g->me, 32);
+    int blocks = (int)std::min<int64_t>(ceil_div(tiles, kHookWarps), 148 * 8);
+    auto kern = g->uniform ? k_hook<true> : k_hook<false>;
+    if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<blocks, kHookWarps * 32, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
+                                                    c->ld, c->L, hooks);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    return IMX_OK;
+}
+
+static int run_hook_enum(imx_ctx *c, unsigned long long *hooks) {
+    imx_graph *g = c->g;
+    const int64_t nseg = (int64_t)c->W * g->nb * 31;
+    if (nseg + 1 > c->nseg_cap) {
+        for (int64_t **p : {&c->seg_a, &c->seg_n, &c->seg_off}) { if (*p) cudaFree(*p); *p = nullptr; }
+        c->nseg_cap = 0;
+        IMX_CUDA(cudaMalloc((void **)&c->seg_a, sizeof(int64_t) * (nseg + 1)));
+        IMX_CUDA(cudaMalloc((void **)&c->seg_n, sizeof(int64_t) * (nseg + 1)));
+        IMX_CUDA(cudaMalloc((void **)&c->seg_off, sizeof(int64_t) * (nseg + 1)));
+        c->nseg_cap = nseg + 1;
+        size_t tb = 0;
+        IMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
+        if (tb > c->scan_tmp_bytes) {
+            if (c->scan_tmp) cudaFree(c->scan_tmp);
+            IMX_CUDA(cudaMalloc(&c->scan_tmp, tb));
+            c->scan_tmp_bytes = tb;
+        }
+    }
+    k_seg_count<<<grid_for(nseg), 256, 0, c->st>>>(c->X, c->W, g->nb, g->btmax, g->boff, g->EH,
+                                                   c->seg_a, c->seg_n);
+    IMX_CHECK_LAUNCH();
+    size_t tb = c->scan_tmp_bytes;
+    IMX_CUDA(cub::DeviceScan::ExclusiveSum(c->scan_tmp, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
+    const int blocks = 148 * 8;
+    if (g->uniform)
+        k_hook_enum<true><<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH,
+                                                     g->ET, c->X, c->ld, c->L, hooks);
+    else
+        k_hook_enum<false><<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH,
+                                                      g->ET, c->X, c->ld, c->L, hooks);
+    IMX_CHECK_LAUNCH();
+    count_launch(c, 3);
+    return IMX_OK;
+}
+
+static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
+    imx_graph *g = c->g;
+    const int64_t n = g->n;
+    if (n == 0) return IMX_OK;
+    const size_t smem = sizeof(int32_t) * c->ld + sizeof(uint32_t) * 3 * kQ * 8;
+    if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
+    const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 8);
+    auto kern = pass == 1 ? (g->uniform ? k_pull<1, true> : k_pull<1, false>)
+                          : (g->uniform ? k_pull<2, true> : k_pull<2, false>);
+    if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<blocks, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld,
+                                       c->L, hooks);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    return IMX_OK;
+}
+
+// Sampler strategy.  Interval enumeration touches only live (edge, lane)
+// pairs but each costs ~4 random label accesses; the pull passes cost two
+// dense membership scans (ALU only) plus random accesses for the non-forest
+// live edges only, but a warp owns a whole row prefix, so a very long prefix
+// (a high-degree vertex with many smaller neighbours) serialises.
+enum { HOOK_ENUM = 0, HOOK_PULL = 1, HOOK_DENSE = 2 };
+static int hook_mode(const imx_graph *g) {
+    const char *m = getenv("IMX_HOOK");
+    if (m && !strcmp(m, "dense")) return HOOK_DENSE;
+    if (m && !strcmp(m, "enum")) return HOOK_ENUM;
+    if (m && !strcmp(m, "pull")) return HOOK_PULL;
+    const char *t = getenv("IMX_PULL_MIN_P");
+    const double pmin = t ? atof(t) : 0.02;
+    const double balanced_prefix = 8.0 * (double)g->me / (148.0 * 64.0);
+    if (g->thr_mean >= pmin && (double)g->max_prefix <= std::max(64.0, balanced_prefix)) return HOOK_PULL;
+    return HOOK_ENUM;
+}
+
+// init + hook phases of one propagate (events bracket them)
+static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_init, cudaEvent_t e_hook) {
+    imx_graph *g = c->g;
+    const int mode = g->me ? hook_mode(g) : HOOK_ENUM;
+    if (mode == HOOK_PULL) {
+        IMX_TRY(run_pull(c, 1, nullptr));
+        if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));
+        IMX_TRY(run_pull(c, 2, hooks));
+    } else {
+        IMX_TRY(run_init(c));
+        if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));
+        if (g->me) IMX_TRY(mode == HOOK_DENSE ? run_hook_dense(c, hooks) : run_hook_enum(c, hooks));
+    }
+    if (e_hook) IMX_CUDA(cudaEventRecord(e_hook, c->st));
+    c->tm.hook_launches++;
+    return IMX_OK;
+}
+
+static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
+    const int64_t n = c->g->n;
+    if (n == 0) return IMX_OK;
+    k_compress<<<grid_for(n * (c->ld >> 2)), 256, 0, c->st>>>(c->L, n, c->ld, c->W, nonroot);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    return IMX_OK;
+}
+
+static int label_sum(imx_ctx *c, int64_t *out) {
+    const int64_t n = c->g->n;
+    IMX_CUDA(cudaMemsetAsync(c->scratch + 4, 0, sizeof(unsigned long long), c->st));
+    if (n) {
+        k_label_sum<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->ld, c->W, c->scratch + 4);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    unsigned long long s = 0;
+    IMX_CUDA(cudaMemcpyAsync(&s, c->scratch + 4, sizeof s, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    *out = (int64_t)s;
+    return IMX_OK;
+}
+
+static void push_stat(imx_prop_stats *st, int mode, int64_t changed, int64_t lsum) {
+    if (!st) return;
+    int i = st->sweeps++;
+    if (i < st->cap) {
+        if (st->changed_pairs) st->changed_pairs[i] = changed;
+        if (st->label_sums) st->label_sums[i] = lsum;
+        if (st->modes) st->modes[i] = mode;
+    }
+}
+
+}  // namespace imx
+
+using namespace imx;
+
+extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
+    CTX_CHECK(c);
+    imx_graph *g = c->g;
+    const int64_t n = g->n;
+    if (st) st->sweeps = 0;
+    unsigned long long *sc = c->scratch;
+    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long) * 4, c->st));
+    IMX_CUDA(cudaEventRecord(c->ev[0], c->st));
+    if (g->m2 > 0) {
+        IMX_TRY(run_sample_cc(c, st ? sc : nullptr, c->ev[1], c->ev[2]));
+        IMX_TRY(run_compress(c, st ? sc + 1 : nullptr));
+    } else {
+        IMX_TRY(run_init(c));
+        IMX_CUDA(cudaEventRecord(c->ev[1], c->st));
+        IMX_CUDA(cudaEventRecord(c->ev[2], c->st));
+    }
+    IMX_CUDA(cudaEventRecord(c->ev[3], c->st));
+    IMX_CUDA(cudaEventSynchronize(c->ev[3]));
+    cudaEventElapsedTime(&c->tm.init_ms, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&c->tm.hook_ms, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&c->tm.compress_ms, c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&c->tm.propagate_ms, c->ev[0], c->ev[3]);
+    c->labels_ready = true;
+    c->memo_ready = false;
+    c->celf_ready = false;
+    if (c->C) { cudaFreeAsync(c->C, c->st); c->C = nullptr; }   // back to encoded mode
+    if (g->m2 == 0) return IMX_OK;  // propagation.py:276-278: edgeless -> identity, no sweeps
+    // One union-find pass reaches the fixpoint: it is reported as one sweep
+    // whose changed count is the number of (vertex, lane) labels that moved
+    // off the identity, followed (when asked) by the no-change sweep that
+    // proves convergence, as the reference's loop does (propagation.py:304-320).
+    int64_t changed = 0, lsum = 0;
+    if (st) {
+        unsigned long long hc[2];
+        IMX_CUDA(cudaMemcpyAsync(hc, sc, sizeof hc, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        IMX_TRY(label_sum(c, &lsum));
+        changed = (int64_t)hc[1];
+        push_stat(st, IMX_MODE_HOOK, changed, lsum);
+    }
+    if (verify || (st && changed > 0)) {
+        IMX_CUDA(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->st));
+        if (g->me) {
+            if (g->uniform)
+                k_verify_edges<true><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->ld, c->L, sc + 2);
+            else
+                k_verify_edges<false><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->ld, c->L, sc + 2);
+            IMX_CHECK_LAUNCH();
+        }
+        k_verify_roots<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->ld, c->W, sc + 2);
+        IMX_CHECK_LAUNCH();
+        count_launch(c, 2);
+        unsigned long long bad = 0;
+        IMX_CUDA(cudaMemcpyAsync(&bad, sc + 2, sizeof bad, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        if (bad) {
+            set_error("propagation self-check failed: %llu violations", bad);
+            return IMX_EINTERNAL;
+        }
+        if (st && changed > 0) push_stat(st, IMX_MODE_VERIFY, 0, lsum);
+    }
+    return IMX_OK;
+}
+
+extern "C" int imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2, float *avg_total_ms,
+                                   float *avg_hook_ms, float *avg_compress_ms, float *avg_init_ms) {
+    CTX_CHECK(c);
+    if (reps < 1) { set_error("reps must be >= 1"); return IMX_EINVAL; }
+    uint4 *fb = nullptr;
+    const int64_t fcnt = (int64_t(256) << 20) / 16;  // 256 MB > 126 MB L2
+    if (flush_l2) IMX_CUDA(cudaMalloc((void **)&fb, fcnt * 16));
+    std::vector<cudaEvent_t> ev(4 * reps);
+    for (auto &e : ev) IMX_CUDA(cudaEventCreate(&e));
+    if (c->C) { cudaFreeAsync(c->C, c->st); c->C = nullptr; }
+    for (int i = 0; i < reps; ++i) {
+        if (fb) k_flush<<<148 * 8, 256, 0, c->st>>>(fb, fcnt, (uint32_t)i);
+        IMX_CUDA(cudaEventRecord(ev[4 * i], c->st));
+        if (c->g->m2) {
+            IMX_TRY(run_sample_cc(c, nullptr, ev[4 * i + 1], ev[4 * i + 2]));
+            IMX_TRY(run_compress(c, nullptr));
+        } else {
+            IMX_TRY(run_init(c));
+            IMX_CUDA(cudaEventRecord(ev[4 * i + 1], c->st));
+            IMX_CUDA(cudaEventRecord(ev[4 * i + 2], c->st));
+        }
+        IMX_CUDA(cudaEventRecord(ev[4 * i + 3], c->st));
+    }
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    double tot = 0, hk = 0, cp = 0, in = 0;
+    for (int i = 0; i < reps; ++i) {
+        float a, b, d, e;
+        cudaEventElapsedTime(&a, ev[4 * i], ev[4 * i + 3]);
+        cudaEventElapsedTime(&b, ev[4 * i + 1], ev[4 * i + 2]);
+        cudaEventElapsedTime(&d, ev[4 * i + 2], ev[4 * i + 3]);
+        cudaEventElapsedTime(&e, ev[4 * i], ev[4 * i + 1]);
+        tot += a; hk += b; cp += d; in += e;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    if (fb) cudaFree(fb);
+    if (avg_total_ms) *avg_total_ms = (float)(tot / reps);
+    if (avg_hook_ms) *avg_hook_ms = (float)(hk / reps);
+    if (avg_compress_ms) *avg_compress_ms = (float)(cp / reps);
+    if (avg_init_ms) *avg_init_ms = (float)(in / reps);
+    c->labels_ready = true;
+    c->memo_ready = false;
+    c->celf_ready = false;
+    return IMX_OK;
+}

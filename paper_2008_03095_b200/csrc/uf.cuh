@@ -1,0 +1,79 @@
+// uf.cuh -- concurrent union-find over one lane of the label matrix.
+//
+// Every lane r is an independent sampled graph; its forest lives in column r
+// of L.  Cells are either ROOT|count (bit 31 set) or a parent pointer to a
+// strictly smaller id, so the root of every tree is its minimum vertex id --
+// exactly the min-id label the reference's propagation converges to (SURVEY
+// S6, propagation.py:1-8).  All accesses go through L2 (relaxed, gpu scope).
+#pragma once
+#include "common.cuh"
+
+namespace imx {
+
+constexpr uint32_t ROOT = 0x80000000u;
+constexpr uint32_t COUNT = 0x7FFFFFFFu;
+
+__device__ __forceinline__ uint32_t *cell(uint32_t *L, int64_t ld, uint32_t v, int r) {
+    return L + (int64_t)v * ld + r;
+}
+__device__ __forceinline__ bool is_root(uint32_t w) { return (w & ROOT) != 0; }
+// label of vertex v from its (compressed) cell word
+__device__ __forceinline__ uint32_t label_of(uint32_t v, uint32_t w) { return is_root(w) ? v : w; }
+
+// Two root searches advanced in lock step so their loads overlap.  Path
+// splitting: every visited node is re-pointed at its grandparent (benign
+// races -- any value ever stored in a cell is an ancestor in the same tree).
+// On entry wa = L[xa], wb = L[xb]; on exit xa, xb are roots.
+__device__ __forceinline__ void find2(uint32_t *L, int64_t ld, int r, uint32_t &xa, uint32_t wa,
+                                      uint32_t &xb, uint32_t wb) {
+    for (;;) {
+        const bool da = is_root(wa), db = is_root(wb);
+        if (da && db) return;
+        uint32_t ga = 0, gb = 0;
+        if (!da) ga = ld_relaxed(cell(L, ld, wa, r));
+        if (!db) gb = ld_relaxed(cell(L, ld, wb, r));
+        if (!da) {
+            if (!is_root(ga)) st_relaxed(cell(L, ld, xa, r), ga);
+            xa = wa;
+            wa = ga;
+        }
+        if (!db) {
+            if (!is_root(gb)) st_relaxed(cell(L, ld, xb, r), gb);
+            xb = wb;
+            wb = gb;
+        }
+    }
+}
+
+// Union of a and b in lane r: CAS-hook the larger root under the smaller.
+// During hooking every root cell is exactly ROOT (member counts are only
+// written by the compress pass).  Returns 1 when a hook happened.
+__device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32_t b, int r) {
+    uint32_t wa = ld_relaxed(cell(L, ld, a, r));
+    uint32_t wb = ld_relaxed(cell(L, ld, b, r));
+    find2(L, ld, r, a, wa, b, wb);
+    while (a != b) {
+        const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+        const uint32_t old = atomicCAS(cell(L, ld, hi, r), ROOT, lo);
+        if (old == ROOT) return 1;
+        a = lo;
+        b = hi;
+        find2(L, ld, r, a, ld_relaxed(cell(L, ld, lo, r)), b, old);
+    }
+    return 0;
+}
+
+// Root of x given its parent p (p = L[x], not a root word); re-points each
+// visited node at its grandparent with atomicMin, so it is safe against the
+// owners' final stores of the root (the smallest id of the tree).
+__device__ __forceinline__ uint32_t find_split(uint32_t *L, int64_t ld, uint32_t x, uint32_t p, int r) {
+    for (;;) {
+        const uint32_t gw = ld_relaxed(cell(L, ld, p, r));
+        if (is_root(gw)) return p;
+        atomicMin(cell(L, ld, x, r), gw);
+        x = p;
+        p = gw;
+    }
+}
+
+}  // namespace imx

@@ -323,43 +323,66 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
     }
 }
 
-// Full compression + component count, one thread per 16-byte quad of a label
-// row (full occupancy: the latency of the root searches is hidden by thread
-// parallelism).  Non-root cells get their root and add 1 to the root cell's
-// member count; root cells are never stored by their owner (their count is
-// being incremented concurrently), only non-root lanes are written back.
+// Full compression + component count.  A CTA owns one 128-lane chunk (a
+// 16-byte quad per thread) and strides over vertices.  Hub vertices -- the
+// kHot smallest ids, which are the roots of the giant components of skewed
+// graphs in nearly every lane -- are read from a shared-memory snapshot of
+// their cells taken at kernel start (roots are final after hooking, and a
+// stale parent pointer is still an ancestor), and members of hub-rooted
+// components are counted in shared memory and flushed once per CTA.  Other
+// non-root cells walk to their root with min-safe path splitting, store it,
+// and add 1 to the root cell's member count.  Root cells are never stored by
+// their owner (their count is being incremented concurrently).
+constexpr int kHot = 32;
+constexpr int kChunkLanes = 128;
+
 __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
                                                   unsigned long long *__restrict__ nonroot) {
+    __shared__ uint32_t hw[kHot][kChunkLanes];   // hub cell snapshot
+    __shared__ uint32_t hc[kHot][kChunkLanes];   // hub-root member counts
+    const int lane0 = blockIdx.y * kChunkLanes;
+    for (int i = threadIdx.x; i < kHot * kChunkLanes; i += blockDim.x) {
+        const int p = i / kChunkLanes, j = i % kChunkLanes;
+        hw[p][j] = (p < n && lane0 + j < W) ? ld_relaxed(L + (int64_t)p * ld + lane0 + j) : ROOT;
+        hc[p][j] = 0;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nq = ld >> 2;
+    const int64_t q = (int64_t)blockIdx.y * 32 + lane;
+    const int r = (int)(q << 2);
     unsigned long long cnt = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * nq;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / nq;
-        const int r = (int)(i - v * nq) << 2;
-        const uint4 l = reinterpret_cast<const uint4 *>(L)[i];
-        const uint32_t w[4] = {l.x, l.y, l.z, l.w};
-        uint32_t pw[4];
+    if (q < nq) {
+        for (int64_t v = (int64_t)blockIdx.x * 8 + warp; v < n; v += (int64_t)gridDim.x * 8) {
+            const uint4 l = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
+            const uint32_t w[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            pw[j] = (r + j < W && !is_root(w[j])) ? ld_relaxed(cell(L, ld, w[j], r + j)) : ROOT;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (r + j >= W || is_root(w[j])) continue;
-            uint32_t x = (uint32_t)v, p = w[j], gw = pw[j];
-            while (!is_root(gw)) {          // path splitting, min-safe
-                atomicMin(cell(L, ld, x, r + j), gw);
-                x = p;
-                p = gw;
-                gw = ld_relaxed(cell(L, ld, p, r + j));
+            for (int j = 0; j < 4; ++j) {
+                if (r + j >= W || is_root(w[j])) continue;
+                const int lj = lane * 4 + j;
+                uint32_t x = (uint32_t)v, p = w[j];
+                uint32_t gw = p < (uint32_t)kHot ? hw[p][lj] : ld_relaxed(cell(L, ld, p, r + j));
+                while (!is_root(gw)) {          // path splitting, min-safe
+                    atomicMin(cell(L, ld, x, r + j), gw);
+                    x = p;
+                    p = gw;
+                    gw = p < (uint32_t)kHot ? hw[p][lj] : ld_relaxed(cell(L, ld, p, r + j));
+                }
+                if (p != w[j]) L[v * ld + r + j] = p;
+                if (p < (uint32_t)kHot) atomicAdd(&hc[p][lj], 1u);
+                else atomicAdd(cell(L, ld, p, r + j), 1u);
+                ++cnt;
             }
-            if (p != w[j]) L[v * ld + r + j] = p;
-            atomicAdd(cell(L, ld, p, r + j), 1u);
-            ++cnt;
         }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHot * kChunkLanes; i += blockDim.x) {
+        const int p = i / kChunkLanes, j = i % kChunkLanes;
+        if (hc[p][j]) atomicAdd(L + (int64_t)p * ld + lane0 + j, hc[p][j]);
     }
     if (nonroot) {
         for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nonroot, cnt);
+        if (lane == 0 && cnt) atomicAdd(nonroot, cnt);
     }
 }
 
@@ -538,7 +561,9 @@ static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_in
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
-    k_compress<<<grid_for(n * (c->ld >> 2)), 256, 0, c->st>>>(c->L, n, c->ld, c->W, nonroot);
+    const int chunks = (int)ceil_div(c->ld, kChunkLanes);
+    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), (148 * 8 + chunks - 1) / chunks));
+    k_compress<<<dim3(bx, chunks), 256, 0, c->st>>>(c->L, n, c->ld, c->W, nonroot);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;

@@ -41,40 +41,32 @@ __global__ void __launch_bounds__(256) k_gains_caller(const uint32_t *__restrict
     }
 }
 
-// Encoded labels: a CTA owns a 128-lane chunk and strides over vertices;
-// the size words of the hub rows (ids < kHot: the giant-component roots) are
-// snapshotted in shared memory, other roots are gathered from L2/HBM.  Each
-// CTA adds its chunk's partial sums into gains[v] (int64 atomics, exact).
-constexpr int kHotG = 32;
+// Encoded labels: warp per vertex, 16-byte quads of its row; the size of a
+// non-root cell's component is gathered from its root's cell through the
+// read-only path (L is not written during memoization, so hub rows stay in
+// L1/texture cache instead of hammering one L2 line).
 __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ L, int64_t n, int64_t ld,
-                                                   int32_t ns, unsigned long long *__restrict__ gains) {
-    __shared__ uint32_t hw[kHotG][128];
-    const int lane0 = blockIdx.y * 128;
-    for (int i = threadIdx.x; i < kHotG * 128; i += blockDim.x) {
-        const int p = i / 128, j = i % 128;
-        hw[p][j] = (p < n && lane0 + j < ns) ? __ldg(L + (int64_t)p * ld + lane0 + j) : ROOT;
-    }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                                   int32_t ns, int64_t *__restrict__ gains) {
+    const int lane = threadIdx.x & 31;
     const int nqs = (ns + 3) >> 2;
-    const int q = blockIdx.y * 32 + lane;
-    const int r = q << 2;
-    for (int64_t v = (int64_t)blockIdx.x * 8 + warp; v < n; v += (int64_t)gridDim.x * 8) {
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = wg; v < n; v += nw) {
+        const uint4 *Lr = reinterpret_cast<const uint4 *>(L + v * ld);
         unsigned long long acc = 0;
-        if (q < nqs) {
-            const uint4 l = __ldg(reinterpret_cast<const uint4 *>(L + v * ld) + q);
+        for (int q = lane; q < nqs; q += 32) {
+            const uint4 l = __ldg(Lr + q);
             const uint32_t w[4] = {l.x, l.y, l.z, l.w};
+            const int r = q << 2;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (r + j >= ns) break;
-                const uint32_t x = w[j];
-                uint32_t rw = x;
-                if (!is_root(x)) rw = x < (uint32_t)kHotG ? hw[x][lane * 4 + j] : __ldg(L + (int64_t)x * ld + r + j);
+                const uint32_t rw = is_root(w[j]) ? w[j] : __ldg(L + (int64_t)w[j] * ld + r + j);
                 acc += (rw & COUNT) + 1u;
             }
         }
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0 && acc) atomicAdd(gains + v, acc);
+        if (lane == 0) gains[v] = (int64_t)acc;
     }
 }
 
@@ -159,11 +151,7 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
         if (c->C) {
             k_gains_caller<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->ns, c->gains);
         } else {
-            IMX_CUDA(cudaMemsetAsync(c->gains, 0, sizeof(int64_t) * n, c->st));
-            const int chunks = std::max(1, (int)ceil_div(c->ns, 128));
-            const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), (148 * 8 + chunks - 1) / chunks));
-            k_gains_enc<<<dim3(bx, chunks), 256, 0, c->st>>>(c->L, n, c->ld, c->ns,
-                                                            reinterpret_cast<unsigned long long *>(c->gains));
+            k_gains_enc<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, n, c->ld, c->ns, c->gains);
         }
         IMX_CHECK_LAUNCH();
         count_launch(c);

@@ -323,66 +323,70 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
     }
 }
 
-// Full compression + component count.  A CTA owns one 128-lane chunk (a
-// 16-byte quad per thread) and strides over vertices.  Hub vertices -- the
-// kHot smallest ids, which are the roots of the giant components of skewed
-// graphs in nearly every lane -- are read from a shared-memory snapshot of
-// their cells taken at kernel start (roots are final after hooking, and a
-// stale parent pointer is still an ancestor), and members of hub-rooted
-// components are counted in shared memory and flushed once per CTA.  Other
+// Full compression + component count, one thread per 16-byte quad of a label
+// row; the grid stride is a multiple of the row length, so a thread keeps
+// the same 4 lanes for all its vertices and the CTAs stream whole rows.
+// Hub vertices (ids < kHot: the roots of the giant components of skewed
+// graphs in nearly every lane) are read through L1 (ld.ca -- their root bit
+// is final and a stale parent pointer is still an ancestor) and members of
+// hub-rooted components are counted in registers, flushed once per thread,
+// so the hub rows see neither hot L2 reads nor per-member atomics.  Other
 // non-root cells walk to their root with min-safe path splitting, store it,
 // and add 1 to the root cell's member count.  Root cells are never stored by
 // their owner (their count is being incremented concurrently).
-constexpr int kHot = 32;
-constexpr int kChunkLanes = 128;
+constexpr int kHot = 4;
+
+__device__ __forceinline__ uint32_t ld_ca(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 
 __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
-                                                  unsigned long long *__restrict__ nonroot) {
-    __shared__ uint32_t hw[kHot][kChunkLanes];   // hub cell snapshot
-    __shared__ uint32_t hc[kHot][kChunkLanes];   // hub-root member counts
-    const int lane0 = blockIdx.y * kChunkLanes;
-    for (int i = threadIdx.x; i < kHot * kChunkLanes; i += blockDim.x) {
-        const int p = i / kChunkLanes, j = i % kChunkLanes;
-        hw[p][j] = (p < n && lane0 + j < W) ? ld_relaxed(L + (int64_t)p * ld + lane0 + j) : ROOT;
-        hc[p][j] = 0;
-    }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                                  int64_t vstep, unsigned long long *__restrict__ nonroot) {
     const int64_t nq = ld >> 2;
-    const int64_t q = (int64_t)blockIdx.y * 32 + lane;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t q = t % nq;
     const int r = (int)(q << 2);
-    unsigned long long cnt = 0;
-    if (q < nq) {
-        for (int64_t v = (int64_t)blockIdx.x * 8 + warp; v < n; v += (int64_t)gridDim.x * 8) {
-            const uint4 l = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
-            const uint32_t w[4] = {l.x, l.y, l.z, l.w};
+    uint32_t hot[kHot][4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (r + j >= W || is_root(w[j])) continue;
-                const int lj = lane * 4 + j;
-                uint32_t x = (uint32_t)v, p = w[j];
-                uint32_t gw = p < (uint32_t)kHot ? hw[p][lj] : ld_relaxed(cell(L, ld, p, r + j));
-                while (!is_root(gw)) {          // path splitting, min-safe
-                    atomicMin(cell(L, ld, x, r + j), gw);
-                    x = p;
-                    p = gw;
-                    gw = p < (uint32_t)kHot ? hw[p][lj] : ld_relaxed(cell(L, ld, p, r + j));
-                }
-                if (p != w[j]) L[v * ld + r + j] = p;
-                if (p < (uint32_t)kHot) atomicAdd(&hc[p][lj], 1u);
-                else atomicAdd(cell(L, ld, p, r + j), 1u);
-                ++cnt;
+    for (int h = 0; h < kHot; ++h)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hot[h][j] = 0;
+    unsigned long long cnt = 0;
+    // threads past the last whole row of the grid would revisit rows
+    for (int64_t v = (t < vstep * nq) ? t / nq : n; v < n; v += vstep) {
+        const uint4 l = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
+        const uint32_t w[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (r + j >= W || is_root(w[j])) continue;
+            uint32_t x = (uint32_t)v, p = w[j];
+            uint32_t gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r + j)) : ld_relaxed(cell(L, ld, p, r + j));
+            while (!is_root(gw)) {          // path splitting, min-safe
+                atomicMin(cell(L, ld, x, r + j), gw);
+                x = p;
+                p = gw;
+                gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r + j)) : ld_relaxed(cell(L, ld, p, r + j));
             }
+            if (p != w[j]) L[v * ld + r + j] = p;
+            if (p < (uint32_t)kHot) {
+#pragma unroll
+                for (int h = 0; h < kHot; ++h) hot[h][j] += (p == (uint32_t)h);
+            } else {
+                atomicAdd(cell(L, ld, p, r + j), 1u);
+            }
+            ++cnt;
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kHot * kChunkLanes; i += blockDim.x) {
-        const int p = i / kChunkLanes, j = i % kChunkLanes;
-        if (hc[p][j]) atomicAdd(L + (int64_t)p * ld + lane0 + j, hc[p][j]);
-    }
+#pragma unroll
+    for (int h = 0; h < kHot; ++h)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (hot[h][j]) atomicAdd(cell(L, ld, h, r + j), hot[h][j]);
     if (nonroot) {
         for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0 && cnt) atomicAdd(nonroot, cnt);
+        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nonroot, cnt);
     }
 }
 
@@ -561,9 +565,16 @@ static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_in
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
-    const int chunks = (int)ceil_div(c->ld, kChunkLanes);
-    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), (148 * 8 + chunks - 1) / chunks));
-    k_compress<<<dim3(bx, chunks), 256, 0, c->st>>>(c->L, n, c->ld, c->W, nonroot);
+    // grid stride = a whole number of rows, so every thread keeps its quad
+    const int64_t nq = c->ld >> 2;
+    const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * 2);
+    const int64_t rows = std::max<int64_t>(1, want / nq);
+    const int64_t threads = rows * nq;
+    const int blocks = (int)ceil_div(threads, 256);
+    // threads beyond rows*nq would break the fixed-quad mapping: size the
+    // stride from the launched thread count, rounded down to whole rows
+    const int64_t vstep = ((int64_t)blocks * 256) / nq;
+    k_compress<<<blocks, 256, 0, c->st>>>(c->L, n, c->ld, c->W, vstep, nonroot);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;

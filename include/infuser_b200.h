@@ -134,33 +134,32 @@ int  imx_copy_labels(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out);
 int  imx_copy_sizes (imx_ctx *c, int32_t r0, int32_t r1, int32_t *out);
 
 /* ---- K6-K8: CELF (selection.py:115-149) ---------------------------------
- * Round-based exact CELF: device keeps prio (last pushed gain), the seed
- * set, per-lane covered-component bitmaps and per-lane covered totals.    */
+ * Round-based exact CELF.  The device keeps the non-seeds sorted by stale
+ * key (-prio, id), the per-lane covered-component bitmaps and the per-lane
+ * covered totals.  The vertices the reference's lazy heap refreshes in a
+ * round are a prefix of that order.                      */
 /* prio: n int64 initial priorities (NULL -> this context's own gains).    */
 int  imx_celf_reset(imx_ctx *c, const int64_t *prio);
-/* max (prio desc, id asc) over non-seeds; *v = -1 when none remain.       */
+/* first vertex of the order (max prio, min id); *v = -1 when none remain. */
 int  imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out);
-/* Collect the non-seeds v != exclude whose key (-prio[v], v) is <=
- * (-g, u), i.e. prio[v] > g or (prio[v] == g and v <= u), into the
- * context's candidate list sorted by that key; copies ids/prio of up to cap
- * of them out and reports the total in *count.                            */
-int  imx_celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude,
-                      int32_t *ids_out, int64_t *prio_out, int64_t cap,
-                      int64_t *count);
-/* marginal_gain (selection.py:63-70) of collected candidates [lo, hi),
- * partial over this window's scored lanes.                                 */
-int  imx_celf_eval_collected(imx_ctx *c, int64_t lo, int64_t hi, int64_t *fresh_out);
+/* marginal_gain (selection.py:63-70), partial over this window's scored
+ * lanes, of order[lo, hi): fresh_out[hi-lo]; ids_out/prio_out receive
+ * order[lo, min(hi+1, len)) (one extra entry: the next stale key); *len_out
+ * = current order length.  Identical ids/prio on every rank.              */
+int  imx_celf_prefix(imx_ctx *c, int64_t lo, int64_t hi, int32_t *ids_out,
+                     int64_t *prio_out, int64_t *fresh_out, int64_t *len_out);
+/* End of a round: commit_seed(u) (selection.py:73-81; *gain_out = partial
+ * newly covered total), drop order[0, k) and merge back the cnt refreshed
+ * vertices ids[] with their fresh gains prio[] (sorted by (-prio, id)).    */
+int  imx_celf_advance(imx_ctx *c, int64_t k, int32_t u, const int32_t *ids,
+                      const int64_t *prio, int64_t cnt, int64_t *gain_out);
 /* marginal_gain of an explicit candidate list.                            */
 int  imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int64_t *out);
-/* prio[ids[i]] = vals[i]                                                   */
-int  imx_celf_set_prio(imx_ctx *c, const int32_t *ids, const int64_t *vals,
-                       int64_t cnt);
-/* commit_seed (selection.py:73-81): own u's component in every scored
- * lane; *gain_out = partial newly covered total.                          */
+/* commit_seed of u without touching the order (per-vertex API).           */
 int  imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out);
 /* Whole CELF loop on one context (single-rank fast path): k seeds and their
  * gains; *trace_len = number of dequeues recorded (fetch with
- * imx_celf_trace).  Requires imx_celf_reset first.                         */
+ * imx_celf_trace).  Requires a fresh imx_celf_reset.                       */
 int  imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out,
                      int64_t *gains_out, int64_t *trace_len);
 /* The trace of the last imx_celf_select: records of 5 int64

@@ -75,10 +75,9 @@ _SIGNATURES = {
     "imx_copy_sizes": (c_i32, [c_void_p, c_i32, c_i32, c_void_p]),
     "imx_celf_reset": (c_i32, [c_void_p, c_void_p]),
     "imx_celf_top": (c_i32, [c_void_p, P(c_i64), P(c_i32)]),
-    "imx_celf_collect": (c_i32, [c_void_p, c_i64, c_i32, c_i32, c_void_p, c_void_p, c_i64, P(c_i64)]),
-    "imx_celf_eval_collected": (c_i32, [c_void_p, c_i64, c_i64, c_void_p]),
+    "imx_celf_prefix": (c_i32, [c_void_p, c_i64, c_i64, c_void_p, c_void_p, c_void_p, P(c_i64)]),
+    "imx_celf_advance": (c_i32, [c_void_p, c_i64, c_i32, c_void_p, c_void_p, c_i64, P(c_i64)]),
     "imx_eval_gains": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p]),
-    "imx_celf_set_prio": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64]),
     "imx_commit": (c_i32, [c_void_p, c_i32, P(c_i64)]),
     "imx_celf_select": (c_i32, [c_void_p, c_i32, c_void_p, c_void_p, P(c_i64)]),
     "imx_celf_trace": (c_i32, [c_void_p, c_void_p, c_i64]),

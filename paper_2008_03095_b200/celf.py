@@ -11,10 +11,8 @@ identical decisions.
 Exactness: on one fixed sample family marginal gains are
 submodular, so the reference's lazy heap (selection.py:131-147) commits in
 round t the vertex u* minimising (-fresh, id) over V\\S, after refreshing --
-in (-stale, id) order -- exactly R_t = {v : (-stale_v, v) <= (-fresh_u*, u*)}.
-Round t therefore evaluates the top-priority vertex, then every vertex whose
-stale key is at most that vertex's fresh key (a superset of R_t), and
-replays R_t as refresh records before the commit record.
+in (-stale, id) order -- exactly R_t = {v : (-stale_v, v) <= (-fresh_u*, u*)},
+which is a prefix of the non-seeds sorted by stale key.
 """
 
 from __future__ import annotations
@@ -86,45 +84,55 @@ def _key_le(pa, va, pb, vb) -> bool:
 
 
 def select_rounds(shard, comm, k: int, batch0: int = 64):
-    """k seeds, their gains and the dequeue trace (T, 5) over a sharded
-    CELF state.  ``shard`` offers celf_top / eval_gains / celf_collect /
-    celf_eval_collected / celf_set_prio / commit (context.DeviceContext).
+    """k seeds, their gains and the dequeue trace (T, 5) over a sharded CELF
+    state.  ``shard`` offers celf_top / celf_prefix / celf_advance
+    (context.DeviceContext); every partial gain is allreduced.
 
-    Round t: evaluate the top-priority vertex; collect every vertex whose
-    stale key is at most that fresh key (sorted by stale key, identical on
-    every rank); evaluate it in doubling batches until the best fresh key is
-    below the next stale key.  Each partial evaluation is allreduced."""
+    Round t >= 1 evaluates prefixes of the stale-key order in doubling
+    batches until the best fresh key is below the next stale key; the
+    refreshed vertices are the prefix whose stale key is at most the
+    winner's fresh key, replayed as refresh records, then the winner commits
+    and the others go back into the order with their fresh keys."""
     seeds, gains, trace = [], [], []
     for t in range(k):
-        g_top, v_top = shard.celf_top()
-        if v_top < 0:
-            raise AssertionError(f"no candidate left at round {t}")
-        best_v, best_f = v_top, g_top
-        if t > 0:
-            f1 = int(comm.allreduce(shard.eval_gains(np.array([v_top], np.int32)))[0])
-            best_f = f1
-            ev_ids, ev_prio, ev_fresh = [v_top], [g_top], [f1]
-            if f1 != g_top:
-                ids, prio = shard.celf_collect(f1, v_top, v_top)
-                lo, b = 0, batch0
-                while lo < len(ids) and not _key_le(best_f, best_v, int(prio[lo]), int(ids[lo])):
-                    hi = min(len(ids), lo + b)
-                    fr = comm.allreduce(shard.celf_eval_collected(lo, hi))
-                    for v, f in zip(ids[lo:hi].tolist(), fr.tolist()):
-                        if _key_le(f, v, best_f, best_v):
-                            best_v, best_f = v, f
-                    ev_ids += ids[lo:hi].tolist()
-                    ev_prio += prio[lo:hi].tolist()
-                    ev_fresh += fr.tolist()
-                    lo, b = hi, 2 * b
-            ev = sorted((-p, v, f) for v, p, f in zip(ev_ids, ev_prio, ev_fresh)
-                        if _key_le(p, v, best_f, best_v))
-            for negp, v, f in ev:
-                trace.append((v, -negp, f, 0, t))
-            batch0 = max(64, len(ev))
-            shard.celf_set_prio(np.array([v for _, v, _ in ev], np.int32),
-                                np.array([f for _, _, f in ev], np.int64))
-        got = int(comm.allreduce(np.array([shard.commit(best_v)], np.int64))[0])
+        back = []
+        if t == 0:
+            best_f, best_v = shard.celf_top()
+            if best_v < 0:
+                raise AssertionError("no candidate left at round 0")
+            kr = 1
+        else:
+            lo, hi = 0, batch0
+            best_v, best_f = -1, -1
+            ids, prio, fresh = [], [], []
+            while True:
+                i, p, f_part, length = shard.celf_prefix(lo, hi)
+                if length == 0:
+                    raise AssertionError(f"no candidate left at round {t}")
+                f = comm.allreduce(f_part)
+                h = min(hi, length)
+                for v, fv in zip(i[: h - lo].tolist(), f.tolist()):
+                    if best_v < 0 or _key_le(fv, v, best_f, best_v):
+                        best_v, best_f = v, fv
+                ids += i[: h - lo].tolist()
+                prio += p[: h - lo].tolist()
+                fresh += f.tolist()
+                if h >= length:
+                    break
+                if _key_le(best_f, best_v, int(p[h - lo]), int(i[h - lo])):
+                    break                       # nothing unevaluated can win
+                lo, hi = h, h + max(batch0, h)
+            kr = 0
+            while kr < len(ids) and _key_le(prio[kr], ids[kr], best_f, best_v):
+                trace.append((ids[kr], prio[kr], fresh[kr], 0, t))
+                if ids[kr] != best_v:
+                    back.append((-fresh[kr], ids[kr]))
+                kr += 1
+            batch0 = max(64, kr)
+        back.sort()
+        got = int(comm.allreduce(np.array([shard.celf_advance(
+            kr, best_v, np.array([v for _, v in back], np.int32),
+            np.array([-g for g, _ in back], np.int64))], np.int64))[0])
         if got != best_f:
             raise AssertionError(f"committed gain {got} != evaluated {best_f} for vertex {best_v}")
         trace.append((best_v, best_f, best_f, 1, t))

@@ -45,7 +45,6 @@ class DeviceContext:
         check(_lib.load().imx_create(self.dg.handle, ptr(X), self.width, self.num_scored,
                                      ctypes.byref(h)))
         self.handle = h
-        self._collect_cap = 1024
 
     def close(self):
         h, self.handle = getattr(self, "handle", None), None
@@ -113,38 +112,35 @@ class DeviceContext:
         check(_lib.load().imx_celf_top(self.handle, ctypes.byref(g), ctypes.byref(v)))
         return int(g.value), int(v.value)
 
-    def celf_collect(self, g: int, u: int, exclude: int):
-        """Ids and stale priorities of the non-seeds v != exclude with
-        (-prio[v], v) <= (-g, u), sorted by that key; they become the pending
-        evaluation list (celf_eval_collected)."""
-        lib = _lib.load()
-        cap = max(1024, self._collect_cap)
-        while True:
-            ids = np.empty(cap, np.int32)
-            pr = np.empty(cap, np.int64)
-            cnt = ctypes.c_int64()
-            check(lib.imx_celf_collect(self.handle, int(g), int(u), int(exclude), ptr(ids),
-                                       ptr(pr), cap, ctypes.byref(cnt)))
-            if cnt.value <= cap:
-                return ids[: cnt.value], pr[: cnt.value]
-            cap = self._collect_cap = int(cnt.value)
+    def celf_prefix(self, lo: int, hi: int):
+        """Evaluate order[lo, hi): (ids, stale prio of order[lo, hi+1) clipped,
+        partial fresh gains of order[lo, hi), current order length)."""
+        cnt = max(0, hi - lo)
+        ids = np.empty(cnt + 1, np.int32)
+        pr = np.empty(cnt + 1, np.int64)
+        fr = np.empty(cnt, np.int64)
+        ln = ctypes.c_int64()
+        check(_lib.load().imx_celf_prefix(self.handle, int(lo), int(hi), ptr(ids), ptr(pr), ptr(fr),
+                                          ctypes.byref(ln)))
+        length = ln.value
+        h = max(lo, min(hi, length))
+        f = min(h + 1, length)
+        return ids[: max(0, f - lo)], pr[: max(0, f - lo)], fr[: h - lo], length
 
-    def celf_eval_collected(self, lo: int, hi: int) -> np.ndarray:
-        out = np.empty(hi - lo, np.int64)
-        if hi > lo:
-            check(_lib.load().imx_celf_eval_collected(self.handle, int(lo), int(hi), ptr(out)))
-        return out
+    def celf_advance(self, k: int, u: int, ids, prio) -> int:
+        """Commit u, drop order[0, k), merge (ids, prio) back; partial gain of u."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        prio = np.ascontiguousarray(prio, dtype=np.int64)
+        g = ctypes.c_int64()
+        check(_lib.load().imx_celf_advance(self.handle, int(k), int(u), ptr(ids), ptr(prio), len(ids),
+                                           ctypes.byref(g)))
+        return int(g.value)
 
     def eval_gains(self, cand) -> np.ndarray:
         cand = np.ascontiguousarray(cand, dtype=np.int32)
         out = np.empty(len(cand), np.int64)
         check(_lib.load().imx_eval_gains(self.handle, ptr(cand), len(cand), ptr(out)))
         return out
-
-    def celf_set_prio(self, ids, vals):
-        ids = np.ascontiguousarray(ids, dtype=np.int32)
-        vals = np.ascontiguousarray(vals, dtype=np.int64)
-        check(_lib.load().imx_celf_set_prio(self.handle, ptr(ids), ptr(vals), len(ids)))
 
     def commit(self, u: int) -> int:
         g = ctypes.c_int64()

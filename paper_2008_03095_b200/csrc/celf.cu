@@ -1,14 +1,18 @@
 // celf.cu -- K6-K8: CELF seed selection on the device (reference
 // select_seeds / marginal_gain / commit_seed, selection.py:63-149).
 //
-// Round-based exact formulation: gains are computed on one
+// Round-based exact formulation.  Gains are computed on one
 // fixed sample family, so marginal gain is submodular and the reference's
-// lazy heap commits, at every round, the lexicographic argmax (max fresh gain,
-// then min id) after refreshing exactly the vertices whose stale key does not
-// exceed the winner's fresh key.  The device keeps the stale priorities, the
-// seed set, the per-lane covered-component bitmaps and per-lane covered
-// totals; each round is a handful of kernels with one or two host syncs, and
-// the dequeue trace is rebuilt exactly on the host.
+// lazy heap commits, at every round, the lexicographic argmax of the fresh
+// gains (max gain, then min id), after refreshing -- in (-stale, id) order --
+// exactly the vertices whose stale key (-stale, id) does not exceed the
+// winner's fresh key.  Those vertices are a PREFIX of the non-seeds sorted by
+// stale key, so the device keeps that order as one sorted array of packed keys
+// (prio << vb | ~id): a round evaluates prefix batches of doubling size until
+// the best fresh key is below the next stale key, drops the refreshed prefix,
+// commits the winner and merges the other refreshed vertices back with their
+// fresh keys.  No per-round scan or sort of all n vertices; one or two host
+// syncs per round; the dequeue trace is the evaluated prefix itself.
 #include <algorithm>
 #include <vector>
 #include <cub/cub.cuh>
@@ -18,48 +22,11 @@
 
 namespace imx {
 
-// ---------------------------------------------------------------------------
-// K6-K8: CELF
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long pack_key(int64_t prio, uint32_t v, int vb) {
     const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
     return ((unsigned long long)prio << vb) | (unsigned long long)(vmask - v);
 }
 
-__global__ void k_top(const int64_t *__restrict__ prio, const uint8_t *__restrict__ inS, int64_t n,
-                      int vb, unsigned long long *__restrict__ out) {
-    unsigned long long best = 0;
-    bool have = false;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        if (inS[v]) continue;
-        unsigned long long k = pack_key(prio[v], (uint32_t)v, vb) + 1ull;  // +1: 0 = none
-        if (!have || k > best) { best = k; have = true; }
-    }
-    for (int o = 16; o; o >>= 1) {
-        unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
-        best = x > best ? x : best;
-    }
-    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
-}
-
-__global__ void k_collect(const int64_t *__restrict__ prio, const uint8_t *__restrict__ inS, int64_t n,
-                          int vb, unsigned long long thr_key, int32_t exclude,
-                          int32_t *__restrict__ cand, unsigned long long *__restrict__ count) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        bool take = !inS[v] && v != exclude && pack_key(prio[v], (uint32_t)v, vb) >= thr_key;
-        unsigned m = __ballot_sync(__activemask(), take);
-        if (!m) continue;
-        int leader = __ffs(m) - 1;
-        unsigned long long base = 0;
-        if ((threadIdx.x & 31) == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
-        base = __shfl_sync(__activemask(), base, leader);
-        if (take) cand[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (int32_t)v;
-    }
-}
-
-// size and label of cell (u, r) (encoded labels, or caller labels + C)
 template <bool ENC>
 __device__ __forceinline__ uint32_t cell_size(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
                                               int64_t ld, uint32_t u, uint32_t w, int r, uint32_t &label) {
@@ -141,183 +108,48 @@ __global__ void k_commit(int32_t u, const uint32_t *__restrict__ L, const uint32
     if (blockIdx.x == 0 && threadIdx.x == 0) inS[u] = 1;
 }
 
-// CELF round header (scratch[8..12]): 0 top key+1, 1 fresh gain of the top,
-// 2 collected count, 3 gain of the last commit, 4 collect threshold key.
-enum { H_TOP = 0, H_F1 = 1, H_COUNT = 2, H_GAIN = 3, H_THR = 4 };
-
-__global__ void k_round_decode(const unsigned long long *__restrict__ hdr, int vb, int32_t *__restrict__ one) {
-    unsigned long long key = hdr[H_TOP];
-    const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
-    one[0] = key ? (int32_t)(vmask - (uint32_t)((key - 1) & vmask)) : -1;
-}
-
-__global__ void k_make_thr(unsigned long long *__restrict__ hdr, const int64_t *__restrict__ f1,
-                           const int32_t *__restrict__ one, int vb) {
-    const int32_t v = one[0];
-    hdr[H_F1] = (unsigned long long)f1[0];
-    hdr[H_THR] = v < 0 ? ~0ull : pack_key(f1[0], (uint32_t)v, vb);
-}
-
-// k_collect with the threshold key and the excluded vertex read from device memory
-__global__ void k_collect_dev(const int64_t *__restrict__ prio, const uint8_t *__restrict__ inS, int64_t n,
-                              int vb, const unsigned long long *__restrict__ hdr,
-                              const int32_t *__restrict__ one, int32_t *__restrict__ cand,
-                              unsigned long long *__restrict__ count) {
-    const unsigned long long thr_key = hdr[H_THR];
-    const int32_t exclude = one[0];
+__global__ void k_pack_keys(const int64_t *__restrict__ prio, int64_t n, int vb, int32_t *__restrict__ ids,
+                            unsigned long long *__restrict__ keys, unsigned long long *__restrict__ maxp) {
+    unsigned long long m = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
-        bool take = !inS[v] && v != exclude && pack_key(prio[v], (uint32_t)v, vb) >= thr_key;
-        unsigned m = __ballot_sync(__activemask(), take);
-        if (!m) continue;
-        int leader = __ffs(m) - 1;
-        unsigned long long base = 0;
-        if ((threadIdx.x & 31) == leader) base = atomicAdd(count, (unsigned long long)__popc(m));
-        base = __shfl_sync(__activemask(), base, leader);
-        if (take) cand[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = (int32_t)v;
+        const int64_t p = prio[v] < 0 ? 0 : prio[v];
+        ids[v] = (int32_t)v;
+        keys[v] = pack_key(p, (uint32_t)v, vb);
+        m = (unsigned long long)p > m ? (unsigned long long)p : m;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+        m = y > m ? y : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(maxp, m);
+}
+
+// merge two key-descending lists (unique keys) into out
+__global__ void k_merge(const int32_t *__restrict__ aid, const unsigned long long *__restrict__ akey, int64_t na,
+                        const int32_t *__restrict__ bid, const unsigned long long *__restrict__ bkey, int64_t nb,
+                        int32_t *__restrict__ oid, unsigned long long *__restrict__ okey) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na + nb;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool in_a = i < na;
+        const int64_t j = in_a ? i : i - na;
+        const unsigned long long key = in_a ? akey[j] : bkey[j];
+        const unsigned long long *other = in_a ? bkey : akey;
+        int64_t lo = 0, hi = in_a ? nb : na;      // number of other keys > key
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (other[mid] > key) lo = mid + 1; else hi = mid;
+        }
+        const int64_t pos = j + lo;
+        oid[pos] = in_a ? aid[j] : bid[j];
+        okey[pos] = key;
     }
 }
-
-__global__ void k_keys_of(const int32_t *__restrict__ ids, int64_t cnt, const int64_t *__restrict__ prio,
-                          int vb, unsigned long long *__restrict__ keys) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
-         i += (int64_t)gridDim.x * blockDim.x)
-        keys[i] = pack_key(prio[ids[i]], (uint32_t)ids[i], vb);
-}
-
-__global__ void k_set_prio(const int32_t *__restrict__ ids, const int64_t *__restrict__ vals,
-                           int64_t cnt, int64_t *__restrict__ prio) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
-         i += (int64_t)gridDim.x * blockDim.x)
-        prio[ids[i]] = vals[i];
-}
-
 
 static void launch_commit(imx_ctx *c, int32_t u, unsigned long long *gain) {
     const int blocks = grid_for(std::max(c->ns, 1));
     if (c->C) k_commit<false><<<blocks, 256, 0, c->st>>>(u, c->L, c->C, c->cov, c->ld, c->ns, c->cw, c->per_sim, c->inS, gain);
     else k_commit<true><<<blocks, 256, 0, c->st>>>(u, c->L, nullptr, c->cov, c->ld, c->ns, c->cw, c->per_sim, c->inS, gain);
-}
-
-}  // namespace imx
-
-using namespace imx;
-
-// ---------------------------------------------------------------------------
-// CELF (selection.py:115-149) -- round-based exact formulation
-// ---------------------------------------------------------------------------
-extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
-    CTX_CHECK(c);
-    if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
-    IMX_TRY(ensure_celf_buffers(c));
-    const int64_t n = c->g->n;
-    if (n) {
-        if (prio) {
-            IMX_CUDA(cudaMemcpyAsync(c->prio, prio, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->st));
-        } else {
-            if (!c->memo_ready) { set_error("gains not computed (call imx_memoize first)"); return IMX_EINVAL; }
-            IMX_CUDA(cudaMemcpyAsync(c->prio, c->gains, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->st));
-        }
-        IMX_CUDA(cudaMemsetAsync(c->inS, 0, n, c->st));
-        IMX_CUDA(cudaMemsetAsync(c->cov, 0, sizeof(uint32_t) * (size_t)n * c->cw, c->st));
-    }
-    IMX_CUDA(cudaMemsetAsync(c->per_sim, 0, sizeof(int64_t) * (c->W + 1), c->st));
-    IMX_CUDA(cudaStreamSynchronize(c->st));
-    c->celf_ready = true;
-    c->ncand = 0;
-    c->trace.clear();
-    return IMX_OK;
-}
-
-
-static int celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
-    const int64_t n = c->g->n;
-    unsigned long long *sc = c->scratch + 5;
-    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
-    if (n) {
-        k_top<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, sc);
-        IMX_CHECK_LAUNCH();
-        count_launch(c);
-    }
-    unsigned long long key = 0;
-    IMX_CUDA(cudaMemcpyAsync(&key, sc, sizeof key, cudaMemcpyDeviceToHost, c->st));
-    IMX_CUDA(cudaStreamSynchronize(c->st));
-    if (!key) { *v_out = -1; *prio_out = 0; return IMX_OK; }
-    key -= 1;
-    const uint64_t vmask = (c->vb >= 32) ? 0xffffffffull : ((1ull << c->vb) - 1);
-    *v_out = (int32_t)(vmask - (key & vmask));
-    *prio_out = (int64_t)(key >> c->vb);
-    return IMX_OK;
-}
-
-extern "C" int imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
-    CELF_CHECK(c);
-    if (!prio_out || !v_out) { set_error("NULL argument"); return IMX_EINVAL; }
-    return celf_top(c, prio_out, v_out);
-}
-
-// Collect the non-seeds whose stale key (-prio, id) is <= (-g, u), sorted by
-// that key on the device (descending packed key == ascending (-prio, id)).
-// The sorted ids stay in c->cand for batch evaluation; ids/prio come back.
-static int celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude, std::vector<int32_t> *ids,
-                        std::vector<int64_t> *pr) {
-    const int64_t n = c->g->n;
-    unsigned long long *sc = c->scratch + 6;
-    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
-    const uint32_t vmask = (c->vb >= 32) ? 0xffffffffu : ((1u << c->vb) - 1u);
-    const unsigned long long thr = ((unsigned long long)g << c->vb) | (unsigned long long)(vmask - (uint32_t)u);
-    if (n) {
-        k_collect<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, thr, exclude, c->cand, sc);
-        IMX_CHECK_LAUNCH();
-        count_launch(c);
-    }
-    unsigned long long cnt = 0;
-    IMX_CUDA(cudaMemcpyAsync(&cnt, sc, sizeof cnt, cudaMemcpyDeviceToHost, c->st));
-    IMX_CUDA(cudaStreamSynchronize(c->st));
-    c->ncand = (int64_t)cnt;
-    ids->resize(cnt);
-    pr->resize(cnt);
-    if (!cnt) return IMX_OK;
-    // keys of the collected ids, then a device radix sort by key
-    unsigned long long *keys = reinterpret_cast<unsigned long long *>(c->fresh);
-    k_keys_of<<<grid_for((int64_t)cnt), 256, 0, c->st>>>(c->cand, (int64_t)cnt, c->prio, c->vb, keys);
-    IMX_CHECK_LAUNCH();
-    count_launch(c);
-    const int end_bit = 64;
-    size_t tmp_bytes = 0;
-    IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, keys, c->keys2, c->cand,
-                                                       c->cand2, (int64_t)cnt, 0, end_bit, c->st));
-    if (tmp_bytes > c->sort_tmp_bytes) {
-        if (c->sort_tmp) cudaFree(c->sort_tmp);
-        c->sort_tmp = nullptr;
-        c->sort_tmp_bytes = 0;
-        IMX_CUDA(cudaMalloc(&c->sort_tmp, tmp_bytes));
-        c->sort_tmp_bytes = tmp_bytes;
-    }
-    IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, tmp_bytes, keys, c->keys2, c->cand,
-                                                       c->cand2, (int64_t)cnt, 0, end_bit, c->st));
-    std::swap(c->cand, c->cand2);
-    std::vector<unsigned long long> hk(cnt);
-    IMX_CUDA(cudaMemcpyAsync(ids->data(), c->cand, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, c->st));
-    IMX_CUDA(cudaMemcpyAsync(hk.data(), c->keys2, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost, c->st));
-    IMX_CUDA(cudaStreamSynchronize(c->st));
-    for (size_t i = 0; i < cnt; ++i) (*pr)[i] = (int64_t)(hk[i] >> c->vb);
-    return IMX_OK;
-}
-
-extern "C" int imx_celf_collect(imx_ctx *c, int64_t g, int32_t u, int32_t exclude, int32_t *ids_out,
-                                int64_t *prio_out, int64_t cap, int64_t *count) {
-    CELF_CHECK(c);
-    if (!count) { set_error("count is NULL"); return IMX_EINVAL; }
-    if (g < 0) { set_error("gain bound must be non-negative"); return IMX_EINVAL; }
-    std::vector<int32_t> ids;
-    std::vector<int64_t> pr;
-    IMX_TRY(celf_collect(c, g, u, exclude, &ids, &pr));
-    *count = (int64_t)ids.size();
-    const int64_t k = std::min<int64_t>(cap, *count);
-    if (k > 0 && ids_out) std::copy(ids.begin(), ids.begin() + k, ids_out);
-    if (k > 0 && prio_out) std::copy(pr.begin(), pr.begin() + k, prio_out);
-    return IMX_OK;
 }
 
 static int celf_eval_dev(imx_ctx *c, const int32_t *dcand, int64_t cnt, int64_t *dout) {
@@ -330,19 +162,172 @@ static int celf_eval_dev(imx_ctx *c, const int32_t *dcand, int64_t cnt, int64_t 
     return IMX_OK;
 }
 
-// evaluate collected[lo, hi) -> fresh_out[hi - lo]
-extern "C" int imx_celf_eval_collected(imx_ctx *c, int64_t lo, int64_t hi, int64_t *fresh_out) {
-    CELF_CHECK(c);
-    if (lo < 0 || hi > c->ncand || lo > hi) {
-        set_error("collected range [%lld, %lld) outside [0, %lld)", (long long)lo, (long long)hi,
-                  (long long)c->ncand);
+static inline int64_t key_prio(const imx_ctx *c, unsigned long long k) { return (int64_t)(k >> c->vb); }
+static inline unsigned long long host_key(const imx_ctx *c, int64_t prio, int32_t v) {
+    const uint64_t vmask = (c->vb >= 32) ? 0xffffffffull : ((1ull << c->vb) - 1);
+    return ((unsigned long long)prio << c->vb) | (vmask - (uint64_t)v);
+}
+
+// evaluate order[lo, hi) of the current order; ids/keys of order[lo, min(hi+1, len))
+// and fresh gains of [lo, hi) land in the caller's host buffers.
+static int celf_prefix(imx_ctx *c, int64_t lo, int64_t hi, int32_t *ids, unsigned long long *keys,
+                       int64_t *fresh) {
+    const int64_t len = c->olen;
+    hi = std::min(hi, len);
+    if (lo >= hi) return IMX_OK;
+    const int64_t base = c->ostart;
+    IMX_TRY(celf_eval_dev(c, c->oid[c->ocur] + base + lo, hi - lo, c->eval_out));
+    const int64_t fetch = std::min(hi + 1, len) - lo;
+    IMX_CUDA(cudaMemcpyAsync(ids, c->oid[c->ocur] + base + lo, sizeof(int32_t) * fetch, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaMemcpyAsync(keys, c->okey[c->ocur] + base + lo, sizeof(unsigned long long) * fetch,
+                             cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaMemcpyAsync(fresh, c->eval_out, sizeof(int64_t) * (hi - lo), cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    c->evaluated += hi - lo;
+    return IMX_OK;
+}
+
+// drop order[0, k), merge cnt (ids, keys) back (keys descending); async
+static int celf_advance(imx_ctx *c, int64_t k, const int32_t *ids, const unsigned long long *keys, int64_t cnt) {
+    if (k > c->olen) { set_error("advance past the end of the candidate order"); return IMX_EINVAL; }
+    c->ostart += k;
+    c->olen -= k;
+    if (cnt <= 0) return IMX_OK;
+    IMX_TRY(ensure_pinned(c, cnt + 8));
+    std::copy(ids, ids + cnt, c->h_ids);
+    std::copy(keys, keys + cnt, reinterpret_cast<unsigned long long *>(c->h_vals) + 8);
+    IMX_CUDA(cudaMemcpyAsync(c->d_ids, c->h_ids, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
+    IMX_CUDA(cudaMemcpyAsync(c->d_vals, c->h_vals + 8, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, c->st));
+    const int nxt = c->ocur ^ 1;
+    k_merge<<<grid_for(c->olen + cnt), 256, 0, c->st>>>(
+        c->oid[c->ocur] + c->ostart, c->okey[c->ocur] + c->ostart, c->olen, c->d_ids,
+        reinterpret_cast<const unsigned long long *>(c->d_vals), cnt, c->oid[nxt], c->okey[nxt]);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    c->ocur = nxt;
+    c->ostart = 0;
+    c->olen += cnt;
+    // the staging buffers are reused next round: make sure the copies are done
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    return IMX_OK;
+}
+
+static inline bool key_le(int64_t pa, int32_t va, int64_t pb, int32_t vb) {
+    // (-pa, va) <= (-pb, vb)
+    return pa > pb || (pa == pb && va <= vb);
+}
+
+}  // namespace imx
+
+using namespace imx;
+
+extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
+    CTX_CHECK(c);
+    if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
+    IMX_TRY(ensure_celf_buffers(c));
+    const int64_t n = c->g->n;
+    int64_t *dprio = c->gains;
+    if (prio) {
+        IMX_CUDA(cudaMemcpyAsync(c->eval_out, prio, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->st));
+        dprio = c->eval_out;
+    } else if (!c->memo_ready) {
+        set_error("gains not computed (call imx_memoize first)");
         return IMX_EINVAL;
     }
-    if (hi == lo) return IMX_OK;
-    IMX_TRY(celf_eval_dev(c, c->cand + lo, hi - lo, c->eval_out));
-    if (fresh_out)
-        IMX_CUDA(cudaMemcpyAsync(fresh_out, c->eval_out, sizeof(int64_t) * (hi - lo), cudaMemcpyDeviceToHost, c->st));
+    unsigned long long *maxp = c->scratch + 9;
+    IMX_CUDA(cudaMemsetAsync(maxp, 0, sizeof(unsigned long long), c->st));
+    if (n) {
+        k_pack_keys<<<grid_for(n), 256, 0, c->st>>>(dprio, n, c->vb, c->oid[1], c->okey[1], maxp);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    unsigned long long mp = 0;
+    IMX_CUDA(cudaMemcpyAsync(&mp, maxp, sizeof mp, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
+    int pbits = 0;
+    while (pbits < 64 && (mp >> pbits)) ++pbits;
+    if (pbits + c->vb > 64) {
+        set_error("gains need %d bits and vertex ids %d: packed CELF keys exceed 64 bits", pbits, c->vb);
+        return IMX_ECONSTRAINT;
+    }
+    if (n) {
+        const int end_bit = std::max(1, pbits + c->vb);
+        size_t tb = 0;
+        IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c->okey[1], c->okey[0], c->oid[1], c->oid[0],
+                                                           n, 0, end_bit, c->st));
+        if (tb > c->sort_tmp_bytes) {
+            if (c->sort_tmp) cudaFree(c->sort_tmp);
+            c->sort_tmp = nullptr;
+            c->sort_tmp_bytes = 0;
+            IMX_CUDA(cudaMalloc(&c->sort_tmp, tb));
+            c->sort_tmp_bytes = tb;
+        }
+        IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, tb, c->okey[1], c->okey[0], c->oid[1],
+                                                           c->oid[0], n, 0, end_bit, c->st));
+        IMX_CUDA(cudaMemsetAsync(c->inS, 0, n, c->st));
+        IMX_CUDA(cudaMemsetAsync(c->cov, 0, sizeof(uint32_t) * (size_t)n * c->cw, c->st));
+    }
+    IMX_CUDA(cudaMemsetAsync(c->per_sim, 0, sizeof(int64_t) * (c->W + 1), c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    c->ocur = 0;
+    c->ostart = 0;
+    c->olen = n;
+    c->celf_ready = true;
+    c->trace.clear();
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
+    CELF_CHECK(c);
+    if (!prio_out || !v_out) { set_error("NULL argument"); return IMX_EINVAL; }
+    if (c->olen == 0) { *v_out = -1; *prio_out = 0; return IMX_OK; }
+    int32_t id;
+    unsigned long long key;
+    IMX_CUDA(cudaMemcpyAsync(&id, c->oid[c->ocur] + c->ostart, sizeof id, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaMemcpyAsync(&key, c->okey[c->ocur] + c->ostart, sizeof key, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    *v_out = id;
+    *prio_out = key_prio(c, key);
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_prefix(imx_ctx *c, int64_t lo, int64_t hi, int32_t *ids_out, int64_t *prio_out,
+                               int64_t *fresh_out, int64_t *len_out) {
+    CELF_CHECK(c);
+    if (lo < 0 || hi < lo) { set_error("prefix range [%lld, %lld) invalid", (long long)lo, (long long)hi); return IMX_EINVAL; }
+    if (len_out) *len_out = c->olen;
+    hi = std::min(hi, c->olen);
+    if (lo >= hi) return IMX_OK;
+    const int64_t fetch = std::min(hi + 1, c->olen) - lo;
+    std::vector<unsigned long long> keys(fetch);
+    std::vector<int32_t> ids(fetch);
+    std::vector<int64_t> fr(hi - lo);
+    IMX_TRY(celf_prefix(c, lo, hi, ids.data(), keys.data(), fr.data()));
+    if (ids_out) std::copy(ids.begin(), ids.end(), ids_out);
+    if (prio_out) for (int64_t i = 0; i < fetch; ++i) prio_out[i] = key_prio(c, keys[i]);
+    if (fresh_out) std::copy(fr.begin(), fr.end(), fresh_out);
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_advance(imx_ctx *c, int64_t k, int32_t u, const int32_t *ids, const int64_t *prio,
+                                int64_t cnt, int64_t *gain_out) {
+    CELF_CHECK(c);
+    if (k < 0 || cnt < 0 || (cnt && (!ids || !prio))) { set_error("bad arguments"); return IMX_EINVAL; }
+    if (u < 0 || u >= c->g->n) { set_error("vertex %d outside vertex range", u); return IMX_EINVAL; }
+    std::vector<unsigned long long> keys(cnt);
+    for (int64_t i = 0; i < cnt; ++i) keys[i] = host_key(c, prio[i], ids[i]);
+    for (int64_t i = 1; i < cnt; ++i)
+        if (keys[i] >= keys[i - 1]) { set_error("re-inserted vertices must be sorted by (-prio, id)"); return IMX_EINVAL; }
+    unsigned long long *sc = c->scratch + 7;
+    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
+    launch_commit(c, u, sc);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    IMX_TRY(celf_advance(c, k, ids, keys.data(), cnt));
+    unsigned long long g = 0;
+    IMX_CUDA(cudaMemcpyAsync(&g, sc, sizeof g, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (gain_out) *gain_out = (int64_t)g;
     return IMX_OK;
 }
 
@@ -366,40 +351,6 @@ extern "C" int imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int6
     return rc;
 }
 
-static int celf_set_prio_async(imx_ctx *c, const int32_t *ids, const int64_t *vals, int64_t cnt) {
-    if (cnt <= 0) return IMX_OK;
-    // staged through the pinned host buffer
-    IMX_TRY(ensure_pinned(c, cnt));
-    std::copy(ids, ids + cnt, c->h_ids);
-    std::copy(vals, vals + cnt, c->h_vals);
-    IMX_CUDA(cudaMemcpyAsync(c->d_ids, c->h_ids, sizeof(int32_t) * cnt, cudaMemcpyHostToDevice, c->st));
-    IMX_CUDA(cudaMemcpyAsync(c->d_vals, c->h_vals, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, c->st));
-    k_set_prio<<<grid_for(cnt), 256, 0, c->st>>>(c->d_ids, c->d_vals, cnt, c->prio);
-    IMX_CHECK_LAUNCH();
-    count_launch(c);
-    return IMX_OK;
-}
-
-extern "C" int imx_celf_set_prio(imx_ctx *c, const int32_t *ids, const int64_t *vals, int64_t cnt) {
-    CELF_CHECK(c);
-    IMX_TRY(celf_set_prio_async(c, ids, vals, cnt));
-    IMX_CUDA(cudaStreamSynchronize(c->st));
-    return IMX_OK;
-}
-
-static int celf_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
-    unsigned long long *sc = c->scratch + 7;
-    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
-    launch_commit(c, u, sc);
-    IMX_CHECK_LAUNCH();
-    count_launch(c);
-    unsigned long long gsum = 0;
-    IMX_CUDA(cudaMemcpyAsync(&gsum, sc, sizeof gsum, cudaMemcpyDeviceToHost, c->st));
-    IMX_CUDA(cudaStreamSynchronize(c->st));
-    if (gain_out) *gain_out = (int64_t)gsum;
-    return IMX_OK;
-}
-
 extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
     CELF_CHECK(c);
     if (u < 0 || u >= c->g->n) { set_error("vertex %d outside vertex range", u); return IMX_EINVAL; }
@@ -407,34 +358,25 @@ extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
     IMX_CUDA(cudaMemcpyAsync(&in, c->inS + u, 1, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
     if (in) { set_error("vertex %d committed twice", u); return IMX_EINTERNAL; }
-    return celf_commit(c, u, gain_out);
+    unsigned long long *sc = c->scratch + 7;
+    IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long), c->st));
+    launch_commit(c, u, sc);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    unsigned long long g = 0;
+    IMX_CUDA(cudaMemcpyAsync(&g, sc, sizeof g, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (gain_out) *gain_out = (int64_t)g;
+    return IMX_OK;
 }
 
-static inline bool key_le(int64_t pa, int32_t va, int64_t pb, int32_t vb) {
-    // (-pa, va) <= (-pb, vb)
-    return pa > pb || (pa == pb && va <= vb);
-}
-
-// Whole CELF loop on one context.  Exactness argument: on a
-// fixed sample set marginal gains are submodular, so the reference's lazy
-// heap commits, at every round t, u* = argmin over V\S of (-fresh, id), after
-// refreshing exactly R_t = {v : (-stale_v, v) <= (-fresh_u*, u*)} in
-// (-stale, id) order.  Round t evaluates the top-priority vertex, collects
-// the vertices whose stale key is at most that vertex's fresh key (nothing
-// else can win), sorts them by stale key and evaluates them in doubling
-// batches until the best fresh key found is below the next stale key -- so
-// the evaluated set is R_t plus at most one batch.
-//
-// Launch pattern per round: top -> decode -> eval(top) -> threshold ->
-// collect run back to back on the stream and end in ONE host sync that reads
-// the round header (top key, its fresh gain, collected count, last commit's
-// gain); the sort and the first batch end in a second sync; the priority
-// update and the commit are left in flight for the next round.
+// The whole CELF loop on one context (single-rank path).
 extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_t *gains_out,
                                int64_t *trace_len) {
     CELF_CHECK(c);
     const int64_t n = c->g->n;
     if (k < 1 || k > n) { set_error("k=%d invalid for n=%lld", k, (long long)n); return IMX_ECONSTRAINT; }
+    if (c->olen != n) { set_error("CELF state already advanced (call imx_celf_reset)"); return IMX_EINVAL; }
     cudaEventRecord(c->ev[6], c->st);
     c->trace.clear();
     c->evaluated = 0;
@@ -442,147 +384,93 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
         c->trace.push_back(v); c->trace.push_back(s); c->trace.push_back(f);
         c->trace.push_back(com); c->trace.push_back(t);
     };
-    unsigned long long *hdr = c->scratch + 8;
-    const uint64_t vmask = (c->vb >= 32) ? 0xffffffffull : ((1ull << c->vb) - 1);
-    IMX_TRY(ensure_pinned(c, 4096));
-    unsigned long long *hh = reinterpret_cast<unsigned long long *>(c->h_vals);  // pinned header copy
-    std::vector<int32_t> eids, ids;
-    std::vector<int64_t> epr, efr, pr, fr;
+    unsigned long long *gain = c->scratch + 7;
+    std::vector<int32_t> ids;
     std::vector<unsigned long long> keys;
-    int64_t batch0 = 64;
-    int64_t pending_gain = -1;   // expected gain of the commit still in flight
+    std::vector<int64_t> fr;
+    std::vector<std::pair<unsigned long long, int32_t>> back;
+    int64_t batch0 = 64, pending = -1, got = 0;
     int32_t pending_v = -1;
-    auto check_gain = [&](int64_t got) -> int {
-        if (pending_gain >= 0 && got != pending_gain) {
-            set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
-                      (long long)got, (long long)pending_gain, pending_v);
-            return IMX_EINTERNAL;
-        }
-        return IMX_OK;
-    };
     for (int32_t t = 0; t < k; ++t) {
-        // ---- phase 1: top, its fresh gain, the collected candidates ----
-        IMX_CUDA(cudaMemsetAsync(hdr + H_TOP, 0, sizeof(unsigned long long), c->st));
-        IMX_CUDA(cudaMemsetAsync(hdr + H_COUNT, 0, sizeof(unsigned long long), c->st));
-        k_top<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, hdr + H_TOP);
-        k_round_decode<<<1, 1, 0, c->st>>>(hdr, c->vb, c->d_one);
-        count_launch(c, 2);
-        if (t > 0) {
-            IMX_TRY(celf_eval_dev(c, c->d_one, 1, c->eval_out));
-            k_make_thr<<<1, 1, 0, c->st>>>(hdr, c->eval_out, c->d_one, c->vb);
-            k_collect_dev<<<grid_for(n, 256), 256, 0, c->st>>>(c->prio, c->inS, n, c->vb, hdr, c->d_one,
-                                                               c->cand, hdr + H_COUNT);
-            count_launch(c, 2);
-        }
-        IMX_CHECK_LAUNCH();
-        IMX_CUDA(cudaMemcpyAsync(hh, hdr, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, c->st));
-        IMX_CUDA(cudaStreamSynchronize(c->st));
-        IMX_TRY(check_gain((int64_t)hh[H_GAIN]));
-        if (!hh[H_TOP]) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
-        const unsigned long long tk = hh[H_TOP] - 1;
-        const int32_t vt = (int32_t)(vmask - (tk & vmask));
-        const int64_t gt = (int64_t)(tk >> c->vb);
-        int64_t best_f = gt;
-        int32_t best_v = vt;
-        if (t > 0) {
-            const int64_t f1 = (int64_t)hh[H_F1];
-            const int64_t cnt = (int64_t)hh[H_COUNT];
-            c->evaluated += 1;
-            best_f = f1;
-            eids.assign(1, vt); epr.assign(1, gt); efr.assign(1, f1);
-            c->ncand = cnt;
-            if (cnt > 0) {
-                // ---- phase 2: sort by stale key, first batch ----
-                unsigned long long *dkeys = reinterpret_cast<unsigned long long *>(c->fresh);
-                k_keys_of<<<grid_for(cnt), 256, 0, c->st>>>(c->cand, cnt, c->prio, c->vb, dkeys);
-                IMX_CHECK_LAUNCH();
-                count_launch(c);
-                size_t tmp_bytes = 0;
-                IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, dkeys, c->keys2, c->cand,
-                                                                   c->cand2, cnt, 0, 64, c->st));
-                if (tmp_bytes > c->sort_tmp_bytes) {
-                    IMX_CUDA(cudaStreamSynchronize(c->st));
-                    if (c->sort_tmp) cudaFree(c->sort_tmp);
-                    c->sort_tmp = nullptr;
-                    c->sort_tmp_bytes = 0;
-                    IMX_CUDA(cudaMalloc(&c->sort_tmp, tmp_bytes * 2));
-                    c->sort_tmp_bytes = tmp_bytes * 2;
-                }
-                IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, tmp_bytes, dkeys, c->keys2, c->cand,
-                                                                   c->cand2, cnt, 0, 64, c->st));
-                std::swap(c->cand, c->cand2);
-                ids.resize(cnt); pr.resize(cnt); fr.resize(cnt); keys.resize(cnt);
-                int64_t lo = 0, b = batch0, fetched = 0;
-                for (;;) {
-                    const int64_t hi = std::min(cnt, lo + b);
-                    const int64_t fetch_to = std::min(cnt, hi + 1);   // +1: next stale key
-                    IMX_TRY(celf_eval_dev(c, c->cand + lo, hi - lo, c->eval_out));
-                    if (fetch_to > fetched) {
-                        IMX_CUDA(cudaMemcpyAsync(ids.data() + fetched, c->cand + fetched,
-                                                 sizeof(int32_t) * (fetch_to - fetched), cudaMemcpyDeviceToHost, c->st));
-                        IMX_CUDA(cudaMemcpyAsync(keys.data() + fetched, c->keys2 + fetched,
-                                                 sizeof(unsigned long long) * (fetch_to - fetched),
-                                                 cudaMemcpyDeviceToHost, c->st));
+        if (c->olen == 0) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
+        int64_t best_f;
+        int32_t best_v;
+        int64_t kr;                   // refreshed prefix length
+        back.clear();
+        if (t == 0) {
+            // fresh_at starts at 0 == len(S): the first pop commits (selection.py:136-141)
+            ids.resize(1);
+            keys.resize(1);
+            IMX_CUDA(cudaMemcpyAsync(ids.data(), c->oid[c->ocur] + c->ostart, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaMemcpyAsync(keys.data(), c->okey[c->ocur] + c->ostart, sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaStreamSynchronize(c->st));
+            best_v = ids[0];
+            best_f = key_prio(c, keys[0]);
+            kr = 1;
+        } else {
+            const int64_t len = c->olen;
+            ids.resize(std::min(len, std::max<int64_t>(batch0, 1)) + 1);
+            keys.resize(ids.size());
+            fr.resize(ids.size());
+            int64_t lo = 0, hi = std::min(len, batch0);
+            best_f = -1;
+            best_v = -1;
+            for (;;) {
+                if ((int64_t)ids.size() < hi + 1) { ids.resize(hi + 1); keys.resize(hi + 1); fr.resize(hi + 1); }
+                IMX_TRY(celf_prefix(c, lo, hi, ids.data() + lo, keys.data() + lo, fr.data() + lo));
+                if (pending >= 0) {        // the previous commit finished before these copies
+                    IMX_CUDA(cudaMemcpy(&got, gain, sizeof got, cudaMemcpyDeviceToHost));
+                    if (got != pending) {
+                        set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                                  (long long)got, (long long)pending, pending_v);
+                        return IMX_EINTERNAL;
                     }
-                    IMX_CUDA(cudaMemcpyAsync(fr.data() + lo, c->eval_out, sizeof(int64_t) * (hi - lo),
-                                             cudaMemcpyDeviceToHost, c->st));
-                    IMX_CUDA(cudaStreamSynchronize(c->st));
-                    for (int64_t i = fetched; i < fetch_to; ++i) pr[i] = (int64_t)(keys[i] >> c->vb);
-                    fetched = std::max(fetched, fetch_to);
-                    for (int64_t i = lo; i < hi; ++i) {
-                        if (key_le(fr[i], ids[i], best_f, best_v)) { best_f = fr[i]; best_v = ids[i]; }
-                        eids.push_back(ids[i]); epr.push_back(pr[i]); efr.push_back(fr[i]);
-                    }
-                    c->evaluated += hi - lo;
-                    lo = hi;
-                    b *= 2;
-                    if (lo >= cnt || key_le(best_f, best_v, pr[lo], ids[lo])) break;
+                    pending = -1;
                 }
+                for (int64_t i = lo; i < hi; ++i)
+                    if (best_v < 0 || key_le(fr[i], ids[i], best_f, best_v)) { best_f = fr[i]; best_v = ids[i]; }
+                if (hi >= len) break;
+                const int64_t np = key_prio(c, keys[hi]);
+                if (key_le(best_f, best_v, np, ids[hi])) break;    // nothing unevaluated can win
+                lo = hi;
+                hi = std::min(len, hi + std::max<int64_t>(batch0, hi));
             }
-            // ---- R_t in (-stale, id) order: refresh records, prio <- fresh ----
-            std::vector<size_t> rt;
-            for (size_t i = 0; i < eids.size(); ++i)
-                if (key_le(epr[i], eids[i], best_f, best_v)) rt.push_back(i);
-            std::sort(rt.begin(), rt.end(), [&](size_t a, size_t b2) {
-                return epr[a] != epr[b2] ? epr[a] > epr[b2] : eids[a] < eids[b2];
-            });
-            IMX_TRY(ensure_pinned(c, (int64_t)rt.size() + 8));
-            hh = reinterpret_cast<unsigned long long *>(c->h_vals);
-            int64_t m = 0;
-            for (size_t i : rt) {
-                rec(eids[i], epr[i], efr[i], 0, t);
-                c->h_ids[m] = eids[i];
-                c->h_vals[8 + m] = efr[i];   // h_vals[0..7] hold the header copy
-                ++m;
+            // R_t = the prefix whose stale key <= best fresh key (sorted by stale key)
+            kr = 0;
+            while (kr < hi && key_le(key_prio(c, keys[kr]), ids[kr], best_f, best_v)) {
+                rec(ids[kr], key_prio(c, keys[kr]), fr[kr], 0, t);
+                if (ids[kr] != best_v) back.emplace_back(host_key(c, fr[kr], ids[kr]), ids[kr]);
+                ++kr;
             }
-            batch0 = std::max<int64_t>(64, m);
-            if (m) {
-                IMX_CUDA(cudaMemcpyAsync(c->d_ids, c->h_ids, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
-                IMX_CUDA(cudaMemcpyAsync(c->d_vals, c->h_vals + 8, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->st));
-                k_set_prio<<<grid_for(m), 256, 0, c->st>>>(c->d_ids, c->d_vals, m, c->prio);
-                IMX_CHECK_LAUNCH();
-                count_launch(c);
-            }
+            batch0 = std::max<int64_t>(64, kr);
         }
-        // ---- commit (in flight; its gain is checked at the next header read) ----
-        IMX_CUDA(cudaMemsetAsync(hdr + H_GAIN, 0, sizeof(unsigned long long), c->st));
-        launch_commit(c, best_v, hdr + H_GAIN);
+        std::sort(back.begin(), back.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+        std::vector<int32_t> bid(back.size());
+        std::vector<unsigned long long> bkey(back.size());
+        for (size_t i = 0; i < back.size(); ++i) { bkey[i] = back[i].first; bid[i] = back[i].second; }
+        IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
+        launch_commit(c, best_v, gain);
         IMX_CHECK_LAUNCH();
         count_launch(c);
-        pending_gain = best_f;
+        IMX_TRY(celf_advance(c, kr, bid.data(), bkey.data(), (int64_t)back.size()));
+        pending = best_f;
         pending_v = best_v;
         rec(best_v, best_f, best_f, 1, t);
         if (seeds_out) seeds_out[t] = best_v;
         if (gains_out) gains_out[t] = best_f;
     }
-    IMX_CUDA(cudaMemcpyAsync(hh, hdr, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
-    IMX_TRY(check_gain((int64_t)hh[H_GAIN]));
+    IMX_CUDA(cudaMemcpy(&got, gain, sizeof got, cudaMemcpyDeviceToHost));
+    if (pending >= 0 && got != pending) {
+        set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                  (long long)got, (long long)pending, pending_v);
+        return IMX_EINTERNAL;
+    }
     cudaEventRecord(c->ev[7], c->st);
     cudaEventSynchronize(c->ev[7]);
     cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
     c->tm.celf_evaluations = c->evaluated;
-    c->ncand = 0;
     if (trace_len) *trace_len = (int64_t)(c->trace.size() / 5);
     return IMX_OK;
 }

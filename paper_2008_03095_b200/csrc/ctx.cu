@@ -33,8 +33,8 @@ void ctx_free(imx_ctx *c) {
     if (c->C) cudaFreeAsync(c->C, c->st);
     c->L = c->C = nullptr;
     if (c->st) cudaStreamSynchronize(c->st);
-    void *ptrs[] = {c->X, c->L, c->C, c->gains, c->prio, c->inS, c->cov, c->per_sim,
-                    c->cand, c->fresh, c->scratch, c->cand2, c->keys2, c->eval_out, c->d_one,
+    void *ptrs[] = {c->X, c->L, c->C, c->gains, c->inS, c->cov, c->per_sim, c->oid[0], c->oid[1],
+                    c->okey[0], c->okey[1], c->scratch, c->eval_out, c->d_one,
                     c->sort_tmp, c->d_ids, c->d_vals, c->seg_a, c->seg_n, c->seg_off, c->scan_tmp};
     for (void *p : ptrs) if (p) cudaFree(p);
     if (c->h_ids) cudaFreeHost(c->h_ids);
@@ -45,16 +45,15 @@ void ctx_free(imx_ctx *c) {
 }
 
 int ensure_celf_buffers(imx_ctx *c) {
-    if (c->prio) return IMX_OK;
+    if (c->inS) return IMX_OK;
     const int64_t n = c->g->n > 0 ? c->g->n : 1;
-    IMX_CUDA(cudaMalloc((void **)&c->prio, sizeof(int64_t) * n));
     IMX_CUDA(cudaMalloc((void **)&c->inS, n));
     IMX_CUDA(cudaMalloc((void **)&c->cov, sizeof(uint32_t) * (size_t)n * c->cw));
     IMX_CUDA(cudaMalloc((void **)&c->per_sim, sizeof(int64_t) * (c->W + 1)));
-    IMX_CUDA(cudaMalloc((void **)&c->cand, sizeof(int32_t) * n));
-    IMX_CUDA(cudaMalloc((void **)&c->fresh, sizeof(int64_t) * n));
-    IMX_CUDA(cudaMalloc((void **)&c->cand2, sizeof(int32_t) * n));
-    IMX_CUDA(cudaMalloc((void **)&c->keys2, sizeof(unsigned long long) * n));
+    for (int b = 0; b < 2; ++b) {
+        IMX_CUDA(cudaMalloc((void **)&c->oid[b], sizeof(int32_t) * n));
+        IMX_CUDA(cudaMalloc((void **)&c->okey[b], sizeof(unsigned long long) * n));
+    }
     IMX_CUDA(cudaMalloc((void **)&c->eval_out, sizeof(int64_t) * n));
     IMX_CUDA(cudaMalloc((void **)&c->d_one, sizeof(int32_t) * 4));
     return IMX_OK;

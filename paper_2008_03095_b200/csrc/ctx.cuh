@@ -34,17 +34,16 @@ struct imx_ctx {
     uint32_t *C = nullptr;        // [n*ld] caller-label mode only
     int64_t *gains = nullptr;     // [n]
     // CELF state
-    int64_t *prio = nullptr;      // [n]
     uint8_t *inS = nullptr;       // [n]
     uint32_t *cov = nullptr;      // [n*cw]
     int64_t *per_sim = nullptr;   // [W]
-    int32_t *cand = nullptr;      // [n]
-    int32_t *cand2 = nullptr;     // [n] sort output
-    int64_t *fresh = nullptr;     // [n] (also sort keys scratch)
-    unsigned long long *keys2 = nullptr;  // [n] sorted keys
     int64_t *eval_out = nullptr;  // [n]
     int32_t *d_one = nullptr;     // [4]
-    int64_t ncand = 0;
+    // candidate order: non-seeds sorted by packed stale key, double-buffered
+    int32_t *oid[2] = {nullptr, nullptr};
+    unsigned long long *okey[2] = {nullptr, nullptr};
+    int ocur = 0;
+    int64_t ostart = 0, olen = 0;
     void *sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
     int32_t *h_ids = nullptr, *d_ids = nullptr;   // pinned staging for prio updates

@@ -16,18 +16,20 @@ from conftest import load_golden
 
 
 class NumpyShard:
-    """Lanes [a, b) of a label/size matrix; same interface as DeviceContext."""
+    """Lanes [a, b) of a label/size matrix; same CELF interface as
+    DeviceContext (celf_top / celf_prefix / celf_advance)."""
 
     def __init__(self, labels, sizes, a, b, num_scored, prio):
         self.L = np.ascontiguousarray(labels[:, a:b])
         self.S = np.ascontiguousarray(sizes[:, a:b])
         self.ns = max(0, min(b, num_scored) - a)
         self.n = labels.shape[0]
-        self.prio = np.asarray(prio, np.int64).copy()
-        self.inS = np.zeros(self.n, bool)
+        prio = np.asarray(prio, np.int64)
+        ids = np.arange(self.n)
+        order = np.lexsort((ids, -prio))
+        self.order = [(int(prio[v]), int(v)) for v in order]   # sorted by (-prio, id)
         self.owned = np.zeros((self.n, self.ns), bool)
         self.per_sim = np.zeros(self.ns, np.int64)
-        self.pending = np.zeros(0, np.int64)
         self.cols = np.arange(self.ns)
 
     def _fresh(self, ids):
@@ -35,36 +37,26 @@ class NumpyShard:
         return np.where(self.owned[lu, self.cols], 0, self.S[lu, self.cols]).sum(axis=1).astype(np.int64)
 
     def celf_top(self):
-        cand = np.flatnonzero(~self.inS)
-        if not len(cand):
+        if not self.order:
             return 0, -1
-        best = cand[np.lexsort((cand, -self.prio[cand]))[0]]
-        return int(self.prio[best]), int(best)
+        return self.order[0]
 
-    def eval_gains(self, ids):
-        return self._fresh(ids)
+    def celf_prefix(self, lo, hi):
+        length = len(self.order)
+        h = max(lo, min(hi, length))
+        f = min(h + 1, length)
+        ids = np.array([v for _, v in self.order[lo:f]], np.int32)
+        pr = np.array([p for p, _ in self.order[lo:f]], np.int64)
+        return ids, pr, self._fresh(ids[: h - lo]), length
 
-    def celf_collect(self, g, u, exclude):
-        v = np.arange(self.n)
-        take = (~self.inS) & (v != exclude) & ((self.prio > g) | ((self.prio == g) & (v <= u)))
-        ids = v[take]
-        ids = ids[np.lexsort((ids, -self.prio[ids]))]
-        self.pending = ids
-        return ids.astype(np.int32), self.prio[ids].copy()
-
-    def celf_eval_collected(self, lo, hi):
-        return self._fresh(self.pending[lo:hi])
-
-    def celf_set_prio(self, ids, vals):
-        self.prio[np.asarray(ids, np.int64)] = vals
-
-    def commit(self, u):
+    def celf_advance(self, k, u, ids, prio):
         lu = self.L[u, : self.ns]
         new = ~self.owned[lu, self.cols]
         gain = int(self.S[lu, self.cols][new].sum())
         self.per_sim[new] += self.S[lu, self.cols][new]
         self.owned[lu, self.cols] = True
-        self.inS[u] = True
+        rest = self.order[k:] + [(int(p), int(v)) for v, p in zip(ids, prio)]
+        self.order = sorted(rest, key=lambda pv: (-pv[0], pv[1]))
         return gain
 
 

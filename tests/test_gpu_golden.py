@@ -129,3 +129,59 @@ def test_every_sampler_strategy_reaches_the_reference_fixpoint(gpu, name, mode, 
     assert stats.changed_pairs[0] == int((labels != np.arange(g.n)[:, None]).sum())
     sizes, gains = gpu.component_sizes_and_gains(labels, randoms.num_scored)
     assert np.array_equal(gains, z["gains"])
+
+
+class ShardSet:
+    """G lane-window contexts on one device presented as one CELF shard whose
+    partial sums are combined on the host (the logical multi-GPU mode of
+    SURVEY section 4; the driver is the one torch.distributed ranks run)."""
+
+    def __init__(self, ctxs):
+        self.ctxs = ctxs
+
+    def celf_top(self):
+        tops = {c.celf_top() for c in self.ctxs}
+        assert len(tops) == 1
+        return tops.pop()
+
+    def celf_prefix(self, lo, hi):
+        parts = [c.celf_prefix(lo, hi) for c in self.ctxs]
+        ids, prio, _, length = parts[0]
+        for p in parts[1:]:
+            assert np.array_equal(p[0], ids) and np.array_equal(p[1], prio) and p[3] == length
+        return ids, prio, sum(p[2] for p in parts), length
+
+    def celf_advance(self, k, u, ids, prio):
+        return sum(c.celf_advance(k, u, ids, prio) for c in self.ctxs)
+
+
+@pytest.mark.parametrize("shards", [2, 3])
+@pytest.mark.parametrize("name", ["er_mid_300", "er_pad20", "er_const1_r16", "cfg_c1"])
+def test_lane_sharded_device_celf_matches_reference(gpu, name, shards):
+    from paper_2008_03095_b200.celf import LocalComm, lane_window, select_rounds
+    from paper_2008_03095_b200.context import DeviceContext
+    z = load_golden(name)
+    g = build_graph(gpu, z)
+    randoms = gpu.SimulationRandoms(int(z["R"]), int(z["master_seed"]))
+    table = gpu.build_hash_table(g)
+    table.bind(g)
+    ctxs = []
+    for rank in range(shards):
+        a, b, scored = lane_window(randoms.padded, randoms.num_scored, rank, shards)
+        c = DeviceContext(g, randoms.values[a:b], scored, a)
+        c.propagate()
+        ctxs.append(c)
+    gains = sum(c.memoize() for c in ctxs)
+    assert np.array_equal(gains, z["gains"])
+    labels = np.concatenate([c.labels() for c in ctxs], axis=1)
+    assert sha(labels) == str(z["labels_sha"])
+    for c in ctxs:
+        c.celf_reset(gains)
+    seeds, sg, trace = select_rounds(ShardSet(ctxs), LocalComm(), int(z["k"]), batch0=8)
+    assert seeds.tolist() == z["seeds"].tolist()
+    assert sg.tolist() == z["seed_gains"].tolist()
+    assert np.array_equal(trace, z["trace"])
+    per_sim = np.concatenate([c.per_sim() for c in ctxs])
+    R = randoms.num_scored
+    se = 0.0 if R < 2 else float(per_sim.std(ddof=1) / np.sqrt(R))
+    assert se == pytest.approx(float(z["spread_se"]), rel=1e-12, abs=1e-15)

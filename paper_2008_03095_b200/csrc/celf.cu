@@ -256,10 +256,10 @@ extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
         IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, c->okey[1], c->okey[0], c->oid[1], c->oid[0],
                                                            n, 0, end_bit, c->st));
         if (tb > c->sort_tmp_bytes) {
-            if (c->sort_tmp) cudaFree(c->sort_tmp);
+            if (c->sort_tmp) cudaFreeAsync(c->sort_tmp, c->st);
             c->sort_tmp = nullptr;
             c->sort_tmp_bytes = 0;
-            IMX_CUDA(cudaMalloc(&c->sort_tmp, tb));
+            IMX_CUDA(pool_alloc(&c->sort_tmp, tb, c->st));
             c->sort_tmp_bytes = tb;
         }
         IMX_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, tb, c->okey[1], c->okey[0], c->oid[1],

@@ -1,11 +1,36 @@
 // ctx.cu -- context lifecycle (imx_create / imx_destroy / imx_get_timings)
 // and buffer management shared by propagate.cu, memo.cu and celf.cu.
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "ctx.cuh"
 
 namespace imx {
+
+// Pinned host staging buffers are recycled process-wide: cudaMallocHost is a
+// millisecond-scale call, and every run_fused creates a fresh context.
+static std::mutex g_pin_mu;
+static std::vector<std::pair<void *, size_t>> g_pin_free;
+
+static cudaError_t pinned_get(void **p, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        for (size_t i = 0; i < g_pin_free.size(); ++i)
+            if (g_pin_free[i].second >= bytes) {
+                *p = g_pin_free[i].first;
+                g_pin_free.erase(g_pin_free.begin() + i);
+                return cudaSuccess;
+            }
+    }
+    return cudaMallocHost(p, bytes);
+}
+
+static void pinned_put(void *p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.emplace_back(p, bytes);
+}
 
 // The label/count matrices come from the device's stream-ordered pool with an
 // unbounded release threshold, so back-to-back runs on the same graph reuse
@@ -36,9 +61,10 @@ void ctx_free(imx_ctx *c) {
     void *ptrs[] = {c->X, c->L, c->C, c->gains, c->inS, c->cov, c->per_sim, c->oid[0], c->oid[1],
                     c->okey[0], c->okey[1], c->scratch, c->eval_out, c->d_one,
                     c->sort_tmp, c->d_ids, c->d_vals, c->seg_a, c->seg_n, c->seg_off, c->scan_tmp};
-    for (void *p : ptrs) if (p) cudaFree(p);
-    if (c->h_ids) cudaFreeHost(c->h_ids);
-    if (c->h_vals) cudaFreeHost(c->h_vals);
+    for (void *p : ptrs) if (p) cudaFreeAsync(p, c->st);
+    if (c->st) cudaStreamSynchronize(c->st);
+    pinned_put(c->h_ids, sizeof(int32_t) * c->stage_cap);
+    pinned_put(c->h_vals, sizeof(int64_t) * c->stage_cap);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
@@ -47,32 +73,33 @@ void ctx_free(imx_ctx *c) {
 int ensure_celf_buffers(imx_ctx *c) {
     if (c->inS) return IMX_OK;
     const int64_t n = c->g->n > 0 ? c->g->n : 1;
-    IMX_CUDA(cudaMalloc((void **)&c->inS, n));
-    IMX_CUDA(cudaMalloc((void **)&c->cov, sizeof(uint32_t) * (size_t)n * c->cw));
-    IMX_CUDA(cudaMalloc((void **)&c->per_sim, sizeof(int64_t) * (c->W + 1)));
+    IMX_CUDA(pool_alloc((void **)&c->inS, n, c->st));
+    IMX_CUDA(pool_alloc((void **)&c->cov, sizeof(uint32_t) * (size_t)n * c->cw, c->st));
+    IMX_CUDA(pool_alloc((void **)&c->per_sim, sizeof(int64_t) * (c->W + 1), c->st));
     for (int b = 0; b < 2; ++b) {
-        IMX_CUDA(cudaMalloc((void **)&c->oid[b], sizeof(int32_t) * n));
-        IMX_CUDA(cudaMalloc((void **)&c->okey[b], sizeof(unsigned long long) * n));
+        IMX_CUDA(pool_alloc((void **)&c->oid[b], sizeof(int32_t) * n, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->okey[b], sizeof(unsigned long long) * n, c->st));
     }
-    IMX_CUDA(cudaMalloc((void **)&c->eval_out, sizeof(int64_t) * n));
-    IMX_CUDA(cudaMalloc((void **)&c->d_one, sizeof(int32_t) * 4));
+    IMX_CUDA(pool_alloc((void **)&c->eval_out, sizeof(int64_t) * n, c->st));
+    IMX_CUDA(pool_alloc((void **)&c->d_one, sizeof(int32_t) * 4, c->st));
     return IMX_OK;
 }
 
 int ensure_pinned(imx_ctx *c, int64_t cnt) {
     if (cnt <= c->stage_cap) return IMX_OK;
     int64_t cap = std::max<int64_t>(cnt, 4096);
-    if (c->h_ids) cudaFreeHost(c->h_ids);
-    if (c->h_vals) cudaFreeHost(c->h_vals);
-    if (c->d_ids) cudaFree(c->d_ids);
-    if (c->d_vals) cudaFree(c->d_vals);
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    pinned_put(c->h_ids, sizeof(int32_t) * c->stage_cap);
+    pinned_put(c->h_vals, sizeof(int64_t) * c->stage_cap);
+    if (c->d_ids) cudaFreeAsync(c->d_ids, c->st);
+    if (c->d_vals) cudaFreeAsync(c->d_vals, c->st);
     c->h_ids = nullptr; c->h_vals = nullptr; c->d_ids = nullptr; c->d_vals = nullptr;
     c->stage_cap = 0;
     IMX_CUDA(cudaStreamSynchronize(c->st));
-    IMX_CUDA(cudaMallocHost((void **)&c->h_ids, sizeof(int32_t) * cap));
-    IMX_CUDA(cudaMallocHost((void **)&c->h_vals, sizeof(int64_t) * cap));
-    IMX_CUDA(cudaMalloc((void **)&c->d_ids, sizeof(int32_t) * cap));
-    IMX_CUDA(cudaMalloc((void **)&c->d_vals, sizeof(int64_t) * cap));
+    IMX_CUDA(pinned_get((void **)&c->h_ids, sizeof(int32_t) * cap));
+    IMX_CUDA(pinned_get((void **)&c->h_vals, sizeof(int64_t) * cap));
+    IMX_CUDA(pool_alloc((void **)&c->d_ids, sizeof(int32_t) * cap, c->st));
+    IMX_CUDA(pool_alloc((void **)&c->d_vals, sizeof(int64_t) * cap, c->st));
     c->stage_cap = cap;
     return IMX_OK;
 }
@@ -116,15 +143,16 @@ extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t
         if (cudaEventCreate(&e) != cudaSuccess) return fail(IMX_ECUDA);
     const size_t cells = (size_t)(n > 0 ? n : 1) * (size_t)c->ld;
     cudaError_t e = cudaSuccess;
-    if ((e = cudaMalloc((void **)&c->X, sizeof(int32_t) * c->ld)) != cudaSuccess ||
+    if ((e = pool_alloc((void **)&c->X, sizeof(int32_t) * c->ld, c->st)) != cudaSuccess ||
         (e = pool_alloc((void **)&c->L, sizeof(uint32_t) * cells, c->st)) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->gains, sizeof(int64_t) * (n + 1))) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->scratch, sizeof(unsigned long long) * 16)) != cudaSuccess) {
+        (e = pool_alloc((void **)&c->gains, sizeof(int64_t) * (n + 1), c->st)) != cudaSuccess ||
+        (e = pool_alloc((void **)&c->scratch, sizeof(unsigned long long) * 16, c->st)) != cudaSuccess) {
         return fail(cuda_fail(e, "cudaMalloc(context)", __FILE__, __LINE__));
     }
     std::vector<int32_t> xpad(c->ld, 0);
     std::copy(X, X + width, xpad.begin());
-    if ((e = cudaMemcpy(c->X, xpad.data(), sizeof(int32_t) * c->ld, cudaMemcpyHostToDevice)) != cudaSuccess)
+    if ((e = cudaMemcpyAsync(c->X, xpad.data(), sizeof(int32_t) * c->ld, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
         return fail(cuda_fail(e, "upload X", __FILE__, __LINE__));
     *out = c;
     return IMX_OK;

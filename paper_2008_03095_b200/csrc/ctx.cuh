@@ -76,7 +76,6 @@ inline void count_launch(imx_ctx *c, int k = 1) {
     note_launch(k);
 }
 
-cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
 int ensure_celf_buffers(imx_ctx *c);
 int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);

@@ -299,11 +299,14 @@ static int grid_for(int64_t work, int threads = 256) {
     return (int)b;
 }
 
+// Every device buffer comes from the stream-ordered pool (pool_alloc, a
+// high release threshold), so building/dropping graphs and contexts back to
+// back does not pay cudaMalloc/cudaFree each time.
 template <class T>
-static int dalloc(T **p, int64_t count) {
+static int dalloc(imx_graph *g, T **p, int64_t count) {
     *p = nullptr;
     if (count <= 0) count = 1;
-    IMX_CUDA(cudaMalloc((void **)p, sizeof(T) * (size_t)count));
+    IMX_CUDA(pool_alloc((void **)p, sizeof(T) * (size_t)count, g->stream));
     return IMX_OK;
 }
 
@@ -312,8 +315,11 @@ void graph_free(imx_graph *g) {
     cudaSetDevice(g->dev);
     void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
                     g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff};
-    for (void *p : ptrs) if (p) cudaFree(p);
-    if (g->stream) cudaStreamDestroy(g->stream);
+    for (void *p : ptrs) if (p) cudaFreeAsync(p, g->stream);
+    if (g->stream) {
+        cudaStreamSynchronize(g->stream);
+        cudaStreamDestroy(g->stream);
+    }
     delete g;
 }
 
@@ -329,12 +335,12 @@ static int graph_finish(imx_graph *g) {
     cudaStream_t st = g->stream;
     const int64_t m2 = g->m2, n = g->n;
     if (!g->src) {
-        IMX_TRY(dalloc(&g->src, m2));
+        IMX_TRY(dalloc(g, &g->src, m2));
         if (m2) { k_src_from_xadj<<<grid_for(m2), 256, 0, st>>>(g->xadj, n, m2, g->src); IMX_CHECK_LAUNCH(); }
     }
-    IMX_TRY(dalloc(&g->hash, m2));
-    IMX_TRY(dalloc(&g->thr, m2));
-    IMX_TRY(dalloc(&g->recip, m2));
+    IMX_TRY(dalloc(g, &g->hash, m2));
+    IMX_TRY(dalloc(g, &g->thr, m2));
+    IMX_TRY(dalloc(g, &g->recip, m2));
     unsigned *dflags;
     IMX_CUDA(cudaMallocAsync((void **)&dflags, sizeof(unsigned), st));
     IMX_CUDA(cudaMemsetAsync(dflags, 0, sizeof(unsigned), st));
@@ -365,7 +371,7 @@ static int graph_finish(imx_graph *g) {
         uint8_t *flag;
         int64_t *cslot, *dcount;
         IMX_CUDA(cudaMallocAsync((void **)&flag, m2, st));
-        IMX_CUDA(cudaMalloc((void **)&cslot, sizeof(int64_t) * m2));
+        IMX_CUDA(pool_alloc((void **)&cslot, sizeof(int64_t) * m2, st));
         IMX_CUDA(cudaMallocAsync((void **)&dcount, sizeof(int64_t), st));
         k_canon_flags<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, flag); note_launch();
         IMX_CHECK_LAUNCH();
@@ -379,9 +385,9 @@ static int graph_finish(imx_graph *g) {
         IMX_CUDA(cudaMemcpyAsync(&me, dcount, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         IMX_CUDA(cudaStreamSynchronize(st));
         g->me = me;
-        IMX_TRY(dalloc(&g->E, me));
-        IMX_TRY(dalloc(&g->EH, me));
-        IMX_TRY(dalloc(&g->ET, me));
+        IMX_TRY(dalloc(g, &g->E, me));
+        IMX_TRY(dalloc(g, &g->EH, me));
+        IMX_TRY(dalloc(g, &g->ET, me));
         g->cslot = cslot;
         cudaFreeAsync(tmp, st);
         cudaFreeAsync(flag, st);
@@ -397,11 +403,11 @@ static int graph_build_index(imx_graph *g) {
     cudaStream_t st = g->stream;
     const int64_t me = g->me;
     const int nb = g->uniform ? 1 : (int)std::min<int64_t>(64, std::max<int64_t>(1, me));
-    if (g->btmax) { cudaFree(g->btmax); g->btmax = nullptr; }
-    if (g->boff) { cudaFree(g->boff); g->boff = nullptr; }
+    if (g->btmax) { cudaFreeAsync(g->btmax, st); g->btmax = nullptr; }
+    if (g->boff) { cudaFreeAsync(g->boff, st); g->boff = nullptr; }
     g->nb = nb;
-    IMX_CUDA(cudaMalloc((void **)&g->btmax, sizeof(int32_t) * nb));
-    IMX_CUDA(cudaMalloc((void **)&g->boff, sizeof(int64_t) * (nb + 1)));
+    IMX_CUDA(pool_alloc((void **)&g->btmax, sizeof(int32_t) * nb, st));
+    IMX_CUDA(pool_alloc((void **)&g->boff, sizeof(int64_t) * (nb + 1), st));
     IMX_CUDA(cudaMemsetAsync(g->btmax, 0, sizeof(int32_t) * nb, st));
     IMX_CUDA(cudaMemsetAsync(g->boff, 0, sizeof(int64_t) * (nb + 1), st));
     if (me == 0) return IMX_OK;
@@ -546,7 +552,7 @@ extern "C" int imx_graph_from_edges(int32_t device, int64_t n, const int64_t *ed
     const int64_t m2 = 2 * k;
     int rc = IMX_OK;
     auto fail = [&](int code) { graph_free(g); return code; };
-    if (dalloc(&g->xadj, n + 1) || dalloc(&g->adj, m2) || dalloc(&g->w, m2) || dalloc(&g->src, m2))
+    if (dalloc(g, &g->xadj, n + 1) || dalloc(g, &g->adj, m2) || dalloc(g, &g->w, m2) || dalloc(g, &g->src, m2))
         return fail(IMX_ENOMEM);
     if (k > 0) {
         int nb = 1;
@@ -619,7 +625,7 @@ extern "C" int imx_graph_from_csr(int32_t device, int64_t n, int64_t m2, const i
     IMX_TRY(graph_new(device, n, m2, &g));
     cudaStream_t st = g->stream;
     auto fail = [&](int code) { graph_free(g); return code; };
-    if (dalloc(&g->xadj, n + 1) || dalloc(&g->adj, m2) || dalloc(&g->w, m2)) return fail(IMX_ENOMEM);
+    if (dalloc(g, &g->xadj, n + 1) || dalloc(g, &g->adj, m2) || dalloc(g, &g->w, m2)) return fail(IMX_ENOMEM);
     if (cudaMemcpyAsync(g->xadj, xadj, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st) != cudaSuccess ||
         (m2 && cudaMemcpyAsync(g->adj, adj, sizeof(int32_t) * m2, cudaMemcpyHostToDevice, st) != cudaSuccess) ||
         (m2 && cudaMemcpyAsync(g->w, weights, sizeof(double) * m2, cudaMemcpyHostToDevice, st) != cudaSuccess))

@@ -478,17 +478,17 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const int64_t nseg = (int64_t)c->W * g->nb * 31;
     if (nseg + 1 > c->nseg_cap) {
-        for (int64_t **p : {&c->seg_a, &c->seg_n, &c->seg_off}) { if (*p) cudaFree(*p); *p = nullptr; }
+        for (int64_t **p : {&c->seg_a, &c->seg_n, &c->seg_off}) { if (*p) cudaFreeAsync(*p, c->st); *p = nullptr; }
         c->nseg_cap = 0;
-        IMX_CUDA(cudaMalloc((void **)&c->seg_a, sizeof(int64_t) * (nseg + 1)));
-        IMX_CUDA(cudaMalloc((void **)&c->seg_n, sizeof(int64_t) * (nseg + 1)));
-        IMX_CUDA(cudaMalloc((void **)&c->seg_off, sizeof(int64_t) * (nseg + 1)));
+        IMX_CUDA(pool_alloc((void **)&c->seg_a, sizeof(int64_t) * (nseg + 1), c->st));
+        IMX_CUDA(pool_alloc((void **)&c->seg_n, sizeof(int64_t) * (nseg + 1), c->st));
+        IMX_CUDA(pool_alloc((void **)&c->seg_off, sizeof(int64_t) * (nseg + 1), c->st));
         c->nseg_cap = nseg + 1;
         size_t tb = 0;
         IMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
         if (tb > c->scan_tmp_bytes) {
-            if (c->scan_tmp) cudaFree(c->scan_tmp);
-            IMX_CUDA(cudaMalloc(&c->scan_tmp, tb));
+            if (c->scan_tmp) cudaFreeAsync(c->scan_tmp, c->st);
+            IMX_CUDA(pool_alloc(&c->scan_tmp, tb, c->st));
             c->scan_tmp_bytes = tb;
         }
     }
@@ -679,7 +679,7 @@ extern "C" int imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2, f
     if (reps < 1) { set_error("reps must be >= 1"); return IMX_EINVAL; }
     uint4 *fb = nullptr;
     const int64_t fcnt = (int64_t(256) << 20) / 16;  // 256 MB > 126 MB L2
-    if (flush_l2) IMX_CUDA(cudaMalloc((void **)&fb, fcnt * 16));
+    if (flush_l2) IMX_CUDA(pool_alloc((void **)&fb, fcnt * 16, c->st));
     std::vector<cudaEvent_t> ev(4 * reps);
     for (auto &e : ev) IMX_CUDA(cudaEventCreate(&e));
     if (c->C) { cudaFreeAsync(c->C, c->st); c->C = nullptr; }
@@ -707,7 +707,7 @@ extern "C" int imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2, f
         tot += a; hk += b; cp += d; in += e;
     }
     for (auto &e : ev) cudaEventDestroy(e);
-    if (fb) cudaFree(fb);
+    if (fb) cudaFreeAsync(fb, c->st);
     if (avg_total_ms) *avg_total_ms = (float)(tot / reps);
     if (avg_hook_ms) *avg_hook_ms = (float)(hk / reps);
     if (avg_compress_ms) *avg_compress_ms = (float)(cp / reps);

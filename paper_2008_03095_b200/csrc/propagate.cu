@@ -178,7 +178,7 @@ __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
 // consecutive j (one binary search over the segment offsets per chunk, then
 // a forward walk), so consecutive threads read consecutive edges of the same
 // hash interval (coalesced) and every thread runs one union per pair.
-constexpr int kEnumChunk = 1024;
+constexpr int kEnumChunk = 128;
 template <bool UNI>
 __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ off, const int64_t *__restrict__ seg_a,
                                                    int64_t nseg, int segs_per_lane,
@@ -342,6 +342,26 @@ __device__ __forceinline__ uint32_t ld_ca(const uint32_t *p) {
     return v;
 }
 
+__device__ __forceinline__ void compress_lane(uint32_t *__restrict__ L, int64_t ld, uint32_t v, uint32_t w,
+                                              uint32_t gw, int r, int j, uint32_t (&hot)[kHot][4],
+                                              unsigned long long &cnt) {
+    uint32_t x = v, p = w;
+    while (!is_root(gw)) {          // path splitting, min-safe
+        atomicMin(cell(L, ld, x, r), gw);
+        x = p;
+        p = gw;
+        gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r)) : ld_relaxed(cell(L, ld, p, r));
+    }
+    if (p != w) L[(int64_t)v * ld + r] = p;
+    if (p < (uint32_t)kHot) {
+#pragma unroll
+        for (int h = 0; h < kHot; ++h) hot[h][j] += (p == (uint32_t)h);
+    } else {
+        atomicAdd(cell(L, ld, p, r), 1u);
+    }
+    ++cnt;
+}
+
 __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
                                                   int64_t vstep, unsigned long long *__restrict__ nonroot) {
     const int64_t nq = ld >> 2;
@@ -354,29 +374,28 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
 #pragma unroll
         for (int j = 0; j < 4; ++j) hot[h][j] = 0;
     unsigned long long cnt = 0;
-    // threads past the last whole row of the grid would revisit rows
-    for (int64_t v = (t < vstep * nq) ? t / nq : n; v < n; v += vstep) {
-        const uint4 l = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
-        const uint32_t w[4] = {l.x, l.y, l.z, l.w};
+    // two rows per iteration and all first-level parent words loaded before
+    // any walk: up to 2 row loads + 8 parent loads in flight per thread
+    for (int64_t v = (t < vstep * nq) ? t / nq : n; v < n; v += 2 * vstep) {
+        const int64_t v2 = v + vstep;
+        const bool has2 = v2 < n;
+        const uint4 l1 = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
+        uint4 l2 = make_uint4(ROOT, ROOT, ROOT, ROOT);
+        if (has2) l2 = *(reinterpret_cast<const uint4 *>(L + v2 * ld) + q);
+        const uint32_t w[8] = {l1.x, l1.y, l1.z, l1.w, l2.x, l2.y, l2.z, l2.w};
+        uint32_t gw[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (r + j >= W || is_root(w[j])) continue;
-            uint32_t x = (uint32_t)v, p = w[j];
-            uint32_t gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r + j)) : ld_relaxed(cell(L, ld, p, r + j));
-            while (!is_root(gw)) {          // path splitting, min-safe
-                atomicMin(cell(L, ld, x, r + j), gw);
-                x = p;
-                p = gw;
-                gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r + j)) : ld_relaxed(cell(L, ld, p, r + j));
-            }
-            if (p != w[j]) L[v * ld + r + j] = p;
-            if (p < (uint32_t)kHot) {
+        for (int k = 0; k < 8; ++k) {
+            const int rj = r + (k & 3);
+            gw[k] = ROOT;
+            if (rj < W && !is_root(w[k]))
+                gw[k] = w[k] < (uint32_t)kHot ? ld_ca(cell(L, ld, w[k], rj)) : ld_relaxed(cell(L, ld, w[k], rj));
+        }
 #pragma unroll
-                for (int h = 0; h < kHot; ++h) hot[h][j] += (p == (uint32_t)h);
-            } else {
-                atomicAdd(cell(L, ld, p, r + j), 1u);
-            }
-            ++cnt;
+        for (int k = 0; k < 8; ++k) {
+            const int rj = r + (k & 3);
+            if (rj >= W || is_root(w[k])) continue;
+            compress_lane(L, ld, (uint32_t)(k < 4 ? v : v2), w[k], gw[k], rj, k & 3, hot, cnt);
         }
     }
 #pragma unroll

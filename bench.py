@@ -306,6 +306,9 @@ def run_ours(args, world, rank, local):
     e2e_s = float(np.mean(times))
     h2d = 8 * (n + 1) + 4 * m2 + 8 * m2 + 4 * len(X)
 
+    traffic_frac = None
+    if traffic:
+        traffic_frac = traffic / (res["total_ms"] / 1e3) / 1e9 / peak
     line = {
         "metric": "fused sample+CC edge-sims/sec (2m*R per converged sample+CC)",
         "value": value, "unit": "edge-sims/s", "n_gpus": world, "steps": args.steps,
@@ -317,6 +320,7 @@ def run_ours(args, world, rank, local):
                    "parallelism": f"R-sharded x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "traffic_frac": traffic_frac,
                      "kernel": "propagate = k_init + k_hook + k_compress (one converged sample+CC)",
                      "model": f"B_es={bes:.3f} B/edge-sim dense-sweep model (SURVEY 8(d)) x 2m*R_gpu",
                      "peak_source": peak_src, "dominant_kernel": dominant,

@@ -14,8 +14,13 @@
 // fresh keys.  No per-round scan or sort of all n vertices; one or two host
 // syncs per round; the dequeue trace is the evaluated prefix itself.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 #include <cub/cub.cuh>
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
 
 #include "ctx.cuh"
 #include "uf.cuh"
@@ -212,6 +217,218 @@ static int celf_advance(imx_ctx *c, int64_t k, const int32_t *ids, const unsigne
     return IMX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// The whole CELF loop as ONE cooperative kernel (single-rank path).
+//
+// Every block keeps the same copy of the round state (order window, best
+// candidate, trace length) and takes the same decisions from the same global
+// data, so grid-wide barriers replace the host round trips of the
+// host-driven loop.  A round: evaluate prefix batches (CTA per candidate),
+// barrier, every block reduces the best fresh key and tests the stop rule;
+// the refreshed prefix length kr is a binary search (keys are sorted); the
+// prefix is written to the trace, the winner committed; the other kr-1
+// refreshed vertices are ranked by their fresh keys (O(kr^2) compare-count,
+// kr <= kMaxRank), scattered, and merged back into the order.  A round that
+// does not fit (trace buffer full, kr too large) stops the kernel with the
+// state saved; the host finishes that round and relaunches.
+// ---------------------------------------------------------------------------
+constexpr int64_t kMaxRank = 16384;
+
+
+template <bool ENC>
+__device__ __forceinline__ int64_t block_eval(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                                              const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
+                                              int32_t cw, int64_t u, unsigned long long *red) {
+    const int nqs = (ns + 3) >> 2;
+    const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
+    unsigned long long acc = 0;
+    for (int q = threadIdx.x; q < nqs; q += blockDim.x) {
+        const uint4 l4 = row[q];
+        const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        uint32_t wd[4], sz[4];
+        const int r = q << 2;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool in = r + j < ns;
+            uint32_t lab = 0;
+            sz[j] = in ? cell_size<ENC>(L, C, ld, (uint32_t)u, lv[j], r + j, lab) : 0u;
+            wd[j] = in ? cov[(int64_t)lab * cw + ((r + j) >> 5)] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (!((wd[j] >> ((r + j) & 31)) & 1u)) acc += sz[j];
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    unsigned long long tot = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += red[k];
+    return (int64_t)tot;
+}
+
+__device__ __forceinline__ unsigned long long block_max(unsigned long long x, unsigned long long *red) {
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+        x = y > x ? y : x;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    unsigned long long m = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = red[k] > m ? red[k] : m;
+    return m;
+}
+
+template <bool ENC>
+__global__ void __launch_bounds__(256) k_celf_rounds(
+    int32_t k, int vb, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, uint32_t *__restrict__ cov,
+    int64_t ld, int32_t ns, int32_t cw, int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
+    int32_t *oid0, int32_t *oid1, unsigned long long *okey0, unsigned long long *okey1,
+    int64_t *__restrict__ fresh, unsigned long long *__restrict__ bkey, int32_t *__restrict__ bid,
+    unsigned long long *__restrict__ skey, int32_t *__restrict__ sid,
+    int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
+    int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned long long red[8];
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+    const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
+    int64_t ostart = st->ostart, olen = st->olen, T = st->trace_len, batch0 = st->batch0;
+    int ocur = st->ocur;
+    int32_t t = st->t;
+    int32_t status = 0;
+    while (t < k) {
+        int32_t *oid = ocur ? oid1 : oid0;
+        unsigned long long *okey = ocur ? okey1 : okey0;
+        if (olen == 0) { status = 3; break; }
+        // the previous round's gain was read by every block before its last barrier
+        if (gtid == 0 && t > st->t) *gain = 0;
+        unsigned long long bestkey;
+        int64_t kr;
+        if (t == 0) {
+            bestkey = okey[ostart];        // fresh_at == len(S) == 0: the first pop commits
+            kr = 1;
+        } else {
+            int64_t lo = 0, hi = olen < batch0 ? olen : batch0;
+            bestkey = 0;
+            for (;;) {
+                for (int64_t i = lo + blockIdx.x; i < hi; i += gridDim.x) {
+                    const int64_t f = block_eval<ENC>(L, C, cov, ld, ns, cw, oid[ostart + i], red);
+                    if (threadIdx.x == 0) fresh[i] = f;
+                }
+                grid.sync();
+                unsigned long long m = 0;
+                for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                    const unsigned long long fk = ((unsigned long long)fresh[i] << vb) |
+                                                  (unsigned long long)(vmask - (uint32_t)oid[ostart + i]);
+                    m = fk > m ? fk : m;
+                }
+                m = block_max(m, red);
+                bestkey = m > bestkey ? m : bestkey;
+                if (hi >= olen || bestkey >= okey[ostart + hi]) break;   // nothing unevaluated can win
+                lo = hi;
+                const int64_t step = batch0 > hi ? batch0 : hi;
+                hi = (olen - hi < step) ? olen : hi + step;
+            }
+            // refreshed prefix: stale key >= best fresh key (keys sorted descending)
+            int64_t a = 0, b = hi;
+            while (a < b) {
+                const int64_t mid = (a + b) >> 1;
+                if (okey[ostart + mid] >= bestkey) a = mid + 1; else b = mid;
+            }
+            kr = a;
+        }
+        const int32_t best_v = (int32_t)(vmask - (uint32_t)(bestkey & vmask));
+        const int64_t best_f = (int64_t)(bestkey >> vb);
+        const int64_t nrec = (t == 0 ? 0 : kr) + 1;
+        if (T + nrec > trace_cap) { status = 2; break; }    // host drains the trace, relaunches
+        if (kr > kMaxRank) { status = 4; break; }           // host runs this round, relaunches
+        // phase 1: trace, refreshed vertices with their fresh keys, commit
+        if (t > 0) {
+            for (int64_t i = gtid; i < kr; i += gthreads) {
+                const int32_t v = oid[ostart + i];
+                const int64_t f = fresh[i];
+                int64_t *rec = trace + 5 * (T + i);
+                rec[0] = v; rec[1] = (int64_t)(okey[ostart + i] >> vb); rec[2] = f; rec[3] = 0; rec[4] = t;
+                bkey[i] = v == best_v ? 0ull : (((unsigned long long)f << vb) | (unsigned long long)(vmask - (uint32_t)v));
+                bid[i] = v;
+            }
+        }
+        if (gtid == 0) {
+            int64_t *rec = trace + 5 * (T + nrec - 1);
+            rec[0] = best_v; rec[1] = best_f; rec[2] = best_f; rec[3] = 1; rec[4] = t;
+            seeds[t] = best_v;
+            sgains[t] = best_f;
+            inS[best_v] = 1;
+        }
+        {
+            unsigned long long acc = 0;
+            for (int64_t r = gtid; r < ns; r += gthreads) {
+                uint32_t lab;
+                const uint32_t sz = cell_size<ENC>(L, C, ld, (uint32_t)best_v, L[(int64_t)best_v * ld + r], (int)r, lab);
+                const uint32_t bit = 1u << (r & 31);
+                const uint32_t old = atomicOr(cov + (int64_t)lab * cw + (r >> 5), bit);
+                if (!(old & bit)) { per_sim[r] += sz; acc += sz; }
+            }
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if ((threadIdx.x & 31) == 0 && acc) atomicAdd(gain, acc);
+        }
+        grid.sync();
+        // phase 2: self-check of the commit; rank + scatter the refreshed vertices
+        const unsigned long long got = *gain;
+        if ((int64_t)got != best_f) {
+            if (gtid == 0) { st->bad_v = best_v; st->bad_want = best_f; st->bad_got = (int64_t)got; }
+            status = 3;
+            break;
+        }
+        const int64_t nback = t == 0 ? 0 : kr - 1;       // the winner is not re-inserted
+        if (nback > 0) {
+            for (int64_t j = gtid; j < kr; j += gthreads) {
+                const unsigned long long kj = bkey[j];
+                int64_t rk = 0;
+                for (int64_t i = 0; i < kr; ++i) rk += bkey[i] > kj;
+                if (rk < nback) { skey[rk] = kj; sid[rk] = bid[j]; }
+            }
+            grid.sync();
+            // phase 3: merge order[kr, olen) with the sorted refreshed vertices
+            int32_t *ob = ocur ? oid0 : oid1;
+            unsigned long long *okb = ocur ? okey0 : okey1;
+            const int64_t na = olen - kr;
+            const unsigned long long *ak = okey + ostart + kr;
+            const int32_t *ai = oid + ostart + kr;
+            for (int64_t i = gtid; i < na + nback; i += gthreads) {
+                const bool in_a = i < na;
+                const int64_t j = in_a ? i : i - na;
+                const unsigned long long key = in_a ? ak[j] : skey[j];
+                const unsigned long long *other = in_a ? skey : ak;
+                int64_t lo2 = 0, hi2 = in_a ? nback : na;
+                while (lo2 < hi2) {
+                    const int64_t mid = (lo2 + hi2) >> 1;
+                    if (other[mid] > key) lo2 = mid + 1; else hi2 = mid;
+                }
+                ob[j + lo2] = in_a ? ai[j] : sid[j];
+                okb[j + lo2] = key;
+            }
+            ocur ^= 1;
+            ostart = 0;
+            olen = na + nback;
+        } else {
+            ostart += kr;
+            olen -= kr;
+        }
+        T += nrec;
+        if (t > 0) batch0 = kr > 64 ? kr : 64;
+        ++t;
+        grid.sync();
+    }
+    if (gtid == 0) {
+        st->ostart = ostart; st->olen = olen; st->ocur = ocur; st->t = t;
+        st->trace_len = T; st->batch0 = batch0;
+        st->status = status ? status : 1;
+    }
+}
+
 static inline bool key_le(int64_t pa, int32_t va, int64_t pb, int32_t vb) {
     // (-pa, va) <= (-pb, vb)
     return pa > pb || (pa == pb && va <= vb);
@@ -370,7 +587,157 @@ extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
     return IMX_OK;
 }
 
-// The whole CELF loop on one context (single-rank path).
+// One round on the host-driven path (prefix batches + advance), synchronous.
+static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seeds_out, int64_t *gains_out) {
+    auto rec = [&](int64_t v, int64_t s, int64_t f, int64_t com) {
+        c->trace.push_back(v); c->trace.push_back(s); c->trace.push_back(f);
+        c->trace.push_back(com); c->trace.push_back(t);
+    };
+    if (c->olen == 0) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
+    std::vector<int32_t> ids;
+    std::vector<unsigned long long> keys;
+    std::vector<int64_t> fr;
+    std::vector<std::pair<unsigned long long, int32_t>> back;
+    int64_t best_f = -1, kr = 1;
+    int32_t best_v = -1;
+    if (t == 0) {
+        ids.resize(1);
+        keys.resize(1);
+        IMX_CUDA(cudaMemcpyAsync(ids.data(), c->oid[c->ocur] + c->ostart, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaMemcpyAsync(keys.data(), c->okey[c->ocur] + c->ostart, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        best_v = ids[0];
+        best_f = key_prio(c, keys[0]);
+    } else {
+        const int64_t len = c->olen;
+        int64_t lo = 0, hi = std::min(len, batch0);
+        for (;;) {
+            if ((int64_t)ids.size() < hi + 1) { ids.resize(hi + 1); keys.resize(hi + 1); fr.resize(hi + 1); }
+            IMX_TRY(celf_prefix(c, lo, hi, ids.data() + lo, keys.data() + lo, fr.data() + lo));
+            for (int64_t i = lo; i < hi; ++i)
+                if (best_v < 0 || key_le(fr[i], ids[i], best_f, best_v)) { best_f = fr[i]; best_v = ids[i]; }
+            if (hi >= len) break;
+            if (key_le(best_f, best_v, key_prio(c, keys[hi]), ids[hi])) break;   // nothing unevaluated can win
+            lo = hi;
+            hi = std::min(len, hi + std::max<int64_t>(batch0, hi));
+        }
+        kr = 0;
+        while (kr < hi && key_le(key_prio(c, keys[kr]), ids[kr], best_f, best_v)) {
+            rec(ids[kr], key_prio(c, keys[kr]), fr[kr], 0);
+            if (ids[kr] != best_v) back.emplace_back(host_key(c, fr[kr], ids[kr]), ids[kr]);
+            ++kr;
+        }
+        batch0 = std::max<int64_t>(64, kr);
+    }
+    std::sort(back.begin(), back.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+    std::vector<int32_t> bid(back.size());
+    std::vector<unsigned long long> bkey(back.size());
+    for (size_t i = 0; i < back.size(); ++i) { bkey[i] = back[i].first; bid[i] = back[i].second; }
+    unsigned long long *gain = c->scratch + 7;
+    IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
+    launch_commit(c, best_v, gain);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    IMX_TRY(celf_advance(c, kr, bid.data(), bkey.data(), (int64_t)back.size()));
+    unsigned long long got = 0;
+    IMX_CUDA(cudaMemcpyAsync(&got, gain, sizeof got, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if ((int64_t)got != best_f) {
+        set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                  (long long)got, (long long)best_f, best_v);
+        return IMX_EINTERNAL;
+    }
+    rec(best_v, best_f, best_f, 1);
+    if (seeds_out) seeds_out[t] = best_v;
+    if (gains_out) gains_out[t] = best_f;
+    return IMX_OK;
+}
+
+// Persistent-kernel path: launch k_celf_rounds for rounds [t, k); returns
+// the kernel's status (1 done, 2 trace full, 4 round too large).
+static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, int32_t *status_out,
+                              int32_t *t_out, int64_t *batch0_out, std::vector<int32_t> &seeds,
+                              std::vector<int64_t> &gains) {
+    const int64_t n = c->g->n;
+    if (!c->cdev) {
+        IMX_CUDA(pool_alloc((void **)&c->cdev, sizeof(CelfDev), c->st));
+        IMX_CUDA(pool_alloc((void **)&c->bkey, sizeof(unsigned long long) * kMaxRank, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->skey, sizeof(unsigned long long) * kMaxRank, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->bid, sizeof(int32_t) * kMaxRank, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->sid, sizeof(int32_t) * kMaxRank, c->st));
+        c->trace_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(4 * n + 4096, 1 << 21));
+        if (const char *tc = getenv("IMX_CELF_TRACE_CAP")) c->trace_cap = std::max<int64_t>(8, atoll(tc));
+        IMX_CUDA(pool_alloc((void **)&c->dtrace, sizeof(int64_t) * 5 * c->trace_cap, c->st));
+    }
+    if (!c->dseeds || c->dseeds_cap < k) {
+        if (c->dseeds) { cudaFreeAsync(c->dseeds, c->st); cudaFreeAsync(c->dsgains, c->st); }
+        IMX_CUDA(pool_alloc((void **)&c->dseeds, sizeof(int32_t) * k, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->dsgains, sizeof(int64_t) * k, c->st));
+        c->dseeds_cap = k;
+    }
+    CelfDev h{};
+    h.ostart = c->ostart; h.olen = c->olen; h.ocur = c->ocur; h.t = t;
+    h.trace_len = 0; h.batch0 = batch0; h.status = 0;
+    IMX_CUDA(cudaMemcpyAsync(c->cdev, &h, sizeof h, cudaMemcpyHostToDevice, c->st));
+    unsigned long long *gain = c->scratch + 7;
+    IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
+    static int grid_cache[2] = {0, 0};
+    const int enc = c->C ? 0 : 1;
+    void *fn = enc ? (void *)k_celf_rounds<true> : (void *)k_celf_rounds<false>;
+    if (!grid_cache[enc]) {
+        int per_sm = 0, sms = 0;
+        IMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+        IMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
+        grid_cache[enc] = std::max(1, std::min(per_sm, 4)) * sms;
+    }
+    int32_t kk = k;
+    int vb = c->vb;
+    const uint32_t *L = c->L, *C = c->C;
+    uint32_t *cov = c->cov;
+    int64_t ld = c->ld;
+    int32_t ns = c->ns, cw = c->cw;
+    int64_t *per_sim = c->per_sim, *fresh = c->eval_out, *trace = c->dtrace, *sg = c->dsgains;
+    uint8_t *inS = c->inS;
+    int32_t *o0 = c->oid[0], *o1 = c->oid[1], *bid = c->bid, *sid = c->sid, *sd = c->dseeds;
+    unsigned long long *k0 = c->okey[0], *k1 = c->okey[1], *bkey = c->bkey, *skey = c->skey;
+    int64_t cap = c->trace_cap;
+    CelfDev *stp = c->cdev;
+    void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
+                    &bkey, &bid, &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp};
+    IMX_CUDA(cudaLaunchCooperativeKernel(fn, grid_cache[enc], 256, args, 0, c->st));
+    count_launch(c);
+    IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (h.status == 3) {
+        if (h.olen == 0) set_error("no candidate left at round %d", h.t);
+        else set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                       (long long)h.bad_got, (long long)h.bad_want, h.bad_v);
+        return IMX_EINTERNAL;
+    }
+    // collect the records and the seeds of the rounds this launch finished
+    if (h.trace_len) {
+        const size_t base = c->trace.size();
+        c->trace.resize(base + 5 * h.trace_len);
+        IMX_CUDA(cudaMemcpyAsync(c->trace.data() + base, c->dtrace, sizeof(int64_t) * 5 * h.trace_len,
+                                 cudaMemcpyDeviceToHost, c->st));
+    }
+    if (h.t > t) {
+        IMX_CUDA(cudaMemcpyAsync(seeds.data() + t, c->dseeds + t, sizeof(int32_t) * (h.t - t), cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaMemcpyAsync(gains.data() + t, c->dsgains + t, sizeof(int64_t) * (h.t - t), cudaMemcpyDeviceToHost, c->st));
+    }
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    c->ostart = h.ostart; c->olen = h.olen; c->ocur = h.ocur;
+    c->evaluated = -1;          // not tracked on the device path
+    *status_out = h.status;
+    *t_out = h.t;
+    *batch0_out = h.batch0;
+    return IMX_OK;
+}
+
+// The whole CELF loop on one context (single-rank path): the persistent
+// cooperative kernel runs the rounds; a round it cannot hold (trace buffer
+// full, refreshed prefix larger than kMaxRank) is finished on the host.
 extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_t *gains_out,
                                int64_t *trace_len) {
     CELF_CHECK(c);
@@ -380,93 +747,27 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     cudaEventRecord(c->ev[6], c->st);
     c->trace.clear();
     c->evaluated = 0;
-    auto rec = [&](int64_t v, int64_t s, int64_t f, int64_t com, int64_t t) {
-        c->trace.push_back(v); c->trace.push_back(s); c->trace.push_back(f);
-        c->trace.push_back(com); c->trace.push_back(t);
-    };
-    unsigned long long *gain = c->scratch + 7;
-    std::vector<int32_t> ids;
-    std::vector<unsigned long long> keys;
-    std::vector<int64_t> fr;
-    std::vector<std::pair<unsigned long long, int32_t>> back;
-    int64_t batch0 = 64, pending = -1, got = 0;
-    int32_t pending_v = -1;
-    for (int32_t t = 0; t < k; ++t) {
-        if (c->olen == 0) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
-        int64_t best_f;
-        int32_t best_v;
-        int64_t kr;                   // refreshed prefix length
-        back.clear();
-        if (t == 0) {
-            // fresh_at starts at 0 == len(S): the first pop commits (selection.py:136-141)
-            ids.resize(1);
-            keys.resize(1);
-            IMX_CUDA(cudaMemcpyAsync(ids.data(), c->oid[c->ocur] + c->ostart, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
-            IMX_CUDA(cudaMemcpyAsync(keys.data(), c->okey[c->ocur] + c->ostart, sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToHost, c->st));
-            IMX_CUDA(cudaStreamSynchronize(c->st));
-            best_v = ids[0];
-            best_f = key_prio(c, keys[0]);
-            kr = 1;
-        } else {
-            const int64_t len = c->olen;
-            ids.resize(std::min(len, std::max<int64_t>(batch0, 1)) + 1);
-            keys.resize(ids.size());
-            fr.resize(ids.size());
-            int64_t lo = 0, hi = std::min(len, batch0);
-            best_f = -1;
-            best_v = -1;
-            for (;;) {
-                if ((int64_t)ids.size() < hi + 1) { ids.resize(hi + 1); keys.resize(hi + 1); fr.resize(hi + 1); }
-                IMX_TRY(celf_prefix(c, lo, hi, ids.data() + lo, keys.data() + lo, fr.data() + lo));
-                if (pending >= 0) {        // the previous commit finished before these copies
-                    IMX_CUDA(cudaMemcpy(&got, gain, sizeof got, cudaMemcpyDeviceToHost));
-                    if (got != pending) {
-                        set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
-                                  (long long)got, (long long)pending, pending_v);
-                        return IMX_EINTERNAL;
-                    }
-                    pending = -1;
-                }
-                for (int64_t i = lo; i < hi; ++i)
-                    if (best_v < 0 || key_le(fr[i], ids[i], best_f, best_v)) { best_f = fr[i]; best_v = ids[i]; }
-                if (hi >= len) break;
-                const int64_t np = key_prio(c, keys[hi]);
-                if (key_le(best_f, best_v, np, ids[hi])) break;    // nothing unevaluated can win
-                lo = hi;
-                hi = std::min(len, hi + std::max<int64_t>(batch0, hi));
-            }
-            // R_t = the prefix whose stale key <= best fresh key (sorted by stale key)
-            kr = 0;
-            while (kr < hi && key_le(key_prio(c, keys[kr]), ids[kr], best_f, best_v)) {
-                rec(ids[kr], key_prio(c, keys[kr]), fr[kr], 0, t);
-                if (ids[kr] != best_v) back.emplace_back(host_key(c, fr[kr], ids[kr]), ids[kr]);
-                ++kr;
-            }
-            batch0 = std::max<int64_t>(64, kr);
+    std::vector<int32_t> seeds(k);
+    std::vector<int64_t> gains(k);
+    int64_t batch0 = 64;
+    int32_t t = 0;
+    const char *mode = getenv("IMX_CELF");
+    const bool host_only = mode && !strcmp(mode, "host");
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->dev);
+    while (t < k) {
+        if (!host_only && coop) {
+            int32_t status = 0, t2 = t;
+            IMX_TRY(celf_device_rounds(c, t, k, batch0, &status, &t2, &batch0, seeds, gains));
+            t = t2;
+            if (status == 1 || t >= k) break;
+            if (status == 2) continue;          // trace drained, relaunch
         }
-        std::sort(back.begin(), back.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
-        std::vector<int32_t> bid(back.size());
-        std::vector<unsigned long long> bkey(back.size());
-        for (size_t i = 0; i < back.size(); ++i) { bkey[i] = back[i].first; bid[i] = back[i].second; }
-        IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
-        launch_commit(c, best_v, gain);
-        IMX_CHECK_LAUNCH();
-        count_launch(c);
-        IMX_TRY(celf_advance(c, kr, bid.data(), bkey.data(), (int64_t)back.size()));
-        pending = best_f;
-        pending_v = best_v;
-        rec(best_v, best_f, best_f, 1, t);
-        if (seeds_out) seeds_out[t] = best_v;
-        if (gains_out) gains_out[t] = best_f;
+        IMX_TRY(celf_host_round(c, t, batch0, seeds.data(), gains.data()));   // status 4 or host mode
+        ++t;
     }
-    IMX_CUDA(cudaStreamSynchronize(c->st));
-    IMX_CUDA(cudaMemcpy(&got, gain, sizeof got, cudaMemcpyDeviceToHost));
-    if (pending >= 0 && got != pending) {
-        set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
-                  (long long)got, (long long)pending, pending_v);
-        return IMX_EINTERNAL;
-    }
+    if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
+    if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);
     cudaEventRecord(c->ev[7], c->st);
     cudaEventSynchronize(c->ev[7]);
     cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);

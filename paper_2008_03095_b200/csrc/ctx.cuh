@@ -22,6 +22,17 @@
 #include "common.cuh"
 #include "graph.cuh"
 
+// device-resident state of the persistent CELF kernel (celf.cu)
+struct CelfDev {
+    // order window
+    int64_t ostart, olen;
+    int32_t ocur, t;
+    int64_t trace_len, batch0;
+    int32_t status;        // 1 done, 2 trace buffer full, 3 self-check failed, 4 round too large
+    int32_t bad_v;
+    int64_t bad_want, bad_got;
+};
+
 struct imx_ctx {
     imx_graph *g = nullptr;
     int dev = 0;
@@ -51,6 +62,15 @@ struct imx_ctx {
     int64_t stage_cap = 0;
     int64_t evaluated = 0;
     std::vector<int64_t> trace;   // 5 per record
+    // persistent CELF kernel state and buffers
+    CelfDev *cdev = nullptr;
+    unsigned long long *bkey = nullptr, *skey = nullptr;
+    int32_t *bid = nullptr, *sid = nullptr;
+    int64_t *dtrace = nullptr;
+    int64_t trace_cap = 0;
+    int32_t *dseeds = nullptr;
+    int64_t *dsgains = nullptr;
+    int32_t dseeds_cap = 0;
     // interval-enumeration sampler
     int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;
     int64_t nseg_cap = 0;

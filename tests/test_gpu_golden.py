@@ -185,3 +185,22 @@ def test_lane_sharded_device_celf_matches_reference(gpu, name, shards):
     R = randoms.num_scored
     se = 0.0 if R < 2 else float(per_sim.std(ddof=1) / np.sqrt(R))
     assert se == pytest.approx(float(z["spread_se"]), rel=1e-12, abs=1e-15)
+
+
+@pytest.mark.parametrize("mode,cap", [("host", None), ("device", None), ("device", "16")])
+@pytest.mark.parametrize("name", ["er_mid_300", "er_big_1000", "kat_path3", "er_const1_r16", "cfg_c1"])
+def test_celf_paths_match_reference_trace(gpu, name, mode, cap, monkeypatch):
+    """Host-driven rounds, the persistent cooperative kernel, and the kernel
+    forced to drain a tiny trace buffer every few rounds give the same seeds
+    and the reference's full dequeue trace."""
+    monkeypatch.setenv("IMX_CELF", mode)
+    if cap:
+        monkeypatch.setenv("IMX_CELF_TRACE_CAP", cap)
+    z = load_golden(name)
+    g = build_graph(gpu, z)
+    run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]),
+                        master_seed=int(z["master_seed"]))
+    assert run.seeds == z["seeds"].tolist()
+    assert run.selection.gains == z["seed_gains"].tolist()
+    assert np.array_equal(run.selection.trace.array, z["trace"])
+    assert run.spread_se == pytest.approx(float(z["spread_se"]), rel=1e-12, abs=1e-15)

@@ -759,9 +759,11 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
         if (!host_only && coop) {
             int32_t status = 0, t2 = t;
             IMX_TRY(celf_device_rounds(c, t, k, batch0, &status, &t2, &batch0, seeds, gains));
+            const bool progressed = t2 > t;
             t = t2;
             if (status == 1 || t >= k) break;
-            if (status == 2) continue;          // trace drained, relaunch
+            if (status == 2 && progressed) continue;   // trace drained, relaunch
+            // status 4, or one round alone overflows the trace buffer: host round
         }
         IMX_TRY(celf_host_round(c, t, batch0, seeds.data(), gains.data()));   // status 4 or host mode
         ++t;

@@ -342,9 +342,17 @@ __device__ __forceinline__ uint32_t ld_ca(const uint32_t *p) {
     return v;
 }
 
-__device__ __forceinline__ void compress_lane(uint32_t *__restrict__ L, int64_t ld, uint32_t v, uint32_t w,
-                                              uint32_t gw, int r, int j, uint32_t (&hot)[kHot][4],
-                                              unsigned long long &cnt) {
+// Walk one non-root cell (v, r) with parent p = w and parent word gw to its
+// root, store the root, count the member.  Hub-rooted members are counted in
+// the warp's shared-memory counters hc[kHot][128] (lane r - r0).
+// slot of lane r in the warp's 128 hub counters: the warp's 32 quads cover
+// lanes r0.. (wrapping around the row when the row is not a multiple of 128)
+__device__ __forceinline__ int hub_slot(int r, int r0, int64_t ld) {
+    return ld >= 128 ? (int)(((int64_t)r - r0 + ld) % ld) : r;
+}
+
+__device__ __forceinline__ void compress_cell(uint32_t *__restrict__ L, int64_t ld, uint32_t v, uint32_t w,
+                                              uint32_t gw, int r, int r0, uint32_t *hc) {
     uint32_t x = v, p = w;
     while (!is_root(gw)) {          // path splitting, min-safe
         atomicMin(cell(L, ld, x, r), gw);
@@ -353,59 +361,87 @@ __device__ __forceinline__ void compress_lane(uint32_t *__restrict__ L, int64_t 
         gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r)) : ld_relaxed(cell(L, ld, p, r));
     }
     if (p != w) L[(int64_t)v * ld + r] = p;
-    if (p < (uint32_t)kHot) {
-#pragma unroll
-        for (int h = 0; h < kHot; ++h) hot[h][j] += (p == (uint32_t)h);
-    } else {
-        atomicAdd(cell(L, ld, p, r), 1u);
-    }
-    ++cnt;
+    if (p < (uint32_t)kHot) atomicAdd(hc + p * 128 + hub_slot(r, r0, ld), 1u);
+    else atomicAdd(cell(L, ld, p, r), 1u);
 }
 
+// Streaming pass over the label rows: a warp reads 32 consecutive 16-byte
+// quads (128 lanes) of two rows per step; the non-root cells of the step are
+// compacted into a per-warp shared-memory queue and walked 32 at a time, so
+// the walks (and their dependent loads) run warp-wide instead of diverging.
+constexpr int kCQ = 32 + 256;
 __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
                                                   int64_t vstep, unsigned long long *__restrict__ nonroot) {
+    __shared__ uint32_t qv[8][kCQ], qw[8][kCQ], qr[8][kCQ];
+    __shared__ uint32_t hcs[8][kHot * 128];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *hc = hcs[warp];
+    for (int i = lane; i < kHot * 128; i += 32) hc[i] = 0;
+    __syncwarp();
     const int64_t nq = ld >> 2;
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t q = t % nq;
     const int r = (int)(q << 2);
-    uint32_t hot[kHot][4];
-#pragma unroll
-    for (int h = 0; h < kHot; ++h)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) hot[h][j] = 0;
+    const int r0 = (int)((t - lane) % nq) << 2;     // first lane of this warp's 128-lane chunk
+    const unsigned FULL = 0xffffffffu;
     unsigned long long cnt = 0;
-    // two rows per iteration and all first-level parent words loaded before
-    // any walk: up to 2 row loads + 8 parent loads in flight per thread
-    for (int64_t v = (t < vstep * nq) ? t / nq : n; v < n; v += 2 * vstep) {
+    int qn = 0;
+    const bool live = t < vstep * nq;
+    // every lane of the warp walks the same v sequence (vstep is a multiple of rows)
+    for (int64_t v = live ? t / nq : n; __any_sync(FULL, v < n); v += 2 * vstep) {
         const int64_t v2 = v + vstep;
-        const bool has2 = v2 < n;
-        const uint4 l1 = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
-        uint4 l2 = make_uint4(ROOT, ROOT, ROOT, ROOT);
-        if (has2) l2 = *(reinterpret_cast<const uint4 *>(L + v2 * ld) + q);
+        uint4 l1 = make_uint4(ROOT, ROOT, ROOT, ROOT), l2 = l1;
+        if (v < n) l1 = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
+        if (v2 < n) l2 = *(reinterpret_cast<const uint4 *>(L + v2 * ld) + q);
         const uint32_t w[8] = {l1.x, l1.y, l1.z, l1.w, l2.x, l2.y, l2.z, l2.w};
-        uint32_t gw[8];
+        unsigned m = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int rj = r + (k & 3);
-            gw[k] = ROOT;
-            if (rj < W && !is_root(w[k]))
-                gw[k] = w[k] < (uint32_t)kHot ? ld_ca(cell(L, ld, w[k], rj)) : ld_relaxed(cell(L, ld, w[k], rj));
+        for (int k = 0; k < 8; ++k)
+            if (r + (k & 3) < W && !is_root(w[k])) m |= 1u << k;
+        const int c = __popc(m);
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int rj = r + (k & 3);
-            if (rj >= W || is_root(w[k])) continue;
-            compress_lane(L, ld, (uint32_t)(k < 4 ? v : v2), w[k], gw[k], rj, k & 3, hot, cnt);
+        int pos = qn + inc - c;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            qv[warp][pos] = (uint32_t)(k < 4 ? v : v2);
+            qw[warp][pos] = w[k];
+            qr[warp][pos] = (uint32_t)(r + (k & 3));
+            ++pos;
+        }
+        qn += __shfl_sync(FULL, inc, 31);
+        cnt += c;
+        __syncwarp();
+        while (qn >= 32) {
+            qn -= 32;
+            const uint32_t cv = qv[warp][qn + lane], cw = qw[warp][qn + lane];
+            const int cr = (int)qr[warp][qn + lane];
+            __syncwarp();
+            const uint32_t gw = cw < (uint32_t)kHot ? ld_ca(cell(L, ld, cw, cr)) : ld_relaxed(cell(L, ld, cw, cr));
+            compress_cell(L, ld, cv, cw, gw, cr, r0, hc);
         }
     }
-#pragma unroll
-    for (int h = 0; h < kHot; ++h)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (hot[h][j]) atomicAdd(cell(L, ld, h, r + j), hot[h][j]);
+    __syncwarp();
+    if (lane < qn) {
+        const uint32_t cv = qv[warp][lane], cw = qw[warp][lane];
+        const int cr = (int)qr[warp][lane];
+        const uint32_t gw = cw < (uint32_t)kHot ? ld_ca(cell(L, ld, cw, cr)) : ld_relaxed(cell(L, ld, cw, cr));
+        compress_cell(L, ld, cv, cw, gw, cr, r0, hc);
+    }
+    __syncwarp();
+    for (int i = lane; i < kHot * 128; i += 32) {
+        if (!hc[i]) continue;
+        const int rr = ld >= 128 ? (int)((r0 + (i & 127)) % ld) : (i & 127);
+        atomicAdd(cell(L, ld, i >> 7, rr), hc[i]);
+    }
     if (nonroot) {
-        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nonroot, cnt);
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+        if (lane == 0 && cnt) atomicAdd(nonroot, cnt);
     }
 }
 

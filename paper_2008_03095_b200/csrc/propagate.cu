@@ -179,7 +179,7 @@ __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
 // a forward walk), so consecutive threads read consecutive edges of the same
 // hash interval (coalesced) and every thread runs one union per pair.
 constexpr int kEnumChunk = 128;
-template <bool UNI>
+template <bool UNI, bool SKIP>
 __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ off, const int64_t *__restrict__ seg_a,
                                                    int64_t nseg, int segs_per_lane,
                                                    const int2 *__restrict__ E, const int32_t *__restrict__ EH,
@@ -209,6 +209,9 @@ __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ o
             const int r = (int)(s / segs_per_lane);
             if (!UNI && !((X[r] ^ EH[e]) < ET[e])) continue;
             const int2 uv = E[e];
+            // after the pull forest pass, a live edge that is its upper
+            // endpoint's first live smaller neighbour is already a tree edge
+            if (SKIP && ld_relaxed(cell(L, ld, (uint32_t)uv.y, r)) == (uint32_t)uv.x) continue;
             nh += unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r);
         }
     }
@@ -529,7 +532,7 @@ static int run_hook_dense(imx_ctx *c, unsigned long long *hooks) {
     return IMX_OK;
 }
 
-static int run_hook_enum(imx_ctx *c, unsigned long long *hooks) {
+static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest = false) {
     imx_graph *g = c->g;
     const int64_t nseg = (int64_t)c->W * g->nb * 31;
     if (nseg + 1 > c->nseg_cap) {
@@ -553,12 +556,10 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks) {
     size_t tb = c->scan_tmp_bytes;
     IMX_CUDA(cub::DeviceScan::ExclusiveSum(c->scan_tmp, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
     const int blocks = 148 * 8;
-    if (g->uniform)
-        k_hook_enum<true><<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH,
-                                                     g->ET, c->X, c->ld, c->L, hooks);
-    else
-        k_hook_enum<false><<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH,
-                                                      g->ET, c->X, c->ld, c->L, hooks);
+    auto kern = g->uniform ? (skip_forest ? k_hook_enum<true, true> : k_hook_enum<true, false>)
+                           : (skip_forest ? k_hook_enum<false, true> : k_hook_enum<false, false>);
+    kern<<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH, g->ET, c->X, c->ld,
+                                    c->L, hooks);
     IMX_CHECK_LAUNCH();
     count_launch(c, 3);
     return IMX_OK;
@@ -586,12 +587,13 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
 // dense membership scans (ALU only) plus random accesses for the non-forest
 // live edges only, but a warp owns a whole row prefix, so a very long prefix
 // (a high-degree vertex with many smaller neighbours) serialises.
-enum { HOOK_ENUM = 0, HOOK_PULL = 1, HOOK_DENSE = 2 };
+enum { HOOK_ENUM = 0, HOOK_PULL = 1, HOOK_DENSE = 2, HOOK_HYBRID = 3 };
 static int hook_mode(const imx_graph *g) {
     const char *m = getenv("IMX_HOOK");
     if (m && !strcmp(m, "dense")) return HOOK_DENSE;
     if (m && !strcmp(m, "enum")) return HOOK_ENUM;
     if (m && !strcmp(m, "pull")) return HOOK_PULL;
+    if (m && !strcmp(m, "hybrid")) return HOOK_HYBRID;
     const char *t = getenv("IMX_PULL_MIN_P");
     const double pmin = t ? atof(t) : 0.02;
     const double balanced_prefix = 8.0 * (double)g->me / (148.0 * 64.0);
@@ -603,10 +605,11 @@ static int hook_mode(const imx_graph *g) {
 static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_init, cudaEvent_t e_hook) {
     imx_graph *g = c->g;
     const int mode = g->me ? hook_mode(g) : HOOK_ENUM;
-    if (mode == HOOK_PULL) {
+    if (mode == HOOK_PULL || mode == HOOK_HYBRID) {
         IMX_TRY(run_pull(c, 1, nullptr));
         if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));
-        IMX_TRY(run_pull(c, 2, hooks));
+        if (mode == HOOK_PULL) IMX_TRY(run_pull(c, 2, hooks));
+        else IMX_TRY(run_hook_enum(c, hooks, true));
     } else {
         IMX_TRY(run_init(c));
         if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));

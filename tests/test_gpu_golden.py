@@ -112,7 +112,7 @@ def test_select_seeds_on_host_arrays_matches_oracle(gpu, orc, name):
     assert gpu.recompute_sigma(labels, res.state) == res.sigma
 
 
-@pytest.mark.parametrize("mode", ["enum", "pull", "dense"])
+@pytest.mark.parametrize("mode", ["enum", "pull", "dense", "hybrid"])
 @pytest.mark.parametrize("name", ["er_big_1000", "er_uniform_r24", "er_wc_r40", "er_const1_r16",
                                   "er_const0_r16", "er_pad20", "kat_dead_middle", "cfg_c1"])
 def test_every_sampler_strategy_reaches_the_reference_fixpoint(gpu, name, mode, monkeypatch):

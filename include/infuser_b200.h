@@ -64,6 +64,16 @@ int  imx_graph_from_edges(int32_t device, int64_t n, const int64_t *edges,
 int  imx_graph_from_csr(int32_t device, int64_t n, int64_t m2,
                         const int64_t *xadj, const int32_t *adj,
                         const double *weights, imx_graph **out);
+/* Seeded synthetic graph generated and built on the device (SURVEY 8(f)
+ * rank 1; the reference's generate_er / generate_rmat, graph.py:444-491, are
+ * host numpy).  kind 0 Erdos-Renyi, 1 R-MAT (params = probs[4], n = 2^scale),
+ * 2 Chung-Lu (cdf = n normalised cumulative expected degrees).  Counter-based
+ * SplitMix64 streams (gen.cu); m > 0: first m distinct non-loop pairs in draw
+ * order (draws = initial candidate count, 0 = auto), m == 0: every distinct
+ * non-loop pair among `draws` candidates.  Unit weights.                    */
+int  imx_graph_generate(int32_t device, int32_t kind, int64_t n, int64_t m,
+                        int64_t draws, uint64_t seed, const double *params,
+                        const double *cdf, imx_graph **out);
 void imx_graph_destroy(imx_graph *g);
 int  imx_graph_dims(const imx_graph *g, int64_t *n, int64_t *m2);
 int  imx_graph_get_csr(imx_graph *g, int64_t *xadj, int32_t *adj, double *weights);

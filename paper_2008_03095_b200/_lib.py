@@ -57,6 +57,8 @@ _SIGNATURES = {
     "imx_launch_count": (c_i64, []),
     "imx_graph_from_edges": (c_i32, [c_i32, c_i64, c_void_p, c_i64, c_void_p, c_f64, P(c_void_p)]),
     "imx_graph_from_csr": (c_i32, [c_i32, c_i64, c_i64, c_void_p, c_void_p, c_void_p, P(c_void_p)]),
+    "imx_graph_generate": (c_i32, [c_i32, c_i32, c_i64, c_i64, c_i64, ctypes.c_uint64, c_void_p, c_void_p,
+                                   P(c_void_p)]),
     "imx_graph_destroy": (None, [c_void_p]),
     "imx_graph_dims": (c_i32, [c_void_p, P(c_i64), P(c_i64)]),
     "imx_graph_get_csr": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -43,26 +43,40 @@ CONFIGS = {
 }
 
 
-def edges(name: str) -> np.ndarray:
+_RMAT = (0.57, 0.19, 0.19, 0.05)
+
+
+def _spec(name: str):
+    """(kind, n, m, draws, probs, cdf) of a config's generator."""
     c = CONFIGS[name]
     if name == "c1":
-        return gen.chung_lu_edges(c.n, 31_000, 2.5, c.seed)
+        return gen.CHUNG_LU, c.n, 31_000, 0, None, gen.chung_lu_cdf(c.n, 2.5)
     if name in ("c2", "c2p1"):
-        return gen.chung_lu_edges(c.n, 174_000, 2.2, c.seed)
+        return gen.CHUNG_LU, c.n, 174_000, 0, None, gen.chung_lu_cdf(c.n, 2.2)
     if name == "c3":
-        return gen.rmat_edges(18, c.seed, m=1_230_000)
+        return gen.RMAT, c.n, 1_230_000, 0, _RMAT, None
     if name == "c4":
-        return gen.rmat_edges(22, c.seed, edge_factor=16)
+        return gen.RMAT, c.n, 0, 16 * c.n, _RMAT, None
     if name == "c5":
-        return gen.er_edges(c.n, 5_000_000, c.seed)
+        return gen.ER, c.n, 5_000_000, 0, None, None
     raise KeyError(name)
 
 
+def edges(name: str) -> np.ndarray:
+    """Host (numpy) edge list -- identical to the device generator's."""
+    kind, n, m, draws, probs, cdf = _spec(name)
+    return gen.edges(kind, n, m, CONFIGS[name].seed, draws, probs, cdf)
+
+
 def build(name: str, edge_list: np.ndarray | None = None):
-    """Device-built Graph with the config's weights applied."""
+    """Graph with the config's weights applied; generated on the device
+    unless an edge list is given."""
     from .graph import Graph
     from .weights import apply_weights, parse_weight_scheme
     c = CONFIGS[name]
-    e = edges(name) if edge_list is None else edge_list
-    g = Graph.from_edges(c.n, e)
+    if edge_list is None:
+        kind, n, m, draws, probs, cdf = _spec(name)
+        g = gen.device_graph(kind, n, m, c.seed, draws, probs, cdf)
+    else:
+        g = Graph.from_edges(c.n, edge_list)
     return apply_weights(g, parse_weight_scheme(c.weights), rng_seed=c.seed)

@@ -686,10 +686,14 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     const int enc = c->C ? 0 : 1;
     void *fn = enc ? (void *)k_celf_rounds<true> : (void *)k_celf_rounds<false>;
     if (!grid_cache[enc]) {
+        // fewer CTAs make the grid barriers cheaper; the evaluation batches
+        // still have one CTA per candidate in flight per SM slot
         int per_sm = 0, sms = 0;
         IMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
         IMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
-        grid_cache[enc] = std::max(1, std::min(per_sm, 4)) * sms;
+        int want = 4;
+        if (const char *b = getenv("IMX_CELF_BPSM")) want = std::max(1, atoi(b));
+        grid_cache[enc] = std::max(1, std::min(per_sm, want)) * sms;
     }
     int32_t kk = k;
     int vb = c->vb;

@@ -536,41 +536,26 @@ extern "C" int imx_device_count(void) {
     return ok;
 }
 
-extern "C" int imx_graph_from_edges(int32_t device, int64_t n, const int64_t *edges, int64_t k,
-                                    const double *w_edge, double w_scalar, imx_graph **out) {
-    if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
-    *out = nullptr;
-    if (n < 0 || n >= (int64_t(1) << 31)) {
-        set_error("vertex count %lld outside [0, 2^31)", (long long)n);
-        return IMX_ECONSTRAINT;
-    }
-    if (k < 0 || k >= (int64_t(1) << 31)) { set_error("edge count %lld invalid", (long long)k); return IMX_EINVAL; }
-    if (k > 0 && !edges) { set_error("edges is NULL"); return IMX_EINVAL; }
-    imx_graph *g;
-    IMX_TRY(graph_new(device, n, 2 * k, &g));
+namespace imx {
+
+// CSR from k undirected edges already on the device (dedges: 2k int64,
+// pairs (u, v)); dw: per-edge weights on the device or NULL (w_scalar).
+int graph_build_from_device_edges(imx_graph *g, const int64_t *dedges, int64_t k, const double *dw,
+                                  double w_scalar) {
     cudaStream_t st = g->stream;
-    const int64_t m2 = 2 * k;
+    const int64_t n = g->n, m2 = 2 * k;
     int rc = IMX_OK;
-    auto fail = [&](int code) { graph_free(g); return code; };
     if (dalloc(g, &g->xadj, n + 1) || dalloc(g, &g->adj, m2) || dalloc(g, &g->w, m2) || dalloc(g, &g->src, m2))
-        return fail(IMX_ENOMEM);
+        return IMX_ENOMEM;
     if (k > 0) {
         int nb = 1;
         while ((int64_t(1) << nb) < n) ++nb;
-        int64_t *dedges = nullptr;
-        double *dw = nullptr;
         uint64_t *keys = nullptr, *keys2 = nullptr;
         uint32_t *vals = nullptr, *vals2 = nullptr;
         unsigned *dflags = nullptr;
         void *tmp = nullptr;
         size_t tmp_bytes = 0;
 #define GF(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { rc = cuda_fail(_e, #call, __FILE__, __LINE__); goto cleanup; } } while (0)
-        GF(cudaMallocAsync((void **)&dedges, sizeof(int64_t) * 2 * k, st));
-        GF(cudaMemcpyAsync(dedges, edges, sizeof(int64_t) * 2 * k, cudaMemcpyHostToDevice, st));
-        if (w_edge) {
-            GF(cudaMallocAsync((void **)&dw, sizeof(double) * k, st));
-            GF(cudaMemcpyAsync(dw, w_edge, sizeof(double) * k, cudaMemcpyHostToDevice, st));
-        }
         GF(cudaMallocAsync((void **)&keys, sizeof(uint64_t) * m2, st));
         GF(cudaMallocAsync((void **)&keys2, sizeof(uint64_t) * m2, st));
         GF(cudaMallocAsync((void **)&vals, sizeof(uint32_t) * m2, st));
@@ -597,18 +582,52 @@ extern "C" int imx_graph_from_edges(int32_t device, int64_t n, const int64_t *ed
             else if (flags & 4u) { set_error("duplicate undirected edges"); rc = IMX_EINVAL; }
         }
     cleanup:
-        cudaFreeAsync(dedges, st); if (dw) cudaFreeAsync(dw, st);
         if (keys) cudaFreeAsync(keys, st); if (keys2) cudaFreeAsync(keys2, st);
         if (vals) cudaFreeAsync(vals, st); if (vals2) cudaFreeAsync(vals2, st);
         if (dflags) cudaFreeAsync(dflags, st); if (tmp) cudaFreeAsync(tmp, st);
 #undef GF
-        if (rc != IMX_OK) return fail(rc);
+        if (rc != IMX_OK) return rc;
     } else {
-        if (cudaMemsetAsync(g->xadj, 0, sizeof(int64_t) * (n + 1), st) != cudaSuccess) return fail(IMX_ECUDA);
+        IMX_CUDA(cudaMemsetAsync(g->xadj, 0, sizeof(int64_t) * (n + 1), st));
     }
-    rc = graph_finish(g);
-    if (rc == IMX_OK) rc = graph_refresh_thresholds(g);
-    if (rc != IMX_OK) return fail(rc);
+    IMX_TRY(graph_finish(g));
+    return graph_refresh_thresholds(g);
+}
+
+int graph_create(int32_t device, int64_t n, int64_t m2, imx_graph **out) { return graph_new(device, n, m2, out); }
+
+}  // namespace imx
+
+extern "C" int imx_graph_from_edges(int32_t device, int64_t n, const int64_t *edges, int64_t k,
+                                    const double *w_edge, double w_scalar, imx_graph **out) {
+    if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
+    *out = nullptr;
+    if (n < 0 || n >= (int64_t(1) << 31)) {
+        set_error("vertex count %lld outside [0, 2^31)", (long long)n);
+        return IMX_ECONSTRAINT;
+    }
+    if (k < 0 || k >= (int64_t(1) << 31)) { set_error("edge count %lld invalid", (long long)k); return IMX_EINVAL; }
+    if (k > 0 && !edges) { set_error("edges is NULL"); return IMX_EINVAL; }
+    imx_graph *g;
+    IMX_TRY(graph_new(device, n, 2 * k, &g));
+    cudaStream_t st = g->stream;
+    int64_t *dedges = nullptr;
+    double *dw = nullptr;
+    int rc = IMX_OK;
+    cudaError_t e = cudaSuccess;
+    if (k > 0) {
+        if ((e = cudaMallocAsync((void **)&dedges, sizeof(int64_t) * 2 * k, st)) == cudaSuccess)
+            e = cudaMemcpyAsync(dedges, edges, sizeof(int64_t) * 2 * k, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && w_edge) {
+            if ((e = cudaMallocAsync((void **)&dw, sizeof(double) * k, st)) == cudaSuccess)
+                e = cudaMemcpyAsync(dw, w_edge, sizeof(double) * k, cudaMemcpyHostToDevice, st);
+        }
+    }
+    rc = e == cudaSuccess ? graph_build_from_device_edges(g, dedges, k, dw, w_scalar)
+                          : cuda_fail(e, "upload edges", __FILE__, __LINE__);
+    if (dedges) cudaFreeAsync(dedges, st);
+    if (dw) cudaFreeAsync(dw, st);
+    if (rc != IMX_OK) { graph_free(g); return rc; }
     *out = g;
     return IMX_OK;
 }

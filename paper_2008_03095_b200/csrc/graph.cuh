@@ -36,4 +36,7 @@ struct imx_graph {
 namespace imx {
 int select_device(int32_t device);
 void graph_free(imx_graph *g);
+int graph_create(int32_t device, int64_t n, int64_t m2, imx_graph **out);
+int graph_build_from_device_edges(imx_graph *g, const int64_t *dedges, int64_t k, const double *dw,
+                                  double w_scalar);
 }

@@ -204,3 +204,32 @@ def test_celf_paths_match_reference_trace(gpu, name, mode, cap, monkeypatch):
     assert run.selection.gains == z["seed_gains"].tolist()
     assert np.array_equal(run.selection.trace.array, z["trace"])
     assert run.spread_se == pytest.approx(float(z["spread_se"]), rel=1e-12, abs=1e-15)
+
+
+@pytest.mark.parametrize("kind,n,m,draws,extra", [
+    (0, 1000, 3000, 0, {}),
+    (0, 5000, 0, 20000, {}),
+    (1, 1 << 12, 20000, 0, {"probs": (0.57, 0.19, 0.19, 0.05)}),
+    (1, 1 << 11, 0, 16 << 11, {"probs": (0.45, 0.22, 0.22, 0.11)}),
+    (2, 3000, 8000, 0, {"gamma": 2.5}),
+])
+def test_device_generator_matches_host_restatement(gpu, kind, n, m, draws, extra):
+    from paper_2008_03095_b200 import generators as gen
+    cdf = gen.chung_lu_cdf(n, extra["gamma"]) if "gamma" in extra else None
+    probs = extra.get("probs")
+    g = gen.device_graph(kind, n, m, 11, draws, probs, cdf)
+    e = gen.edges(kind, n, m, 11, draws, probs, cdf)
+    ref = gpu.Graph.from_edges(n, e)
+    assert np.array_equal(g.xadj, ref.xadj) and np.array_equal(g.adj, ref.adj)
+    if m:
+        assert g.num_undirected_edges == m
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_config_graphs_are_the_golden_graphs(gpu, cfg):
+    from paper_2008_03095_b200 import configs
+    z = load_golden(f"cfg_{cfg}")
+    g = configs.build(cfg)
+    check_array(z, "xadj", g.xadj)
+    check_array(z, "adj", g.adj)
+    check_array(z, "weights", g.weights)

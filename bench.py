@@ -245,8 +245,7 @@ def run_ours(args, world, rank, local):
     imx.set_device(local)
     c = configs.CONFIGS[args.config]
     t0 = time.perf_counter()
-    edges = configs.edges(args.config)
-    g = configs.build(args.config, edges)
+    g = configs.build(args.config)          # generated + CSR-built on the device
     t_build = time.perf_counter() - t0
     n, m2, R, K = g.n, g.m, c.R, c.K
     X = imx.SimulationRandoms(R, 0).values

@@ -74,7 +74,7 @@ struct imx_ctx {
     // non-root work list (propagate.cu) and roots of non-trivial components
     unsigned long long *wl_ent = nullptr, *rt_ent = nullptr, *wl_cnt = nullptr;  // wl_cnt[0..1]
     int64_t wl_cap = 0, wl_total = 0;
-    bool wl_enabled = false, wl_valid = false, wl_decided = false;
+    bool wl_enabled = false, wl_valid = false;
     // interval-enumeration sampler
     int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;
     int64_t nseg_cap = 0;

@@ -46,9 +46,7 @@ __global__ void __launch_bounds__(256) k_gains_caller(const uint32_t *__restrict
 // read-only path (L is not written during memoization, so hub rows stay in
 // L1/texture cache instead of hammering one L2 line).
 __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ L, int64_t n, int64_t ld,
-                                                   int32_t ns, int64_t *__restrict__ gains,
-                                                   const unsigned long long *__restrict__ wl_ok) {
-    if (wl_ok && *wl_ok) return;                    // gains come from the work lists
+                                                   int32_t ns, int64_t *__restrict__ gains) {
     const int lane = threadIdx.x & 31;
     const int nqs = (ns + 3) >> 2;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -76,9 +74,7 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
 // v's cells in non-trivial components of scored lanes, of (component size - 1)
 // = the root cell's member count -- non-root cells from the non-root list,
 // root cells from the root list -- so only non-trivial cells are visited.
-__global__ void k_gains_fill(int64_t *__restrict__ gains, int64_t n, int64_t ns,
-                             const unsigned long long *__restrict__ wl_ok) {
-    if (!*wl_ok) return;
+__global__ void k_gains_fill(int64_t *__restrict__ gains, int64_t n, int64_t ns) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x)
         gains[v] = ns;
@@ -88,7 +84,6 @@ __global__ void __launch_bounds__(256) k_gains_wl(const uint32_t *__restrict__ L
                                                   const unsigned long long *__restrict__ roots,
                                                   const unsigned long long *__restrict__ cnts, int64_t cap,
                                                   unsigned long long *__restrict__ gains) {
-    if (!cnts[2]) return;                           // the work list overflowed: full-scan gains ran
     const int64_t nnr = (int64_t)(cnts[0] < (unsigned long long)cap ? cnts[0] : (unsigned long long)cap);
     const int64_t nr = (int64_t)(cnts[1] < (unsigned long long)cap ? cnts[1] : (unsigned long long)cap);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnr + nr;
@@ -184,16 +179,14 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
     if (n) {
         if (c->C) {
             k_gains_caller<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->ns, c->gains);
+        } else if (c->wl_valid) {
+            k_gains_fill<<<grid_for(n), 256, 0, c->st>>>(c->gains, n, c->ns);
+            k_gains_wl<<<grid_for(2 * c->wl_total + 1), 256, 0, c->st>>>(
+                c->L, c->ld, c->ns, c->wl_ent, c->rt_ent, c->wl_cnt, c->wl_cap,
+                reinterpret_cast<unsigned long long *>(c->gains));
+            count_launch(c);
         } else {
-            const unsigned long long *ok = c->wl_valid ? c->wl_cnt + 2 : nullptr;
-            if (ok) {
-                k_gains_fill<<<grid_for(n), 256, 0, c->st>>>(c->gains, n, c->ns, ok);
-                const int64_t est = std::min<int64_t>(c->wl_cap, (int64_t)(c->g->thr_mean * c->g->me * c->W) + 1);
-                k_gains_wl<<<grid_for(2 * est), 256, 0, c->st>>>(c->L, c->ld, c->ns, c->wl_ent, c->rt_ent, c->wl_cnt,
-                                                                 c->wl_cap, reinterpret_cast<unsigned long long *>(c->gains));
-                count_launch(c, 2);
-            }
-            k_gains_enc<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, n, c->ld, c->ns, c->gains, ok);
+            k_gains_enc<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, n, c->ld, c->ns, c->gains);
         }
         IMX_CHECK_LAUNCH();
         count_launch(c);

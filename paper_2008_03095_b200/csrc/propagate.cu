@@ -398,9 +398,7 @@ __device__ __forceinline__ void compress_cell(uint32_t *__restrict__ L, int64_t 
 // the walks (and their dependent loads) run warp-wide instead of diverging.
 constexpr int kCQ = 32 + 256;
 __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
-                                                  int64_t vstep, unsigned long long *__restrict__ nonroot,
-                                                  const unsigned long long *__restrict__ wl_ok) {
-    if (wl_ok && *wl_ok) return;                    // compressed from the work list already
+                                                  int64_t vstep, unsigned long long *__restrict__ nonroot) {
     __shared__ uint32_t qv[8][kCQ], qw[8][kCQ], qr[8][kCQ];
     __shared__ uint32_t hcs[8][kHot * 128];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -484,14 +482,8 @@ constexpr int kHubLanesWL = 2048;
 __global__ void __launch_bounds__(256) k_compress_wl(uint32_t *__restrict__ L, int64_t ld,
                                                      const unsigned long long *__restrict__ ent,
                                                      const unsigned long long *__restrict__ cntp, int64_t cap,
-                                                     Worklist roots, unsigned long long *__restrict__ ok,
-                                                     unsigned long long *__restrict__ nonroot) {
+                                                     Worklist roots) {
     __shared__ uint32_t hub[kHot][kHubLanesWL];
-    if (*cntp > (unsigned long long)cap) return;     // overflow: the full scan runs instead
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        *ok = 1;
-        if (nonroot) *nonroot = *cntp;
-    }
     for (int i = threadIdx.x; i < kHot * kHubLanesWL; i += blockDim.x) (&hub[0][0])[i] = 0;
     __syncthreads();
     const int64_t total = (int64_t)(*cntp < (unsigned long long)cap ? *cntp : (unsigned long long)cap);
@@ -610,28 +602,29 @@ static Worklist wl_of(imx_ctx *c) {
 }
 
 // Size the non-root work list from the expected number of live (edge, lane)
-// pairs (each union or forest link makes at most one non-root) once per
-// context; disabled when it would not fit comfortably next to the label
-// matrix.  Overflow is detected on the device (k_compress_wl), and the
-// full-scan kernels then take over without a host round trip.
+// pairs (each union or forest link makes at most one non-root); disabled when
+// it would not fit comfortably next to the label matrix.
 static int prepare_worklists(imx_ctx *c) {
     imx_graph *g = c->g;
-    if (!c->wl_decided) {
-        c->wl_decided = true;
-        const char *m = getenv("IMX_WORKLIST");
-        const double live = g->thr_mean * (double)g->me * (double)c->W;
-        const int64_t cap = (int64_t)std::min<double>((double)g->n * (double)c->W, 1.25 * live + 65536.0);
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
-        c->wl_enabled = !(m && !strcmp(m, "off")) && g->me > 0 && 16.0 * (double)cap < 0.25 * (double)free_b;
-        if (c->wl_enabled) {
-            IMX_CUDA(pool_alloc((void **)&c->wl_ent, sizeof(unsigned long long) * cap, c->st));
-            IMX_CUDA(pool_alloc((void **)&c->rt_ent, sizeof(unsigned long long) * cap, c->st));
-            IMX_CUDA(pool_alloc((void **)&c->wl_cnt, sizeof(unsigned long long) * 4, c->st));
-            c->wl_cap = cap;
-        }
+    const char *m = getenv("IMX_WORKLIST");
+    const double live = g->thr_mean * (double)g->me * (double)c->W;
+    int64_t cap = (int64_t)std::min<double>((double)g->n * (double)c->W, 1.25 * live + 65536.0);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const bool fits = 2.0 * 8.0 * (double)cap < 0.25 * (double)free_b + 2.0 * 8.0 * (double)c->wl_cap;
+    c->wl_enabled = !(m && !strcmp(m, "off")) && g->me > 0 && fits;
+    if (!c->wl_enabled) return IMX_OK;
+    if (cap > c->wl_cap) {
+        if (c->wl_ent) cudaFreeAsync(c->wl_ent, c->st);
+        if (c->rt_ent) cudaFreeAsync(c->rt_ent, c->st);
+        c->wl_ent = c->rt_ent = nullptr;
+        c->wl_cap = 0;
+        IMX_CUDA(pool_alloc((void **)&c->wl_ent, sizeof(unsigned long long) * cap, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->rt_ent, sizeof(unsigned long long) * cap, c->st));
+        c->wl_cap = cap;
     }
-    if (c->wl_enabled) IMX_CUDA(cudaMemsetAsync(c->wl_cnt, 0, sizeof(unsigned long long) * 4, c->st));
+    if (!c->wl_cnt) IMX_CUDA(pool_alloc((void **)&c->wl_cnt, sizeof(unsigned long long) * 2, c->st));
+    IMX_CUDA(cudaMemsetAsync(c->wl_cnt, 0, sizeof(unsigned long long) * 2, c->st));
     return IMX_OK;
 }
 
@@ -742,22 +735,26 @@ static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_in
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
-    const unsigned long long *wl_ok = nullptr;
     c->wl_valid = false;
     if (c->wl_enabled) {
-        // wl_cnt: [0] non-roots, [1] roots, [2] 1 when the list held every non-root
-        Worklist roots;
-        roots.cnt = c->wl_cnt + 1;
-        roots.ent = c->rt_ent;
-        roots.cap = c->wl_cap;
-        const int64_t est = std::min<int64_t>(c->wl_cap, (int64_t)(c->g->thr_mean * c->g->me * c->W) + 1);
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(est, 256), 148 * 8));
-        k_compress_wl<<<blocks, 256, 0, c->st>>>(c->L, c->ld, c->wl_ent, c->wl_cnt, c->wl_cap, roots,
-                                                  c->wl_cnt + 2, nonroot);
-        IMX_CHECK_LAUNCH();
-        count_launch(c);
-        wl_ok = c->wl_cnt + 2;
-        c->wl_valid = true;       // "maybe": the device flag decides
+        unsigned long long cnt = 0;
+        IMX_CUDA(cudaMemcpyAsync(&cnt, c->wl_cnt, sizeof cnt, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        if ((int64_t)cnt <= c->wl_cap) {
+            Worklist roots;
+            roots.cnt = c->wl_cnt + 1;
+            roots.ent = c->rt_ent;
+            roots.cap = c->wl_cap;
+            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)cnt, 256), 148 * 8));
+            k_compress_wl<<<blocks, 256, 0, c->st>>>(c->L, c->ld, c->wl_ent, c->wl_cnt, c->wl_cap, roots);
+            IMX_CHECK_LAUNCH();
+            count_launch(c);
+            if (nonroot) IMX_CUDA(cudaMemcpyAsync(nonroot, c->wl_cnt, sizeof(unsigned long long),
+                                                  cudaMemcpyDeviceToDevice, c->st));
+            c->wl_valid = true;
+            c->wl_total = (int64_t)cnt;
+            return IMX_OK;
+        }
     }
     // grid stride = a whole number of rows, so every thread keeps its quad
     const int64_t nq = c->ld >> 2;
@@ -765,8 +762,10 @@ static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t rows = std::max<int64_t>(1, want / nq);
     const int64_t threads = rows * nq;
     const int blocks = (int)ceil_div(threads, 256);
+    // threads beyond rows*nq would break the fixed-quad mapping: size the
+    // stride from the launched thread count, rounded down to whole rows
     const int64_t vstep = ((int64_t)blocks * 256) / nq;
-    k_compress<<<blocks, 256, 0, c->st>>>(c->L, n, c->ld, c->W, vstep, nonroot, wl_ok);
+    k_compress<<<blocks, 256, 0, c->st>>>(c->L, n, c->ld, c->W, vstep, nonroot);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;

@@ -71,10 +71,6 @@ struct imx_ctx {
     int32_t *dseeds = nullptr;
     int64_t *dsgains = nullptr;
     int32_t dseeds_cap = 0;
-    // non-root work list (propagate.cu) and roots of non-trivial components
-    unsigned long long *wl_ent = nullptr, *rt_ent = nullptr, *wl_cnt = nullptr;  // wl_cnt[0..1]
-    int64_t wl_cap = 0, wl_total = 0;
-    bool wl_enabled = false, wl_valid = false;
     // interval-enumeration sampler
     int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;
     int64_t nseg_cap = 0;

@@ -70,35 +70,6 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
     }
 }
 
-// Gains from the work lists (propagate.cu): gains[v] = ns + the sum, over
-// v's cells in non-trivial components of scored lanes, of (component size - 1)
-// = the root cell's member count -- non-root cells from the non-root list,
-// root cells from the root list -- so only non-trivial cells are visited.
-__global__ void k_gains_fill(int64_t *__restrict__ gains, int64_t n, int64_t ns) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x)
-        gains[v] = ns;
-}
-__global__ void __launch_bounds__(256) k_gains_wl(const uint32_t *__restrict__ L, int64_t ld, int32_t ns,
-                                                  const unsigned long long *__restrict__ nonroots,
-                                                  const unsigned long long *__restrict__ roots,
-                                                  const unsigned long long *__restrict__ cnts, int64_t cap,
-                                                  unsigned long long *__restrict__ gains) {
-    const int64_t nnr = (int64_t)(cnts[0] < (unsigned long long)cap ? cnts[0] : (unsigned long long)cap);
-    const int64_t nr = (int64_t)(cnts[1] < (unsigned long long)cap ? cnts[1] : (unsigned long long)cap);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnr + nr;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const bool is_root_entry = i >= nnr;
-        const unsigned long long e = is_root_entry ? roots[i - nnr] : nonroots[i];
-        const uint32_t v = (uint32_t)(e >> 32);
-        const int r = (int)(e & 0xffffffffu);
-        if (r >= ns) continue;
-        const uint32_t root = is_root_entry ? v : __ldg(L + (int64_t)v * ld + r);
-        const uint32_t cntw = __ldg(L + (int64_t)root * ld + r);
-        atomicAdd(gains + v, (unsigned long long)(cntw & COUNT));
-    }
-}
-
 // decoded labels / sizes of rows [v0, v0+cnt), lanes [r0, r1) -> dense out
 template <bool ENC>
 __global__ void k_labels_window(const uint32_t *__restrict__ L, int64_t v0, int64_t cnt, int64_t ld,
@@ -179,12 +150,6 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
     if (n) {
         if (c->C) {
             k_gains_caller<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->ns, c->gains);
-        } else if (c->wl_valid) {
-            k_gains_fill<<<grid_for(n), 256, 0, c->st>>>(c->gains, n, c->ns);
-            k_gains_wl<<<grid_for(2 * c->wl_total + 1), 256, 0, c->st>>>(
-                c->L, c->ld, c->ns, c->wl_ent, c->rt_ent, c->wl_cnt, c->wl_cap,
-                reinterpret_cast<unsigned long long *>(c->gains));
-            count_launch(c);
         } else {
             k_gains_enc<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, n, c->ld, c->ns, c->gains);
         }
@@ -230,7 +195,6 @@ extern "C" int imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t 
     c->labels_ready = true;
     c->memo_ready = false;
     c->celf_ready = false;
-    c->wl_valid = false;
     return IMX_OK;
 }
 

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict
                                                           const int32_t *__restrict__ ET, int32_t tu, int64_t me,
                                                           const int32_t *__restrict__ X, int32_t W, int64_t ld,
                                                           uint32_t *__restrict__ L,
-                                                          unsigned long long *__restrict__ hooks, Worklist wl) {
+                                                          unsigned long long *__restrict__ hooks) {
     extern __shared__ int4 smem4[];
     int32_t *sX = reinterpret_cast<int32_t *>(smem4);
     for (int i = threadIdx.x; i < ld; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
@@ -114,21 +114,13 @@ __global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict
                     const uint32_t a = qlo[qn + lane], bb = qhi[qn + lane];
                     const int r = (int)qr[qn + lane];
                     __syncwarp();
-                    const uint32_t hk = unite(L, ld, a, bb, r);
-                    nh += hk != NO_HOOK;
-                    wl_push(wl, FULL, hk != NO_HOOK, wl_key(hk, r));
+                    nh += unite(L, ld, a, bb, r);
                 }
             }
         }
     }
     __syncwarp();
-    {
-        uint32_t hk = NO_HOOK;
-        int rr = 0;
-        if (lane < qn) { rr = (int)qr[lane]; hk = unite(L, ld, qlo[lane], qhi[lane], rr); }
-        nh += hk != NO_HOOK;
-        wl_push(wl, FULL, hk != NO_HOOK, wl_key(hk, rr));
-    }
+    if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
     if (hooks) {
         for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
         if (lane == 0 && nh) atomicAdd(hooks, nh);
@@ -193,7 +185,7 @@ __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ o
                                                    const int2 *__restrict__ E, const int32_t *__restrict__ EH,
                                                    const int32_t *__restrict__ ET, const int32_t *__restrict__ X,
                                                    int64_t ld, uint32_t *__restrict__ L,
-                                                   unsigned long long *__restrict__ hooks, Worklist wl) {
+                                                   unsigned long long *__restrict__ hooks) {
     const int64_t total = off[nseg];
     const int lane = threadIdx.x & 31;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -211,23 +203,16 @@ __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ o
         }
         s = __shfl_sync(0xffffffffu, s, 0);
         const int64_t jend = (total - j0 < kEnumChunk) ? total : j0 + kEnumChunk;
-        for (int64_t jb = j0; jb < jend; jb += 32) {       // warp-uniform trip count
-            const int64_t j = jb + lane;
-            uint32_t hk = NO_HOOK;
-            int r = 0;
-            if (j < jend) {
-                while (off[s + 1] <= j) ++s;
-                const int64_t e = seg_a[s] + (j - off[s]);
-                r = (int)(s / segs_per_lane);
-                bool live = UNI || ((X[r] ^ EH[e]) < ET[e]);
-                const int2 uv = E[e];
-                // after the pull forest pass, a live edge that is its upper
-                // endpoint's first live smaller neighbour is already a tree edge
-                if (SKIP && live && ld_relaxed(cell(L, ld, (uint32_t)uv.y, r)) == (uint32_t)uv.x) live = false;
-                if (live) hk = unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r);
-            }
-            nh += hk != NO_HOOK;
-            wl_push(wl, 0xffffffffu, hk != NO_HOOK, wl_key(hk, r));
+        for (int64_t j = j0 + lane; j < jend; j += 32) {
+            while (off[s + 1] <= j) ++s;
+            const int64_t e = seg_a[s] + (j - off[s]);
+            const int r = (int)(s / segs_per_lane);
+            if (!UNI && !((X[r] ^ EH[e]) < ET[e])) continue;
+            const int2 uv = E[e];
+            // after the pull forest pass, a live edge that is its upper
+            // endpoint's first live smaller neighbour is already a tree edge
+            if (SKIP && ld_relaxed(cell(L, ld, (uint32_t)uv.y, r)) == (uint32_t)uv.x) continue;
+            nh += unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r);
         }
     }
     if (hooks) {
@@ -251,7 +236,7 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
                                               const int32_t *__restrict__ hash, const int32_t *__restrict__ thr,
                                               int32_t tu, int64_t n, const int32_t *__restrict__ X, int32_t W,
                                               int64_t ld, uint32_t *__restrict__ L,
-                                              unsigned long long *__restrict__ hooks, Worklist wl) {
+                                              unsigned long long *__restrict__ hooks) {
     extern __shared__ int4 smem4[];
     int32_t *sX = reinterpret_cast<int32_t *>(smem4);
     for (int i = threadIdx.x; i < ld; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
@@ -322,27 +307,18 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
                         const uint32_t a = qlo[qn + lane], bb = qhi[qn + lane];
                         const int rr = (int)qr[qn + lane];
                         __syncwarp();
-                        const uint32_t hk = unite(L, ld, a, bb, rr);
-                        nh += hk != NO_HOOK;
-                        wl_push(wl, FULL, hk != NO_HOOK, wl_key(hk, rr));
+                        nh += unite(L, ld, a, bb, rr);
                     }
                 }
             }
-            if (PASS == 1) {
-                if (active)
-                    *(reinterpret_cast<uint4 *>(L + v * ld) + qd) = make_uint4(best[0], best[1], best[2], best[3]);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) wl_push(wl, FULL, active && best[j] != ROOT, wl_key((uint32_t)v, r + j));
+            if (PASS == 1 && active) {
+                *(reinterpret_cast<uint4 *>(L + v * ld) + qd) = make_uint4(best[0], best[1], best[2], best[3]);
             }
         }
     }
     if (PASS == 2) {
         __syncwarp();
-        uint32_t hk = NO_HOOK;
-        int rr = 0;
-        if (lane < qn) { rr = (int)qr[lane]; hk = unite(L, ld, qlo[lane], qhi[lane], rr); }
-        nh += hk != NO_HOOK;
-        wl_push(wl, FULL, hk != NO_HOOK, wl_key(hk, rr));
+        if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
     }
     if (hooks) {
         for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
@@ -472,58 +448,6 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
     }
 }
 
-// Compression over the work list: one thread per non-root cell recorded
-// while sampling (only the non-trivial cells; ~5% of all cells on the C2
-// workload).  Members of hub-rooted components (ids < kHot, lanes < 2048) are
-// counted in shared memory and flushed once per CTA.  The atomicAdd that
-// finds a root's count still 0 is the first member of a non-trivial
-// component: it appends that root to the root list (for the gains pass).
-constexpr int kHubLanesWL = 2048;
-__global__ void __launch_bounds__(256) k_compress_wl(uint32_t *__restrict__ L, int64_t ld,
-                                                     const unsigned long long *__restrict__ ent,
-                                                     const unsigned long long *__restrict__ cntp, int64_t cap,
-                                                     Worklist roots) {
-    __shared__ uint32_t hub[kHot][kHubLanesWL];
-    for (int i = threadIdx.x; i < kHot * kHubLanesWL; i += blockDim.x) (&hub[0][0])[i] = 0;
-    __syncthreads();
-    const int64_t total = (int64_t)(*cntp < (unsigned long long)cap ? *cntp : (unsigned long long)cap);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += stride) {   // block-uniform
-        const int64_t i = base + threadIdx.x;
-        bool first = false;
-        uint32_t p = 0;
-        int r = 0;
-        if (i < total) {
-            const unsigned long long e = ent[i];
-            const uint32_t v = (uint32_t)(e >> 32);
-            r = (int)(e & 0xffffffffu);
-            const uint32_t w = ld_relaxed(cell(L, ld, v, r));
-            uint32_t x = v;
-            p = w;
-            uint32_t gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r)) : ld_relaxed(cell(L, ld, p, r));
-            while (!is_root(gw)) {
-                atomicMin(cell(L, ld, x, r), gw);
-                x = p;
-                p = gw;
-                gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r)) : ld_relaxed(cell(L, ld, p, r));
-            }
-            if (p != w) L[(int64_t)v * ld + r] = p;
-            if (p < (uint32_t)kHot && r < kHubLanesWL) atomicAdd(&hub[p][r], 1u);
-            else first = atomicAdd(cell(L, ld, p, r), 1u) == ROOT;
-        }
-        wl_push(roots, 0xffffffffu, first, wl_key(p, r));
-    }
-    __syncthreads();
-    for (int i0 = 0; i0 < kHot * kHubLanesWL; i0 += blockDim.x) {     // block-uniform
-        const int i = i0 + threadIdx.x;
-        const uint32_t c = (&hub[0][0])[i];
-        const int p = i / kHubLanesWL, r = i % kHubLanesWL;
-        bool first = false;
-        if (c) first = atomicAdd(cell(L, ld, (uint32_t)p, r), c) == ROOT;
-        wl_push(roots, 0xffffffffu, first, wl_key((uint32_t)p, r));
-    }
-}
-
 // Verification sweep: live (edge, lane) pairs whose endpoint labels differ,
 // and non-root cells that do not point at a smaller root.
 template <bool UNI>
@@ -593,41 +517,6 @@ int run_init(imx_ctx *c) {
     return IMX_OK;
 }
 
-static Worklist wl_of(imx_ctx *c) {
-    Worklist w;
-    w.cnt = c->wl_cnt;
-    w.ent = c->wl_ent;
-    w.cap = c->wl_enabled ? c->wl_cap : 0;
-    return w;
-}
-
-// Size the non-root work list from the expected number of live (edge, lane)
-// pairs (each union or forest link makes at most one non-root); disabled when
-// it would not fit comfortably next to the label matrix.
-static int prepare_worklists(imx_ctx *c) {
-    imx_graph *g = c->g;
-    const char *m = getenv("IMX_WORKLIST");
-    const double live = g->thr_mean * (double)g->me * (double)c->W;
-    int64_t cap = (int64_t)std::min<double>((double)g->n * (double)c->W, 1.25 * live + 65536.0);
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const bool fits = 2.0 * 8.0 * (double)cap < 0.25 * (double)free_b + 2.0 * 8.0 * (double)c->wl_cap;
-    c->wl_enabled = !(m && !strcmp(m, "off")) && g->me > 0 && fits;
-    if (!c->wl_enabled) return IMX_OK;
-    if (cap > c->wl_cap) {
-        if (c->wl_ent) cudaFreeAsync(c->wl_ent, c->st);
-        if (c->rt_ent) cudaFreeAsync(c->rt_ent, c->st);
-        c->wl_ent = c->rt_ent = nullptr;
-        c->wl_cap = 0;
-        IMX_CUDA(pool_alloc((void **)&c->wl_ent, sizeof(unsigned long long) * cap, c->st));
-        IMX_CUDA(pool_alloc((void **)&c->rt_ent, sizeof(unsigned long long) * cap, c->st));
-        c->wl_cap = cap;
-    }
-    if (!c->wl_cnt) IMX_CUDA(pool_alloc((void **)&c->wl_cnt, sizeof(unsigned long long) * 2, c->st));
-    IMX_CUDA(cudaMemsetAsync(c->wl_cnt, 0, sizeof(unsigned long long) * 2, c->st));
-    return IMX_OK;
-}
-
 static int run_hook_dense(imx_ctx *c, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const size_t smem = sizeof(int32_t) * c->ld + sizeof(uint32_t) * 3 * kQ * kHookWarps;
@@ -637,7 +526,7 @@ static int run_hook_dense(imx_ctx *c, unsigned long long *hooks) {
     auto kern = g->uniform ? k_hook<true> : k_hook<false>;
     if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<blocks, kHookWarps * 32, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
-                                                    c->ld, c->L, hooks, wl_of(c));
+                                                    c->ld, c->L, hooks);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;
@@ -670,7 +559,7 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest
     auto kern = g->uniform ? (skip_forest ? k_hook_enum<true, true> : k_hook_enum<true, false>)
                            : (skip_forest ? k_hook_enum<false, true> : k_hook_enum<false, false>);
     kern<<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH, g->ET, c->X, c->ld,
-                                    c->L, hooks, wl_of(c));
+                                    c->L, hooks);
     IMX_CHECK_LAUNCH();
     count_launch(c, 3);
     return IMX_OK;
@@ -687,7 +576,7 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
                           : (g->uniform ? k_pull<2, true> : k_pull<2, false>);
     if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<blocks, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld,
-                                       c->L, hooks, wl_of(c));
+                                       c->L, hooks);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;
@@ -715,7 +604,6 @@ static int hook_mode(const imx_graph *g) {
 // init + hook phases of one propagate (events bracket them)
 static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_init, cudaEvent_t e_hook) {
     imx_graph *g = c->g;
-    IMX_TRY(prepare_worklists(c));
     const int mode = g->me ? hook_mode(g) : HOOK_ENUM;
     if (mode == HOOK_PULL || mode == HOOK_HYBRID) {
         IMX_TRY(run_pull(c, 1, nullptr));
@@ -735,27 +623,6 @@ static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_in
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
-    c->wl_valid = false;
-    if (c->wl_enabled) {
-        unsigned long long cnt = 0;
-        IMX_CUDA(cudaMemcpyAsync(&cnt, c->wl_cnt, sizeof cnt, cudaMemcpyDeviceToHost, c->st));
-        IMX_CUDA(cudaStreamSynchronize(c->st));
-        if ((int64_t)cnt <= c->wl_cap) {
-            Worklist roots;
-            roots.cnt = c->wl_cnt + 1;
-            roots.ent = c->rt_ent;
-            roots.cap = c->wl_cap;
-            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)cnt, 256), 148 * 8));
-            k_compress_wl<<<blocks, 256, 0, c->st>>>(c->L, c->ld, c->wl_ent, c->wl_cnt, c->wl_cap, roots);
-            IMX_CHECK_LAUNCH();
-            count_launch(c);
-            if (nonroot) IMX_CUDA(cudaMemcpyAsync(nonroot, c->wl_cnt, sizeof(unsigned long long),
-                                                  cudaMemcpyDeviceToDevice, c->st));
-            c->wl_valid = true;
-            c->wl_total = (int64_t)cnt;
-            return IMX_OK;
-        }
-    }
     // grid stride = a whole number of rows, so every thread keeps its quad
     const int64_t nq = c->ld >> 2;
     const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * 2);
@@ -805,7 +672,6 @@ extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (st) st->sweeps = 0;
-    c->wl_valid = false;
     unsigned long long *sc = c->scratch;
     IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long) * 4, c->st));
     IMX_CUDA(cudaEventRecord(c->ev[0], c->st));

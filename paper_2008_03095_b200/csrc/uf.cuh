@@ -47,49 +47,20 @@ __device__ __forceinline__ void find2(uint32_t *L, int64_t ld, int r, uint32_t &
 
 // Union of a and b in lane r: CAS-hook the larger root under the smaller.
 // During hooking every root cell is exactly ROOT (member counts are only
-// written by the compress pass).  Returns the vertex whose cell was hooked
-// (it just became a non-root) or NO_HOOK.
-constexpr uint32_t NO_HOOK = 0xFFFFFFFFu;
-__device__ __forceinline__ uint32_t unite(uint32_t *L, int64_t ld, uint32_t a, uint32_t b, int r) {
+// written by the compress pass).  Returns 1 when a hook happened.
+__device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32_t b, int r) {
     uint32_t wa = ld_relaxed(cell(L, ld, a, r));
     uint32_t wb = ld_relaxed(cell(L, ld, b, r));
     find2(L, ld, r, a, wa, b, wb);
     while (a != b) {
         const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
         const uint32_t old = atomicCAS(cell(L, ld, hi, r), ROOT, lo);
-        if (old == ROOT) return hi;
+        if (old == ROOT) return 1;
         a = lo;
         b = hi;
         find2(L, ld, r, a, ld_relaxed(cell(L, ld, lo, r)), b, old);
     }
-    return NO_HOOK;
-}
-
-// Work list of (vertex, lane) cells: the cells that became non-roots while
-// sampling (so compression and gains only visit non-trivial cells), and the
-// roots of non-trivial components found by compression.  Entries are
-// vertex << 32 | lane; appends are warp-aggregated (one atomic per warp).
-struct Worklist {
-    unsigned long long *cnt;
-    unsigned long long *ent;
-    int64_t cap;
-};
-__device__ __forceinline__ unsigned long long wl_key(uint32_t v, int r) {
-    return ((unsigned long long)v << 32) | (uint32_t)r;
-}
-// all threads of `act` must call it together
-__device__ __forceinline__ void wl_push(const Worklist &wl, unsigned act, bool has, unsigned long long val) {
-    if (wl.cap == 0) return;
-    const unsigned m = __ballot_sync(act, has);
-    if (!m) return;
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(wl.cnt, (unsigned long long)__popc(m));
-    base = __shfl_sync(act, base, leader);
-    if (has) {
-        const unsigned long long i = base + __popc(m & ((1u << lane) - 1u));
-        if ((int64_t)i < wl.cap) wl.ent[i] = val;
-    }
+    return 0;
 }
 
 // Root of x given its parent p (p = L[x], not a root word); re-points each

@@ -233,18 +233,3 @@ def test_config_graphs_are_the_golden_graphs(gpu, cfg):
     check_array(z, "xadj", g.xadj)
     check_array(z, "adj", g.adj)
     check_array(z, "weights", g.weights)
-
-
-@pytest.mark.parametrize("worklist", ["on", "off"])
-@pytest.mark.parametrize("mode", ["enum", "pull", "dense"])
-@pytest.mark.parametrize("name", ["er_big_1000", "er_pad20", "er_const1_r16", "cfg_c1", "er_wc_r40"])
-def test_worklist_and_full_scan_memo_agree(gpu, name, mode, worklist, monkeypatch):
-    monkeypatch.setenv("IMX_HOOK", mode)
-    monkeypatch.setenv("IMX_WORKLIST", worklist)
-    z = load_golden(name)
-    g = build_graph(gpu, z)
-    run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))
-    assert sha(run.labels) == str(z["labels_sha"])
-    assert sha(run.sizes) == str(z["sizes_sha"])
-    assert run.seeds == z["seeds"].tolist()
-    assert np.array_equal(run.selection.trace.array, z["trace"])

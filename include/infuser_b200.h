@@ -182,6 +182,23 @@ int  imx_per_sim(imx_ctx *c, int64_t *out);
 /* owned bitmap rows: [n][ceil(num_scored/32)] uint32 (SeedState.owned).  */
 int  imx_copy_owned(imx_ctx *c, uint32_t *bits_out);
 
+/* ---- evaluation (evaluation.py) -----------------------------------------
+ * evaluate_seeds (evaluation.py:101-136) on fresh rng-sampled worlds: world j
+ * of chunk c (c = j / chunk) consumes draws [(j mod chunk)*E, ..+E) of numpy
+ * PCG64 stream c, given as 4 uint64 per chunk {state_hi, state_lo, inc_hi,
+ * inc_lo} (default_rng(SeedSequence(seed).spawn(..)[c]).bit_generator.state);
+ * edge e (canonical slots, slot order) is live iff random() < max(w, w_recip).
+ * counts_out[j] = reached-set size of world j (seeds: k distinct ids).     */
+int  imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k, int64_t r_eval,
+                        const uint64_t *streams, int64_t chunk, int64_t *counts_out);
+/* sampling_cdf (evaluation.py:157-183): values (hash[canon[i*stride]] ^
+ * X[r]) / H_MAX over strided canonical slots and r < scored; outputs the
+ * numpy-rule histogram over `edges` (bins+1 ascending f64), the exact KS
+ * distance to U(0,1) and the number of values.                            */
+int  imx_sampling_cdf(imx_graph *g, const int32_t *X, int32_t scored, int64_t stride,
+                      int32_t bins, const double *edges, int64_t *counts_out,
+                      double *ks_out, int64_t *nvals_out);
+
 /* ---- measurement --------------------------------------------------------
  * Device time (CUDA events on the context stream) of the last call of each
  * phase and the number of kernels this context launched so far.           */

@@ -230,3 +230,74 @@ int64_t oracle_celf(int64_t n, int64_t W, const int32_t *labels, const int32_t *
     free(heap); free(fresh_at); free(owned);
     return ntrace;
 }
+
+/* ------------------------------------------------------------------------
+ * evaluate_seeds worker (evaluation.py:70-98, 101-136): world j of chunk c
+ * draws E doubles from numpy PCG64 stream c (state/inc given by the caller,
+ * taken from default_rng(SeedSequence(seed).spawn(..)[c])), starting at
+ * draw (j mod chunk) * E; edge e is live iff random() < probs[e]; the count
+ * is the size of the union of the seed components.  random() is numpy's
+ * next_double: (next64 >> 11) * 2^-53; next64 is the XSL-RR output of the
+ * 128-bit LCG state after the step (pcg64.h).
+ * ------------------------------------------------------------------------ */
+typedef unsigned __int128 o_u128;
+static inline o_u128 o_pcg_mult(void) {
+    return ((o_u128)0x2360ED051FC65DA4ULL << 64) | (o_u128)0x4385DF649FCCF645ULL;
+}
+static inline uint64_t o_pcg_out(o_u128 s) {
+    unsigned rot = (unsigned)(s >> 122);
+    uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+static o_u128 o_pcg_advance(o_u128 s, o_u128 inc, uint64_t d) {
+    o_u128 am = 1, ap = 0, cm = o_pcg_mult(), cp = inc;
+    while (d) {
+        if (d & 1) { am *= cm; ap = ap * cm + cp; }
+        cp = (cm + 1) * cp; cm *= cm; d >>= 1;
+    }
+    return am * s + ap;
+}
+static int32_t o_find(int32_t *par, int32_t x) {
+    while (par[x] != x) { par[x] = par[par[x]]; x = par[x]; }
+    return x;
+}
+
+void oracle_evaluate(int64_t n, int64_t E, const int32_t *cu, const int32_t *cv, const double *probs,
+                     const int32_t *seeds, int32_t k, int64_t r_eval, const uint64_t *streams,
+                     int64_t chunk, int64_t *counts, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    const o_u128 M = o_pcg_mult();
+#pragma omp parallel
+    {
+        int32_t *par = (int32_t *)malloc(sizeof(int32_t) * (n ? n : 1));
+        int64_t *sz = (int64_t *)malloc(sizeof(int64_t) * (n ? n : 1));
+        int64_t *stamp = (int64_t *)malloc(sizeof(int64_t) * (n ? n : 1));
+        for (int64_t v = 0; v < n; ++v) stamp[v] = -1;
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t j = 0; j < r_eval; ++j) {
+            const uint64_t *sv = streams + 4 * (j / chunk);
+            const o_u128 inc = ((o_u128)sv[2] << 64) | sv[3];
+            o_u128 s = o_pcg_advance(((o_u128)sv[0] << 64) | sv[1], inc, (uint64_t)(j % chunk) * (uint64_t)E);
+            for (int64_t v = 0; v < n; ++v) { par[v] = (int32_t)v; sz[v] = 1; }
+            for (int64_t e = 0; e < E; ++e) {
+                s = s * M + inc;
+                const double u = (double)(o_pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+                if (!(u < probs[e])) continue;
+                int32_t a = o_find(par, cu[e]), b = o_find(par, cv[e]);
+                if (a == b) continue;
+                if (sz[a] < sz[b]) { int32_t t = a; a = b; b = t; }
+                par[b] = a;
+                sz[a] += sz[b];
+            }
+            int64_t tot = 0;
+            for (int32_t i = 0; i < k; ++i) {
+                const int32_t r = o_find(par, seeds[i]);
+                if (stamp[r] != j) { stamp[r] = j; tot += sz[r]; }
+            }
+            counts[j] = tot;
+        }
+        free(par); free(sz); free(stamp);
+    }
+}

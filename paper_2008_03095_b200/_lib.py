@@ -85,6 +85,9 @@ _SIGNATURES = {
     "imx_celf_trace": (c_i32, [c_void_p, c_void_p, c_i64]),
     "imx_per_sim": (c_i32, [c_void_p, c_void_p]),
     "imx_copy_owned": (c_i32, [c_void_p, c_void_p]),
+    "imx_evaluate_seeds": (c_i32, [c_void_p, c_void_p, c_i32, c_i64, c_void_p, c_i64, c_void_p]),
+    "imx_sampling_cdf": (c_i32, [c_void_p, c_void_p, c_i32, c_i64, c_i32, c_void_p, c_void_p, P(c_f64),
+                                 P(c_i64)]),
     "imx_get_timings": (c_i32, [c_void_p, P(Timings)]),
     "imx_bench_propagate": (c_i32, [c_void_p, c_i32, c_i32, P(c_f32), P(c_f32), P(c_f32), P(c_f32)]),
 }

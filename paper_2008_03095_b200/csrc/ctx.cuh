@@ -99,6 +99,10 @@ inline void count_launch(imx_ctx *c, int k = 1) {
 int ensure_celf_buffers(imx_ctx *c);
 int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);
+// raw label-matrix passes shared with the evaluation worlds (evaluation.cu)
+int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
+int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
+                    cudaStream_t st);
 
 }  // namespace imx
 

@@ -507,13 +507,19 @@ __global__ void k_flush(uint4 *buf, int64_t cnt, uint32_t salt) {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-int run_init(imx_ctx *c) {
-    const int64_t n = c->g->n;
+int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st) {
     if (n == 0) return IMX_OK;
-    const int64_t cells4 = n * (c->ld >> 2);
-    k_init<<<grid_for(cells4), 256, 0, c->st>>>(c->L, cells4);
+    const int64_t cells4 = n * (ld >> 2);
+    k_init<<<grid_for(cells4), 256, 0, st>>>(L, cells4);
     IMX_CHECK_LAUNCH();
-    count_launch(c);
+    note_launch();
+    return IMX_OK;
+}
+
+int run_init(imx_ctx *c) {
+    if (c->g->n == 0) return IMX_OK;
+    IMX_TRY(launch_init(c->L, c->g->n, c->ld, c->st));
+    c->tm.kernel_launches++;
     return IMX_OK;
 }
 
@@ -620,11 +626,11 @@ static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_in
     return IMX_OK;
 }
 
-static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
-    const int64_t n = c->g->n;
+int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
+                    cudaStream_t st) {
     if (n == 0) return IMX_OK;
     // grid stride = a whole number of rows, so every thread keeps its quad
-    const int64_t nq = c->ld >> 2;
+    const int64_t nq = ld >> 2;
     const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * 2);
     const int64_t rows = std::max<int64_t>(1, want / nq);
     const int64_t threads = rows * nq;
@@ -632,9 +638,16 @@ static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     // threads beyond rows*nq would break the fixed-quad mapping: size the
     // stride from the launched thread count, rounded down to whole rows
     const int64_t vstep = ((int64_t)blocks * 256) / nq;
-    k_compress<<<blocks, 256, 0, c->st>>>(c->L, n, c->ld, c->W, vstep, nonroot);
+    k_compress<<<blocks, 256, 0, st>>>(L, n, ld, W, vstep, nonroot);
     IMX_CHECK_LAUNCH();
-    count_launch(c);
+    note_launch();
+    return IMX_OK;
+}
+
+static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
+    if (c->g->n == 0) return IMX_OK;
+    IMX_TRY(launch_compress(c->L, c->g->n, c->ld, c->W, nonroot, c->st));
+    c->tm.kernel_launches++;
     return IMX_OK;
 }
 

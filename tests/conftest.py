@@ -19,7 +19,24 @@ def pytest_configure(config):
 
 
 def golden_names(prefix: str = "") -> list[str]:
-    return sorted(p.stem for p in GOLDEN.glob(f"{prefix}*.npz"))
+    """Pipeline fixtures by default; evaluation ones under "eval_" / "cdf_"."""
+    names = sorted(p.stem for p in GOLDEN.glob(f"{prefix}*.npz"))
+    if not prefix:
+        names = [n for n in names if not n.startswith(("eval_", "cdf_"))]
+    return names
+
+
+def golden_graph(z: dict):
+    """(xadj, adj, weights) of an evaluation fixture; config graphs are
+    rebuilt from this repo's host generator (weights of the config scheme)."""
+    if "cfg" in z:
+        import oracle
+        from paper_2008_03095_b200 import configs
+        c = configs.CONFIGS[str(z["cfg"])]
+        xadj, adj, _ = oracle.csr_from_edges(c.n, configs.edges(str(z["cfg"])))
+        w = np.full(len(adj), float(c.weights.split(":")[1]))
+        return xadj, adj, w
+    return z["xadj"], z["adj"], z["weights"]
 
 
 def load_golden(name: str) -> dict:

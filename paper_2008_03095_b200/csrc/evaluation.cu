@@ -84,19 +84,60 @@ __global__ void k_eval_edges(const int64_t *__restrict__ cslot, int64_t me, cons
     }
 }
 
+// Jump tables.  The state of world w at edge e0 = j*kRun of its run is
+//   S(w, e0) = A_j * S_w + C_j,   S_w = state at the world's first draw,
+// with (A_j, C_j) the affine map of j*kRun LCG steps (same for every world
+// of the chunk), so a hook thread starts with one 128-bit multiply-add
+// instead of an O(log) jump.
+constexpr int kRun = 512;
+__global__ void k_eval_jumps(int64_t nruns, uint64_t i_hi, uint64_t i_lo, ulonglong2 *__restrict__ jt) {
+    const u128 inc = ((u128)i_hi << 64) | i_lo;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nruns;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        u128 am = 1, ap = 0, cm = pcg_mult(), cp = inc;
+        for (uint64_t d = (uint64_t)j * kRun; d; d >>= 1) {
+            if (d & 1) {
+                am *= cm;
+                ap = ap * cm + cp;
+            }
+            cp = (cm + 1) * cp;
+            cm *= cm;
+        }
+        jt[2 * j] = make_ulonglong2((uint64_t)(am >> 64), (uint64_t)am);
+        jt[2 * j + 1] = make_ulonglong2((uint64_t)(ap >> 64), (uint64_t)ap);
+    }
+}
+
+__global__ void k_eval_worlds(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, int64_t pos0,
+                              int32_t nw, int64_t me, ulonglong2 *__restrict__ ws) {
+    const u128 S0 = ((u128)s_hi << 64) | s_lo, inc = ((u128)i_hi << 64) | i_lo;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nw; r += gridDim.x * blockDim.x) {
+        const u128 s = pcg_advance(S0, inc, (uint64_t)(pos0 + r) * (uint64_t)me);
+        ws[r] = make_ulonglong2((uint64_t)(s >> 64), (uint64_t)s);
+    }
+}
+
 // One thread per (world lane, run of kRun edges); a CTA = 128 consecutive
 // worlds of one run, so the run's edges are staged once in shared memory and
-// the label cells of a vertex are touched by consecutive lanes.
-constexpr int kRun = 256;
+// the label cells of a vertex are touched by consecutive lanes.  Live
+// (edge, world) pairs go to a per-warp queue and are united 32 at a time,
+// so the root searches run warp-wide instead of at the live density.
 __global__ void __launch_bounds__(128) k_eval_hook(const int2 *__restrict__ ce, const uint64_t *__restrict__ t53,
-                                                   int64_t me, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi,
-                                                   uint64_t i_lo, int64_t pos0, int32_t nw, uint32_t *L,
-                                                   int64_t ld) {
+                                                   int64_t me, const ulonglong2 *__restrict__ jt,
+                                                   const ulonglong2 *__restrict__ ws, uint64_t i_hi,
+                                                   uint64_t i_lo, int32_t nw, uint32_t *L, int64_t ld) {
     __shared__ int2 se[kRun];
     __shared__ uint64_t st[kRun];
-    const u128 S0 = ((u128)s_hi << 64) | s_lo, inc = ((u128)i_hi << 64) | i_lo, M = pcg_mult();
+    __shared__ uint32_t qe[4][64];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    const u128 inc = ((u128)i_hi << 64) | i_lo, M = pcg_mult();
     const int r = blockIdx.x * 128 + threadIdx.x;
+    const bool act = r < nw;
+    u128 Sw = 0;
+    if (act) Sw = ((u128)ws[r].x << 64) | ws[r].y;
     const int64_t nruns = (me + kRun - 1) / kRun;
+    uint32_t *q = qe[warp];
     for (int64_t j = blockIdx.y; j < nruns; j += gridDim.y) {
         const int64_t e0 = j * kRun;
         const int cnt = (int)(me - e0 < kRun ? me - e0 : kRun);
@@ -106,12 +147,31 @@ __global__ void __launch_bounds__(128) k_eval_hook(const int2 *__restrict__ ce, 
             st[i] = t53[e0 + i];
         }
         __syncthreads();
-        if (r >= nw) continue;
-        u128 s = pcg_advance(S0, inc, (uint64_t)(pos0 + r) * (uint64_t)me + (uint64_t)e0);
+        const ulonglong2 a2 = jt[2 * j], c2 = jt[2 * j + 1];
+        u128 s = (((u128)a2.x << 64) | a2.y) * Sw + (((u128)c2.x << 64) | c2.y);
+        int qn = 0;
         for (int i = 0; i < cnt; ++i) {
             s = s * M + inc;
-            if ((pcg_output(s) >> 11) < st[i]) unite(L, ld, (uint32_t)se[i].x, (uint32_t)se[i].y, r);
+            const bool live = act && (pcg_output(s) >> 11) < st[i];
+            const unsigned m = __ballot_sync(FULL, live);
+            if (!m) continue;
+            if (live) q[qn + __popc(m & ((1u << lane) - 1))] = ((uint32_t)i << 8) | (uint32_t)threadIdx.x;
+            qn += __popc(m);
+            __syncwarp();
+            if (qn >= 32) {
+                qn -= 32;
+                const uint32_t x = q[qn + lane];
+                __syncwarp();
+                const int2 ed = se[x >> 8];
+                unite(L, ld, (uint32_t)ed.x, (uint32_t)ed.y, blockIdx.x * 128 + (int)(x & 255));
+            }
         }
+        if (lane < qn) {
+            const uint32_t x = q[lane];
+            const int2 ed = se[x >> 8];
+            unite(L, ld, (uint32_t)ed.x, (uint32_t)ed.y, blockIdx.x * 128 + (int)(x & 255));
+        }
+        __syncwarp();
     }
 }
 
@@ -215,6 +275,7 @@ extern "C" int imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k,
     uint32_t *L = nullptr, *bm = nullptr;
     int32_t *dseeds = nullptr;
     unsigned long long *dcounts = nullptr;
+    ulonglong2 *jt = nullptr, *ws = nullptr;
     int rc = IMX_OK;
     auto fail = [&](cudaError_t e, const char *what) { rc = cuda_fail(e, what, __FILE__, __LINE__); };
     do {
@@ -224,6 +285,8 @@ extern "C" int imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k,
         if ((e = pool_alloc((void **)&L, sizeof(uint32_t) * std::max<int64_t>(n, 1) * ld, st))) { fail(e, "alloc"); break; }
         if ((e = pool_alloc((void **)&bm, sizeof(uint32_t) * std::max<int64_t>(n, 1) * bw, st))) { fail(e, "alloc"); break; }
         if ((e = pool_alloc((void **)&dseeds, sizeof(int32_t) * k, st))) { fail(e, "alloc"); break; }
+        if ((e = pool_alloc((void **)&jt, sizeof(ulonglong2) * 2 * std::max<int64_t>((me + kRun - 1) / kRun, 1), st))) { fail(e, "alloc"); break; }
+        if ((e = pool_alloc((void **)&ws, sizeof(ulonglong2) * B, st))) { fail(e, "alloc"); break; }
         if ((e = pool_alloc((void **)&dcounts, sizeof(unsigned long long) * r_eval, st))) { fail(e, "alloc"); break; }
         if ((e = cudaMemcpyAsync(dseeds, seeds, sizeof(int32_t) * k, cudaMemcpyHostToDevice, st))) { fail(e, "copy"); break; }
         if ((e = cudaMemsetAsync(dcounts, 0, sizeof(unsigned long long) * r_eval, st))) { fail(e, "memset"); break; }
@@ -235,13 +298,19 @@ extern "C" int imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k,
         for (int64_t c0 = 0, ci = 0; c0 < r_eval && rc == IMX_OK; c0 += chunk, ++ci) {
             const int64_t cc = std::min<int64_t>(chunk, r_eval - c0);
             const uint64_t *sv = streams + 4 * ci;
+            if (me) {
+                k_eval_jumps<<<grid_for(nruns, 128), 128, 0, st>>>(nruns, sv[2], sv[3], jt);
+                note_launch();
+            }
             for (int64_t o = 0; o < cc; o += B) {
                 const int32_t nw = (int32_t)std::min<int64_t>(B, cc - o);
                 if ((rc = launch_init(L, n, ld, st))) break;
                 if (me) {
+                    k_eval_worlds<<<grid_for(nw, 128), 128, 0, st>>>(sv[0], sv[1], sv[2], sv[3], o, nw, me, ws);
+                    note_launch();
                     const int gx = (int)((nw + 127) / 128);
                     const int gy = (int)std::min<int64_t>(nruns, std::max<int64_t>(1, 148 * 16 / gx));
-                    k_eval_hook<<<dim3(gx, gy), 128, 0, st>>>(ce, t53, me, sv[0], sv[1], sv[2], sv[3], o, nw, L, ld);
+                    k_eval_hook<<<dim3(gx, gy), 128, 0, st>>>(ce, t53, me, jt, ws, sv[2], sv[3], nw, L, ld);
                     note_launch();
                     if ((e = cudaGetLastError())) { fail(e, "k_eval_hook"); break; }
                     if ((rc = launch_compress(L, n, ld, nw, nullptr, st))) break;
@@ -262,6 +331,8 @@ extern "C" int imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k,
     cudaFreeAsync(bm, st);
     cudaFreeAsync(dseeds, st);
     cudaFreeAsync(dcounts, st);
+    cudaFreeAsync(jt, st);
+    cudaFreeAsync(ws, st);
     return rc;
 }
 

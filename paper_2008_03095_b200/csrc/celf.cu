@@ -233,6 +233,7 @@ static int celf_advance(imx_ctx *c, int64_t k, const int32_t *ids, const unsigne
 // state saved; the host finishes that round and relaunches.
 // ---------------------------------------------------------------------------
 constexpr int64_t kMaxRank = 16384;
+constexpr int64_t kSmemBack = 2048;     // refreshed keys staged in shared memory for the merge
 
 
 template <bool ENC>
@@ -267,6 +268,39 @@ __device__ __forceinline__ int64_t block_eval(const uint32_t *__restrict__ L, co
     return (int64_t)tot;
 }
 
+// Number of leading entries of the descending array a[0, n) that are > key
+// (GE: >= key), by one warp: a 33-ary search (32 pivots per step, one
+// coalesced-free load per lane), so ~log33(n) dependent loads instead of
+// log2(n).  Every lane returns the result.
+template <bool GE>
+__device__ __forceinline__ int64_t warp_count_above(const unsigned long long *a, int64_t n,
+                                                    unsigned long long key) {
+    const int lane = threadIdx.x & 31;
+    int64_t lo = 0, hi = n;                 // answer in [lo, hi]
+    while (hi - lo > 32) {
+        const int64_t span = hi - lo;
+        const int64_t p = lo + (span * (lane + 1)) / 33;
+        const unsigned long long x = a[p];
+        const int c = __popc(__ballot_sync(0xffffffffu, GE ? x >= key : x > key));
+        const int64_t nlo = c == 0 ? lo : lo + (span * c) / 33 + 1;
+        const int64_t nhi = c == 32 ? hi : lo + (span * (c + 1)) / 33;
+        lo = nlo;
+        hi = nhi;
+    }
+    bool in = false;
+    if (lane < hi - lo) {
+        const unsigned long long x = a[lo + lane];
+        in = GE ? x >= key : x > key;
+    }
+    return lo + __popc(__ballot_sync(0xffffffffu, in));
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ unsigned long long block_max(unsigned long long x, unsigned long long *red) {
     for (int o = 16; o; o >>= 1) {
         const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
@@ -288,9 +322,11 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
     int64_t *__restrict__ fresh, unsigned long long *__restrict__ bkey, int32_t *__restrict__ bid,
     unsigned long long *__restrict__ skey, int32_t *__restrict__ sid,
     int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
-    int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st) {
+    int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
+    int32_t bpct) {
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned long long red[8];
+    __shared__ unsigned long long sback[kSmemBack];
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
@@ -298,6 +334,14 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
     int ocur = st->ocur;
     int32_t t = st->t;
     int32_t status = 0;
+    const bool prof = gtid == 0;
+    unsigned long long pf[6] = {0, 0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
+#define PROF_MARK(i)                                 \
+    if (prof) {                                      \
+        const unsigned long long _t = gtimer();      \
+        pf[i] += _t - tp;                            \
+        tp = _t;                                     \
+    }
     while (t < k) {
         int32_t *oid = ocur ? oid1 : oid0;
         unsigned long long *okey = ocur ? okey1 : okey0;
@@ -318,6 +362,7 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
                     if (threadIdx.x == 0) fresh[i] = f;
                 }
                 grid.sync();
+                if (prof) { pf[4]++; pf[5] += hi - lo; }
                 unsigned long long m = 0;
                 for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
                     const unsigned long long fk = ((unsigned long long)fresh[i] << vb) |
@@ -332,13 +377,9 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
                 hi = (olen - hi < step) ? olen : hi + step;
             }
             // refreshed prefix: stale key >= best fresh key (keys sorted descending)
-            int64_t a = 0, b = hi;
-            while (a < b) {
-                const int64_t mid = (a + b) >> 1;
-                if (okey[ostart + mid] >= bestkey) a = mid + 1; else b = mid;
-            }
-            kr = a;
+            kr = warp_count_above<true>(okey + ostart, hi, bestkey);
         }
+        PROF_MARK(0);
         const int32_t best_v = (int32_t)(vmask - (uint32_t)(bestkey & vmask));
         const int64_t best_f = (int64_t)(bestkey >> vb);
         const int64_t nrec = (t == 0 ? 0 : kr) + 1;
@@ -375,6 +416,7 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
             if ((threadIdx.x & 31) == 0 && acc) atomicAdd(gain, acc);
         }
         grid.sync();
+        PROF_MARK(1);
         // phase 2: self-check of the commit; rank + scatter the refreshed vertices
         const unsigned long long got = *gain;
         if ((int64_t)got != best_f) {
@@ -384,31 +426,47 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
         }
         const int64_t nback = t == 0 ? 0 : kr - 1;       // the winner is not re-inserted
         if (nback > 0) {
-            for (int64_t j = gtid; j < kr; j += gthreads) {
+            // rank of each refreshed key among them: one warp per key, the
+            // comparisons spread over the lanes (coalesced 256-byte loads)
+            const int lane = threadIdx.x & 31;
+            for (int64_t j = gtid >> 5; j < kr; j += gthreads >> 5) {
                 const unsigned long long kj = bkey[j];
                 int64_t rk = 0;
-                for (int64_t i = 0; i < kr; ++i) rk += bkey[i] > kj;
-                if (rk < nback) { skey[rk] = kj; sid[rk] = bid[j]; }
+                for (int64_t i = lane; i < kr; i += 32) rk += bkey[i] > kj;
+                for (int o = 16; o; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+                if (lane == 0 && rk < nback) { skey[rk] = kj; sid[rk] = bid[j]; }
             }
             grid.sync();
+            PROF_MARK(2);
             // phase 3: merge order[kr, olen) with the sorted refreshed vertices
             int32_t *ob = ocur ? oid0 : oid1;
             unsigned long long *okb = ocur ? okey0 : okey1;
             const int64_t na = olen - kr;
             const unsigned long long *ak = okey + ostart + kr;
             const int32_t *ai = oid + ostart + kr;
-            for (int64_t i = gtid; i < na + nback; i += gthreads) {
-                const bool in_a = i < na;
-                const int64_t j = in_a ? i : i - na;
-                const unsigned long long key = in_a ? ak[j] : skey[j];
-                const unsigned long long *other = in_a ? skey : ak;
-                int64_t lo2 = 0, hi2 = in_a ? nback : na;
+            // order entries: shift by the refreshed keys above them (binary
+            // search in a shared-memory copy of the sorted refreshed keys)
+            const bool in_smem = nback <= kSmemBack;
+            if (in_smem) {
+                for (int64_t i = threadIdx.x; i < nback; i += blockDim.x) sback[i] = skey[i];
+                __syncthreads();
+            }
+            const unsigned long long *sk = in_smem ? sback : skey;
+            for (int64_t i = gtid; i < na; i += gthreads) {
+                const unsigned long long key = ak[i];
+                int64_t lo2 = 0, hi2 = nback;
                 while (lo2 < hi2) {
                     const int64_t mid = (lo2 + hi2) >> 1;
-                    if (other[mid] > key) lo2 = mid + 1; else hi2 = mid;
+                    if (sk[mid] > key) lo2 = mid + 1; else hi2 = mid;
                 }
-                ob[j + lo2] = in_a ? ai[j] : sid[j];
-                okb[j + lo2] = key;
+                ob[i + lo2] = ai[i];
+                okb[i + lo2] = key;
+            }
+            // refreshed entries: shift by the order keys above them (warp search)
+            for (int64_t j = gtid >> 5; j < nback; j += gthreads >> 5) {
+                const unsigned long long key = sk[j];
+                const int64_t pos = j + warp_count_above<false>(ak, na, key);
+                if (lane == 0) { ob[pos] = sid[j]; okb[pos] = key; }
             }
             ocur ^= 1;
             ostart = 0;
@@ -418,11 +476,14 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
             olen -= kr;
         }
         T += nrec;
-        if (t > 0) batch0 = kr > 64 ? kr : 64;
+        if (t > 0) batch0 = kr * bpct / 100 > 64 ? kr * bpct / 100 : 64;
         ++t;
         grid.sync();
+        PROF_MARK(3);
     }
+#undef PROF_MARK
     if (gtid == 0) {
+        for (int i = 0; i < 6; ++i) st->prof[i] += pf[i];
         st->ostart = ostart; st->olen = olen; st->ocur = ocur; st->t = t;
         st->trace_len = T; st->batch0 = batch0;
         st->status = status ? status : 1;
@@ -707,12 +768,19 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     unsigned long long *k0 = c->okey[0], *k1 = c->okey[1], *bkey = c->bkey, *skey = c->skey;
     int64_t cap = c->trace_cap;
     CelfDev *stp = c->cdev;
+    // next round's first batch = bpct% of this round's refreshed prefix
+    int32_t bpct = 100;
+    if (const char *b = getenv("IMX_CELF_BATCH_PCT")) bpct = std::max(1, atoi(b));
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
-                    &bkey, &bid, &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp};
+                    &bkey, &bid, &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct};
     IMX_CUDA(cudaLaunchCooperativeKernel(fn, grid_cache[enc], 256, args, 0, c->st));
     count_launch(c);
     IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (getenv("IMX_CELF_PROFILE"))
+        fprintf(stderr, "[celf] rounds %d..%d grid %d: eval %.1f us, commit %.1f us, rank %.1f us, merge %.1f us; "
+                "%llu eval steps, %llu evaluations\n", t, h.t, grid_cache[enc], h.prof[0] * 1e-3, h.prof[1] * 1e-3,
+                h.prof[2] * 1e-3, h.prof[3] * 1e-3, h.prof[4], h.prof[5]);
     if (h.status == 3) {
         if (h.olen == 0) set_error("no candidate left at round %d", h.t);
         else set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",

@@ -66,6 +66,9 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // process-wide count of this library's kernel launches (imx_launch_count)
 void note_launch(int64_t k = 1);
+// recycled non-blocking streams (graph.cu)
+cudaError_t acquire_stream(int dev, cudaStream_t *st);
+void release_stream(int dev, cudaStream_t st);
 // stream-ordered allocation from the device's pool (ctx.cu)
 cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
 

@@ -67,7 +67,7 @@ void ctx_free(imx_ctx *c) {
     pinned_put(c->h_ids, sizeof(int32_t) * c->stage_cap);
     pinned_put(c->h_vals, sizeof(int64_t) * c->stage_cap);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
-    if (c->st) cudaStreamDestroy(c->st);
+    release_stream(c->dev, c->st);
     delete c;
 }
 
@@ -139,7 +139,7 @@ extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t
     for (auto &e : c->ev) e = nullptr;
     const int64_t n = g->n;
     auto fail = [&](int code) { ctx_free(c); return code; };
-    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return fail(IMX_ECUDA);
+    if (acquire_stream(c->dev, &c->st) != cudaSuccess) return fail(IMX_ECUDA);
     for (auto &e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return fail(IMX_ECUDA);
     const size_t cells = (size_t)(n > 0 ? n : 1) * (size_t)c->ld;

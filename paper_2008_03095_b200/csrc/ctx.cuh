@@ -31,6 +31,9 @@ struct CelfDev {
     int32_t status;        // 1 done, 2 trace buffer full, 3 self-check failed, 4 round too large
     int32_t bad_v;
     int64_t bad_want, bad_got;
+    // phase times (ns, %globaltimer on block 0): eval, commit, rank, merge;
+    // [4] eval batch steps, [5] evaluations (IMX_CELF_PROFILE prints them)
+    unsigned long long prof[6];
 };
 
 struct imx_ctx {

@@ -156,7 +156,7 @@ extern "C" int imx_graph_generate(int32_t device, int32_t kind, int64_t n, int64
     }
     IMX_TRY(select_device(device));
     cudaStream_t st;
-    IMX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    IMX_CUDA(acquire_stream(device, &st));
     double *dcdf = nullptr;
     uint64_t *ukeys = nullptr;
     uint32_t *uidx = nullptr;
@@ -208,8 +208,7 @@ extern "C" int imx_graph_generate(int32_t device, int32_t kind, int64_t n, int64
     if (rc == IMX_OK) rc = graph_create(device, n, 2 * k, &g);
     if (rc == IMX_OK) rc = graph_build_from_device_edges(g, dedges, k, nullptr, 1.0);
     for (void *p : {(void *)dcdf, (void *)ukeys, (void *)uidx, (void *)dedges}) if (p) cudaFreeAsync(p, st);
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
+    release_stream(device, st);
     if (rc != IMX_OK) { if (g) graph_free(g); return rc; }
     *out = g;
     return IMX_OK;

@@ -14,9 +14,11 @@
 // (lo < hi) edge list in slot order is the work list of the hook kernel.
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstring>
 #include <vector>
+#include <chrono>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -28,6 +30,31 @@ namespace imx {
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
 void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// Non-blocking streams are recycled per device: graphs and contexts are
+// often built and dropped back to back (one per run_fused), and creating a
+// stream costs tens of microseconds.
+static std::mutex g_stream_mu;
+static std::vector<std::pair<int, cudaStream_t>> g_streams;
+cudaError_t acquire_stream(int dev, cudaStream_t *st) {
+    {
+        std::lock_guard<std::mutex> lk(g_stream_mu);
+        for (size_t i = 0; i < g_streams.size(); ++i)
+            if (g_streams[i].first == dev) {
+                *st = g_streams[i].second;
+                g_streams.erase(g_streams.begin() + i);
+                return cudaSuccess;
+            }
+    }
+    return cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
+}
+void release_stream(int dev, cudaStream_t st) {
+    if (!st) return;
+    cudaStreamSynchronize(st);
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    if (g_streams.size() < 64) g_streams.emplace_back(dev, st);
+    else cudaStreamDestroy(st);
+}
 
 void set_error(const char *fmt, ...) {
     char buf[1024];
@@ -128,14 +155,17 @@ __global__ void k_src_from_xadj(const int64_t *__restrict__ xadj, int64_t n, int
     }
 }
 
-// reciprocal slot of (u, v): position of u in row v (rows sorted ascending)
+// reciprocal slot of (u, v): position of u in row v (rows sorted ascending);
+// flags: 8 = a slot without reciprocal, 32 = adjacency entry outside 0..n-1
 __global__ void k_reciprocal(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
-                             const int32_t *__restrict__ src, int64_t m2,
+                             const int32_t *__restrict__ src, int64_t n, int64_t m2,
                              int64_t *__restrict__ recip, unsigned *__restrict__ flags) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
          s += (int64_t)gridDim.x * blockDim.x) {
         int32_t u = src[s], v = adj[s];
+        if (v < 0 || v >= n) { recip[s] = -1; atomicOr(flags, 32u | 8u); continue; }
         int64_t lo = xadj[v], hi = xadj[v + 1];
+        if (lo < 0 || hi > m2 || lo > hi) { recip[s] = -1; atomicOr(flags, 64u | 8u); continue; }
         while (lo < hi) {
             int64_t mid = (lo + hi) >> 1;
             if (adj[mid] < u) lo = mid + 1; else hi = mid;
@@ -157,22 +187,49 @@ __global__ void k_slot_hashes(const int32_t *__restrict__ src, const int32_t *__
 __device__ __forceinline__ int32_t thr_of(double w) {
     return (int32_t)(int64_t)(w * 2147483647.0);
 }
+// Build statistics gathered by the analysis kernels and read back with ONE
+// device->host copy (graph_analyze).
+struct GStats {
+    unsigned flags;
+    int32_t tmin, tmax;
+    int32_t pad;
+    unsigned long long maxp;   // max #smaller neighbours (k_max_prefix)
+    unsigned long long tsum;   // sum of canonical-slot thresholds
+    int64_t me;                // canonical slots (DeviceSelect count)
+};
+__global__ void k_stats_init(GStats *gs) {
+    gs->flags = 0; gs->tmin = INT32_MAX; gs->tmax = INT32_MIN; gs->pad = 0;
+    gs->maxp = 0; gs->tsum = 0; gs->me = 0;
+}
+
+// thresholds (symmetrized over valid reciprocal slots when recip != NULL),
+// their range over all slots and their sum over the canonical slots
 __global__ void k_thresholds(const double *__restrict__ w, const int64_t *__restrict__ recip,
-                             int64_t m2, int32_t *__restrict__ thr,
-                             int32_t *__restrict__ tmin, int32_t *__restrict__ tmax) {
+                             const int32_t *__restrict__ src, const int32_t *__restrict__ adj,
+                             int64_t m2, int32_t *__restrict__ thr, GStats *__restrict__ gs) {
     int32_t lmin = INT32_MAX, lmax = INT32_MIN;
+    unsigned long long lsum = 0;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
          s += (int64_t)gridDim.x * blockDim.x) {
         int32_t t = thr_of(w[s]);
-        if (recip) { int32_t t2 = thr_of(w[recip[s]]); t = t2 > t ? t2 : t; }
+        if (recip) {
+            const int64_t r = recip[s];
+            if (r >= 0) { const int32_t t2 = thr_of(w[r]); t = t2 > t ? t2 : t; }
+        }
         thr[s] = t;
         lmin = min(lmin, t); lmax = max(lmax, t);
+        if (src[s] < adj[s]) lsum += (unsigned long long)(uint32_t)t;
     }
     for (int o = 16; o; o >>= 1) {
         lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
         lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
     }
-    if ((threadIdx.x & 31) == 0) { atomicMin(tmin, lmin); atomicMax(tmax, lmax); }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&gs->tmin, lmin);
+        atomicMax(&gs->tmax, lmax);
+        if (lsum) atomicAdd(&gs->tsum, lsum);
+    }
 }
 
 __global__ void k_weights_range(const double *__restrict__ w, int64_t m2, unsigned *flags) {
@@ -194,25 +251,18 @@ __global__ void k_fill_edges(const int64_t *__restrict__ cslot, int64_t me,
                              const int32_t *__restrict__ src, const int32_t *__restrict__ adj,
                              const int32_t *__restrict__ hash, const int32_t *__restrict__ thr,
                              int2 *__restrict__ E, int32_t *__restrict__ EH,
-                             int32_t *__restrict__ ET) {
+                             int32_t *__restrict__ ET, uint32_t *__restrict__ iota) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < me;
          e += (int64_t)gridDim.x * blockDim.x) {
         int64_t s = cslot[e];
         E[e] = make_int2(src[s], adj[s]);
         EH[e] = hash[s];
         ET[e] = thr[s];
+        iota[e] = (uint32_t)e;
     }
 }
 
 // sorted-index construction --------------------------------------------------
-__global__ void k_iota_thr_keys(const int32_t *__restrict__ ET, int64_t me, uint32_t *__restrict__ keys,
-                                uint32_t *__restrict__ vals) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < me;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        keys[e] = (uint32_t)ET[e];
-        vals[e] = (uint32_t)e;
-    }
-}
 // position p of the threshold-sorted order -> bucket p*nb/me; key = bucket<<32 | hash
 __global__ void k_bucket_hash_keys(const uint32_t *__restrict__ by_thr, int64_t me, int nb,
                                    const int32_t *__restrict__ EH, uint64_t *__restrict__ keys,
@@ -237,28 +287,51 @@ __global__ void k_permute_edges(const uint32_t *__restrict__ perm, int64_t me,
         ET[j] = ET0[e];
     }
 }
-// bucket offsets from the sorted keys; per-bucket max threshold
+// bucket offsets from the sorted keys; per-bucket max threshold (reduced
+// per warp over equal buckets first: the keys are sorted, so a warp sees one
+// or two buckets and the atomics do not pile up on 64 addresses)
 __global__ void k_bucket_meta(const uint64_t *__restrict__ keys, int64_t me, int nb,
                               const int32_t *__restrict__ ET, int64_t *__restrict__ boff,
                               int32_t *__restrict__ btmax) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < me;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        const int b = (int)(keys[j] >> 32);
-        const int bp = j ? (int)(keys[j - 1] >> 32) : -1;
-        for (int q = bp + 1; q <= b; ++q) boff[q] = j;
-        if (j == me - 1)
-            for (int q = b + 1; q <= nb; ++q) boff[q] = me;
-        atomicMax(btmax + b, ET[j]);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < me; j0 += stride) {
+        const int64_t j = j0 + threadIdx.x;
+        const bool in = j < me;
+        const int b = in ? (int)(keys[j] >> 32) : -1;
+        if (in) {
+            const int bp = j ? (int)(keys[j - 1] >> 32) : -1;
+            for (int q = bp + 1; q <= b; ++q) boff[q] = j;
+            if (j == me - 1)
+                for (int q = b + 1; q <= nb; ++q) boff[q] = me;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int t = in ? ET[j] : INT32_MIN;
+        const int m = __reduce_max_sync(peers, t);
+        if (in && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMax(btmax + b, m);
     }
+}
+
+__global__ void k_uniform_meta(int64_t me, int32_t thr, int64_t *__restrict__ boff, int32_t *__restrict__ btmax) {
+    boff[0] = 0;
+    boff[1] = me;
+    btmax[0] = thr;
+}
+
+// CSR offsets must be non-decreasing within [0, m2] (flag 64)
+__global__ void k_check_xadj(const int64_t *__restrict__ xadj, int64_t n, int64_t m2, unsigned *__restrict__ flags) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        if (xadj[v] < 0 || xadj[v + 1] > m2 || xadj[v + 1] < xadj[v]) atomicOr(flags, 64u);
 }
 
 // number of neighbours smaller than v = lower_bound(row v, v) - xadj[v]
 __global__ void k_max_prefix(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, int64_t n,
-                             unsigned long long *__restrict__ out) {
+                             int64_t m2, unsigned long long *__restrict__ out) {
     unsigned long long best = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         int64_t lo = xadj[v], hi = xadj[v + 1];
+        if (lo < 0 || hi > m2 || lo > hi) continue;     // corrupt offsets: flagged by k_check_xadj
         const int64_t s0 = lo;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
@@ -274,15 +347,6 @@ __global__ void k_max_prefix(const int64_t *__restrict__ xadj, const int32_t *__
     if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
 }
 
-__global__ void k_sum_thr(const int32_t *__restrict__ ET, int64_t me, unsigned long long *__restrict__ out) {
-    unsigned long long acc = 0;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < me;
-         e += (int64_t)gridDim.x * blockDim.x)
-        acc += (unsigned long long)(uint32_t)ET[e];
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
-}
-
 __global__ void k_murmur_pairs(const uint32_t *__restrict__ lo, const uint32_t *__restrict__ hi,
                                int64_t cnt, uint32_t *__restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
@@ -293,6 +357,26 @@ __global__ void k_murmur_pairs(const uint32_t *__restrict__ lo, const uint32_t *
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
+// IMX_GRAPH_PROFILE=1: host wall time of each graph-build phase (stream
+// synchronised at every mark, so the marks themselves add syncs)
+struct PhaseClock {
+    bool on = false;
+    std::chrono::steady_clock::time_point t;
+    void start() {
+        on = getenv("IMX_GRAPH_PROFILE") != nullptr;
+        t = std::chrono::steady_clock::now();
+    }
+    void mark(const char *what, cudaStream_t st) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[graph] %-22s %8.1f us\n", what,
+                std::chrono::duration<double, std::micro>(now - t).count());
+        t = now;
+    }
+};
+static PhaseClock g_clock;
+
 static int grid_for(int64_t work, int threads = 256) {
     int64_t b = ceil_div(work > 0 ? work : 1, threads);
     if (b > 148 * 32) b = 148 * 32;
@@ -316,89 +400,14 @@ void graph_free(imx_graph *g) {
     void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
                     g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff};
     for (void *p : ptrs) if (p) cudaFreeAsync(p, g->stream);
-    if (g->stream) {
-        cudaStreamSynchronize(g->stream);
-        cudaStreamDestroy(g->stream);
-    }
+    release_stream(g->dev, g->stream);
     delete g;
-}
-
-static int read_flags(imx_graph *g, unsigned *dflags, unsigned *out) {
-    IMX_CUDA(cudaMemcpyAsync(out, dflags, sizeof(unsigned), cudaMemcpyDeviceToHost, g->stream));
-    IMX_CUDA(cudaStreamSynchronize(g->stream));
-    return IMX_OK;
-}
-
-// Derived per-slot data: sources (if missing), reciprocal, hashes, thresholds,
-// canonical edge list.
-static int graph_finish(imx_graph *g) {
-    cudaStream_t st = g->stream;
-    const int64_t m2 = g->m2, n = g->n;
-    if (!g->src) {
-        IMX_TRY(dalloc(g, &g->src, m2));
-        if (m2) { k_src_from_xadj<<<grid_for(m2), 256, 0, st>>>(g->xadj, n, m2, g->src); IMX_CHECK_LAUNCH(); }
-    }
-    IMX_TRY(dalloc(g, &g->hash, m2));
-    IMX_TRY(dalloc(g, &g->thr, m2));
-    IMX_TRY(dalloc(g, &g->recip, m2));
-    unsigned *dflags;
-    IMX_CUDA(cudaMallocAsync((void **)&dflags, sizeof(unsigned), st));
-    IMX_CUDA(cudaMemsetAsync(dflags, 0, sizeof(unsigned), st));
-    if (m2) {
-        k_reciprocal<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, m2, g->recip, dflags); note_launch();
-        IMX_CHECK_LAUNCH();
-        k_slot_hashes<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, g->hash); note_launch();
-        IMX_CHECK_LAUNCH();
-    }
-    unsigned flags = 0;
-    IMX_TRY(read_flags(g, dflags, &flags));
-    g->symmetric = (flags & 8u) == 0 && (m2 % 2 == 0);
-    cudaFreeAsync(dflags, st);
-    if (m2) {
-        unsigned long long *dmax, hmax = 0;
-        IMX_CUDA(cudaMallocAsync((void **)&dmax, sizeof(unsigned long long), st));
-        IMX_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
-        k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, dmax); note_launch();
-        IMX_CHECK_LAUNCH();
-        IMX_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof hmax, cudaMemcpyDeviceToHost, st));
-        IMX_CUDA(cudaStreamSynchronize(st));
-        cudaFreeAsync(dmax, st);
-        g->max_prefix = (int64_t)hmax;
-    }
-    // canonical edge list
-    g->me = 0;
-    if (m2) {
-        uint8_t *flag;
-        int64_t *cslot, *dcount;
-        IMX_CUDA(cudaMallocAsync((void **)&flag, m2, st));
-        IMX_CUDA(pool_alloc((void **)&cslot, sizeof(int64_t) * m2, st));
-        IMX_CUDA(cudaMallocAsync((void **)&dcount, sizeof(int64_t), st));
-        k_canon_flags<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, flag); note_launch();
-        IMX_CHECK_LAUNCH();
-        size_t tmp_bytes = 0;
-        thrust::counting_iterator<int64_t> it(0);
-        IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flag, cslot, dcount, m2, st));
-        void *tmp;
-        IMX_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
-        IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flag, cslot, dcount, m2, st));
-        int64_t me = 0;
-        IMX_CUDA(cudaMemcpyAsync(&me, dcount, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        IMX_CUDA(cudaStreamSynchronize(st));
-        g->me = me;
-        IMX_TRY(dalloc(g, &g->E, me));
-        IMX_TRY(dalloc(g, &g->EH, me));
-        IMX_TRY(dalloc(g, &g->ET, me));
-        g->cslot = cslot;
-        cudaFreeAsync(tmp, st);
-        cudaFreeAsync(flag, st);
-        cudaFreeAsync(dcount, st);
-    }
-    return IMX_OK;
 }
 
 // Sort the undirected edges by (threshold bucket, hash) so the sampler can
 // enumerate the edges live in a lane as at most 31 hash intervals per bucket
 // (the reference's index sweep, propagation.py:104-163, on the device).
+// Stream-ordered, no host synchronisation.
 static int graph_build_index(imx_graph *g) {
     cudaStream_t st = g->stream;
     const int64_t me = g->me;
@@ -408,94 +417,164 @@ static int graph_build_index(imx_graph *g) {
     g->nb = nb;
     IMX_CUDA(pool_alloc((void **)&g->btmax, sizeof(int32_t) * nb, st));
     IMX_CUDA(pool_alloc((void **)&g->boff, sizeof(int64_t) * (nb + 1), st));
-    IMX_CUDA(cudaMemsetAsync(g->btmax, 0, sizeof(int32_t) * nb, st));
-    IMX_CUDA(cudaMemsetAsync(g->boff, 0, sizeof(int64_t) * (nb + 1), st));
-    if (me == 0) return IMX_OK;
-    uint32_t *k32 = nullptr, *k32b = nullptr, *v32 = nullptr, *v32b = nullptr;
+    if (me == 0) {
+        IMX_CUDA(cudaMemsetAsync(g->btmax, 0, sizeof(int32_t) * nb, st));
+        IMX_CUDA(cudaMemsetAsync(g->boff, 0, sizeof(int64_t) * (nb + 1), st));
+        return IMX_OK;
+    }
+    uint32_t *k32b = nullptr, *v32 = nullptr, *v32b = nullptr, *v32c = nullptr;
     uint64_t *k64 = nullptr, *k64b = nullptr;
     int2 *E0 = nullptr;
     int32_t *EH0 = nullptr, *ET0 = nullptr;
     void *tmp = nullptr;
-    size_t tb = 0, tb2 = 0;
+    size_t tb = 0;
     int rc = IMX_OK;
 #define GI(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { rc = cuda_fail(_e, #call, __FILE__, __LINE__); goto done; } } while (0)
-    GI(cudaMallocAsync((void **)&v32, sizeof(uint32_t) * me, st));
-    GI(cudaMallocAsync((void **)&v32b, sizeof(uint32_t) * me, st));
-    GI(cudaMallocAsync((void **)&k64, sizeof(uint64_t) * me, st));
-    GI(cudaMallocAsync((void **)&k64b, sizeof(uint64_t) * me, st));
-    GI(cub::DeviceRadixSort::SortPairs(nullptr, tb, k64, k64b, v32, v32b, me, 0, 64, st));
-    if (nb > 1) {
-        GI(cudaMallocAsync((void **)&k32, sizeof(uint32_t) * me, st));
-        GI(cudaMallocAsync((void **)&k32b, sizeof(uint32_t) * me, st));
-        GI(cub::DeviceRadixSort::SortPairs(nullptr, tb2, k32, k32b, v32, v32b, me, 0, 32, st));
-    }
-    GI(cudaMallocAsync(&tmp, std::max(tb, tb2), st));
-    if (nb > 1) {
-        k_iota_thr_keys<<<grid_for(me), 256, 0, st>>>(g->ET, me, k32, v32); note_launch();
+    GI(pool_alloc((void **)&E0, sizeof(int2) * me, st));
+    GI(pool_alloc((void **)&EH0, sizeof(int32_t) * me, st));
+    GI(pool_alloc((void **)&ET0, sizeof(int32_t) * me, st));
+    GI(pool_alloc((void **)&v32, sizeof(uint32_t) * me, st));
+    GI(pool_alloc((void **)&v32b, sizeof(uint32_t) * me, st));
+    GI(pool_alloc((void **)&k32b, sizeof(uint32_t) * me, st));
+    k_fill_edges<<<grid_for(me), 256, 0, st>>>(g->cslot, me, g->src, g->adj, g->hash, g->thr, E0, EH0, ET0, v32);
+    note_launch();
+    GI(cudaGetLastError());
+    g_clock.mark("index: alloc+fill", st);
+    if (nb == 1) {
+        // one bucket: the order is by hash alone (31-bit keys)
+        const uint32_t *hk = reinterpret_cast<const uint32_t *>(EH0);
+        GI(cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, k32b, v32, v32b, (int)me, 0, 31, st));
+        GI(pool_alloc(&tmp, tb, st));
+        GI(cub::DeviceRadixSort::SortPairs(tmp, tb, hk, k32b, v32, v32b, (int)me, 0, 31, st));
+        note_launch(4);
+        g_clock.mark("index: sort", st);
+        k_permute_edges<<<grid_for(me), 256, 0, st>>>(v32b, me, E0, EH0, ET0, g->E, g->EH, g->ET); note_launch();
         GI(cudaGetLastError());
-        GI(cub::DeviceRadixSort::SortPairs(tmp, tb2, k32, k32b, v32, v32b, me, 0, 32, st));
-        k_bucket_hash_keys<<<grid_for(me), 256, 0, st>>>(v32b, me, nb, g->EH, k64, v32); note_launch();
+        k_uniform_meta<<<1, 1, 0, st>>>(me, g->thr_u, g->boff, g->btmax); note_launch();
+        GI(cudaGetLastError());
     } else {
-        k_bucket_hash_keys<<<grid_for(me), 256, 0, st>>>(nullptr, me, 1, g->EH, k64, v32); note_launch();
-    }
-    GI(cudaGetLastError());
-    GI(cub::DeviceRadixSort::SortPairs(tmp, tb, k64, k64b, v32, v32b, me, 0, 40, st));
-    GI(cudaMallocAsync((void **)&E0, sizeof(int2) * me, st));
-    GI(cudaMallocAsync((void **)&EH0, sizeof(int32_t) * me, st));
-    GI(cudaMallocAsync((void **)&ET0, sizeof(int32_t) * me, st));
-    GI(cudaMemcpyAsync(E0, g->E, sizeof(int2) * me, cudaMemcpyDeviceToDevice, st));
-    GI(cudaMemcpyAsync(EH0, g->EH, sizeof(int32_t) * me, cudaMemcpyDeviceToDevice, st));
-    GI(cudaMemcpyAsync(ET0, g->ET, sizeof(int32_t) * me, cudaMemcpyDeviceToDevice, st));
-    k_permute_edges<<<grid_for(me), 256, 0, st>>>(v32b, me, E0, EH0, ET0, g->E, g->EH, g->ET); note_launch();
-    GI(cudaGetLastError());
-    k_bucket_meta<<<grid_for(me), 256, 0, st>>>(k64b, me, nb, g->ET, g->boff, g->btmax); note_launch();
-    GI(cudaGetLastError());
-    {
-        unsigned long long *dsum = reinterpret_cast<unsigned long long *>(k64);   // reuse scratch
-        GI(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long), st));
-        k_sum_thr<<<grid_for(me), 256, 0, st>>>(g->ET, me, dsum); note_launch();
-        unsigned long long hs = 0;
-        GI(cudaMemcpyAsync(&hs, dsum, sizeof hs, cudaMemcpyDeviceToHost, st));
-        GI(cudaStreamSynchronize(st));
-        g->thr_mean = (double)hs / (double)me / 2147483647.0;
+        size_t tb2 = 0;
+        GI(pool_alloc((void **)&k64, sizeof(uint64_t) * me, st));
+        GI(pool_alloc((void **)&k64b, sizeof(uint64_t) * me, st));
+        GI(pool_alloc((void **)&v32c, sizeof(uint32_t) * me, st));
+        const uint32_t *tk = reinterpret_cast<const uint32_t *>(ET0);
+        GI(cub::DeviceRadixSort::SortPairs(nullptr, tb, tk, k32b, v32, v32b, (int)me, 0, 32, st));
+        GI(cub::DeviceRadixSort::SortPairs(nullptr, tb2, k64, k64b, v32, v32c, (int)me, 0, 40, st));
+        GI(pool_alloc(&tmp, std::max(tb, tb2), st));
+        GI(cub::DeviceRadixSort::SortPairs(tmp, tb, tk, k32b, v32, v32b, (int)me, 0, 32, st));
+        g_clock.mark("index: thr sort", st);
+        k_bucket_hash_keys<<<grid_for(me), 256, 0, st>>>(v32b, me, nb, EH0, k64, v32); note_launch();
+        GI(cudaGetLastError());
+        GI(cub::DeviceRadixSort::SortPairs(tmp, tb2, k64, k64b, v32, v32c, (int)me, 0, 40, st));
+        note_launch(8);
+        g_clock.mark("index: bucket sort", st);
+        k_permute_edges<<<grid_for(me), 256, 0, st>>>(v32c, me, E0, EH0, ET0, g->E, g->EH, g->ET); note_launch();
+        GI(cudaGetLastError());
+        GI(cudaMemsetAsync(g->btmax, 0, sizeof(int32_t) * nb, st));
+        GI(cudaMemsetAsync(g->boff, 0, sizeof(int64_t) * (nb + 1), st));
+        k_bucket_meta<<<grid_for(me), 256, 0, st>>>(k64b, me, nb, g->ET, g->boff, g->btmax); note_launch();
+        GI(cudaGetLastError());
     }
 done:
-    for (void *p : {(void *)k32, (void *)k32b, (void *)v32, (void *)v32b, (void *)k64, (void *)k64b,
+    for (void *p : {(void *)k32b, (void *)v32, (void *)v32b, (void *)v32c, (void *)k64, (void *)k64b,
                     (void *)E0, (void *)EH0, (void *)ET0, tmp})
         if (p) cudaFreeAsync(p, st);
 #undef GI
     return rc;
 }
 
-// thresholds from current weights (symmetrized over reciprocal slots when the
-// graph is symmetric) and refresh the edge list's hash/thr columns
-static int graph_refresh_thresholds(imx_graph *g) {
+// Derived per-slot data and the sampler index, with ONE host round trip for
+// the statistics the host needs (symmetry, max prefix, canonical count,
+// threshold range and sum).  structure = build sources (if missing),
+// reciprocal slots, hashes and the canonical edge list (new CSR); otherwise
+// only the thresholds and the index are refreshed (new weights / hashes).
+static int graph_analyze(imx_graph *g, bool structure) {
     cudaStream_t st = g->stream;
-    const int64_t m2 = g->m2;
-    g->uniform = 1;
-    g->thr_u = 0;
+    const int64_t m2 = g->m2, n = g->n;
+    GStats *gs = nullptr;
+    IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
+    k_stats_init<<<1, 1, 0, st>>>(gs); note_launch();
+    if (structure) {
+        if (!g->src) {
+            IMX_TRY(dalloc(g, &g->src, m2));
+            if (m2) { k_src_from_xadj<<<grid_for(m2), 256, 0, st>>>(g->xadj, n, m2, g->src); note_launch(); }
+        }
+        IMX_TRY(dalloc(g, &g->hash, m2));
+        IMX_TRY(dalloc(g, &g->thr, m2));
+        IMX_TRY(dalloc(g, &g->recip, m2));
+        IMX_TRY(dalloc(g, &g->cslot, m2));
+        if (m2) {
+            k_reciprocal<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, n, m2, g->recip, &gs->flags);
+            k_slot_hashes<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, g->hash);
+            k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, m2, &gs->maxp);
+            k_check_xadj<<<grid_for(n), 256, 0, st>>>(g->xadj, n, m2, &gs->flags);
+            note_launch(4);
+            IMX_CHECK_LAUNCH();
+            uint8_t *flag;
+            IMX_CUDA(pool_alloc((void **)&flag, m2, st));
+            k_canon_flags<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, flag); note_launch();
+            size_t tmp_bytes = 0;
+            thrust::counting_iterator<int64_t> it(0);
+            IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flag, g->cslot, &gs->me, m2, st));
+            void *tmp;
+            IMX_CUDA(pool_alloc(&tmp, tmp_bytes, st));
+            IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flag, g->cslot, &gs->me, m2, st));
+            note_launch(2);
+            cudaFreeAsync(tmp, st);
+            cudaFreeAsync(flag, st);
+        }
+    }
+    // thresholds: symmetrized through the reciprocal slots unless the
+    // adjacency is known not to be symmetric (a structure pass decides below)
+    const bool sym_try = structure || g->symmetric;
     if (m2) {
-        int32_t *mm;
-        IMX_CUDA(cudaMallocAsync((void **)&mm, 2 * sizeof(int32_t), st));
-        int32_t init[2] = {INT32_MAX, INT32_MIN};
-        IMX_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
-        k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, g->symmetric ? g->recip : nullptr, m2,
-                                                   g->thr, mm, mm + 1); note_launch();
-        IMX_CHECK_LAUNCH();
-        int32_t res[2];
-        IMX_CUDA(cudaMemcpyAsync(res, mm, sizeof res, cudaMemcpyDeviceToHost, st));
-        IMX_CUDA(cudaStreamSynchronize(st));
-        cudaFreeAsync(mm, st);
-        g->uniform = res[0] == res[1];
-        g->thr_u = res[0];
-    }
-    if (g->me) {
-        k_fill_edges<<<grid_for(g->me), 256, 0, st>>>(g->cslot, g->me, g->src, g->adj, g->hash,
-                                                      g->thr, g->E, g->EH, g->ET); note_launch();
+        k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, sym_try ? g->recip : nullptr, g->src, g->adj, m2,
+                                                   g->thr, gs);
+        note_launch();
         IMX_CHECK_LAUNCH();
     }
+    GStats h;
+    IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
+    IMX_CUDA(cudaStreamSynchronize(st));
+    g_clock.mark("analysis (1 sync)", st);
+    if (structure) {
+        if (h.flags & 64u) {
+            cudaFreeAsync(gs, st);
+            set_error("corrupt CSR offsets");
+            return IMX_EINVAL;
+        }
+        if (h.flags & 32u) {
+            cudaFreeAsync(gs, st);
+            set_error("adjacency entry outside 0..n-1");
+            return IMX_EINVAL;
+        }
+        g->symmetric = (h.flags & 8u) == 0 && (m2 % 2 == 0);
+        g->max_prefix = (int64_t)h.maxp;
+        g->me = m2 ? h.me : 0;
+        if (g->me >= (int64_t(1) << 31)) {
+            cudaFreeAsync(gs, st);
+            set_error("%lld undirected edges exceed 2^31 - 1", (long long)g->me);
+            return IMX_ECONSTRAINT;
+        }
+        if (m2 && !g->symmetric) {        // rare: thresholds without symmetrization
+            k_stats_init<<<1, 1, 0, st>>>(gs);
+            k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, nullptr, g->src, g->adj, m2, g->thr, gs);
+            note_launch(2);
+            IMX_CHECK_LAUNCH();
+            IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
+            IMX_CUDA(cudaStreamSynchronize(st));
+        }
+        IMX_TRY(dalloc(g, &g->E, g->me));
+        IMX_TRY(dalloc(g, &g->EH, g->me));
+        IMX_TRY(dalloc(g, &g->ET, g->me));
+    }
+    cudaFreeAsync(gs, st);
+    g->uniform = m2 ? (h.tmin == h.tmax) : 1;
+    g->thr_u = m2 ? h.tmin : 0;
+    g->thr_mean = g->me ? (double)h.tsum / (double)g->me / 2147483647.0 : 0.0;
     IMX_TRY(graph_build_index(g));
     IMX_CUDA(cudaStreamSynchronize(st));
+    g_clock.mark("sampler index", st);
     return IMX_OK;
 }
 
@@ -505,7 +584,7 @@ static int graph_new(int32_t device, int64_t n, int64_t m2, imx_graph **out) {
     g->dev = device;
     g->n = n;
     g->m2 = m2;
-    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (acquire_stream(device, &g->stream) != cudaSuccess) {
         delete g;
         set_error("cudaStreamCreate failed");
         return IMX_ECUDA;
@@ -590,8 +669,7 @@ int graph_build_from_device_edges(imx_graph *g, const int64_t *dedges, int64_t k
     } else {
         IMX_CUDA(cudaMemsetAsync(g->xadj, 0, sizeof(int64_t) * (n + 1), st));
     }
-    IMX_TRY(graph_finish(g));
-    return graph_refresh_thresholds(g);
+    return graph_analyze(g, true);
 }
 
 int graph_create(int32_t device, int64_t n, int64_t m2, imx_graph **out) { return graph_new(device, n, m2, out); }
@@ -637,20 +715,21 @@ extern "C" int imx_graph_from_csr(int32_t device, int64_t n, int64_t m2, const i
     if (!out || !xadj || (m2 && (!adj || !weights))) { set_error("NULL argument"); return IMX_EINVAL; }
     *out = nullptr;
     if (n < 0 || n >= (int64_t(1) << 31)) { set_error("vertex count %lld outside [0, 2^31)", (long long)n); return IMX_ECONSTRAINT; }
+    g_clock.start();
+    // offsets are checked on the device (k_check_xadj) before anything uses them
     if (xadj[0] != 0 || xadj[n] != m2) { set_error("corrupt CSR offsets"); return IMX_EINVAL; }
-    for (int64_t v = 0; v < n; ++v)
-        if (xadj[v + 1] < xadj[v]) { set_error("corrupt CSR offsets"); return IMX_EINVAL; }
     imx_graph *g;
     IMX_TRY(graph_new(device, n, m2, &g));
     cudaStream_t st = g->stream;
+    g_clock.mark("validate+stream", st);
     auto fail = [&](int code) { graph_free(g); return code; };
     if (dalloc(g, &g->xadj, n + 1) || dalloc(g, &g->adj, m2) || dalloc(g, &g->w, m2)) return fail(IMX_ENOMEM);
     if (cudaMemcpyAsync(g->xadj, xadj, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st) != cudaSuccess ||
         (m2 && cudaMemcpyAsync(g->adj, adj, sizeof(int32_t) * m2, cudaMemcpyHostToDevice, st) != cudaSuccess) ||
         (m2 && cudaMemcpyAsync(g->w, weights, sizeof(double) * m2, cudaMemcpyHostToDevice, st) != cudaSuccess))
         return fail(cuda_fail(cudaGetLastError(), "upload csr", __FILE__, __LINE__));
-    int rc = graph_finish(g);
-    if (rc == IMX_OK) rc = graph_refresh_thresholds(g);
+    g_clock.mark("upload csr", st);
+    int rc = graph_analyze(g, true);
     if (rc != IMX_OK) return fail(rc);
     *out = g;
     return IMX_OK;
@@ -701,7 +780,8 @@ extern "C" int imx_graph_set_weights(imx_graph *g, const double *weights) {
         k_weights_range<<<grid_for(g->m2), 256, 0, st>>>(tmp, g->m2, dflags); note_launch();
         IMX_CHECK_LAUNCH();
         unsigned flags = 0;
-        IMX_TRY(read_flags(g, dflags, &flags));
+        IMX_CUDA(cudaMemcpyAsync(&flags, dflags, sizeof flags, cudaMemcpyDeviceToHost, st));
+        IMX_CUDA(cudaStreamSynchronize(st));
         cudaFreeAsync(dflags, st);
         if (flags & 16u) {
             cudaFreeAsync(tmp, st);
@@ -711,7 +791,7 @@ extern "C" int imx_graph_set_weights(imx_graph *g, const double *weights) {
         IMX_CUDA(cudaMemcpyAsync(g->w, tmp, sizeof(double) * g->m2, cudaMemcpyDeviceToDevice, st));
         cudaFreeAsync(tmp, st);
     }
-    return graph_refresh_thresholds(g);
+    return graph_analyze(g, false);
 }
 
 extern "C" int imx_graph_hashes(imx_graph *g, int32_t *out) {
@@ -735,7 +815,7 @@ extern "C" int imx_graph_set_hashes(imx_graph *g, const int32_t *hashes) {
             IMX_CHECK_LAUNCH();
         }
     }
-    return graph_refresh_thresholds(g);
+    return graph_analyze(g, false);
 }
 
 extern "C" int imx_graph_thresholds(imx_graph *g, int32_t symmetrize, int32_t *thr_out,
@@ -748,16 +828,17 @@ extern "C" int imx_graph_thresholds(imx_graph *g, int32_t symmetrize, int32_t *t
         if (symmetrize) {
             IMX_CUDA(cudaMemcpyAsync(thr_out, g->thr, sizeof(int32_t) * g->m2, cudaMemcpyDeviceToHost, st));
         } else {
-            int32_t *tmp, *mm;
-            IMX_CUDA(cudaMallocAsync((void **)&tmp, sizeof(int32_t) * g->m2, st));
-            IMX_CUDA(cudaMallocAsync((void **)&mm, 2 * sizeof(int32_t), st));
-            int32_t init[2] = {INT32_MAX, INT32_MIN};
-            IMX_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
-            k_thresholds<<<grid_for(g->m2), 256, 0, st>>>(g->w, nullptr, g->m2, tmp, mm, mm + 1); note_launch();
+            int32_t *tmp;
+            GStats *gs;
+            IMX_CUDA(pool_alloc((void **)&tmp, sizeof(int32_t) * g->m2, st));
+            IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
+            k_stats_init<<<1, 1, 0, st>>>(gs);
+            k_thresholds<<<grid_for(g->m2), 256, 0, st>>>(g->w, nullptr, g->src, g->adj, g->m2, tmp, gs);
+            note_launch(2);
             IMX_CHECK_LAUNCH();
             IMX_CUDA(cudaMemcpyAsync(thr_out, tmp, sizeof(int32_t) * g->m2, cudaMemcpyDeviceToHost, st));
             cudaFreeAsync(tmp, st);
-            cudaFreeAsync(mm, st);
+            cudaFreeAsync(gs, st);
         }
         IMX_CUDA(cudaStreamSynchronize(st));
     }

@@ -105,7 +105,7 @@ int run_init(imx_ctx *c);
 // raw label-matrix passes shared with the evaluation worlds (evaluation.cu)
 int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
-                    cudaStream_t st);
+                    cudaStream_t st, int *launches = nullptr);
 
 }  // namespace imx
 

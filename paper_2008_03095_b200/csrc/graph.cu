@@ -206,9 +206,11 @@ __global__ void k_stats_init(GStats *gs) {
 // their range over all slots and their sum over the canonical slots
 __global__ void k_thresholds(const double *__restrict__ w, const int64_t *__restrict__ recip,
                              const int32_t *__restrict__ src, const int32_t *__restrict__ adj,
-                             int64_t m2, int32_t *__restrict__ thr, GStats *__restrict__ gs) {
+                             const int32_t *__restrict__ hash, int64_t m2, int32_t *__restrict__ thr,
+                             GStats *__restrict__ gs) {
     int32_t lmin = INT32_MAX, lmax = INT32_MIN;
     unsigned long long lsum = 0;
+    bool neg = false;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
          s += (int64_t)gridDim.x * blockDim.x) {
         int32_t t = thr_of(w[s]);
@@ -219,7 +221,9 @@ __global__ void k_thresholds(const double *__restrict__ w, const int64_t *__rest
         thr[s] = t;
         lmin = min(lmin, t); lmax = max(lmax, t);
         if (src[s] < adj[s]) lsum += (unsigned long long)(uint32_t)t;
+        if (hash && hash[s] < 0) neg = true;     // a caller's table outside 31 bits
     }
+    if (__any_sync(0xffffffffu, neg) && (threadIdx.x & 31) == 0) atomicOr(&gs->flags, 128u);
     for (int o = 16; o; o >>= 1) {
         lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
         lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
@@ -317,6 +321,25 @@ __global__ void k_uniform_meta(int64_t me, int32_t thr, int64_t *__restrict__ bo
     btmax[0] = thr;
 }
 
+// lut[b][k] = lower_bound of (k << shift) among bucket b's sorted hashes
+__global__ void k_build_lut(const int32_t *__restrict__ EH, const int64_t *__restrict__ boff, int nb, int bits,
+                            int32_t *__restrict__ lut) {
+    const int64_t per = ((int64_t)1 << bits) + 1;
+    const int shift = 31 - bits;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb * per;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(i / per);
+        const int64_t k = i - b * per;
+        const uint64_t key = (uint64_t)k << shift;
+        int64_t lo = boff[b], hi = boff[b + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((uint64_t)(uint32_t)EH[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        lut[i] = (int32_t)lo;
+    }
+}
+
 // CSR offsets must be non-decreasing within [0, m2] (flag 64)
 __global__ void k_check_xadj(const int64_t *__restrict__ xadj, int64_t n, int64_t m2, unsigned *__restrict__ flags) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
@@ -398,7 +421,7 @@ void graph_free(imx_graph *g) {
     if (!g) return;
     cudaSetDevice(g->dev);
     void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
-                    g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff};
+                    g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff, g->lut};
     for (void *p : ptrs) if (p) cudaFreeAsync(p, g->stream);
     release_stream(g->dev, g->stream);
     delete g;
@@ -414,12 +437,19 @@ static int graph_build_index(imx_graph *g) {
     const int nb = g->uniform ? 1 : (int)std::min<int64_t>(64, std::max<int64_t>(1, me));
     if (g->btmax) { cudaFreeAsync(g->btmax, st); g->btmax = nullptr; }
     if (g->boff) { cudaFreeAsync(g->boff, st); g->boff = nullptr; }
+    if (g->lut) { cudaFreeAsync(g->lut, st); g->lut = nullptr; }
     g->nb = nb;
+    int bits = 6;
+    while (bits < 16 && ((int64_t)1 << (bits + 1)) <= me / nb) ++bits;
+    g->lut_bits = bits;
+    const int64_t lut_n = (int64_t)nb * (((int64_t)1 << bits) + 1);
     IMX_CUDA(pool_alloc((void **)&g->btmax, sizeof(int32_t) * nb, st));
     IMX_CUDA(pool_alloc((void **)&g->boff, sizeof(int64_t) * (nb + 1), st));
+    IMX_CUDA(pool_alloc((void **)&g->lut, sizeof(int32_t) * lut_n, st));
     if (me == 0) {
         IMX_CUDA(cudaMemsetAsync(g->btmax, 0, sizeof(int32_t) * nb, st));
         IMX_CUDA(cudaMemsetAsync(g->boff, 0, sizeof(int64_t) * (nb + 1), st));
+        IMX_CUDA(cudaMemsetAsync(g->lut, 0, sizeof(int32_t) * lut_n, st));
         return IMX_OK;
     }
     uint32_t *k32b = nullptr, *v32 = nullptr, *v32b = nullptr, *v32c = nullptr;
@@ -475,6 +505,8 @@ static int graph_build_index(imx_graph *g) {
         k_bucket_meta<<<grid_for(me), 256, 0, st>>>(k64b, me, nb, g->ET, g->boff, g->btmax); note_launch();
         GI(cudaGetLastError());
     }
+    k_build_lut<<<grid_for(lut_n), 256, 0, st>>>(g->EH, g->boff, nb, bits, g->lut); note_launch();
+    GI(cudaGetLastError());
 done:
     for (void *p : {(void *)k32b, (void *)v32, (void *)v32b, (void *)v32c, (void *)k64, (void *)k64b,
                     (void *)E0, (void *)EH0, (void *)ET0, tmp})
@@ -528,8 +560,8 @@ static int graph_analyze(imx_graph *g, bool structure) {
     // adjacency is known not to be symmetric (a structure pass decides below)
     const bool sym_try = structure || g->symmetric;
     if (m2) {
-        k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, sym_try ? g->recip : nullptr, g->src, g->adj, m2,
-                                                   g->thr, gs);
+        k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, sym_try ? g->recip : nullptr, g->src, g->adj, g->hash,
+                                                   m2, g->thr, gs);
         note_launch();
         IMX_CHECK_LAUNCH();
     }
@@ -558,7 +590,7 @@ static int graph_analyze(imx_graph *g, bool structure) {
         }
         if (m2 && !g->symmetric) {        // rare: thresholds without symmetrization
             k_stats_init<<<1, 1, 0, st>>>(gs);
-            k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, nullptr, g->src, g->adj, m2, g->thr, gs);
+            k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, nullptr, g->src, g->adj, g->hash, m2, g->thr, gs);
             note_launch(2);
             IMX_CHECK_LAUNCH();
             IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -569,6 +601,7 @@ static int graph_analyze(imx_graph *g, bool structure) {
         IMX_TRY(dalloc(g, &g->ET, g->me));
     }
     cudaFreeAsync(gs, st);
+    g->hash_neg = (h.flags & 128u) != 0;
     g->uniform = m2 ? (h.tmin == h.tmax) : 1;
     g->thr_u = m2 ? h.tmin : 0;
     g->thr_mean = g->me ? (double)h.tsum / (double)g->me / 2147483647.0 : 0.0;
@@ -833,7 +866,7 @@ extern "C" int imx_graph_thresholds(imx_graph *g, int32_t symmetrize, int32_t *t
             IMX_CUDA(pool_alloc((void **)&tmp, sizeof(int32_t) * g->m2, st));
             IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
             k_stats_init<<<1, 1, 0, st>>>(gs);
-            k_thresholds<<<grid_for(g->m2), 256, 0, st>>>(g->w, nullptr, g->src, g->adj, g->m2, tmp, gs);
+            k_thresholds<<<grid_for(g->m2), 256, 0, st>>>(g->w, nullptr, g->src, g->adj, nullptr, g->m2, tmp, gs);
             note_launch(2);
             IMX_CHECK_LAUNCH();
             IMX_CUDA(cudaMemcpyAsync(thr_out, tmp, sizeof(int32_t) * g->m2, cudaMemcpyDeviceToHost, st));

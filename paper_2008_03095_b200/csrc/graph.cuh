@@ -26,10 +26,16 @@ struct imx_graph {
     int nb = 1;              // threshold buckets
     int32_t *btmax = nullptr;// [nb]  max threshold of each bucket
     int64_t *boff = nullptr; // [nb+1] bucket offsets into E/EH/ET
+    // hash-prefix lookup: lut[b*(2^lut_bits+1) + k] = first edge of bucket b
+    // whose hash >> (31 - lut_bits) >= k, so a lower_bound over a bucket is
+    // one lookup + a short binary search
+    int32_t *lut = nullptr;
+    int lut_bits = 0;
     int32_t thr_u = 0;       // the threshold when uniform
     int64_t max_prefix = 0;  // max over v of #neighbours smaller than v
     double thr_mean = 0;     // mean canonical-edge threshold / H_MAX = mean live fraction
     int uniform = 1;         // all thresholds equal
+    int hash_neg = 0;        // some hash has bit 31 set (caller table): no interval enumeration
     int symmetric = 1;
 };
 

@@ -139,10 +139,25 @@ __global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict
 // per-edge thresholds a bucket's interval uses the bucket's max threshold
 // and each enumerated edge is re-tested exactly ((x ^ h) < thr, strict).
 // ---------------------------------------------------------------------------
+// lower_bound of key (< 2^32) among bucket b's sorted hashes via the prefix LUT
+__device__ __forceinline__ int64_t hash_lower_bound(const int32_t *__restrict__ EH, const int32_t *__restrict__ lut,
+                                                    int bits, const int64_t *__restrict__ boff, int b,
+                                                    uint64_t key) {
+    if (key >= (1ull << 31)) return boff[b + 1];
+    const int64_t per = ((int64_t)1 << bits) + 1;
+    const int64_t k = (int64_t)(key >> (31 - bits));
+    int64_t lo = lut[b * per + k], hi = lut[b * per + k + 1];
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint64_t)(uint32_t)EH[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
                             const int32_t *__restrict__ btmax, const int64_t *__restrict__ boff,
-                            const int32_t *__restrict__ EH, int64_t *__restrict__ seg_a,
-                            int64_t *__restrict__ seg_n) {
+                            const int32_t *__restrict__ EH, const int32_t *__restrict__ lut, int bits,
+                            int64_t *__restrict__ seg_a, int64_t *__restrict__ seg_n) {
     const int64_t nseg = (int64_t)W * nb * 31;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
          s += (int64_t)gridDim.x * blockDim.x) {
@@ -155,18 +170,8 @@ __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
             const uint32_t x = (uint32_t)X[r];
             const uint64_t start = ((uint64_t)((t ^ x) >> (i + 1)) << (i + 1)) | (uint64_t)(x & (1u << i));
             const uint64_t end = start + (1ull << i);
-            int64_t lo = boff[b], hi = boff[b + 1];
-            while (lo < hi) {  // lower_bound(start)
-                const int64_t mid = (lo + hi) >> 1;
-                if ((uint64_t)(uint32_t)EH[mid] < start) lo = mid + 1; else hi = mid;
-            }
-            a = lo;
-            hi = boff[b + 1];
-            while (lo < hi) {  // lower_bound(end)
-                const int64_t mid = (lo + hi) >> 1;
-                if ((uint64_t)(uint32_t)EH[mid] < end) lo = mid + 1; else hi = mid;
-            }
-            cnt = lo - a;
+            a = hash_lower_bound(EH, lut, bits, boff, b, start);
+            cnt = hash_lower_bound(EH, lut, bits, boff, b, end) - a;
         }
         seg_a[s] = a;
         seg_n[s] = cnt;
@@ -354,8 +359,8 @@ __device__ __forceinline__ int hub_slot(int r, int r0, int64_t ld) {
     return ld >= 128 ? (int)(((int64_t)r - r0 + ld) % ld) : r;
 }
 
-__device__ __forceinline__ void compress_cell(uint32_t *__restrict__ L, int64_t ld, uint32_t v, uint32_t w,
-                                              uint32_t gw, int r, int r0, uint32_t *hc) {
+__device__ __forceinline__ void compress_cell(uint32_t *__restrict__ L, int64_t ld, int64_t lw, uint32_t v,
+                                              uint32_t w, uint32_t gw, int r, int r0, uint32_t *hc) {
     uint32_t x = v, p = w;
     while (!is_root(gw)) {          // path splitting, min-safe
         atomicMin(cell(L, ld, x, r), gw);
@@ -364,7 +369,7 @@ __device__ __forceinline__ void compress_cell(uint32_t *__restrict__ L, int64_t 
         gw = p < (uint32_t)kHot ? ld_ca(cell(L, ld, p, r)) : ld_relaxed(cell(L, ld, p, r));
     }
     if (p != w) L[(int64_t)v * ld + r] = p;
-    if (p < (uint32_t)kHot) atomicAdd(hc + p * 128 + hub_slot(r, r0, ld), 1u);
+    if (p < (uint32_t)kHot) atomicAdd(hc + p * 128 + hub_slot(r, r0, lw), 1u);
     else atomicAdd(cell(L, ld, p, r), 1u);
 }
 
@@ -372,16 +377,18 @@ __device__ __forceinline__ void compress_cell(uint32_t *__restrict__ L, int64_t 
 // quads (128 lanes) of two rows per step; the non-root cells of the step are
 // compacted into a per-warp shared-memory queue and walked 32 at a time, so
 // the walks (and their dependent loads) run warp-wide instead of diverging.
-constexpr int kCQ = 32 + 256;
+constexpr int kCRows = 2;                // label rows per thread per step
+constexpr int kCQ = 32 + 32 * 4 * kCRows;  // drain threshold + one step's worth of appends
 __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
-                                                  int64_t vstep, unsigned long long *__restrict__ nonroot) {
+                                                  int64_t nq, int64_t vstep,
+                                                  unsigned long long *__restrict__ nonroot) {
     __shared__ uint32_t qv[8][kCQ], qw[8][kCQ], qr[8][kCQ];
     __shared__ uint32_t hcs[8][kHot * 128];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t *hc = hcs[warp];
     for (int i = lane; i < kHot * 128; i += 32) hc[i] = 0;
     __syncwarp();
-    const int64_t nq = ld >> 2;
+    const int64_t lw = nq << 2;     // lanes per row of this pass (a window of the row)
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t q = t % nq;
     const int r = (int)(q << 2);
@@ -391,15 +398,18 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
     int qn = 0;
     const bool live = t < vstep * nq;
     // every lane of the warp walks the same v sequence (vstep is a multiple of rows)
-    for (int64_t v = live ? t / nq : n; __any_sync(FULL, v < n); v += 2 * vstep) {
-        const int64_t v2 = v + vstep;
-        uint4 l1 = make_uint4(ROOT, ROOT, ROOT, ROOT), l2 = l1;
-        if (v < n) l1 = *(reinterpret_cast<const uint4 *>(L + v * ld) + q);
-        if (v2 < n) l2 = *(reinterpret_cast<const uint4 *>(L + v2 * ld) + q);
-        const uint32_t w[8] = {l1.x, l1.y, l1.z, l1.w, l2.x, l2.y, l2.z, l2.w};
+    for (int64_t v = live ? t / nq : n; __any_sync(FULL, v < n); v += kCRows * vstep) {
+        uint32_t w[4 * kCRows];
+#pragma unroll
+        for (int i = 0; i < kCRows; ++i) {       // kCRows independent 16-byte row loads in flight
+            const int64_t vi = v + i * vstep;
+            uint4 l = make_uint4(ROOT, ROOT, ROOT, ROOT);
+            if (vi < n) l = *(reinterpret_cast<const uint4 *>(L + vi * ld) + q);
+            w[4 * i] = l.x; w[4 * i + 1] = l.y; w[4 * i + 2] = l.z; w[4 * i + 3] = l.w;
+        }
         unsigned m = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < 4 * kCRows; ++k)
             if (r + (k & 3) < W && !is_root(w[k])) m |= 1u << k;
         const int c = __popc(m);
         int inc = c;
@@ -409,13 +419,15 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
             if (lane >= o) inc += y;
         }
         int pos = qn + inc - c;
-        while (m) {
-            const int k = __ffs(m) - 1;
-            m &= m - 1;
-            qv[warp][pos] = (uint32_t)(k < 4 ? v : v2);
-            qw[warp][pos] = w[k];
-            qr[warp][pos] = (uint32_t)(r + (k & 3));
-            ++pos;
+        // compile-time cell index: the row words stay in registers
+#pragma unroll
+        for (int k = 0; k < 4 * kCRows; ++k) {
+            if ((m >> k) & 1u) {
+                qv[warp][pos] = (uint32_t)(v + (k >> 2) * vstep);
+                qw[warp][pos] = w[k];
+                qr[warp][pos] = (uint32_t)(r + (k & 3));
+                ++pos;
+            }
         }
         qn += __shfl_sync(FULL, inc, 31);
         cnt += c;
@@ -426,7 +438,7 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
             const int cr = (int)qr[warp][qn + lane];
             __syncwarp();
             const uint32_t gw = cw < (uint32_t)kHot ? ld_ca(cell(L, ld, cw, cr)) : ld_relaxed(cell(L, ld, cw, cr));
-            compress_cell(L, ld, cv, cw, gw, cr, r0, hc);
+            compress_cell(L, ld, lw, cv, cw, gw, cr, r0, hc);
         }
     }
     __syncwarp();
@@ -434,12 +446,12 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
         const uint32_t cv = qv[warp][lane], cw = qw[warp][lane];
         const int cr = (int)qr[warp][lane];
         const uint32_t gw = cw < (uint32_t)kHot ? ld_ca(cell(L, ld, cw, cr)) : ld_relaxed(cell(L, ld, cw, cr));
-        compress_cell(L, ld, cv, cw, gw, cr, r0, hc);
+        compress_cell(L, ld, lw, cv, cw, gw, cr, r0, hc);
     }
     __syncwarp();
     for (int i = lane; i < kHot * 128; i += 32) {
         if (!hc[i]) continue;
-        const int rr = ld >= 128 ? (int)((r0 + (i & 127)) % ld) : (i & 127);
+        const int rr = lw >= 128 ? (int)((r0 + (i & 127)) % lw) : (i & 127);
         atomicAdd(cell(L, ld, i >> 7, rr), hc[i]);
     }
     if (nonroot) {
@@ -556,8 +568,10 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest
             c->scan_tmp_bytes = tb;
         }
     }
-    k_seg_count<<<grid_for(nseg), 256, 0, c->st>>>(c->X, c->W, g->nb, g->btmax, g->boff, g->EH,
-                                                   c->seg_a, c->seg_n);
+    // one segment per thread: the two lookups per segment are latency-bound
+    const int sblocks = (int)std::min<int64_t>(ceil_div(nseg, 128), 148 * 64);
+    k_seg_count<<<sblocks, 128, 0, c->st>>>(c->X, c->W, g->nb, g->btmax, g->boff, g->EH, g->lut,
+                                            g->lut_bits, c->seg_a, c->seg_n);
     IMX_CHECK_LAUNCH();
     size_t tb = c->scan_tmp_bytes;
     IMX_CUDA(cub::DeviceScan::ExclusiveSum(c->scan_tmp, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
@@ -597,6 +611,8 @@ enum { HOOK_ENUM = 0, HOOK_PULL = 1, HOOK_DENSE = 2, HOOK_HYBRID = 3 };
 static int hook_mode(const imx_graph *g) {
     const char *m = getenv("IMX_HOOK");
     if (m && !strcmp(m, "dense")) return HOOK_DENSE;
+    // enumeration assumes 31-bit hashes ((x ^ h) >= 0); the scans test exactly
+    if (g->hash_neg) return HOOK_PULL;
     if (m && !strcmp(m, "enum")) return HOOK_ENUM;
     if (m && !strcmp(m, "pull")) return HOOK_PULL;
     if (m && !strcmp(m, "hybrid")) return HOOK_HYBRID;
@@ -626,28 +642,45 @@ static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_in
     return IMX_OK;
 }
 
+// Lanes per compress pass: the whole row, or (IMX_COMPRESS_WINDOW / large
+// label matrices) windows of lanes whose n*window*4 bytes stay L2-resident,
+// so the dependent parent reads and root-count atomics hit L2.
+static int64_t compress_window(int64_t n, int64_t ld) {
+    if (const char *e = getenv("IMX_COMPRESS_WINDOW")) {
+        const int64_t w = atoll(e);
+        if (w > 0) return std::min<int64_t>(ld, std::max<int64_t>(4, w / 4 * 4));
+    }
+    return ld;
+}
+
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
-                    cudaStream_t st) {
+                    cudaStream_t st, int *launches) {
     if (n == 0) return IMX_OK;
-    // grid stride = a whole number of rows, so every thread keeps its quad
-    const int64_t nq = ld >> 2;
-    const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * 2);
-    const int64_t rows = std::max<int64_t>(1, want / nq);
-    const int64_t threads = rows * nq;
-    const int blocks = (int)ceil_div(threads, 256);
-    // threads beyond rows*nq would break the fixed-quad mapping: size the
-    // stride from the launched thread count, rounded down to whole rows
-    const int64_t vstep = ((int64_t)blocks * 256) / nq;
-    k_compress<<<blocks, 256, 0, st>>>(L, n, ld, W, vstep, nonroot);
-    IMX_CHECK_LAUNCH();
-    note_launch();
+    const int64_t win = compress_window(n, ld);
+    if (launches) *launches = (int)ceil_div(W, win);
+    for (int64_t l0 = 0; l0 < W; l0 += win) {
+        const int32_t wl = (int32_t)std::min<int64_t>(win, W - l0);
+        // grid stride = a whole number of rows, so every thread keeps its quad
+        const int64_t nq = (wl + 3) >> 2;
+        const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * 2);
+        const int64_t rows = std::max<int64_t>(1, want / nq);
+        const int64_t threads = rows * nq;
+        const int blocks = (int)ceil_div(threads, 256);
+        // threads beyond rows*nq would break the fixed-quad mapping: size the
+        // stride from the launched thread count, rounded down to whole rows
+        const int64_t vstep = ((int64_t)blocks * 256) / nq;
+        k_compress<<<blocks, 256, 0, st>>>(L + l0, n, ld, wl, nq, vstep, nonroot);
+        IMX_CHECK_LAUNCH();
+        note_launch();
+    }
     return IMX_OK;
 }
 
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     if (c->g->n == 0) return IMX_OK;
-    IMX_TRY(launch_compress(c->L, c->g->n, c->ld, c->W, nonroot, c->st));
-    c->tm.kernel_launches++;
+    int k = 0;
+    IMX_TRY(launch_compress(c->L, c->g->n, c->ld, c->W, nonroot, c->st, &k));
+    c->tm.kernel_launches += k;
     return IMX_OK;
 }
 

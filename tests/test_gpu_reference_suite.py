@@ -516,3 +516,21 @@ def test_criterion_6_determinism_of_seeded_runs(gpu):
     assert a.seeds == b.seeds and a.selection.sigma == b.selection.sigma
     assert np.array_equal(a.labels, b.labels)
     assert np.array_equal(a.selection.trace.array, b.selection.trace.array)
+
+
+@pytest.mark.parametrize("mode", [None, "enum", "dense"])
+def test_caller_table_with_bit31_hashes_propagates_exactly(gpu, orc, mode, monkeypatch):
+    # a caller-built EdgeHashTable may hold negative words: (X ^ h) is then
+    # negative and always below thr (hashing.py:141-150); the device must not
+    # use interval enumeration for such a table
+    if mode:
+        monkeypatch.setenv("IMX_HOOK", mode)
+    g = weighted_er(gpu, 400, 6, "uniform:0.02,0.3", graph_seed=3, weight_seed=4)
+    h = gpu.build_hash_table(g).hashes.copy()
+    h[h % 7 == 0] |= np.int32(-2**31)          # reciprocal slots keep equal values
+    table = gpu.EdgeHashTable(h)
+    randoms = gpu.SimulationRandoms(40, master_seed=6)
+    labels = gpu.propagate(g, table, randoms)
+    thr = orc.thresholds(g.weights, orc.reciprocal(g.xadj, g.adj))
+    want = orc.propagate(g.xadj, g.adj, h, thr, randoms.values, nthreads=4)[0]
+    assert np.array_equal(labels, want)

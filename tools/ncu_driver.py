@@ -10,9 +10,10 @@ from paper_2008_03095_b200.context import DeviceContext
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 c = configs.CONFIGS[cfg]
+R = int(sys.argv[3]) if len(sys.argv) > 3 else c.R     # lane override (smaller label matrix for ncu)
 g = configs.build(cfg)
-X = imx.SimulationRandoms(c.R, 0).values
-ctx = DeviceContext(g, X, c.R)
+X = imx.SimulationRandoms(R, 0).values
+ctx = DeviceContext(g, X, R)
 res = ctx.bench_propagate(reps, flush_l2=True)
 ctx.memoize(want_gains=False)
 print(cfg, res)

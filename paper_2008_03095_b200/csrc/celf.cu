@@ -295,10 +295,51 @@ __device__ __forceinline__ int64_t warp_count_above(const unsigned long long *a,
     return lo + __popc(__ballot_sync(0xffffffffu, in));
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// marginal gain of u (u < 0: none) by a group of gsz threads (tid in the
+// group); per-warp partial sums meet in the group's shared accumulator.
+// Every thread of the CTA must call it (it has a CTA barrier).
+template <bool ENC>
+__device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
+                                              const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
+                                              int32_t cw, int64_t u, int tid, int gsz,
+                                              unsigned long long *acc_sh) {
+    unsigned long long acc = 0;
+    if (u >= 0) {
+        const int nqs = (ns + 3) >> 2;
+        const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
+        for (int q = tid; q < nqs; q += gsz) {
+            const uint4 l4 = row[q];
+            const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            uint32_t wd[4], sz[4];
+            const int r = q << 2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool in = r + j < ns;
+                uint32_t lab = 0;
+                sz[j] = in ? cell_size<ENC>(L, C, ld, (uint32_t)u, lv[j], r + j, lab) : 0u;
+                wd[j] = in ? cov[(int64_t)lab * cw + ((r + j) >> 5)] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (!((wd[j] >> ((r + j) & 31)) & 1u)) acc += sz[j];
+        }
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(acc_sh, acc);
+    __syncthreads();
+    return (int64_t)*acc_sh;
 }
 
 __device__ __forceinline__ unsigned long long block_max(unsigned long long x, unsigned long long *red) {
@@ -315,7 +356,7 @@ __device__ __forceinline__ unsigned long long block_max(unsigned long long x, un
 }
 
 template <bool ENC>
-__global__ void __launch_bounds__(256) k_celf_rounds(
+__global__ void __launch_bounds__(256, 4) k_celf_rounds(
     int32_t k, int vb, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, uint32_t *__restrict__ cov,
     int64_t ld, int32_t ns, int32_t cw, int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
     int32_t *oid0, int32_t *oid1, unsigned long long *okey0, unsigned long long *okey1,
@@ -323,10 +364,13 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
     unsigned long long *__restrict__ skey, int32_t *__restrict__ sid,
     int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
-    int32_t bpct) {
+    int32_t bpct, int32_t ngroup) {
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned long long red[8];
     __shared__ unsigned long long sback[kSmemBack];
+    __shared__ unsigned long long gacc[8];
+    if (threadIdx.x < 8) gacc[threadIdx.x] = 0;
+    __syncthreads();
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
     const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
@@ -334,8 +378,12 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
     int ocur = st->ocur;
     int32_t t = st->t;
     int32_t status = 0;
+    int32_t sstep = 0;                          // evaluation steps so far (uniform)
     const bool prof = gtid == 0;
-    unsigned long long pf[6] = {0, 0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
+    __shared__ unsigned long long pf[10];       // phase clock of block 0 (IMX_CELF_PROFILE)
+    if (threadIdx.x < 10) pf[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long tp = prof ? gtimer() : 0, ts = 0;
 #define PROF_MARK(i)                                 \
     if (prof) {                                      \
         const unsigned long long _t = gtimer();      \
@@ -357,21 +405,34 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
             int64_t lo = 0, hi = olen < batch0 ? olen : batch0;
             bestkey = 0;
             for (;;) {
-                for (int64_t i = lo + blockIdx.x; i < hi; i += gridDim.x) {
-                    const int64_t f = block_eval<ENC>(L, C, cov, ld, ns, cw, oid[ostart + i], red);
-                    if (threadIdx.x == 0) fresh[i] = f;
+                if (prof) ts = gtimer();
+                // slot (sstep+2)&3 was last read before the previous barrier
+                if (gtid == 0) st->smax[(sstep + 2) & 3] = 0;
+                // ngroup candidates per CTA at a time, 256/ngroup threads each
+                for (int64_t base = lo + (int64_t)blockIdx.x * ngroup; base < hi;
+                     base += (int64_t)gridDim.x * ngroup) {
+                    const int gsz = blockDim.x / ngroup, g = threadIdx.x / gsz;
+                    const int64_t i = base + g;
+                    const int64_t f = group_eval<ENC>(L, C, cov, ld, ns, cw, i < hi ? (int64_t)oid[ostart + i] : -1,
+                                                      threadIdx.x - g * gsz, gsz, gacc + g);
+                    if (threadIdx.x == g * gsz && i < hi) {
+                        fresh[i] = f;
+                        atomicMax(&st->smax[sstep & 3], ((unsigned long long)f << vb) |
+                                                        (unsigned long long)(vmask - (uint32_t)oid[ostart + i]));
+                    }
+                    __syncthreads();
+                    if (threadIdx.x < ngroup) gacc[threadIdx.x] = 0;
+                    __syncthreads();
                 }
+                if (prof) { const unsigned long long x = gtimer(); pf[6] += x - ts; ts = x; }
                 grid.sync();
-                if (prof) { pf[4]++; pf[5] += hi - lo; }
-                unsigned long long m = 0;
-                for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-                    const unsigned long long fk = ((unsigned long long)fresh[i] << vb) |
-                                                  (unsigned long long)(vmask - (uint32_t)oid[ostart + i]);
-                    m = fk > m ? fk : m;
-                }
-                m = block_max(m, red);
+                if (prof) { const unsigned long long x = gtimer(); pf[7] += x - ts; ts = x; pf[4]++; pf[5] += hi - lo; }
+                const unsigned long long m = ld_relaxed64(&st->smax[sstep & 3]);
+                ++sstep;
                 bestkey = m > bestkey ? m : bestkey;
-                if (hi >= olen || bestkey >= okey[ostart + hi]) break;   // nothing unevaluated can win
+                const bool stop = hi >= olen || bestkey >= okey[ostart + hi];   // nothing unevaluated can win
+                if (prof) pf[8] += gtimer() - ts;
+                if (stop) break;
                 lo = hi;
                 const int64_t step = batch0 > hi ? batch0 : hi;
                 hi = (olen - hi < step) ? olen : hi + step;
@@ -385,15 +446,34 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
         const int64_t nrec = (t == 0 ? 0 : kr) + 1;
         if (T + nrec > trace_cap) { status = 2; break; }    // host drains the trace, relaunches
         if (kr > kMaxRank) { status = 4; break; }           // host runs this round, relaunches
-        // phase 1: trace, refreshed vertices with their fresh keys, commit
+        // phase 1: trace records; the refreshed vertices ranked by their fresh
+        // keys (fresh[] / order ids of the evaluated prefix are complete since
+        // the last evaluation barrier) and scattered sorted; commit
+        const int64_t nback = t == 0 ? 0 : kr - 1;       // the winner is not re-inserted
+        const int lane = threadIdx.x & 31;
         if (t > 0) {
             for (int64_t i = gtid; i < kr; i += gthreads) {
                 const int32_t v = oid[ostart + i];
                 const int64_t f = fresh[i];
                 int64_t *rec = trace + 5 * (T + i);
                 rec[0] = v; rec[1] = (int64_t)(okey[ostart + i] >> vb); rec[2] = f; rec[3] = 0; rec[4] = t;
-                bkey[i] = v == best_v ? 0ull : (((unsigned long long)f << vb) | (unsigned long long)(vmask - (uint32_t)v));
-                bid[i] = v;
+            }
+            // one warp per refreshed key; its rank = #fresh keys above it minus
+            // the winner's (the unique maximum)
+            for (int64_t j = gtid >> 5; j < kr; j += gthreads >> 5) {
+                const int32_t vj = oid[ostart + j];
+                if (vj == best_v) continue;
+                const unsigned long long kj = ((unsigned long long)fresh[j] << vb) |
+                                              (unsigned long long)(vmask - (uint32_t)vj);
+                int64_t rk = 0;
+                for (int64_t i = lane; i < kr; i += 32) {
+                    const unsigned long long ki = ((unsigned long long)fresh[i] << vb) |
+                                                  (unsigned long long)(vmask - (uint32_t)oid[ostart + i]);
+                    rk += ki > kj;
+                }
+                for (int o = 16; o; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+                rk -= 1;
+                if (lane == 0) { skey[rk] = kj; sid[rk] = vj; }
             }
         }
         if (gtid == 0) {
@@ -417,28 +497,15 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
         }
         grid.sync();
         PROF_MARK(1);
-        // phase 2: self-check of the commit; rank + scatter the refreshed vertices
+        // phase 2: self-check of the commit, then merge order[kr, olen) with
+        // the sorted refreshed vertices
         const unsigned long long got = *gain;
         if ((int64_t)got != best_f) {
             if (gtid == 0) { st->bad_v = best_v; st->bad_want = best_f; st->bad_got = (int64_t)got; }
             status = 3;
             break;
         }
-        const int64_t nback = t == 0 ? 0 : kr - 1;       // the winner is not re-inserted
         if (nback > 0) {
-            // rank of each refreshed key among them: one warp per key, the
-            // comparisons spread over the lanes (coalesced 256-byte loads)
-            const int lane = threadIdx.x & 31;
-            for (int64_t j = gtid >> 5; j < kr; j += gthreads >> 5) {
-                const unsigned long long kj = bkey[j];
-                int64_t rk = 0;
-                for (int64_t i = lane; i < kr; i += 32) rk += bkey[i] > kj;
-                for (int o = 16; o; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
-                if (lane == 0 && rk < nback) { skey[rk] = kj; sid[rk] = bid[j]; }
-            }
-            grid.sync();
-            PROF_MARK(2);
-            // phase 3: merge order[kr, olen) with the sorted refreshed vertices
             int32_t *ob = ocur ? oid0 : oid1;
             unsigned long long *okb = ocur ? okey0 : okey1;
             const int64_t na = olen - kr;
@@ -483,7 +550,7 @@ __global__ void __launch_bounds__(256) k_celf_rounds(
     }
 #undef PROF_MARK
     if (gtid == 0) {
-        for (int i = 0; i < 6; ++i) st->prof[i] += pf[i];
+        for (int i = 0; i < 10; ++i) st->prof[i] += pf[i];
         st->ostart = ostart; st->olen = olen; st->ocur = ocur; st->t = t;
         st->trace_len = T; st->batch0 = batch0;
         st->status = status ? status : 1;
@@ -769,18 +836,24 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     int64_t cap = c->trace_cap;
     CelfDev *stp = c->cdev;
     // next round's first batch = bpct% of this round's refreshed prefix
-    int32_t bpct = 100;
+    int32_t bpct = 150;
     if (const char *b = getenv("IMX_CELF_BATCH_PCT")) bpct = std::max(1, atoi(b));
+    // candidates evaluated side by side per CTA (1, 2, 4 or 8)
+    int32_t ngroup = 1;
+    if (const char *gv = getenv("IMX_CELF_GROUPS")) ngroup = std::min(8, std::max(1, atoi(gv)));
+    while (ngroup & (ngroup - 1)) --ngroup;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
-                    &bkey, &bid, &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct};
+                    &bkey, &bid, &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup};
     IMX_CUDA(cudaLaunchCooperativeKernel(fn, grid_cache[enc], 256, args, 0, c->st));
     count_launch(c);
     IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
     if (getenv("IMX_CELF_PROFILE"))
         fprintf(stderr, "[celf] rounds %d..%d grid %d: eval %.1f us, commit %.1f us, rank %.1f us, merge %.1f us; "
-                "%llu eval steps, %llu evaluations\n", t, h.t, grid_cache[enc], h.prof[0] * 1e-3, h.prof[1] * 1e-3,
-                h.prof[2] * 1e-3, h.prof[3] * 1e-3, h.prof[4], h.prof[5]);
+                "%llu eval steps, %llu evaluations (block 0 evals %.1f us, eval barrier %.1f us, batch max %.1f us)\n",
+                t, h.t, grid_cache[enc], h.prof[0] * 1e-3, h.prof[1] * 1e-3,
+                h.prof[2] * 1e-3, h.prof[3] * 1e-3, h.prof[4], h.prof[5], h.prof[6] * 1e-3, h.prof[7] * 1e-3,
+                h.prof[8] * 1e-3);
     if (h.status == 3) {
         if (h.olen == 0) set_error("no candidate left at round %d", h.t);
         else set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",

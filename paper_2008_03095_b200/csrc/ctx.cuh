@@ -32,8 +32,12 @@ struct CelfDev {
     int32_t bad_v;
     int64_t bad_want, bad_got;
     // phase times (ns, %globaltimer on block 0): eval, commit, rank, merge;
-    // [4] eval batch steps, [5] evaluations (IMX_CELF_PROFILE prints them)
-    unsigned long long prof[6];
+    // [4] eval batch steps, [5] evaluations; eval step split: [6] block 0's
+    // own evaluations, [7] barrier wait, [8] batch max + stop test
+    // (IMX_CELF_PROFILE prints them)
+    unsigned long long prof[10];
+    // per-step maximum fresh key of the evaluated batch, 4 rotating slots
+    unsigned long long smax[4];
 };
 
 struct imx_ctx {

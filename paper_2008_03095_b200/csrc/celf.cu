@@ -618,7 +618,7 @@ extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
     c->ostart = 0;
     c->olen = n;
     c->celf_ready = true;
-    c->trace.clear();
+    c->trace_n = 0;
     return IMX_OK;
 }
 
@@ -718,8 +718,9 @@ extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
 // One round on the host-driven path (prefix batches + advance), synchronous.
 static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seeds_out, int64_t *gains_out) {
     auto rec = [&](int64_t v, int64_t s, int64_t f, int64_t com) {
-        c->trace.push_back(v); c->trace.push_back(s); c->trace.push_back(f);
-        c->trace.push_back(com); c->trace.push_back(t);
+        int64_t *o = c->trace + c->trace_n;
+        o[0] = v; o[1] = s; o[2] = f; o[3] = com; o[4] = t;
+        c->trace_n += 5;
     };
     if (c->olen == 0) { set_error("no candidate left at round %d", t); return IMX_EINTERNAL; }
     std::vector<int32_t> ids;
@@ -750,6 +751,7 @@ static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seed
             lo = hi;
             hi = std::min(len, hi + std::max<int64_t>(batch0, hi));
         }
+        IMX_TRY(trace_reserve(c, c->trace_n + 5 * (hi + 1)));
         kr = 0;
         while (kr < hi && key_le(key_prio(c, keys[kr]), ids[kr], best_f, best_v)) {
             rec(ids[kr], key_prio(c, keys[kr]), fr[kr], 0);
@@ -776,6 +778,7 @@ static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seed
                   (long long)got, (long long)best_f, best_v);
         return IMX_EINTERNAL;
     }
+    IMX_TRY(trace_reserve(c, c->trace_n + 5));
     rec(best_v, best_f, best_f, 1);
     if (seeds_out) seeds_out[t] = best_v;
     if (gains_out) gains_out[t] = best_f;
@@ -862,9 +865,10 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     }
     // collect the records and the seeds of the rounds this launch finished
     if (h.trace_len) {
-        const size_t base = c->trace.size();
-        c->trace.resize(base + 5 * h.trace_len);
-        IMX_CUDA(cudaMemcpyAsync(c->trace.data() + base, c->dtrace, sizeof(int64_t) * 5 * h.trace_len,
+        const int64_t base = c->trace_n;
+        IMX_TRY(trace_reserve(c, base + 5 * h.trace_len));
+        c->trace_n = base + 5 * h.trace_len;
+        IMX_CUDA(cudaMemcpyAsync(c->trace + base, c->dtrace, sizeof(int64_t) * 5 * h.trace_len,
                                  cudaMemcpyDeviceToHost, c->st));
     }
     if (h.t > t) {
@@ -890,7 +894,7 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     if (k < 1 || k > n) { set_error("k=%d invalid for n=%lld", k, (long long)n); return IMX_ECONSTRAINT; }
     if (c->olen != n) { set_error("CELF state already advanced (call imx_celf_reset)"); return IMX_EINVAL; }
     cudaEventRecord(c->ev[6], c->st);
-    c->trace.clear();
+    c->trace_n = 0;
     c->evaluated = 0;
     std::vector<int32_t> seeds(k);
     std::vector<int64_t> gains(k);
@@ -919,15 +923,15 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     cudaEventSynchronize(c->ev[7]);
     cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
     c->tm.celf_evaluations = c->evaluated;
-    if (trace_len) *trace_len = (int64_t)(c->trace.size() / 5);
+    if (trace_len) *trace_len = c->trace_n / 5;
     return IMX_OK;
 }
 
 extern "C" int imx_celf_trace(imx_ctx *c, int64_t *out, int64_t cap) {
     CTX_CHECK(c);
-    const int64_t len = (int64_t)(c->trace.size() / 5);
+    const int64_t len = c->trace_n / 5;
     const int64_t k = std::min(cap, len);
-    if (k > 0 && out) std::copy(c->trace.begin(), c->trace.begin() + 5 * k, out);
+    if (k > 0 && out) memcpy(out, c->trace, sizeof(int64_t) * 5 * k);
     return IMX_OK;
 }
 

@@ -69,6 +69,9 @@ void note_launch(int64_t k = 1);
 // recycled non-blocking streams (graph.cu)
 cudaError_t acquire_stream(int dev, cudaStream_t *st);
 void release_stream(int dev, cudaStream_t st);
+// host->device copy of a pageable buffer, staged through pinned memory by
+// host threads when large (upload.cu)
+cudaError_t upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t st);
 // stream-ordered allocation from the device's pool (ctx.cu)
 cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
 

@@ -1,6 +1,7 @@
 // ctx.cu -- context lifecycle (imx_create / imx_destroy / imx_get_timings)
 // and buffer management shared by propagate.cu, memo.cu and celf.cu.
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -13,20 +14,25 @@ namespace imx {
 static std::mutex g_pin_mu;
 static std::vector<std::pair<void *, size_t>> g_pin_free;
 
-static cudaError_t pinned_get(void **p, size_t bytes) {
+cudaError_t pinned_get(void **p, size_t bytes) {
     {
+        // best fit, so small requests do not take the large staging buffers
         std::lock_guard<std::mutex> lk(g_pin_mu);
+        size_t best = g_pin_free.size();
         for (size_t i = 0; i < g_pin_free.size(); ++i)
-            if (g_pin_free[i].second >= bytes) {
-                *p = g_pin_free[i].first;
-                g_pin_free.erase(g_pin_free.begin() + i);
-                return cudaSuccess;
-            }
+            if (g_pin_free[i].second >= bytes &&
+                (best == g_pin_free.size() || g_pin_free[i].second < g_pin_free[best].second))
+                best = i;
+        if (best < g_pin_free.size()) {
+            *p = g_pin_free[best].first;
+            g_pin_free.erase(g_pin_free.begin() + best);
+            return cudaSuccess;
+        }
     }
     return cudaMallocHost(p, bytes);
 }
 
-static void pinned_put(void *p, size_t bytes) {
+void pinned_put(void *p, size_t bytes) {
     if (!p) return;
     std::lock_guard<std::mutex> lk(g_pin_mu);
     g_pin_free.emplace_back(p, bytes);
@@ -66,6 +72,7 @@ void ctx_free(imx_ctx *c) {
     if (c->st) cudaStreamSynchronize(c->st);
     pinned_put(c->h_ids, sizeof(int32_t) * c->stage_cap);
     pinned_put(c->h_vals, sizeof(int64_t) * c->stage_cap);
+    pinned_put(c->trace, sizeof(int64_t) * c->trace_hcap);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
     release_stream(c->dev, c->st);
     delete c;
@@ -168,3 +175,18 @@ extern "C" int imx_get_timings(imx_ctx *c, imx_timings *out) {
     *out = c->tm;
     return IMX_OK;
 }
+
+namespace imx {
+// grow the pinned host trace buffer to hold at least cnt int64 (keeps content)
+int trace_reserve(imx_ctx *c, int64_t cnt) {
+    if (cnt <= c->trace_hcap) return IMX_OK;
+    const int64_t cap = std::max<int64_t>(cnt, std::max<int64_t>(2 * c->trace_hcap, 1 << 16));
+    int64_t *p = nullptr;
+    IMX_CUDA(pinned_get((void **)&p, sizeof(int64_t) * cap));
+    if (c->trace_n) memcpy(p, c->trace, sizeof(int64_t) * c->trace_n);
+    pinned_put(c->trace, sizeof(int64_t) * c->trace_hcap);
+    c->trace = p;
+    c->trace_hcap = cap;
+    return IMX_OK;
+}
+}  // namespace imx

@@ -68,7 +68,10 @@ struct imx_ctx {
     int64_t *h_vals = nullptr, *d_vals = nullptr;
     int64_t stage_cap = 0;
     int64_t evaluated = 0;
-    std::vector<int64_t> trace;   // 5 per record
+    // dequeue trace, 5 int64 per record, in pinned host memory (the device
+    // trace is copied straight into it)
+    int64_t *trace = nullptr;
+    int64_t trace_n = 0, trace_hcap = 0;
     // persistent CELF kernel state and buffers
     CelfDev *cdev = nullptr;
     unsigned long long *bkey = nullptr, *skey = nullptr;
@@ -104,6 +107,9 @@ inline void count_launch(imx_ctx *c, int k = 1) {
 }
 
 int ensure_celf_buffers(imx_ctx *c);
+int trace_reserve(imx_ctx *c, int64_t cnt);
+cudaError_t pinned_get(void **p, size_t bytes);
+void pinned_put(void *p, size_t bytes);
 int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);
 // raw label-matrix passes shared with the evaluation worlds (evaluation.cu)

@@ -728,10 +728,10 @@ extern "C" int imx_graph_from_edges(int32_t device, int64_t n, const int64_t *ed
     cudaError_t e = cudaSuccess;
     if (k > 0) {
         if ((e = cudaMallocAsync((void **)&dedges, sizeof(int64_t) * 2 * k, st)) == cudaSuccess)
-            e = cudaMemcpyAsync(dedges, edges, sizeof(int64_t) * 2 * k, cudaMemcpyHostToDevice, st);
+            e = upload_h2d(dedges, edges, sizeof(int64_t) * 2 * k, st);
         if (e == cudaSuccess && w_edge) {
             if ((e = cudaMallocAsync((void **)&dw, sizeof(double) * k, st)) == cudaSuccess)
-                e = cudaMemcpyAsync(dw, w_edge, sizeof(double) * k, cudaMemcpyHostToDevice, st);
+                e = upload_h2d(dw, w_edge, sizeof(double) * k, st);
         }
     }
     rc = e == cudaSuccess ? graph_build_from_device_edges(g, dedges, k, dw, w_scalar)
@@ -757,9 +757,9 @@ extern "C" int imx_graph_from_csr(int32_t device, int64_t n, int64_t m2, const i
     g_clock.mark("validate+stream", st);
     auto fail = [&](int code) { graph_free(g); return code; };
     if (dalloc(g, &g->xadj, n + 1) || dalloc(g, &g->adj, m2) || dalloc(g, &g->w, m2)) return fail(IMX_ENOMEM);
-    if (cudaMemcpyAsync(g->xadj, xadj, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        (m2 && cudaMemcpyAsync(g->adj, adj, sizeof(int32_t) * m2, cudaMemcpyHostToDevice, st) != cudaSuccess) ||
-        (m2 && cudaMemcpyAsync(g->w, weights, sizeof(double) * m2, cudaMemcpyHostToDevice, st) != cudaSuccess))
+    if (upload_h2d(g->xadj, xadj, sizeof(int64_t) * (n + 1), st) != cudaSuccess ||
+        (m2 && upload_h2d(g->adj, adj, sizeof(int32_t) * m2, st) != cudaSuccess) ||
+        (m2 && upload_h2d(g->w, weights, sizeof(double) * m2, st) != cudaSuccess))
         return fail(cuda_fail(cudaGetLastError(), "upload csr", __FILE__, __LINE__));
     g_clock.mark("upload csr", st);
     int rc = graph_analyze(g, true);
@@ -806,7 +806,7 @@ extern "C" int imx_graph_set_weights(imx_graph *g, const double *weights) {
     if (g->m2) {
         double *tmp;
         IMX_CUDA(cudaMallocAsync((void **)&tmp, sizeof(double) * g->m2, st));
-        IMX_CUDA(cudaMemcpyAsync(tmp, weights, sizeof(double) * g->m2, cudaMemcpyHostToDevice, st));
+        IMX_CUDA(upload_h2d(tmp, weights, sizeof(double) * g->m2, st));
         unsigned *dflags;
         IMX_CUDA(cudaMallocAsync((void **)&dflags, sizeof(unsigned), st));
         IMX_CUDA(cudaMemsetAsync(dflags, 0, sizeof(unsigned), st));

@@ -444,8 +444,11 @@ __global__ void __launch_bounds__(256, 4) k_celf_rounds(
         const int32_t best_v = (int32_t)(vmask - (uint32_t)(bestkey & vmask));
         const int64_t best_f = (int64_t)(bestkey >> vb);
         const int64_t nrec = (t == 0 ? 0 : kr) + 1;
-        if (T + nrec > trace_cap) { status = 2; break; }    // host drains the trace, relaunches
-        if (kr > kMaxRank) { status = 4; break; }           // host runs this round, relaunches
+        if (T + nrec > trace_cap || kr > kMaxRank) {
+            if (gtid == 0) { st->big_key = bestkey; st->big_kr = kr; }
+            status = T + nrec > trace_cap ? 2 : 4;        // 2: host drains the trace and relaunches
+            break;                                        // (or finishes an oversized round)
+        }
         // phase 1: trace records; the refreshed vertices ranked by their fresh
         // keys (fresh[] / order ids of the evaluated prefix are complete since
         // the last evaluation barrier) and scattered sorted; commit
@@ -851,6 +854,8 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     count_launch(c);
     IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
+    c->big_key = h.big_key;
+    c->big_kr = (h.status == 2 || h.status == 4) ? h.big_kr : 0;
     if (getenv("IMX_CELF_PROFILE"))
         fprintf(stderr, "[celf] rounds %d..%d grid %d: eval %.1f us, commit %.1f us, rank %.1f us, merge %.1f us; "
                 "%llu eval steps, %llu evaluations (block 0 evals %.1f us, eval barrier %.1f us, batch max %.1f us)\n",
@@ -884,6 +889,101 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     return IMX_OK;
 }
 
+// An oversized round (refreshed prefix > kMaxRank, or more trace records than
+// the kernel's buffer) finished with device-wide primitives: the persistent
+// kernel stopped after evaluating the prefix (fresh[0, hi) and the best key
+// are on the device), so nothing is re-evaluated; the refreshed vertices are
+// radix-sorted by fresh key instead of ranked pairwise.
+__global__ void k_big_round_prep(const int32_t *__restrict__ oid, const unsigned long long *__restrict__ okey,
+                                 const int64_t *__restrict__ fresh, int64_t kr, int vb, int32_t best_v,
+                                 int64_t best_f, int32_t t, int64_t *__restrict__ rec,
+                                 unsigned long long *__restrict__ keys, int32_t *__restrict__ ids) {
+    const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= kr;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t *r = rec + 5 * i;
+        if (i == kr) {          // the commit record follows the refresh records
+            r[0] = best_v; r[1] = best_f; r[2] = best_f; r[3] = 1; r[4] = t;
+            continue;
+        }
+        const int32_t v = oid[i];
+        const int64_t f = fresh[i];
+        r[0] = v; r[1] = (int64_t)(okey[i] >> vb); r[2] = f; r[3] = 0; r[4] = t;
+        keys[i] = v == best_v ? 0ull : (((unsigned long long)f << vb) | (unsigned long long)(vmask - (uint32_t)v));
+        ids[i] = v;
+    }
+}
+
+static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<int32_t> &seeds,
+                          std::vector<int64_t> &gains) {
+    const int64_t kr = c->big_kr;
+    const unsigned long long bestkey = c->big_key;
+    const uint64_t vmask = (c->vb >= 32) ? 0xffffffffull : ((1ull << c->vb) - 1);
+    const int32_t best_v = (int32_t)(vmask - (bestkey & vmask));
+    const int64_t best_f = (int64_t)(bestkey >> c->vb);
+    cudaStream_t st = c->st;
+    int32_t *oid = c->oid[c->ocur] + c->ostart;
+    unsigned long long *okey = c->okey[c->ocur] + c->ostart;
+    int64_t *rec = nullptr;
+    unsigned long long *keys = nullptr, *skeys = nullptr;
+    int32_t *ids = nullptr, *sids = nullptr;
+    void *tmp = nullptr;
+    size_t tb = 0;
+    int rc = IMX_OK;
+#define GB(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { rc = cuda_fail(_e, #call, __FILE__, __LINE__); goto done; } } while (0)
+    GB(pool_alloc((void **)&rec, sizeof(int64_t) * 5 * (kr + 1), st));
+    GB(pool_alloc((void **)&keys, sizeof(unsigned long long) * kr, st));
+    GB(pool_alloc((void **)&skeys, sizeof(unsigned long long) * kr, st));
+    GB(pool_alloc((void **)&ids, sizeof(int32_t) * kr, st));
+    GB(pool_alloc((void **)&sids, sizeof(int32_t) * kr, st));
+    k_big_round_prep<<<grid_for(kr + 1), 256, 0, st>>>(oid, okey, c->eval_out, kr, c->vb, best_v, best_f, t, rec,
+                                                        keys, ids);
+    GB(cudaGetLastError());
+    GB(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys, skeys, ids, sids, kr, 0, 64, st));
+    GB(pool_alloc(&tmp, tb, st));
+    GB(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, keys, skeys, ids, sids, kr, 0, 64, st));
+    count_launch(c, 5);
+    {
+        unsigned long long *gain = c->scratch + 7;
+        GB(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), st));
+        launch_commit(c, best_v, gain);
+        GB(cudaGetLastError());
+        count_launch(c);
+        // merge order[kr, olen) with the kr-1 sorted refreshed vertices (the
+        // winner's key 0 sorts last and is dropped)
+        const int64_t na = c->olen - kr, nback = kr - 1;
+        const int nxt = c->ocur ^ 1;
+        k_merge<<<grid_for(na + nback), 256, 0, st>>>(oid + kr, okey + kr, na, sids, skeys, nback, c->oid[nxt],
+                                                      c->okey[nxt]);
+        GB(cudaGetLastError());
+        count_launch(c);
+        const int64_t base = c->trace_n;
+        if ((rc = trace_reserve(c, base + 5 * (kr + 1))) != IMX_OK) goto done;
+        GB(cudaMemcpyAsync(c->trace + base, rec, sizeof(int64_t) * 5 * (kr + 1), cudaMemcpyDeviceToHost, st));
+        unsigned long long got = 0;
+        GB(cudaMemcpyAsync(&got, gain, sizeof got, cudaMemcpyDeviceToHost, st));
+        GB(cudaStreamSynchronize(st));
+        if ((int64_t)got != best_f) {
+            set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                      (long long)got, (long long)best_f, best_v);
+            rc = IMX_EINTERNAL;
+            goto done;
+        }
+        c->trace_n = base + 5 * (kr + 1);
+        c->ocur = nxt;
+        c->ostart = 0;
+        c->olen = na + nback;
+        seeds[t] = best_v;
+        gains[t] = best_f;
+        batch0 = std::max<int64_t>(64, kr);
+    }
+done:
+    for (void *p : {(void *)rec, (void *)keys, (void *)skeys, (void *)ids, (void *)sids, tmp})
+        if (p) cudaFreeAsync(p, st);
+#undef GB
+    return rc;
+}
+
 // The whole CELF loop on one context (single-rank path): the persistent
 // cooperative kernel runs the rounds; a round it cannot hold (trace buffer
 // full, refreshed prefix larger than kMaxRank) is finished on the host.
@@ -911,8 +1011,16 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
             const bool progressed = t2 > t;
             t = t2;
             if (status == 1 || t >= k) break;
-            if (status == 2 && progressed) continue;   // trace drained, relaunch
-            // status 4, or one round alone overflows the trace buffer: host round
+            // a round the kernel can never hold (refreshed prefix > kMaxRank, or
+            // more records than the whole trace buffer) is finished right here
+            // from its evaluated prefix; otherwise drain the trace and relaunch
+            const bool oversized = c->big_kr > 0 && (status == 4 || c->big_kr + 1 > c->trace_cap);
+            if (t > 0 && oversized) {
+                IMX_TRY(celf_big_round(c, t, batch0, seeds, gains));
+                ++t;
+                continue;
+            }
+            if (status == 2 && progressed) continue;
         }
         IMX_TRY(celf_host_round(c, t, batch0, seeds.data(), gains.data()));   // status 4 or host mode
         ++t;

@@ -38,6 +38,10 @@ struct CelfDev {
     unsigned long long prof[10];
     // per-step maximum fresh key of the evaluated batch, 4 rotating slots
     unsigned long long smax[4];
+    // a round the kernel cannot hold (status 2/4): its best fresh key and
+    // refreshed prefix length (fresh[] holds the evaluated prefix)
+    unsigned long long big_key;
+    int64_t big_kr;
 };
 
 struct imx_ctx {
@@ -78,6 +82,8 @@ struct imx_ctx {
     int32_t *bid = nullptr, *sid = nullptr;
     int64_t *dtrace = nullptr;
     int64_t trace_cap = 0;
+    unsigned long long big_key = 0;   // last kernel stop on an oversized round
+    int64_t big_kr = 0;
     int32_t *dseeds = nullptr;
     int64_t *dsgains = nullptr;
     int32_t dseeds_cap = 0;

@@ -233,3 +233,25 @@ def test_config_graphs_are_the_golden_graphs(gpu, cfg):
     check_array(z, "xadj", g.xadj)
     check_array(z, "adj", g.adj)
     check_array(z, "weights", g.weights)
+
+
+@pytest.mark.parametrize("trace_cap", [None, "5000"])
+def test_celf_oversized_round_matches_oracle(gpu, orc, trace_cap, monkeypatch):
+    # two paths with p=1: after the first commit every vertex of the long path
+    # has a stale gain above the best fresh one, so round 1 refreshes ~18k
+    # vertices -- more than the persistent kernel ranks pairwise (and, with a
+    # small trace buffer, more records than it holds); the round is finished
+    # with device sort + merge from the kernel's evaluated prefix
+    if trace_cap:
+        monkeypatch.setenv("IMX_CELF_TRACE_CAP", trace_cap)
+    a, b = 18_000, 4_000
+    e1 = np.column_stack([np.arange(a - 1), np.arange(1, a)])
+    e2 = np.column_stack([np.arange(a, a + b - 1), np.arange(a + 1, a + b)])
+    g = gpu.Graph.from_edges(a + b, np.vstack([e1, e2]).astype(np.int64), 1.0)
+    run = gpu.run_fused(g, 4, num_simulations=16, master_seed=3)
+    want = orc.run_fused(g.xadj, g.adj, g.weights, 4, 16, 3, nthreads=4)
+    assert [int(s) for s in run.seeds] == want["seeds"].tolist()
+    assert list(run.selection.gains) == want["seed_gains"].tolist()
+    got = run.selection.trace.array
+    assert len(got) > 16384
+    assert np.array_equal(got, want["trace"])

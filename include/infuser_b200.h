@@ -199,6 +199,26 @@ int  imx_sampling_cdf(imx_graph *g, const int32_t *X, int32_t scored, int64_t st
                       int32_t bins, const double *edges, int64_t *counts_out,
                       double *ks_out, int64_t *nvals_out);
 
+/* ---- graph files (graph.py:269-437) --------------------------------------
+ * Native parser of a whitespace-separated "u v [w]" text edge list
+ * (load_edge_list, graph.py:273-330): comments / blank lines skipped, ids
+ * compacted in order of first appearance, self-loops dropped, duplicate
+ * undirected edges collapse to the first occurrence.  On IMX_EFORMAT,
+ * *err_kind: 1 field count (*err_aux = fields), 2 non-numeric field,
+ * 3 weight outside [0, 1] (err_text = the weight field), 4 no edges,
+ * 5 cannot open (*err_aux = errno), 6 id beyond int64, 7 id space full;
+ * *err_line = 1-based line, err_text = the stripped line (kinds 1, 2, 6).  */
+typedef struct imx_edge_list imx_edge_list;
+int  imx_edge_list_parse(const char *path, imx_edge_list **out, int64_t *err_line,
+                         int32_t *err_kind, int64_t *err_aux, char *err_text,
+                         int64_t err_text_cap);
+int  imx_edge_list_dims(const imx_edge_list *e, int64_t *n_vertices, int64_t *n_edges);
+/* edges: 2 int64 per edge (compact ids), weights: f64 per edge,
+ * orig_ids: int64 per compact id.                                          */
+int  imx_edge_list_copy(const imx_edge_list *e, int64_t *edges, double *weights,
+                        int64_t *orig_ids);
+void imx_edge_list_free(imx_edge_list *e);
+
 /* ---- measurement --------------------------------------------------------
  * Device time (CUDA events on the context stream) of the last call of each
  * phase and the number of kernels this context launched so far.           */

@@ -8,9 +8,11 @@ libinfuser_b200.so (include/infuser_b200.h).  There is no CPU fallback.
 """
 
 from ._lib import ConstraintError, GraphFormatError, set_device
+from .estimator import InfluenceMaximizer
 from .evaluation import (KS_UNIFORM_BOUND, SamplingCdf, evaluate_seeds, sampling_cdf,
                          write_cdf_tsv)
 from .graph import MAX_VERTICES, Graph
+from .io import load_csr, load_edge_list, load_graph, save_csr, write_edge_list
 from .hashing import (H_MAX, LANE_WIDTH, EdgeHashTable, SimulationRandoms, build_hash_table,
                       lane_membership, murmur3_32, sample_prob, slot_thresholds, threshold)
 from .pipeline import FusedRun, run_fused
@@ -24,6 +26,7 @@ from .weights import (Constant, FromFile, NormalClamped, UniformRange, WeightedC
 __version__ = "0.1.0"
 
 __all__ = [
+    "InfluenceMaximizer", "load_csr", "load_edge_list", "load_graph", "save_csr", "write_edge_list",
     "KS_UNIFORM_BOUND", "SamplingCdf", "evaluate_seeds", "sampling_cdf", "write_cdf_tsv",
     "ConstraintError", "Constant", "EdgeHashTable", "FromFile", "FusedRun", "Graph",
     "GraphFormatError", "H_MAX", "LANE_WIDTH", "MAX_VERTICES", "NormalClamped",

@@ -88,6 +88,10 @@ _SIGNATURES = {
     "imx_evaluate_seeds": (c_i32, [c_void_p, c_void_p, c_i32, c_i64, c_void_p, c_i64, c_void_p]),
     "imx_sampling_cdf": (c_i32, [c_void_p, c_void_p, c_i32, c_i64, c_i32, c_void_p, c_void_p, P(c_f64),
                                  P(c_i64)]),
+    "imx_edge_list_parse": (c_i32, [ctypes.c_char_p, P(c_void_p), P(c_i64), P(c_i32), P(c_i64), c_void_p, c_i64]),
+    "imx_edge_list_dims": (c_i32, [c_void_p, P(c_i64), P(c_i64)]),
+    "imx_edge_list_copy": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "imx_edge_list_free": (None, [c_void_p]),
     "imx_get_timings": (c_i32, [c_void_p, P(Timings)]),
     "imx_bench_propagate": (c_i32, [c_void_p, c_i32, c_i32, P(c_f32), P(c_f32), P(c_f32), P(c_f32)]),
 }

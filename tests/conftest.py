@@ -19,10 +19,11 @@ def pytest_configure(config):
 
 
 def golden_names(prefix: str = "") -> list[str]:
-    """Pipeline fixtures by default; evaluation ones under "eval_" / "cdf_"."""
+    """Pipeline fixtures by default; evaluation / file-format / estimator ones
+    under "eval_", "cdf_", "io_", "est_"."""
     names = sorted(p.stem for p in GOLDEN.glob(f"{prefix}*.npz"))
     if not prefix:
-        names = [n for n in names if not n.startswith(("eval_", "cdf_"))]
+        names = [n for n in names if not n.startswith(("eval_", "cdf_", "io_", "est_"))]
     return names
 
 

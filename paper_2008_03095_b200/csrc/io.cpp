@@ -16,6 +16,10 @@
 #include <climits>
 #include <strings.h>
 #include <algorithm>
+#include <charconv>
+#include <system_error>
+#include <thread>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -61,7 +65,30 @@ int parse_int(const char *s, size_t n, int64_t *out) {
 
 // Python float(): decimal / exponent / inf / infinity / nan with an optional
 // sign, underscores only between digits, no hex.  0 ok, 1 not a number.
+int parse_float_slow(const char *s, size_t n, double *out);
+
 int parse_float(const char *s, size_t n, double *out) {
+    // fast path (no underscores): std::from_chars is correctly rounded like
+    // strtod / Python; it takes no leading '+', and Python takes no "+-"
+    if (!memchr(s, '_', n)) {
+        if (memchr(s, '(', n) || memchr(s, 'x', n) || memchr(s, 'X', n)) return 1;
+        const char *b = s, *e = s + n;
+        if (b < e && *b == '+') {
+            ++b;
+            if (b < e && (*b == '-' || *b == '+')) return 1;
+        }
+        if (b == e) return 1;
+        double v;
+        const auto r = std::from_chars(b, e, v, std::chars_format::general);
+        if (r.ec == std::errc::result_out_of_range) return parse_float_slow(s, n, out);   // +-inf / 0 like Python
+        if (r.ec != std::errc() || r.ptr != e) return 1;
+        *out = v;
+        return 0;
+    }
+    return parse_float_slow(s, n, out);
+}
+
+int parse_float_slow(const char *s, size_t n, double *out) {
     std::string t;
     t.reserve(n);
     for (size_t i = 0; i < n; ++i) {
@@ -94,11 +121,15 @@ int parse_float(const char *s, size_t n, double *out) {
     return 0;
 }
 
-// open-addressing int64 -> int32 map (first-appearance ids)
+// open-addressing int64 -> int32 map (first-appearance ids); one slot =
+// key + value + used flag in 16 bytes, so a probe is one cache line
 struct IdMap {
-    std::vector<int64_t> keys;
-    std::vector<int32_t> vals;
-    std::vector<uint8_t> used;
+    struct Slot {
+        int64_t key;
+        int32_t val;
+        int32_t used;
+    };
+    std::vector<Slot> slots;
     size_t count = 0, mask = 0;
     IdMap() { rehash(1 << 16); }
     static uint64_t mix(uint64_t x) {
@@ -106,28 +137,25 @@ struct IdMap {
         return x;
     }
     void rehash(size_t cap) {
-        std::vector<int64_t> ok;
-        std::vector<int32_t> ov;
-        std::vector<uint8_t> ou;
-        ok.swap(keys); ov.swap(vals); ou.swap(used);
-        keys.assign(cap, 0); vals.assign(cap, 0); used.assign(cap, 0);
+        std::vector<Slot> old;
+        old.swap(slots);
+        slots.assign(cap, Slot{0, 0, 0});
         mask = cap - 1;
-        for (size_t i = 0; i < ou.size(); ++i)
-            if (ou[i]) place(ok[i], ov[i]);
-    }
-    void place(int64_t k, int32_t v) {
-        size_t h = mix((uint64_t)k) & mask;
-        while (used[h]) h = (h + 1) & mask;
-        used[h] = 1; keys[h] = k; vals[h] = v;
+        for (const Slot &o : old)
+            if (o.used) {
+                size_t h = mix((uint64_t)o.key) & mask;
+                while (slots[h].used) h = (h + 1) & mask;
+                slots[h] = o;
+            }
     }
     int32_t get_or_add(int64_t k, std::vector<int64_t> &orig) {
         size_t h = mix((uint64_t)k) & mask;
-        while (used[h]) {
-            if (keys[h] == k) return vals[h];
+        while (slots[h].used) {
+            if (slots[h].key == k) return slots[h].val;
             h = (h + 1) & mask;
         }
         const int32_t v = (int32_t)orig.size();
-        used[h] = 1; keys[h] = k; vals[h] = v;
+        slots[h] = Slot{k, v, 1};
         orig.push_back(k);
         if (++count * 2 > mask + 1) rehash((mask + 1) * 2);
         return v;
@@ -172,6 +200,78 @@ struct imx_edge_list {
     std::vector<double> weights;
 };
 
+namespace {
+
+// one parsed line that survives to the compaction pass
+struct Rec {
+    int64_t u, v;
+    double w;
+};
+
+// per-chunk result of the parallel pass
+struct Chunk {
+    const char *begin = nullptr, *end = nullptr;
+    std::vector<Rec> recs;
+    int64_t lines = 0;
+    int err_kind = 0;           // first error of the chunk (0: none)
+    int64_t err_line = 0, err_aux = 0;
+    const char *err_txt = nullptr;
+    size_t err_len = 0;
+};
+
+// next line start after position p (\n, \r\n or a lone \r ends a line)
+const char *next_line(const char *p, const char *end) {
+    while (p < end && *p != '\n' && *p != '\r') ++p;
+    if (p < end) {
+        if (*p == '\r' && p + 1 < end && p[1] == '\n') p += 2;
+        else ++p;
+    }
+    return p;
+}
+
+void parse_chunk(Chunk &c) {
+    const char *p = c.begin, *end = c.end;
+    c.recs.reserve((size_t)((end - p) / 16));
+    while (p < end) {
+        const char *ls = p, *le = p;
+        while (le < end && *le != '\n' && *le != '\r') ++le;
+        p = next_line(le, end);
+        ++c.lines;
+        const char *a = ls, *b = le;
+        while (a < b && is_ws((unsigned char)*a)) ++a;
+        while (b > a && is_ws((unsigned char)b[-1])) --b;
+        if (a == b || *a == '#') continue;
+        const char *fs[4];
+        size_t fl[4];
+        int nf = 0;
+        for (const char *q = a; q < b;) {
+            while (q < b && is_ws((unsigned char)*q)) ++q;
+            if (q >= b) break;
+            const char *st = q;
+            while (q < b && !is_ws((unsigned char)*q)) ++q;
+            if (nf < 4) { fs[nf] = st; fl[nf] = (size_t)(q - st); }
+            ++nf;
+        }
+        auto err = [&](int kind, int64_t aux, const char *t, size_t n) {
+            c.err_kind = kind; c.err_line = c.lines; c.err_aux = aux; c.err_txt = t; c.err_len = n;
+        };
+        if (nf != 2 && nf != 3) { err(1, nf, a, (size_t)(b - a)); return; }
+        int64_t u = 0, v = 0;
+        double w = 1.0;
+        const int ru = parse_int(fs[0], fl[0], &u), rv = ru ? 0 : parse_int(fs[1], fl[1], &v);
+        if (ru == 2 || rv == 2) { err(6, 0, a, (size_t)(b - a)); return; }     // beyond int64 (OverflowError)
+        if (ru || rv || (nf == 3 && parse_float(fs[2], fl[2], &w))) { err(2, 0, a, (size_t)(b - a)); return; }
+        if (!(w >= 0.0 && w <= 1.0)) { err(3, 0, fs[2], fl[2]); return; }
+        if (u == v) continue;                 // self-loops register no ids
+        c.recs.push_back(Rec{u, v, w});
+    }
+}
+
+}  // namespace
+
+// Two passes: the lines are split into chunks at line boundaries and parsed
+// (fields, numbers, validation) by host threads; the first-appearance id
+// compaction and the first-occurrence dedupe then run in file order.
 extern "C" int imx_edge_list_parse(const char *path, imx_edge_list **out, int64_t *err_line, int32_t *err_kind,
                                    int64_t *err_aux, char *err_text, int64_t err_text_cap) {
     if (!path || !out) return IMX_EINVAL;
@@ -190,77 +290,80 @@ extern "C" int imx_edge_list_parse(const char *path, imx_edge_list **out, int64_
     FILE *f = fopen(path, "rb");
     if (!f) return fail(5, 0, errno, nullptr, 0);
     std::vector<char> buf;
-    {
+    if (fseek(f, 0, SEEK_END) == 0) {
+        const long sz = ftell(f);
+        if (sz > 0) buf.resize((size_t)sz);
+        fseek(f, 0, SEEK_SET);
+        if (!buf.empty() && fread(buf.data(), 1, buf.size(), f) != buf.size()) buf.clear();
+    }
+    if (buf.empty()) {                        // unseekable or short read: stream it
         char tmp[1 << 16];
         size_t r;
+        fseek(f, 0, SEEK_SET);
         while ((r = fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + r);
-        fclose(f);
+    }
+    fclose(f);
+    const bool prof = getenv("IMX_PARSE_PROFILE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
+    const char *base = buf.data(), *end = base + buf.size();
+    unsigned hw = std::thread::hardware_concurrency();
+    int nt = (int)std::min<size_t>(std::max(1u, std::min(hw, 16u)), std::max<size_t>(1, buf.size() >> 20));
+    if (const char *e = getenv("IMX_PARSE_THREADS")) nt = std::max(1, atoi(e));
+    std::vector<Chunk> ch(nt);
+    const char *cur = base;
+    for (int i = 0; i < nt; ++i) {
+        const char *stop = i + 1 == nt ? end : base + (buf.size() * (size_t)(i + 1)) / nt;
+        if (stop < cur) stop = cur;
+        if (stop > base && stop < end && stop[-1] == '\r' && *stop == '\n') ++stop;       // keep \r\n together
+        else if (stop > base && stop < end && stop[-1] != '\n' && stop[-1] != '\r') stop = next_line(stop, end);
+        ch[i].begin = cur;
+        ch[i].end = stop;
+        cur = stop;
+    }
+    {
+        std::vector<std::thread> th;
+        for (int i = 1; i < nt; ++i) th.emplace_back(parse_chunk, std::ref(ch[i]));
+        parse_chunk(ch[0]);
+        for (auto &t : th) t.join();
+    }
+    auto t1 = now();
+    int64_t lines_before = 0;
+    for (int i = 0; i < nt; ++i) {
+        if (ch[i].err_kind)
+            return fail(ch[i].err_kind, lines_before + ch[i].err_line, ch[i].err_aux, ch[i].err_txt, ch[i].err_len);
+        lines_before += ch[i].lines;
     }
     imx_edge_list *el = new imx_edge_list();
     IdMap ids;
     PairSet seen;
-    const char *p = buf.data(), *end = p + buf.size();
-    int64_t lineno = 0;
-    while (p < end) {
-        // one line: up to \n, \r\n or a lone \r (universal newlines)
-        const char *ls = p, *le = p;
-        while (le < end && *le != '\n' && *le != '\r') ++le;
-        p = le;
-        if (p < end) {
-            if (*p == '\r' && p + 1 < end && p[1] == '\n') p += 2;
-            else ++p;
+    size_t total = 0;
+    for (auto &c : ch) total += c.recs.size();
+    el->edges.reserve(2 * total);
+    el->weights.reserve(total);
+    for (auto &c : ch) {
+        for (const Rec &r : c.recs) {
+            const int32_t cu = ids.get_or_add(r.u, el->orig);
+            const int32_t cv = ids.get_or_add(r.v, el->orig);
+            if (el->orig.size() >= ((size_t)1 << 31) - 1) {
+                delete el;
+                return fail(7, lines_before, 0, nullptr, 0);      // id space exhausted
+            }
+            const uint32_t lo = (uint32_t)(cu < cv ? cu : cv), hi = (uint32_t)(cu < cv ? cv : cu);
+            if (!seen.insert(((uint64_t)lo << 32) | hi)) continue;
+            el->edges.push_back(cu);
+            el->edges.push_back(cv);
+            el->weights.push_back(r.w);
         }
-        ++lineno;
-        const char *a = ls, *b = le;
-        while (a < b && is_ws((unsigned char)*a)) ++a;
-        while (b > a && is_ws((unsigned char)b[-1])) --b;
-        if (a == b || *a == '#') continue;
-        const char *fs[4];
-        size_t fl[4];
-        int nf = 0;
-        for (const char *q = a; q < b;) {
-            while (q < b && is_ws((unsigned char)*q)) ++q;
-            if (q >= b) break;
-            const char *s = q;
-            while (q < b && !is_ws((unsigned char)*q)) ++q;
-            if (nf < 4) { fs[nf] = s; fl[nf] = (size_t)(q - s); }
-            ++nf;
-        }
-        if (nf != 2 && nf != 3) {
-            delete el;
-            return fail(1, lineno, nf, a, (size_t)(b - a));
-        }
-        int64_t u = 0, v = 0;
-        double w = 1.0;
-        int ru = parse_int(fs[0], fl[0], &u), rv = ru ? 0 : parse_int(fs[1], fl[1], &v);
-        if (ru == 2 || rv == 2) {
-            delete el;
-            return fail(6, lineno, 0, a, (size_t)(b - a));       // beyond int64 (OverflowError)
-        }
-        if (ru || rv || (nf == 3 && parse_float(fs[2], fl[2], &w))) {
-            delete el;
-            return fail(2, lineno, 0, a, (size_t)(b - a));
-        }
-        if (!(w >= 0.0 && w <= 1.0)) {
-            delete el;
-            return fail(3, lineno, 0, fs[2], fl[2]);
-        }
-        if (u == v) continue;
-        const int32_t cu = ids.get_or_add(u, el->orig);
-        const int32_t cv = ids.get_or_add(v, el->orig);
-        const uint32_t lo = (uint32_t)(cu < cv ? cu : cv), hi = (uint32_t)(cu < cv ? cv : cu);
-        if (!seen.insert(((uint64_t)lo << 32) | hi)) continue;
-        el->edges.push_back(cu);
-        el->edges.push_back(cv);
-        el->weights.push_back(w);
-        if (el->orig.size() >= ((size_t)1 << 31) - 1) {
-            delete el;
-            return fail(7, lineno, 0, nullptr, 0);               // id space exhausted
-        }
+        std::vector<Rec>().swap(c.recs);
     }
+    if (prof)
+        fprintf(stderr, "[parse] %d threads: fields+numbers %.1f ms, compaction+dedupe %.1f ms\n", nt,
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(now() - t1).count());
     if (el->weights.empty()) {
         delete el;
-        return fail(4, lineno, 0, nullptr, 0);
+        return fail(4, lines_before, 0, nullptr, 0);
     }
     *out = el;
     return IMX_OK;

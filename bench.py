@@ -55,10 +55,17 @@ def dist_setup(args):
     if world > 1:
         import torch
         import torch.distributed as dist
-        if args.impl == "ours":
+        if args.impl == "ours" and os.environ.get("IMX_BENCH_BACKEND", "nccl") == "nccl":
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
+            # gloo: the reference arm, or a functional check of the N>1 code
+            # path with several ranks sharing the visible GPUs (no device-side
+            # collective: the gloo allreduces run on host tensors)
+            if args.impl == "ours":
+                dev = local % max(1, torch.cuda.device_count())
+                torch.cuda.set_device(dev)
+                os.environ["INFUSER_DEVICE"] = str(dev)
             dist.init_process_group("gloo")
     return world, rank, local
 
@@ -242,7 +249,7 @@ def run_ours(args, world, rank, local):
     from paper_2008_03095_b200 import _lib, configs
     from paper_2008_03095_b200.celf import lane_window
     from paper_2008_03095_b200.context import DeviceContext
-    imx.set_device(local)
+    imx.set_device(int(os.environ.get("INFUSER_DEVICE", local)))
     c = configs.CONFIGS[args.config]
     t0 = time.perf_counter()
     g = configs.build(args.config)          # generated + CSR-built on the device

@@ -107,7 +107,8 @@ cudaError_t upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t st
     if (const char *e = getenv("IMX_UPLOAD_STAGED_MIN")) thresh = (size_t)atoll(e);
     if (bytes < thresh) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
     std::lock_guard<std::mutex> lk(g_upload_mu);
-    const size_t chunk = std::min<size_t>(bytes, (size_t)8 << 20);
+    size_t chunk = std::min<size_t>(bytes, (size_t)8 << 20);
+    if (const char *e = getenv("IMX_UPLOAD_CHUNK")) chunk = std::min<size_t>(bytes, std::max<size_t>(4096, (size_t)atoll(e)));
     void *slot[2] = {nullptr, nullptr};
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaError_t e = cudaSuccess;

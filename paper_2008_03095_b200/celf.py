@@ -94,6 +94,12 @@ def select_rounds(shard, comm, k: int, batch0: int = 64):
     winner's fresh key, replayed as refresh records, then the winner commits
     and the others go back into the order with their fresh keys."""
     seeds, gains, trace = [], [], []
+    pending = None              # (local commit gain, expected, vertex) checked with the next allreduce
+
+    def check(total):
+        if total != pending[1]:
+            raise AssertionError(f"committed gain {total} != evaluated {pending[1]} for vertex {pending[2]}")
+
     for t in range(k):
         back = []
         if t == 0:
@@ -109,7 +115,13 @@ def select_rounds(shard, comm, k: int, batch0: int = 64):
                 i, p, f_part, length = shard.celf_prefix(lo, hi)
                 if length == 0:
                     raise AssertionError(f"no candidate left at round {t}")
-                f = comm.allreduce(f_part)
+                if pending is not None:     # last round's commit check rides along
+                    f = comm.allreduce(np.append(np.asarray(f_part, np.int64), pending[0]))
+                    check(int(f[-1]))
+                    pending = None
+                    f = f[:-1]
+                else:
+                    f = comm.allreduce(f_part)
                 h = min(hi, length)
                 for v, fv in zip(i[: h - lo].tolist(), f.tolist()):
                     if best_v < 0 or _key_le(fv, v, best_f, best_v):
@@ -130,11 +142,14 @@ def select_rounds(shard, comm, k: int, batch0: int = 64):
                 kr += 1
             batch0 = max(64, kr)
         back.sort()
-        got = int(comm.allreduce(np.array([shard.celf_advance(
-            kr, best_v, np.array([v for _, v in back], np.int32),
-            np.array([-g for g, _ in back], np.int64))], np.int64))[0])
-        if got != best_f:
-            raise AssertionError(f"committed gain {got} != evaluated {best_f} for vertex {best_v}")
+        local = shard.celf_advance(kr, best_v, np.array([v for _, v in back], np.int32),
+                                   np.array([-g for g, _ in back], np.int64))
+        if t == k - 1:                  # no later evaluation allreduce to ride on
+            pending = (local, best_f, best_v)
+            check(int(comm.allreduce(np.array([local], np.int64))[0]))
+            pending = None
+        else:
+            pending = (local, best_f, best_v)
         trace.append((best_v, best_f, best_f, 1, t))
         seeds.append(best_v)
         gains.append(best_f)

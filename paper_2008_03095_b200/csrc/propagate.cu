@@ -398,14 +398,23 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
     int qn = 0;
     const bool live = t < vstep * nq;
     // every lane of the warp walks the same v sequence (vstep is a multiple of rows)
-    for (int64_t v = live ? t / nq : n; __any_sync(FULL, v < n); v += kCRows * vstep) {
+    // software-pipelined row stream: the next step's kCRows 16-byte loads are
+    // issued before this step's cells are queued and walked (a stale word is
+    // harmless: roots stay roots and any parent read is still an ancestor)
+    uint4 nxt[kCRows];
+    const int64_t v_first = live ? t / nq : n;
+#pragma unroll
+    for (int i = 0; i < kCRows; ++i) {
+        const int64_t vi = v_first + i * vstep;
+        nxt[i] = vi < n ? *(reinterpret_cast<const uint4 *>(L + vi * ld) + q) : make_uint4(ROOT, ROOT, ROOT, ROOT);
+    }
+    for (int64_t v = v_first; __any_sync(FULL, v < n); v += kCRows * vstep) {
         uint32_t w[4 * kCRows];
 #pragma unroll
-        for (int i = 0; i < kCRows; ++i) {       // kCRows independent 16-byte row loads in flight
-            const int64_t vi = v + i * vstep;
-            uint4 l = make_uint4(ROOT, ROOT, ROOT, ROOT);
-            if (vi < n) l = *(reinterpret_cast<const uint4 *>(L + vi * ld) + q);
-            w[4 * i] = l.x; w[4 * i + 1] = l.y; w[4 * i + 2] = l.z; w[4 * i + 3] = l.w;
+        for (int i = 0; i < kCRows; ++i) {
+            w[4 * i] = nxt[i].x; w[4 * i + 1] = nxt[i].y; w[4 * i + 2] = nxt[i].z; w[4 * i + 3] = nxt[i].w;
+            const int64_t vi = v + (kCRows + i) * vstep;
+            nxt[i] = vi < n ? *(reinterpret_cast<const uint4 *>(L + vi * ld) + q) : make_uint4(ROOT, ROOT, ROOT, ROOT);
         }
         unsigned m = 0;
 #pragma unroll

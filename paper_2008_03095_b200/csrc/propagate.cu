@@ -617,7 +617,7 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
 // live edges only, but a warp owns a whole row prefix, so a very long prefix
 // (a high-degree vertex with many smaller neighbours) serialises.
 enum { HOOK_ENUM = 0, HOOK_PULL = 1, HOOK_DENSE = 2, HOOK_HYBRID = 3 };
-static int hook_mode(const imx_graph *g) {
+static int hook_mode(const imx_graph *g, int32_t W) {
     const char *m = getenv("IMX_HOOK");
     if (m && !strcmp(m, "dense")) return HOOK_DENSE;
     // enumeration assumes 31-bit hashes ((x ^ h) >= 0); the scans test exactly
@@ -628,14 +628,18 @@ static int hook_mode(const imx_graph *g) {
     const char *t = getenv("IMX_PULL_MIN_P");
     const double pmin = t ? atof(t) : 0.02;
     const double balanced_prefix = 8.0 * (double)g->me / (148.0 * 64.0);
-    if (g->thr_mean >= pmin && (double)g->max_prefix <= std::max(64.0, balanced_prefix)) return HOOK_PULL;
+    const bool balanced = (double)g->max_prefix <= std::max(64.0, balanced_prefix);
+    if (g->thr_mean >= pmin && balanced) return HOOK_PULL;
+    // small dense work (C1: 31k edges x 128 lanes): two scans beat the
+    // enumeration's segment count + scan + launch chain
+    if (balanced && (double)g->me * (double)W <= 3.2e7) return HOOK_PULL;
     return HOOK_ENUM;
 }
 
 // init + hook phases of one propagate (events bracket them)
 static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_init, cudaEvent_t e_hook) {
     imx_graph *g = c->g;
-    const int mode = g->me ? hook_mode(g) : HOOK_ENUM;
+    const int mode = g->me ? hook_mode(g, c->W) : HOOK_ENUM;
     if (mode == HOOK_PULL || mode == HOOK_HYBRID) {
         IMX_TRY(run_pull(c, 1, nullptr));
         if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));

@@ -236,21 +236,26 @@ __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ o
 // not a vertex's first live smaller neighbour -- 4-30% of the live pairs on
 // the benchmark graphs -- through the per-warp queue of k_hook.
 // ---------------------------------------------------------------------------
-template <int PASS, bool UNI>
+template <int PASS, bool UNI, int LPT>
 __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                                               const int32_t *__restrict__ hash, const int32_t *__restrict__ thr,
                                               int32_t tu, int64_t n, const int32_t *__restrict__ X, int32_t W,
                                               int64_t ld, uint32_t *__restrict__ L,
                                               unsigned long long *__restrict__ hooks) {
+    // LPT lanes per thread (4 or 8): each edge's loads and the loop overhead
+    // are shared by LPT membership tests
+    constexpr int Q = LPT / 4;                // 16-byte quads per thread
     extern __shared__ int4 smem4[];
     int32_t *sX = reinterpret_cast<int32_t *>(smem4);
-    for (int i = threadIdx.x; i < ld; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
+    const int64_t ldp = (ld + LPT - 1) / LPT * LPT;   // staged X padded to whole thread groups
+    for (int i = threadIdx.x; i < ldp; i += blockDim.x) sX[i] = (i < W) ? X[i] : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t *qlo = reinterpret_cast<uint32_t *>(sX + ld) + warp * 3 * kQ;
-    uint32_t *qhi = qlo + kQ;
-    uint32_t *qr = qhi + kQ;
+    constexpr int PQ = 32 + 32 * LPT;         // drain threshold + one edge's appends
+    uint32_t *qlo = reinterpret_cast<uint32_t *>(sX + ldp) + warp * 3 * PQ;
+    uint32_t *qhi = qlo + PQ;
+    uint32_t *qr = qhi + PQ;
     __syncthreads();
-    const int nq = (int)(ld >> 2);
+    const int ng = (int)(ldp / LPT);          // lane groups per row
     const unsigned FULL = 0xffffffffu;
     int qn = 0;
     unsigned long long nh = 0;
@@ -258,66 +263,74 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = wg; v < n; v += nw) {
         const int64_t s0 = xadj[v], s1 = xadj[v + 1];
-        for (int c0 = 0; c0 < nq; c0 += 32) {
-            const int qd = c0 + lane;
-            const bool active = qd < nq;
-            int4 x = make_int4(0, 0, 0, 0);
-            if (active) x = smem4[qd];
-            const int r = qd << 2;
-            unsigned valid = 0xFu;
-            if (r + 4 > W) valid = (1u << (W > r ? W - r : 0)) - 1u;
+        for (int c0 = 0; c0 < ng; c0 += 32) {
+            const int gi = c0 + lane;
+            const bool active = gi < ng;
+            const int r = gi * LPT;
+            int32_t x[LPT];
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+                const int4 q4 = active ? smem4[gi * Q + k] : make_int4(0, 0, 0, 0);
+                x[4 * k] = q4.x; x[4 * k + 1] = q4.y; x[4 * k + 2] = q4.z; x[4 * k + 3] = q4.w;
+            }
+            unsigned valid = (1u << LPT) - 1u;
+            if (r + LPT > W) valid = (1u << (W > r ? W - r : 0)) - 1u;
             if (!active) valid = 0;
-            uint32_t best[4] = {ROOT, ROOT, ROOT, ROOT};
+            uint32_t best[LPT];
+#pragma unroll
+            for (int k = 0; k < LPT; ++k) best[k] = ROOT;
             unsigned seen = 0;
             for (int64_t sl = s0; sl < s1; ++sl) {
                 const uint32_t u = (uint32_t)__ldg(adj + sl);
                 if (u >= (uint32_t)v) break;
                 const int32_t h = __ldg(hash + sl);
                 const int32_t t = UNI ? tu : __ldg(thr + sl);
-                unsigned live = ((unsigned)((x.x ^ h) < t)) | ((unsigned)((x.y ^ h) < t) << 1) |
-                                ((unsigned)((x.z ^ h) < t) << 2) | ((unsigned)((x.w ^ h) < t) << 3);
+                unsigned live = 0;
+#pragma unroll
+                for (int k = 0; k < LPT; ++k) live |= (unsigned)((x[k] ^ h) < t) << k;
                 live &= valid;
                 if (PASS == 1) {
-                    unsigned fresh = live & ~seen;
-                    while (fresh) {
-                        const int j = __ffs(fresh) - 1;
-                        fresh &= fresh - 1;
-                        best[j] = u;
-                    }
+                    const unsigned fresh = live & ~seen;        // first live (= smallest) neighbour
+#pragma unroll
+                    for (int k = 0; k < LPT; ++k) best[k] = ((fresh >> k) & 1u) ? u : best[k];
                     seen |= live;
                 } else {
                     unsigned rest = live & seen;
                     seen |= live;
                     if (!__any_sync(FULL, rest != 0)) continue;
-                    const int k = __popc(rest);
-                    int inc = k;
+                    const int kk = __popc(rest);
+                    int inc = kk;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const int y = __shfl_up_sync(FULL, inc, o);
                         if (lane >= o) inc += y;
                     }
-                    int pos = qn + inc - k;
+                    int pos = qn + inc - kk;
                     while (rest) {
-                        const int b = __ffs(rest) - 1;
+                        const int bb = __ffs(rest) - 1;
                         rest &= rest - 1;
                         qlo[pos] = u;
                         qhi[pos] = (uint32_t)v;
-                        qr[pos] = (uint32_t)(r + b);
+                        qr[pos] = (uint32_t)(r + bb);
                         ++pos;
                     }
                     qn += __shfl_sync(FULL, inc, 31);
                     __syncwarp();
                     while (qn >= 32) {
                         qn -= 32;
-                        const uint32_t a = qlo[qn + lane], bb = qhi[qn + lane];
+                        const uint32_t a2 = qlo[qn + lane], b2 = qhi[qn + lane];
                         const int rr = (int)qr[qn + lane];
                         __syncwarp();
-                        nh += unite(L, ld, a, bb, rr);
+                        nh += unite(L, ld, a2, b2, rr);
                     }
                 }
             }
             if (PASS == 1 && active) {
-                *(reinterpret_cast<uint4 *>(L + v * ld) + qd) = make_uint4(best[0], best[1], best[2], best[3]);
+#pragma unroll
+                for (int k = 0; k < Q; ++k)
+                    if (r + 4 * k < ld)
+                        *(reinterpret_cast<uint4 *>(L + v * ld + r) + k) =
+                            make_uint4(best[4 * k], best[4 * k + 1], best[4 * k + 2], best[4 * k + 3]);
             }
         }
     }
@@ -598,11 +611,17 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (n == 0) return IMX_OK;
-    const size_t smem = sizeof(int32_t) * c->ld + sizeof(uint32_t) * 3 * kQ * 8;
+    // 8 lanes per thread once a row spans several warp-widths of quads
+    const bool wide = c->W >= 256;
+    const int lpt = wide ? 8 : 4;
+    const int64_t ldp = (c->ld + lpt - 1) / lpt * lpt;
+    const size_t smem = sizeof(int32_t) * ldp + sizeof(uint32_t) * 3 * (32 + 32 * lpt) * 8;
     if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
     const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 8);
-    auto kern = pass == 1 ? (g->uniform ? k_pull<1, true> : k_pull<1, false>)
-                          : (g->uniform ? k_pull<2, true> : k_pull<2, false>);
+    auto kern = wide ? (pass == 1 ? (g->uniform ? k_pull<1, true, 8> : k_pull<1, false, 8>)
+                                  : (g->uniform ? k_pull<2, true, 8> : k_pull<2, false, 8>))
+                     : (pass == 1 ? (g->uniform ? k_pull<1, true, 4> : k_pull<1, false, 4>)
+                                  : (g->uniform ? k_pull<2, true, 4> : k_pull<2, false, 4>));
     if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<blocks, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld,
                                        c->L, hooks);

@@ -114,7 +114,7 @@ def test_select_seeds_on_host_arrays_matches_oracle(gpu, orc, name):
 
 @pytest.mark.parametrize("mode", ["enum", "pull", "dense", "hybrid"])
 @pytest.mark.parametrize("name", ["er_big_1000", "er_uniform_r24", "er_wc_r40", "er_const1_r16",
-                                  "er_const0_r16", "er_pad20", "kat_dead_middle", "cfg_c1"])
+                                  "er_const0_r16", "er_pad20", "kat_dead_middle", "cfg_c1", "cfg_c2"])
 def test_every_sampler_strategy_reaches_the_reference_fixpoint(gpu, name, mode, monkeypatch):
     """The three sampler/hook strategies (interval enumeration, pull
     first-hop forest + rest unions, dense edge-major scan) give the
@@ -255,3 +255,19 @@ def test_celf_oversized_round_matches_oracle(gpu, orc, trace_cap, monkeypatch):
     got = run.selection.trace.array
     assert len(got) > 16384
     assert np.array_equal(got, want["trace"])
+
+
+@pytest.mark.parametrize("cfg,R", [("c2p1", 512), ("c5", 256)])
+def test_wide_lane_strategies_agree_at_config_scale(gpu, cfg, R, monkeypatch):
+    """8-lanes-per-thread pull passes (W >= 256) vs interval enumeration on
+    config graphs: identical labels (both are exact; the fixpoint is unique)."""
+    from paper_2008_03095_b200 import configs
+    g = configs.build(cfg)
+    randoms = gpu.SimulationRandoms(R, 1)
+    table = gpu.build_hash_table(g)
+    out = {}
+    for mode in ("pull", "enum", "hybrid"):
+        monkeypatch.setenv("IMX_HOOK", mode)
+        out[mode] = gpu.propagate(g, table, randoms)
+    assert np.array_equal(out["pull"], out["enum"])
+    assert np.array_equal(out["hybrid"], out["enum"])

@@ -122,13 +122,14 @@ __global__ void k_eval_worlds(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint6
 // the label cells of a vertex are touched by consecutive lanes.  Live
 // (edge, world) pairs go to a per-warp queue and are united 32 at a time,
 // so the root searches run warp-wide instead of at the live density.
+constexpr int kGrp = 8;                   // draws per thread between warp-level enqueues
 __global__ void __launch_bounds__(128) k_eval_hook(const int2 *__restrict__ ce, const uint64_t *__restrict__ t53,
                                                    int64_t me, const ulonglong2 *__restrict__ jt,
                                                    const ulonglong2 *__restrict__ ws, uint64_t i_hi,
                                                    uint64_t i_lo, int32_t nw, uint32_t *L, int64_t ld) {
     __shared__ int2 se[kRun];
-    __shared__ uint64_t st[kRun];
-    __shared__ uint32_t qe[4][64];
+    __shared__ uint64_t st[kRun + kGrp];
+    __shared__ uint32_t qe[4][32 + 32 * kGrp];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu;
     const u128 inc = ((u128)i_hi << 64) | i_lo, M = pcg_mult();
@@ -138,38 +139,61 @@ __global__ void __launch_bounds__(128) k_eval_hook(const int2 *__restrict__ ce, 
     if (act) Sw = ((u128)ws[r].x << 64) | ws[r].y;
     const int64_t nruns = (me + kRun - 1) / kRun;
     uint32_t *q = qe[warp];
+    const int rbase = blockIdx.x * 128;
     for (int64_t j = blockIdx.y; j < nruns; j += gridDim.y) {
         const int64_t e0 = j * kRun;
         const int cnt = (int)(me - e0 < kRun ? me - e0 : kRun);
         __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += 128) {
-            se[i] = ce[e0 + i];
-            st[i] = t53[e0 + i];
+        for (int i = threadIdx.x; i < kRun + kGrp; i += 128) {
+            if (i < cnt) {
+                se[i] = ce[e0 + i];
+                st[i] = t53[e0 + i];
+            } else {
+                st[i] = 0;                    // never live: draws past the run are discarded
+            }
         }
         __syncthreads();
         const ulonglong2 a2 = jt[2 * j], c2 = jt[2 * j + 1];
         u128 s = (((u128)a2.x << 64) | a2.y) * Sw + (((u128)c2.x << 64) | c2.y);
         int qn = 0;
-        for (int i = 0; i < cnt; ++i) {
-            s = s * M + inc;
-            const bool live = act && (pcg_output(s) >> 11) < st[i];
-            const unsigned m = __ballot_sync(FULL, live);
-            if (!m) continue;
-            if (live) q[qn + __popc(m & ((1u << lane) - 1))] = ((uint32_t)i << 8) | (uint32_t)threadIdx.x;
-            qn += __popc(m);
+        for (int i0 = 0; i0 < cnt; i0 += kGrp) {
+            // kGrp LCG steps, live edges as a bit mask (no per-draw warp vote)
+            unsigned bits = 0;
+#pragma unroll
+            for (int k = 0; k < kGrp; ++k) {
+                s = s * M + inc;
+                bits |= (unsigned)((pcg_output(s) >> 11) < st[i0 + k]) << k;
+            }
+            if (!act) bits = 0;
+            if (!__any_sync(FULL, bits)) continue;
+            // warp prefix sum of the live counts -> queue slots
+            const int c = __popc(bits);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int pos = qn + incl - c;
+            while (bits) {
+                const int k = __ffs(bits) - 1;
+                bits &= bits - 1;
+                q[pos++] = ((uint32_t)(i0 + k) << 8) | (uint32_t)threadIdx.x;
+            }
+            qn += __shfl_sync(FULL, incl, 31);
             __syncwarp();
-            if (qn >= 32) {
+            while (qn >= 32) {
                 qn -= 32;
                 const uint32_t x = q[qn + lane];
                 __syncwarp();
                 const int2 ed = se[x >> 8];
-                unite(L, ld, (uint32_t)ed.x, (uint32_t)ed.y, blockIdx.x * 128 + (int)(x & 255));
+                unite(L, ld, (uint32_t)ed.x, (uint32_t)ed.y, rbase + (int)(x & 255));
             }
         }
         if (lane < qn) {
             const uint32_t x = q[lane];
             const int2 ed = se[x >> 8];
-            unite(L, ld, (uint32_t)ed.x, (uint32_t)ed.y, blockIdx.x * 128 + (int)(x & 255));
+            unite(L, ld, (uint32_t)ed.x, (uint32_t)ed.y, rbase + (int)(x & 255));
         }
         __syncwarp();
     }

@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(256, 4) k_celf_rounds(
     int32_t k, int vb, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, uint32_t *__restrict__ cov,
     int64_t ld, int32_t ns, int32_t cw, int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
     int32_t *oid0, int32_t *oid1, unsigned long long *okey0, unsigned long long *okey1,
-    int64_t *__restrict__ fresh, unsigned long long *__restrict__ bkey, int32_t *__restrict__ bid,
+    int64_t *__restrict__ fresh,
     unsigned long long *__restrict__ skey, int32_t *__restrict__ sid,
     int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
@@ -796,9 +796,7 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     const int64_t n = c->g->n;
     if (!c->cdev) {
         IMX_CUDA(pool_alloc((void **)&c->cdev, sizeof(CelfDev), c->st));
-        IMX_CUDA(pool_alloc((void **)&c->bkey, sizeof(unsigned long long) * kMaxRank, c->st));
         IMX_CUDA(pool_alloc((void **)&c->skey, sizeof(unsigned long long) * kMaxRank, c->st));
-        IMX_CUDA(pool_alloc((void **)&c->bid, sizeof(int32_t) * kMaxRank, c->st));
         IMX_CUDA(pool_alloc((void **)&c->sid, sizeof(int32_t) * kMaxRank, c->st));
         c->trace_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(4 * n + 4096, 1 << 21));
         if (const char *tc = getenv("IMX_CELF_TRACE_CAP")) c->trace_cap = std::max<int64_t>(8, atoll(tc));
@@ -837,8 +835,8 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     int32_t ns = c->ns, cw = c->cw;
     int64_t *per_sim = c->per_sim, *fresh = c->eval_out, *trace = c->dtrace, *sg = c->dsgains;
     uint8_t *inS = c->inS;
-    int32_t *o0 = c->oid[0], *o1 = c->oid[1], *bid = c->bid, *sid = c->sid, *sd = c->dseeds;
-    unsigned long long *k0 = c->okey[0], *k1 = c->okey[1], *bkey = c->bkey, *skey = c->skey;
+    int32_t *o0 = c->oid[0], *o1 = c->oid[1], *sid = c->sid, *sd = c->dseeds;
+    unsigned long long *k0 = c->okey[0], *k1 = c->okey[1], *skey = c->skey;
     int64_t cap = c->trace_cap;
     CelfDev *stp = c->cdev;
     // next round's first batch = bpct% of this round's refreshed prefix
@@ -849,7 +847,7 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     if (const char *gv = getenv("IMX_CELF_GROUPS")) ngroup = std::min(8, std::max(1, atoi(gv)));
     while (ngroup & (ngroup - 1)) --ngroup;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
-                    &bkey, &bid, &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup};
+                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup};
     IMX_CUDA(cudaLaunchCooperativeKernel(fn, grid_cache[enc], 256, args, 0, c->st));
     count_launch(c);
     IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
@@ -857,7 +855,7 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     c->big_key = h.big_key;
     c->big_kr = (h.status == 2 || h.status == 4) ? h.big_kr : 0;
     if (getenv("IMX_CELF_PROFILE"))
-        fprintf(stderr, "[celf] rounds %d..%d grid %d: eval %.1f us, commit %.1f us, rank %.1f us, merge %.1f us; "
+        fprintf(stderr, "[celf] rounds %d..%d grid %d: eval %.1f us, trace+rank+commit %.1f us, (unused) %.1f us, merge %.1f us; "
                 "%llu eval steps, %llu evaluations (block 0 evals %.1f us, eval barrier %.1f us, batch max %.1f us)\n",
                 t, h.t, grid_cache[enc], h.prof[0] * 1e-3, h.prof[1] * 1e-3,
                 h.prof[2] * 1e-3, h.prof[3] * 1e-3, h.prof[4], h.prof[5], h.prof[6] * 1e-3, h.prof[7] * 1e-3,

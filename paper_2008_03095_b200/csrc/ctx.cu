@@ -67,7 +67,7 @@ void ctx_free(imx_ctx *c) {
     void *ptrs[] = {c->X, c->L, c->C, c->gains, c->inS, c->cov, c->per_sim, c->oid[0], c->oid[1],
                     c->okey[0], c->okey[1], c->scratch, c->eval_out, c->d_one,
                     c->sort_tmp, c->d_ids, c->d_vals, c->seg_a, c->seg_n, c->seg_off, c->scan_tmp,
-                    c->cdev, c->bkey, c->skey, c->bid, c->sid, c->dtrace, c->dseeds, c->dsgains};
+                    c->cdev, c->skey, c->sid, c->dtrace, c->dseeds, c->dsgains};
     for (void *p : ptrs) if (p) cudaFreeAsync(p, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     pinned_put(c->h_ids, sizeof(int32_t) * c->stage_cap);

@@ -78,8 +78,8 @@ struct imx_ctx {
     int64_t trace_n = 0, trace_hcap = 0;
     // persistent CELF kernel state and buffers
     CelfDev *cdev = nullptr;
-    unsigned long long *bkey = nullptr, *skey = nullptr;
-    int32_t *bid = nullptr, *sid = nullptr;
+    unsigned long long *skey = nullptr;   // refreshed keys ranked by fresh gain
+    int32_t *sid = nullptr;
     int64_t *dtrace = nullptr;
     int64_t trace_cap = 0;
     unsigned long long big_key = 0;   // last kernel stop on an oversized round

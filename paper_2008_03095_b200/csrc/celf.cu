@@ -408,8 +408,42 @@ __global__ void __launch_bounds__(256, 4) k_celf_rounds(
                 if (prof) ts = gtimer();
                 // slot (sstep+2)&3 was last read before the previous barrier
                 if (gtid == 0) st->smax[(sstep + 2) & 3] = 0;
-                // ngroup candidates per CTA at a time, 256/ngroup threads each
-                for (int64_t base = lo + (int64_t)blockIdx.x * ngroup; base < hi;
+                // huge batches (a round that refreshes most vertices): throughput
+                // over latency -- a warp per candidate, per-warp max folded once
+                const bool wide = hi - lo > (int64_t)gridDim.x * 8 && ns <= 4096;
+                if (wide) {
+                    unsigned long long wmax = 0;
+                    const int wl = threadIdx.x & 31;
+                    for (int64_t i = lo + (gtid >> 5); i < hi; i += gthreads >> 5) {
+                        const int64_t u = oid[ostart + i];
+                        const int nqs = (ns + 3) >> 2;
+                        const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
+                        unsigned long long acc = 0;
+                        for (int q = wl; q < nqs; q += 32) {
+                            const uint4 l4 = row[q];
+                            const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+                            uint32_t wd[4], sz[4];
+                            const int r = q << 2;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const bool in = r + j < ns;
+                                uint32_t lab = 0;
+                                sz[j] = in ? cell_size<ENC>(L, C, ld, (uint32_t)u, lv[j], r + j, lab) : 0u;
+                                wd[j] = in ? cov[(int64_t)lab * cw + ((r + j) >> 5)] : 0xffffffffu;
+                            }
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if (!((wd[j] >> ((r + j) & 31)) & 1u)) acc += sz[j];
+                        }
+                        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                        if (wl == 0) fresh[i] = (int64_t)acc;
+                        const unsigned long long fk = (acc << vb) | (unsigned long long)(vmask - (uint32_t)u);
+                        wmax = fk > wmax ? fk : wmax;
+                    }
+                    if (wl == 0 && wmax) atomicMax(&st->smax[sstep & 3], wmax);
+                }
+                // otherwise ngroup candidates per CTA at a time, 256/ngroup threads each
+                for (int64_t base = lo + (int64_t)blockIdx.x * ngroup; !wide && base < hi;
                      base += (int64_t)gridDim.x * ngroup) {
                     const int gsz = blockDim.x / ngroup, g = threadIdx.x / gsz;
                     const int64_t i = base + g;

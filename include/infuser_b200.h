@@ -176,6 +176,11 @@ int  imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out,
  * (vertex, stale_gain, fresh_gain, committed, seeds_before) -- TraceRecord,
  * selection.py:25-33 -- up to cap records.                                 */
 int  imx_celf_trace(imx_ctx *c, int64_t *out, int64_t cap);
+/* The same trace without a copy: *out = the context's pinned host buffer of
+ * *len records (NULL when empty), now owned by the caller -- release it with
+ * imx_host_free.  The context starts a new buffer for its next select.     */
+int  imx_celf_trace_take(imx_ctx *c, int64_t **out, int64_t *len);
+void imx_host_free(void *p);
 /* per_sim[r] = covered vertices of lane r (SelectionResult.spread_se,
  * selection.py:105-112), for this window's scored lanes.                  */
 int  imx_per_sim(imx_ctx *c, int64_t *out);

@@ -83,6 +83,8 @@ _SIGNATURES = {
     "imx_commit": (c_i32, [c_void_p, c_i32, P(c_i64)]),
     "imx_celf_select": (c_i32, [c_void_p, c_i32, c_void_p, c_void_p, P(c_i64)]),
     "imx_celf_trace": (c_i32, [c_void_p, c_void_p, c_i64]),
+    "imx_celf_trace_take": (c_i32, [c_void_p, P(c_void_p), P(c_i64)]),
+    "imx_host_free": (None, [c_void_p]),
     "imx_per_sim": (c_i32, [c_void_p, c_void_p]),
     "imx_copy_owned": (c_i32, [c_void_p, c_void_p]),
     "imx_evaluate_seeds": (c_i32, [c_void_p, c_void_p, c_i32, c_i64, c_void_p, c_i64, c_void_p]),

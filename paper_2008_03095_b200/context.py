@@ -10,6 +10,7 @@ per-rank "shard" the multi-GPU CELF driver (celf.py) talks to.
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -28,6 +29,19 @@ def empty_graph(n: int):
     g = Graph(np.zeros(n + 1, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float64),
               np.arange(n, dtype=np.int64))
     return g
+
+
+def _take_trace(handle) -> np.ndarray:
+    """The (T, 5) trace as a zero-copy view of the library's pinned buffer,
+    returned to the library's pinned cache when the array is collected."""
+    lib = _lib.load()
+    p, n = ctypes.c_void_p(), ctypes.c_int64()
+    check(lib.imx_celf_trace_take(handle, ctypes.byref(p), ctypes.byref(n)))
+    if not p.value:
+        return np.empty((0, 5), np.int64)
+    buf = (ctypes.c_int64 * (5 * n.value)).from_address(p.value)
+    weakref.finalize(buf, lib.imx_host_free, p.value)
+    return np.frombuffer(buf, dtype=np.int64).reshape(n.value, 5)
 
 
 class DeviceContext:
@@ -154,9 +168,7 @@ class DeviceContext:
         gains = np.empty(k, np.int64)
         tl = ctypes.c_int64()
         check(lib.imx_celf_select(self.handle, int(k), ptr(seeds), ptr(gains), ctypes.byref(tl)))
-        trace = np.empty((tl.value, 5), np.int64)
-        check(lib.imx_celf_trace(self.handle, ptr(trace), tl.value))
-        return seeds, gains, trace
+        return seeds, gains, _take_trace(self.handle)
 
     def per_sim(self) -> np.ndarray:
         out = np.empty(self.num_scored, np.int64)

@@ -1067,6 +1067,20 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     return IMX_OK;
 }
 
+extern "C" int imx_celf_trace_take(imx_ctx *c, int64_t **out, int64_t *len) {
+    CTX_CHECK(c);
+    if (!out || !len) { set_error("NULL argument"); return IMX_EINVAL; }
+    *len = c->trace_n / 5;
+    *out = nullptr;
+    if (*len == 0) return IMX_OK;
+    *out = c->trace;
+    pinned_lend(c->trace, sizeof(int64_t) * c->trace_hcap);
+    c->trace = nullptr;
+    c->trace_n = 0;
+    c->trace_hcap = 0;
+    return IMX_OK;
+}
+
 extern "C" int imx_celf_trace(imx_ctx *c, int64_t *out, int64_t cap) {
     CTX_CHECK(c);
     const int64_t len = c->trace_n / 5;

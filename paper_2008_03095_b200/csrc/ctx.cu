@@ -38,6 +38,14 @@ void pinned_put(void *p, size_t bytes) {
     g_pin_free.emplace_back(p, bytes);
 }
 
+// pinned buffers handed to the caller (imx_celf_trace_take) and their sizes
+static std::vector<std::pair<void *, size_t>> g_pin_lent;
+
+void pinned_lend(void *p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_lent.emplace_back(p, bytes);
+}
+
 // The label/count matrices come from the device's stream-ordered pool with an
 // unbounded release threshold, so back-to-back runs on the same graph reuse
 // the memory instead of paying cudaMalloc/cudaFree every time.
@@ -190,3 +198,21 @@ int trace_reserve(imx_ctx *c, int64_t cnt) {
     return IMX_OK;
 }
 }  // namespace imx
+
+using namespace imx;
+
+// return a buffer lent by imx_celf_trace_take to the pinned cache
+extern "C" void imx_host_free(void *p) {
+    if (!p) return;
+    size_t bytes = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        for (size_t i = 0; i < g_pin_lent.size(); ++i)
+            if (g_pin_lent[i].first == p) {
+                bytes = g_pin_lent[i].second;
+                g_pin_lent.erase(g_pin_lent.begin() + i);
+                break;
+            }
+    }
+    if (bytes) pinned_put(p, bytes);
+}

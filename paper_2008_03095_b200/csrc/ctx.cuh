@@ -116,6 +116,7 @@ int ensure_celf_buffers(imx_ctx *c);
 int trace_reserve(imx_ctx *c, int64_t cnt);
 cudaError_t pinned_get(void **p, size_t bytes);
 void pinned_put(void *p, size_t bytes);
+void pinned_lend(void *p, size_t bytes);   // handed to the caller; imx_host_free returns it
 int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);
 // raw label-matrix passes shared with the evaluation worlds (evaluation.cu)

@@ -271,3 +271,26 @@ def test_wide_lane_strategies_agree_at_config_scale(gpu, cfg, R, monkeypatch):
         out[mode] = gpu.propagate(g, table, randoms)
     assert np.array_equal(out["pull"], out["enum"])
     assert np.array_equal(out["hybrid"], out["enum"])
+
+
+def test_trace_buffers_are_owned_by_their_results(gpu):
+    """celf_select hands its pinned trace buffer to the result (zero copy);
+    a second select on the same context must not touch the first trace."""
+    from paper_2008_03095_b200.context import DeviceContext
+    z = load_golden("er_mid_300")
+    g = build_graph(gpu, z)
+    randoms = gpu.SimulationRandoms(int(z["R"]), int(z["master_seed"]))
+    gpu.build_hash_table(g).bind(g)
+    ctx = DeviceContext(g, randoms.values, randoms.num_scored)
+    ctx.propagate()
+    ctx.memoize(want_gains=False)
+    ctx.celf_reset(None)
+    s1, g1, t1 = ctx.celf_select(int(z["k"]))
+    ctx.celf_reset(None)
+    s2, g2, t2 = ctx.celf_select(2)
+    assert np.array_equal(t1, z["trace"])
+    assert t2.shape[0] < t1.shape[0] and np.array_equal(t2, z["trace"][: len(t2)])
+    del t1
+    import gc
+    gc.collect()
+    assert np.array_equal(t2, z["trace"][: len(t2)])

@@ -141,7 +141,19 @@ __global__ void k_xadj_from_src(const int32_t *__restrict__ src, int64_t m2, int
     }
 }
 
-// src[s] = row of slot s (np.repeat over degrees, graph.py:75-78)
+// src[s] = row of slot s (np.repeat over degrees, graph.py:75-78): one warp
+// per vertex writes its row (coalesced, no search)
+__global__ void k_src_rows(const int64_t *__restrict__ xadj, int64_t n, int64_t m2, int32_t *__restrict__ src) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t a = xadj[v], b = xadj[v + 1];
+        if (a < 0 || b > m2 || a > b) continue;      // corrupt offsets: flagged by k_check_xadj
+        for (int64_t s = a + lane; s < b; s += 32) src[s] = (int32_t)v;
+    }
+}
+
+// (binary-search form, kept for callers that only have the offsets)
 __global__ void k_src_from_xadj(const int64_t *__restrict__ xadj, int64_t n, int64_t m2,
                                 int32_t *__restrict__ src) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
@@ -155,24 +167,27 @@ __global__ void k_src_from_xadj(const int64_t *__restrict__ xadj, int64_t n, int
     }
 }
 
-// reciprocal slot of (u, v): position of u in row v (rows sorted ascending);
-// flags: 8 = a slot without reciprocal, 32 = adjacency entry outside 0..n-1
+// Reciprocal slots and symmetrized thresholds in one pass.  Only slots with
+// u < v search (u in the larger id's row v); each such pair writes both
+// directions of recip and of thr = max(thr(w[s]), thr(w[reciprocal])), and
+// the threshold statistics.  recip starts at -1; k_recip_check flags slots
+// no search reached and duplicate slots.  flags: 8 = a slot without
+// reciprocal, 32 = adjacency entry outside 0..n-1, 64 = corrupt offsets.
+struct GStats;
 __global__ void k_reciprocal(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
-                             const int32_t *__restrict__ src, int64_t n, int64_t m2,
-                             int64_t *__restrict__ recip, unsigned *__restrict__ flags) {
+                             const int32_t *__restrict__ src, const double *__restrict__ w, int64_t n,
+                             int64_t m2, int64_t *__restrict__ recip, int32_t *__restrict__ thr,
+                             GStats *__restrict__ gs);
+__global__ void k_recip_check(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                              const int32_t *__restrict__ src, const int64_t *__restrict__ recip,
+                              int64_t m2, unsigned *__restrict__ flags) {
+    bool bad = false;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
          s += (int64_t)gridDim.x * blockDim.x) {
-        int32_t u = src[s], v = adj[s];
-        if (v < 0 || v >= n) { recip[s] = -1; atomicOr(flags, 32u | 8u); continue; }
-        int64_t lo = xadj[v], hi = xadj[v + 1];
-        if (lo < 0 || hi > m2 || lo > hi) { recip[s] = -1; atomicOr(flags, 64u | 8u); continue; }
-        while (lo < hi) {
-            int64_t mid = (lo + hi) >> 1;
-            if (adj[mid] < u) lo = mid + 1; else hi = mid;
-        }
-        if (lo < xadj[v + 1] && adj[lo] == u && lo != s) recip[s] = lo;
-        else { recip[s] = -1; atomicOr(flags, 8u); }
+        // unpaired, or a repeated neighbour in a sorted row (it pairs once)
+        bad |= recip[s] < 0 || (s > 0 && s > xadj[src[s]] && adj[s] == adj[s - 1]);
     }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 8u);
 }
 
 __global__ void k_slot_hashes(const int32_t *__restrict__ src, const int32_t *__restrict__ adj,
@@ -236,6 +251,52 @@ __global__ void k_thresholds(const double *__restrict__ w, const int64_t *__rest
     }
 }
 
+__global__ void k_reciprocal(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                             const int32_t *__restrict__ src, const double *__restrict__ w, int64_t n,
+                             int64_t m2, int64_t *__restrict__ recip, int32_t *__restrict__ thr,
+                             GStats *__restrict__ gs) {
+    int32_t lmin = INT32_MAX, lmax = INT32_MIN;
+    unsigned long long lsum = 0;
+    unsigned fl = 0;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = src[s], v = adj[s];
+        if (v < 0 || v >= n) { fl |= 32u | 8u; continue; }
+        if (u >= v) { if (u == v) fl |= 8u; continue; }          // paired from the other side
+        int64_t lo = xadj[v], hi = xadj[v + 1];
+        if (lo < 0 || hi > m2 || lo > hi) { fl |= 64u | 8u; continue; }
+        const int64_t end = hi;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (adj[mid] < u) lo = mid + 1; else hi = mid;
+        }
+        if (lo < end && adj[lo] == u) {
+            recip[s] = lo;
+            recip[lo] = s;
+            const int32_t t1 = thr_of(w[s]), t2 = thr_of(w[lo]);
+            const int32_t t = t1 > t2 ? t1 : t2;
+            thr[s] = t;
+            thr[lo] = t;
+            lmin = min(lmin, t); lmax = max(lmax, t);
+            lsum += (unsigned long long)(uint32_t)t;
+        } else {
+            fl |= 8u;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+        lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&gs->tmin, lmin);
+        atomicMax(&gs->tmax, lmax);
+        if (lsum) atomicAdd(&gs->tsum, lsum);
+        if (fl) atomicOr(&gs->flags, fl);
+    }
+}
+
 __global__ void k_weights_range(const double *__restrict__ w, int64_t m2, unsigned *flags) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
          s += (int64_t)gridDim.x * blockDim.x) {
@@ -289,6 +350,18 @@ __global__ void k_permute_edges(const uint32_t *__restrict__ perm, int64_t me,
         E[j] = E0[e];
         EH[j] = EH0[e];
         ET[j] = ET0[e];
+    }
+}
+// one threshold bucket: the sorted keys are the hashes and every threshold
+// is thr_u, so only the endpoints are gathered
+__global__ void k_permute_uniform(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ keys, int64_t me,
+                                  const int2 *__restrict__ E0, int32_t tu, int2 *__restrict__ E,
+                                  int32_t *__restrict__ EH, int32_t *__restrict__ ET) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < me;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        E[j] = E0[perm[j]];
+        EH[j] = (int32_t)keys[j];
+        ET[j] = tu;
     }
 }
 // bucket offsets from the sorted keys; per-bucket max threshold (reduced
@@ -478,7 +551,8 @@ static int graph_build_index(imx_graph *g) {
         GI(cub::DeviceRadixSort::SortPairs(tmp, tb, hk, k32b, v32, v32b, (int)me, 0, 31, st));
         note_launch(4);
         g_clock.mark("index: sort", st);
-        k_permute_edges<<<grid_for(me), 256, 0, st>>>(v32b, me, E0, EH0, ET0, g->E, g->EH, g->ET); note_launch();
+        k_permute_uniform<<<grid_for(me), 256, 0, st>>>(v32b, k32b, me, E0, g->thr_u, g->E, g->EH, g->ET);
+        note_launch();
         GI(cudaGetLastError());
         k_uniform_meta<<<1, 1, 0, st>>>(me, g->thr_u, g->boff, g->btmax); note_launch();
         GI(cudaGetLastError());
@@ -529,14 +603,21 @@ static int graph_analyze(imx_graph *g, bool structure) {
     if (structure) {
         if (!g->src) {
             IMX_TRY(dalloc(g, &g->src, m2));
-            if (m2) { k_src_from_xadj<<<grid_for(m2), 256, 0, st>>>(g->xadj, n, m2, g->src); note_launch(); }
+            if (m2) {
+                IMX_CUDA(cudaMemsetAsync(g->src, 0, sizeof(int32_t) * m2, st));   // rows of corrupt offsets
+                k_src_rows<<<grid_for(n * 32), 256, 0, st>>>(g->xadj, n, m2, g->src);
+                note_launch();
+            }
         }
         IMX_TRY(dalloc(g, &g->hash, m2));
         IMX_TRY(dalloc(g, &g->thr, m2));
         IMX_TRY(dalloc(g, &g->recip, m2));
         IMX_TRY(dalloc(g, &g->cslot, m2));
         if (m2) {
-            k_reciprocal<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, n, m2, g->recip, &gs->flags);
+            IMX_CUDA(cudaMemsetAsync(g->recip, 0xff, sizeof(int64_t) * m2, st));     // -1
+            k_reciprocal<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, g->w, n, m2, g->recip, g->thr, gs);
+            k_recip_check<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, g->recip, m2, &gs->flags);
+            note_launch();
             k_slot_hashes<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, g->hash);
             k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, m2, &gs->maxp);
             k_check_xadj<<<grid_for(n), 256, 0, st>>>(g->xadj, n, m2, &gs->flags);
@@ -558,8 +639,9 @@ static int graph_analyze(imx_graph *g, bool structure) {
     }
     // thresholds: symmetrized through the reciprocal slots unless the
     // adjacency is known not to be symmetric (a structure pass decides below)
+    // (a structure pass computed them with the reciprocal search)
     const bool sym_try = structure || g->symmetric;
-    if (m2) {
+    if (m2 && !structure) {
         k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, sym_try ? g->recip : nullptr, g->src, g->adj, g->hash,
                                                    m2, g->thr, gs);
         note_launch();

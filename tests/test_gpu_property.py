@@ -1,0 +1,54 @@
+"""Randomised parity: many small seeded graphs (isolated vertices, hubs,
+paths, p in {0, 1, random}, widths that are not multiples of 32, k up to n)
+through every sampler strategy and the whole pipeline vs the C oracle."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def random_graph(rng):
+    n = int(rng.integers(2, 160))
+    kind = rng.integers(0, 4)
+    if kind == 0:        # sparse random
+        m = int(rng.integers(0, 3 * n))
+        e = rng.integers(0, n, size=(m, 2))
+    elif kind == 1:      # star + noise
+        e = np.column_stack([np.zeros(n - 1, int), np.arange(1, n)])
+        e = np.vstack([e, rng.integers(0, n, size=(n // 3, 2))])
+    elif kind == 2:      # path with chords
+        e = np.column_stack([np.arange(n - 1), np.arange(1, n)])
+        e = np.vstack([e, rng.integers(0, n, size=(n // 5, 2))])
+    else:                # dense-ish block + isolated tail
+        h = max(2, n // 3)
+        e = rng.integers(0, h, size=(4 * h, 2))
+    e = e[e[:, 0] != e[:, 1]]
+    lo, hi = np.minimum(e[:, 0], e[:, 1]), np.maximum(e[:, 0], e[:, 1])
+    key = np.unique(lo * n + hi)
+    e = np.column_stack([key // n, key % n]).astype(np.int64)
+    p = rng.choice([0.0, 1.0, -1.0, -1.0, -1.0])
+    w = rng.random(len(e)) if p < 0 else np.full(len(e), p)
+    return n, e, w
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_graphs_match_oracle(gpu, orc, seed, monkeypatch):
+    rng = np.random.default_rng(1000 + seed)
+    n, e, w = random_graph(rng)
+    g = gpu.Graph.from_edges(n, e, w)
+    R = int(rng.integers(1, 300))
+    k = int(rng.integers(1, n + 1))
+    want = orc.run_fused(g.xadj, g.adj, g.weights, k, R, seed, nthreads=2)
+    for mode in ("enum", "pull", "dense", "hybrid", None):
+        if mode:
+            monkeypatch.setenv("IMX_HOOK", mode)
+        else:
+            monkeypatch.delenv("IMX_HOOK", raising=False)
+        run = gpu.run_fused(g, k, num_simulations=R, master_seed=seed)
+        assert np.array_equal(run.labels, want["labels"]), mode          # (n, padded R)
+        assert np.array_equal(run.sizes, want["sizes"]), mode
+        assert [int(s) for s in run.seeds] == want["seeds"].tolist(), mode
+        assert list(run.selection.gains) == want["seed_gains"].tolist(), mode
+        assert np.array_equal(run.selection.trace.array, want["trace"]), mode
+        assert run.spread_se == pytest.approx(want["spread_se"], rel=1e-12, abs=0)

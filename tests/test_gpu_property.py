@@ -52,3 +52,16 @@ def test_random_graphs_match_oracle(gpu, orc, seed, monkeypatch):
         assert list(run.selection.gains) == want["seed_gains"].tolist(), mode
         assert np.array_equal(run.selection.trace.array, want["trace"]), mode
         assert run.spread_se == pytest.approx(want["spread_se"], rel=1e-12, abs=0)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_evaluate_matches_oracle(gpu, orc, seed):
+    from paper_2008_03095_b200.evaluation import evaluate_counts
+    rng = np.random.default_rng(5000 + seed)
+    n, e, w = random_graph(rng)
+    g = gpu.Graph.from_edges(n, e, w)
+    seeds = rng.integers(0, n, size=int(rng.integers(1, 12)))
+    r_eval = int(rng.choice([1, 7, 4095, 4096, 4097, 9000]))
+    got = evaluate_counts(g, seeds, r_eval, seed)
+    want = orc.evaluate_counts(g.xadj, g.adj, g.weights, seeds, r_eval, seed, nthreads=2)
+    assert np.array_equal(got, want)

@@ -54,15 +54,25 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
     for (int64_t v = wg; v < n; v += nw) {
         const uint4 *Lr = reinterpret_cast<const uint4 *>(L + v * ld);
         unsigned long long acc = 0;
-        for (int q = lane; q < nqs; q += 32) {
-            const uint4 l = __ldg(Lr + q);
-            const uint32_t w[4] = {l.x, l.y, l.z, l.w};
-            const int r = q << 2;
+        // two quads per step, all eight root gathers issued before any is used
+        for (int q0 = lane; q0 < nqs; q0 += 64) {
+            uint32_t w[8];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (r + j >= ns) break;
-                const uint32_t rw = is_root(w[j]) ? w[j] : __ldg(L + (int64_t)w[j] * ld + r + j);
-                acc += (rw & COUNT) + 1u;
+            for (int h = 0; h < 2; ++h) {
+                const int q = q0 + 32 * h;
+                const uint4 l = q < nqs ? __ldg(Lr + q) : make_uint4(ROOT, ROOT, ROOT, ROOT);
+                w[4 * h] = l.x; w[4 * h + 1] = l.y; w[4 * h + 2] = l.z; w[4 * h + 3] = l.w;
+            }
+            uint32_t rw[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int r = ((q0 + 32 * (k >> 2)) << 2) + (k & 3);
+                rw[k] = is_root(w[k]) ? w[k] : __ldg(L + (int64_t)w[k] * ld + r);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int r = ((q0 + 32 * (k >> 2)) << 2) + (k & 3);
+                if (r < ns) acc += (rw[k] & COUNT) + 1u;
             }
         }
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

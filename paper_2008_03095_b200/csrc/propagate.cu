@@ -454,6 +454,20 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
         qn += __shfl_sync(FULL, inc, 31);
         cnt += c;
         __syncwarp();
+        // drain 64 at a time when possible: both parent words are loaded
+        // before either walk starts
+        while (qn >= 64) {
+            qn -= 64;
+            const uint32_t cv = qv[warp][qn + lane], cw = qw[warp][qn + lane];
+            const int cr = (int)qr[warp][qn + lane];
+            const uint32_t dv = qv[warp][qn + 32 + lane], dw = qw[warp][qn + 32 + lane];
+            const int dr = (int)qr[warp][qn + 32 + lane];
+            __syncwarp();
+            const uint32_t gw = cw < (uint32_t)kHot ? ld_ca(cell(L, ld, cw, cr)) : ld_relaxed(cell(L, ld, cw, cr));
+            const uint32_t hw = dw < (uint32_t)kHot ? ld_ca(cell(L, ld, dw, dr)) : ld_relaxed(cell(L, ld, dw, dr));
+            compress_cell(L, ld, lw, cv, cw, gw, cr, r0, hc);
+            compress_cell(L, ld, lw, dv, dw, hw, dr, r0, hc);
+        }
         while (qn >= 32) {
             qn -= 32;
             const uint32_t cv = qv[warp][qn + lane], cw = qw[warp][qn + lane];

@@ -454,8 +454,25 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
         qn += __shfl_sync(FULL, inc, 31);
         cnt += c;
         __syncwarp();
-        // drain 64 at a time when possible: both parent words are loaded
-        // before either walk starts
+        // drain 128 / 64 at a time when possible: every parent word is loaded
+        // before any walk starts
+        while (qn >= 128) {
+            qn -= 128;
+            uint32_t xv[4], xw[4], xg[4];
+            int xr[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                xv[h] = qv[warp][qn + 32 * h + lane];
+                xw[h] = qw[warp][qn + 32 * h + lane];
+                xr[h] = (int)qr[warp][qn + 32 * h + lane];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                xg[h] = xw[h] < (uint32_t)kHot ? ld_ca(cell(L, ld, xw[h], xr[h])) : ld_relaxed(cell(L, ld, xw[h], xr[h]));
+#pragma unroll
+            for (int h = 0; h < 4; ++h) compress_cell(L, ld, lw, xv[h], xw[h], xg[h], xr[h], r0, hc);
+        }
         while (qn >= 64) {
             qn -= 64;
             const uint32_t cv = qv[warp][qn + lane], cw = qw[warp][qn + lane];

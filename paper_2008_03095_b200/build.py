@@ -35,14 +35,30 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """One object per source, compiled in parallel (no device code crosses
+    translation units), then one shared link."""
     if not force and up_to_date():
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
+    objdir = OUT.parent / "obj"
+    objdir.mkdir(exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+    hdr_t = max(p.stat().st_mtime for p in HEADERS)
+    jobs = []
+    for src in SOURCES:
+        obj = objdir / (src.name + ".o")
+        if force or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, hdr_t):
+            cmd = [nvcc(), *compile_flags, "-c", "-o", str(obj), str(src)]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            jobs.append(subprocess.Popen(cmd))
+    if any(j.wait() != 0 for j in jobs):
+        raise subprocess.CalledProcessError(1, "nvcc")
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES)]
+    link = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *(str(objdir / (s.name + ".o")) for s in SOURCES)]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     os.replace(tmp, OUT)
     return OUT
 

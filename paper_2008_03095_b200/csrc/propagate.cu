@@ -184,29 +184,39 @@ __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
 // a forward walk), so consecutive threads read consecutive edges of the same
 // hash interval (coalesced) and every thread runs one union per pair.
 constexpr int kEnumChunk = 128;
+
+// largest s in [0, nseg) with off[s] <= j (off nondecreasing, off[0] = 0),
+// by the whole warp: a 33-ary search -- 32 pivots per step, one load each,
+// so ~log33(nseg) dependent loads instead of log2(nseg) on one lane
+__device__ __forceinline__ int64_t seg_search(const int64_t *__restrict__ off, int64_t nseg, int64_t j, int lane) {
+    int64_t lo = 0, hi = nseg;      // off[lo] <= j; hi == nseg or off[hi] > j
+    while (hi - lo > 1) {
+        const int64_t span = hi - lo;
+        const int64_t piv = lo + span * (lane + 1) / 33;
+        const unsigned b = __ballot_sync(0xffffffffu, __ldg(off + piv) <= j);
+        const int c = __popc(b);    // pivots are nondecreasing: b is a prefix of ones
+        const int64_t plo = __shfl_sync(0xffffffffu, piv, c > 0 ? c - 1 : 0);
+        const int64_t phi = __shfl_sync(0xffffffffu, piv, c < 32 ? c : 31);
+        if (c > 0) lo = plo;
+        if (c < 32) hi = phi;
+    }
+    return lo;
+}
+// Segments [s_lo, s_hi) (whole lanes) only.
 template <bool UNI, bool SKIP>
 __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ off, const int64_t *__restrict__ seg_a,
-                                                   int64_t nseg, int segs_per_lane,
+                                                   int64_t s_lo, int64_t s_hi, int segs_per_lane,
                                                    const int2 *__restrict__ E, const int32_t *__restrict__ EH,
                                                    const int32_t *__restrict__ ET, const int32_t *__restrict__ X,
                                                    int64_t ld, uint32_t *__restrict__ L,
                                                    unsigned long long *__restrict__ hooks) {
-    const int64_t total = off[nseg];
+    const int64_t jlo = off[s_lo], total = off[s_hi];
     const int lane = threadIdx.x & 31;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long nh = 0;
-    for (int64_t j0 = wg * kEnumChunk; j0 < total; j0 += nw * kEnumChunk) {
-        int64_t s = 0;
-        if (lane == 0) {
-            int64_t lo = 0, hi = nseg;       // largest s with off[s] <= j0
-            while (hi - lo > 1) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (off[mid] <= j0) lo = mid; else hi = mid;
-            }
-            s = lo;
-        }
-        s = __shfl_sync(0xffffffffu, s, 0);
+    for (int64_t j0 = jlo + wg * kEnumChunk; j0 < total; j0 += nw * kEnumChunk) {
+        int64_t s = s_lo + seg_search(off + s_lo, s_hi - s_lo, j0, lane);
         const int64_t jend = (total - j0 < kEnumChunk) ? total : j0 + kEnumChunk;
         for (int64_t j = j0 + lane; j < jend; j += 32) {
             while (off[s + 1] <= j) ++s;
@@ -631,8 +641,20 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest
     const int blocks = 148 * 8;
     auto kern = g->uniform ? (skip_forest ? k_hook_enum<true, true> : k_hook_enum<true, false>)
                            : (skip_forest ? k_hook_enum<false, true> : k_hook_enum<false, false>);
-    kern<<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, nseg, g->nb * 31, g->E, g->EH, g->ET, c->X, c->ld,
-                                    c->L, hooks);
+    // lanes per launch (IMX_ENUM_BLOCK, default all): launches run one after
+    // the other.  Measured: narrower blocks are slower on every config (C3:
+    // 7.2 ms at 2048 lanes, 8.5 ms at 256, 17.9 ms at 16) -- crowding the
+    // warps onto few lanes' trees costs more than the L2 reuse gains.
+    const char *eb = getenv("IMX_ENUM_BLOCK");
+    const int lb = eb && atoi(eb) > 0 ? atoi(eb) : c->W;
+    const int spl = g->nb * 31;
+    for (int l0 = 0; l0 < c->W; l0 += lb) {
+        const int l1 = std::min(c->W, l0 + lb);
+        kern<<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, (int64_t)l0 * spl, (int64_t)l1 * spl, spl, g->E, g->EH,
+                                        g->ET, c->X, c->ld, c->L, hooks);
+        IMX_CHECK_LAUNCH();
+        if (l1 < c->W) count_launch(c);
+    }
     IMX_CHECK_LAUNCH();
     count_launch(c, 3);
     return IMX_OK;

@@ -20,6 +20,30 @@ __device__ __forceinline__ bool is_root(uint32_t w) { return (w & ROOT) != 0; }
 // label of vertex v from its (compressed) cell word
 __device__ __forceinline__ uint32_t label_of(uint32_t v, uint32_t w) { return is_root(w) ? v : w; }
 
+// Hub cells during hooking.  On skewed graphs the lowest ids are the hubs
+// and the roots of the giant components, so every union in those
+// components ends at the same few cells of a lane: one L2 sector serialises
+// them.  Vertex 0 is a root in every lane (nothing is smaller), so its cell
+// is never read; the other hub ids below kHotHook are read through L1.  A
+// stale word is safe: a stale ROOT only makes a union link under, or
+// compare against, a node that is no longer a root but still has a smaller
+// id than what is linked under it (the tree stays min-rooted and the CAS on
+// a stale root fails and reports its parent); a stale parent is an ancestor.
+#ifndef IMX_HOT_HOOK
+#define IMX_HOT_HOOK 4
+#endif
+constexpr uint32_t kHotHook = IMX_HOT_HOOK;
+
+__device__ __forceinline__ uint32_t ld_hook(uint32_t *L, int64_t ld, uint32_t v, int r) {
+    if (kHotHook > 0 && v < kHotHook) {
+        if (v == 0) return ROOT;
+        uint32_t w;
+        asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(w) : "l"(cell(L, ld, v, r)));
+        return w;
+    }
+    return ld_relaxed(cell(L, ld, v, r));
+}
+
 // Two root searches advanced in lock step so their loads overlap.  Path
 // splitting: every visited node is re-pointed at its grandparent (benign
 // races -- any value ever stored in a cell is an ancestor in the same tree).
@@ -30,8 +54,8 @@ __device__ __forceinline__ void find2(uint32_t *L, int64_t ld, int r, uint32_t &
         const bool da = is_root(wa), db = is_root(wb);
         if (da && db) return;
         uint32_t ga = 0, gb = 0;
-        if (!da) ga = ld_relaxed(cell(L, ld, wa, r));
-        if (!db) gb = ld_relaxed(cell(L, ld, wb, r));
+        if (!da) ga = ld_hook(L, ld, wa, r);
+        if (!db) gb = ld_hook(L, ld, wb, r);
         if (!da) {
             if (!is_root(ga)) st_relaxed(cell(L, ld, xa, r), ga);
             xa = wa;
@@ -49,8 +73,8 @@ __device__ __forceinline__ void find2(uint32_t *L, int64_t ld, int r, uint32_t &
 // During hooking every root cell is exactly ROOT (member counts are only
 // written by the compress pass).  Returns 1 when a hook happened.
 __device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32_t b, int r) {
-    uint32_t wa = ld_relaxed(cell(L, ld, a, r));
-    uint32_t wb = ld_relaxed(cell(L, ld, b, r));
+    uint32_t wa = ld_hook(L, ld, a, r);
+    uint32_t wb = ld_hook(L, ld, b, r);
     find2(L, ld, r, a, wa, b, wb);
     while (a != b) {
         const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
@@ -58,7 +82,7 @@ __device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32
         if (old == ROOT) return 1;
         a = lo;
         b = hi;
-        find2(L, ld, r, a, ld_relaxed(cell(L, ld, lo, r)), b, old);
+        find2(L, ld, r, a, ld_hook(L, ld, lo, r), b, old);
     }
     return 0;
 }

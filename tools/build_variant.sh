@@ -1,0 +1,18 @@
+#!/bin/bash
+# Build a variant of libinfuser_b200.so with extra nvcc defines, for A/B runs:
+#   tools/build_variant.sh TAG -DNAME=VALUE ...  ->  paper_2008_03095_b200/lib/variants/libinfuser_b200_TAG.so
+# select it with INFUSER_B200_LIB=<path>
+set -e
+cd "$(dirname "$0")/.."
+tag=$1; shift
+out=paper_2008_03095_b200/lib/variants/$tag
+mkdir -p $out
+F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -diag-suppress 1444 $*"
+objs=""
+for s in graph.cu gen.cu ctx.cu propagate.cu memo.cu celf.cu evaluation.cu upload.cu io.cpp; do
+  nvcc $F -c -o $out/$s.o paper_2008_03095_b200/csrc/$s &
+  objs="$objs $out/$s.o"
+done
+wait
+nvcc $F -shared -cudart static -o paper_2008_03095_b200/lib/variants/libinfuser_b200_$tag.so $objs
+echo paper_2008_03095_b200/lib/variants/libinfuser_b200_$tag.so

@@ -290,21 +290,37 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
 #pragma unroll
             for (int k = 0; k < LPT; ++k) best[k] = ROOT;
             unsigned seen = 0;
+            // software-pipelined slot loads: the next slot's id, hash and
+            // threshold are in flight while this slot is tested
+            uint32_t nu = (uint32_t)v;
+            int32_t nhs = 0, nt = tu;
+            if (s0 < s1) {
+                nu = (uint32_t)__ldg(adj + s0);
+                nhs = __ldg(hash + s0);
+                if (!UNI) nt = __ldg(thr + s0);
+            }
             for (int64_t sl = s0; sl < s1; ++sl) {
-                const uint32_t u = (uint32_t)__ldg(adj + sl);
+                const uint32_t u = nu;
+                const int32_t h = nhs, t = UNI ? tu : nt;
                 if (u >= (uint32_t)v) break;
-                const int32_t h = __ldg(hash + sl);
-                const int32_t t = UNI ? tu : __ldg(thr + sl);
-                unsigned live = 0;
-#pragma unroll
-                for (int k = 0; k < LPT; ++k) live |= (unsigned)((x[k] ^ h) < t) << k;
-                live &= valid;
-                if (PASS == 1) {
-                    const unsigned fresh = live & ~seen;        // first live (= smallest) neighbour
-#pragma unroll
-                    for (int k = 0; k < LPT; ++k) best[k] = ((fresh >> k) & 1u) ? u : best[k];
-                    seen |= live;
+                if (sl + 1 < s1) {
+                    nu = (uint32_t)__ldg(adj + sl + 1);
+                    nhs = __ldg(hash + sl + 1);
+                    if (!UNI) nt = __ldg(thr + sl + 1);
                 } else {
+                    nu = (uint32_t)v;
+                }
+                if (PASS == 1) {
+                    // rows ascend, so the first live neighbour is the
+                    // smallest: one predicated min per lane
+#pragma unroll
+                    for (int k = 0; k < LPT; ++k)
+                        if ((x[k] ^ h) < t) best[k] = min(best[k], u);
+                } else {
+                    unsigned live = 0;
+#pragma unroll
+                    for (int k = 0; k < LPT; ++k) live |= (unsigned)((x[k] ^ h) < t) << k;
+                    live &= valid;
                     unsigned rest = live & seen;
                     seen |= live;
                     if (!__any_sync(FULL, rest != 0)) continue;
@@ -334,6 +350,11 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
                         nh += unite(L, ld, a2, b2, rr);
                     }
                 }
+            }
+            if (PASS == 1) {
+#pragma unroll
+                for (int k = 0; k < LPT; ++k)
+                    if (!((valid >> k) & 1u)) best[k] = ROOT;   // padding lanes stay roots
             }
             if (PASS == 1 && active) {
 #pragma unroll

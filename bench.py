@@ -130,6 +130,15 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def pinned(a):
+    """Copy of a numpy array in page-locked host memory."""
+    import torch
+    t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+    out = t.numpy()
+    out[...] = a          # out.base keeps the pinned tensor alive
+    return out
+
+
 def allreduce_max(x, world):
     if world == 1:
         return x
@@ -300,8 +309,9 @@ def run_ours(args, world, rank, local):
     ctx.propagate(verify=True)
     ctx.close()
 
-    # ---- e2e: public API with host buffers ----
-    host = imx.Graph(g.xadj, g.adj, g.weights, g.orig_ids)
+    # ---- e2e: public API with host buffers (pinned, as a serving caller
+    # would keep its graph) ----
+    host = imx.Graph(pinned(g.xadj), pinned(g.adj), pinned(g.weights), g.orig_ids)
     e2e_steps = args.e2e_steps or args.steps
     times, d2h = [], 0
     for i in range(args.warmup + e2e_steps):

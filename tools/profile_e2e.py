@@ -9,9 +9,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2008_03095_b200 as imx
 from paper_2008_03095_b200 import configs
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "c2"
 c = configs.CONFIGS[cfg]
 g = configs.build(cfg)
+if "--pinned" in sys.argv:
+    from bench import pinned
+    g = imx.Graph(pinned(g.xadj), pinned(g.adj), pinned(g.weights), g.orig_ids)
 for _ in range(2):
     gi = imx.Graph(g.xadj, g.adj, g.weights, g.orig_ids)
     run = imx.run_fused(gi, c.K, c.R, 0)

@@ -121,6 +121,10 @@ int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);
 // raw label-matrix passes shared with the evaluation worlds (evaluation.cu)
 int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
+// 16-byte quads of rows [0, n) from one row layout to another (row strides
+// sld, dld; nq quads per row): lane tiles in and out of contiguous scratch
+int launch_tile_copy(const uint32_t *src, int64_t sld, uint32_t *dst, int64_t dld, int64_t n, int nq,
+                     cudaStream_t st);
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
                     cudaStream_t st, int *launches = nullptr);
 

@@ -794,6 +794,14 @@ __global__ void k_tile_copy(const uint32_t *__restrict__ src, int64_t sld, uint3
     }
 }
 
+int launch_tile_copy(const uint32_t *src, int64_t sld, uint32_t *dst, int64_t dld, int64_t n, int nq,
+                     cudaStream_t st) {
+    k_tile_copy<<<grid_for(n * nq), 256, 0, st>>>(src, sld, dst, dld, n, nq);
+    IMX_CHECK_LAUNCH();
+    note_launch();
+    return IMX_OK;
+}
+
 // Lanes per compression tile: a very wide label matrix of a graph whose
 // 32-lane slice is L2-sized is compressed in tiles of 32 lanes copied to a
 // contiguous [n][32] scratch (one 128-byte line per row), so the parent reads

@@ -130,6 +130,38 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def random_access(summ, matrix_bytes, t_s):
+    """Union-find kernels (hook + compress) against the random-access
+    roofline.  Their L2 sectors and DRAM bytes per propagate come from ncu
+    (profiles/ncu_<cfg>_summary.json), the time is their live device time;
+    the reference rates are the measured random 4-byte gathers of
+    tools/gather_probe.cu (profiles/r01_gather_probe.jsonl): one 32-byte
+    sector per access, over a working set the size of the label matrix (all
+    DRAM misses) and over an L2-resident 64 MB one.  dram_frac = the kernels'
+    DRAM sectors/s over the probe's random-access rate; it exceeds 1 when
+    coalesced row streams dominate (the probe is the random-access ceiling,
+    not the streaming one)."""
+    uf = {k: v for k, v in summ["kernels"].items()
+          if k.startswith(("k_hook", "k_pull<2", "k_compress", "k_tile_copy"))}
+    sectors = sum(v["l2_read_sectors"] + v["l2_atom_sectors"] + v["l2_red_sectors"] + v["l2_write_sectors"]
+                  for v in uf.values())
+    dram = sum(v["dram_read_B"] + v["dram_write_B"] for v in uf.values())
+    probe = ROOT / "profiles" / "r01_gather_probe.jsonl"
+    rows = [json.loads(x) for x in probe.read_text().splitlines() if x.strip()] if probe.exists() else []
+    rows = sorted((r for r in rows if r["kind"] == "gather"), key=lambda r: r["bytes"])
+    ref = next((r for r in rows if r["bytes"] >= matrix_bytes), rows[-1] if rows else None)
+    l2ref = next((r for r in rows if r["bytes"] >= (64 << 20)), None)
+    out = {"kernels": sorted(uf), "l2_sectors": sectors, "dram_bytes": dram,
+           "l2_gsectors_per_s": sectors / t_s / 1e9, "dram_gsectors_per_s": dram / 32 / t_s / 1e9}
+    if ref:
+        out["probe_random_gsectors_per_s"] = ref["g_accesses_per_s"]
+        out["probe_bytes"] = ref["bytes"]
+        out["dram_frac"] = out["dram_gsectors_per_s"] / ref["g_accesses_per_s"]
+    if l2ref:
+        out["probe_l2_resident_gsectors_per_s"] = l2ref["g_accesses_per_s"]
+    return out
+
+
 def pinned(a):
     """Copy of a numpy array in page-locked host memory."""
     import torch
@@ -298,12 +330,15 @@ def run_ours(args, world, rank, local):
     kern = {k: res[k] for k in ("init_ms", "hook_ms", "compress_ms")}
     dominant = max(kern, key=kern.get)
     prof = ROOT / "profiles" / f"ncu_{args.config}_summary.json"
-    traffic = None
-    if prof.exists():
+    traffic, rand = None, None
+    if prof.exists() and W == R:
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_propagate")
+            summ = json.loads(prof.read_text())
+            traffic = summ.get("dram_bytes_per_propagate")
+            rand = random_access(summ, n * ((W + 3) // 4 * 4) * 4,
+                                 (res["hook_ms"] + res["compress_ms"]) / 1e3)
         except Exception:
-            traffic = None
+            traffic, rand = None, None
 
     # ---- correctness guard on the measured context ----
     ctx.propagate(verify=True)
@@ -346,7 +381,7 @@ def run_ours(args, world, rank, local):
                      "kernel": "propagate = k_init + k_hook + k_compress (one converged sample+CC)",
                      "model": f"B_es={bes:.3f} B/edge-sim dense-sweep model (SURVEY 8(d)) x 2m*R_gpu",
                      "peak_source": peak_src, "dominant_kernel": dominant,
-                     "kernel_ms": kern},
+                     "kernel_ms": kern, "random_access": rand},
         "e2e": {"value": units_total / e2e_s, "unit": "edge-sims/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "k_seed_wall_s": e2e_s, "seeds_head": seeds[:5], "spread": spread},

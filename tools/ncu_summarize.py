@@ -1,8 +1,10 @@
-"""Per-kernel DRAM bytes / time of one propagate from an ncu CSV (raw page,
---metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum)
--> profiles/r01_c2_ncu_full_propagate.json + profiles/ncu_c2_summary.json.
+"""Per-kernel DRAM bytes, L2 sectors and time of ONE propagate from an ncu
+CSV (tools/ncu_configs.sh: --csv --print-units base, metrics
+gpu__time_duration, dram__bytes_{read,write}, lts__t_sectors_srcunit_tex_op_
+{read,atom,red,write}[_lookup_hit]) -> profiles/ncu_<cfg>_summary.json, which
+bench.py reads for roofline.traffic and roofline.random_access.
 
-    python tools/ncu_summarize.py gpurun_out/prop_metrics.csv
+    python tools/ncu_summarize.py c2 [gpurun_out/ncu_c2.csv]
 """
 import csv
 import json
@@ -10,37 +12,69 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-rows = list(csv.reader(open(sys.argv[1])))
-# ncu --csv --print-units base: one row per (kernel, metric)
+cfg = sys.argv[1]
+src = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "gpurun_out" / f"ncu_{cfg}.csv"
+lines = src.read_text().splitlines()
+start_row = next(j for j, l in enumerate(lines) if l.startswith('"ID"'))
+rows = list(csv.reader(lines[start_row:]))
 hdr = rows[0]
-iK, iM, iV, iU = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
-                  hdr.index("Metric Unit"))
-iID = hdr.index("ID")
+iK, iM, iV, iID = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
 kern = {}
 for r in rows[1:]:
     if len(r) <= iV:
         continue
-    k = kern.setdefault(int(r[iID]), {"Kernel Name": r[iK]})
-    v = float(r[iV].replace(",", "")) if r[iV] else 0.0
-    unit = r[iU]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "ms": 1e3,
-             "usecond": 1, "nsecond": 1e-3, "msecond": 1e3}.get(unit, 1)
-    k[r[iM]] = v * scale
+    k = kern.setdefault(int(r[iID]), {"kernel": r[iK].split("(")[0].replace("void ", "")})
+    k[r[iM]] = float(r[iV].replace(",", "")) if r[iV] else 0.0
 ks = [kern[i] for i in sorted(kern)]
-# the kernels of ONE propagate: from the last k_init / k_pull<1 up to and including k_compress
-start = max(i for i, k in enumerate(ks) if "k_init" in k["Kernel Name"] or "k_pull<1" in k["Kernel Name"])
-end = next(i for i in range(start, len(ks)) if "k_compress" in ks[i]["Kernel Name"])
-one = ks[start:end + 1]
-rd = sum(k.get("dram__bytes_read.sum", 0) for k in one)
-wr = sum(k.get("dram__bytes_write.sum", 0) for k in one)
-t = sum(k.get("gpu__time_duration.sum", 0) for k in one)
-(ROOT / "profiles" / "r01_c2_ncu_full_propagate.json").write_text(json.dumps(one, indent=1))
-(ROOT / "profiles" / "ncu_c2_summary.json").write_text(json.dumps({
-    "config": "c2",
-    "source": "profiles/r01_c2_ncu_full_propagate.json (ncu, kernels of one propagate, bytes in B, times in us)",
-    "dram_bytes_per_propagate": rd + wr, "dram_read_MB": rd / 1e6, "dram_write_MB": wr / 1e6,
-    "kernel_time_us_serialized": t}, indent=1))
-print(f"{len(one)} kernels, read {rd/1e6:.1f} MB, write {wr/1e6:.1f} MB, {t:.1f} us serialized")
+# the kernels of ONE propagate: after the last L2 flush, up to the last
+# compress kernel (tiled compress: copy-in / compress / copy-out per tile)
+first = max(i for i, k in enumerate(ks) if k["kernel"].endswith("k_flush")) + 1
+stop = next((i for i in range(first, len(ks)) if "k_gains" in ks[i]["kernel"]), len(ks))   # memoize follows
+last = max(i for i in range(first, stop) if "k_compress" in ks[i]["kernel"] or "k_tile_copy" in ks[i]["kernel"])
+one = ks[first:last + 1]
+
+S = "lts__t_sectors_srcunit_tex_op_"
+
+
+def tot(key):
+    return sum(k.get(key, 0.0) for k in one)
+
+
+groups = {}
 for k in one:
-    print(f"  {k['Kernel Name'][:60]:60s} {k.get('gpu__time_duration.sum',0):8.1f} us "
-          f"R {k.get('dram__bytes_read.sum',0)/1e6:7.1f} MB W {k.get('dram__bytes_write.sum',0)/1e6:7.1f} MB")
+    name = k["kernel"].replace("imx::", "")
+    g = groups.setdefault(name, {"launches": 0, "time_us": 0.0, "dram_read_B": 0.0, "dram_write_B": 0.0,
+                                 "l2_read_sectors": 0.0, "l2_read_hit_sectors": 0.0, "l2_atom_sectors": 0.0,
+                                 "l2_red_sectors": 0.0, "l2_write_sectors": 0.0})
+    g["launches"] += 1
+    g["time_us"] += k.get("gpu__time_duration.sum", 0.0) / 1e3
+    g["dram_read_B"] += k.get("dram__bytes_read.sum", 0.0)
+    g["dram_write_B"] += k.get("dram__bytes_write.sum", 0.0)
+    g["l2_read_sectors"] += k.get(S + "read.sum", 0.0)
+    g["l2_read_hit_sectors"] += k.get(S + "read_lookup_hit.sum", 0.0)
+    g["l2_atom_sectors"] += k.get(S + "atom.sum", 0.0)
+    g["l2_red_sectors"] += k.get(S + "red.sum", 0.0)
+    g["l2_write_sectors"] += k.get(S + "write.sum", 0.0)
+rd, wr = tot("dram__bytes_read.sum"), tot("dram__bytes_write.sum")
+l2 = tot(S + "read.sum") + tot(S + "atom.sum") + tot(S + "red.sum") + tot(S + "write.sum")
+t_us = tot("gpu__time_duration.sum") / 1e3
+summary = {
+    "config": cfg,
+    "source": f"ncu --replay-mode application (tools/ncu_configs.sh), kernels of one propagate after an L2 flush; "
+              f"serialised, cold-cache launch times",
+    "dram_bytes_per_propagate": rd + wr,
+    "dram_read_MB": rd / 1e6,
+    "dram_write_MB": wr / 1e6,
+    "l2_sectors_per_propagate": l2,
+    "l2_read_hit_rate": tot(S + "read_lookup_hit.sum") / max(1.0, tot(S + "read.sum")),
+    "kernel_time_us_serialized": t_us,
+    "kernels": groups,
+}
+out = ROOT / "profiles" / f"ncu_{cfg}_summary.json"
+out.write_text(json.dumps(summary, indent=1))
+print(f"{cfg}: {len(one)} launches, DRAM {rd / 1e6:.1f} MB read + {wr / 1e6:.1f} MB write, "
+      f"L2 {l2 / 1e6:.1f} M sectors, {t_us:.1f} us serialised -> {out.relative_to(ROOT)}")
+for name, g in groups.items():
+    print(f"  {name:32s} x{g['launches']:<4d} {g['time_us']:9.1f} us  DRAM {(g['dram_read_B'] + g['dram_write_B']) / 1e6:9.1f} MB"
+          f"  L2 rd {g['l2_read_sectors'] / 1e6:7.1f}M (hit {g['l2_read_hit_sectors'] / max(1, g['l2_read_sectors']):.2f})"
+          f" atom {g['l2_atom_sectors'] / 1e6:6.1f}M red {g['l2_red_sectors'] / 1e6:6.1f}M wr {g['l2_write_sectors'] / 1e6:6.1f}M")

@@ -218,12 +218,48 @@ __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ o
     for (int64_t j0 = jlo + wg * kEnumChunk; j0 < total; j0 += nw * kEnumChunk) {
         int64_t s = s_lo + seg_search(off + s_lo, s_hi - s_lo, j0, lane);
         const int64_t jend = (total - j0 < kEnumChunk) ? total : j0 + kEnumChunk;
-        for (int64_t j = j0 + lane; j < jend; j += 32) {
+        if (!UNI) {
+            // per-edge thresholds: the membership re-test gates the union
+            for (int64_t j = j0 + lane; j < jend; j += 32) {
+                while (off[s + 1] <= j) ++s;
+                const int64_t e = seg_a[s] + (j - off[s]);
+                const int r = (int)(s / segs_per_lane);
+                if (!((X[r] ^ EH[e]) < ET[e])) continue;
+                const int2 uv = E[e];
+                if (SKIP && ld_relaxed(cell(L, ld, (uint32_t)uv.y, r)) == (uint32_t)uv.x) continue;
+                nh += unite(L, ld, (uint32_t)uv.x, (uint32_t)uv.y, r);
+            }
+            continue;
+        }
+        // uniform threshold, two-stage pipeline: the next pair's segment
+        // walk and edge load are issued before this pair's union, so the
+        // edge fetch overlaps the root searches (C4 hook 23.5 -> 22.7 ms;
+        // with per-edge thresholds the extra live state costs more than
+        // it hides, C3 7.1 -> 8.0 ms)
+        int64_t j = j0 + lane;
+        int2 nuv = make_int2(0, 0);
+        int32_t nhh = 0, ntt = 1, nxx = 0;
+        int nr = 0;
+        if (j < jend) {
             while (off[s + 1] <= j) ++s;
             const int64_t e = seg_a[s] + (j - off[s]);
-            const int r = (int)(s / segs_per_lane);
-            if (!UNI && !((X[r] ^ EH[e]) < ET[e])) continue;
-            const int2 uv = E[e];
+            nr = (int)(s / segs_per_lane);
+            nuv = E[e];
+            if (!UNI) { nhh = EH[e]; ntt = ET[e]; nxx = X[nr]; }
+        }
+        for (; j < jend; j += 32) {
+            const int2 uv = nuv;
+            const int r = nr;
+            const bool live = UNI || (nxx ^ nhh) < ntt;
+            const int64_t jn = j + 32;
+            if (jn < jend) {
+                while (off[s + 1] <= jn) ++s;
+                const int64_t e = seg_a[s] + (jn - off[s]);
+                nr = (int)(s / segs_per_lane);
+                nuv = E[e];
+                if (!UNI) { nhh = EH[e]; ntt = ET[e]; nxx = X[nr]; }
+            }
+            if (!live) continue;
             // after the pull forest pass, a live edge that is its upper
             // endpoint's first live smaller neighbour is already a tree edge
             if (SKIP && ld_relaxed(cell(L, ld, (uint32_t)uv.y, r)) == (uint32_t)uv.x) continue;

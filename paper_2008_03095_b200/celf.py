@@ -83,6 +83,12 @@ def _key_le(pa, va, pb, vb) -> bool:
     return pa > pb or (pa == pb and va <= vb)
 
 
+def _lex_best(ids: np.ndarray, gains: np.ndarray):
+    """(gain, id) of the lexicographic best of a batch: max gain, then min id."""
+    j = int(np.lexsort((ids, -gains))[0])
+    return int(gains[j]), int(ids[j])
+
+
 def select_rounds(shard, comm, k: int, batch0: int = 64):
     """k seeds, their gains and the dequeue trace (T, 5) over a sharded CELF
     state.  ``shard`` offers celf_top / celf_prefix / celf_advance
@@ -92,7 +98,9 @@ def select_rounds(shard, comm, k: int, batch0: int = 64):
     batches until the best fresh key is below the next stale key; the
     refreshed vertices are the prefix whose stale key is at most the
     winner's fresh key, replayed as refresh records, then the winner commits
-    and the others go back into the order with their fresh keys."""
+    and the others go back into the order with their fresh keys.  The
+    per-round host work is vectorised (numpy), so a round costs its device
+    calls and allreduces, not a Python loop over the refreshed prefix."""
     seeds, gains, trace = [], [], []
     pending = None              # (local commit gain, expected, vertex) checked with the next allreduce
 
@@ -101,16 +109,17 @@ def select_rounds(shard, comm, k: int, batch0: int = 64):
             raise AssertionError(f"committed gain {total} != evaluated {pending[1]} for vertex {pending[2]}")
 
     for t in range(k):
-        back = []
         if t == 0:
             best_f, best_v = shard.celf_top()
             if best_v < 0:
                 raise AssertionError("no candidate left at round 0")
             kr = 1
+            back_ids = np.empty(0, np.int32)
+            back_prio = np.empty(0, np.int64)
         else:
             lo, hi = 0, batch0
             best_v, best_f = -1, -1
-            ids, prio, fresh = [], [], []
+            ids_l, prio_l, fresh_l = [], [], []
             while True:
                 i, p, f_part, length = shard.celf_prefix(lo, hi)
                 if length == 0:
@@ -123,35 +132,45 @@ def select_rounds(shard, comm, k: int, batch0: int = 64):
                 else:
                     f = comm.allreduce(f_part)
                 h = min(hi, length)
-                for v, fv in zip(i[: h - lo].tolist(), f.tolist()):
-                    if best_v < 0 or _key_le(fv, v, best_f, best_v):
-                        best_v, best_f = v, fv
-                ids += i[: h - lo].tolist()
-                prio += p[: h - lo].tolist()
-                fresh += f.tolist()
+                bi = np.asarray(i[: h - lo], np.int64)
+                bf = np.asarray(f, np.int64)
+                if len(bi):
+                    g_b, v_b = _lex_best(bi, bf)
+                    if best_v < 0 or _key_le(g_b, v_b, best_f, best_v):
+                        best_v, best_f = v_b, g_b
+                ids_l.append(bi)
+                prio_l.append(np.asarray(p[: h - lo], np.int64))
+                fresh_l.append(bf)
                 if h >= length:
                     break
                 if _key_le(best_f, best_v, int(p[h - lo]), int(i[h - lo])):
                     break                       # nothing unevaluated can win
                 lo, hi = h, h + max(batch0, h)
-            kr = 0
-            while kr < len(ids) and _key_le(prio[kr], ids[kr], best_f, best_v):
-                trace.append((ids[kr], prio[kr], fresh[kr], 0, t))
-                if ids[kr] != best_v:
-                    back.append((-fresh[kr], ids[kr]))
-                kr += 1
+            ids = np.concatenate(ids_l)
+            prio = np.concatenate(prio_l)
+            fresh = np.concatenate(fresh_l)
+            # the order is sorted by (-prio, id): the refreshed vertices are the
+            # prefix whose stale key is at most the winner's fresh key
+            le = (prio > best_f) | ((prio == best_f) & (ids <= best_v))
+            kr = int(np.argmin(le)) if not le.all() else len(le)
+            rec = np.empty((kr, 5), np.int64)
+            rec[:, 0], rec[:, 1], rec[:, 2], rec[:, 3], rec[:, 4] = ids[:kr], prio[:kr], fresh[:kr], 0, t
+            trace.append(rec)
+            keep = ids[:kr] != best_v
+            bi, bg = ids[:kr][keep], fresh[:kr][keep]
+            o = np.lexsort((bi, -bg))             # back into the order sorted by (-fresh, id)
+            back_ids = bi[o].astype(np.int32)
+            back_prio = bg[o]
             batch0 = max(64, kr)
-        back.sort()
-        local = shard.celf_advance(kr, best_v, np.array([v for _, v in back], np.int32),
-                                   np.array([-g for g, _ in back], np.int64))
+        local = shard.celf_advance(kr, best_v, back_ids, back_prio)
         if t == k - 1:                  # no later evaluation allreduce to ride on
             pending = (local, best_f, best_v)
             check(int(comm.allreduce(np.array([local], np.int64))[0]))
             pending = None
         else:
             pending = (local, best_f, best_v)
-        trace.append((best_v, best_f, best_f, 1, t))
+        trace.append(np.array([[best_v, best_f, best_f, 1, t]], np.int64))
         seeds.append(best_v)
         gains.append(best_f)
-    return (np.asarray(seeds, np.int32), np.asarray(gains, np.int64),
-            np.asarray(trace, np.int64).reshape(-1, 5))
+    tr = np.concatenate(trace) if trace else np.empty((0, 5), np.int64)
+    return np.asarray(seeds, np.int32), np.asarray(gains, np.int64), tr.reshape(-1, 5)

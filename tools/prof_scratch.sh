@@ -1,13 +1,2 @@
 V=paper_2008_03095_b200/lib/variants
-IMX_HOOK=enum timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-bm() { cfg=$1; shift; for t in "$@"; do lib=$V/libinfuser_b200_$t.so; [ $t = new ] && lib=paper_2008_03095_b200/lib/libinfuser_b200.so; INFUSER_B200_LIB=$lib timeout 300 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/t_${cfg}_$t.json 2>gpurun_out/t_${cfg}_$t.err; python - $cfg $t <<'PY'
-import json,sys
-try:
-    d=json.loads(open(f'gpurun_out/t_{sys.argv[1]}_{sys.argv[2]}.json').read().strip().splitlines()[-1]); r=d['roofline']
-    print(sys.argv[1], sys.argv[2], round(d['ms_per_step'],3), {k:round(v,3) for k,v in r['kernel_ms'].items()}, 'e2e', round(d['e2e']['k_seed_wall_s']*1e3,2))
-except Exception as e: print(sys.argv[1:], 'fail', e)
-PY
-done; }
-bm c3 base new base new
-bm c2 base new
-bm c4 base new
+for t in base new base new; do lib=$V/libinfuser_b200_$t.so; [ $t = new ] && lib=paper_2008_03095_b200/lib/libinfuser_b200.so; echo $t; INFUSER_B200_LIB=$lib python tools/profile_e2e.py c2 --pinned 2>&1 | head -2 | cut -c 1-330; done

@@ -1,18 +1,13 @@
 V=paper_2008_03095_b200/lib/variants
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-IMX_HOOK=enum timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-IMX_HOOK=dense timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-bm() { cfg=$1; shift; for t in "$@"; do lib=$V/libinfuser_b200_$t.so; [ $t = new ] && lib=paper_2008_03095_b200/lib/libinfuser_b200.so; INFUSER_B200_LIB=$lib timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/t_${cfg}_$t.json 2>gpurun_out/t_${cfg}_$t.err; python - $cfg $t <<'PY'
+IMX_ENUM_BLOCK=64 IMX_HOOK=enum timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+bm() { cfg=$1; shift; for t in "$@"; do lib=$V/libinfuser_b200_${t%%:*}.so; [ ${t%%:*} = new ] && lib=paper_2008_03095_b200/lib/libinfuser_b200.so; IMX_ENUM_BLOCK=${t##*:} INFUSER_B200_LIB=$lib timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/t_${cfg}_x.json 2>gpurun_out/t_${cfg}_x.err; python - $cfg $t <<'PY'
 import json,sys
 try:
-    d=json.loads(open(f'gpurun_out/t_{sys.argv[1]}_{sys.argv[2]}.json').read().strip().splitlines()[-1]); r=d['roofline']
+    d=json.loads(open(f'gpurun_out/t_{sys.argv[1]}_x.json').read().strip().splitlines()[-1]); r=d['roofline']
     print(sys.argv[1], sys.argv[2], round(d['ms_per_step'],4), {k:round(v,4) for k,v in r['kernel_ms'].items()}, 'e2e', round(d['e2e']['k_seed_wall_s']*1e3,3))
 except Exception as e: print(sys.argv[1:], 'fail', e)
 PY
 done; }
-bm c2 base new
-bm c2p1 base new
-bm c3 base new
-bm c4 base new
-bm c5 base new
-bm c1 base new
+bm c2 base:0 new:0 new:512 new:256 new:128 base:256
+bm c4 new:0 new:512 new:256
+bm c3 new:0 new:1024 new:512

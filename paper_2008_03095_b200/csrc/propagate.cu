@@ -183,7 +183,10 @@ __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
 // consecutive j (one binary search over the segment offsets per chunk, then
 // a forward walk), so consecutive threads read consecutive edges of the same
 // hash interval (coalesced) and every thread runs one union per pair.
-constexpr int kEnumChunk = 128;
+#ifndef IMX_ENUM_CHUNK
+#define IMX_ENUM_CHUNK 128
+#endif
+constexpr int kEnumChunk = IMX_ENUM_CHUNK;
 
 // largest s in [0, nseg) with off[s] <= j (off nondecreasing, off[0] = 0),
 // by the whole warp: a 33-ary search -- 32 pivots per step, one load each,

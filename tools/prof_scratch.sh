@@ -1,6 +1,5 @@
 V=paper_2008_03095_b200/lib/variants
-IMX_ENUM_BLOCK=64 IMX_HOOK=enum timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-bm() { cfg=$1; shift; for t in "$@"; do lib=$V/libinfuser_b200_${t%%:*}.so; [ ${t%%:*} = new ] && lib=paper_2008_03095_b200/lib/libinfuser_b200.so; IMX_ENUM_BLOCK=${t##*:} INFUSER_B200_LIB=$lib timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/t_${cfg}_x.json 2>gpurun_out/t_${cfg}_x.err; python - $cfg $t <<'PY'
+bm() { cfg=$1; shift; for t in "$@"; do lib=$V/libinfuser_b200_$t.so; INFUSER_B200_LIB=$lib timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/t_${cfg}_x.json 2>gpurun_out/t_${cfg}_x.err; python - $cfg $t <<'PY'
 import json,sys
 try:
     d=json.loads(open(f'gpurun_out/t_{sys.argv[1]}_x.json').read().strip().splitlines()[-1]); r=d['roofline']
@@ -8,6 +7,6 @@ try:
 except Exception as e: print(sys.argv[1:], 'fail', e)
 PY
 done; }
-bm c2 base:0 new:0 new:512 new:256 new:128 base:256
-bm c4 new:0 new:512 new:256
-bm c3 new:0 new:1024 new:512
+bm c2 base ch64 ch256 ch512
+bm c3 base ch64 ch256 ch512
+bm c4 base ch64 ch256 ch512

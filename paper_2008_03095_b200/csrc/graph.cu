@@ -494,7 +494,8 @@ void graph_free(imx_graph *g) {
     if (!g) return;
     cudaSetDevice(g->dev);
     void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
-                    g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff, g->lut};
+                    g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff, g->lut,
+                    g->heavy, g->hs_v, g->hs_a, g->hs_len};
     for (void *p : ptrs) if (p) cudaFreeAsync(p, g->stream);
     release_stream(g->dev, g->stream);
     delete g;

@@ -285,12 +285,25 @@ __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ o
 // not a vertex's first live smaller neighbour -- 4-30% of the live pairs on
 // the benchmark graphs -- through the per-warp queue of k_hook.
 // ---------------------------------------------------------------------------
-template <int PASS, bool UNI, int LPT>
+//
+// Heavy rows (HEAVY = true): a vertex whose smaller-neighbour prefix exceeds
+// T slots would serialise one warp (C3: prefixes up to 3358 slots, 2048
+// lanes, ~170 live smaller neighbours per lane to unite).  Its prefix is cut
+// into slices of T slots, one warp per slice: pass 1 folds the slice's first
+// live neighbour into the row with atomicMin (the light pass wrote the row
+// as roots), pass 2 unites every live neighbour except the one the row
+// points at (the forest edge; a pointer moved up by path splitting only
+// makes the skipped or the extra union one between already-joined trees).
+// The light passes skip heavy rows (heavy[v] != 0).
+template <int PASS, bool UNI, int LPT, bool HEAVY>
 __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                                               const int32_t *__restrict__ hash, const int32_t *__restrict__ thr,
                                               int32_t tu, int64_t n, const int32_t *__restrict__ X, int32_t W,
                                               int64_t ld, uint32_t *__restrict__ L,
-                                              unsigned long long *__restrict__ hooks) {
+                                              unsigned long long *__restrict__ hooks,
+                                              const uint8_t *__restrict__ heavy, const int32_t *__restrict__ hs_v,
+                                              const int64_t *__restrict__ hs_a, const int32_t *__restrict__ hs_len,
+                                              int64_t nhs) {
     // LPT lanes per thread (4 or 8): each edge's loads and the loop overhead
     // are shared by LPT membership tests
     constexpr int Q = LPT / 4;                // 16-byte quads per thread
@@ -310,8 +323,19 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
     unsigned long long nh = 0;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t v = wg; v < n; v += nw) {
-        const int64_t s0 = xadj[v], s1 = xadj[v + 1];
+    const int64_t items = HEAVY ? nhs : n;
+    for (int64_t it = wg; it < items; it += nw) {
+        int64_t v, s0, s1;
+        if (HEAVY) {
+            v = hs_v[it];
+            s0 = hs_a[it];
+            s1 = s0 + hs_len[it];
+        } else {
+            v = it;
+            s0 = xadj[v];
+            s1 = xadj[v + 1];
+            if (heavy && heavy[v]) s1 = s0;      // heavy row: roots here, slices below
+        }
         for (int c0 = 0; c0 < ng; c0 += 32) {
             const int gi = c0 + lane;
             const bool active = gi < ng;
@@ -329,6 +353,15 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
 #pragma unroll
             for (int k = 0; k < LPT; ++k) best[k] = ROOT;
             unsigned seen = 0;
+            uint32_t par[HEAVY && PASS == 2 ? LPT : 1];
+            if (HEAVY && PASS == 2) {
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                    const uint4 p4 = (active && r + 4 * k < ld)
+                        ? *(reinterpret_cast<const uint4 *>(L + v * ld + r) + k) : make_uint4(ROOT, ROOT, ROOT, ROOT);
+                    par[4 * k] = p4.x; par[4 * k + 1] = p4.y; par[4 * k + 2] = p4.z; par[4 * k + 3] = p4.w;
+                }
+            }
             // software-pipelined slot loads: the next slot's id, hash and
             // threshold are in flight while this slot is tested
             uint32_t nu = (uint32_t)v;
@@ -360,8 +393,16 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
 #pragma unroll
                     for (int k = 0; k < LPT; ++k) live |= (unsigned)((x[k] ^ h) < t) << k;
                     live &= valid;
-                    unsigned rest = live & seen;
-                    seen |= live;
+                    unsigned rest;
+                    if (HEAVY) {
+                        unsigned fe = 0;     // lanes whose row points at u: the forest edge
+#pragma unroll
+                        for (int k = 0; k < LPT; ++k) fe |= (unsigned)(par[k] == u) << k;
+                        rest = live & ~fe;
+                    } else {
+                        rest = live & seen;
+                        seen |= live;
+                    }
                     if (!__any_sync(FULL, rest != 0)) continue;
                     const int kk = __popc(rest);
                     int inc = kk;
@@ -395,7 +436,11 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
                 for (int k = 0; k < LPT; ++k)
                     if (!((valid >> k) & 1u)) best[k] = ROOT;   // padding lanes stay roots
             }
-            if (PASS == 1 && active) {
+            if (PASS == 1 && active && HEAVY) {
+#pragma unroll
+                for (int k = 0; k < LPT; ++k)
+                    if (best[k] != ROOT) atomicMin(L + v * ld + r + k, best[k]);
+            } else if (PASS == 1 && active) {
 #pragma unroll
                 for (int k = 0; k < Q; ++k)
                     if (r + 4 * k < ld)
@@ -720,10 +765,103 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest
     return IMX_OK;
 }
 
+// ---- heavy rows of the pull sampler ---------------------------------------
+__global__ void k_heavy_count(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, int64_t n, int T,
+                              uint8_t *__restrict__ heavy, int32_t *__restrict__ pre, int64_t *__restrict__ nsl) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = xadj[v], hi = xadj[v + 1];
+        const int64_t s0 = lo;
+        while (lo < hi) {                     // first slot with adj >= v (rows ascend)
+            const int64_t mid = (lo + hi) >> 1;
+            if (adj[mid] < (int32_t)v) lo = mid + 1; else hi = mid;
+        }
+        const int64_t p = lo - s0;
+        const bool h = p > T;
+        heavy[v] = h;
+        pre[v] = (int32_t)p;
+        nsl[v] = h ? (p + T - 1) / T : 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) nsl[n] = 0;
+}
+
+__global__ void k_heavy_fill(const int64_t *__restrict__ xadj, int64_t n, int T, const int32_t *__restrict__ pre,
+                             const int64_t *__restrict__ nsl, const int64_t *__restrict__ off,
+                             int32_t *__restrict__ hv, int64_t *__restrict__ ha, int32_t *__restrict__ hl) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = nsl[v];
+        for (int64_t i = 0; i < k; ++i) {
+            hv[off[v] + i] = (int32_t)v;
+            ha[off[v] + i] = xadj[v] + i * T;
+            hl[off[v] + i] = (int32_t)((pre[v] - i * T) < T ? (pre[v] - i * T) : T);
+        }
+    }
+}
+
+// A warp owns a whole smaller-neighbour prefix in the light pull passes; the
+// graph is balanced when no prefix is long against the per-warp share of the
+// edges.
+static bool prefix_balanced(const imx_graph *g) {
+    const double balanced_prefix = 8.0 * (double)g->me / (148.0 * 64.0);
+    return (double)g->max_prefix <= std::max(64.0, balanced_prefix);
+}
+
+// slots per heavy slice: IMX_PULL_HEAVY (0 = no splitting), else 8 for
+// unbalanced graphs (C3: 8.5 ms by enumeration, 7.1 / 5.2 / 5.0 ms pulled
+// with 64 / 32 / 16 / 8-slot slices: 7.1 / 5.2 / 5.0 / 4.8) and no splitting for balanced ones, where
+// the extra passes only add work (C2p1: 0.47 -> 0.58 ms at 32)
+static int pull_heavy_T(const imx_graph *g) {
+    if (const char *e = getenv("IMX_PULL_HEAVY")) return std::max(0, atoi(e));
+    return prefix_balanced(g) ? 0 : 8;
+}
+
+// the heavy-row slices of the graph for slice length T, cached on the graph
+static int ensure_heavy(imx_ctx *c, int T) {
+    imx_graph *g = c->g;
+    if (g->heavy_T == T) return IMX_OK;
+    for (void **p : {(void **)&g->heavy, (void **)&g->hs_v, (void **)&g->hs_a, (void **)&g->hs_len}) {
+        if (*p) cudaFreeAsync(*p, c->st);
+        *p = nullptr;
+    }
+    g->nhs = 0;
+    g->heavy_T = -1;
+    if (T <= 0 || g->max_prefix <= T) { g->heavy_T = T; return IMX_OK; }
+    const int64_t n = g->n;
+    int32_t *pre = nullptr;
+    int64_t *nsl = nullptr, *off = nullptr;
+    IMX_CUDA(pool_alloc((void **)&g->heavy, n, c->st));
+    IMX_CUDA(pool_alloc((void **)&pre, sizeof(int32_t) * n, c->st));
+    IMX_CUDA(pool_alloc((void **)&nsl, sizeof(int64_t) * (n + 1), c->st));
+    IMX_CUDA(pool_alloc((void **)&off, sizeof(int64_t) * (n + 1), c->st));
+    k_heavy_count<<<grid_for(n), 256, 0, c->st>>>(g->xadj, g->adj, n, T, g->heavy, pre, nsl);
+    IMX_CHECK_LAUNCH();
+    size_t tb = 0;
+    IMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nsl, off, n + 1, c->st));
+    void *tmp = nullptr;
+    IMX_CUDA(pool_alloc(&tmp, tb, c->st));
+    IMX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nsl, off, n + 1, c->st));
+    int64_t total = 0;
+    IMX_CUDA(cudaMemcpyAsync(&total, off + n, sizeof total, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (total > 0) {
+        IMX_CUDA(pool_alloc((void **)&g->hs_v, sizeof(int32_t) * total, c->st));
+        IMX_CUDA(pool_alloc((void **)&g->hs_a, sizeof(int64_t) * total, c->st));
+        IMX_CUDA(pool_alloc((void **)&g->hs_len, sizeof(int32_t) * total, c->st));
+        k_heavy_fill<<<grid_for(n), 256, 0, c->st>>>(g->xadj, n, T, pre, nsl, off, g->hs_v, g->hs_a, g->hs_len);
+        IMX_CHECK_LAUNCH();
+    }
+    note_launch(total > 0 ? 4 : 3);
+    for (void *p : {(void *)pre, (void *)nsl, (void *)off, tmp}) cudaFreeAsync(p, c->st);
+    IMX_CUDA(cudaStreamSynchronize(c->st));   // the slices are shared by every context of the graph
+    g->nhs = total;
+    g->heavy_T = T;
+    return IMX_OK;
+}
+
 static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (n == 0) return IMX_OK;
+    IMX_TRY(ensure_heavy(c, pull_heavy_T(g)));
     // 8 lanes per thread once a row spans several warp-widths of quads
     const bool wide = c->W >= 256;
     const int lpt = wide ? 8 : 4;
@@ -731,15 +869,26 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     const size_t smem = sizeof(int32_t) * ldp + sizeof(uint32_t) * 3 * (32 + 32 * lpt) * 8;
     if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
     const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 8);
-    auto kern = wide ? (pass == 1 ? (g->uniform ? k_pull<1, true, 8> : k_pull<1, false, 8>)
-                                  : (g->uniform ? k_pull<2, true, 8> : k_pull<2, false, 8>))
-                     : (pass == 1 ? (g->uniform ? k_pull<1, true, 4> : k_pull<1, false, 4>)
-                                  : (g->uniform ? k_pull<2, true, 4> : k_pull<2, false, 4>));
-    if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<blocks, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld,
-                                       c->L, hooks);
-    IMX_CHECK_LAUNCH();
-    count_launch(c);
+    using KF = void (*)(const int64_t *, const int32_t *, const int32_t *, const int32_t *, int32_t, int64_t,
+                        const int32_t *, int32_t, int64_t, uint32_t *, unsigned long long *, const uint8_t *,
+                        const int32_t *, const int64_t *, const int32_t *, int64_t);
+    // [heavy][pass-1][uniform][wide]
+    static const KF kerns[2][2][2][2] = {
+        {{{k_pull<1, false, 4, false>, k_pull<1, false, 8, false>}, {k_pull<1, true, 4, false>, k_pull<1, true, 8, false>}},
+         {{k_pull<2, false, 4, false>, k_pull<2, false, 8, false>}, {k_pull<2, true, 4, false>, k_pull<2, true, 8, false>}}},
+        {{{k_pull<1, false, 4, true>, k_pull<1, false, 8, true>}, {k_pull<1, true, 4, true>, k_pull<1, true, 8, true>}},
+         {{k_pull<2, false, 4, true>, k_pull<2, false, 8, true>}, {k_pull<2, true, 4, true>, k_pull<2, true, 8, true>}}}};
+    const int hv = g->nhs > 0 ? 2 : 1;
+    for (int h = 0; h < hv; ++h) {
+        KF kern = kerns[h][pass - 1][g->uniform ? 1 : 0][wide ? 1 : 0];
+        if (smem > 48 * 1024)
+            IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int hb = h ? (int)std::min<int64_t>(ceil_div(g->nhs, 8), 148 * 8) : blocks;
+        kern<<<hb, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld, c->L, hooks,
+                                       g->nhs > 0 ? g->heavy : nullptr, g->hs_v, g->hs_a, g->hs_len, g->nhs);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
     return IMX_OK;
 }
 
@@ -759,8 +908,9 @@ static int hook_mode(const imx_graph *g, int32_t W) {
     if (m && !strcmp(m, "hybrid")) return HOOK_HYBRID;
     const char *t = getenv("IMX_PULL_MIN_P");
     const double pmin = t ? atof(t) : 0.02;
-    const double balanced_prefix = 8.0 * (double)g->me / (148.0 * 64.0);
-    const bool balanced = (double)g->max_prefix <= std::max(64.0, balanced_prefix);
+    // long prefixes are split into slices (heavy rows), so they only
+    // unbalance the pull passes when splitting is off
+    const bool balanced = pull_heavy_T(g) > 0 || prefix_balanced(g);
     if (g->thr_mean >= pmin && balanced) return HOOK_PULL;
     // small dense work (C1: 31k edges x 128 lanes): two scans beat the
     // enumeration's segment count + scan + launch chain

@@ -65,3 +65,43 @@ def test_random_evaluate_matches_oracle(gpu, orc, seed):
     got = evaluate_counts(g, seeds, r_eval, seed)
     want = orc.evaluate_counts(g.xadj, g.adj, g.weights, seeds, r_eval, seed, nthreads=2)
     assert np.array_equal(got, want)
+
+
+def hub_on_top_graph(rng):
+    """Hubs with the LARGEST ids (long smaller-neighbour prefixes): the pull
+    sampler splits such rows into slices (heavy rows) by default."""
+    n = int(rng.integers(300, 700))
+    parts = [rng.integers(0, n, size=(2 * n, 2))]
+    for h in range(n - 3, n):
+        nb = np.flatnonzero(rng.random(h) < 0.6)
+        parts.append(np.column_stack([nb, np.full(len(nb), h)]))
+    e = np.vstack(parts)
+    e = e[e[:, 0] != e[:, 1]]
+    lo, hi = np.minimum(e[:, 0], e[:, 1]), np.maximum(e[:, 0], e[:, 1])
+    key = np.unique(lo * n + hi)
+    e = np.column_stack([key // n, key % n]).astype(np.int64)
+    return n, e, rng.random(len(e)) * 0.3
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_heavy_rows_match_oracle(gpu, orc, seed, monkeypatch):
+    """Pull passes with heavy-row slices (default slice length, and 1-slot
+    slices) through the whole pipeline vs the oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    n, e, w = hub_on_top_graph(rng)
+    g = gpu.Graph.from_edges(n, e, w)
+    R = int(rng.choice([24, 100, 256, 300]))
+    k = int(rng.integers(1, 12))
+    want = orc.run_fused(g.xadj, g.adj, g.weights, k, R, seed, nthreads=2)
+    for mode, heavy in ((None, None), ("pull", None), ("pull", "1"), ("hybrid", "3"), ("pull", "0")):
+        for var, val in (("IMX_HOOK", mode), ("IMX_PULL_HEAVY", heavy)):
+            if val is None:
+                monkeypatch.delenv(var, raising=False)
+            else:
+                monkeypatch.setenv(var, val)
+        run = gpu.run_fused(g, k, num_simulations=R, master_seed=seed)
+        tag = (mode, heavy)
+        assert np.array_equal(run.labels, want["labels"]), tag
+        assert np.array_equal(run.sizes, want["sizes"]), tag
+        assert [int(s) for s in run.seeds] == want["seeds"].tolist(), tag
+        assert np.array_equal(run.selection.trace.array, want["trace"]), tag

@@ -14,6 +14,7 @@ R = int(sys.argv[3]) if len(sys.argv) > 3 else c.R     # lane override (smaller 
 g = configs.build(cfg)
 X = imx.SimulationRandoms(R, 0).values
 ctx = DeviceContext(g, X, R)
+ctx.propagate()          # one-time per-graph setup (sampler index, heavy-row slices) outside the window
 res = ctx.bench_propagate(reps, flush_l2=True)
 ctx.memoize(want_gains=False)
 print(cfg, res)

@@ -362,26 +362,24 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
                     par[4 * k] = p4.x; par[4 * k + 1] = p4.y; par[4 * k + 2] = p4.z; par[4 * k + 3] = p4.w;
                 }
             }
-            // software-pipelined slot loads: the next slot's id, hash and
-            // threshold are in flight while this slot is tested
-            uint32_t nu = (uint32_t)v;
-            int32_t nhs = 0, nt = tu;
-            if (s0 < s1) {
-                nu = (uint32_t)__ldg(adj + s0);
-                nhs = __ldg(hash + s0);
-                if (!UNI) nt = __ldg(thr + s0);
+            // the prefix in batches of 32 slots: one coalesced load per
+            // batch (lane i holds slot b0 + i), the slots then broadcast by
+            // shuffles -- one memory round trip per 32 slots, not per slot
+            for (int64_t b0 = s0; b0 < s1; b0 += 32) {
+            const int64_t sb = b0 + lane;
+            uint32_t bu = (uint32_t)v;
+            int32_t bh = 0, bt = tu;
+            if (sb < s1) {
+                bu = (uint32_t)__ldg(adj + sb);
+                bh = __ldg(hash + sb);
+                if (!UNI) bt = __ldg(thr + sb);
             }
-            for (int64_t sl = s0; sl < s1; ++sl) {
-                const uint32_t u = nu;
-                const int32_t h = nhs, t = UNI ? tu : nt;
-                if (u >= (uint32_t)v) break;
-                if (sl + 1 < s1) {
-                    nu = (uint32_t)__ldg(adj + sl + 1);
-                    nhs = __ldg(hash + sl + 1);
-                    if (!UNI) nt = __ldg(thr + sl + 1);
-                } else {
-                    nu = (uint32_t)v;
-                }
+            // rows ascend, so the smaller neighbours are a prefix of the batch
+            const int cnt = __popc(__ballot_sync(FULL, bu < (uint32_t)v));
+            for (int j = 0; j < cnt; ++j) {
+                const uint32_t u = __shfl_sync(FULL, bu, j);
+                const int32_t h = __shfl_sync(FULL, bh, j);
+                const int32_t t = UNI ? tu : __shfl_sync(FULL, bt, j);
                 if (PASS == 1) {
                     // rows ascend, so the first live neighbour is the
                     // smallest: one predicated min per lane
@@ -430,6 +428,8 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
                         nh += unite(L, ld, a2, b2, rr);
                     }
                 }
+            }
+            if (cnt < 32) break;         // the prefix ended inside this batch
             }
             if (PASS == 1) {
 #pragma unroll

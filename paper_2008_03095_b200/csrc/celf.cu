@@ -342,19 +342,6 @@ __device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, co
     return (int64_t)*acc_sh;
 }
 
-__device__ __forceinline__ unsigned long long block_max(unsigned long long x, unsigned long long *red) {
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
-        x = y > x ? y : x;
-    }
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
-    __syncthreads();
-    unsigned long long m = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = red[k] > m ? red[k] : m;
-    return m;
-}
-
 template <bool ENC>
 __global__ void __launch_bounds__(256, 4) k_celf_rounds(
     int32_t k, int vb, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, uint32_t *__restrict__ cov,
@@ -366,7 +353,6 @@ __global__ void __launch_bounds__(256, 4) k_celf_rounds(
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
     int32_t bpct, int32_t ngroup) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ unsigned long long red[8];
     __shared__ unsigned long long sback[kSmemBack];
     __shared__ unsigned long long gacc[8];
     if (threadIdx.x < 8) gacc[threadIdx.x] = 0;

@@ -85,8 +85,8 @@ def _key_le(pa, va, pb, vb) -> bool:
 
 def _lex_best(ids: np.ndarray, gains: np.ndarray):
     """(gain, id) of the lexicographic best of a batch: max gain, then min id."""
-    j = int(np.lexsort((ids, -gains))[0])
-    return int(gains[j]), int(ids[j])
+    g = gains.max()
+    return int(g), int(ids[gains == g].min())
 
 
 def select_rounds(shard, comm, k: int, batch0: int = 64):
@@ -158,7 +158,12 @@ def select_rounds(shard, comm, k: int, batch0: int = 64):
             trace.append(rec)
             keep = ids[:kr] != best_v
             bi, bg = ids[:kr][keep], fresh[:kr][keep]
-            o = np.lexsort((bi, -bg))             # back into the order sorted by (-fresh, id)
+            # back into the order sorted by (-fresh, id): one argsort of the
+            # packed key fresh * 2^32 + (2^32 - 1 - id) when gains fit 31 bits
+            if len(bg) and bg.max() < (1 << 31):
+                o = np.argsort(-((bg << 32) | (0xFFFFFFFF - bi)), kind="stable")
+            else:
+                o = np.lexsort((bi, -bg))
             back_ids = bi[o].astype(np.int32)
             back_prio = bg[o]
             batch0 = max(64, kr)

@@ -33,3 +33,13 @@ for rep in range(3):
     same = s1.tolist() == s2.tolist() and np.array_equal(np.asarray(tr1), tr2)
     print(f"{cfg}: persistent kernel {1e3 * (t1 - t0):.2f} ms, host-driven rounds {1e3 * (t3 - t2):.2f} ms "
           f"({c.K} rounds, {len(tr2)} trace records), identical={same}")
+
+if "--profile" in sys.argv:
+    import cProfile
+    import pstats
+    ctx.celf_reset(gains)
+    pr = cProfile.Profile()
+    pr.enable()
+    select_rounds(ctx, LocalComm(), c.K)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(12)

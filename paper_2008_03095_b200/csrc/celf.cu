@@ -212,8 +212,8 @@ static int celf_advance(imx_ctx *c, int64_t k, const int32_t *ids, const unsigne
     c->ocur = nxt;
     c->ostart = 0;
     c->olen += cnt;
-    // the staging buffers are reused next round: make sure the copies are done
-    IMX_CUDA(cudaStreamSynchronize(c->st));
+    // the staging buffers are reused next round: both callers read the commit
+    // gain back and synchronise the stream before returning
     return IMX_OK;
 }
 

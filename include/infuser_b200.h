@@ -172,6 +172,15 @@ int  imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out);
  * imx_celf_trace).  Requires a fresh imx_celf_reset.                       */
 int  imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out,
                      int64_t *gains_out, int64_t *trace_len);
+/* The same loop over a lane shard of a multi-rank run (select_rounds,
+ * celf.py): allreduce(buf, n, user) must replace buf[0, n) by its int64 sum
+ * over the ranks (every rank calls it in the same order); partial gains of
+ * each evaluated batch and the commit self-check go through it.  Requires a
+ * fresh imx_celf_reset with the GLOBAL initial gains.                       */
+typedef int (*imx_allreduce_fn)(int64_t *buf, int64_t n, void *user);
+int  imx_celf_select_sharded(imx_ctx *c, int32_t k, imx_allreduce_fn allreduce,
+                             void *user, int32_t *seeds_out, int64_t *gains_out,
+                             int64_t *trace_len);
 /* The trace of the last imx_celf_select: records of 5 int64
  * (vertex, stale_gain, fresh_gain, committed, seeds_before) -- TraceRecord,
  * selection.py:25-33 -- up to cap records.                                 */

@@ -82,6 +82,7 @@ _SIGNATURES = {
     "imx_eval_gains": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p]),
     "imx_commit": (c_i32, [c_void_p, c_i32, P(c_i64)]),
     "imx_celf_select": (c_i32, [c_void_p, c_i32, c_void_p, c_void_p, P(c_i64)]),
+    "imx_celf_select_sharded": (c_i32, [c_void_p, c_i32, c_void_p, c_void_p, c_void_p, c_void_p, P(c_i64)]),
     "imx_celf_trace": (c_i32, [c_void_p, c_void_p, c_i64]),
     "imx_celf_trace_take": (c_i32, [c_void_p, P(c_void_p), P(c_i64)]),
     "imx_host_free": (None, [c_void_p]),

@@ -17,6 +17,9 @@ import numpy as np
 from . import _lib
 from ._lib import MODE_NAMES, PropStats, Timings, check, ptr
 
+# int (*)(int64_t *buf, int64_t n, void *user): imx_allreduce_fn
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, ctypes.c_void_p)
+
 __all__ = ["DeviceContext", "empty_graph"]
 
 _EMPTY = {}
@@ -168,6 +171,33 @@ class DeviceContext:
         gains = np.empty(k, np.int64)
         tl = ctypes.c_int64()
         check(lib.imx_celf_select(self.handle, int(k), ptr(seeds), ptr(gains), ctypes.byref(tl)))
+        return seeds, gains, _take_trace(self.handle)
+
+    def celf_select_sharded(self, k: int, comm):
+        """The CELF loop over this context's lane shard with the per-batch
+        int64 sums over ranks done by ``comm.allreduce`` (celf.select_rounds
+        semantics, driven from native code): (seeds, gains, trace (T, 5))."""
+        lib = _lib.load()
+        seeds = np.empty(k, np.int32)
+        gains = np.empty(k, np.int64)
+        tl = ctypes.c_int64()
+        err = []
+
+        def reduce(buf, n, _user):
+            try:
+                a = np.ctypeslib.as_array(buf, shape=(n,))
+                a[:] = comm.allreduce(a.copy())
+                return 0
+            except BaseException as e:          # surfaced after the call
+                err.append(e)
+                return 1
+
+        cb = ALLREDUCE_FN(reduce)
+        rc = lib.imx_celf_select_sharded(self.handle, int(k), ctypes.cast(cb, ctypes.c_void_p), None,
+                                         ptr(seeds), ptr(gains), ctypes.byref(tl))
+        if err:
+            raise err[0]
+        check(rc)
         return seeds, gains, _take_trace(self.handle)
 
     def per_sim(self) -> np.ndarray:

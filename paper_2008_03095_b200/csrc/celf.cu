@@ -739,7 +739,46 @@ extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
 }
 
 // One round on the host-driven path (prefix batches + advance), synchronous.
-static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seeds_out, int64_t *gains_out) {
+// Sharded rounds (imx_celf_select_sharded): every evaluated batch's partial
+// gains are summed over the ranks by the caller's allreduce before any
+// decision, so all ranks take identical ones; the previous round's commit
+// self-check rides along as one extra element of the next batch.
+struct ShardReduce {
+    imx_allreduce_fn fn = nullptr;
+    void *user = nullptr;
+    bool pending = false;           // a commit gain waits for its check
+    int64_t pending_got = 0, pending_want = 0;
+    int32_t pending_v = -1;
+    std::vector<int64_t> buf;
+};
+
+static int shard_check(const ShardReduce &sr, int64_t total) {
+    if (total != sr.pending_want) {
+        set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                  (long long)total, (long long)sr.pending_want, sr.pending_v);
+        return IMX_EINTERNAL;
+    }
+    return IMX_OK;
+}
+
+// allreduce of fr[0, cnt) (+ the pending commit gain) in place
+static int shard_reduce(ShardReduce &sr, int64_t *fr, int64_t cnt) {
+    sr.buf.assign(fr, fr + cnt);
+    if (sr.pending) sr.buf.push_back(sr.pending_got);
+    if (sr.fn((int64_t *)sr.buf.data(), (int64_t)sr.buf.size(), sr.user) != 0) {
+        set_error("allreduce callback failed");
+        return IMX_EINTERNAL;
+    }
+    std::copy(sr.buf.begin(), sr.buf.begin() + cnt, fr);
+    if (sr.pending) {
+        IMX_TRY(shard_check(sr, sr.buf[cnt]));
+        sr.pending = false;
+    }
+    return IMX_OK;
+}
+
+static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seeds_out, int64_t *gains_out,
+                           ShardReduce *sr = nullptr) {
     auto rec = [&](int64_t v, int64_t s, int64_t f, int64_t com) {
         int64_t *o = c->trace + c->trace_n;
         o[0] = v; o[1] = s; o[2] = f; o[3] = com; o[4] = t;
@@ -767,6 +806,7 @@ static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seed
         for (;;) {
             if ((int64_t)ids.size() < hi + 1) { ids.resize(hi + 1); keys.resize(hi + 1); fr.resize(hi + 1); }
             IMX_TRY(celf_prefix(c, lo, hi, ids.data() + lo, keys.data() + lo, fr.data() + lo));
+            if (sr) IMX_TRY(shard_reduce(*sr, fr.data() + lo, hi - lo));
             for (int64_t i = lo; i < hi; ++i)
                 if (best_v < 0 || key_le(fr[i], ids[i], best_f, best_v)) { best_f = fr[i]; best_v = ids[i]; }
             if (hi >= len) break;
@@ -796,7 +836,12 @@ static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seed
     unsigned long long got = 0;
     IMX_CUDA(cudaMemcpyAsync(&got, gain, sizeof got, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
-    if ((int64_t)got != best_f) {
+    if (sr) {                       // partial gain: checked after the next allreduce
+        sr->pending = true;
+        sr->pending_got = (int64_t)got;
+        sr->pending_want = best_f;
+        sr->pending_v = best_v;
+    } else if ((int64_t)got != best_f) {
         set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
                   (long long)got, (long long)best_f, best_v);
         return IMX_EINTERNAL;
@@ -1042,6 +1087,38 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
         }
         IMX_TRY(celf_host_round(c, t, batch0, seeds.data(), gains.data()));   // status 4 or host mode
         ++t;
+    }
+    if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
+    if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);
+    cudaEventRecord(c->ev[7], c->st);
+    cudaEventSynchronize(c->ev[7]);
+    cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
+    c->tm.celf_evaluations = c->evaluated;
+    if (trace_len) *trace_len = c->trace_n / 5;
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_select_sharded(imx_ctx *c, int32_t k, imx_allreduce_fn allreduce, void *user,
+                                       int32_t *seeds_out, int64_t *gains_out, int64_t *trace_len) {
+    CELF_CHECK(c);
+    const int64_t n = c->g->n;
+    if (!allreduce) { set_error("allreduce callback is NULL"); return IMX_EINVAL; }
+    if (k < 1 || k > n) { set_error("k=%d invalid for n=%lld", k, (long long)n); return IMX_ECONSTRAINT; }
+    if (c->olen != n) { set_error("CELF state already advanced (call imx_celf_reset)"); return IMX_EINVAL; }
+    cudaEventRecord(c->ev[6], c->st);
+    c->trace_n = 0;
+    c->evaluated = 0;
+    std::vector<int32_t> seeds(k);
+    std::vector<int64_t> gains(k);
+    ShardReduce sr;
+    sr.fn = allreduce;
+    sr.user = user;
+    int64_t batch0 = 64;
+    for (int32_t t = 0; t < k; ++t) IMX_TRY(celf_host_round(c, t, batch0, seeds.data(), gains.data(), &sr));
+    if (sr.pending) {               // the last commit has no later batch to ride on
+        int64_t g = sr.pending_got;
+        if (allreduce(&g, 1, user) != 0) { set_error("allreduce callback failed"); return IMX_EINTERNAL; }
+        IMX_TRY(shard_check(sr, g));
     }
     if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
     if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);

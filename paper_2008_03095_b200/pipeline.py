@@ -16,7 +16,7 @@ import time
 
 import numpy as np
 
-from .celf import LocalComm, TorchComm, lane_window, select_rounds
+from .celf import LocalComm, TorchComm, lane_window
 from .context import DeviceContext
 from .graph import Graph
 from .hashing import EdgeHashTable, SimulationRandoms, build_hash_table
@@ -121,7 +121,8 @@ def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0
         seeds, gains_k, trace = ctx.celf_select(k)
     else:
         ctx.celf_reset(gains)
-        seeds, gains_k, trace = select_rounds(ctx, comm, k)
+        # the select_rounds loop, driven from native code with comm's allreduce
+        seeds, gains_k, trace = ctx.celf_select_sharded(k, comm)
     selection = result_from_context(ctx, seeds, gains_k, trace, randoms.num_scored)
     if comm.size > 1:
         per_sim = np.concatenate(comm.allgather(ctx.per_sim()))

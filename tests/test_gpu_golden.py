@@ -294,3 +294,75 @@ def test_trace_buffers_are_owned_by_their_results(gpu):
     import gc
     gc.collect()
     assert np.array_equal(t2, z["trace"][: len(t2)])
+
+
+class _ThreadGroupComm:
+    """Ranks as threads of one process (one lane shard each, same device):
+    allreduce = barrier-synchronised int64 sum, for the native sharded loop."""
+
+    def __init__(self, size):
+        import threading
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.bufs = [None] * size
+
+    def rank(self, r):
+        group = self
+
+        class _Comm:
+            rank, size = r, group.size
+
+            def allreduce(self, x):
+                group.bufs[r] = np.asarray(x, np.int64).copy()
+                group.barrier.wait()
+                total = np.sum(group.bufs, axis=0)
+                group.barrier.wait()
+                return total
+
+        return _Comm()
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3])
+@pytest.mark.parametrize("name", ["er_mid_300", "er_pad20", "er_const1_r16", "cfg_c1", "kat_ties"])
+def test_native_sharded_celf_matches_reference(gpu, name, shards):
+    """imx_celf_select_sharded: each lane shard runs the native round loop in
+    its own thread, partial gains summed through the callback; every shard
+    must produce the reference's seeds, gains and full trace."""
+    import threading
+    from paper_2008_03095_b200.celf import lane_window
+    from paper_2008_03095_b200.context import DeviceContext
+    z = load_golden(name)
+    g = build_graph(gpu, z)
+    randoms = gpu.SimulationRandoms(int(z["R"]), int(z["master_seed"]))
+    table = gpu.build_hash_table(g)
+    table.bind(g)
+    ctxs = []
+    for rank in range(shards):
+        a, b, scored = lane_window(randoms.padded, randoms.num_scored, rank, shards)
+        c = DeviceContext(g, randoms.values[a:b], scored, a)
+        c.propagate()
+        ctxs.append(c)
+    gains = sum(c.memoize() for c in ctxs)
+    for c in ctxs:
+        c.celf_reset(gains)
+    grp = _ThreadGroupComm(shards)
+    out = [None] * shards
+    errs = []
+
+    def run(r):
+        try:
+            out[r] = ctxs[r].celf_select_sharded(int(z["k"]), grp.rank(r))
+        except BaseException as e:       # noqa: BLE001 -- re-raised below
+            errs.append(e)
+            grp.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(shards)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for seeds, sg, trace in out:
+        assert seeds.tolist() == z["seeds"].tolist()
+        assert sg.tolist() == z["seed_gains"].tolist()
+        assert np.array_equal(np.asarray(trace), z["trace"])

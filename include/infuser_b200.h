@@ -131,6 +131,10 @@ int  imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st);
  * histogram over all lanes, int64 gains over the scored lanes.
  * gains_out may be NULL (gains stay on the device for CELF).              */
 int  imx_memoize(imx_ctx *c, int64_t *gains_out);
+/* Fuse the memo into propagation where the labels are compressed in lane
+ * tiles (very wide label matrices): the gains are summed from each tile
+ * while it is on chip, and the next imx_memoize only copies them out.      */
+int  imx_set_fuse_memo(imx_ctx *c, int32_t on);
 
 /* Load labels (and optionally sizes; NULL -> recomputed from labels) from
  * the host instead of propagating: select_seeds / initial_marginal_gains on

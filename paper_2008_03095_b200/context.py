@@ -93,6 +93,10 @@ class DeviceContext:
                 [MODE_NAMES[int(x)] for x in modes[:k]])
 
     # -- K4/K5 ------------------------------------------------------------------
+    def set_fuse_memo(self, on: bool = True):
+        """Sum the gains inside the next propagations' tiled compression."""
+        check(_lib.load().imx_set_fuse_memo(self.handle, 1 if on else 0))
+
     def memoize(self, want_gains: bool = True):
         out = np.empty(self.n, np.int64) if want_gains else None
         check(_lib.load().imx_memoize(self.handle, ptr(out)))

@@ -96,6 +96,9 @@ struct imx_ctx {
     unsigned long long *scratch = nullptr;  // [16]; [8..12] = CELF round header
     bool labels_ready = false, memo_ready = false, celf_ready = false;
     cudaEvent_t ev[8];
+    // memoisation fused into the tiled compression (imx_set_fuse_memo): the
+    // last propagate left the gains in `gains` (gains_fused)
+    bool fuse_memo = false, gains_fused = false;
     imx_timings tm{};
 };
 
@@ -125,6 +128,8 @@ int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
 // sld, dld; nq quads per row): lane tiles in and out of contiguous scratch
 int launch_tile_copy(const uint32_t *src, int64_t sld, uint32_t *dst, int64_t dld, int64_t n, int nq,
                      cudaStream_t st);
+int launch_gains_tile(const uint32_t *T, int64_t n, int64_t tld, int32_t ns_t, int first, int64_t *gains,
+                      cudaStream_t st);
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
                     cudaStream_t st, int *launches = nullptr);
 

@@ -80,6 +80,46 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
     }
 }
 
+// Gains of one compressed lane tile T[n][tld] (lanes l0.. of the matrix, the
+// first ns_t of them scored), while the tile is still in L2 (the tiled
+// compression of propagate.cu, when the caller fused the memo into it): 8
+// threads per row, a thread per 16-byte quad, root gathers inside the tile;
+// gains[v] = (first tile ? 0 : gains[v]) + the row's tile sum.
+__global__ void __launch_bounds__(256) k_gains_tile(const uint32_t *__restrict__ T, int64_t n, int64_t tld,
+                                                    int32_t ns_t, int first, int64_t *__restrict__ gains) {
+    const int64_t nthreads = n * 8;
+    const int nqr = (int)(tld >> 2);
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < nthreads; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const int64_t v = i >> 3;
+        const int q = (int)(i & 7);
+        unsigned long long acc = 0;
+        if (i < nthreads && q < nqr && 4 * q < ns_t) {
+            const uint4 l = __ldg(reinterpret_cast<const uint4 *>(T + v * tld) + q);
+            const uint32_t w[4] = {l.x, l.y, l.z, l.w};
+            uint32_t rw[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                rw[k] = (is_root(w[k]) || 4 * q + k >= ns_t) ? w[k] : __ldg(T + (int64_t)w[k] * tld + 4 * q + k);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (4 * q + k < ns_t) acc += (rw[k] & COUNT) + 1u;
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (i < nthreads && q == 0) gains[v] = (first ? 0 : gains[v]) + (int64_t)acc;
+    }
+}
+
+int launch_gains_tile(const uint32_t *T, int64_t n, int64_t tld, int32_t ns_t, int first, int64_t *gains,
+                      cudaStream_t st) {
+    if (n == 0) return IMX_OK;
+    k_gains_tile<<<grid_for(n * 8), 256, 0, st>>>(T, n, tld, ns_t, first, gains);
+    IMX_CHECK_LAUNCH();
+    note_launch();
+    return IMX_OK;
+}
+
 // decoded labels / sizes of rows [v0, v0+cnt), lanes [r0, r1) -> dense out
 template <bool ENC>
 __global__ void k_labels_window(const uint32_t *__restrict__ L, int64_t v0, int64_t cnt, int64_t ld,
@@ -157,7 +197,9 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
     if (!c->labels_ready) { set_error("labels not computed (call imx_propagate first)"); return IMX_EINVAL; }
     const int64_t n = c->g->n;
     IMX_CUDA(cudaEventRecord(c->ev[4], c->st));
-    if (n) {
+    if (n && c->gains_fused && !c->C) {
+        // already summed by the tiled compression of the last propagate
+    } else if (n) {
         if (c->C) {
             k_gains_caller<<<grid_for(n * 32), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->ns, c->gains);
         } else {
@@ -177,6 +219,7 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
 
 extern "C" int imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t *sizes, int64_t ldh) {
     CTX_CHECK(c);
+    c->gains_fused = false;
     const int64_t n = c->g->n;
     if (!labels && n) { set_error("labels is NULL"); return IMX_EINVAL; }
     if (ldh < c->W) { set_error("row stride %lld < width %d", (long long)ldh, c->W); return IMX_EINVAL; }

@@ -1026,12 +1026,19 @@ static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
         k_tile_copy<<<grid_for(n * nq), 256, 0, c->st>>>(c->L + l0, c->ld, T, tld, n, nq);
         int k = 0;
         rc = launch_compress(T, n, tld, wl, nonroot, c->st, &k);
+        if (rc == IMX_OK && c->fuse_memo && !c->C) {
+            // the memo's gains over this tile's scored lanes, while it is in L2
+            const int32_t ns_t = (int32_t)std::max<int64_t>(0, std::min<int64_t>(wl, c->ns - l0));
+            if (l0 == 0 || ns_t > 0) rc = launch_gains_tile(T, n, tld, ns_t, l0 == 0, c->gains, c->st);
+            c->tm.kernel_launches++;
+        }
         k_tile_copy<<<grid_for(n * nq), 256, 0, c->st>>>(T, tld, c->L + l0, c->ld, n, nq);
         count_launch(c, 2);
         c->tm.kernel_launches += k;
     }
     cudaFreeAsync(T, c->st);
     IMX_CHECK_LAUNCH();
+    if (rc == IMX_OK && c->fuse_memo && !c->C) c->gains_fused = true;
     return rc;
 }
 
@@ -1064,8 +1071,15 @@ static void push_stat(imx_prop_stats *st, int mode, int64_t changed, int64_t lsu
 
 using namespace imx;
 
+extern "C" int imx_set_fuse_memo(imx_ctx *c, int32_t on) {
+    CTX_CHECK(c);
+    c->fuse_memo = on != 0;
+    return IMX_OK;
+}
+
 extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
     CTX_CHECK(c);
+    c->gains_fused = false;
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (st) st->sweeps = 0;
@@ -1131,6 +1145,7 @@ extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
 extern "C" int imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2, float *avg_total_ms,
                                    float *avg_hook_ms, float *avg_compress_ms, float *avg_init_ms) {
     CTX_CHECK(c);
+    c->gains_fused = false;
     if (reps < 1) { set_error("reps must be >= 1"); return IMX_EINVAL; }
     uint4 *fb = nullptr;
     const int64_t fcnt = (int64_t(256) << 20) / 16;  // 256 MB > 126 MB L2

@@ -105,7 +105,7 @@ def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0
 
     t = time.perf_counter()
     a, b, scored = lane_window(randoms.padded, randoms.num_scored, comm.rank, comm.size)
-    ctx, _ = propagated_context(g, table, randoms.values[a:b], scored, lane0=a)
+    ctx, _ = propagated_context(g, table, randoms.values[a:b], scored, lane0=a, fuse_memo=True)
     timings["propagate"] = time.perf_counter() - t
 
     t = time.perf_counter()

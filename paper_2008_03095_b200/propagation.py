@@ -47,11 +47,15 @@ def _width(randoms, num_simulations) -> int:
 
 
 def propagated_context(g: Graph, table: EdgeHashTable | None, X: np.ndarray, num_scored: int,
-                       verify: bool = False, stats: bool = False, lane0: int = 0):
-    """Create a context for lanes X on g, bind the hash table, propagate."""
+                       verify: bool = False, stats: bool = False, lane0: int = 0,
+                       fuse_memo: bool = False):
+    """Create a context for lanes X on g, bind the hash table, propagate
+    (with the memo fused into a tiled compression when ``fuse_memo``)."""
     if table is not None:
         table.bind(g)
     ctx = DeviceContext(g, X, num_scored, lane0)
+    if fuse_memo:
+        ctx.set_fuse_memo(True)
     st = ctx.propagate(verify=verify, stats=stats)
     return ctx, st
 

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <vector>
 #include <chrono>
+#include <functional>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -273,6 +274,7 @@ __global__ void k_reciprocal(const int64_t *__restrict__ xadj, const int32_t *__
         if (lo < end && adj[lo] == u) {
             recip[s] = lo;
             recip[lo] = s;
+            if (!w) continue;                 // thresholds later (k_thresholds)
             const int32_t t1 = thr_of(w[s]), t2 = thr_of(w[lo]);
             const int32_t t = t1 > t2 ? t1 : t2;
             thr[s] = t;
@@ -595,7 +597,10 @@ done:
 // threshold range and sum).  structure = build sources (if missing),
 // reciprocal slots, hashes and the canonical edge list (new CSR); otherwise
 // only the thresholds and the index are refreshed (new weights / hashes).
-static int graph_analyze(imx_graph *g, bool structure) {
+// late_weights (structure pass only): enqueues the weight upload after the
+// weight-free structure kernels and makes the graph stream wait for it; the
+// pairing then runs without thresholds and k_thresholds follows the upload
+static int graph_analyze(imx_graph *g, bool structure, const std::function<int()> &late_weights = nullptr) {
     cudaStream_t st = g->stream;
     const int64_t m2 = g->m2, n = g->n;
     GStats *gs = nullptr;
@@ -616,7 +621,8 @@ static int graph_analyze(imx_graph *g, bool structure) {
         IMX_TRY(dalloc(g, &g->cslot, m2));
         if (m2) {
             IMX_CUDA(cudaMemsetAsync(g->recip, 0xff, sizeof(int64_t) * m2, st));     // -1
-            k_reciprocal<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, g->w, n, m2, g->recip, g->thr, gs);
+            k_reciprocal<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, late_weights ? nullptr : g->w, n,
+                                                        m2, g->recip, g->thr, gs);
             k_recip_check<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, g->recip, m2, &gs->flags);
             note_launch();
             k_slot_hashes<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, g->hash);
@@ -638,11 +644,13 @@ static int graph_analyze(imx_graph *g, bool structure) {
             cudaFreeAsync(flag, st);
         }
     }
+    if (late_weights) IMX_TRY(late_weights());
     // thresholds: symmetrized through the reciprocal slots unless the
     // adjacency is known not to be symmetric (a structure pass decides below)
-    // (a structure pass computed them with the reciprocal search)
+    // (a structure pass computed them with the reciprocal search, unless the
+    // weights arrive late)
     const bool sym_try = structure || g->symmetric;
-    if (m2 && !structure) {
+    if (m2 && (!structure || late_weights)) {
         k_thresholds<<<grid_for(m2), 256, 0, st>>>(g->w, sym_try ? g->recip : nullptr, g->src, g->adj, g->hash,
                                                    m2, g->thr, gs);
         note_launch();
@@ -841,11 +849,37 @@ extern "C" int imx_graph_from_csr(int32_t device, int64_t n, int64_t m2, const i
     auto fail = [&](int code) { graph_free(g); return code; };
     if (dalloc(g, &g->xadj, n + 1) || dalloc(g, &g->adj, m2) || dalloc(g, &g->w, m2)) return fail(IMX_ENOMEM);
     if (upload_h2d(g->xadj, xadj, sizeof(int64_t) * (n + 1), st) != cudaSuccess ||
-        (m2 && upload_h2d(g->adj, adj, sizeof(int32_t) * m2, st) != cudaSuccess) ||
-        (m2 && upload_h2d(g->w, weights, sizeof(double) * m2, st) != cudaSuccess))
+        (m2 && upload_h2d(g->adj, adj, sizeof(int32_t) * m2, st) != cudaSuccess))
         return fail(cuda_fail(cudaGetLastError(), "upload csr", __FILE__, __LINE__));
+    // large graphs: the weights (8 bytes per slot, the biggest array) go up on
+    // a second stream while the weight-free structure kernels run
+    const char *lw = getenv("IMX_LATE_WEIGHTS");
+    const bool late = m2 > 0 && (lw ? atoi(lw) != 0 : m2 >= ((int64_t)1 << 22));
+    if (!late && m2 && upload_h2d(g->w, weights, sizeof(double) * m2, st) != cudaSuccess)
+        return fail(cuda_fail(cudaGetLastError(), "upload weights", __FILE__, __LINE__));
     g_clock.mark("upload csr", st);
-    int rc = graph_analyze(g, true);
+    cudaStream_t wst = nullptr;
+    cudaEvent_t wev = nullptr;
+    if (late) {
+        // g->w was allocated on st: the weight stream starts after that (and
+        // not after the structure kernels, which it is meant to overlap)
+        if (acquire_stream(device, &wst) != cudaSuccess ||
+            cudaEventCreateWithFlags(&wev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventRecord(wev, st) != cudaSuccess || cudaStreamWaitEvent(wst, wev, 0) != cudaSuccess) {
+            if (wst) release_stream(device, wst);
+            if (wev) cudaEventDestroy(wev);
+            return fail(cuda_fail(cudaGetLastError(), "weight stream", __FILE__, __LINE__));
+        }
+    }
+    auto upload_weights = [&]() -> int {
+        IMX_CUDA(upload_h2d(g->w, weights, sizeof(double) * m2, wst));
+        IMX_CUDA(cudaEventRecord(wev, wst));
+        IMX_CUDA(cudaStreamWaitEvent(st, wev, 0));
+        return IMX_OK;
+    };
+    int rc = late ? graph_analyze(g, true, upload_weights) : graph_analyze(g, true);
+    if (wst) release_stream(device, wst);
+    if (wev) cudaEventDestroy(wev);
     if (rc != IMX_OK) return fail(rc);
     *out = g;
     return IMX_OK;

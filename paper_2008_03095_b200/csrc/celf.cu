@@ -342,6 +342,11 @@ __device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, co
     return (int64_t)*acc_sh;
 }
 
+#ifndef IMX_CELF_STEP_PER_CTA
+#define IMX_CELF_STEP_PER_CTA 256
+#endif
+constexpr int64_t kStepPerCta = IMX_CELF_STEP_PER_CTA;
+
 template <bool ENC>
 __global__ void __launch_bounds__(256, 4) k_celf_rounds(
     int32_t k, int vb, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, uint32_t *__restrict__ cov,
@@ -454,7 +459,13 @@ __global__ void __launch_bounds__(256, 4) k_celf_rounds(
                 if (prof) pf[8] += gtimer() - ts;
                 if (stop) break;
                 lo = hi;
-                const int64_t step = batch0 > hi ? batch0 : hi;
+                // doubling batches, but at most ~256 candidates per CTA per
+                // step: a round that refreshes millions of vertices (C4's
+                // round 1 after the hub) would otherwise evaluate up to twice
+                // its refreshed prefix in the last doubling
+                int64_t step = batch0 > hi ? batch0 : hi;
+                const int64_t cap = (int64_t)gridDim.x * kStepPerCta;
+                if (step > cap) step = cap;
                 hi = (olen - hi < step) ? olen : hi + step;
             }
             // refreshed prefix: stale key >= best fresh key (keys sorted descending)

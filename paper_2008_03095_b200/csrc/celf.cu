@@ -348,7 +348,10 @@ __device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, co
 constexpr int64_t kStepPerCta = IMX_CELF_STEP_PER_CTA;
 
 template <bool ENC>
-__global__ void __launch_bounds__(256, 4) k_celf_rounds(
+#ifndef IMX_CELF_MINB
+#define IMX_CELF_MINB 4
+#endif
+__global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
     int32_t k, int vb, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, uint32_t *__restrict__ cov,
     int64_t ld, int32_t ns, int32_t cw, int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
     int32_t *oid0, int32_t *oid1, unsigned long long *okey0, unsigned long long *okey1,

@@ -857,6 +857,15 @@ static int ensure_heavy(imx_ctx *c, int T) {
     return IMX_OK;
 }
 
+// blocks per SM of the pull grids (IMX_PULL_BPSM, default 16): about three
+// times what fits at once -- later waves of blocks measured faster than one
+// resident wave (C3: 4.76 / 4.65 / 4.55 ms at one wave / 8 / 16 per SM;
+// C2p1 0.487 / 0.464 / 0.443 ms; 32 per SM is slower on C2p1)
+static int pull_bpsm() {
+    const char *e = getenv("IMX_PULL_BPSM");
+    return e && atoi(e) > 0 ? atoi(e) : 16;
+}
+
 static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const int64_t n = g->n;
@@ -868,7 +877,7 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     const int64_t ldp = (c->ld + lpt - 1) / lpt * lpt;
     const size_t smem = sizeof(int32_t) * ldp + sizeof(uint32_t) * 3 * (32 + 32 * lpt) * 8;
     if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
-    const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 8);
+    const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * pull_bpsm());
     using KF = void (*)(const int64_t *, const int32_t *, const int32_t *, const int32_t *, int32_t, int64_t,
                         const int32_t *, int32_t, int64_t, uint32_t *, unsigned long long *, const uint8_t *,
                         const int32_t *, const int64_t *, const int32_t *, int64_t);
@@ -883,7 +892,7 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
         KF kern = kerns[h][pass - 1][g->uniform ? 1 : 0][wide ? 1 : 0];
         if (smem > 48 * 1024)
             IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int hb = h ? (int)std::min<int64_t>(ceil_div(g->nhs, 8), 148 * 8) : blocks;
+        const int hb = h ? (int)std::min<int64_t>(ceil_div(g->nhs, 8), 148 * pull_bpsm()) : blocks;
         kern<<<hb, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld, c->L, hooks,
                                        g->nhs > 0 ? g->heavy : nullptr, g->hs_v, g->hs_a, g->hs_len, g->nhs);
         IMX_CHECK_LAUNCH();

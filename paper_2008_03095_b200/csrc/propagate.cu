@@ -743,7 +743,11 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest
     IMX_CHECK_LAUNCH();
     size_t tb = c->scan_tmp_bytes;
     IMX_CUDA(cub::DeviceScan::ExclusiveSum(c->scan_tmp, tb, c->seg_n, c->seg_off, nseg + 1, c->st));
-    const int blocks = 148 * 8;
+    // blocks per SM: one resident wave, or two for huge enumerations (C4's
+    // 307M live pairs: 22.4 -> 21.8 ms; C2's 1.8M pairs prefer one)
+    const char *eb_env = getenv("IMX_ENUM_BPSM");
+    const double pairs = (double)g->me * (double)c->W * g->thr_mean;
+    const int blocks = 148 * (eb_env && atoi(eb_env) > 0 ? atoi(eb_env) : (pairs > 1e8 ? 16 : 8));
     auto kern = g->uniform ? (skip_forest ? k_hook_enum<true, true> : k_hook_enum<true, false>)
                            : (skip_forest ? k_hook_enum<false, true> : k_hook_enum<false, false>);
     // lanes per launch (IMX_ENUM_BLOCK, default all): launches run one after
@@ -966,7 +970,12 @@ int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long
         const int32_t wl = (int32_t)std::min<int64_t>(win, W - l0);
         // grid stride = a whole number of rows, so every thread keeps its quad
         const int64_t nq = (wl + 3) >> 2;
-        const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * 2);
+        // threads: one resident wave (148 x 2048) for small matrices, four
+        // for large ones (C2 77 -> 68 us at one; C3 1.06 -> 1.00 ms, C4 6.35
+        // -> 5.85 ms at four)
+        const char *cw_env = getenv("IMX_COMPRESS_WAVES");
+        const int waves = cw_env && atoi(cw_env) > 0 ? atoi(cw_env) : (n * nq >= ((int64_t)1 << 26) ? 4 : 1);
+        const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * waves);
         const int64_t rows = std::max<int64_t>(1, want / nq);
         const int64_t threads = rows * nq;
         const int blocks = (int)ceil_div(threads, 256);

@@ -876,7 +876,8 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     if (n == 0) return IMX_OK;
     IMX_TRY(ensure_heavy(c, pull_heavy_T(g)));
     // 8 lanes per thread once a row spans several warp-widths of quads
-    const bool wide = c->W >= 256;
+    const char *wm = getenv("IMX_PULL_WIDE_MIN");
+    const bool wide = c->W >= (wm && atoi(wm) > 0 ? atoi(wm) : 256);
     const int lpt = wide ? 8 : 4;
     const int64_t ldp = (c->ld + lpt - 1) / lpt * lpt;
     const size_t smem = sizeof(int32_t) * ldp + sizeof(uint32_t) * 3 * (32 + 32 * lpt) * 8;

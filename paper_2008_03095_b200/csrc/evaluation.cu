@@ -333,7 +333,9 @@ extern "C" int imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k,
                     k_eval_worlds<<<grid_for(nw, 128), 128, 0, st>>>(sv[0], sv[1], sv[2], sv[3], o, nw, me, ws);
                     note_launch();
                     const int gx = (int)((nw + 127) / 128);
-                    const int gy = (int)std::min<int64_t>(nruns, std::max<int64_t>(1, 148 * 16 / gx));
+                    const char *hb = getenv("IMX_EVAL_BPSM");
+                    const int64_t bpsm = hb && atoi(hb) > 0 ? atoi(hb) : 64;   // C2 2.31M -> 2.42M worlds/s against 16
+                    const int gy = (int)std::min<int64_t>(nruns, std::max<int64_t>(1, 148 * bpsm / gx));
                     k_eval_hook<<<dim3(gx, gy), 128, 0, st>>>(ce, t53, me, jt, ws, sv[2], sv[3], nw, L, ld);
                     note_launch();
                     if ((e = cudaGetLastError())) { fail(e, "k_eval_hook"); break; }

@@ -162,7 +162,8 @@ extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t
     if ((e = pool_alloc((void **)&c->X, sizeof(int32_t) * c->ld, c->st)) != cudaSuccess ||
         (e = pool_alloc((void **)&c->L, sizeof(uint32_t) * cells, c->st)) != cudaSuccess ||
         (e = pool_alloc((void **)&c->gains, sizeof(int64_t) * (n + 1), c->st)) != cudaSuccess ||
-        (e = pool_alloc((void **)&c->scratch, sizeof(unsigned long long) * 16, c->st)) != cudaSuccess) {
+        (e = pool_alloc((void **)&c->scratch, sizeof(unsigned long long) * 16, c->st)) != cudaSuccess ||
+        (e = cudaMemsetAsync(c->scratch, 0, sizeof(unsigned long long) * 16, c->st)) != cudaSuccess) {
         return fail(cuda_fail(e, "cudaMalloc(context)", __FILE__, __LINE__));
     }
     std::vector<int32_t> xpad(c->ld, 0);

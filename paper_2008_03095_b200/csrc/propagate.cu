@@ -154,6 +154,33 @@ __device__ __forceinline__ int64_t hash_lower_bound(const int32_t *__restrict__ 
     return lo;
 }
 
+// both bounds of a segment, the two searches advanced in lock step so their
+// dependent loads overlap (the same result as two hash_lower_bound calls)
+__device__ __forceinline__ void hash_lower_bound2(const int32_t *__restrict__ EH, const int32_t *__restrict__ lut,
+                                                  int bits, const int64_t *__restrict__ boff, int b, uint64_t k1,
+                                                  uint64_t k2, int64_t &r1, int64_t &r2) {
+    const int64_t per = ((int64_t)1 << bits) + 1;
+    const int64_t end = boff[b + 1];
+    int64_t lo1 = end, hi1 = end, lo2 = end, hi2 = end;
+    if (k1 < (1ull << 31)) {
+        const int64_t q = (int64_t)(k1 >> (31 - bits));
+        lo1 = lut[b * per + q]; hi1 = lut[b * per + q + 1];
+    }
+    if (k2 < (1ull << 31)) {
+        const int64_t q = (int64_t)(k2 >> (31 - bits));
+        lo2 = lut[b * per + q]; hi2 = lut[b * per + q + 1];
+    }
+    while (lo1 < hi1 || lo2 < hi2) {
+        const int64_t m1 = (lo1 + hi1) >> 1, m2 = (lo2 + hi2) >> 1;
+        const bool a1 = lo1 < hi1, a2 = lo2 < hi2;
+        const uint32_t h1 = a1 ? (uint32_t)EH[m1] : 0u, h2 = a2 ? (uint32_t)EH[m2] : 0u;
+        if (a1) { if ((uint64_t)h1 < k1) lo1 = m1 + 1; else hi1 = m1; }
+        if (a2) { if ((uint64_t)h2 < k2) lo2 = m2 + 1; else hi2 = m2; }
+    }
+    r1 = lo1;
+    r2 = lo2;
+}
+
 __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
                             const int32_t *__restrict__ btmax, const int64_t *__restrict__ boff,
                             const int32_t *__restrict__ EH, const int32_t *__restrict__ lut, int bits,
@@ -170,8 +197,9 @@ __global__ void k_seg_count(const int32_t *__restrict__ X, int32_t W, int nb,
             const uint32_t x = (uint32_t)X[r];
             const uint64_t start = ((uint64_t)((t ^ x) >> (i + 1)) << (i + 1)) | (uint64_t)(x & (1u << i));
             const uint64_t end = start + (1ull << i);
-            a = hash_lower_bound(EH, lut, bits, boff, b, start);
-            cnt = hash_lower_bound(EH, lut, bits, boff, b, end) - a;
+            int64_t e;
+            hash_lower_bound2(EH, lut, bits, boff, b, start, end, a, e);
+            cnt = e - a;
         }
         seg_a[s] = a;
         seg_n[s] = cnt;

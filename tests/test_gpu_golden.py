@@ -366,3 +366,34 @@ def test_native_sharded_celf_matches_reference(gpu, name, shards):
         assert seeds.tolist() == z["seeds"].tolist()
         assert sg.tolist() == z["seed_gains"].tolist()
         assert np.array_equal(np.asarray(trace), z["trace"])
+
+
+@pytest.mark.parametrize("tile", ["4", "8", "12"])
+@pytest.mark.parametrize("name", ["er_mid_300", "er_big_1000", "er_pad20", "cfg_c1"])
+def test_tiled_compress_and_fused_memo_match_reference(gpu, name, tile, monkeypatch):
+    """Lane-tiled compression (the default only for very wide label matrices)
+    with the memo fused into it (run_fused), forced on small cases: labels,
+    sizes, seeds, gains and the full trace equal the reference's."""
+    monkeypatch.setenv("IMX_COMPRESS_TILE", tile)
+    z = load_golden(name)
+    g = build_graph(gpu, z)
+    run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))
+    check_array(z, "labels", run.labels)
+    check_array(z, "sizes", run.sizes)
+    assert run.seeds == z["seeds"].tolist()
+    assert run.selection.gains == z["seed_gains"].tolist()
+    assert np.array_equal(run.selection.trace.array, z["trace"])
+
+
+@pytest.mark.parametrize("name", ["er_mid_300", "er_big_1000", "cfg_c1", "cfg_c2"])
+def test_late_weight_upload_matches_reference(gpu, name, monkeypatch):
+    """Host-CSR graphs with the weights uploaded on a second stream behind the
+    structure kernels (the default above 4M slots), forced on small cases."""
+    monkeypatch.setenv("IMX_LATE_WEIGHTS", "1")
+    z = load_golden(name)
+    g0 = build_graph(gpu, z)
+    g = gpu.Graph(g0.xadj, g0.adj, g0.weights, g0.orig_ids)        # host arrays -> imx_graph_from_csr
+    assert np.array_equal(gpu.slot_thresholds(g), gpu.slot_thresholds(g0))
+    run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))
+    assert run.seeds == z["seeds"].tolist()
+    assert np.array_equal(run.selection.trace.array, z["trace"])

@@ -181,6 +181,7 @@ extern "C" void imx_destroy(imx_ctx *c) { ctx_free(c); }
 extern "C" int imx_get_timings(imx_ctx *c, imx_timings *out) {
     CTX_CHECK(c);
     if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
+    settle_timings(c);
     *out = c->tm;
     return IMX_OK;
 }

@@ -96,6 +96,8 @@ struct imx_ctx {
     unsigned long long *scratch = nullptr;  // [16]; [8..12] = CELF round header
     bool labels_ready = false, memo_ready = false, celf_ready = false;
     cudaEvent_t ev[8];
+    // phase timings not read back yet: 1 = propagate (ev 0-3), 2 = memo (ev 4-5)
+    int tm_pending = 0;
     // memoisation fused into the tiled compression (imx_set_fuse_memo): the
     // last propagate left the gains in `gains` (gains_fused)
     bool fuse_memo = false, gains_fused = false;
@@ -108,6 +110,22 @@ inline int grid_for(int64_t work, int threads = 256) {
     int64_t b = ceil_div(work > 0 ? work : 1, threads);
     if (b > 148 * 16) b = 148 * 16;
     return (int)b;
+}
+
+// read the pending phase times (waits for their end events)
+inline void settle_timings(imx_ctx *c) {
+    if (c->tm_pending & 1) {
+        if (cudaEventSynchronize(c->ev[3]) == cudaSuccess) {
+            cudaEventElapsedTime(&c->tm.init_ms, c->ev[0], c->ev[1]);
+            cudaEventElapsedTime(&c->tm.hook_ms, c->ev[1], c->ev[2]);
+            cudaEventElapsedTime(&c->tm.compress_ms, c->ev[2], c->ev[3]);
+            cudaEventElapsedTime(&c->tm.propagate_ms, c->ev[0], c->ev[3]);
+        }
+    }
+    if (c->tm_pending & 2) {
+        if (cudaEventSynchronize(c->ev[5]) == cudaSuccess) cudaEventElapsedTime(&c->tm.memoize_ms, c->ev[4], c->ev[5]);
+    }
+    c->tm_pending = 0;
 }
 
 inline void count_launch(imx_ctx *c, int k = 1) {

@@ -1142,11 +1142,10 @@ extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
         IMX_CUDA(cudaEventRecord(c->ev[2], c->st));
     }
     IMX_CUDA(cudaEventRecord(c->ev[3], c->st));
-    IMX_CUDA(cudaEventSynchronize(c->ev[3]));
-    cudaEventElapsedTime(&c->tm.init_ms, c->ev[0], c->ev[1]);
-    cudaEventElapsedTime(&c->tm.hook_ms, c->ev[1], c->ev[2]);
-    cudaEventElapsedTime(&c->tm.compress_ms, c->ev[2], c->ev[3]);
-    cudaEventElapsedTime(&c->tm.propagate_ms, c->ev[0], c->ev[3]);
+    // no host sync here: the caller's next calls (memo, CELF reset) are
+    // enqueued while the device still propagates; the phase times are read
+    // when asked for (imx_get_timings)
+    c->tm_pending |= 1;
     c->labels_ready = true;
     c->memo_ready = false;
     c->celf_ready = false;

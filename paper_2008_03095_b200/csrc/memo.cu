@@ -114,7 +114,10 @@ __global__ void __launch_bounds__(256) k_gains_tile(const uint32_t *__restrict__
 int launch_gains_tile(const uint32_t *T, int64_t n, int64_t tld, int32_t ns_t, int first, int64_t *gains,
                       cudaStream_t st) {
     if (n == 0) return IMX_OK;
-    k_gains_tile<<<grid_for(n * 8), 256, 0, st>>>(T, n, tld, ns_t, first, gains);
+    const char *e = getenv("IMX_GAINS_TILE_BPSM");
+    const int64_t bpsm = e && atoi(e) > 0 ? atoi(e) : 16;
+    const int gb = (int)std::min<int64_t>(ceil_div(n * 8, 256), 148 * bpsm);
+    k_gains_tile<<<gb, 256, 0, st>>>(T, n, tld, ns_t, first, gains);
     IMX_CHECK_LAUNCH();
     note_launch();
     return IMX_OK;

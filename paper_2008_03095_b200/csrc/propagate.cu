@@ -1030,9 +1030,16 @@ __global__ void k_tile_copy(const uint32_t *__restrict__ src, int64_t sld, uint3
     }
 }
 
+// tile copies: IMX_TILE_COPY_BPSM blocks per SM (default 64: C5 compress 59.3 -> 58.5 ms against 16)
+static int tile_copy_grid(int64_t work) {
+    const char *e = getenv("IMX_TILE_COPY_BPSM");
+    const int64_t bpsm = e && atoi(e) > 0 ? atoi(e) : 64;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * bpsm));
+}
+
 int launch_tile_copy(const uint32_t *src, int64_t sld, uint32_t *dst, int64_t dld, int64_t n, int nq,
                      cudaStream_t st) {
-    k_tile_copy<<<grid_for(n * nq), 256, 0, st>>>(src, sld, dst, dld, n, nq);
+    k_tile_copy<<<tile_copy_grid(n * nq), 256, 0, st>>>(src, sld, dst, dld, n, nq);
     IMX_CHECK_LAUNCH();
     note_launch();
     return IMX_OK;
@@ -1070,7 +1077,7 @@ static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
         const int32_t wl = (int32_t)std::min<int64_t>(tw, c->W - l0);
         const int64_t tld = (wl + 3) / 4 * 4;
         const int nq = (int)(tld >> 2);
-        k_tile_copy<<<grid_for(n * nq), 256, 0, c->st>>>(c->L + l0, c->ld, T, tld, n, nq);
+        k_tile_copy<<<tile_copy_grid(n * nq), 256, 0, c->st>>>(c->L + l0, c->ld, T, tld, n, nq);
         int k = 0;
         rc = launch_compress(T, n, tld, wl, nonroot, c->st, &k);
         if (rc == IMX_OK && c->fuse_memo && !c->C) {
@@ -1079,7 +1086,7 @@ static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
             if (l0 == 0 || ns_t > 0) rc = launch_gains_tile(T, n, tld, ns_t, l0 == 0, c->gains, c->st);
             c->tm.kernel_launches++;
         }
-        k_tile_copy<<<grid_for(n * nq), 256, 0, c->st>>>(T, tld, c->L + l0, c->ld, n, nq);
+        k_tile_copy<<<tile_copy_grid(n * nq), 256, 0, c->st>>>(T, tld, c->L + l0, c->ld, n, nq);
         count_launch(c, 2);
         c->tm.kernel_launches += k;
     }

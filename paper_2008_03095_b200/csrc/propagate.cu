@@ -837,13 +837,14 @@ static bool prefix_balanced(const imx_graph *g) {
     return (double)g->max_prefix <= std::max(64.0, balanced_prefix);
 }
 
-// slots per heavy slice: IMX_PULL_HEAVY (0 = no splitting), else 8 for
-// unbalanced graphs (C3: 8.5 ms by enumeration, 7.1 / 5.2 / 5.0 ms pulled
-// with 64 / 32 / 16 / 8-slot slices: 7.1 / 5.2 / 5.0 / 4.8) and no splitting for balanced ones, where
+// slots per heavy slice: IMX_PULL_HEAVY (0 = no splitting), else 10 for
+// unbalanced graphs (C3: 8.5 ms by enumeration; pulled with 4 / 6 / 8 / 10 /
+// 12 / 16 / 24-slot slices 4.80 / 4.56 / 4.49 / 4.41 / 4.42 / 4.52 / 4.57 ms --
+// pass 1 prefers long slices, pass 2 short ones) and no splitting for balanced ones, where
 // the extra passes only add work (C2p1: 0.47 -> 0.58 ms at 32)
 static int pull_heavy_T(const imx_graph *g) {
     if (const char *e = getenv("IMX_PULL_HEAVY")) return std::max(0, atoi(e));
-    return prefix_balanced(g) ? 0 : 8;
+    return prefix_balanced(g) ? 0 : 10;
 }
 
 // the heavy-row slices of the graph for slice length T, cached on the graph

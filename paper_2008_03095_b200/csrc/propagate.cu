@@ -1000,11 +1000,13 @@ int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long
         const int32_t wl = (int32_t)std::min<int64_t>(win, W - l0);
         // grid stride = a whole number of rows, so every thread keeps its quad
         const int64_t nq = (wl + 3) >> 2;
-        // threads: one resident wave (148 x 2048) for small matrices, four
-        // for large ones (C2 77 -> 68 us at one; C3 1.06 -> 1.00 ms, C4 6.35
-        // -> 5.85 ms at four)
+        // threads: one resident wave (148 x 2048) for small matrices, more for
+        // large ones (C2 77 -> 68 us at one wave instead of two; C3 1.06 ->
+        // 0.98 ms at eight; C4 6.35 -> 5.46 ms at sixteen)
         const char *cw_env = getenv("IMX_COMPRESS_WAVES");
-        const int waves = cw_env && atoi(cw_env) > 0 ? atoi(cw_env) : (n * nq >= ((int64_t)1 << 26) ? 4 : 1);
+        const int64_t quads = n * nq;
+        const int waves = cw_env && atoi(cw_env) > 0 ? atoi(cw_env)
+                          : (quads < ((int64_t)1 << 26) ? 1 : (quads < ((int64_t)1 << 29) ? 8 : 16));
         const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * waves);
         const int64_t rows = std::max<int64_t>(1, want / nq);
         const int64_t threads = rows * nq;

@@ -497,7 +497,8 @@ void graph_free(imx_graph *g) {
     cudaSetDevice(g->dev);
     void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
                     g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff, g->lut,
-                    g->heavy, g->hs_v, g->hs_a, g->hs_len};
+                    g->hv[0].heavy, g->hv[0].hs_v, g->hv[0].hs_a, g->hv[0].hs_len,
+                    g->hv[1].heavy, g->hv[1].hs_v, g->hv[1].hs_a, g->hv[1].hs_len};
     for (void *p : ptrs) if (p) cudaFreeAsync(p, g->stream);
     release_stream(g->dev, g->stream);
     delete g;

@@ -37,15 +37,18 @@ struct imx_graph {
     int uniform = 1;         // all thresholds equal
     int hash_neg = 0;        // some hash has bit 31 set (caller table): no interval enumeration
     int symmetric = 1;
-    // pull sampler: vertices whose smaller-neighbour prefix exceeds heavy_T
-    // slots (heavy[v] = 1) and their prefix slices (vertex, first slot,
-    // length), built on first use (propagate.cu, ensure_heavy)
-    int heavy_T = -1;
-    uint8_t *heavy = nullptr;
-    int32_t *hs_v = nullptr;
-    int64_t *hs_a = nullptr;
-    int32_t *hs_len = nullptr;
-    int64_t nhs = 0;
+    // pull sampler, one table per pass: vertices whose smaller-neighbour
+    // prefix exceeds hv[p].T slots (heavy[v] = 1) and their prefix slices
+    // (vertex, first slot, length), built on first use (propagate.cu,
+    // ensure_heavy)
+    struct HeavySlices {
+        int T = -1;
+        uint8_t *heavy = nullptr;
+        int32_t *hs_v = nullptr;
+        int64_t *hs_a = nullptr;
+        int32_t *hs_len = nullptr;
+        int64_t nhs = 0;
+    } hv[2];
 };
 
 namespace imx {

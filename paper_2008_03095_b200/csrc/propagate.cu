@@ -848,24 +848,25 @@ static int pull_heavy_T(const imx_graph *g) {
 }
 
 // the heavy-row slices of the graph for slice length T, cached on the graph
-static int ensure_heavy(imx_ctx *c, int T) {
+static int ensure_heavy(imx_ctx *c, int pass, int T) {
     imx_graph *g = c->g;
-    if (g->heavy_T == T) return IMX_OK;
-    for (void **p : {(void **)&g->heavy, (void **)&g->hs_v, (void **)&g->hs_a, (void **)&g->hs_len}) {
+    auto &H = g->hv[pass - 1];
+    if (H.T == T) return IMX_OK;
+    for (void **p : {(void **)&H.heavy, (void **)&H.hs_v, (void **)&H.hs_a, (void **)&H.hs_len}) {
         if (*p) cudaFreeAsync(*p, c->st);
         *p = nullptr;
     }
-    g->nhs = 0;
-    g->heavy_T = -1;
-    if (T <= 0 || g->max_prefix <= T) { g->heavy_T = T; return IMX_OK; }
+    H.nhs = 0;
+    H.T = -1;
+    if (T <= 0 || g->max_prefix <= T) { H.T = T; return IMX_OK; }
     const int64_t n = g->n;
     int32_t *pre = nullptr;
     int64_t *nsl = nullptr, *off = nullptr;
-    IMX_CUDA(pool_alloc((void **)&g->heavy, n, c->st));
+    IMX_CUDA(pool_alloc((void **)&H.heavy, n, c->st));
     IMX_CUDA(pool_alloc((void **)&pre, sizeof(int32_t) * n, c->st));
     IMX_CUDA(pool_alloc((void **)&nsl, sizeof(int64_t) * (n + 1), c->st));
     IMX_CUDA(pool_alloc((void **)&off, sizeof(int64_t) * (n + 1), c->st));
-    k_heavy_count<<<grid_for(n), 256, 0, c->st>>>(g->xadj, g->adj, n, T, g->heavy, pre, nsl);
+    k_heavy_count<<<grid_for(n), 256, 0, c->st>>>(g->xadj, g->adj, n, T, H.heavy, pre, nsl);
     IMX_CHECK_LAUNCH();
     size_t tb = 0;
     IMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nsl, off, n + 1, c->st));
@@ -876,17 +877,17 @@ static int ensure_heavy(imx_ctx *c, int T) {
     IMX_CUDA(cudaMemcpyAsync(&total, off + n, sizeof total, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
     if (total > 0) {
-        IMX_CUDA(pool_alloc((void **)&g->hs_v, sizeof(int32_t) * total, c->st));
-        IMX_CUDA(pool_alloc((void **)&g->hs_a, sizeof(int64_t) * total, c->st));
-        IMX_CUDA(pool_alloc((void **)&g->hs_len, sizeof(int32_t) * total, c->st));
-        k_heavy_fill<<<grid_for(n), 256, 0, c->st>>>(g->xadj, n, T, pre, nsl, off, g->hs_v, g->hs_a, g->hs_len);
+        IMX_CUDA(pool_alloc((void **)&H.hs_v, sizeof(int32_t) * total, c->st));
+        IMX_CUDA(pool_alloc((void **)&H.hs_a, sizeof(int64_t) * total, c->st));
+        IMX_CUDA(pool_alloc((void **)&H.hs_len, sizeof(int32_t) * total, c->st));
+        k_heavy_fill<<<grid_for(n), 256, 0, c->st>>>(g->xadj, n, T, pre, nsl, off, H.hs_v, H.hs_a, H.hs_len);
         IMX_CHECK_LAUNCH();
     }
     note_launch(total > 0 ? 4 : 3);
     for (void *p : {(void *)pre, (void *)nsl, (void *)off, tmp}) cudaFreeAsync(p, c->st);
     IMX_CUDA(cudaStreamSynchronize(c->st));   // the slices are shared by every context of the graph
-    g->nhs = total;
-    g->heavy_T = T;
+    H.nhs = total;
+    H.T = T;
     return IMX_OK;
 }
 
@@ -903,7 +904,14 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (n == 0) return IMX_OK;
-    IMX_TRY(ensure_heavy(c, pull_heavy_T(g)));
+    // pass 1 (atomicMin per slice and lane) prefers longer slices than
+    // pass 2 (unions per slice): its table uses IMX_PULL_HEAVY1 (3) x T slots
+    // (C3 pass 1 0.94 -> 0.83 ms)
+    const int T2 = pull_heavy_T(g);
+    const char *h1 = getenv("IMX_PULL_HEAVY1");
+    const int T = pass == 1 && T2 > 0 ? T2 * (h1 && atoi(h1) > 0 ? atoi(h1) : 3) : T2;
+    IMX_TRY(ensure_heavy(c, pass, T));
+    const auto &H = g->hv[pass - 1];
     // 8 lanes per thread once a row spans several warp-widths of quads
     const char *wm = getenv("IMX_PULL_WIDE_MIN");
     const bool wide = c->W >= (wm && atoi(wm) > 0 ? atoi(wm) : 256);
@@ -921,14 +929,14 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
          {{k_pull<2, false, 4, false>, k_pull<2, false, 8, false>}, {k_pull<2, true, 4, false>, k_pull<2, true, 8, false>}}},
         {{{k_pull<1, false, 4, true>, k_pull<1, false, 8, true>}, {k_pull<1, true, 4, true>, k_pull<1, true, 8, true>}},
          {{k_pull<2, false, 4, true>, k_pull<2, false, 8, true>}, {k_pull<2, true, 4, true>, k_pull<2, true, 8, true>}}}};
-    const int hv = g->nhs > 0 ? 2 : 1;
+    const int hv = H.nhs > 0 ? 2 : 1;
     for (int h = 0; h < hv; ++h) {
         KF kern = kerns[h][pass - 1][g->uniform ? 1 : 0][wide ? 1 : 0];
         if (smem > 48 * 1024)
             IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int hb = h ? (int)std::min<int64_t>(ceil_div(g->nhs, 8), 148 * pull_bpsm()) : blocks;
+        const int hb = h ? (int)std::min<int64_t>(ceil_div(H.nhs, 8), 148 * pull_bpsm()) : blocks;
         kern<<<hb, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld, c->L, hooks,
-                                       g->nhs > 0 ? g->heavy : nullptr, g->hs_v, g->hs_a, g->hs_len, g->nhs);
+                                       H.nhs > 0 ? H.heavy : nullptr, H.hs_v, H.hs_a, H.hs_len, H.nhs);
         IMX_CHECK_LAUNCH();
         count_launch(c);
     }

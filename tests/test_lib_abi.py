@@ -51,3 +51,27 @@ def test_product_package_never_imports_the_oracle():
     for py in pkg.rglob("*.py"):
         src = py.read_text()
         assert "import oracle" not in src and "from oracle" not in src, py
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/infuser_b200.h compiles as C99 (no C++ or torch types at the
+    boundary) and a C program links against the library's symbols."""
+    import shutil
+    import subprocess
+    from paper_2008_03095_b200 import _lib
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc unavailable")
+    src = tmp_path / "abi.c"
+    src.write_text('#include "infuser_b200.h"\n'
+                   "int main(void) {\n"
+                   "    const char *(*err)(void) = imx_last_error;\n"
+                   "    imx_allreduce_fn f = 0;\n"
+                   "    (void)f;\n"
+                   "    return err == 0;\n"
+                   "}\n")
+    lib = _lib.library_path()
+    out = subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-I", str(ROOT / "include"), str(src),
+                          "-o", str(tmp_path / "abi"), str(lib), f"-Wl,-rpath,{lib.parent}"],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr

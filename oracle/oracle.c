@@ -15,6 +15,9 @@
  *     sweeps; the reference's index/sparse sweeps reach the same fixpoint)
  *   - component sizes and int64 gains     propagation.py:371-390
  *   - CELF with a (-gain, id) min-heap    selection.py:115-149
+ *   - config-scale checker: union-find labels per lane (oracles.py:112-133),
+ *     lane-chunked sizes + fresh-gain tables, and the same CELF heap driven
+ *     by the fresh-gain table (selection.py:63-70, 115-149)
  *
  * Threads: the lanes are independent samples, so lane blocks are split over
  * OpenMP threads; each thread runs its own lanes to their fixpoint in place
@@ -228,6 +231,163 @@ int64_t oracle_celf(int64_t n, int64_t W, const int32_t *labels, const int32_t *
         ++ntrace;
     }
     free(heap); free(fresh_at); free(owned);
+    return ntrace;
+}
+
+/* ------------------------------------------------------------------------
+ * Config-scale checker: the same fixpoint and the same
+ * selection as above, restated so that they run lane chunk by lane chunk on
+ * graphs whose full (n, R) matrices do not fit the dense restatement's time
+ * budget (C4: 4.19M x 1024, C5: 1M x 8192).
+ * ------------------------------------------------------------------------ */
+
+/* Component labels by union-find over the live edges of each lane -- the
+ * reference's own independent label oracle is a per-lane BFS
+ * (oracles.py:112-133, bfs_component_labels); any exact CC algorithm reaches
+ * the unique fixpoint of propagate (propagation.py:1-8: every vertex gets
+ * the minimum id of its component).  Roots are kept minimal (the larger root
+ * is linked under the smaller), so find(v) is that minimum.  Membership is
+ * the reference's strict signed (X[r] ^ h) < thr (hashing.py:141-150), each
+ * undirected edge tested once from its lower endpoint's row.  Lanes are
+ * processed 8 at a time per thread (one parent array per lane). */
+static inline int32_t uf_find(int32_t *p, int32_t x) {
+    while (p[x] != x) { p[x] = p[p[x]]; x = p[x]; }
+    return x;
+}
+
+void oracle_uf_labels(int64_t n, const int64_t *xadj, const int32_t *adj, const int32_t *hashes,
+                      const int32_t *thr, int32_t thr_uniform, const int32_t *X, int64_t W,
+                      int32_t *labels, int nthreads) {
+    enum { B = 8 };
+    const int64_t nblocks = (W + B - 1) / B;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel
+    {
+        int32_t *par = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n ? n : 1) * B);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t b = 0; b < nblocks; ++b) {
+            const int64_t r0 = b * B, nb = (W - r0) < B ? (W - r0) : B;
+            int32_t x[B];
+            for (int j = 0; j < B; ++j) x[j] = j < nb ? X[r0 + j] : 0;
+            for (int j = 0; j < nb; ++j)
+                for (int64_t v = 0; v < n; ++v) par[j * n + v] = (int32_t)v;
+            for (int64_t v = 0; v < n; ++v) {
+                for (int64_t s = xadj[v]; s < xadj[v + 1]; ++s) {
+                    const int32_t u = adj[s];
+                    if (u <= v) continue;                 /* each undirected edge once */
+                    const int32_t h = hashes[s], t = thr ? thr[s] : thr_uniform;
+                    unsigned live = 0;
+                    for (int j = 0; j < B; ++j) live |= (unsigned)((x[j] ^ h) < t) << j;
+                    live &= (1u << nb) - 1u;
+                    while (live) {
+                        const int j = __builtin_ctz(live);
+                        live &= live - 1;
+                        int32_t *p = par + j * n;
+                        int32_t a = uf_find(p, (int32_t)v), c = uf_find(p, u);
+                        if (a == c) continue;
+                        if (a < c) p[c] = a; else p[a] = c;
+                    }
+                }
+            }
+            for (int j = 0; j < nb; ++j) {
+                int32_t *p = par + j * n;
+                for (int64_t v = 0; v < n; ++v) labels[v * W + r0 + j] = uf_find(p, (int32_t)v);
+            }
+        }
+        free(par);
+    }
+}
+
+/* One lane chunk of the selection check.  labels / sizes are this chunk's
+ * (n, W) columns, lanes [0, ns) of it scored.  Given the claimed seed
+ * sequence seeds[0..K), component c of lane r is covered from step
+ * cs(c, r) = min{t : labels[seeds[t]][r] == c} on (K if never).  The
+ * reference's marginal_gain (selection.py:63-70) of v at step t -- given
+ * S_<t = seeds[0..t) -- sums size(comp(v, r)) over the lanes where
+ * t <= cs(comp(v, r), r); it is accumulated as a difference table
+ * D[(K+1) x n] (D[0][v] += size, D[cs+1][v] -= size), so the prefix sums
+ * over t of all chunks' D give every fresh gain of every step.  sizes_out
+ * is component_sizes (propagation.py:349-356) of the chunk; per_sim[r]
+ * (lanes < ns) counts the vertices covered after all K seeds
+ * (SelectionResult.spread_se, selection.py:106-112). */
+void oracle_chunk_cover(int64_t n, int64_t W, const int32_t *labels, int64_t ns, const int32_t *seeds,
+                        int32_t K, int32_t *sizes_out, int64_t *D, int64_t *per_sim, int nthreads) {
+    int32_t *cs = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * W > 0 ? n * W : 1));
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n * W; ++i) { sizes_out[i] = 0; cs[i] = K; }
+    /* rows in order (each label row read once, contiguous); the histogram
+     * scatters into row labels[v][r] <= v */
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; ++v)
+        for (int64_t r = 0; r < W; ++r) {
+#pragma omp atomic
+            sizes_out[(int64_t)labels[v * W + r] * W + r] += 1;
+        }
+    for (int32_t t = K - 1; t >= 0; --t)
+        for (int64_t r = 0; r < W; ++r) cs[(int64_t)labels[(int64_t)seeds[t] * W + r] * W + r] = t;
+    for (int64_t r = 0; r < ns; ++r) per_sim[r] = 0;
+#pragma omp parallel
+    {
+        int64_t *cov = (int64_t *)calloc((size_t)(ns > 0 ? ns : 1), sizeof(int64_t));
+#pragma omp for schedule(static)
+        for (int64_t v = 0; v < n; ++v) {
+            for (int64_t r = 0; r < ns; ++r) {
+                const int64_t l = labels[v * W + r];
+                const int64_t sz = sizes_out[l * W + r];
+                const int32_t c = cs[l * W + r];
+                D[v] += sz;
+                if (c < K) { D[(int64_t)(c + 1) * n + v] -= sz; cov[r] += 1; }
+            }
+        }
+#pragma omp critical
+        for (int64_t r = 0; r < ns; ++r) per_sim[r] += cov[r];
+        free(cov);
+    }
+    free(cs);
+}
+
+/* select_seeds (selection.py:115-149) driven by a table of fresh gains:
+ * F[t][v] = marginal_gain(v) given the first t seeds (t < K).  The heap,
+ * fresh_at rule and trace are exactly oracle_celf's; only marginal_gain is a
+ * table lookup.  Returns the number of dequeues (trace records). */
+int64_t oracle_celf_fresh(int64_t n, int32_t k, const int64_t *F, int32_t *seeds_out, int64_t *gains_out,
+                          int64_t *trace, int64_t trace_cap) {
+    if (k < 1 || k > n) return -1;
+    hkey *heap = (hkey *)malloc(sizeof(hkey) * (size_t)n);
+    int64_t *fresh_at = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    for (int64_t v = 0; v < n; ++v) { heap[v].neg = -F[v]; heap[v].v = (int32_t)v; }
+    int64_t len = n;
+    for (int64_t i = n / 2 - 1; i >= 0; --i) sift_down(heap, len, i);
+    int32_t nseeds = 0;
+    int64_t ntrace = 0;
+    while (nseeds < k) {
+        hkey top = heap[0];
+        heap[0] = heap[--len];
+        sift_down(heap, len, 0);
+        const int32_t u = top.v;
+        const int64_t stale = -top.neg;
+        int64_t rec[5];
+        if (fresh_at[u] == nseeds) {
+            seeds_out[nseeds] = u;
+            gains_out[nseeds] = stale;
+            rec[0] = u; rec[1] = stale; rec[2] = stale; rec[3] = 1; rec[4] = nseeds;
+            ++nseeds;
+        } else {
+            const int64_t f = F[(int64_t)nseeds * n + u];
+            fresh_at[u] = nseeds;
+            heap[len].neg = -f; heap[len].v = u;
+            sift_up(heap, len++);
+            rec[0] = u; rec[1] = stale; rec[2] = f; rec[3] = 0; rec[4] = nseeds;
+        }
+        if (trace && ntrace < trace_cap) memcpy(trace + 5 * ntrace, rec, sizeof rec);
+        ++ntrace;
+    }
+    free(heap); free(fresh_at);
     return ntrace;
 }
 

@@ -16,6 +16,7 @@ sys.path.insert(0, str(ROOT))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100) and libinfuser_b200.so")
     config.addinivalue_line("markers", "slow: long-running")
+    config.addinivalue_line("markers", "scale: full BASELINE-config parity (minutes on the GPU box)")
 
 
 def golden_names(prefix: str = "") -> list[str]:

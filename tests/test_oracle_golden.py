@@ -130,3 +130,67 @@ def test_oracle_celf_equals_stepwise_argmax(orc):
         seeds.append(u)
         owned[labels[u, :ns], cols] = True
     assert seeds == z["seeds"].tolist()
+
+
+# ---- the config-scale checker, pinned on every fixture ----
+
+@pytest.mark.parametrize("name", ALL)
+def test_oracle_uf_labels_match_reference(orc, name):
+    """Per-lane union-find labels == the reference's propagate labels."""
+    z = load_golden(name)
+    xadj, adj, _ = orc.csr_from_edges(int(z["n"]), z["edges"].astype(np.int64))
+    w = _golden_weights(orc, z, xadj, adj)
+    thr = orc.thresholds(w, orc.reciprocal(xadj, adj))
+    uni = len(thr) > 0 and bool((thr == thr[0]).all())
+    labels = orc.uf_labels(xadj, adj, orc.hash_table(xadj, adj), int(thr[0]) if uni else thr,
+                           z["X"], nthreads=4)
+    if "labels" in z:
+        assert np.array_equal(labels, z["labels"])
+    assert sha(labels) == str(z["labels_sha"])
+
+
+@pytest.mark.parametrize("chunks", ["one", "ragged", "reversed"])
+@pytest.mark.parametrize("name", ALL)
+def test_oracle_selection_check_matches_reference(orc, name, chunks):
+    """Lane-chunked sizes + fresh-gain table + heap == the reference's
+    sizes, initial gains, seeds, seed gains, trace and spread_se, for any
+    lane chunking (the checker used at config scale on the GPU box)."""
+    z = load_golden(name)
+    n, R, k = int(z["n"]), int(z["R"]), int(z["k"])
+    xadj, adj, _ = orc.csr_from_edges(n, z["edges"].astype(np.int64))
+    w = _golden_weights(orc, z, xadj, adj)
+    thr = orc.thresholds(w, orc.reciprocal(xadj, adj))
+    labels = orc.uf_labels(xadj, adj, orc.hash_table(xadj, adj), thr, z["X"], nthreads=4)
+    W = labels.shape[1]
+    cuts = {"one": [0, W], "ragged": sorted({0, min(W, 3), min(W, 11), W}),
+            "reversed": [0, W // 2, W]}[chunks]
+    spans = list(zip(cuts[:-1], cuts[1:]))
+    if chunks == "reversed":
+        spans = spans[::-1]
+    chk = orc.SelectionCheck(n, k, z["seeds"], R)
+    sizes = np.empty_like(labels)
+    for a, b in spans:
+        sizes[:, a:b] = chk.add_chunk(labels[:, a:b], a, nthreads=3)
+    out = chk.result()
+    assert sha(sizes) == str(z["sizes_sha"])
+    assert np.array_equal(out["gains"], z["gains"])
+    assert out["seeds"].tolist() == z["seeds"].tolist()
+    assert out["seed_gains"].tolist() == z["seed_gains"].tolist()
+    assert out["sigma"] == int(z["sigma"])
+    assert np.array_equal(out["trace"], z["trace"])
+    assert out["spread_se"] == pytest.approx(float(z["spread_se"]), rel=1e-12, abs=1e-15)
+
+
+def test_oracle_selection_check_flags_a_wrong_seed(orc):
+    """A claimed sequence that deviates at step t yields the reference's
+    seeds up to t and a different seed at t (so the comparison fails)."""
+    z = load_golden("er_mid_300")
+    n, R, k = int(z["n"]), int(z["R"]), int(z["k"])
+    claimed = z["seeds"].copy()
+    other = next(v for v in range(n) if v not in set(claimed.tolist()))
+    claimed[2] = other
+    chk = orc.SelectionCheck(n, k, claimed, R)
+    chk.add_chunk(z["labels"], 0)
+    out = chk.result()
+    assert out["seeds"][:3].tolist() == z["seeds"][:3].tolist()
+    assert out["seeds"].tolist() != claimed.tolist()

@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["LocalComm", "TorchComm", "select_rounds", "lane_window"]
+__all__ = ["LocalComm", "TorchComm", "select_rounds", "lane_window", "gather_owned"]
 
 
 class LocalComm:
@@ -68,6 +68,24 @@ class TorchComm:
         v = np.zeros(self.size, np.int64)
         v[self.rank] = k
         return self.allreduce(v)
+
+
+def gather_owned(ctx, comm) -> np.ndarray:
+    """SeedState.owned (n, num_scored) of a sharded run: every rank's covered
+    bitmap over its lane window (imx_copy_owned), all-gathered and
+    concatenated along the lanes in rank order (= lane order)."""
+    bits = ctx.owned_bits()                                    # (n, ceil(ns_local/32)) uint32
+    n = bits.shape[0]
+    counts = comm.allgather(np.array([ctx.num_scored], np.int64))
+    parts = comm.allgather(bits.astype(np.int64).reshape(-1))
+    out = []
+    for p, c in zip(parts, counts):
+        ns = int(c[0])
+        if ns == 0:
+            continue
+        b = np.asarray(p, np.int64).astype(np.uint32).reshape(n, -1)
+        out.append(np.unpackbits(b.view(np.uint8), axis=1, bitorder="little")[:, :ns].astype(bool))
+    return np.concatenate(out, axis=1) if out else np.zeros((n, 0), bool)
 
 
 def lane_window(padded: int, num_scored: int, rank: int, size: int):

@@ -108,8 +108,13 @@ class DeviceContext:
             sizes = np.ascontiguousarray(sizes, dtype=np.int32)
             if sizes.shape != labels.shape:
                 raise ValueError(f"sizes shape {sizes.shape} != labels shape {labels.shape}")
-        check(_lib.load().imx_load_labels(self.handle, ptr(labels), ptr(sizes),
-                                          labels.shape[1] if labels.ndim == 2 else self.width))
+        try:
+            check(_lib.load().imx_load_labels(self.handle, ptr(labels), ptr(sizes),
+                                              labels.shape[1] if labels.ndim == 2 else self.width))
+        except ValueError as e:
+            if "label outside" in str(e):     # the reference's numpy gather raises IndexError
+                raise IndexError(str(e)) from None
+            raise
 
     def labels(self, r0: int = 0, r1: int | None = None) -> np.ndarray:
         r1 = self.width if r1 is None else r1

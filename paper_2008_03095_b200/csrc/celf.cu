@@ -603,6 +603,17 @@ static inline bool key_le(int64_t pa, int32_t va, int64_t pb, int32_t vb) {
 
 using namespace imx;
 
+// caller priorities below the memoized gains: the round-based CELF needs
+// every stale priority to bound its vertex's fresh gain
+__global__ void k_check_prio(const int64_t *__restrict__ prio, const int64_t *__restrict__ gains, int64_t n,
+                             unsigned long long *__restrict__ bad) {
+    unsigned long long b = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        b += prio[v] < gains[v];
+    for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, b);
+}
+
 extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
     CTX_CHECK(c);
     if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
@@ -618,6 +629,21 @@ extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
     }
     unsigned long long *maxp = c->scratch + 9;
     IMX_CUDA(cudaMemsetAsync(maxp, 0, sizeof(unsigned long long), c->st));
+    if (prio && c->memo_ready && n) {
+        // the round-based CELF (and its kernel) assume prio >= the fresh
+        // gains; with the memo at hand, refuse caller priorities that are not
+        unsigned long long *bad = c->scratch + 13, nb = 0;
+        IMX_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), c->st));
+        k_check_prio<<<grid_for(n), 256, 0, c->st>>>(dprio, c->gains, n, bad);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+        IMX_CUDA(cudaMemcpyAsync(&nb, bad, sizeof nb, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
+        if (nb) {
+            set_error("CELF priorities below the memoized gains for %llu vertices (they must be upper bounds)", nb);
+            return IMX_EINVAL;
+        }
+    }
     if (n) {
         k_pack_keys<<<grid_for(n), 256, 0, c->st>>>(dprio, n, c->vb, c->oid[1], c->okey[1], maxp);
         IMX_CHECK_LAUNCH();
@@ -893,7 +919,7 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     IMX_CUDA(cudaMemcpyAsync(c->cdev, &h, sizeof h, cudaMemcpyHostToDevice, c->st));
     unsigned long long *gain = c->scratch + 7;
     IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
-    static int grid_cache[2] = {0, 0};
+    int *grid_cache = c->celf_grid;
     const int enc = c->C ? 0 : 1;
     void *fn = enc ? (void *)k_celf_rounds<true> : (void *)k_celf_rounds<false>;
     if (!grid_cache[enc]) {

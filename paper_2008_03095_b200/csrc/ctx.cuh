@@ -87,13 +87,14 @@ struct imx_ctx {
     int32_t *dseeds = nullptr;
     int64_t *dsgains = nullptr;
     int32_t dseeds_cap = 0;
+    int celf_grid[2] = {0, 0};        // cooperative grid of k_celf_rounds<ENC> on this context's device
     // interval-enumeration sampler
     int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;
     int64_t nseg_cap = 0;
     void *scan_tmp = nullptr;
     size_t scan_tmp_bytes = 0;
     // misc
-    unsigned long long *scratch = nullptr;  // [16]; [8..12] = CELF round header
+    unsigned long long *scratch = nullptr;  // [16]: per-call counters (4 label sum, 6 bad labels, 7 commit gain, 9 max prio, 13 bad prio)
     bool labels_ready = false, memo_ready = false, celf_ready = false;
     cudaEvent_t ev[8];
     // phase timings not read back yet: 1 = propagate (ev 0-3), 2 = memo (ev 4-5)

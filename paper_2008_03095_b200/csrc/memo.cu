@@ -155,16 +155,45 @@ __global__ void k_sizes_window(const uint32_t *__restrict__ L, const uint32_t *_
 }
 
 // full histogram of caller labels (component_sizes, propagation.py:349-356)
+// sizes of caller labels: a thread per (32-row chunk, lane), the chunk's rows
+// walked in order with a run-length count per lane, so a run of equal labels
+// (hub components: label 0 in most rows of most lanes) costs one atomic
+// instead of one per cell; loads stay coalesced (consecutive threads,
+// consecutive lanes of the same row)
+constexpr int kHistRows = 32;
 __global__ void k_hist_full(const uint32_t *__restrict__ L, uint32_t *__restrict__ C, int64_t n, int64_t ld,
                             int32_t W, unsigned *__restrict__ bad) {
+    const int64_t chunks = (n + kHistRows - 1) / kHistRows;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks * (int64_t)W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ch = i / W;
+        const int r = (int)(i - ch * W);
+        const int64_t v1 = (ch + 1) * kHistRows < n ? (ch + 1) * kHistRows : n;
+        uint32_t cur = 0, cnt = 0;
+        for (int64_t v = ch * kHistRows; v < v1; ++v) {
+            const uint32_t l = L[v * ld + r];
+            if (l >= (uint32_t)n) { atomicOr(bad, 1u); continue; }
+            if (l != cur && cnt) { atomicAdd(C + (int64_t)cur * ld + r, cnt); cnt = 0; }
+            cur = l;
+            ++cnt;
+        }
+        if (cnt) atomicAdd(C + (int64_t)cur * ld + r, cnt);
+    }
+}
+
+// caller labels with caller sizes: every label in 0..n-1 and every size >= 0
+// (the reference raises IndexError on a bad label, selection.py:63-81)
+__global__ void k_check_loaded(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, int64_t n,
+                               int64_t ld, int32_t W, unsigned *__restrict__ bad) {
+    unsigned b = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / W;
         const int r = (int)(i - v * W);
-        const uint32_t l = L[v * ld + r];
-        if (l >= (uint32_t)n) { atomicOr(bad, 1u); continue; }
-        atomicAdd(C + (int64_t)l * ld + r, 1u);
+        b |= L[v * ld + r] >= (uint32_t)n ? 1u : 0u;
+        b |= (C[v * ld + r] & 0x80000000u) ? 2u : 0u;
     }
+    if (b) atomicOr(bad, b);
 }
 
 // copy rows of a decoded window out through a device staging buffer
@@ -245,15 +274,22 @@ extern "C" int imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t 
         if (sizes) {
             IMX_CUDA(cudaMemcpy2DAsync(c->C, sizeof(uint32_t) * c->ld, sizes, sizeof(int32_t) * ldh,
                                        sizeof(int32_t) * c->W, n, cudaMemcpyHostToDevice, c->st));
+            k_check_loaded<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, bad);
+            IMX_CHECK_LAUNCH();
+            count_launch(c);
         } else {
-            k_hist_full<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, bad);
+            k_hist_full<<<grid_for(ceil_div(n, kHistRows) * c->W), 256, 0, c->st>>>(c->L, c->C, n, c->ld, c->W, bad);
             IMX_CHECK_LAUNCH();
             count_launch(c);
         }
         unsigned hb = 0;
         IMX_CUDA(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, c->st));
         IMX_CUDA(cudaStreamSynchronize(c->st));
-        if (hb) { set_error("label outside 0..n-1"); return IMX_EINVAL; }
+        if (hb) {
+            c->labels_ready = false;
+            set_error(hb & 1u ? "label outside 0..n-1" : "negative component size");
+            return IMX_EINVAL;
+        }
     }
     c->labels_ready = true;
     c->memo_ready = false;

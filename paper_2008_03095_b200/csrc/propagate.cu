@@ -1062,10 +1062,12 @@ int launch_tile_copy(const uint32_t *src, int64_t sld, uint32_t *dst, int64_t dl
 // and root-count atomics of a tile hit L2.  Measured: C5 (n=1M, 8192 lanes)
 // 73 -> 60 ms; C3 / C4 (fewer non-roots per row, or n*128 B >> L2) are
 // slower tiled, so they stay in place.  0 = compress in place.
-static int64_t compress_tile(int64_t n, int64_t ld) {
+static int64_t compress_tile(int64_t n, int64_t ld, bool fuse_memo) {
     if (const char *e = getenv("IMX_COMPRESS_TILE")) {
         const int64_t t = atoll(e);
-        return t > 0 ? std::min<int64_t>(ld, std::max<int64_t>(4, t / 4 * 4)) : 0;
+        // k_gains_tile sums 32 lanes (8 quads) per row: the fused memo caps the tile
+        const int64_t cap = fuse_memo ? std::min<int64_t>(ld, 32) : ld;
+        return t > 0 ? std::min<int64_t>(cap, std::max<int64_t>(4, t / 4 * 4)) : 0;
     }
     if (n > ((int64_t)1 << 20) || (double)n * ld * 4 < 8e9) return 0;
     return 32;
@@ -1074,7 +1076,7 @@ static int64_t compress_tile(int64_t n, int64_t ld) {
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
-    const int64_t tw = compress_tile(n, c->ld);
+    const int64_t tw = compress_tile(n, c->ld, c->fuse_memo && !c->C);
     if (!tw) {
         int k = 0;
         IMX_TRY(launch_compress(c->L, n, c->ld, c->W, nonroot, c->st, &k));

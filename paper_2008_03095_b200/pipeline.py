@@ -128,7 +128,7 @@ def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0
         per_sim = np.concatenate(comm.allgather(ctx.per_sim()))
         selection.state._per_sim = per_sim
         selection.state._ctx = None
-        selection.state._owned_ctx = ctx
+        selection.state._shard = (ctx, comm)
     timings["select"] = time.perf_counter() - t
     timings["total"] = sum(timings.values())
     return FusedRun(g, selection, ctx, table, randoms, timings, comm)

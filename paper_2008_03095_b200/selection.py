@@ -16,6 +16,7 @@ bitmaps, attached on first use.
 from __future__ import annotations
 
 import csv
+import heapq
 from collections.abc import Sequence
 from dataclasses import dataclass
 
@@ -54,6 +55,7 @@ class SeedState:
         self._ctx = ctx
         self._ctx_key = None
         self._per_sim = per_sim
+        self._shard = None        # (ctx, comm): this rank's lane window of a sharded run
 
     @classmethod
     def empty(cls, n: int, num_scored: int) -> "SeedState":
@@ -61,6 +63,9 @@ class SeedState:
 
     @property
     def owned(self) -> np.ndarray:
+        if self._shard is not None:
+            from .celf import gather_owned
+            return gather_owned(*self._shard)
         if self._ctx is not None:
             return self._ctx.owned()
         if self._owned is None:
@@ -71,6 +76,7 @@ class SeedState:
     def owned(self, value):
         self._owned = np.asarray(value, dtype=bool)
         self._ctx = None
+        self._shard = None
 
     def seed_label_sets(self) -> list:
         """Per-simulation sets of owned labels."""
@@ -226,9 +232,44 @@ def select_seeds(g, labels: np.ndarray, sizes: np.ndarray, initial_gains: np.nda
     num_scored = labels.shape[1] if num_scored is None else int(num_scored)
     ctx = DeviceContext(empty_graph(n), np.zeros(labels.shape[1], np.int32), num_scored)
     ctx.load_labels(labels, sizes)
-    ctx.celf_reset(np.asarray(initial_gains, dtype=np.int64))
-    seeds, gains, trace = ctx.celf_select(k)
+    init = np.asarray(initial_gains, dtype=np.int64)
+    if init.shape != (n,):
+        raise ValueError(f"initial_gains shape {init.shape} != ({n},)")
+    memo = ctx.memoize(want_gains=True)
+    if (init < memo).any():
+        # priorities that under-estimate some gain: the round-based CELF
+        # needs upper bounds, so run the reference's lazy heap itself, every
+        # marginal gain and commit still on the device
+        seeds, gains, trace = _lazy_heap(ctx, init, k)
+    else:
+        ctx.celf_reset(init)
+        seeds, gains, trace = ctx.celf_select(k)
     return result_from_context(ctx, seeds, gains, trace, num_scored)
+
+
+def _lazy_heap(ctx: DeviceContext, initial_gains: np.ndarray, k: int):
+    """select_seeds' heap loop (reference selection.py:128-147) with
+    marginal_gain / commit_seed on the device: exact for any priorities."""
+    ctx.celf_reset(None)
+    queue = [(-int(g), v) for v, g in enumerate(initial_gains.tolist())]
+    heapq.heapify(queue)
+    fresh_at = np.zeros(len(initial_gains), dtype=np.int64)
+    seeds, gains, trace = [], [], []
+    while len(seeds) < k:
+        neg, u = heapq.heappop(queue)
+        stale = -neg
+        if fresh_at[u] == len(seeds):
+            ctx.commit(u)
+            trace.append((u, stale, stale, 1, len(seeds)))
+            seeds.append(u)
+            gains.append(stale)
+        else:
+            fresh = int(ctx.eval_gains(np.array([u], np.int32))[0])
+            fresh_at[u] = len(seeds)
+            heapq.heappush(queue, (-fresh, u))
+            trace.append((u, stale, fresh, 0, len(seeds)))
+    return (np.asarray(seeds, np.int32), np.asarray(gains, np.int64),
+            np.asarray(trace, np.int64).reshape(-1, 5))
 
 
 def write_trace_csv(trace: list, path) -> None:

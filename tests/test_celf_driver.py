@@ -36,6 +36,18 @@ class NumpyShard:
         lu = self.L[np.asarray(ids, np.int64)][:, : self.ns]
         return np.where(self.owned[lu, self.cols], 0, self.S[lu, self.cols]).sum(axis=1).astype(np.int64)
 
+    @property
+    def num_scored(self):
+        return self.ns
+
+    def owned_bits(self):
+        """The covered bitmap as DeviceContext.owned_bits returns it."""
+        cw = max(1, (self.ns + 31) // 32)
+        packed = np.packbits(self.owned, axis=1, bitorder="little")
+        out = np.zeros((self.n, 4 * cw), np.uint8)
+        out[:, : packed.shape[1]] = packed
+        return out.view(np.uint32)
+
     def celf_top(self):
         if not self.order:
             return 0, -1
@@ -96,7 +108,7 @@ def _free_port():
 
 def _rank_main(rank, world, port, name, out_dir):
     import torch.distributed as dist
-    from paper_2008_03095_b200.celf import TorchComm, lane_window, select_rounds
+    from paper_2008_03095_b200.celf import TorchComm, gather_owned, lane_window, select_rounds
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -111,8 +123,9 @@ def _rank_main(rank, world, port, name, out_dir):
         shard = NumpyShard(labels, sizes, a, b, R, gains)
         seeds, sg, trace = select_rounds(shard, comm, k, batch0=8)
         per_sim = np.concatenate(comm.allgather(shard.per_sim))
+        owned = gather_owned(shard, comm)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), seeds=seeds, sg=sg, trace=trace,
-                 gains=gains, per_sim=per_sim)
+                 gains=gains, per_sim=per_sim, owned=owned)
     finally:
         dist.destroy_process_group()
 
@@ -131,3 +144,8 @@ def test_two_rank_gloo_driver_matches_single_rank(tmp_path, name):
         assert got["sg"].tolist() == z["seed_gains"].tolist()
         assert np.array_equal(got["trace"], z["trace"])
         assert float(got["per_sim"].std(ddof=1) / np.sqrt(R)) == pytest.approx(float(z["spread_se"]))
+        # SeedState.owned of a sharded run: every rank sees all lanes
+        want = np.zeros((labels.shape[0], R), bool)
+        for u in z["seeds"].tolist():
+            want[labels[u, :R], np.arange(R)] = True
+        assert np.array_equal(got["owned"], want)

@@ -1,0 +1,113 @@
+"""Input guards on the caller-array entry points (GPU).
+
+The reference indexes numpy arrays with caller labels (IndexError on a bad
+label, selection.py:63-81) and runs a lazy heap that is exact for ANY
+priorities (selection.py:128-147).  The device path must neither read nor
+write out of bounds on bad labels, nor go wrong on priorities that are not
+upper bounds of the gains.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(gpu, n, width, ns=None):
+    from paper_2008_03095_b200.context import DeviceContext, empty_graph
+    return DeviceContext(empty_graph(n), np.zeros(width, np.int32), width if ns is None else ns)
+
+
+@pytest.mark.parametrize("bad", [-1, 10, 1 << 30])
+@pytest.mark.parametrize("with_sizes", [False, True])
+def test_load_labels_rejects_out_of_range_labels(gpu, bad, with_sizes):
+    labels = np.tile(np.arange(10, dtype=np.int32)[:, None], (1, 8))
+    labels[3, 5] = bad
+    sizes = np.ones_like(labels) if with_sizes else None
+    ctx = _ctx(gpu, 10, 8)
+    with pytest.raises(IndexError):
+        ctx.load_labels(labels, sizes)
+    with pytest.raises(ValueError):        # nothing usable was loaded
+        ctx.memoize()
+
+
+def test_load_labels_rejects_negative_sizes(gpu):
+    labels = np.tile(np.arange(10, dtype=np.int32)[:, None], (1, 8))
+    sizes = np.ones_like(labels)
+    sizes[2, 1] = -4
+    with pytest.raises(ValueError, match="negative"):
+        _ctx(gpu, 10, 8).load_labels(labels, sizes)
+
+
+def test_caller_labels_hub_histogram(gpu, orc):
+    """k_hist_full's run-length aggregation: long runs of one label (a hub
+    component) and ragged row counts give the oracle's sizes and gains."""
+    rng = np.random.default_rng(5)
+    n, W = 1000 + 7, 40
+    labels = np.zeros((n, W), np.int32)
+    for r in range(W):
+        comp = rng.integers(0, 3, n)
+        labels[:, r] = np.where(comp == 0, 0, np.arange(n))
+        labels[0, r] = 0
+    ctx = _ctx(gpu, n, W, 37)
+    ctx.load_labels(labels)
+    gains = ctx.memoize()
+    sizes, want = orc.sizes_gains(labels, 37)
+    assert np.array_equal(ctx.sizes(), sizes)
+    assert np.array_equal(gains, want)
+
+
+@pytest.mark.parametrize("name", ["er_mid_300", "er_big_1000", "kat_ties"])
+def test_select_seeds_with_underestimating_priorities(gpu, orc, name):
+    """Caller priorities below the true gains: the reference's heap commits
+    the top stale entry at round 0 and refreshes lazily; the device path must
+    give its exact seeds, gains and trace."""
+    z = load_golden(name)
+    labels, sizes = orc.run_fused(*_graph(orc, z), int(z["k"]), int(z["R"]), int(z["master_seed"]),
+                                  nthreads=4)["labels"], None
+    sizes, gains = orc.sizes_gains(labels, int(z["R"]))
+    rng = np.random.default_rng(1)
+    init = gains - rng.integers(0, np.maximum(gains, 1) + 1)           # some below, some equal
+    init[rng.integers(0, len(init), 5)] += 10 ** 6                    # a few far above
+    n = labels.shape[0]
+    g = gpu.Graph.from_edges(n, z["edges"].astype(np.int64))
+    res = gpu.select_seeds(g, labels, sizes, init, int(z["k"]), int(z["R"]))
+    s, sg, tr, _ = orc.celf(labels, sizes, init, int(z["k"]), int(z["R"]))
+    assert res.seeds == s.tolist()
+    assert res.gains == sg.tolist()
+    assert np.array_equal(res.trace.array, tr)
+
+
+def _graph(orc, z):
+    xadj, adj, _ = orc.csr_from_edges(int(z["n"]), z["edges"].astype(np.int64))
+    w = z["weights"] if "weights" in z else np.full(len(adj), float(str(z["scheme"]).split(":")[1]))
+    return xadj, adj, w
+
+
+def test_celf_reset_refuses_priorities_below_the_memo(gpu, orc):
+    z = load_golden("er_mid_300")
+    labels = z["labels"]
+    ctx = _ctx(gpu, labels.shape[0], labels.shape[1])
+    ctx.load_labels(labels)
+    gains = ctx.memoize()
+    low = gains.copy()
+    low[np.argmax(gains)] -= 1
+    with pytest.raises(ValueError, match="upper bounds"):
+        ctx.celf_reset(low)
+    ctx.celf_reset(gains + 1)              # over-estimates are fine
+
+
+@pytest.mark.parametrize("tile", ["64", "128"])
+def test_wide_compress_tile_with_fused_memo_is_capped(gpu, tile, monkeypatch):
+    """IMX_COMPRESS_TILE above 32 with the memo fused into the tiled
+    compression: the tile is capped at k_gains_tile's 32 lanes, so the gains
+    (and everything after them) stay the reference's."""
+    monkeypatch.setenv("IMX_COMPRESS_TILE", tile)
+    z = load_golden("er_big_1000")
+    from test_gpu_golden import build_graph
+    g = build_graph(gpu, z)
+    run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))
+    assert run.seeds == z["seeds"].tolist()
+    assert np.array_equal(run.selection.trace.array, z["trace"])

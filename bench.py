@@ -1,25 +1,38 @@
 #!/usr/bin/env python
 """Benchmark of the fused sample + CC hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
+                    [--scaling strong|weak] [--impl ours|reference] [--parity full|off]
+
+Workload: config 4 by default (R-MAT scale 22, 4.19M vertices, ~64M edges,
+p=0.005, R=1024, K=100) -- the largest BASELINE config; C5 is the other
+single-GPU one (--config c5).
 
 Metric: fused sample+CC edge-sims/s.  One converged sample + CC of all R
 simulations counts 2m*R edge-sims (2m directed slots, R lanes) -- the work of
 one full sweep of the dense model.  `value` is that
 rate with the CSR and X resident in HBM (device-timed with CUDA events on the
-library's stream, L2 flushed by a 256 MB write before every step);
-`e2e` is the same rate measured through the public API
-(`run_fused(g, K, R)` on a host Graph: CSR upload, hash, propagate, memo,
-CELF for K seeds, results back to the host), and `k_seed_wall_s` is that
-step's wall time (BASELINE's second metric).  `cpu_baseline` is the CPU
-oracle (oracle/, a C/OpenMP restatement of the reference's dense label
-propagation + CELF) timed on this host in the same run.
+library's stream; the label matrix (17 GB at C4) is far larger than L2 and a
+256 MB write flushes L2 before every step anyway); `e2e` is the same rate
+measured through the public API (`run_fused(g, K, R)` on a host Graph in
+pinned memory: CSR upload, hash, propagate, memo, CELF for K seeds, seeds /
+gains / trace back to the host), and `k_seed_wall_s` is that step's wall time
+(BASELINE's second metric).  `parity` compares the last e2e run with the CPU
+oracle on every lane (oracle/scale_check.py, outside every timed region).
+`cpu_baseline` is the CPU oracle (oracle/, a C/OpenMP restatement of the
+reference's dense label propagation + CELF) timed on this host in the same run.
 
-With --gpus N > 1 (torchrun) every GPU simulates the config's R lanes (weak
-scaling: one simulation of R*N lanes sharded into N lane windows, no data-path
-collective in propagate); value = all ranks' edge-sims / max-over-ranks time.
-The e2e run selects seeds over all R*N simulations (int64 allreduces of the
-partial gains, celf.select_rounds).
+Roofline: `frac` = the propagate's DRAM bytes (ncu, profiles/
+ncu_<cfg>_summary.json, stamped with the library's source hash and refused
+when stale) / its live device time / the measured HBM peak.
+
+With --gpus N > 1 (torchrun) the config's R simulations are sharded into N
+lane windows (--scaling strong, the default: R/N lanes per GPU, as
+north_star's "each GPU holds the full CSR and R/N simulations") or every GPU
+simulates R lanes (--scaling weak: one simulation of R*N lanes); there is no
+data-path collective in propagate; value = all ranks' edge-sims /
+max-over-ranks time.  The e2e run selects seeds over all simulations (int64
+allreduces of the gains and CELF partial sums).
 """
 
 from __future__ import annotations
@@ -43,7 +56,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--parity", default="full", choices=["full", "off"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -193,11 +208,8 @@ def cpu_baseline(cfg, g_host, R, K, budget_s):
     import oracle
     oracle.build()
     threads = os.cpu_count() or 1
-    xadj, adj, w = g_host.xadj, g_host.adj, g_host.weights
-    hashes = oracle.hash_table(xadj, adj)
-    thr = oracle.thresholds(w, oracle.reciprocal(xadj, adj))
-    uniform = bool((thr == thr[0]).all())
-    t_arg = int(thr[0]) if uniform else thr
+    from oracle.scale_check import host_sampler_inputs
+    xadj, adj, hashes, t_arg = host_sampler_inputs(g_host)
     X = oracle.randoms(R, 0)
     # size the lane sample to the budget: probe 8 lanes first
     t0 = time.perf_counter()
@@ -218,41 +230,50 @@ def cpu_baseline(cfg, g_host, R, K, budget_s):
     return out
 
 
+METRIC = "fused sample+CC edge-sims/sec (2m*R per converged sample+CC)"
+
+
+def job_lanes(R, world, scaling):
+    """(total simulations, lanes per GPU) of the job."""
+    if scaling == "weak":
+        return R * world, R
+    return R, -(-R // world)
+
+
+def config_dict(c, n, m2, world, scaling):
+    """The workload description -- identical for both arms."""
+    R_total, per_gpu = job_lanes(c.R, world, scaling)
+    return {"workload": c.description, "n": int(n), "m2": int(m2), "R": int(R_total), "K": c.K,
+            "lanes_per_gpu": int(per_gpu),
+            "l2": "label matrix >> L2; a 256 MB write flushes L2 before every timed step",
+            "parallelism": f"R-sharded x{world} ({scaling}: {per_gpu} lanes per GPU)"}
+
+
 def run_reference(args, world, rank):
-    """--impl reference: the CPU oracle (the reference path restated in C)
-    on the host cores, same config/metric; rank 0 only."""
+    """--impl reference: the CPU oracle (the reference path restated in C;
+    the reference itself is pure Python and cannot run C4/C5 in minutes) on
+    the host cores, same config/metric; rank 0 only.  Each step is a bounded
+    lane chunk of the workload (propagate + sizes/gains + CELF of that
+    chunk): the line is labelled "chunked"."""
     if rank != 0:
         return
     import oracle
     from paper_2008_03095_b200 import configs
     oracle.build()
     c = configs.CONFIGS[args.config]
-    edges = configs.edges(args.config)
-    from paper_2008_03095_b200.weights import parse_weight_scheme
-    xadj, adj, _ = oracle.csr_from_edges(c.n, edges)
-    scheme = parse_weight_scheme(c.weights)
-    if hasattr(scheme, "p"):
-        w = np.full(len(adj), scheme.p)
-    else:  # per-edge normal draws in canonical-slot order (graph.py:251-259)
-        src = oracle.sources(xadj)
-        canon = np.flatnonzero(src < adj)
-        rec = oracle.reciprocal(xadj, adj)
-        draws = np.clip(np.random.default_rng(c.seed).normal(scheme.mean, scheme.std,
-                                                              size=len(canon)), 0, 1)
-        w = np.empty(len(adj))
-        w[canon] = draws
-        w[rec[canon]] = draws
+    from oracle.scale_check import config_host_graph
+    xadj, adj, w = config_host_graph(args.config)
     threads = os.cpu_count() or 1
     hashes = oracle.hash_table(xadj, adj)
-    thr = oracle.thresholds(w, oracle.reciprocal(xadj, adj))
-    uniform = bool((thr == thr[0]).all())
-    t_arg = int(thr[0]) if uniform else thr
-    X = oracle.randoms(c.R, 0)
+    uniform = bool((w == w[0]).all())
+    t_arg = int(oracle.thresholds(w[:1])[0]) if uniform else oracle.thresholds(w, oracle.reciprocal(xadj, adj))
+    R_total, _ = job_lanes(c.R, world, args.scaling)
+    X = oracle.randoms(R_total, 0)
     t0 = time.perf_counter()
     oracle.propagate(xadj, adj, hashes, t_arg, X[:8], threads)
     per_lane = max((time.perf_counter() - t0) / 8, 1e-6)
     per_step = max(1.0, 150.0 / max(1, args.steps + args.warmup))
-    lanes = int(min(c.R, max(8, (per_step / per_lane) // 8 * 8)))
+    lanes = int(min(R_total, max(8, (per_step / per_lane) // 8 * 8)))
     Xs = X[:lanes]
     prop, tot = [], []
     for i in range(args.warmup + args.steps):
@@ -267,25 +288,45 @@ def run_reference(args, world, rank):
             tot.append(t2 - t0)
     units = len(adj) * lanes
     value = units / float(np.mean(prop))
-    sample = (f"{args.config} lanes 0..{lanes} of {c.R} per step (oracle: dense min-label "
-              f"propagation to fixpoint in {sweeps} sweeps + sizes/gains + CELF heap, "
-              f"{threads} OpenMP threads)")
+    chunked = lanes < R_total
+    sample = (f"{args.config} lanes 0..{lanes} of {R_total} per step{' (chunked)' if chunked else ''}: "
+              f"oracle dense min-label propagation to fixpoint in {sweeps} sweeps + sizes/gains + CELF "
+              f"heap of that chunk, {threads} OpenMP threads")
     line = {
-        "impl": "reference", "metric": "fused sample+CC edge-sims/sec (2m*R per converged sample+CC)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "edge-sims/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(prop)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic",
-        "config": {"workload": c.description, "n": c.n, "m2": int(len(adj)), "R": c.R,
-                   "K": c.K, "lanes_per_step": lanes},
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded generator, graph_seed=weight_seed=config#, master_seed=0)",
+        "config": config_dict(c, c.n, len(adj), world, args.scaling),
+        "chunked": chunked, "lanes_per_step": lanes,
         "cpu_baseline": {"value": value, "unit": "edge-sims/s", "cores": threads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": units / float(np.mean(tot)), "unit": "edge-sims/s",
                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                "k_seed_wall_s": float(np.mean(tot)) * c.R / lanes},
+                "k_seed_wall_s": (float(np.mean(tot)) * R_total / lanes) if chunked else float(np.mean(tot)),
+                "k_seed_wall_note": ("propagate+memo+CELF of a lane chunk scaled linearly to R (CELF "
+                                     "refresh counts are not linear in R: indicative only)") if chunked
+                                    else "full K-seed run"},
         "sweeps": int(sweeps),
     }
     print(json.dumps(line), flush=True)
+
+
+def traffic_at_head(cfg, W, R):
+    """The propagate's ncu DRAM bytes (profiles/ncu_<cfg>_summary.json) if it
+    was captured from this very library build at this width; else None and
+    the reason."""
+    from paper_2008_03095_b200.build import source_hash
+    prof = ROOT / "profiles" / f"ncu_{cfg}_summary.json"
+    if not prof.exists():
+        return None, "no ncu summary"
+    summ = json.loads(prof.read_text())
+    if W != R:
+        return None, f"ncu summary is for {R} lanes, this run has {W} per GPU"
+    if summ.get("src_hash") != source_hash():
+        return None, f"ncu summary stale (src {summ.get('src_hash')} != {source_hash()})"
+    return summ, None
 
 
 def run_ours(args, world, rank, local):
@@ -298,10 +339,8 @@ def run_ours(args, world, rank, local):
     t0 = time.perf_counter()
     g = configs.build(args.config)          # generated + CSR-built on the device
     t_build = time.perf_counter() - t0
-    n, m2, R, K = g.n, g.m, c.R, c.K
-    # weak scaling: every GPU simulates the config's R lanes; the job is one
-    # simulation of R * N lanes sharded by lane windows (no data-path collective)
-    R_total = R * world
+    n, m2, K = g.n, g.m, c.K
+    R_total, _ = job_lanes(c.R, world, args.scaling)
     X = imx.SimulationRandoms(R_total, 0).values
     a, b, scored = lane_window(len(X), R_total, rank, world)
     W = b - a
@@ -326,19 +365,37 @@ def run_ours(args, world, rank, local):
     per_gpu = m2 * W / (res["total_ms"] / 1e3)
     peak, peak_src = peaks()
     bes = b_es(n, m2, W, per_edge)
-    achieved = per_gpu * bes / 1e9
     kern = {k: res[k] for k in ("init_ms", "hook_ms", "compress_ms")}
     dominant = max(kern, key=kern.get)
-    prof = ROOT / "profiles" / f"ncu_{args.config}_summary.json"
-    traffic, rand = None, None
-    if prof.exists() and W == R:
-        try:
-            summ = json.loads(prof.read_text())
-            traffic = summ.get("dram_bytes_per_propagate")
-            rand = random_access(summ, n * ((W + 3) // 4 * 4) * 4,
-                                 (res["hook_ms"] + res["compress_ms"]) / 1e3)
-        except Exception:
-            traffic, rand = None, None
+    summ, stale = traffic_at_head(args.config, W, c.R)
+    roof = {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+            "traffic": None, "peak_source": peak_src,
+            "kernel": "propagate = init + sample/hook + compress kernels (one converged sample+CC)",
+            "kernel_ms": kern, "dominant_phase": dominant,
+            "model": {"B_es": bes, "note": "dense fused-sweep model of SURVEY 8(d): bytes a dense "
+                      "min-label sweep would move; the union-find path moves fewer (it never reads "
+                      "dead (edge, lane) pairs), so this ratio is not a roofline fraction",
+                      "model_gbs": per_gpu * bes / 1e9, "model_frac": per_gpu * bes / 1e9 / peak}}
+    if summ is not None:
+        traffic = float(summ["dram_bytes_per_propagate"])
+        achieved = traffic / (res["total_ms"] / 1e3) / 1e9
+        roof.update({"achieved": achieved, "frac": achieved / peak, "traffic": traffic,
+                     "traffic_src_hash": summ["src_hash"],
+                     "traffic_source": "ncu dram__bytes_read+write of one propagate at this source hash "
+                                       "(profiles/ncu_%s_summary.json); time = live CUDA events" % args.config,
+                     "bytes_per_edge_sim": traffic / (m2 * W),
+                     "random_access": random_access(summ, n * ((W + 3) // 4 * 4) * 4,
+                                                    (res["hook_ms"] + res["compress_ms"]) / 1e3)})
+        phases = {}
+        for ph, keys in (("init_ms", ("k_init", "k_pull<1")), ("hook_ms", ("k_seg", "cub::", "k_hook", "k_pull<2")),
+                         ("compress_ms", ("k_compress", "k_tile_copy", "k_gains_tile"))):
+            bts = sum(v["dram_read_B"] + v["dram_write_B"] for k, v in summ["kernels"].items()
+                      if k.startswith(keys))
+            phases[ph] = {"ms": res[ph], "dram_bytes": bts,
+                          "frac": bts / (res[ph] / 1e3) / 1e9 / peak if res[ph] > 0 else None}
+        roof["phases"] = phases
+    else:
+        roof["traffic_note"] = stale
 
     # ---- correctness guard on the measured context ----
     ctx.propagate(verify=True)
@@ -348,9 +405,10 @@ def run_ours(args, world, rank, local):
     # would keep its graph) ----
     host = imx.Graph(pinned(g.xadj), pinned(g.adj), pinned(g.weights), g.orig_ids)
     e2e_steps = args.e2e_steps or args.steps
-    times, d2h = [], 0
+    times, d2h, run = [], 0, None
     for i in range(args.warmup + e2e_steps):
         gi = imx.Graph(host.xadj, host.adj, host.weights, host.orig_ids)
+        run = None
         barrier(world)
         t0 = time.perf_counter()
         run = imx.run_fused(gi, K, num_simulations=R_total, master_seed=0)
@@ -359,38 +417,34 @@ def run_ours(args, world, rank, local):
         if i >= args.warmup:
             times.append(allreduce_max(dt, world))
             d2h = 4 * K + 8 * K + 40 * len(run.selection.trace)
-        del run
     e2e_s = float(np.mean(times))
     h2d = 8 * (n + 1) + 4 * m2 + 8 * m2 + 4 * len(X)
 
-    traffic_frac = None
-    if traffic:
-        traffic_frac = traffic / (res["total_ms"] / 1e3) / 1e9 / peak
     line = {
-        "metric": "fused sample+CC edge-sims/sec (2m*R per converged sample+CC)",
+        "metric": METRIC,
         "value": value, "unit": "edge-sims/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded generator, graph_seed=weight_seed=config#, master_seed=0)",
-        "config": {"workload": c.description, "n": n, "m2": m2, "R": R_total, "K": K,
-                   "lanes_per_gpu": W, "l2": "flushed (256 MB write) before every step",
-                   "parallelism": f"R-sharded x{world} (weak: {R} lanes per GPU)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "traffic_frac": traffic_frac,
-                     "kernel": "propagate = k_init + k_hook + k_compress (one converged sample+CC)",
-                     "model": f"B_es={bes:.3f} B/edge-sim dense-sweep model (SURVEY 8(d)) x 2m*R_gpu",
-                     "peak_source": peak_src, "dominant_kernel": dominant,
-                     "kernel_ms": kern, "random_access": rand},
+        "config": config_dict(c, n, m2, world, args.scaling),
+        "roofline": roof,
         "e2e": {"value": units_total / e2e_s, "unit": "edge-sims/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "k_seed_wall_s": e2e_s, "seeds_head": seeds[:5], "spread": spread},
+                "k_seed_wall_s": e2e_s, "seeds_head": seeds[:5], "spread": spread,
+                "timings_last": {k: round(v, 5) for k, v in run.timings.items()}},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "graph_build_s": t_build,
     }
+    if rank == 0 and world == 1 and args.parity == "full":
+        from oracle.scale_check import check_fused_run
+        try:
+            line["parity"] = check_fused_run(run, gi, K, R_total, 0)
+        except Exception as e:            # noqa: BLE001 -- reported, never fatal to the bench
+            line["parity"] = {"ok": False, "error": repr(e)}
+    del run
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, host, R, K, args.cpu_budget_s)
+        line["cpu_baseline"] = cpu_baseline(args.config, host, c.R, K, args.cpu_budget_s)
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -392,6 +392,87 @@ int64_t oracle_celf_fresh(int64_t n, int32_t k, const int64_t *F, int32_t *seeds
 }
 
 /* ------------------------------------------------------------------------
+ * Config graphs on the host at C4 scale (the CPU reference arm's setup and
+ * the tests' host CSR): the repo's counter-based generator
+ * (paper_2008_03095_b200/generators.py, restated here in C) and
+ * Graph.from_edges (graph.py:124-155) for a sorted unique edge-key list.
+ * ------------------------------------------------------------------------ */
+static inline uint64_t g_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static inline double g_unit(uint64_t r) { return (double)(r >> 11) * (1.0 / 9007199254740992.0); }
+static inline uint64_t g_below(uint64_t r, uint64_t n) {
+    return ((r >> 32) * n + (((r & 0xFFFFFFFFull) * n) >> 32)) >> 32;
+}
+
+/* candidate keys lo * n + hi (UINT64_MAX for self-loops) of draws
+ * [first, first + count): kind 0 ER, 1 R-MAT (probs a, b, c, d), 2 Chung-Lu
+ * (cdf[n]) -- generators.py _candidates */
+void oracle_gen_candidates(int kind, int64_t n, uint64_t seed, int64_t first, int64_t count,
+                           const double *probs, const double *cdf, uint64_t *out, int nthreads) {
+    const uint64_t ms = g_mix64(seed), nn = (uint64_t)n;
+    int scale = 0;
+    while ((2ll << scale) <= n) ++scale;
+    double ca = 0, cb = 0, cc = 0;
+    if (kind == 1) {
+        const double tot = probs[0] + probs[1] + probs[2] + probs[3];
+        ca = probs[0] / tot; cb = (probs[0] + probs[1]) / tot; cc = (probs[0] + probs[1] + probs[2]) / tot;
+    }
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t j = 0; j < count; ++j) {
+        const uint64_t i = (uint64_t)(first + j);
+        uint64_t u = 0, v = 0;
+        if (kind == 0) {
+            u = g_below(g_mix64(ms ^ (2 * i)), nn);
+            v = g_below(g_mix64(ms ^ (2 * i + 1)), nn);
+        } else if (kind == 1) {
+            for (int l = 0; l < scale; ++l) {
+                const double x = g_unit(g_mix64(ms ^ (64 * i + (uint64_t)l)));
+                const uint64_t down = x >= cb, right = (x >= ca && x < cb) || x >= cc;
+                u = (u << 1) | down;
+                v = (v << 1) | right;
+            }
+        } else {
+            const double x1 = g_unit(g_mix64(ms ^ (2 * i))), x2 = g_unit(g_mix64(ms ^ (2 * i + 1)));
+            int64_t lo = 0, hi = n;                    /* searchsorted(cdf, x, 'right') */
+            while (lo < hi) { int64_t m = (lo + hi) >> 1; if (cdf[m] <= x1) lo = m + 1; else hi = m; }
+            u = (uint64_t)(lo < n - 1 ? lo : n - 1);
+            lo = 0; hi = n;
+            while (lo < hi) { int64_t m = (lo + hi) >> 1; if (cdf[m] <= x2) lo = m + 1; else hi = m; }
+            v = (uint64_t)(lo < n - 1 ? lo : n - 1);
+        }
+        out[j] = u == v ? UINT64_MAX : (u < v ? u : v) * nn + (u < v ? v : u);
+    }
+}
+
+/* Graph.from_edges (graph.py:124-155) of m unique undirected edges given as
+ * keys lo * n + hi in ascending order: rows sorted by (src, dst).  In key
+ * order every edge (l, v) with l < v precedes every edge (v, h), so one pass
+ * appending to per-row cursors writes each row already sorted. */
+void oracle_csr_from_sorted_keys(int64_t n, int64_t m, const uint64_t *keys, int64_t *xadj, int32_t *adj) {
+    memset(xadj, 0, sizeof(int64_t) * (size_t)(n + 1));
+    for (int64_t e = 0; e < m; ++e) {
+        ++xadj[keys[e] / (uint64_t)n + 1];
+        ++xadj[keys[e] % (uint64_t)n + 1];
+    }
+    for (int64_t v = 0; v < n; ++v) xadj[v + 1] += xadj[v];
+    int64_t *cur = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    memcpy(cur, xadj, sizeof(int64_t) * (size_t)n);
+    for (int64_t e = 0; e < m; ++e) {
+        const int64_t lo = (int64_t)(keys[e] / (uint64_t)n), hi = (int64_t)(keys[e] % (uint64_t)n);
+        adj[cur[lo]++] = (int32_t)hi;
+        adj[cur[hi]++] = (int32_t)lo;
+    }
+    free(cur);
+}
+
+/* ------------------------------------------------------------------------
  * evaluate_seeds worker (evaluation.py:70-98, 101-136): world j of chunk c
  * draws E doubles from numpy PCG64 stream c (state/inc given by the caller,
  * taken from default_rng(SeedSequence(seed).spawn(..)[c])), starting at

@@ -29,6 +29,31 @@ import numpy as np
 import oracle
 
 
+def config_host_graph(cfg):
+    """(xadj, adj, weights) of a BASELINE config built on the host only --
+    the repo's config generator restated in C (oracle.config_csr) and the
+    config's weight scheme as apply_weights draws it (per-edge schemes: one
+    draw per canonical slot in slot order, graph.py:251-259)."""
+    from paper_2008_03095_b200 import configs
+    from paper_2008_03095_b200.weights import parse_weight_scheme
+    c = configs.CONFIGS[cfg]
+    kind, n, m, draws, probs, cdf = configs._spec(cfg)
+    xadj, adj = oracle.config_csr(kind, n, m, c.seed, draws, probs, cdf)
+    scheme = parse_weight_scheme(c.weights)
+    if hasattr(scheme, "p"):
+        w = np.full(len(adj), float(scheme.p))
+    else:
+        src = oracle.sources(xadj)
+        canon = np.flatnonzero(src < adj)
+        rec = oracle.reciprocal(xadj, adj)
+        draws = np.clip(np.random.default_rng(c.seed).normal(scheme.mean, scheme.std,
+                                                              size=len(canon)), 0, 1)
+        w = np.empty(len(adj))
+        w[canon] = draws
+        w[rec[canon]] = draws
+    return xadj, adj, w
+
+
 def host_sampler_inputs(g):
     """(xadj, adj, hashes, thr) of a Graph on the host; thr is an int when
     every slot has the same threshold (uniform schemes)."""

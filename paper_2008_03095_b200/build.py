@@ -20,6 +20,18 @@ NVCC_FLAGS = [
 ]
 
 
+def source_hash() -> str:
+    """sha256 (16 hex) over the library's sources, headers and flags: stamps
+    the ncu summaries under profiles/ so bench.py can refuse a stale one
+    (the GPU box has no git history)."""
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for p in sorted(SOURCES + HEADERS, key=lambda q: q.name):
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()[:16]
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (Path(cand).exists() or cand == "nvcc"):

@@ -101,9 +101,14 @@ def edges(kind: int, n: int, m: int, seed: int, draws: int = 0, probs=None, cdf=
     while True:
         keys = np.concatenate([_candidates(kind, n, seed, s, min(chunk, draws - s), probs, cdf)
                                for s in range(0, draws, chunk)])
-        uniq, first = np.unique(keys, return_index=True)
-        ok = uniq != _M64
-        uniq, first = uniq[ok], first[ok]
+        # first draw of every distinct key (np.unique(return_index) without
+        # its slow generic path on tens of millions of uint64 keys)
+        order = np.argsort(keys, kind="stable")
+        srt = keys[order]
+        head = np.ones(len(srt), bool)
+        head[1:] = srt[1:] != srt[:-1]
+        head &= srt != _M64
+        uniq, first = srt[head], order[head]
         if m == 0 or len(uniq) >= m:
             break
         draws = min(draws + draws // 2, 1 << 31)

@@ -194,3 +194,20 @@ def test_oracle_selection_check_flags_a_wrong_seed(orc):
     out = chk.result()
     assert out["seeds"][:3].tolist() == z["seeds"][:3].tolist()
     assert out["seeds"].tolist() != claimed.tolist()
+
+
+@pytest.mark.parametrize("kind,n,m,draws,extra", [
+    (0, 1000, 3000, 0, {}),
+    (1, 1 << 12, 0, 16 << 12, {"probs": (0.57, 0.19, 0.19, 0.05)}),
+    (1, 1 << 11, 5000, 0, {"probs": (0.45, 0.22, 0.22, 0.11)}),
+    (2, 3000, 8000, 0, {"gamma": 2.5}),
+])
+def test_oracle_config_csr_equals_numpy_generator(orc, kind, n, m, draws, extra):
+    """The C restatement of the config generator + sorted-key CSR equals the
+    numpy generator (generators.edges) + Graph.from_edges restatement."""
+    from paper_2008_03095_b200 import generators as gen
+    cdf = gen.chung_lu_cdf(n, extra["gamma"]) if "gamma" in extra else None
+    probs = extra.get("probs")
+    xadj, adj = orc.config_csr(kind, n, m, 11, draws, probs, cdf)
+    wx, wa, _ = orc.csr_from_edges(n, gen.edges(kind, n, m, 11, draws, probs, cdf))
+    assert np.array_equal(xadj, wx) and np.array_equal(adj, wa)

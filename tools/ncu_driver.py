@@ -17,4 +17,6 @@ ctx = DeviceContext(g, X, R)
 ctx.propagate()          # one-time per-graph setup (sampler index, heavy-row slices) outside the window
 res = ctx.bench_propagate(reps, flush_l2=True)
 ctx.memoize(want_gains=False)
+from paper_2008_03095_b200.build import source_hash
 print(cfg, res)
+print(f"src_hash={source_hash()}")

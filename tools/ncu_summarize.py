@@ -58,8 +58,15 @@ for k in one:
 rd, wr = tot("dram__bytes_read.sum"), tot("dram__bytes_write.sum")
 l2 = tot(S + "read.sum") + tot(S + "atom.sum") + tot(S + "red.sum") + tot(S + "write.sum")
 t_us = tot("gpu__time_duration.sum") / 1e3
+sys.path.insert(0, str(ROOT))
+from paper_2008_03095_b200.build import source_hash  # noqa: E402
+
+log = src.with_suffix(".log")
+stamp = next((l.split("=", 1)[1].strip() for l in (log.read_text().splitlines() if log.exists() else [])
+              if l.startswith("src_hash=")), None) or source_hash()
 summary = {
     "config": cfg,
+    "src_hash": stamp,
     "source": f"ncu --replay-mode application (tools/ncu_configs.sh), kernels of one propagate after an L2 flush; "
               f"serialised, cold-cache launch times",
     "dram_bytes_per_propagate": rd + wr,

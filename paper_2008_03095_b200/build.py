@@ -8,7 +8,7 @@ import sys
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-SOURCES = [PKG / "csrc" / f for f in ("graph.cu", "gen.cu", "ctx.cu", "propagate.cu", "memo.cu", "celf.cu", "evaluation.cu", "upload.cu", "io.cpp")]
+SOURCES = [PKG / "csrc" / f for f in ("graph.cu", "gen.cu", "ctx.cu", "propagate.cu", "scan.cu", "memo.cu", "celf.cu", "evaluation.cu", "upload.cu", "io.cpp")]
 HEADERS = list((PKG / "csrc").glob("*.cuh")) + [PKG.parent / "include" / "infuser_b200.h"]
 OUT = PKG / "lib" / "libinfuser_b200.so"
 

@@ -75,6 +75,7 @@ void ctx_free(imx_ctx *c) {
     void *ptrs[] = {c->X, c->L, c->C, c->gains, c->inS, c->cov, c->per_sim, c->oid[0], c->oid[1],
                     c->okey[0], c->okey[1], c->scratch, c->eval_out, c->d_one,
                     c->sort_tmp, c->d_ids, c->d_vals, c->seg_a, c->seg_n, c->seg_off, c->scan_tmp,
+                    c->scan_xs, c->scan_perm, c->scan_boff, c->scan_ctr,
                     c->cdev, c->skey, c->sid, c->dtrace, c->dseeds, c->dsgains};
     for (void *p : ptrs) if (p) cudaFreeAsync(p, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
@@ -168,6 +169,7 @@ extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t
     }
     std::vector<int32_t> xpad(c->ld, 0);
     std::copy(X, X + width, xpad.begin());
+    c->hX.assign(X, X + width);
     if ((e = cudaMemcpyAsync(c->X, xpad.data(), sizeof(int32_t) * c->ld, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
         (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
         return fail(cuda_fail(e, "upload X", __FILE__, __LINE__));

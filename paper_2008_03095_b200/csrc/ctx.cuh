@@ -93,6 +93,14 @@ struct imx_ctx {
     int64_t nseg_cap = 0;
     void *scan_tmp = nullptr;
     size_t scan_tmp_bytes = 0;
+    // scan sampler (scan.cu): lanes of every chunk of scan_cw lanes sorted by
+    // X >> scan_kb; scan_boff = bucket offsets per chunk
+    std::vector<int32_t> hX;          // the context's words on the host
+    int32_t *scan_xs = nullptr;
+    uint16_t *scan_perm = nullptr;
+    int32_t *scan_boff = nullptr;
+    unsigned long long *scan_ctr = nullptr;   // [scan_nchunks] work counters of one launch
+    int scan_kb = -1, scan_nb = 0, scan_cw = 0, scan_nchunks = 0;
     // misc
     unsigned long long *scratch = nullptr;  // [16]: per-call counters (4 label sum, 6 bad labels, 7 commit gain, 9 max prio, 13 bad prio)
     bool labels_ready = false, memo_ready = false, celf_ready = false;
@@ -141,6 +149,11 @@ void pinned_put(void *p, size_t bytes);
 void pinned_lend(void *p, size_t bytes);   // handed to the caller; imx_host_free returns it
 int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);
+// heavy-row slices of the graph for slice length T, cached on the graph (propagate.cu)
+int ensure_heavy(imx_ctx *c, int pass, int T);
+// the scan sampler (scan.cu)
+bool scan_eligible(const imx_graph *g);
+int run_scan(imx_ctx *c, int pass, unsigned long long *hooks);
 // raw label-matrix passes shared with the evaluation worlds (evaluation.cu)
 int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
 // 16-byte quads of rows [0, n) from one row layout to another (row strides

@@ -848,7 +848,7 @@ static int pull_heavy_T(const imx_graph *g) {
 }
 
 // the heavy-row slices of the graph for slice length T, cached on the graph
-static int ensure_heavy(imx_ctx *c, int pass, int T) {
+int ensure_heavy(imx_ctx *c, int pass, int T) {
     imx_graph *g = c->g;
     auto &H = g->hv[pass - 1];
     if (H.T == T) return IMX_OK;
@@ -948,15 +948,20 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
 // dense membership scans (ALU only) plus random accesses for the non-forest
 // live edges only, but a warp owns a whole row prefix, so a very long prefix
 // (a high-degree vertex with many smaller neighbours) serialises.
-enum { HOOK_ENUM = 0, HOOK_PULL = 1, HOOK_DENSE = 2, HOOK_HYBRID = 3 };
+enum { HOOK_ENUM = 0, HOOK_PULL = 1, HOOK_DENSE = 2, HOOK_HYBRID = 3, HOOK_SCAN = 4 };
 static int hook_mode(const imx_graph *g, int32_t W) {
     const char *m = getenv("IMX_HOOK");
     if (m && !strcmp(m, "dense")) return HOOK_DENSE;
-    // enumeration assumes 31-bit hashes ((x ^ h) >= 0); the scans test exactly
+    // enumeration and the lane buckets assume 31-bit hashes ((x ^ h) >= 0);
+    // the pull scans test exactly
     if (g->hash_neg) return HOOK_PULL;
     if (m && !strcmp(m, "enum")) return HOOK_ENUM;
     if (m && !strcmp(m, "pull")) return HOOK_PULL;
     if (m && !strcmp(m, "hybrid")) return HOOK_HYBRID;
+    if (m && !strcmp(m, "scan")) return scan_eligible(g) ? HOOK_SCAN : HOOK_PULL;
+    // uniform thresholds: the bucketed pull forest (scan.cu), except for
+    // small dense work, where the plain pull passes win (C1: 0.039 vs 0.067 ms)
+    if (scan_eligible(g) && (double)g->me * (double)W > 3.2e7) return HOOK_SCAN;
     const char *t = getenv("IMX_PULL_MIN_P");
     const double pmin = t ? atof(t) : 0.02;
     // long prefixes are split into slices (heavy rows), so they only
@@ -973,7 +978,11 @@ static int hook_mode(const imx_graph *g, int32_t W) {
 static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_init, cudaEvent_t e_hook) {
     imx_graph *g = c->g;
     const int mode = g->me ? hook_mode(g, c->W) : HOOK_ENUM;
-    if (mode == HOOK_PULL || mode == HOOK_HYBRID) {
+    if (mode == HOOK_SCAN) {
+        IMX_TRY(run_scan(c, 1, nullptr));
+        if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));
+        IMX_TRY(run_scan(c, 2, hooks));
+    } else if (mode == HOOK_PULL || mode == HOOK_HYBRID) {
         IMX_TRY(run_pull(c, 1, nullptr));
         if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));
         if (mode == HOOK_PULL) IMX_TRY(run_pull(c, 2, hooks));

@@ -1,0 +1,329 @@
+// scan.cu -- sampler "scan": the pull forest with lanes bucketed by the top
+// bits of their simulation word (uniform thresholds).
+//
+// Membership of edge slot s in lane r is (X[r] ^ h_s) < t (hashing.py:141-150,
+// strict, 31-bit words).  With t <= 2^k, (x ^ h) < t forces x >> k == h >> k,
+// so for a slot with hash h only the lanes whose word shares h's top 31-k
+// bits can be live: C4 (t = 0.005 * 2^31 < 2^24) keeps 1 lane in 128, C5
+// (p = 0.05) 1 in 16.  At context setup the lanes of every chunk of <= 1024
+// lanes are sorted by x >> kb (kb >= k) into buckets; a slot then tests only
+// its bucket's lanes instead of all of them -- the reference's _xor_below
+// interval idea (propagation.py:104-118) applied to the lane side, so the
+// adjacency is still read once per row and reused across every lane.
+//
+// Pass 1 (replaces k_init): a warp owns a vertex row.  It stages the row of
+// the chunk in shared memory (all ROOT), walks v's smaller-neighbour prefix
+// in ascending order (rows are sorted, graph.py:149), and for every live
+// (slot, lane) keeps the first -- i.e. smallest -- live smaller neighbour:
+// L[v][r] = that neighbour (a parent pointer to a smaller id) or ROOT.  The
+// row is then written with 16-byte coalesced stores: a forest of live edges,
+// no random access.
+// Pass 2: the same walk; every live pair that is not its lane's first live
+// neighbour (the forest edge) is united through a per-warp shared-memory
+// queue (uf.cuh unite), 32 unions at a time.
+// Heavy rows (prefix > T slots) are cut into slices of T slots, one warp
+// each: pass 1 folds the slice's first live neighbours into the row with
+// atomicMin (the light pass wrote the row as ROOT), pass 2 unites every live
+// neighbour except the one the row points at.
+//
+// Correctness does not depend on the buckets: a bucket is a superset of the
+// live lanes and every candidate is re-tested exactly.
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "ctx.cuh"
+#include "uf.cuh"
+
+namespace imx {
+
+constexpr int kScanCW = 1024;        // lanes per chunk: a 4 KB shared row per warp
+constexpr int kScanWarps = 8;
+constexpr int kScanQ = 64;           // per-warp union queue: drain at 32, one step adds <= 32
+constexpr int kScanMaxBucketBits = 10;
+
+template <int PASS, bool HEAVY>
+__global__ void __launch_bounds__(kScanWarps * 32)
+k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const int32_t *__restrict__ hash,
+       int32_t t, int kb, int nb, int cw, int nchunks, const int32_t *__restrict__ xs_all,
+       const uint16_t *__restrict__ perm_all, const int32_t *__restrict__ boff_all, int64_t n, int32_t W,
+       int64_t ld, uint32_t *__restrict__ L, unsigned long long *__restrict__ hooks,
+       const uint8_t *__restrict__ heavy, const int32_t *__restrict__ hs_v, const int64_t *__restrict__ hs_a,
+       const int32_t *__restrict__ hs_len, int64_t nhs, unsigned long long *__restrict__ ctr, int grab) {
+    extern __shared__ int4 smem4[];
+    // 16-byte aligned sections (run_scan sizes them): per-warp first-live
+    // flags, per-warp union queues (pass 2), the chunk's lane tables
+    uint8_t *flags_all = reinterpret_cast<uint8_t *>(smem4);                   // [warps][cw]
+    uint32_t *queues = reinterpret_cast<uint32_t *>(flags_all + kScanWarps * cw);   // [warps][3][kScanQ]
+    int32_t *sxs = reinterpret_cast<int32_t *>(queues + (PASS == 2 ? kScanWarps * 3 * kScanQ : 0));
+    int32_t *sboff = sxs + cw;                                                   // [nb + 1]
+    uint16_t *sperm = reinterpret_cast<uint16_t *>(sboff + nb + 1);              // [cw]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t *flag = flags_all + warp * cw;
+    uint32_t *qlo = queues + warp * 3 * kScanQ, *qhi = qlo + kScanQ, *qr = qhi + kScanQ;
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int qn = 0;
+    unsigned long long nh = 0;
+    const int64_t items = HEAVY ? nhs : n;
+    for (int c = 0; c < nchunks; ++c) {
+        const int r0 = c * cw;
+        const int rwc = (int)min((int64_t)cw, ld - r0);  // row cells of this chunk (incl. padding)
+        __syncthreads();
+        for (int i = threadIdx.x; i < cw; i += blockDim.x) {
+            sxs[i] = xs_all[(int64_t)c * cw + i];
+            sperm[i] = perm_all[(int64_t)c * cw + i];
+        }
+        for (int i = threadIdx.x; i <= nb; i += blockDim.x) sboff[i] = boff_all[(int64_t)c * (nb + 1) + i];
+        __syncthreads();
+        for (;;) {
+            // dynamic distribution: rows differ by orders of magnitude in
+            // prefix length, so warps take small batches from a counter
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(ctr + c, (unsigned long long)grab);
+            base = __shfl_sync(FULL, base, 0);
+            if ((int64_t)base >= items) break;
+            const int cntv = (int)(min((int64_t)base + grab, items) - (int64_t)base);
+            // the grab's row bounds in one coalesced load (light rows); the
+            // next row's first slot batch is loaded while this row is worked
+            int64_t xa = 0;
+            bool hv_l = false;
+            if (!HEAVY) {
+                if (lane <= cntv) xa = __ldg(xadj + base + lane);
+                if (heavy && lane < cntv) hv_l = heavy[base + lane] != 0;
+            }
+            const unsigned hmask = __ballot_sync(FULL, hv_l);
+            auto bounds = [&](int k, int64_t &v, int64_t &s0, int64_t &s1) {
+                if (HEAVY) {
+                    v = hs_v[base + k];
+                    s0 = hs_a[base + k];
+                    s1 = s0 + hs_len[base + k];
+                } else {
+                    v = (int64_t)base + k;
+                    s0 = __shfl_sync(FULL, xa, k);
+                    s1 = __shfl_sync(FULL, xa, k + 1);
+                    if ((hmask >> k) & 1u) s1 = s0;        // heavy row: ROOT here, slices below
+                }
+            };
+            auto batch = [&](int64_t b0, int64_t s1, int64_t v, uint32_t &bu, int32_t &bh) {
+                const int64_t sb = b0 + lane;
+                bu = (uint32_t)v;
+                bh = 0;
+                if (sb < s1) {
+                    bu = (uint32_t)__ldg(adj + sb);
+                    bh = __ldg(hash + sb);
+                }
+            };
+            int64_t v, s0, s1;
+            uint32_t bu0;
+            int32_t bh0;
+            bounds(0, v, s0, s1);
+            batch(s0, s1, v, bu0, bh0);
+            for (int k = 0; k < cntv; ++k) {
+                int64_t nv = 0, ns0 = 0, ns1 = 0;
+                uint32_t nbu = 0;
+                int32_t nbh = 0;
+                // pass 1 prefetches the next row's first batch; pass 2 keeps
+                // its registers for the unions (prefetching there measured
+                // slower: C5 pass 2 15.8 -> 21.3 ms)
+                if (PASS == 1 && k + 1 < cntv) {
+                    bounds(k + 1, nv, ns0, ns1);
+                    batch(ns0, ns1, nv, nbu, nbh);
+                }
+                if (PASS == 2 && k > 0) {
+                    bounds(k, v, s0, s1);
+                    batch(s0, s1, v, bu0, bh0);
+                }
+                uint32_t *Lv = L + v * ld + r0;
+                if (PASS == 1 && !HEAVY) {                 // the row starts as all roots
+                    uint4 *o4 = reinterpret_cast<uint4 *>(Lv);
+                    for (int q = lane; q < (rwc >> 2); q += 32) o4[q] = make_uint4(ROOT, ROOT, ROOT, ROOT);
+                }
+                // any smaller neighbour (rows ascend: the first slot says)
+                const bool has = s0 < s1 && __shfl_sync(FULL, bu0, 0) < (uint32_t)v;
+                if (has) {
+                if (PASS == 1 || !HEAVY) {
+                    uint4 *f4 = reinterpret_cast<uint4 *>(flag);
+                    for (int q = lane; q < (cw >> 4); q += 32) f4[q] = make_uint4(0, 0, 0, 0);
+                }
+                __syncwarp();
+                for (int64_t b0 = s0; b0 < s1; b0 += 32) {
+                    uint32_t bu = bu0;
+                    int32_t bh = bh0;
+                    if (b0 != s0) batch(b0, s1, v, bu, bh);
+                    // rows ascend: the smaller neighbours are a prefix of the batch
+                    const int cnt = __popc(__ballot_sync(FULL, bu < (uint32_t)v));
+                    for (int j = 0; j < cnt; ++j) {
+                        const uint32_t u = __shfl_sync(FULL, bu, j);
+                        const int32_t h = __shfl_sync(FULL, bh, j);
+                        const int bk = (int)((uint32_t)h >> kb);
+                        const int lo = sboff[bk], hi = sboff[bk + 1];
+                        for (int i0 = lo; i0 < hi; i0 += 32) {
+                            const int i = i0 + lane;
+                            const bool live = i < hi && (sxs[i] ^ h) < t;
+                            const int p = live ? sperm[i] : 0;
+                            if (PASS == 1) {
+                                // ascending slots: the first live neighbour is the smallest
+                                if (live && !flag[p]) {
+                                    flag[p] = 1;
+                                    if (HEAVY) atomicMin(Lv + p, u);
+                                    else Lv[p] = u;
+                                }
+                            } else {
+                                bool un = false;
+                                if (live) {
+                                    if (HEAVY) {
+                                        un = ld_relaxed(Lv + p) != u;   // all but the forest edge
+                                    } else {
+                                        un = flag[p] != 0;              // all but the first live neighbour
+                                        flag[p] = 1;
+                                    }
+                                }
+                                const unsigned b = __ballot_sync(FULL, un);
+                                if (un) {
+                                    const int pos = qn + __popc(b & lt_mask);
+                                    qlo[pos] = u;
+                                    qhi[pos] = (uint32_t)v;
+                                    qr[pos] = (uint32_t)(r0 + p);
+                                }
+                                qn += __popc(b);
+                                __syncwarp();
+                                if (qn >= 32) {
+                                    qn -= 32;
+                                    const uint32_t a2 = qlo[qn + lane], b2 = qhi[qn + lane];
+                                    const int rr = (int)qr[qn + lane];
+                                    __syncwarp();
+                                    nh += unite(L, ld, a2, b2, rr);
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    if (cnt < 32) break;                   // the prefix ended inside this batch
+                }
+                }
+                if (PASS == 1) { v = nv; s0 = ns0; s1 = ns1; bu0 = nbu; bh0 = nbh; }
+            }
+        }
+    }
+    if (PASS == 2) {
+        __syncwarp();
+        if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
+    }
+    if (hooks) {
+        for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
+        if (lane == 0 && nh) atomicAdd(hooks, nh);
+    }
+}
+
+// ---- host side ---------------------------------------------------------------
+
+// bucket shift for threshold t: smallest k with t <= 2^k, raised so that
+// there are at most 2^kScanMaxBucketBits buckets
+static int scan_kb(int32_t t) {
+    int k = 0;
+    while (k < 31 && ((int64_t)1 << k) < (int64_t)t) ++k;
+    return std::max(k, 31 - kScanMaxBucketBits);
+}
+
+bool scan_eligible(const imx_graph *g) {
+    if (const char *e = getenv("IMX_SCAN")) if (!atoi(e)) return false;
+    return g->uniform && !g->hash_neg && g->thr_u > 0;
+}
+
+// the per-chunk lane tables for this context's X and the graph's threshold
+static int ensure_scan_tables(imx_ctx *c) {
+    const int kb = scan_kb(c->g->thr_u);
+    if (c->scan_xs && c->scan_kb == kb) return IMX_OK;
+    for (void **p : {(void **)&c->scan_xs, (void **)&c->scan_perm, (void **)&c->scan_boff}) {
+        if (*p) cudaFreeAsync(*p, c->st);
+        *p = nullptr;
+    }
+    const int cw = std::min<int>(kScanCW, (c->W + 15) & ~15);
+    const int nchunks = (c->W + cw - 1) / cw;
+    const int nb = 1 << (31 - kb);
+    std::vector<int32_t> xs((size_t)nchunks * cw, 0), boff((size_t)nchunks * (nb + 1), 0);
+    std::vector<uint16_t> perm((size_t)nchunks * cw, 0);
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int r0 = ch * cw, cnt = std::min(cw, c->W - r0);
+        std::vector<int> idx(cnt);
+        for (int i = 0; i < cnt; ++i) idx[i] = i;
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+            return ((uint32_t)c->hX[r0 + a] >> kb) < ((uint32_t)c->hX[r0 + b] >> kb);
+        });
+        int32_t *bo = boff.data() + (size_t)ch * (nb + 1);
+        for (int i = 0; i < cnt; ++i) {
+            xs[(size_t)ch * cw + i] = c->hX[r0 + idx[i]];
+            perm[(size_t)ch * cw + i] = (uint16_t)idx[i];
+            ++bo[((uint32_t)c->hX[r0 + idx[i]] >> kb) + 1];
+        }
+        for (int b = 0; b < nb; ++b) bo[b + 1] += bo[b];
+    }
+    IMX_CUDA(pool_alloc((void **)&c->scan_xs, sizeof(int32_t) * xs.size(), c->st));
+    IMX_CUDA(pool_alloc((void **)&c->scan_perm, sizeof(uint16_t) * perm.size(), c->st));
+    IMX_CUDA(pool_alloc((void **)&c->scan_boff, sizeof(int32_t) * boff.size(), c->st));
+    if (c->scan_ctr) cudaFreeAsync(c->scan_ctr, c->st);
+    IMX_CUDA(pool_alloc((void **)&c->scan_ctr, sizeof(unsigned long long) * nchunks, c->st));
+    IMX_CUDA(cudaMemcpyAsync(c->scan_xs, xs.data(), sizeof(int32_t) * xs.size(), cudaMemcpyHostToDevice, c->st));
+    IMX_CUDA(cudaMemcpyAsync(c->scan_perm, perm.data(), sizeof(uint16_t) * perm.size(), cudaMemcpyHostToDevice, c->st));
+    IMX_CUDA(cudaMemcpyAsync(c->scan_boff, boff.data(), sizeof(int32_t) * boff.size(), cudaMemcpyHostToDevice, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));     // the host vectors go out of scope
+    c->scan_kb = kb;
+    c->scan_nb = nb;
+    c->scan_cw = cw;
+    c->scan_nchunks = nchunks;
+    return IMX_OK;
+}
+
+// slice length of heavy rows (IMX_SCAN_HEAVY, default 512 slots): a slice
+// costs a warp one row load (pass 2) or one atomicMin per live lane (pass 1)
+static int scan_heavy_T() {
+    const char *e = getenv("IMX_SCAN_HEAVY");
+    return e ? std::max(0, atoi(e)) : 512;
+}
+
+static int scan_bpsm() {
+    const char *e = getenv("IMX_SCAN_BPSM");
+    return e && atoi(e) > 0 ? atoi(e) : 8;
+}
+
+int run_scan(imx_ctx *c, int pass, unsigned long long *hooks) {
+    imx_graph *g = c->g;
+    const int64_t n = g->n;
+    if (n == 0) return IMX_OK;
+    IMX_TRY(ensure_scan_tables(c));
+    const int T = scan_heavy_T();
+    IMX_TRY(ensure_heavy(c, pass, T));
+    const auto &H = g->hv[pass - 1];
+    const int cw = c->scan_cw, nb = c->scan_nb;
+    // cw is a multiple of 16, so every section keeps 16-byte alignment
+    const size_t smem = (size_t)kScanWarps * cw + (pass == 2 ? sizeof(uint32_t) * kScanWarps * 3 * kScanQ : 0) +
+                        sizeof(int32_t) * cw + sizeof(int32_t) * (nb + 1) + sizeof(uint16_t) * cw;
+    using KF = void (*)(const int64_t *, const int32_t *, const int32_t *, int32_t, int, int, int, int,
+                        const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, uint32_t *,
+                        unsigned long long *, const uint8_t *, const int32_t *, const int64_t *, const int32_t *,
+                        int64_t, unsigned long long *, int);
+    static const KF kerns[2][2] = {{k_scan<1, false>, k_scan<1, true>}, {k_scan<2, false>, k_scan<2, true>}};
+    const int hv = H.nhs > 0 ? 2 : 1;
+    for (int h = 0; h < hv; ++h) {
+        KF kern = kerns[pass - 1][h];
+        IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int64_t items = h ? H.nhs : n;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, kScanWarps), 148 * scan_bpsm()));
+        // items per counter grab: up to 16 rows, fewer when that would leave
+        // warps idle (C2: 37k rows over ~9.5k warps)
+        const int64_t warps = (int64_t)blocks * kScanWarps;
+        const int grab = h ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, items / (warps * 8)));
+        IMX_CUDA(cudaMemsetAsync(c->scan_ctr, 0, sizeof(unsigned long long) * c->scan_nchunks, c->st));
+        kern<<<blocks, kScanWarps * 32, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr_u, c->scan_kb, nb, cw,
+                                                       c->scan_nchunks, c->scan_xs, c->scan_perm, c->scan_boff, n,
+                                                       c->W, c->ld, c->L, pass == 2 ? hooks : nullptr,
+                                                       H.nhs > 0 ? H.heavy : nullptr, H.hs_v, H.hs_a, H.hs_len,
+                                                       H.nhs, c->scan_ctr, grab);
+        IMX_CHECK_LAUNCH();
+        count_launch(c);
+    }
+    return IMX_OK;
+}
+
+}  // namespace imx

@@ -112,7 +112,7 @@ def test_select_seeds_on_host_arrays_matches_oracle(gpu, orc, name):
     assert gpu.recompute_sigma(labels, res.state) == res.sigma
 
 
-@pytest.mark.parametrize("mode", ["enum", "pull", "dense", "hybrid"])
+@pytest.mark.parametrize("mode", ["enum", "pull", "dense", "hybrid", "scan"])
 @pytest.mark.parametrize("name", ["er_big_1000", "er_uniform_r24", "er_wc_r40", "er_const1_r16",
                                   "er_const0_r16", "er_pad20", "kat_dead_middle", "cfg_c1", "cfg_c2"])
 def test_every_sampler_strategy_reaches_the_reference_fixpoint(gpu, name, mode, monkeypatch):
@@ -266,10 +266,11 @@ def test_wide_lane_strategies_agree_at_config_scale(gpu, cfg, R, monkeypatch):
     randoms = gpu.SimulationRandoms(R, 1)
     table = gpu.build_hash_table(g)
     out = {}
-    for mode in ("pull", "enum", "hybrid"):
+    for mode in ("pull", "enum", "hybrid", "scan"):
         monkeypatch.setenv("IMX_HOOK", mode)
         out[mode] = gpu.propagate(g, table, randoms)
     assert np.array_equal(out["pull"], out["enum"])
+    assert np.array_equal(out["scan"], out["enum"])
     assert np.array_equal(out["hybrid"], out["enum"])
 
 

@@ -40,7 +40,7 @@ def test_random_graphs_match_oracle(gpu, orc, seed, monkeypatch):
     R = int(rng.integers(1, 300))
     k = int(rng.integers(1, n + 1))
     want = orc.run_fused(g.xadj, g.adj, g.weights, k, R, seed, nthreads=2)
-    for mode in ("enum", "pull", "dense", "hybrid", None):
+    for mode in ("enum", "pull", "dense", "hybrid", "scan", None):
         if mode:
             monkeypatch.setenv("IMX_HOOK", mode)
         else:
@@ -105,3 +105,27 @@ def test_heavy_rows_match_oracle(gpu, orc, seed, monkeypatch):
         assert np.array_equal(run.sizes, want["sizes"]), tag
         assert [int(s) for s in run.seeds] == want["seeds"].tolist(), tag
         assert np.array_equal(run.selection.trace.array, want["trace"]), tag
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_scan_heavy_rows_match_oracle(gpu, orc, seed, monkeypatch):
+    """The bucketed pull forest (uniform thresholds) with heavy-row slices of
+    1, 3 and 512 slots and with splitting off, through the whole pipeline."""
+    rng = np.random.default_rng(9000 + seed)
+    n, e, _ = hub_on_top_graph(rng)
+    p = float(rng.choice([0.003, 0.02, 0.2, 0.9]))
+    g = gpu.Graph.from_edges(n, e, p)
+    R = int(rng.choice([8, 24, 100, 256, 1100, 2100]))
+    k = int(rng.integers(1, 12))
+    want = orc.run_fused(g.xadj, g.adj, g.weights, k, R, seed, nthreads=2)
+    monkeypatch.setenv("IMX_HOOK", "scan")
+    for heavy in (None, "1", "3", "0"):
+        if heavy is None:
+            monkeypatch.delenv("IMX_SCAN_HEAVY", raising=False)
+        else:
+            monkeypatch.setenv("IMX_SCAN_HEAVY", heavy)
+        run = gpu.run_fused(g, k, num_simulations=R, master_seed=seed)
+        assert np.array_equal(run.labels, want["labels"]), heavy
+        assert np.array_equal(run.sizes, want["sizes"]), heavy
+        assert [int(s) for s in run.seeds] == want["seeds"].tolist(), heavy
+        assert np.array_equal(run.selection.trace.array, want["trace"]), heavy

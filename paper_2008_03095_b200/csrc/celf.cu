@@ -346,6 +346,10 @@ __device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, co
 #define IMX_CELF_STEP_PER_CTA 256
 #endif
 constexpr int64_t kStepPerCta = IMX_CELF_STEP_PER_CTA;
+#ifndef IMX_CELF_FIRST_CAP
+#define IMX_CELF_FIRST_CAP 16384
+#endif
+constexpr int64_t kFirstBatchCap = IMX_CELF_FIRST_CAP;
 
 template <bool ENC>
 #ifndef IMX_CELF_MINB
@@ -580,7 +584,12 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
             olen -= kr;
         }
         T += nrec;
+        // next round's first batch: 1.5x this round's refreshed prefix, but at
+        // most kFirstBatchCap -- one huge round (C4's round 1 refreshes 2.3M
+        // vertices after the hub) must not make the next round evaluate
+        // millions speculatively (C4: 4.66M -> ~2.5M evaluations)
         if (t > 0) batch0 = kr * bpct / 100 > 64 ? kr * bpct / 100 : 64;
+        if (batch0 > kFirstBatchCap) batch0 = kFirstBatchCap;
         ++t;
         grid.sync();
         PROF_MARK(3);
@@ -861,7 +870,7 @@ static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seed
             if (ids[kr] != best_v) back.emplace_back(host_key(c, fr[kr], ids[kr]), ids[kr]);
             ++kr;
         }
-        batch0 = std::max<int64_t>(64, kr);
+        batch0 = std::min<int64_t>(kFirstBatchCap, std::max<int64_t>(64, kr));
     }
     std::sort(back.begin(), back.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
     std::vector<int32_t> bid(back.size());
@@ -1078,7 +1087,7 @@ static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<in
         c->olen = na + nback;
         seeds[t] = best_v;
         gains[t] = best_f;
-        batch0 = std::max<int64_t>(64, kr);
+        batch0 = std::min<int64_t>(kFirstBatchCap, std::max<int64_t>(64, kr));
     }
 done:
     for (void *p : {(void *)rec, (void *)keys, (void *)skeys, (void *)ids, (void *)sids, tmp})

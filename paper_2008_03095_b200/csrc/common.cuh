@@ -72,6 +72,7 @@ void release_stream(int dev, cudaStream_t st);
 // host->device copy of a pageable buffer, staged through pinned memory by
 // host threads when large (upload.cu)
 cudaError_t upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t st);
+bool host_pinned_ptr(const void *p);
 // stream-ordered allocation from the device's pool (ctx.cu)
 cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
 

@@ -110,6 +110,8 @@ struct imx_ctx {
     // memoisation fused into the tiled compression (imx_set_fuse_memo): the
     // last propagate left the gains in `gains` (gains_fused)
     bool fuse_memo = false, gains_fused = false;
+    // the last sampler launch used a deferred graph's speculative threshold
+    bool spec_used = false;
     imx_timings tm{};
 };
 

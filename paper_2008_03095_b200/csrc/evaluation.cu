@@ -287,6 +287,8 @@ extern "C" int imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k,
     for (int32_t i = 0; i < k; ++i)
         if (seeds[i] < 0 || seeds[i] >= n) { set_error("seed outside vertex range"); return IMX_EINVAL; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(graph_settle(g));          // weights of a deferred graph
+    IMX_TRY(ensure_recip(g));          // p = max(w, w[reciprocal]) per canonical edge
     cudaStream_t st = g->stream;
     // worlds per batch: the label matrix stays under ~4 GiB
     int64_t B = std::min<int64_t>(chunk, 4096);

@@ -20,6 +20,7 @@
 #include <vector>
 #include <chrono>
 #include <functional>
+#include <thread>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -212,10 +213,45 @@ struct GStats {
     unsigned long long maxp;   // max #smaller neighbours (k_max_prefix)
     unsigned long long tsum;   // sum of canonical-slot thresholds
     int64_t me;                // canonical slots (DeviceSelect count)
+    unsigned long long symsum; // sum of mix(u, v) - mix(v, u) over slots (k_sym_check)
 };
 __global__ void k_stats_init(GStats *gs) {
     gs->flags = 0; gs->tmin = INT32_MAX; gs->tmax = INT32_MIN; gs->pad = 0;
-    gs->maxp = 0; gs->tsum = 0; gs->me = 0;
+    gs->maxp = 0; gs->tsum = 0; gs->me = 0; gs->symsum = 0;
+}
+
+// Symmetry of a large host CSR without the reciprocal search (deferred
+// path): rows strictly ascending (no duplicate, no self-loop) and the slot
+// multiset equal to its transpose, tested as sum(mix(u, v) - mix(v, u)) == 0
+// over all slots mod 2^64 (mix = SplitMix64 of the ordered pair).  The exact
+// pairing (k_reciprocal) runs later if anything needs it and re-checks.
+// flags: 8 = not symmetric / unsorted, 32 = entry outside 0..n-1.
+__device__ __forceinline__ unsigned long long pair_mix(uint32_t a, uint32_t b) {
+    unsigned long long z = ((unsigned long long)a << 32 | b) + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__global__ void k_sym_check(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                            const int32_t *__restrict__ src, int64_t n, int64_t m2, GStats *__restrict__ gs) {
+    unsigned long long sum = 0;
+    unsigned fl = 0;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = src[s], v = adj[s];
+        if (v < 0 || v >= n) { fl |= 32u | 8u; continue; }
+        if (u == v) fl |= 8u;
+        if (s > xadj[u] && adj[s - 1] >= v) fl |= 8u;
+        sum += pair_mix((uint32_t)u, (uint32_t)v) - pair_mix((uint32_t)v, (uint32_t)u);
+    }
+    for (int o = 16; o; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (sum) atomicAdd(&gs->symsum, sum);
+        if (fl) atomicOr(&gs->flags, fl);
+    }
 }
 
 // thresholds (symmetrized over valid reciprocal slots when recip != NULL),
@@ -495,6 +531,7 @@ static int dalloc(imx_graph *g, T **p, int64_t count) {
 void graph_free(imx_graph *g) {
     if (!g) return;
     cudaSetDevice(g->dev);
+    if (g->thr_pending) graph_settle(g);    // joins the weight upload
     void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
                     g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff, g->lut,
                     g->hv[0].heavy, g->hv[0].hs_v, g->hv[0].hs_a, g->hv[0].hs_len,
@@ -516,6 +553,11 @@ static int graph_build_index(imx_graph *g) {
     if (g->boff) { cudaFreeAsync(g->boff, st); g->boff = nullptr; }
     if (g->lut) { cudaFreeAsync(g->lut, st); g->lut = nullptr; }
     g->nb = nb;
+    if (!g->E) {
+        IMX_CUDA(pool_alloc((void **)&g->E, sizeof(int2) * std::max<int64_t>(1, me), st));
+        IMX_CUDA(pool_alloc((void **)&g->EH, sizeof(int32_t) * std::max<int64_t>(1, me), st));
+        IMX_CUDA(pool_alloc((void **)&g->ET, sizeof(int32_t) * std::max<int64_t>(1, me), st));
+    }
     int bits = 6;
     while (bits < 16 && ((int64_t)1 << (bits + 1)) <= me / nb) ++bits;
     g->lut_bits = bits;
@@ -688,18 +730,199 @@ static int graph_analyze(imx_graph *g, bool structure, const std::function<int()
             IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
             IMX_CUDA(cudaStreamSynchronize(st));
         }
-        IMX_TRY(dalloc(g, &g->E, g->me));
-        IMX_TRY(dalloc(g, &g->EH, g->me));
-        IMX_TRY(dalloc(g, &g->ET, g->me));
     }
     cudaFreeAsync(gs, st);
     g->hash_neg = (h.flags & 128u) != 0;
     g->uniform = m2 ? (h.tmin == h.tmax) : 1;
     g->thr_u = m2 ? h.tmin : 0;
     g->thr_mean = g->me ? (double)h.tsum / (double)g->me / 2147483647.0 : 0.0;
-    IMX_TRY(graph_build_index(g));
+    g->index_ready = false;          // built on first use (ensure_index)
+    return IMX_OK;
+}
+
+// imx_graph_from_csr for large graphs: the structure (sources, hashes, max
+// prefix, offsets, symmetry, canonical slots) on the graph stream with one
+// host sync; the weights and their raw per-slot thresholds on a second
+// stream, not waited for (graph_settle).  Until then the graph claims the
+// speculative uniform threshold of weights[0].
+static int graph_analyze_deferred(imx_graph *g, const double *weights) {
+    cudaStream_t st = g->stream;
+    const int64_t m2 = g->m2, n = g->n;
+    GStats *gs = nullptr;
+    IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
+    k_stats_init<<<1, 1, 0, st>>>(gs); note_launch();
+    IMX_TRY(dalloc(g, &g->src, m2));
+    IMX_TRY(dalloc(g, &g->hash, m2));
+    IMX_TRY(dalloc(g, &g->thr, m2));
+    IMX_TRY(dalloc(g, &g->cslot, m2));
+    IMX_CUDA(cudaMemsetAsync(g->src, 0, sizeof(int32_t) * m2, st));   // rows of corrupt offsets
+    k_src_rows<<<grid_for(n * 32), 256, 0, st>>>(g->xadj, n, m2, g->src);
+    k_check_xadj<<<grid_for(n), 256, 0, st>>>(g->xadj, n, m2, &gs->flags);
+    k_sym_check<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, n, m2, gs);
+    k_slot_hashes<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, g->hash);
+    k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, m2, &gs->maxp);
+    note_launch(5);
+    IMX_CHECK_LAUNCH();
+    {
+        uint8_t *flag;
+        IMX_CUDA(pool_alloc((void **)&flag, m2, st));
+        k_canon_flags<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, flag); note_launch();
+        size_t tmp_bytes = 0;
+        thrust::counting_iterator<int64_t> it(0);
+        IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flag, g->cslot, &gs->me, m2, st));
+        void *tmp;
+        IMX_CUDA(pool_alloc(&tmp, tmp_bytes, st));
+        IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flag, g->cslot, &gs->me, m2, st));
+        note_launch(2);
+        cudaFreeAsync(tmp, st);
+        cudaFreeAsync(flag, st);
+    }
+    // the weight stream: upload, then (after the structure) raw thresholds
+    cudaEvent_t ev_struct = nullptr;
+    IMX_CUDA(cudaEventCreateWithFlags(&ev_struct, cudaEventDisableTiming));
+    IMX_CUDA(cudaEventRecord(ev_struct, st));
+    IMX_CUDA(acquire_stream(g->dev, &g->wst));
+    IMX_CUDA(cudaEventCreateWithFlags(&g->wev, cudaEventDisableTiming));
+    IMX_CUDA(pool_alloc(&g->wstats_d, sizeof(GStats), st));
+    IMX_CUDA(cudaMallocHost(&g->wstats_h, sizeof(GStats)));
+    IMX_CUDA(cudaStreamWaitEvent(g->wst, ev_struct, 0));      // buffers allocated on st
+    GStats *wd = static_cast<GStats *>(g->wstats_d);
+    GStats *wh = static_cast<GStats *>(g->wstats_h);
+    auto finish = [g, m2, wd, wh]() -> int {
+        cudaStream_t ws = g->wst;
+        k_stats_init<<<1, 1, 0, ws>>>(wd);
+        k_thresholds<<<grid_for(m2), 256, 0, ws>>>(g->w, nullptr, g->src, g->adj, g->hash, m2, g->thr, wd);
+        note_launch(2);
+        IMX_CHECK_LAUNCH();
+        IMX_CUDA(cudaMemcpyAsync(wh, wd, sizeof(GStats), cudaMemcpyDeviceToHost, ws));
+        IMX_CUDA(cudaEventRecord(g->wev, ws));
+        return IMX_OK;
+    };
+    const size_t wbytes = sizeof(double) * (size_t)m2;
+    if (host_pinned_ptr(weights)) {
+        IMX_CUDA(cudaMemcpyAsync(g->w, weights, wbytes, cudaMemcpyHostToDevice, g->wst));
+        IMX_TRY(finish());
+    } else {
+        // pageable weights: the staged upload blocks its thread, so it runs
+        // on its own host thread (joined by graph_settle)
+        const int dev = g->dev;
+        g->wthread = new std::thread([g, weights, wbytes, finish, dev]() {
+            cudaSetDevice(dev);
+            cudaError_t e = upload_h2d(g->w, weights, wbytes, g->wst);
+            g->wthread_rc = e != cudaSuccess ? cuda_fail(e, "upload weights", __FILE__, __LINE__) : finish();
+        });
+    }
+    g->thr_pending = true;
+    GStats h;
+    IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
     IMX_CUDA(cudaStreamSynchronize(st));
-    g_clock.mark("sampler index", st);
+    cudaEventDestroy(ev_struct);
+    cudaFreeAsync(gs, st);
+    g_clock.mark("structure (1 sync)", st);
+    if (h.flags & 64u) { set_error("corrupt CSR offsets"); return IMX_EINVAL; }
+    if (h.flags & 32u) { set_error("adjacency entry outside 0..n-1"); return IMX_EINVAL; }
+    g->symmetric = (h.flags & 8u) == 0 && h.symsum == 0 && (m2 % 2 == 0);
+    g->max_prefix = (int64_t)h.maxp;
+    g->me = h.me;
+    if (g->me >= (int64_t(1) << 31)) {
+        set_error("%lld undirected edges exceed 2^31 - 1", (long long)g->me);
+        return IMX_ECONSTRAINT;
+    }
+    g->recip_ready = false;
+    g->index_ready = false;
+    g->hash_neg = 0;                     // fresh 31-bit hashes
+    // speculation: every slot's threshold is weights[0]'s (hashing.py:135-138)
+    const int32_t t0 = (int32_t)(int64_t)(weights[0] * 2147483647.0);
+    g->uniform = 1;
+    g->thr_u = t0;
+    g->thr_mean = (double)t0 / 2147483647.0;
+    return IMX_OK;
+}
+
+}  // namespace imx
+
+namespace imx {
+
+int graph_settle(imx_graph *g) {
+    if (!g->thr_pending) return IMX_OK;
+    g->thr_pending = false;
+    if (g->wthread) {
+        auto *t = static_cast<std::thread *>(g->wthread);
+        t->join();
+        delete t;
+        g->wthread = nullptr;
+    }
+    int rc = g->wthread_rc;
+    cudaError_t e = cudaEventSynchronize(g->wev);
+    if (rc == IMX_OK && e != cudaSuccess) rc = cuda_fail(e, "weights", __FILE__, __LINE__);
+    GStats h = *static_cast<GStats *>(g->wstats_h);
+    cudaEventDestroy(g->wev);
+    g->wev = nullptr;
+    release_stream(g->dev, g->wst);
+    g->wst = nullptr;
+    cudaFreeHost(g->wstats_h);
+    g->wstats_h = nullptr;
+    cudaFreeAsync(g->wstats_d, g->stream);
+    g->wstats_d = nullptr;
+    if (rc != IMX_OK) return rc;
+    if (g->m2 && h.tmin != h.tmax && g->symmetric) {
+        // per-slot thresholds: symmetrized through the reciprocal slots
+        IMX_TRY(ensure_recip(g));
+        GStats *gs;
+        IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), g->stream));
+        k_stats_init<<<1, 1, 0, g->stream>>>(gs);
+        k_thresholds<<<grid_for(g->m2), 256, 0, g->stream>>>(g->w, g->recip, g->src, g->adj, g->hash, g->m2,
+                                                             g->thr, gs);
+        note_launch(2);
+        IMX_CHECK_LAUNCH();
+        IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, g->stream));
+        IMX_CUDA(cudaStreamSynchronize(g->stream));
+        cudaFreeAsync(gs, g->stream);
+    }
+    g->hash_neg = (h.flags & 128u) != 0;
+    g->uniform = g->m2 ? (h.tmin == h.tmax) : 1;
+    g->thr_u = g->m2 ? h.tmin : 0;
+    g->thr_mean = g->me ? (double)h.tsum / (double)g->me / 2147483647.0 : 0.0;
+    g->index_ready = false;
+    return IMX_OK;
+}
+
+int ensure_recip(imx_graph *g) {
+    if (g->recip_ready) return IMX_OK;
+    cudaStream_t st = g->stream;
+    const int64_t m2 = g->m2;
+    GStats *gs;
+    IMX_TRY(dalloc(g, &g->recip, m2));
+    IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
+    k_stats_init<<<1, 1, 0, st>>>(gs);
+    if (m2) {
+        IMX_CUDA(cudaMemsetAsync(g->recip, 0xff, sizeof(int64_t) * m2, st));     // -1
+        k_reciprocal<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, nullptr, g->n, m2, g->recip,
+                                                    g->thr, gs);
+        k_recip_check<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, g->recip, m2, &gs->flags);
+        note_launch(3);
+        IMX_CHECK_LAUNCH();
+    }
+    GStats h;
+    IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
+    IMX_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(gs, st);
+    if (h.flags & 8u) {
+        g->symmetric = 0;
+        set_error("adjacency is not symmetric");
+        return IMX_EFORMAT;
+    }
+    g->recip_ready = true;
+    return IMX_OK;
+}
+
+int ensure_index(imx_graph *g) {
+    IMX_TRY(graph_settle(g));
+    if (g->index_ready) return IMX_OK;
+    IMX_TRY(graph_build_index(g));
+    // built on the graph stream; its users run on context streams
+    IMX_CUDA(cudaStreamSynchronize(g->stream));
+    g->index_ready = true;
     return IMX_OK;
 }
 
@@ -853,34 +1076,20 @@ extern "C" int imx_graph_from_csr(int32_t device, int64_t n, int64_t m2, const i
         (m2 && upload_h2d(g->adj, adj, sizeof(int32_t) * m2, st) != cudaSuccess))
         return fail(cuda_fail(cudaGetLastError(), "upload csr", __FILE__, __LINE__));
     // large graphs: the weights (8 bytes per slot, the biggest array) go up on
-    // a second stream while the weight-free structure kernels run
+    // a second stream and are not waited for (graph_analyze_deferred)
     const char *lw = getenv("IMX_LATE_WEIGHTS");
     const bool late = m2 > 0 && (lw ? atoi(lw) != 0 : m2 >= ((int64_t)1 << 22));
-    if (!late && m2 && upload_h2d(g->w, weights, sizeof(double) * m2, st) != cudaSuccess)
+    if (late) {
+        g_clock.mark("upload csr", st);
+        const int rc = graph_analyze_deferred(g, weights);
+        if (rc != IMX_OK) return fail(rc);
+        *out = g;
+        return IMX_OK;
+    }
+    if (m2 && upload_h2d(g->w, weights, sizeof(double) * m2, st) != cudaSuccess)
         return fail(cuda_fail(cudaGetLastError(), "upload weights", __FILE__, __LINE__));
     g_clock.mark("upload csr", st);
-    cudaStream_t wst = nullptr;
-    cudaEvent_t wev = nullptr;
-    if (late) {
-        // g->w was allocated on st: the weight stream starts after that (and
-        // not after the structure kernels, which it is meant to overlap)
-        if (acquire_stream(device, &wst) != cudaSuccess ||
-            cudaEventCreateWithFlags(&wev, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventRecord(wev, st) != cudaSuccess || cudaStreamWaitEvent(wst, wev, 0) != cudaSuccess) {
-            if (wst) release_stream(device, wst);
-            if (wev) cudaEventDestroy(wev);
-            return fail(cuda_fail(cudaGetLastError(), "weight stream", __FILE__, __LINE__));
-        }
-    }
-    auto upload_weights = [&]() -> int {
-        IMX_CUDA(upload_h2d(g->w, weights, sizeof(double) * m2, wst));
-        IMX_CUDA(cudaEventRecord(wev, wst));
-        IMX_CUDA(cudaStreamWaitEvent(st, wev, 0));
-        return IMX_OK;
-    };
-    int rc = late ? graph_analyze(g, true, upload_weights) : graph_analyze(g, true);
-    if (wst) release_stream(device, wst);
-    if (wev) cudaEventDestroy(wev);
+    const int rc = graph_analyze(g, true);
     if (rc != IMX_OK) return fail(rc);
     *out = g;
     return IMX_OK;
@@ -898,6 +1107,7 @@ extern "C" int imx_graph_dims(const imx_graph *g, int64_t *n, int64_t *m2) {
 extern "C" int imx_graph_get_csr(imx_graph *g, int64_t *xadj, int32_t *adj, double *weights) {
     if (!g) { set_error("graph is NULL"); return IMX_EINVAL; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(graph_settle(g));
     cudaStream_t st = g->stream;
     if (xadj) IMX_CUDA(cudaMemcpyAsync(xadj, g->xadj, sizeof(int64_t) * (g->n + 1), cudaMemcpyDeviceToHost, st));
     if (adj && g->m2) IMX_CUDA(cudaMemcpyAsync(adj, g->adj, sizeof(int32_t) * g->m2, cudaMemcpyDeviceToHost, st));
@@ -910,6 +1120,8 @@ extern "C" int imx_graph_reciprocal(imx_graph *g, int64_t *recip) {
     if (!g || (!recip && g->m2)) { set_error("NULL argument"); return IMX_EINVAL; }
     if (!g->symmetric) { set_error("adjacency is not symmetric"); return IMX_EFORMAT; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(graph_settle(g));
+    IMX_TRY(ensure_recip(g));
     if (g->m2) {
         IMX_CUDA(cudaMemcpyAsync(recip, g->recip, sizeof(int64_t) * g->m2, cudaMemcpyDeviceToHost, g->stream));
         IMX_CUDA(cudaStreamSynchronize(g->stream));
@@ -920,6 +1132,8 @@ extern "C" int imx_graph_reciprocal(imx_graph *g, int64_t *recip) {
 extern "C" int imx_graph_set_weights(imx_graph *g, const double *weights) {
     if (!g || (!weights && g->m2)) { set_error("NULL argument"); return IMX_EINVAL; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(graph_settle(g));
+    if (g->symmetric) IMX_TRY(ensure_recip(g));
     cudaStream_t st = g->stream;
     if (g->m2) {
         double *tmp;
@@ -958,6 +1172,8 @@ extern "C" int imx_graph_hashes(imx_graph *g, int32_t *out) {
 extern "C" int imx_graph_set_hashes(imx_graph *g, const int32_t *hashes) {
     if (!g) { set_error("NULL argument"); return IMX_EINVAL; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(graph_settle(g));
+    if (g->symmetric) IMX_TRY(ensure_recip(g));
     if (g->m2) {
         if (hashes) {
             IMX_CUDA(cudaMemcpyAsync(g->hash, hashes, sizeof(int32_t) * g->m2, cudaMemcpyHostToDevice, g->stream));
@@ -973,6 +1189,7 @@ extern "C" int imx_graph_thresholds(imx_graph *g, int32_t symmetrize, int32_t *t
                                     int32_t *uniform_out) {
     if (!g || (!thr_out && g->m2)) { set_error("NULL argument"); return IMX_EINVAL; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(graph_settle(g));
     cudaStream_t st = g->stream;
     if (symmetrize && !g->symmetric) { set_error("adjacency is not symmetric"); return IMX_EFORMAT; }
     if (g->m2) {

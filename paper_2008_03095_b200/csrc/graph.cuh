@@ -41,6 +41,20 @@ struct imx_graph {
     // prefix exceeds hv[p].T slots (heavy[v] = 1) and their prefix slices
     // (vertex, first slot, length), built on first use (propagate.cu,
     // ensure_heavy)
+    // Large host CSRs (imx_graph_from_csr): the weights -- the biggest
+    // array, 8 bytes per slot -- go up on a second stream and their per-slot
+    // thresholds are computed there, while the caller already propagates with
+    // the speculative uniform threshold thr_u = threshold(weights[0]);
+    // graph_settle() waits for them and says whether the speculation held.
+    // The reciprocal slots and the enumeration index are built on first use.
+    bool thr_pending = false;
+    cudaStream_t wst = nullptr;
+    cudaEvent_t wev = nullptr;
+    void *wstats_d = nullptr, *wstats_h = nullptr;   // GStats (device, pinned host)
+    void *wthread = nullptr;                           // std::thread of a pageable upload
+    int wthread_rc = 0;
+    bool recip_ready = true;
+    bool index_ready = false;
     struct HeavySlices {
         int T = -1;
         uint8_t *heavy = nullptr;
@@ -57,4 +71,9 @@ void graph_free(imx_graph *g);
 int graph_create(int32_t device, int64_t n, int64_t m2, imx_graph **out);
 int graph_build_from_device_edges(imx_graph *g, const int64_t *dedges, int64_t k, const double *dw,
                                   double w_scalar);
+// the deferred weights/thresholds are in (waits for them); the lazily built
+// reciprocal slots and sampler index
+int graph_settle(imx_graph *g);
+int ensure_recip(imx_graph *g);
+int ensure_index(imx_graph *g);
 }

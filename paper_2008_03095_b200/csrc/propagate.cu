@@ -975,9 +975,20 @@ static int hook_mode(const imx_graph *g, int32_t W) {
 }
 
 // init + hook phases of one propagate (events bracket them)
+static bool needs_index(int mode) { return mode == HOOK_ENUM || mode == HOOK_DENSE || mode == HOOK_HYBRID; }
+
 static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_init, cudaEvent_t e_hook) {
     imx_graph *g = c->g;
-    const int mode = g->me ? hook_mode(g, c->W) : HOOK_ENUM;
+    int mode = g->me ? hook_mode(g, c->W) : HOOK_ENUM;
+    if (g->me && needs_index(mode)) {
+        // the edge index needs the settled thresholds (ensure_index waits for
+        // deferred weights), which may change the strategy
+        IMX_TRY(ensure_index(g));
+        mode = hook_mode(g, c->W);
+        if (needs_index(mode)) IMX_TRY(ensure_index(g));
+    }
+    // scan / pull with a deferred graph run on the speculative threshold
+    c->spec_used = g->thr_pending;
     if (mode == HOOK_SCAN) {
         IMX_TRY(run_scan(c, 1, nullptr));
         if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));
@@ -1163,8 +1174,23 @@ extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
     IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long) * 4, c->st));
     IMX_CUDA(cudaEventRecord(c->ev[0], c->st));
     if (g->m2 > 0) {
+        const int32_t t_spec = g->thr_u;
         IMX_TRY(run_sample_cc(c, st ? sc : nullptr, c->ev[1], c->ev[2]));
         IMX_TRY(run_compress(c, st ? sc + 1 : nullptr));
+        if (c->spec_used) {
+            // the propagate ran on the speculative uniform threshold while the
+            // weights were still uploading: wait for them (the device is busy
+            // meanwhile) and run again if the thresholds are not that one
+            IMX_TRY(graph_settle(g));
+            c->spec_used = false;
+            if (!g->uniform || g->thr_u != t_spec || g->hash_neg) {
+                c->gains_fused = false;
+                IMX_CUDA(cudaMemsetAsync(sc, 0, sizeof(unsigned long long) * 4, c->st));
+                IMX_CUDA(cudaEventRecord(c->ev[0], c->st));
+                IMX_TRY(run_sample_cc(c, st ? sc : nullptr, c->ev[1], c->ev[2]));
+                IMX_TRY(run_compress(c, st ? sc + 1 : nullptr));
+            }
+        }
     } else {
         IMX_TRY(run_init(c));
         IMX_CUDA(cudaEventRecord(c->ev[1], c->st));
@@ -1194,6 +1220,7 @@ extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
         push_stat(st, IMX_MODE_HOOK, changed, lsum);
     }
     if (verify || (st && changed > 0)) {
+        if (g->me) IMX_TRY(ensure_index(g));
         IMX_CUDA(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->st));
         if (g->me) {
             if (g->uniform)
@@ -1222,6 +1249,7 @@ extern "C" int imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2, f
     CTX_CHECK(c);
     c->gains_fused = false;
     if (reps < 1) { set_error("reps must be >= 1"); return IMX_EINVAL; }
+    IMX_TRY(graph_settle(c->g));
     uint4 *fb = nullptr;
     const int64_t fcnt = (int64_t(256) << 20) / 16;  // 256 MB > 126 MB L2
     if (flush_l2) IMX_CUDA(pool_alloc((void **)&fb, fcnt * 16, c->st));

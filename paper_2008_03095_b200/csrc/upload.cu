@@ -102,6 +102,9 @@ std::mutex g_upload_mu;   // one staged upload at a time (the pool and slots are
 
 // the source is page-locked host memory (cudaHostAlloc / registered): the
 // DMA reads it directly at the link rate (55 GB/s measured), no staging
+static bool host_pinned(const void *p);
+bool host_pinned_ptr(const void *p) { return host_pinned(p); }
+
 static bool host_pinned(const void *p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {

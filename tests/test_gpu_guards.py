@@ -111,3 +111,76 @@ def test_wide_compress_tile_with_fused_memo_is_capped(gpu, tile, monkeypatch):
     run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))
     assert run.seeds == z["seeds"].tolist()
     assert np.array_equal(run.selection.trace.array, z["trace"])
+
+
+# ---- deferred weights (large host CSRs; forced on small ones) ----------------
+
+def _deferred_graph(gpu, xadj, adj, w, pinned=False):
+    if pinned:
+        import torch
+
+        def pin(a):
+            t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+            out = t.numpy()
+            out[...] = a
+            return out
+        xadj, adj, w = pin(xadj), pin(adj), pin(w)
+    return gpu.Graph(xadj, adj, w, np.arange(len(xadj) - 1, dtype=np.int64))
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("case", ["uniform", "first_differs", "last_differs", "zero_first"])
+def test_deferred_weights_speculation(gpu, orc, case, pinned, monkeypatch):
+    """The weights of a large host CSR arrive after the propagate started on
+    the speculative threshold of weights[0]; whatever the weights turn out to
+    be, the result is the oracle's (the propagate reruns when the speculation
+    fails)."""
+    monkeypatch.setenv("IMX_LATE_WEIGHTS", "1")
+    z = load_golden("er_big_1000")
+    xadj, adj, _ = orc.csr_from_edges(int(z["n"]), z["edges"].astype(np.int64))
+    w = np.full(len(adj), 0.05)
+    rec = orc.reciprocal(xadj, adj)
+    if case == "first_differs":
+        w[[0, rec[0]]] = 0.3
+    elif case == "last_differs":
+        w[[-1, rec[-1]]] = 0.6
+    elif case == "zero_first":
+        w[[0, rec[0]]] = 0.0
+    g = _deferred_graph(gpu, xadj, adj, w, pinned)
+    run = gpu.run_fused(g, 5, num_simulations=40, master_seed=2)
+    want = orc.run_fused(xadj, adj, w, 5, 40, 2, nthreads=4)
+    assert np.array_equal(run.labels, want["labels"])
+    assert run.seeds == want["seeds"].tolist()
+    assert np.array_equal(run.selection.trace.array, want["trace"])
+    assert np.array_equal(gpu.slot_thresholds(g), want["thr"])
+
+
+def test_deferred_weights_asymmetric_csr_is_refused(gpu, monkeypatch):
+    monkeypatch.setenv("IMX_LATE_WEIGHTS", "1")
+    xadj = np.array([0, 2, 3, 4], np.int64)
+    adj = np.array([1, 2, 0, 1], np.int32)          # 0-2 has no 2-0
+    g = gpu.Graph(xadj, adj, np.full(4, 0.5), np.arange(3, dtype=np.int64))
+    with pytest.raises(Exception, match="symmetric"):
+        gpu.run_fused(g, 1, num_simulations=8)
+
+
+def test_deferred_weights_unsorted_row_is_refused(gpu, monkeypatch):
+    monkeypatch.setenv("IMX_LATE_WEIGHTS", "1")
+    xadj = np.array([0, 2, 3, 4], np.int64)
+    adj = np.array([2, 1, 0, 0], np.int32)          # row 0 not ascending
+    g = gpu.Graph(xadj, adj, np.full(4, 0.5), np.arange(3, dtype=np.int64))
+    with pytest.raises(Exception, match="symmetric"):
+        gpu.run_fused(g, 1, num_simulations=8)
+
+
+def test_deferred_weights_evaluate_and_reciprocal(gpu, orc, monkeypatch):
+    """Consumers of the lazily built reciprocal slots on a deferred graph."""
+    monkeypatch.setenv("IMX_LATE_WEIGHTS", "1")
+    z = load_golden("er_mid_300")
+    xadj, adj, _ = orc.csr_from_edges(int(z["n"]), z["edges"].astype(np.int64))
+    g = _deferred_graph(gpu, xadj, adj, z["weights"])
+    assert np.array_equal(g.reciprocal_slots, orc.reciprocal(xadj, adj))
+    from paper_2008_03095_b200.evaluation import evaluate_counts
+    got = evaluate_counts(g, np.array([1, 5, 9]), 300, 4)
+    want = orc.evaluate_counts(xadj, adj, z["weights"], np.array([1, 5, 9]), 300, 4, nthreads=2)
+    assert np.array_equal(got, want)

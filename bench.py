@@ -387,7 +387,8 @@ def run_ours(args, world, rank, local):
                      "random_access": random_access(summ, n * ((W + 3) // 4 * 4) * 4,
                                                     (res["hook_ms"] + res["compress_ms"]) / 1e3)})
         phases = {}
-        for ph, keys in (("init_ms", ("k_init", "k_pull<1")), ("hook_ms", ("k_seg", "cub::", "k_hook", "k_pull<2")),
+        for ph, keys in (("init_ms", ("k_init", "k_pull<1", "k_scan<1")),
+                         ("hook_ms", ("k_seg", "cub::", "k_hook", "k_pull<2", "k_scan<2")),
                          ("compress_ms", ("k_compress", "k_tile_copy", "k_gains_tile"))):
             bts = sum(v["dram_read_B"] + v["dram_write_B"] for k, v in summ["kernels"].items()
                       if k.startswith(keys))

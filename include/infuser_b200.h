@@ -39,9 +39,11 @@ extern "C" {
 #define IMX_ECONSTRAINT -5  /* documented limit violated -> ConstraintError   */
 #define IMX_EFORMAT    -6   /* malformed graph          -> GraphFormatError   */
 #define IMX_EINTERNAL  -7   /* failed self-check        -> AssertionError     */
+#define IMX_ENCCL      -8   /* NCCL error               -> RuntimeError       */
 
 typedef struct imx_graph imx_graph;   /* device-resident symmetric CSR        */
 typedef struct imx_ctx   imx_ctx;     /* device-resident labels/sizes/CELF    */
+typedef struct imx_comm  imx_comm;    /* int64 sums over the ranks of a run   */
 
 /* ---- library ----------------------------------------------------------- */
 const char *imx_last_error(void);
@@ -185,6 +187,36 @@ typedef int (*imx_allreduce_fn)(int64_t *buf, int64_t n, void *user);
 int  imx_celf_select_sharded(imx_ctx *c, int32_t k, imx_allreduce_fn allreduce,
                              void *user, int32_t *seeds_out, int64_t *gains_out,
                              int64_t *trace_len);
+/* ---- multi-rank data plane ----------------------------------
+ * Replaces the reference's thread-pool split of the lanes
+ * (propagation.py:209-216, 244-251) by ranks holding lane windows; their
+ * int64 partial sums (memo gains, CELF batch gains, commit self-checks) are
+ * added on the device, in place, on the context's stream.
+ *   NCCL:  rank 0 gets an id (imx_comm_unique_id), the launcher sends it to
+ *          every rank, each rank calls imx_comm_create (ncclCommInitRank;
+ *          libnccl.so.2 is opened at first use).
+ *   LOCAL: ranks as threads of one process (one GPU; tests): one group,
+ *          one imx_comm_create_local per rank.
+ * A context with an attached communicator (imx_ctx_attach_comm) allreduces
+ * the gains inside imx_memoize and runs imx_celf_select_comm.              */
+#define IMX_COMM_ID_BYTES 128
+int  imx_comm_unique_id(uint8_t *id_out /* IMX_COMM_ID_BYTES */);
+int  imx_comm_create(int32_t device, int32_t nranks, int32_t rank, const uint8_t *id,
+                     imx_comm **out);
+int  imx_local_group_create(int32_t nranks, void **group_out);
+void imx_local_group_destroy(void *group);
+int  imx_comm_create_local(void *group, int32_t rank, int32_t device, imx_comm **out);
+void imx_comm_destroy(imx_comm *comm);
+/* host buf[0, n) <- its sum over the ranks (through device memory)         */
+int  imx_comm_allreduce(imx_comm *comm, int64_t *buf, int64_t n);
+int  imx_ctx_attach_comm(imx_ctx *c, imx_comm *comm /* NULL detaches */);
+/* select_seeds over the lane shards of an attached communicator: the
+ * round-based CELF of imx_celf_select_sharded with every batch's partial
+ * gains and the commit self-check summed on the device (no host bounce of
+ * the data); every rank calls it.  Requires imx_memoize (which allreduced
+ * the gains) and imx_celf_reset(c, NULL).  selection.py:115-149.           */
+int  imx_celf_select_comm(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_t *gains_out,
+                          int64_t *trace_len);
 /* The trace of the last imx_celf_select: records of 5 int64
  * (vertex, stale_gain, fresh_gain, committed, seeds_before) -- TraceRecord,
  * selection.py:25-33 -- up to cap records.                                 */

@@ -25,6 +25,8 @@ IMX_ENODEV = -4
 IMX_ECONSTRAINT = -5
 IMX_EFORMAT = -6
 IMX_EINTERNAL = -7
+IMX_ENCCL = -8
+COMM_ID_BYTES = 128
 
 MODE_NAMES = {0: "init", 1: "hook", 2: "compress", 3: "verify"}
 
@@ -97,6 +99,15 @@ _SIGNATURES = {
     "imx_edge_list_copy": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "imx_edge_list_free": (None, [c_void_p]),
     "imx_get_timings": (c_i32, [c_void_p, P(Timings)]),
+    "imx_comm_unique_id": (c_i32, [c_void_p]),
+    "imx_comm_create": (c_i32, [c_i32, c_i32, c_i32, c_void_p, P(c_void_p)]),
+    "imx_local_group_create": (c_i32, [c_i32, P(c_void_p)]),
+    "imx_local_group_destroy": (None, [c_void_p]),
+    "imx_comm_create_local": (c_i32, [c_void_p, c_i32, c_i32, P(c_void_p)]),
+    "imx_comm_destroy": (None, [c_void_p]),
+    "imx_comm_allreduce": (c_i32, [c_void_p, c_void_p, c_i64]),
+    "imx_ctx_attach_comm": (c_i32, [c_void_p, c_void_p]),
+    "imx_celf_select_comm": (c_i32, [c_void_p, c_i32, c_void_p, c_void_p, P(c_i64)]),
     "imx_bench_propagate": (c_i32, [c_void_p, c_i32, c_i32, P(c_f32), P(c_f32), P(c_f32), P(c_f32)]),
 }
 
@@ -154,6 +165,8 @@ def check(rc: int) -> None:
         raise MemoryError(msg)
     if rc == IMX_EINTERNAL:
         raise AssertionError(msg)
+    if rc == IMX_ENCCL:
+        raise RuntimeError(msg)
     raise RuntimeError(msg or f"libinfuser_b200 error {rc}")
 
 

@@ -8,7 +8,7 @@ import sys
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-SOURCES = [PKG / "csrc" / f for f in ("graph.cu", "gen.cu", "ctx.cu", "propagate.cu", "scan.cu", "memo.cu", "celf.cu", "evaluation.cu", "upload.cu", "io.cpp")]
+SOURCES = [PKG / "csrc" / f for f in ("graph.cu", "gen.cu", "ctx.cu", "propagate.cu", "scan.cu", "memo.cu", "celf.cu", "comm.cu", "evaluation.cu", "upload.cu", "io.cpp")]
 HEADERS = list((PKG / "csrc").glob("*.cuh")) + [PKG.parent / "include" / "infuser_b200.h"]
 OUT = PKG / "lib" / "libinfuser_b200.so"
 
@@ -17,6 +17,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
     "-diag-suppress", "1444",
+    "-ldl",
 ]
 
 
@@ -54,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     OUT.parent.mkdir(parents=True, exist_ok=True)
     objdir = OUT.parent / "obj"
     objdir.mkdir(exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static", "-ldl")]
     hdr_t = max(p.stat().st_mtime for p in HEADERS)
     jobs = []
     for src in SOURCES:

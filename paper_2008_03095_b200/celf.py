@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["LocalComm", "TorchComm", "select_rounds", "lane_window", "gather_owned"]
+__all__ = ["LocalComm", "TorchComm", "NativeComm", "select_rounds", "lane_window", "gather_owned"]
 
 
 class LocalComm:
@@ -68,6 +68,101 @@ class TorchComm:
         v = np.zeros(self.size, np.int64)
         v[self.rank] = k
         return self.allreduce(v)
+
+
+class NativeComm:
+    """The library's device data plane for a sharded run (csrc/comm.cu):
+    partial sums are added on the GPU, in place, on the context's stream.
+
+    ``from_torch()`` builds an NCCL communicator over a torch.distributed
+    group (rank 0's NCCL unique id is broadcast through the group);
+    ``local_group(n)`` builds n ranks that are threads of this process on one
+    device (the test double: NCCL refuses two ranks per GPU)."""
+
+    _cache: dict = {}
+
+    def __init__(self, handle, rank: int, size: int, group=None):
+        self.handle = handle
+        self.rank = int(rank)
+        self.size = int(size)
+        self._group = group                  # a LOCAL group outlives its comms
+
+    @classmethod
+    def from_torch(cls, group=None, device: int | None = None) -> "NativeComm":
+        import ctypes
+        import torch.distributed as dist
+        from . import _lib
+        from ._lib import check
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+        if device is None:
+            device = _lib.current_device()
+        key = (id(group), rank, size, device)
+        if key in cls._cache:
+            return cls._cache[key]
+        idbuf = (ctypes.c_uint8 * _lib.COMM_ID_BYTES)()
+        if rank == 0:
+            check(_lib.load().imx_comm_unique_id(idbuf))
+        obj = [bytes(idbuf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        idbuf = (ctypes.c_uint8 * _lib.COMM_ID_BYTES).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        check(_lib.load().imx_comm_create(int(device), size, rank, idbuf, ctypes.byref(h)))
+        comm = cls(h, rank, size)
+        cls._cache[key] = comm
+        return comm
+
+    @classmethod
+    def local_group(cls, nranks: int, device: int = 0) -> list:
+        import ctypes
+        from . import _lib
+        from ._lib import check
+        lib = _lib.load()
+        grp = ctypes.c_void_p()
+        check(lib.imx_local_group_create(int(nranks), ctypes.byref(grp)))
+        owner = _LocalGroupOwner(grp)
+        out = []
+        for r in range(nranks):
+            h = ctypes.c_void_p()
+            check(lib.imx_comm_create_local(grp, r, int(device), ctypes.byref(h)))
+            out.append(cls(h, r, nranks, owner))
+        return out
+
+    def allreduce(self, x: np.ndarray) -> np.ndarray:
+        from . import _lib
+        from ._lib import check, ptr
+        a = np.ascontiguousarray(x, dtype=np.int64).copy()
+        check(_lib.load().imx_comm_allreduce(self.handle, ptr(a), len(a)))
+        return a
+
+    def allgather(self, x: np.ndarray) -> list:
+        """Through allreduce: every rank writes its slot of a zero buffer."""
+        x = np.ascontiguousarray(x, dtype=np.int64).reshape(-1)
+        cnt = np.zeros(self.size, np.int64)
+        cnt[self.rank] = len(x)
+        cnt = self.allreduce(cnt)
+        off = np.concatenate([[0], np.cumsum(cnt)])
+        buf = np.zeros(int(off[-1]), np.int64)
+        buf[off[self.rank]:off[self.rank + 1]] = x
+        buf = self.allreduce(buf)
+        return [buf[off[r]:off[r + 1]] for r in range(self.size)]
+
+    def close(self):
+        from . import _lib
+        h, self.handle = self.handle, None
+        if h:
+            _lib.load().imx_comm_destroy(h)
+
+
+class _LocalGroupOwner:
+    def __init__(self, grp):
+        self.grp = grp
+
+    def __del__(self):
+        try:
+            from . import _lib
+            _lib.load().imx_local_group_destroy(self.grp)
+        except Exception:
+            pass
 
 
 def gather_owned(ctx, comm) -> np.ndarray:

@@ -209,6 +209,22 @@ class DeviceContext:
         check(rc)
         return seeds, gains, _take_trace(self.handle)
 
+    def attach_comm(self, comm) -> None:
+        """Sum this context's partials (memo gains, CELF batches) over the
+        ranks of ``comm`` (a NativeComm) on the device."""
+        self._comm = comm                      # keeps the communicator alive
+        check(_lib.load().imx_ctx_attach_comm(self.handle, None if comm is None else comm.handle))
+
+    def celf_select_comm(self, k: int):
+        """CELF over the lane shards of the attached communicator:
+        (seeds, gains, trace (T, 5)); every rank calls it."""
+        lib = _lib.load()
+        seeds = np.empty(k, np.int32)
+        gains = np.empty(k, np.int64)
+        tl = ctypes.c_int64()
+        check(lib.imx_celf_select_comm(self.handle, int(k), ptr(seeds), ptr(gains), ctypes.byref(tl)))
+        return seeds, gains, _take_trace(self.handle)
+
     def per_sim(self) -> np.ndarray:
         out = np.empty(self.num_scored, np.int64)
         check(_lib.load().imx_per_sim(self.handle, ptr(out)))

@@ -175,20 +175,28 @@ static inline unsigned long long host_key(const imx_ctx *c, int64_t prio, int32_
 
 // evaluate order[lo, hi) of the current order; ids/keys of order[lo, min(hi+1, len))
 // and fresh gains of [lo, hi) land in the caller's host buffers.
+// With a communicator (comm), the batch's partial gains -- and, when pend is
+// given, one extra element: the previous commit's partial gain -- are summed
+// over the ranks on the device before the copy; *pend then holds the sum.
 static int celf_prefix(imx_ctx *c, int64_t lo, int64_t hi, int32_t *ids, unsigned long long *keys,
-                       int64_t *fresh) {
+                       int64_t *fresh, imx_comm *comm = nullptr, int64_t *pend = nullptr) {
     const int64_t len = c->olen;
     hi = std::min(hi, len);
     if (lo >= hi) return IMX_OK;
-    const int64_t base = c->ostart;
-    IMX_TRY(celf_eval_dev(c, c->oid[c->ocur] + base + lo, hi - lo, c->eval_out));
+    const int64_t base = c->ostart, cnt = hi - lo;
+    IMX_TRY(celf_eval_dev(c, c->oid[c->ocur] + base + lo, cnt, c->eval_out));
+    if (comm) {
+        if (pend) IMX_CUDA(cudaMemcpyAsync(c->eval_out + cnt, pend, sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+        IMX_TRY(comm_allreduce_i64(comm, c->eval_out, cnt + (pend ? 1 : 0), c->st));
+        if (pend) IMX_CUDA(cudaMemcpyAsync(pend, c->eval_out + cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+    }
     const int64_t fetch = std::min(hi + 1, len) - lo;
     IMX_CUDA(cudaMemcpyAsync(ids, c->oid[c->ocur] + base + lo, sizeof(int32_t) * fetch, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaMemcpyAsync(keys, c->okey[c->ocur] + base + lo, sizeof(unsigned long long) * fetch,
                              cudaMemcpyDeviceToHost, c->st));
-    IMX_CUDA(cudaMemcpyAsync(fresh, c->eval_out, sizeof(int64_t) * (hi - lo), cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaMemcpyAsync(fresh, c->eval_out, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
-    c->evaluated += hi - lo;
+    c->evaluated += cnt;
     return IMX_OK;
 }
 
@@ -363,8 +371,11 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
     unsigned long long *__restrict__ skey, int32_t *__restrict__ sid,
     int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
-    int32_t bpct, int32_t ngroup) {
+    int32_t bpct, int32_t ngroup, int64_t *__restrict__ xbuf, int64_t xcap) {
     cg::grid_group grid = cg::this_grid();
+    const bool xm = xcap > 0;                  // exchange mode (sharded run)
+    // a stop that waits for the host (done, trace full, error, big round)
+    if (xm && st->status != 0 && st->status != 5) return;
     __shared__ unsigned long long sback[kSmemBack];
     __shared__ unsigned long long gacc[8];
     if (threadIdx.x < 8) gacc[threadIdx.x] = 0;
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
         unsigned long long *okey = ocur ? okey1 : okey0;
         if (olen == 0) { status = 3; break; }
         // the previous round's gain was read by every block before its last barrier
-        if (gtid == 0 && t > st->t) *gain = 0;
+        if (gtid == 0 && (t > st->t || (xm && t > 0))) *gain = 0;
         unsigned long long bestkey;
         int64_t kr;
         if (t == 0) {
@@ -402,8 +413,48 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
         } else {
             int64_t lo = 0, hi = olen < batch0 ? olen : batch0;
             bestkey = 0;
+            bool resume = false;
+            if (xm && st->xphase == 1) {       // the exchanged batch of the paused launch
+                lo = st->xlo;
+                hi = st->xhi;
+                bestkey = st->xbest;
+                resume = true;
+            } else if (xm && hi - lo > xcap) {
+                hi = lo + xcap;
+            }
             for (;;) {
                 if (prof) ts = gtimer();
+                unsigned long long m;
+                if (resume) {
+                    // the sums over the ranks: into fresh[lo, hi), their max key
+                    resume = false;
+                    unsigned long long lmax = 0;
+                    for (int64_t i = lo + gtid; i < hi; i += gthreads) {
+                        const int64_t f = xbuf[i - lo];
+                        fresh[i] = f;
+                        const unsigned long long fk = ((unsigned long long)f << vb) |
+                                                      (unsigned long long)(vmask - (uint32_t)oid[ostart + i]);
+                        lmax = fk > lmax ? fk : lmax;
+                    }
+                    for (int o = 16; o; o >>= 1) {
+                        const unsigned long long y = __shfl_xor_sync(0xffffffffu, lmax, o);
+                        lmax = y > lmax ? y : lmax;
+                    }
+                    if ((threadIdx.x & 31) == 0 && lmax) atomicMax(&st->smax[3], lmax);
+                    bool bad = false;
+                    if (st->xpend && xbuf[xcap] != st->xpend_want) bad = true;   // commit self-check
+                    grid.sync();
+                    m = ld_relaxed64(&st->smax[3]);
+                    if (bad) {
+                        if (gtid == 0) { st->bad_v = st->xpend_v; st->bad_want = st->xpend_want; st->bad_got = xbuf[xcap]; }
+                        status = 3;
+                        break;
+                    }
+                    grid.sync();                 // every block read smax[3] and xpend
+                    if (gtid == 0) { st->smax[3] = 0; st->xpend = 0; st->xphase = 0; }
+                } else {
+                // slot (sstep+2)&3 was last read before the previous barrier
+                if (gtid == 0) st->smax[(sstep + 2) & 3] = 0;
                 // slot (sstep+2)&3 was last read before the previous barrier
                 if (gtid == 0) st->smax[(sstep + 2) & 3] = 0;
                 // huge batches (a round that refreshes most vertices): throughput
@@ -434,11 +485,14 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                                 if (!((wd[j] >> ((r + j) & 31)) & 1u)) acc += sz[j];
                         }
                         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                        if (wl == 0) fresh[i] = (int64_t)acc;
+                        if (wl == 0) {
+                            if (xm) xbuf[i - lo] = (int64_t)acc;
+                            else fresh[i] = (int64_t)acc;
+                        }
                         const unsigned long long fk = (acc << vb) | (unsigned long long)(vmask - (uint32_t)u);
                         wmax = fk > wmax ? fk : wmax;
                     }
-                    if (wl == 0 && wmax) atomicMax(&st->smax[sstep & 3], wmax);
+                    if (!xm && wl == 0 && wmax) atomicMax(&st->smax[sstep & 3], wmax);
                 }
                 // otherwise ngroup candidates per CTA at a time, 256/ngroup threads each
                 for (int64_t base = lo + (int64_t)blockIdx.x * ngroup; !wide && base < hi;
@@ -448,18 +502,32 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                     const int64_t f = group_eval<ENC>(L, C, cov, ld, ns, cw, i < hi ? (int64_t)oid[ostart + i] : -1,
                                                       threadIdx.x - g * gsz, gsz, gacc + g);
                     if (threadIdx.x == g * gsz && i < hi) {
-                        fresh[i] = f;
-                        atomicMax(&st->smax[sstep & 3], ((unsigned long long)f << vb) |
-                                                        (unsigned long long)(vmask - (uint32_t)oid[ostart + i]));
+                        if (xm) {
+                            xbuf[i - lo] = f;
+                        } else {
+                            fresh[i] = f;
+                            atomicMax(&st->smax[sstep & 3], ((unsigned long long)f << vb) |
+                                                            (unsigned long long)(vmask - (uint32_t)oid[ostart + i]));
+                        }
                     }
                     __syncthreads();
                     if (threadIdx.x < ngroup) gacc[threadIdx.x] = 0;
                     __syncthreads();
                 }
+                if (xm) {
+                    // pause: the host sums the partials over the ranks, relaunches
+                    if (gtid == 0) {
+                        st->xphase = 1; st->xlo = lo; st->xhi = hi; st->xbest = bestkey;
+                        xbuf[xcap] = st->xpend ? st->xpend_got : 0;
+                    }
+                    status = 5;
+                    break;
+                }
                 if (prof) { const unsigned long long x = gtimer(); pf[6] += x - ts; ts = x; }
                 grid.sync();
                 if (prof) { const unsigned long long x = gtimer(); pf[7] += x - ts; ts = x; pf[4]++; pf[5] += hi - lo; }
-                const unsigned long long m = ld_relaxed64(&st->smax[sstep & 3]);
+                m = ld_relaxed64(&st->smax[sstep & 3]);
+                }
                 ++sstep;
                 bestkey = m > bestkey ? m : bestkey;
                 const bool stop = hi >= olen || bestkey >= okey[ostart + hi];   // nothing unevaluated can win
@@ -471,10 +539,12 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                 // round 1 after the hub) would otherwise evaluate up to twice
                 // its refreshed prefix in the last doubling
                 int64_t step = batch0 > hi ? batch0 : hi;
-                const int64_t cap = (int64_t)gridDim.x * kStepPerCta;
+                int64_t cap = (int64_t)gridDim.x * kStepPerCta;
+                if (xm && cap > xcap) cap = xcap;          // a batch fits the exchange buffer
                 if (step > cap) step = cap;
                 hi = (olen - hi < step) ? olen : hi + step;
             }
+            if (status) break;                            // paused for an exchange, or a failed check
             // refreshed prefix: stale key >= best fresh key (keys sorted descending)
             kr = warp_count_above<true>(okey + ostart, hi, bestkey);
         }
@@ -539,9 +609,12 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
         grid.sync();
         PROF_MARK(1);
         // phase 2: self-check of the commit, then merge order[kr, olen) with
-        // the sorted refreshed vertices
+        // the sorted refreshed vertices (exchange mode: the gain is this
+        // rank's part; it is summed with the next batch and checked then)
         const unsigned long long got = *gain;
-        if ((int64_t)got != best_f) {
+        if (xm) {
+            if (gtid == 0) { st->xpend = 1; st->xpend_v = best_v; st->xpend_want = best_f; st->xpend_got = (int64_t)got; }
+        } else if ((int64_t)got != best_f) {
             if (gtid == 0) { st->bad_v = best_v; st->bad_want = best_f; st->bad_got = (int64_t)got; }
             status = 3;
             break;
@@ -600,6 +673,8 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
         st->ostart = ostart; st->olen = olen; st->ocur = ocur; st->t = t;
         st->trace_len = T; st->batch0 = batch0;
         st->status = status ? status : 1;
+        // done in exchange mode: the last commit's part goes out with one more exchange
+        if (xm && !status) xbuf[xcap] = st->xpend ? st->xpend_got : 0;
     }
 }
 
@@ -793,7 +868,8 @@ extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
 // decision, so all ranks take identical ones; the previous round's commit
 // self-check rides along as one extra element of the next batch.
 struct ShardReduce {
-    imx_allreduce_fn fn = nullptr;
+    imx_allreduce_fn fn = nullptr;    // host callback, or
+    imx_comm *comm = nullptr;         // the device data plane (comm.cu)
     void *user = nullptr;
     bool pending = false;           // a commit gain waits for its check
     int64_t pending_got = 0, pending_want = 0;
@@ -854,8 +930,19 @@ static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seed
         int64_t lo = 0, hi = std::min(len, batch0);
         for (;;) {
             if ((int64_t)ids.size() < hi + 1) { ids.resize(hi + 1); keys.resize(hi + 1); fr.resize(hi + 1); }
-            IMX_TRY(celf_prefix(c, lo, hi, ids.data() + lo, keys.data() + lo, fr.data() + lo));
-            if (sr) IMX_TRY(shard_reduce(*sr, fr.data() + lo, hi - lo));
+            if (sr && sr->comm) {
+                // partial gains summed on the device, the pending commit check with them
+                int64_t pend = sr->pending_got;
+                IMX_TRY(celf_prefix(c, lo, hi, ids.data() + lo, keys.data() + lo, fr.data() + lo, sr->comm,
+                                    sr->pending ? &pend : nullptr));
+                if (sr->pending) {
+                    IMX_TRY(shard_check(*sr, pend));
+                    sr->pending = false;
+                }
+            } else {
+                IMX_TRY(celf_prefix(c, lo, hi, ids.data() + lo, keys.data() + lo, fr.data() + lo));
+                if (sr) IMX_TRY(shard_reduce(*sr, fr.data() + lo, hi - lo));
+            }
             for (int64_t i = lo; i < hi; ++i)
                 if (best_v < 0 || key_le(fr[i], ids[i], best_f, best_v)) { best_f = fr[i]; best_v = ids[i]; }
             if (hi >= len) break;
@@ -960,8 +1047,9 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     int32_t ngroup = 1;
     if (const char *gv = getenv("IMX_CELF_GROUPS")) ngroup = std::min(8, std::max(1, atoi(gv)));
     while (ngroup & (ngroup - 1)) --ngroup;
+    int64_t *xbuf = nullptr, xcap = 0;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
-                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup};
+                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap};
     IMX_CUDA(cudaLaunchCooperativeKernel(fn, grid_cache[enc], 256, args, 0, c->st));
     count_launch(c);
     IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
@@ -1027,7 +1115,7 @@ __global__ void k_big_round_prep(const int32_t *__restrict__ oid, const unsigned
 }
 
 static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<int32_t> &seeds,
-                          std::vector<int64_t> &gains) {
+                          std::vector<int64_t> &gains, int64_t *partial_gain = nullptr) {
     const int64_t kr = c->big_kr;
     const unsigned long long bestkey = c->big_key;
     const uint64_t vmask = (c->vb >= 32) ? 0xffffffffull : ((1ull << c->vb) - 1);
@@ -1075,7 +1163,9 @@ static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<in
         unsigned long long got = 0;
         GB(cudaMemcpyAsync(&got, gain, sizeof got, cudaMemcpyDeviceToHost, st));
         GB(cudaStreamSynchronize(st));
-        if ((int64_t)got != best_f) {
+        if (partial_gain) {
+            *partial_gain = (int64_t)got;       // one rank's part: checked after the next exchange
+        } else if ((int64_t)got != best_f) {
             set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
                       (long long)got, (long long)best_f, best_v);
             rc = IMX_EINTERNAL;
@@ -1099,6 +1189,173 @@ done:
 // The whole CELF loop on one context (single-rank path): the persistent
 // cooperative kernel runs the rounds; a round it cannot hold (trace buffer
 // full, refreshed prefix larger than kMaxRank) is finished on the host.
+// Sharded CELF driven by the device (exchange mode).  The persistent kernel
+// runs the rounds exactly as on one rank but pauses after every evaluated
+// batch, leaving this rank's partial gains in the exchange buffer; the host
+// only enqueues the sum over the ranks (comm_allreduce_i64: ncclAllReduce in
+// place on the context stream) and the next launch, which resumes from the
+// summed batch.  No host decision and no host copy of the data sit inside
+// the loop: the host reads the kernel state with a lag of kXchgChunk
+// launches, and since every rank reaches the same state at the same launch,
+// all ranks enqueue the same collectives.  Launches after a stop are no-ops.
+constexpr int64_t kXchgCap = 16384;     // candidates per exchanged batch
+constexpr int kXchgChunk = 2;           // launches between state reads
+
+static int celf_select_xchg(imx_ctx *c, int32_t k, std::vector<int32_t> &seeds, std::vector<int64_t> &gains) {
+    const int64_t n = c->g->n;
+    // the buffers of celf_device_rounds
+    if (!c->cdev) {
+        IMX_CUDA(pool_alloc((void **)&c->cdev, sizeof(CelfDev), c->st));
+        IMX_CUDA(pool_alloc((void **)&c->skey, sizeof(unsigned long long) * kMaxRank, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->sid, sizeof(int32_t) * kMaxRank, c->st));
+        c->trace_cap = std::max<int64_t>(1 << 16, std::min<int64_t>(4 * n + 4096, 1 << 21));
+        if (const char *tc = getenv("IMX_CELF_TRACE_CAP")) c->trace_cap = std::max<int64_t>(8, atoll(tc));
+        IMX_CUDA(pool_alloc((void **)&c->dtrace, sizeof(int64_t) * 5 * c->trace_cap, c->st));
+    }
+    if (!c->dseeds || c->dseeds_cap < k) {
+        if (c->dseeds) { cudaFreeAsync(c->dseeds, c->st); cudaFreeAsync(c->dsgains, c->st); }
+        IMX_CUDA(pool_alloc((void **)&c->dseeds, sizeof(int32_t) * k, c->st));
+        IMX_CUDA(pool_alloc((void **)&c->dsgains, sizeof(int64_t) * k, c->st));
+        c->dseeds_cap = k;
+    }
+    int64_t xcap = kXchgCap;
+    if (const char *e = getenv("IMX_CELF_XCHG_CAP")) xcap = std::max<int64_t>(1, atoll(e));
+    int64_t *xbuf = nullptr;
+    IMX_CUDA(pool_alloc((void **)&xbuf, sizeof(int64_t) * (xcap + 1), c->st));
+    IMX_CUDA(cudaMemsetAsync(xbuf, 0, sizeof(int64_t) * (xcap + 1), c->st));
+    CelfDev h{};
+    h.ostart = c->ostart; h.olen = c->olen; h.ocur = c->ocur; h.t = 0;
+    h.batch0 = 64;
+    IMX_CUDA(cudaMemcpyAsync(c->cdev, &h, sizeof h, cudaMemcpyHostToDevice, c->st));
+    unsigned long long *gain = c->scratch + 7;
+    IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
+    const int enc = c->C ? 0 : 1;
+    void *fn = enc ? (void *)k_celf_rounds<true> : (void *)k_celf_rounds<false>;
+    if (!c->celf_grid[enc]) {
+        int per_sm = 0, sms = 0;
+        IMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+        IMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
+        int want = 4;
+        if (const char *b = getenv("IMX_CELF_BPSM")) want = std::max(1, atoi(b));
+        c->celf_grid[enc] = std::max(1, std::min(per_sm, want)) * sms;
+    }
+    int32_t kk = k, bpct = 150, ngroup = 1;
+    if (const char *b = getenv("IMX_CELF_BATCH_PCT")) bpct = std::max(1, atoi(b));
+    int vb = c->vb;
+    const uint32_t *L = c->L, *C = c->C;
+    uint32_t *cov = c->cov;
+    int64_t ld = c->ld;
+    int32_t ns = c->ns, cw = c->cw;
+    int64_t *per_sim = c->per_sim, *fresh = c->eval_out, *trace = c->dtrace, *sg = c->dsgains;
+    uint8_t *inS = c->inS;
+    int32_t *o0 = c->oid[0], *o1 = c->oid[1], *sid = c->sid, *sd = c->dseeds;
+    unsigned long long *k0 = c->okey[0], *k1 = c->okey[1], *skey = c->skey;
+    int64_t cap = c->trace_cap;
+    CelfDev *stp = c->cdev;
+    void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
+                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap};
+    CelfDev *snap = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int rc = IMX_OK;
+    auto drain_trace = [&](CelfDev &s) -> int {
+        if (s.trace_len) {
+            const int64_t base = c->trace_n;
+            IMX_TRY(trace_reserve(c, base + 5 * s.trace_len));
+            IMX_CUDA(cudaMemcpyAsync(c->trace + base, c->dtrace, sizeof(int64_t) * 5 * s.trace_len,
+                                     cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaStreamSynchronize(c->st));
+            c->trace_n = base + 5 * s.trace_len;
+            s.trace_len = 0;
+        }
+        return IMX_OK;
+    };
+    auto body = [&]() -> int {
+        IMX_CUDA(pinned_get((void **)&snap, sizeof(CelfDev) * 2));
+        for (auto &e : ev) IMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        int slot = 0, pending = -1;
+        for (;;) {
+            for (int j = 0; j < kXchgChunk; ++j) {
+                IMX_CUDA(cudaLaunchCooperativeKernel(fn, c->celf_grid[enc], 256, args, 0, c->st));
+                count_launch(c);
+                IMX_TRY(comm_allreduce_i64(c->comm, xbuf, xcap + 1, c->st));
+            }
+            IMX_CUDA(cudaMemcpyAsync(snap + slot, c->cdev, sizeof(CelfDev), cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaEventRecord(ev[slot], c->st));
+            const int look = pending;
+            pending = slot;
+            slot ^= 1;
+            if (look < 0) continue;
+            IMX_CUDA(cudaEventSynchronize(ev[look]));
+            const int32_t status = snap[look].status;
+            if (status == 0 || status == 5) continue;
+            // a stop: everything enqueued after it was a no-op; act on the current state
+            IMX_CUDA(cudaStreamSynchronize(c->st));
+            IMX_CUDA(cudaMemcpy(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost));
+            pending = -1;
+            if (h.status == 3) {
+                if (h.olen == 0) set_error("no candidate left at round %d", h.t);
+                else set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                               (long long)h.bad_got, (long long)h.bad_want, h.bad_v);
+                return IMX_EINTERNAL;
+            }
+            IMX_TRY(drain_trace(h));
+            if (h.status == 1) return IMX_OK;
+            // trace buffer full (2) or a round the kernel cannot hold (4)
+            c->ostart = h.ostart; c->olen = h.olen; c->ocur = h.ocur;
+            const bool oversized = h.big_kr > 0 && (h.status == 4 || h.big_kr + 1 > c->trace_cap);
+            if (h.t > 0 && oversized) {
+                c->big_key = h.big_key;
+                c->big_kr = h.big_kr;
+                int64_t b0 = h.batch0, part = 0;
+                std::vector<int32_t> sdum(k);
+                std::vector<int64_t> gdum(k);
+                IMX_TRY(celf_big_round(c, h.t, b0, sdum, gdum, &part));
+                IMX_CUDA(cudaMemcpyAsync(c->dseeds + h.t, &sdum[h.t], sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+                IMX_CUDA(cudaMemcpyAsync(c->dsgains + h.t, &gdum[h.t], sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+                h.xpend = 1; h.xpend_v = sdum[h.t]; h.xpend_want = gdum[h.t]; h.xpend_got = part;
+                h.ostart = c->ostart; h.olen = c->olen; h.ocur = c->ocur;
+                h.t += 1;
+                h.batch0 = b0;
+            }
+            h.status = 0;
+            h.xphase = 0;
+            h.big_kr = 0;
+            IMX_CUDA(cudaMemcpyAsync(c->cdev, &h, sizeof h, cudaMemcpyHostToDevice, c->st));
+            IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
+            IMX_CUDA(cudaStreamSynchronize(c->st));
+            if (h.t >= k) {        // the big round was the last one: finish like a done kernel
+                h.status = 1;
+                return IMX_OK;
+            }
+        }
+    };
+    rc = body();
+    if (rc == IMX_OK) {
+        // the last commit's part goes out with one more exchange
+        int64_t part = h.xpend ? h.xpend_got : 0;
+        IMX_CUDA(cudaMemcpyAsync(xbuf + xcap, &part, sizeof part, cudaMemcpyHostToDevice, c->st));
+        rc = comm_allreduce_i64(c->comm, xbuf + xcap, 1, c->st);
+        int64_t tot = 0;
+        if (rc == IMX_OK) {
+            IMX_CUDA(cudaMemcpyAsync(&tot, xbuf + xcap, sizeof tot, cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaMemcpyAsync(seeds.data(), c->dseeds, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaMemcpyAsync(gains.data(), c->dsgains, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, c->st));
+            IMX_CUDA(cudaStreamSynchronize(c->st));
+            if (h.xpend && tot != h.xpend_want) {
+                set_error("CELF self-check: committed gain %lld != evaluated %lld for vertex %d",
+                          (long long)tot, (long long)h.xpend_want, h.xpend_v);
+                rc = IMX_EINTERNAL;
+            }
+            c->ostart = h.ostart; c->olen = h.olen; c->ocur = h.ocur;
+        }
+    }
+    for (auto &e : ev) if (e) cudaEventDestroy(e);
+    if (snap) pinned_put(snap, sizeof(CelfDev) * 2);
+    cudaFreeAsync(xbuf, c->st);
+    c->evaluated = -1;
+    return rc;
+}
+
 extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_t *gains_out,
                                int64_t *trace_len) {
     CELF_CHECK(c);
@@ -1167,6 +1424,55 @@ extern "C" int imx_celf_select_sharded(imx_ctx *c, int32_t k, imx_allreduce_fn a
     if (sr.pending) {               // the last commit has no later batch to ride on
         int64_t g = sr.pending_got;
         if (allreduce(&g, 1, user) != 0) { set_error("allreduce callback failed"); return IMX_EINTERNAL; }
+        IMX_TRY(shard_check(sr, g));
+    }
+    if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
+    if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);
+    cudaEventRecord(c->ev[7], c->st);
+    cudaEventSynchronize(c->ev[7]);
+    cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
+    c->tm.celf_evaluations = c->evaluated;
+    if (trace_len) *trace_len = c->trace_n / 5;
+    return IMX_OK;
+}
+
+extern "C" int imx_celf_select_comm(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_t *gains_out,
+                                    int64_t *trace_len) {
+    CELF_CHECK(c);
+    const int64_t n = c->g->n;
+    if (!c->comm) { set_error("no communicator attached (imx_ctx_attach_comm)"); return IMX_EINVAL; }
+    if (k < 1 || k > n) { set_error("k=%d invalid for n=%lld", k, (long long)n); return IMX_ECONSTRAINT; }
+    if (c->olen != n) { set_error("CELF state already advanced (call imx_celf_reset)"); return IMX_EINVAL; }
+    cudaEventRecord(c->ev[6], c->st);
+    c->trace_n = 0;
+    c->evaluated = 0;
+    std::vector<int32_t> seeds(k);
+    std::vector<int64_t> gains(k);
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->dev);
+    const char *mode = getenv("IMX_CELF");
+    if (coop && !(mode && !strcmp(mode, "host"))) {
+        IMX_TRY(celf_select_xchg(c, k, seeds, gains));
+        if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
+        if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);
+        cudaEventRecord(c->ev[7], c->st);
+        cudaEventSynchronize(c->ev[7]);
+        cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
+        c->tm.celf_evaluations = c->evaluated;
+        if (trace_len) *trace_len = c->trace_n / 5;
+        return IMX_OK;
+    }
+    ShardReduce sr;
+    sr.comm = c->comm;
+    int64_t batch0 = 64;
+    for (int32_t t = 0; t < k; ++t) IMX_TRY(celf_host_round(c, t, batch0, seeds.data(), gains.data(), &sr));
+    if (sr.pending) {               // the last commit has no later batch to ride on
+        int64_t *d = c->eval_out;
+        IMX_CUDA(cudaMemcpyAsync(d, &sr.pending_got, sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+        IMX_TRY(comm_allreduce_i64(c->comm, d, 1, c->st));
+        int64_t g = 0;
+        IMX_CUDA(cudaMemcpyAsync(&g, d, sizeof g, cudaMemcpyDeviceToHost, c->st));
+        IMX_CUDA(cudaStreamSynchronize(c->st));
         IMX_TRY(shard_check(sr, g));
     }
     if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);

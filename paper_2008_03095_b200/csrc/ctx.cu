@@ -97,7 +97,7 @@ int ensure_celf_buffers(imx_ctx *c) {
         IMX_CUDA(pool_alloc((void **)&c->oid[b], sizeof(int32_t) * n, c->st));
         IMX_CUDA(pool_alloc((void **)&c->okey[b], sizeof(unsigned long long) * n, c->st));
     }
-    IMX_CUDA(pool_alloc((void **)&c->eval_out, sizeof(int64_t) * n, c->st));
+    IMX_CUDA(pool_alloc((void **)&c->eval_out, sizeof(int64_t) * (n + 1), c->st));   // + a commit check (celf_prefix)
     IMX_CUDA(pool_alloc((void **)&c->d_one, sizeof(int32_t) * 4, c->st));
     return IMX_OK;
 }

@@ -42,6 +42,16 @@ struct CelfDev {
     // refreshed prefix length (fresh[] holds the evaluated prefix)
     unsigned long long big_key;
     int64_t big_kr;
+    // exchange mode (sharded runs, celf_select_xchg): the kernel pauses with
+    // status 5 after writing an evaluated batch's partial gains to the
+    // exchange buffer; the host sums them over the ranks (NCCL) and
+    // relaunches, which resumes at xphase 1 with batch [xlo, xhi) and the
+    // round's best key so far.  A commit's partial gain rides in the
+    // exchange buffer's last slot and is checked at the next resume.
+    int32_t xphase, xpend, xpend_v, xpad;
+    int64_t xlo, xhi;
+    unsigned long long xbest;
+    int64_t xpend_want, xpend_got;
 };
 
 struct imx_ctx {
@@ -110,6 +120,8 @@ struct imx_ctx {
     // memoisation fused into the tiled compression (imx_set_fuse_memo): the
     // last propagate left the gains in `gains` (gains_fused)
     bool fuse_memo = false, gains_fused = false;
+    // ranks of a sharded run (comm.cu); NULL = single rank
+    imx_comm *comm = nullptr;
     // the last sampler launch used a deferred graph's speculative threshold
     bool spec_used = false;
     imx_timings tm{};
@@ -153,6 +165,8 @@ int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);
 // heavy-row slices of the graph for slice length T, cached on the graph (propagate.cu)
 int ensure_heavy(imx_ctx *c, int pass, int T);
+// buf[0, n) on the device <- its sum over the communicator's ranks (comm.cu)
+int comm_allreduce_i64(imx_comm *cm, int64_t *dbuf, int64_t n, cudaStream_t st);
 // the scan sampler (scan.cu)
 bool scan_eligible(const imx_graph *g);
 int run_scan(imx_ctx *c, int pass, unsigned long long *hooks);

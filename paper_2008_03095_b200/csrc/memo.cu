@@ -246,6 +246,8 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
         IMX_CHECK_LAUNCH();
         count_launch(c);
     }
+    // ranks of a sharded run: the gains are sums over every rank's lanes
+    if (c->comm && n) IMX_TRY(comm_allreduce_i64(c->comm, c->gains, n, c->st));
     IMX_CUDA(cudaEventRecord(c->ev[5], c->st));
     c->tm_pending |= 2;             // memoize_ms is read when the timings are asked for
     if (gains_out && n) {

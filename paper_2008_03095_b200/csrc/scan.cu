@@ -68,7 +68,8 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
     const int64_t items = HEAVY ? nhs : n;
     for (int c = 0; c < nchunks; ++c) {
         const int r0 = c * cw;
-        const int rwc = (int)min((int64_t)cw, ld - r0);  // row cells of this chunk (incl. padding)
+        // row cells of this chunk; the last chunk also covers the row padding
+        const int rwc = (int)(c == nchunks - 1 ? ld - r0 : min((int64_t)cw, ld - r0));
         __syncthreads();
         for (int i = threadIdx.x; i < cw; i += blockDim.x) {
             sxs[i] = xs_all[(int64_t)c * cw + i];

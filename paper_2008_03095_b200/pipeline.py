@@ -16,7 +16,7 @@ import time
 
 import numpy as np
 
-from .celf import LocalComm, TorchComm, lane_window
+from .celf import LocalComm, NativeComm, TorchComm, lane_window
 from .context import DeviceContext
 from .graph import Graph
 from .hashing import EdgeHashTable, SimulationRandoms, build_hash_table
@@ -89,6 +89,19 @@ def default_comm():
     return LocalComm()
 
 
+def native_comm(comm):
+    """The device data plane for comm: itself if it is a NativeComm, an NCCL
+    NativeComm for a torch.distributed NCCL group (IMX_NATIVE_COMM=0 keeps
+    the torch allreduces), else None (gloo / single rank)."""
+    import os
+    if isinstance(comm, NativeComm):
+        return comm
+    if (isinstance(comm, TorchComm) and comm.size > 1 and comm.device.type == "cuda"
+            and os.environ.get("IMX_NATIVE_COMM", "1") != "0"):
+        return NativeComm.from_torch(comm.group)
+    return None
+
+
 def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0,
               n_threads: int = 1, comm=None) -> FusedRun:
     """Select k seeds over ``num_simulations`` memoized implicit samples
@@ -108,8 +121,12 @@ def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0
     ctx, _ = propagated_context(g, table, randoms.values[a:b], scored, lane0=a, fuse_memo=True)
     timings["propagate"] = time.perf_counter() - t
 
+    native = native_comm(comm) if comm.size > 1 else None
     t = time.perf_counter()
     if comm.size == 1:
+        ctx.memoize(want_gains=False)
+    elif native is not None:
+        ctx.attach_comm(native)           # gains summed over the ranks on the device
         ctx.memoize(want_gains=False)
     else:
         gains = comm.allreduce(ctx.memoize(want_gains=True))
@@ -119,6 +136,9 @@ def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0
     if comm.size == 1:
         ctx.celf_reset(None)
         seeds, gains_k, trace = ctx.celf_select(k)
+    elif native is not None:
+        ctx.celf_reset(None)
+        seeds, gains_k, trace = ctx.celf_select_comm(k)
     else:
         ctx.celf_reset(gains)
         # the select_rounds loop, driven from native code with comm's allreduce

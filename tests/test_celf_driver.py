@@ -149,3 +149,13 @@ def test_two_rank_gloo_driver_matches_single_rank(tmp_path, name):
         for u in z["seeds"].tolist():
             want[labels[u, :R], np.arange(R)] = True
         assert np.array_equal(got["owned"], want)
+
+
+def test_native_comm_is_only_used_for_nccl_groups():
+    """run_fused's data-plane choice: gloo groups and single ranks keep the
+    host path; NativeComm objects are used as given."""
+    from paper_2008_03095_b200.celf import LocalComm, NativeComm
+    from paper_2008_03095_b200.pipeline import native_comm
+    assert native_comm(LocalComm()) is None
+    fake = NativeComm(None, 0, 2)
+    assert native_comm(fake) is fake

@@ -34,14 +34,14 @@ __device__ __forceinline__ unsigned long long pack_key(int64_t prio, uint32_t v,
 
 template <bool ENC>
 __device__ __forceinline__ uint32_t cell_size(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
-                                              int64_t ld, uint32_t u, uint32_t w, int r, uint32_t &label) {
+                                              const Lay &ld, uint32_t u, uint32_t w, int r, uint32_t &label) {
     if (ENC) {
         if (is_root(w)) { label = u; return (w & COUNT) + 1u; }
         label = w;
-        return (L[(int64_t)w * ld + r] & COUNT) + 1u;
+        return (L[ld.off(w, r)] & COUNT) + 1u;
     }
     label = w;
-    return C[(int64_t)w * ld + r];
+    return C[ld.off(w, r)];
 }
 
 // marginal_gain (selection.py:63-70): sum over scored lanes of the component
@@ -53,17 +53,17 @@ constexpr int kEvalThreads = 128;
 template <bool ENC>
 __global__ void __launch_bounds__(kEvalThreads) k_eval(const int32_t *__restrict__ cand, int64_t cnt,
                                                        const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
-                                                       const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
+                                                       const uint32_t *__restrict__ cov, Lay ld, int32_t ns,
                                                        int32_t cw, int64_t *__restrict__ out) {
     __shared__ unsigned long long part[kEvalThreads / 32];
     const int nqs = (ns + 3) >> 2;
     for (int64_t i = blockIdx.x; i < cnt; i += gridDim.x) {
         const int64_t u = cand[i];
         if (u < 0) { if (threadIdx.x == 0) out[i] = 0; continue; }
-        const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
+        const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
         unsigned long long acc = 0;
         for (int q = threadIdx.x; q < nqs; q += kEvalThreads) {
-            const uint4 l4 = row[q];
+            const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
             const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
             uint32_t wd[4], s[4];
             const int r = q << 2;
@@ -94,13 +94,13 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const int32_t *__restrict
 // per_sim[r] += its size when newly owned (K8, SelectionResult.spread_se)
 template <bool ENC>
 __global__ void k_commit(int32_t u, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
-                         uint32_t *__restrict__ cov, int64_t ld, int32_t ns, int32_t cw,
+                         uint32_t *__restrict__ cov, Lay ld, int32_t ns, int32_t cw,
                          int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
                          unsigned long long *__restrict__ gain) {
     unsigned long long acc = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ns; r += gridDim.x * blockDim.x) {
         uint32_t lab;
-        const uint32_t s = cell_size<ENC>(L, C, ld, (uint32_t)u, L[(int64_t)u * ld + r], r, lab);
+        const uint32_t s = cell_size<ENC>(L, C, ld, (uint32_t)u, L[ld.off(u, r)], r, lab);
         const uint32_t bit = 1u << (r & 31);
         const uint32_t old = atomicOr(cov + (int64_t)lab * cw + (r >> 5), bit);
         if (!(old & bit)) {
@@ -153,15 +153,15 @@ __global__ void k_merge(const int32_t *__restrict__ aid, const unsigned long lon
 
 static void launch_commit(imx_ctx *c, int32_t u, unsigned long long *gain) {
     const int blocks = grid_for(std::max(c->ns, 1));
-    if (c->C) k_commit<false><<<blocks, 256, 0, c->st>>>(u, c->L, c->C, c->cov, c->ld, c->ns, c->cw, c->per_sim, c->inS, gain);
-    else k_commit<true><<<blocks, 256, 0, c->st>>>(u, c->L, nullptr, c->cov, c->ld, c->ns, c->cw, c->per_sim, c->inS, gain);
+    if (c->C) k_commit<false><<<blocks, 256, 0, c->st>>>(u, c->L, c->C, c->cov, c->lay, c->ns, c->cw, c->per_sim, c->inS, gain);
+    else k_commit<true><<<blocks, 256, 0, c->st>>>(u, c->L, nullptr, c->cov, c->lay, c->ns, c->cw, c->per_sim, c->inS, gain);
 }
 
 static int celf_eval_dev(imx_ctx *c, const int32_t *dcand, int64_t cnt, int64_t *dout) {
     if (cnt <= 0) return IMX_OK;
     const int blocks = (int)std::min<int64_t>(cnt, 148 * 16);
-    if (c->C) k_eval<false><<<blocks, kEvalThreads, 0, c->st>>>(dcand, cnt, c->L, c->C, c->cov, c->ld, c->ns, c->cw, dout);
-    else k_eval<true><<<blocks, kEvalThreads, 0, c->st>>>(dcand, cnt, c->L, nullptr, c->cov, c->ld, c->ns, c->cw, dout);
+    if (c->C) k_eval<false><<<blocks, kEvalThreads, 0, c->st>>>(dcand, cnt, c->L, c->C, c->cov, c->lay, c->ns, c->cw, dout);
+    else k_eval<true><<<blocks, kEvalThreads, 0, c->st>>>(dcand, cnt, c->L, nullptr, c->cov, c->lay, c->ns, c->cw, dout);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;
@@ -246,13 +246,13 @@ constexpr int64_t kSmemBack = 2048;     // refreshed keys staged in shared memor
 
 template <bool ENC>
 __device__ __forceinline__ int64_t block_eval(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
-                                              const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
+                                              const uint32_t *__restrict__ cov, Lay ld, int32_t ns,
                                               int32_t cw, int64_t u, unsigned long long *red) {
     const int nqs = (ns + 3) >> 2;
-    const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
+    const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
     unsigned long long acc = 0;
     for (int q = threadIdx.x; q < nqs; q += blockDim.x) {
-        const uint4 l4 = row[q];
+        const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
         const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
         uint32_t wd[4], sz[4];
         const int r = q << 2;
@@ -320,15 +320,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Every thread of the CTA must call it (it has a CTA barrier).
 template <bool ENC>
 __device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
-                                              const uint32_t *__restrict__ cov, int64_t ld, int32_t ns,
+                                              const uint32_t *__restrict__ cov, Lay ld, int32_t ns,
                                               int32_t cw, int64_t u, int tid, int gsz,
                                               unsigned long long *acc_sh) {
     unsigned long long acc = 0;
     if (u >= 0) {
         const int nqs = (ns + 3) >> 2;
-        const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
+        const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
         for (int q = tid; q < nqs; q += gsz) {
-            const uint4 l4 = row[q];
+            const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
             const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
             uint32_t wd[4], sz[4];
             const int r = q << 2;
@@ -365,7 +365,7 @@ template <bool ENC>
 #endif
 __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
     int32_t k, int vb, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C, uint32_t *__restrict__ cov,
-    int64_t ld, int32_t ns, int32_t cw, int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
+    Lay ld, int32_t ns, int32_t cw, int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
     int32_t *oid0, int32_t *oid1, unsigned long long *okey0, unsigned long long *okey1,
     int64_t *__restrict__ fresh,
     unsigned long long *__restrict__ skey, int32_t *__restrict__ sid,
@@ -466,10 +466,10 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                     for (int64_t i = lo + (gtid >> 5); i < hi; i += gthreads >> 5) {
                         const int64_t u = oid[ostart + i];
                         const int nqs = (ns + 3) >> 2;
-                        const uint4 *row = reinterpret_cast<const uint4 *>(L + u * ld);
+                        const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
                         unsigned long long acc = 0;
                         for (int q = wl; q < nqs; q += 32) {
-                            const uint4 l4 = row[q];
+                            const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
                             const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
                             uint32_t wd[4], sz[4];
                             const int r = q << 2;
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
             unsigned long long acc = 0;
             for (int64_t r = gtid; r < ns; r += gthreads) {
                 uint32_t lab;
-                const uint32_t sz = cell_size<ENC>(L, C, ld, (uint32_t)best_v, L[(int64_t)best_v * ld + r], (int)r, lab);
+                const uint32_t sz = cell_size<ENC>(L, C, ld, (uint32_t)best_v, L[ld.off(best_v, r)], (int)r, lab);
                 const uint32_t bit = 1u << (r & 31);
                 const uint32_t old = atomicOr(cov + (int64_t)lab * cw + (r >> 5), bit);
                 if (!(old & bit)) { per_sim[r] += sz; acc += sz; }
@@ -1032,7 +1032,7 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     int vb = c->vb;
     const uint32_t *L = c->L, *C = c->C;
     uint32_t *cov = c->cov;
-    int64_t ld = c->ld;
+    Lay ld = c->lay;
     int32_t ns = c->ns, cw = c->cw;
     int64_t *per_sim = c->per_sim, *fresh = c->eval_out, *trace = c->dtrace, *sg = c->dsgains;
     uint8_t *inS = c->inS;
@@ -1244,7 +1244,7 @@ static int celf_select_xchg(imx_ctx *c, int32_t k, std::vector<int32_t> &seeds, 
     int vb = c->vb;
     const uint32_t *L = c->L, *C = c->C;
     uint32_t *cov = c->cov;
-    int64_t ld = c->ld;
+    Lay ld = c->lay;
     int32_t ns = c->ns, cw = c->cw;
     int64_t *per_sim = c->per_sim, *fresh = c->eval_out, *trace = c->dtrace, *sg = c->dsgains;
     uint8_t *inS = c->inS;

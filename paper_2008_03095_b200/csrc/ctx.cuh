@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "graph.cuh"
+#include "uf.cuh"
 
 // device-resident state of the persistent CELF kernel (celf.cu)
 struct CelfDev {
@@ -59,7 +60,10 @@ struct imx_ctx {
     int dev = 0;
     cudaStream_t st = nullptr;
     int32_t W = 0, ns = 0, cw = 0;
-    int64_t ld = 0;
+    int64_t ld = 0;               // cells per vertex: W rounded up to 4 (rows) or to the tile width
+    // layout of L (uf.cuh): rows, or lane tiles for very wide contexts
+    // (lay_native); caller labels (imx_load_labels) always use rows
+    imx::Lay lay, lay_native;
     int vb = 0;                   // bits for vertex ids in packed CELF keys
     int32_t *X = nullptr;         // [ld]
     uint32_t *L = nullptr;        // [n*ld]
@@ -172,14 +176,10 @@ bool scan_eligible(const imx_graph *g);
 int run_scan(imx_ctx *c, int pass, unsigned long long *hooks);
 // raw label-matrix passes shared with the evaluation worlds (evaluation.cu)
 int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
-// 16-byte quads of rows [0, n) from one row layout to another (row strides
-// sld, dld; nq quads per row): lane tiles in and out of contiguous scratch
-int launch_tile_copy(const uint32_t *src, int64_t sld, uint32_t *dst, int64_t dld, int64_t n, int nq,
-                     cudaStream_t st);
 int launch_gains_tile(const uint32_t *T, int64_t n, int64_t tld, int32_t ns_t, int first, int64_t *gains,
                       cudaStream_t st);
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
-                    cudaStream_t st, int *launches = nullptr);
+                    cudaStream_t st, int *launches = nullptr, int64_t window = 0);
 
 }  // namespace imx
 

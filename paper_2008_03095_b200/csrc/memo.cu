@@ -45,14 +45,13 @@ __global__ void __launch_bounds__(256) k_gains_caller(const uint32_t *__restrict
 // non-root cell's component is gathered from its root's cell through the
 // read-only path (L is not written during memoization, so hub rows stay in
 // L1/texture cache instead of hammering one L2 line).
-__global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ L, int64_t n, int64_t ld,
+__global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ L, int64_t n, Lay y,
                                                    int32_t ns, int64_t *__restrict__ gains) {
     const int lane = threadIdx.x & 31;
     const int nqs = (ns + 3) >> 2;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = wg; v < n; v += nw) {
-        const uint4 *Lr = reinterpret_cast<const uint4 *>(L + v * ld);
         unsigned long long acc = 0;
         // two quads per step, all eight root gathers issued before any is used
         for (int q0 = lane; q0 < nqs; q0 += 64) {
@@ -60,14 +59,15 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int q = q0 + 32 * h;
-                const uint4 l = q < nqs ? __ldg(Lr + q) : make_uint4(ROOT, ROOT, ROOT, ROOT);
+                const uint4 l = q < nqs ? __ldg(reinterpret_cast<const uint4 *>(L + y.off(v, 4 * q)))
+                                        : make_uint4(ROOT, ROOT, ROOT, ROOT);
                 w[4 * h] = l.x; w[4 * h + 1] = l.y; w[4 * h + 2] = l.z; w[4 * h + 3] = l.w;
             }
             uint32_t rw[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int r = ((q0 + 32 * (k >> 2)) << 2) + (k & 3);
-                rw[k] = is_root(w[k]) ? w[k] : __ldg(L + (int64_t)w[k] * ld + r);
+                rw[k] = is_root(w[k]) ? w[k] : __ldg(L + y.off(w[k], r));
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -92,9 +92,9 @@ __global__ void __launch_bounds__(256) k_gains_tile(const uint32_t *__restrict__
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < nthreads; i0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = i0 + threadIdx.x;
         const int64_t v = i >> 3;
-        const int q = (int)(i & 7);
         unsigned long long acc = 0;
-        if (i < nthreads && q < nqr && 4 * q < ns_t) {
+        // 8 threads per row, each a quad of lanes every 8 quads
+        for (int q = (int)(i & 7); i < nthreads && q < nqr && 4 * q < ns_t; q += 8) {
             const uint4 l = __ldg(reinterpret_cast<const uint4 *>(T + v * tld) + q);
             const uint32_t w[4] = {l.x, l.y, l.z, l.w};
             uint32_t rw[4];
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) k_gains_tile(const uint32_t *__restrict__
         }
 #pragma unroll
         for (int o = 4; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (i < nthreads && q == 0) gains[v] = (first ? 0 : gains[v]) + (int64_t)acc;
+        if (i < nthreads && (i & 7) == 0) gains[v] = (first ? 0 : gains[v]) + (int64_t)acc;
     }
 }
 
@@ -125,20 +125,20 @@ int launch_gains_tile(const uint32_t *T, int64_t n, int64_t tld, int32_t ns_t, i
 
 // decoded labels / sizes of rows [v0, v0+cnt), lanes [r0, r1) -> dense out
 template <bool ENC>
-__global__ void k_labels_window(const uint32_t *__restrict__ L, int64_t v0, int64_t cnt, int64_t ld,
+__global__ void k_labels_window(const uint32_t *__restrict__ L, int64_t v0, int64_t cnt, Lay y,
                                 int32_t r0, int32_t r1, int32_t *__restrict__ out) {
     const int w = r1 - r0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt * (int64_t)w;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = v0 + i / w;
         const int r = r0 + (int)(i % w);
-        const uint32_t x = L[v * ld + r];
+        const uint32_t x = L[y.off(v, r)];
         out[i] = (int32_t)(ENC ? label_of((uint32_t)v, x) : x);
     }
 }
 template <bool ENC>
 __global__ void k_sizes_window(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
-                               int64_t v0, int64_t cnt, int64_t ld, int32_t r0, int32_t r1,
+                               int64_t v0, int64_t cnt, Lay y, int32_t r0, int32_t r1,
                                int32_t *__restrict__ out) {
     const int w = r1 - r0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt * (int64_t)w;
@@ -146,10 +146,10 @@ __global__ void k_sizes_window(const uint32_t *__restrict__ L, const uint32_t *_
         const int64_t v = v0 + i / w;
         const int r = r0 + (int)(i % w);
         if (ENC) {
-            const uint32_t x = L[v * ld + r];
+            const uint32_t x = L[y.off(v, r)];
             out[i] = is_root(x) ? (int32_t)((x & COUNT) + 1u) : 0;
         } else {
-            out[i] = (int32_t)C[v * ld + r];
+            out[i] = (int32_t)C[y.off(v, r)];
         }
     }
 }
@@ -240,7 +240,7 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
                 // against 16; C3 0.443 -> 0.430 ms)
                 const char *mg = getenv("IMX_MEMO_BPSM");
                 const int gb = (int)std::min<int64_t>(ceil_div(n * 32, 256), 148 * (mg && atoi(mg) > 0 ? atoi(mg) : 64));
-                k_gains_enc<<<gb, 256, 0, c->st>>>(c->L, n, c->ld, c->ns, c->gains);
+                k_gains_enc<<<gb, 256, 0, c->st>>>(c->L, n, c->lay, c->ns, c->gains);
             }
         }
         IMX_CHECK_LAUNCH();
@@ -265,6 +265,7 @@ extern "C" int imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t 
     if (!labels && n) { set_error("labels is NULL"); return IMX_EINVAL; }
     if (ldh < c->W) { set_error("row stride %lld < width %d", (long long)ldh, c->W); return IMX_EINVAL; }
     if (!c->C) IMX_CUDA(pool_alloc((void **)&c->C, sizeof(uint32_t) * (size_t)(n > 0 ? n : 1) * c->ld, c->st));
+    c->lay = Lay(c->ld);             // caller labels and sizes: rows
     if (n) {
         const size_t bytes = sizeof(uint32_t) * (size_t)n * c->ld;
         IMX_CUDA(cudaMemsetAsync(c->L, 0, bytes, c->st));
@@ -306,8 +307,8 @@ extern "C" int imx_copy_labels(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out)
     if (c->g->n == 0 || r1 == r0) return IMX_OK;
     const bool enc = c->C == nullptr;
     return copy_window(c, r0, r1, out, [&](int64_t v0, int64_t cnt, int32_t *tmp) {
-        if (enc) k_labels_window<true><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, v0, cnt, c->ld, r0, r1, tmp);
-        else k_labels_window<false><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, v0, cnt, c->ld, r0, r1, tmp);
+        if (enc) k_labels_window<true><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, v0, cnt, c->lay, r0, r1, tmp);
+        else k_labels_window<false><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, v0, cnt, c->lay, r0, r1, tmp);
     });
 }
 
@@ -318,7 +319,7 @@ extern "C" int imx_copy_sizes(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out) 
     if (c->g->n == 0 || r1 == r0) return IMX_OK;
     const bool enc = c->C == nullptr;
     return copy_window(c, r0, r1, out, [&](int64_t v0, int64_t cnt, int32_t *tmp) {
-        if (enc) k_sizes_window<true><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, nullptr, v0, cnt, c->ld, r0, r1, tmp);
-        else k_sizes_window<false><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, c->C, v0, cnt, c->ld, r0, r1, tmp);
+        if (enc) k_sizes_window<true><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, nullptr, v0, cnt, c->lay, r0, r1, tmp);
+        else k_sizes_window<false><<<grid_for(cnt * (r1 - r0)), 256, 0, c->st>>>(c->L, c->C, v0, cnt, c->lay, r0, r1, tmp);
     });
 }

@@ -51,7 +51,7 @@ template <bool UNI>
 __global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
                                                           const int32_t *__restrict__ ET, int32_t tu, int64_t me,
                                                           const int32_t *__restrict__ X, int32_t W, int64_t ld,
-                                                          uint32_t *__restrict__ L,
+                                                          Lay y, uint32_t *__restrict__ L,
                                                           unsigned long long *__restrict__ hooks) {
     extern __shared__ int4 smem4[];
     int32_t *sX = reinterpret_cast<int32_t *>(smem4);
@@ -114,13 +114,13 @@ __global__ void __launch_bounds__(kHookWarps * 32) k_hook(const int2 *__restrict
                     const uint32_t a = qlo[qn + lane], bb = qhi[qn + lane];
                     const int r = (int)qr[qn + lane];
                     __syncwarp();
-                    nh += unite(L, ld, a, bb, r);
+                    nh += unite(L, y, a, bb, r);
                 }
             }
         }
     }
     __syncwarp();
-    if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
+    if (lane < qn) nh += unite(L, y, qlo[lane], qhi[lane], (int)qr[lane]);
     if (hooks) {
         for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
         if (lane == 0 && nh) atomicAdd(hooks, nh);
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(256) k_hook_enum(const int64_t *__restrict__ o
                                                    int64_t s_lo, int64_t s_hi, int segs_per_lane,
                                                    const int2 *__restrict__ E, const int32_t *__restrict__ EH,
                                                    const int32_t *__restrict__ ET, const int32_t *__restrict__ X,
-                                                   int64_t ld, uint32_t *__restrict__ L,
+                                                   Lay ld, uint32_t *__restrict__ L,
                                                    unsigned long long *__restrict__ hooks) {
     const int64_t jlo = off[s_lo], total = off[s_hi];
     const int lane = threadIdx.x & 31;
@@ -327,7 +327,7 @@ template <int PASS, bool UNI, int LPT, bool HEAVY>
 __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                                               const int32_t *__restrict__ hash, const int32_t *__restrict__ thr,
                                               int32_t tu, int64_t n, const int32_t *__restrict__ X, int32_t W,
-                                              int64_t ld, uint32_t *__restrict__ L,
+                                              int64_t ld, Lay y, uint32_t *__restrict__ L,
                                               unsigned long long *__restrict__ hooks,
                                               const uint8_t *__restrict__ heavy, const int32_t *__restrict__ hs_v,
                                               const int64_t *__restrict__ hs_a, const int32_t *__restrict__ hs_len,
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
 #pragma unroll
                 for (int k = 0; k < Q; ++k) {
                     const uint4 p4 = (active && r + 4 * k < ld)
-                        ? *(reinterpret_cast<const uint4 *>(L + v * ld + r) + k) : make_uint4(ROOT, ROOT, ROOT, ROOT);
+                        ? *reinterpret_cast<const uint4 *>(L + y.off(v, r + 4 * k)) : make_uint4(ROOT, ROOT, ROOT, ROOT);
                     par[4 * k] = p4.x; par[4 * k + 1] = p4.y; par[4 * k + 2] = p4.z; par[4 * k + 3] = p4.w;
                 }
             }
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
                         const uint32_t a2 = qlo[qn + lane], b2 = qhi[qn + lane];
                         const int rr = (int)qr[qn + lane];
                         __syncwarp();
-                        nh += unite(L, ld, a2, b2, rr);
+                        nh += unite(L, y, a2, b2, rr);
                     }
                 }
             }
@@ -467,19 +467,19 @@ __global__ void __launch_bounds__(256) k_pull(const int64_t *__restrict__ xadj, 
             if (PASS == 1 && active && HEAVY) {
 #pragma unroll
                 for (int k = 0; k < LPT; ++k)
-                    if (best[k] != ROOT) atomicMin(L + v * ld + r + k, best[k]);
+                    if (best[k] != ROOT) atomicMin(L + y.off(v, r + k), best[k]);
             } else if (PASS == 1 && active) {
 #pragma unroll
                 for (int k = 0; k < Q; ++k)
                     if (r + 4 * k < ld)
-                        *(reinterpret_cast<uint4 *>(L + v * ld + r) + k) =
+                        *reinterpret_cast<uint4 *>(L + y.off(v, r + 4 * k)) =
                             make_uint4(best[4 * k], best[4 * k + 1], best[4 * k + 2], best[4 * k + 3]);
             }
         }
     }
     if (PASS == 2) {
         __syncwarp();
-        if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
+        if (lane < qn) nh += unite(L, y, qlo[lane], qhi[lane], (int)qr[lane]);
     }
     if (hooks) {
         for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
 template <bool UNI>
 __global__ void k_verify_edges(const int2 *__restrict__ E, const int32_t *__restrict__ EH,
                                const int32_t *__restrict__ ET, int32_t tu, int64_t me,
-                               const int32_t *__restrict__ X, int32_t W, int64_t ld,
+                               const int32_t *__restrict__ X, int32_t W, Lay y,
                                const uint32_t *__restrict__ L, unsigned long long *__restrict__ bad) {
     const int lane = threadIdx.x & 31;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -673,34 +673,34 @@ __global__ void k_verify_edges(const int2 *__restrict__ E, const int32_t *__rest
         const int32_t t = UNI ? tu : ET[e];
         for (int r = lane; r < W; r += 32)
             if ((X[r] ^ h) < t &&
-                label_of(uv.x, L[(int64_t)uv.x * ld + r]) != label_of(uv.y, L[(int64_t)uv.y * ld + r]))
+                label_of(uv.x, L[y.off(uv.x, r)]) != label_of(uv.y, L[y.off(uv.y, r)]))
                 ++nb;
     }
     for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
     if (lane == 0 && nb) atomicAdd(bad, nb);
 }
-__global__ void k_verify_roots(const uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
+__global__ void k_verify_roots(const uint32_t *__restrict__ L, int64_t n, Lay y, int32_t W,
                                unsigned long long *__restrict__ bad) {
     unsigned long long nb = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / W;
         const int r = (int)(i - v * W);
-        const uint32_t w = L[v * ld + r];
-        if (!is_root(w) && (w >= (uint32_t)v || !is_root(L[(int64_t)w * ld + r]))) ++nb;
+        const uint32_t w = L[y.off(v, r)];
+        if (!is_root(w) && (w >= (uint32_t)v || !is_root(L[y.off(w, r)]))) ++nb;
     }
     for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
     if ((threadIdx.x & 31) == 0 && nb) atomicAdd(bad, nb);
 }
 
-__global__ void k_label_sum(const uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
+__global__ void k_label_sum(const uint32_t *__restrict__ L, int64_t n, Lay y, int32_t W,
                             unsigned long long *__restrict__ out) {
     unsigned long long s = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * (int64_t)W;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / W;
         const int r = (int)(i - v * W);
-        s += label_of((uint32_t)v, L[v * ld + r]);
+        s += label_of((uint32_t)v, L[y.off(v, r)]);
     }
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
@@ -740,7 +740,7 @@ static int run_hook_dense(imx_ctx *c, unsigned long long *hooks) {
     auto kern = g->uniform ? k_hook<true> : k_hook<false>;
     if (smem > 48 * 1024) IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<blocks, kHookWarps * 32, smem, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W,
-                                                    c->ld, c->L, hooks);
+                                                    c->ld, c->lay, c->L, hooks);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;
@@ -788,7 +788,7 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest
     for (int l0 = 0; l0 < c->W; l0 += lb) {
         const int l1 = std::min(c->W, l0 + lb);
         kern<<<blocks, 256, 0, c->st>>>(c->seg_off, c->seg_a, (int64_t)l0 * spl, (int64_t)l1 * spl, spl, g->E, g->EH,
-                                        g->ET, c->X, c->ld, c->L, hooks);
+                                        g->ET, c->X, c->lay, c->L, hooks);
         IMX_CHECK_LAUNCH();
         if (l1 < c->W) count_launch(c);
     }
@@ -921,7 +921,7 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     if (smem > 200 * 1024) { set_error("width %d too large for one context", c->W); return IMX_EINVAL; }
     const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * pull_bpsm());
     using KF = void (*)(const int64_t *, const int32_t *, const int32_t *, const int32_t *, int32_t, int64_t,
-                        const int32_t *, int32_t, int64_t, uint32_t *, unsigned long long *, const uint8_t *,
+                        const int32_t *, int32_t, int64_t, Lay, uint32_t *, unsigned long long *, const uint8_t *,
                         const int32_t *, const int64_t *, const int32_t *, int64_t);
     // [heavy][pass-1][uniform][wide]
     static const KF kerns[2][2][2][2] = {
@@ -935,7 +935,7 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
         if (smem > 48 * 1024)
             IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int hb = h ? (int)std::min<int64_t>(ceil_div(H.nhs, 8), 148 * pull_bpsm()) : blocks;
-        kern<<<hb, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld, c->L, hooks,
+        kern<<<hb, 256, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr, g->thr_u, n, c->X, c->W, c->ld, c->lay, c->L, hooks,
                                        H.nhs > 0 ? H.heavy : nullptr, H.hs_v, H.hs_a, H.hs_len, H.nhs);
         IMX_CHECK_LAUNCH();
         count_launch(c);
@@ -1020,9 +1020,9 @@ static int64_t compress_window(int64_t n, int64_t ld) {
 }
 
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
-                    cudaStream_t st, int *launches) {
+                    cudaStream_t st, int *launches, int64_t window) {
     if (n == 0) return IMX_OK;
-    const int64_t win = compress_window(n, ld);
+    const int64_t win = window > 0 ? window : compress_window(n, ld);
     if (launches) *launches = (int)ceil_div(W, win);
     for (int64_t l0 = 0; l0 < W; l0 += win) {
         const int32_t wl = (int32_t)std::min<int64_t>(win, W - l0);
@@ -1049,91 +1049,53 @@ int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long
     return IMX_OK;
 }
 
-// 16-byte quads of rows [0, n) between two label layouts (row strides sld,
-// dld; nq quads per row)
-__global__ void k_tile_copy(const uint32_t *__restrict__ src, int64_t sld, uint32_t *__restrict__ dst, int64_t dld,
-                            int64_t n, int nq) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * nq;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / nq;
-        const int q = (int)(i - v * nq);
-        reinterpret_cast<uint4 *>(dst + v * dld)[q] = reinterpret_cast<const uint4 *>(src + v * sld)[q];
-    }
-}
-
-// tile copies: IMX_TILE_COPY_BPSM blocks per SM (default 64: C5 compress 59.3 -> 58.5 ms against 16)
-static int tile_copy_grid(int64_t work) {
-    const char *e = getenv("IMX_TILE_COPY_BPSM");
-    const int64_t bpsm = e && atoi(e) > 0 ? atoi(e) : 64;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 148 * bpsm));
-}
-
-int launch_tile_copy(const uint32_t *src, int64_t sld, uint32_t *dst, int64_t dld, int64_t n, int nq,
-                     cudaStream_t st) {
-    k_tile_copy<<<tile_copy_grid(n * nq), 256, 0, st>>>(src, sld, dst, dld, n, nq);
-    IMX_CHECK_LAUNCH();
-    note_launch();
-    return IMX_OK;
-}
-
-// Lanes per compression tile: a very wide label matrix of a graph whose
-// 32-lane slice is L2-sized is compressed in tiles of 32 lanes copied to a
-// contiguous [n][32] scratch (one 128-byte line per row), so the parent reads
-// and root-count atomics of a tile hit L2.  Measured: C5 (n=1M, 8192 lanes)
-// 73 -> 60 ms; C3 / C4 (fewer non-roots per row, or n*128 B >> L2) are
-// slower tiled, so they stay in place.  0 = compress in place.
-static int64_t compress_tile(int64_t n, int64_t ld, bool fuse_memo) {
-    if (const char *e = getenv("IMX_COMPRESS_TILE")) {
-        const int64_t t = atoll(e);
-        // k_gains_tile sums 32 lanes (8 quads) per row: the fused memo caps the tile
-        const int64_t cap = fuse_memo ? std::min<int64_t>(ld, 32) : ld;
-        return t > 0 ? std::min<int64_t>(cap, std::max<int64_t>(4, t / 4 * 4)) : 0;
-    }
-    if (n > ((int64_t)1 << 20) || (double)n * ld * 4 < 8e9) return 0;
-    return 32;
-}
-
+// Compression of the whole matrix.  Lane-tiled contexts (ctx.cu) compress
+// tile by tile in place: a tile is a contiguous [n][tl] block, so its walks
+// and root-count atomics stay in L2 (C5: 128 MB tiles of 32 lanes), and the
+// memo fused into the propagate (imx_set_fuse_memo) sums each tile's gains
+// while it is still on chip.
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
-    const int64_t tw = compress_tile(n, c->ld, c->fuse_memo && !c->C);
-    if (!tw) {
+    if (!c->lay.tiled()) {
         int k = 0;
         IMX_TRY(launch_compress(c->L, n, c->ld, c->W, nonroot, c->st, &k));
         c->tm.kernel_launches += k;
         return IMX_OK;
     }
-    uint32_t *T = nullptr;
-    IMX_CUDA(pool_alloc((void **)&T, sizeof(uint32_t) * n * tw, c->st));
-    int rc = IMX_OK;
-    for (int64_t l0 = 0; l0 < c->W && rc == IMX_OK; l0 += tw) {
-        const int32_t wl = (int32_t)std::min<int64_t>(tw, c->W - l0);
-        const int64_t tld = (wl + 3) / 4 * 4;
-        const int nq = (int)(tld >> 2);
-        k_tile_copy<<<tile_copy_grid(n * nq), 256, 0, c->st>>>(c->L + l0, c->ld, T, tld, n, nq);
-        int k = 0;
-        rc = launch_compress(T, n, tld, wl, nonroot, c->st, &k);
-        if (rc == IMX_OK && c->fuse_memo && !c->C) {
-            // the memo's gains over this tile's scored lanes, while it is in L2
-            const int32_t ns_t = (int32_t)std::max<int64_t>(0, std::min<int64_t>(wl, c->ns - l0));
-            if (l0 == 0 || ns_t > 0) rc = launch_gains_tile(T, n, tld, ns_t, l0 == 0, c->gains, c->st);
-            c->tm.kernel_launches++;
+    // each tile in windows of 32 lanes: a window is one 128-byte line per row,
+    // so its walks stay in L2 (C5, 64-lane tiles: compress 40.1 -> 33.2 ms; the
+    // tiles themselves are 64 lanes wide because the pass-1 row stores lose
+    // DRAM locality at 128 bytes per tile: 10.8 vs 20.1 ms at 32)
+    const int64_t tl = c->lay.ld, tiles = c->ld / tl;
+    const int64_t win = std::min<int64_t>(tl, 32);
+    const bool fuse = c->fuse_memo && !c->C;
+    for (int64_t t = 0; t < tiles; ++t) {
+        uint32_t *T = c->L + t * c->lay.tstride;
+        for (int64_t w0 = 0; w0 < tl; w0 += win) {
+            const int64_t l0 = t * tl + w0;
+            if (l0 >= c->W) break;
+            const int32_t wl = (int32_t)std::min<int64_t>(win, c->W - l0);
+            int k = 0;
+            IMX_TRY(launch_compress(T + w0, n, tl, wl, nonroot, c->st, &k, win));
+            c->tm.kernel_launches += k;
+            if (fuse) {
+                // the memo's gains over this window's scored lanes, while it is in L2
+                const int32_t ns_w = (int32_t)std::max<int64_t>(0, std::min<int64_t>(wl, c->ns - l0));
+                if (l0 == 0 || ns_w > 0) IMX_TRY(launch_gains_tile(T + w0, n, tl, ns_w, l0 == 0, c->gains, c->st));
+                c->tm.kernel_launches++;
+            }
         }
-        k_tile_copy<<<tile_copy_grid(n * nq), 256, 0, c->st>>>(T, tld, c->L + l0, c->ld, n, nq);
-        count_launch(c, 2);
-        c->tm.kernel_launches += k;
     }
-    cudaFreeAsync(T, c->st);
-    IMX_CHECK_LAUNCH();
-    if (rc == IMX_OK && c->fuse_memo && !c->C) c->gains_fused = true;
-    return rc;
+    if (fuse) c->gains_fused = true;
+    return IMX_OK;
 }
 
 static int label_sum(imx_ctx *c, int64_t *out) {
     const int64_t n = c->g->n;
     IMX_CUDA(cudaMemsetAsync(c->scratch + 4, 0, sizeof(unsigned long long), c->st));
     if (n) {
-        k_label_sum<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->ld, c->W, c->scratch + 4);
+        k_label_sum<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->lay, c->W, c->scratch + 4);
         IMX_CHECK_LAUNCH();
         count_launch(c);
     }
@@ -1167,6 +1129,8 @@ extern "C" int imx_set_fuse_memo(imx_ctx *c, int32_t on) {
 extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
     CTX_CHECK(c);
     c->gains_fused = false;
+    if (c->C) { cudaFreeAsync(c->C, c->st); c->C = nullptr; }   // back to encoded mode
+    c->lay = c->lay_native;
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (st) st->sweeps = 0;
@@ -1224,12 +1188,12 @@ extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
         IMX_CUDA(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->st));
         if (g->me) {
             if (g->uniform)
-                k_verify_edges<true><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->ld, c->L, sc + 2);
+                k_verify_edges<true><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->lay, c->L, sc + 2);
             else
-                k_verify_edges<false><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->ld, c->L, sc + 2);
+                k_verify_edges<false><<<grid_for(g->me * 32), 256, 0, c->st>>>(g->E, g->EH, g->ET, g->thr_u, g->me, c->X, c->W, c->lay, c->L, sc + 2);
             IMX_CHECK_LAUNCH();
         }
-        k_verify_roots<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->ld, c->W, sc + 2);
+        k_verify_roots<<<grid_for(n * c->W), 256, 0, c->st>>>(c->L, n, c->lay, c->W, sc + 2);
         IMX_CHECK_LAUNCH();
         count_launch(c, 2);
         unsigned long long bad = 0;
@@ -1256,6 +1220,7 @@ extern "C" int imx_bench_propagate(imx_ctx *c, int32_t reps, int32_t flush_l2, f
     std::vector<cudaEvent_t> ev(4 * reps);
     for (auto &e : ev) IMX_CUDA(cudaEventCreate(&e));
     if (c->C) { cudaFreeAsync(c->C, c->st); c->C = nullptr; }
+    c->lay = c->lay_native;
     for (int i = 0; i < reps; ++i) {
         if (fb) k_flush<<<148 * 8, 256, 0, c->st>>>(fb, fcnt, (uint32_t)i);
         IMX_CUDA(cudaEventRecord(ev[4 * i], c->st));

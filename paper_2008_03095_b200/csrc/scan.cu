@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kScanWarps * 32)
 k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const int32_t *__restrict__ hash,
        int32_t t, int kb, int nb, int cw, int nchunks, const int32_t *__restrict__ xs_all,
        const uint16_t *__restrict__ perm_all, const int32_t *__restrict__ boff_all, int64_t n, int32_t W,
-       int64_t ld, uint32_t *__restrict__ L, unsigned long long *__restrict__ hooks,
+       int64_t ld, Lay y, uint32_t *__restrict__ L, unsigned long long *__restrict__ hooks,
        const uint8_t *__restrict__ heavy, const int32_t *__restrict__ hs_v, const int64_t *__restrict__ hs_a,
        const int32_t *__restrict__ hs_len, int64_t nhs, unsigned long long *__restrict__ ctr, int grab) {
     extern __shared__ int4 smem4[];
@@ -135,10 +135,9 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                     bounds(k, v, s0, s1);
                     batch(s0, s1, v, bu0, bh0);
                 }
-                uint32_t *Lv = L + v * ld + r0;
                 if (PASS == 1 && !HEAVY) {                 // the row starts as all roots
-                    uint4 *o4 = reinterpret_cast<uint4 *>(Lv);
-                    for (int q = lane; q < (rwc >> 2); q += 32) o4[q] = make_uint4(ROOT, ROOT, ROOT, ROOT);
+                    for (int q = lane; q < (rwc >> 2); q += 32)
+                        *reinterpret_cast<uint4 *>(L + y.off(v, r0 + 4 * q)) = make_uint4(ROOT, ROOT, ROOT, ROOT);
                 }
                 // any smaller neighbour (rows ascend: the first slot says)
                 const bool has = s0 < s1 && __shfl_sync(FULL, bu0, 0) < (uint32_t)v;
@@ -167,14 +166,14 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                                 // ascending slots: the first live neighbour is the smallest
                                 if (live && !flag[p]) {
                                     flag[p] = 1;
-                                    if (HEAVY) atomicMin(Lv + p, u);
-                                    else Lv[p] = u;
+                                    if (HEAVY) atomicMin(L + y.off(v, r0 + p), u);
+                                    else L[y.off(v, r0 + p)] = u;
                                 }
                             } else {
                                 bool un = false;
                                 if (live) {
                                     if (HEAVY) {
-                                        un = ld_relaxed(Lv + p) != u;   // all but the forest edge
+                                        un = ld_relaxed(L + y.off(v, r0 + p)) != u;   // all but the forest edge
                                     } else {
                                         un = flag[p] != 0;              // all but the first live neighbour
                                         flag[p] = 1;
@@ -194,7 +193,7 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                                     const uint32_t a2 = qlo[qn + lane], b2 = qhi[qn + lane];
                                     const int rr = (int)qr[qn + lane];
                                     __syncwarp();
-                                    nh += unite(L, ld, a2, b2, rr);
+                                    nh += unite(L, y, a2, b2, rr);
                                 }
                             }
                         }
@@ -209,7 +208,7 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
     }
     if (PASS == 2) {
         __syncwarp();
-        if (lane < qn) nh += unite(L, ld, qlo[lane], qhi[lane], (int)qr[lane]);
+        if (lane < qn) nh += unite(L, y, qlo[lane], qhi[lane], (int)qr[lane]);
     }
     if (hooks) {
         for (int o = 16; o; o >>= 1) nh += __shfl_xor_sync(FULL, nh, o);
@@ -301,7 +300,7 @@ int run_scan(imx_ctx *c, int pass, unsigned long long *hooks) {
     const size_t smem = (size_t)kScanWarps * cw + (pass == 2 ? sizeof(uint32_t) * kScanWarps * 3 * kScanQ : 0) +
                         sizeof(int32_t) * cw + sizeof(int32_t) * (nb + 1) + sizeof(uint16_t) * cw;
     using KF = void (*)(const int64_t *, const int32_t *, const int32_t *, int32_t, int, int, int, int,
-                        const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, uint32_t *,
+                        const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, Lay, uint32_t *,
                         unsigned long long *, const uint8_t *, const int32_t *, const int64_t *, const int32_t *,
                         int64_t, unsigned long long *, int);
     static const KF kerns[2][2] = {{k_scan<1, false>, k_scan<1, true>}, {k_scan<2, false>, k_scan<2, true>}};
@@ -318,7 +317,7 @@ int run_scan(imx_ctx *c, int pass, unsigned long long *hooks) {
         IMX_CUDA(cudaMemsetAsync(c->scan_ctr, 0, sizeof(unsigned long long) * c->scan_nchunks, c->st));
         kern<<<blocks, kScanWarps * 32, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr_u, c->scan_kb, nb, cw,
                                                        c->scan_nchunks, c->scan_xs, c->scan_perm, c->scan_boff, n,
-                                                       c->W, c->ld, c->L, pass == 2 ? hooks : nullptr,
+                                                       c->W, c->ld, c->lay, c->L, pass == 2 ? hooks : nullptr,
                                                        H.nhs > 0 ? H.heavy : nullptr, H.hs_v, H.hs_a, H.hs_len,
                                                        H.nhs, c->scan_ctr, grab);
         IMX_CHECK_LAUNCH();

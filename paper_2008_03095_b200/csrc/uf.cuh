@@ -13,8 +13,37 @@ namespace imx {
 constexpr uint32_t ROOT = 0x80000000u;
 constexpr uint32_t COUNT = 0x7FFFFFFFu;
 
-__device__ __forceinline__ uint32_t *cell(uint32_t *L, int64_t ld, uint32_t v, int r) {
-    return L + (int64_t)v * ld + r;
+// Layout of a label matrix.  Rows (the default): cell (v, r) at v * ld + r,
+// simulation-contiguous (propagation.py:1-8).  Lane tiles (very wide
+// contexts, ctx.cu): tiles of tl = 2^tsh lanes, each tile a contiguous
+// [n][tl] block, so the walks of one tile's compression stay in L2 without a
+// copy: cell (v, r) at (r >> tsh) * tstride + v * tl + (r & tmask).  An
+// int64 row length converts to the row layout, so code that only ever sees
+// rows keeps passing ld.
+struct Lay {
+    int64_t ld;          // cells per contiguous row run: the row, or tl
+    int64_t tstride;     // cells per tile (0: rows)
+    int tsh;             // tile of lane r = r >> tsh (31: rows)
+    uint32_t tmask;
+    __host__ __device__ Lay(int64_t row_ld = 0) : ld(row_ld), tstride(0), tsh(31), tmask(0x7fffffffu) {}
+    __host__ __device__ static Lay tiles(int64_t n, int shift) {
+        Lay y((int64_t)1 << shift);
+        y.tstride = n << shift;
+        y.tsh = shift;
+        y.tmask = (1u << shift) - 1u;
+        return y;
+    }
+    __host__ __device__ bool tiled() const { return tstride != 0; }
+    __host__ __device__ int64_t off(int64_t v, int r) const {
+        return (int64_t)(r >> tsh) * tstride + v * ld + (int64_t)(r & tmask);
+    }
+};
+
+__device__ __forceinline__ uint32_t *cell(uint32_t *L, const Lay &y, uint32_t v, int r) {
+    return L + y.off(v, r);
+}
+__device__ __forceinline__ const uint32_t *cell(const uint32_t *L, const Lay &y, uint32_t v, int r) {
+    return L + y.off(v, r);
 }
 __device__ __forceinline__ bool is_root(uint32_t w) { return (w & ROOT) != 0; }
 // label of vertex v from its (compressed) cell word
@@ -34,7 +63,7 @@ __device__ __forceinline__ uint32_t label_of(uint32_t v, uint32_t w) { return is
 #endif
 constexpr uint32_t kHotHook = IMX_HOT_HOOK;
 
-__device__ __forceinline__ uint32_t ld_hook(uint32_t *L, int64_t ld, uint32_t v, int r) {
+__device__ __forceinline__ uint32_t ld_hook(uint32_t *L, const Lay &ld, uint32_t v, int r) {
     if (kHotHook > 0 && v < kHotHook) {
         if (v == 0) return ROOT;
         uint32_t w;
@@ -48,7 +77,7 @@ __device__ __forceinline__ uint32_t ld_hook(uint32_t *L, int64_t ld, uint32_t v,
 // splitting: every visited node is re-pointed at its grandparent (benign
 // races -- any value ever stored in a cell is an ancestor in the same tree).
 // On entry wa = L[xa], wb = L[xb]; on exit xa, xb are roots.
-__device__ __forceinline__ void find2(uint32_t *L, int64_t ld, int r, uint32_t &xa, uint32_t wa,
+__device__ __forceinline__ void find2(uint32_t *L, const Lay &ld, int r, uint32_t &xa, uint32_t wa,
                                       uint32_t &xb, uint32_t wb) {
     for (;;) {
         const bool da = is_root(wa), db = is_root(wb);
@@ -72,7 +101,7 @@ __device__ __forceinline__ void find2(uint32_t *L, int64_t ld, int r, uint32_t &
 // Union of a and b in lane r: CAS-hook the larger root under the smaller.
 // During hooking every root cell is exactly ROOT (member counts are only
 // written by the compress pass).  Returns 1 when a hook happened.
-__device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32_t b, int r) {
+__device__ __forceinline__ int unite(uint32_t *L, const Lay &ld, uint32_t a, uint32_t b, int r) {
     uint32_t wa = ld_hook(L, ld, a, r);
     uint32_t wb = ld_hook(L, ld, b, r);
     find2(L, ld, r, a, wa, b, wb);
@@ -90,7 +119,7 @@ __device__ __forceinline__ int unite(uint32_t *L, int64_t ld, uint32_t a, uint32
 // Root of x given its parent p (p = L[x], not a root word); re-points each
 // visited node at its grandparent with atomicMin, so it is safe against the
 // owners' final stores of the root (the smallest id of the tree).
-__device__ __forceinline__ uint32_t find_split(uint32_t *L, int64_t ld, uint32_t x, uint32_t p, int r) {
+__device__ __forceinline__ uint32_t find_split(uint32_t *L, const Lay &ld, uint32_t x, uint32_t p, int r) {
     for (;;) {
         const uint32_t gw = ld_relaxed(cell(L, ld, p, r));
         if (is_root(gw)) return p;

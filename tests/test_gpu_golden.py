@@ -369,13 +369,17 @@ def test_native_sharded_celf_matches_reference(gpu, name, shards):
         assert np.array_equal(np.asarray(trace), z["trace"])
 
 
-@pytest.mark.parametrize("tile", ["4", "8", "12"])
-@pytest.mark.parametrize("name", ["er_mid_300", "er_big_1000", "er_pad20", "cfg_c1"])
-def test_tiled_compress_and_fused_memo_match_reference(gpu, name, tile, monkeypatch):
-    """Lane-tiled compression (the default only for very wide label matrices)
-    with the memo fused into it (run_fused), forced on small cases: labels,
-    sizes, seeds, gains and the full trace equal the reference's."""
-    monkeypatch.setenv("IMX_COMPRESS_TILE", tile)
+@pytest.mark.parametrize("mode", [None, "pull", "enum", "dense", "scan"])
+@pytest.mark.parametrize("tile", ["4", "8", "32", "64"])
+@pytest.mark.parametrize("name", ["er_mid_300", "er_big_1000", "er_pad20", "cfg_c1", "er_const1_r16"])
+def test_lane_tiled_layout_matches_reference(gpu, name, tile, mode, monkeypatch):
+    """The lane-tiled label layout (the default only for very wide label
+    matrices: [W/tl][n][tl], compressed tile by tile with the memo fused in)
+    forced on small cases, with every sampler: labels, sizes, seeds, gains
+    and the full trace equal the reference's."""
+    monkeypatch.setenv("IMX_TILE_LANES", tile)
+    if mode:
+        monkeypatch.setenv("IMX_HOOK", mode)
     z = load_golden(name)
     g = build_graph(gpu, z)
     run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))

@@ -100,11 +100,11 @@ def test_celf_reset_refuses_priorities_below_the_memo(gpu, orc):
 
 
 @pytest.mark.parametrize("tile", ["64", "128"])
-def test_wide_compress_tile_with_fused_memo_is_capped(gpu, tile, monkeypatch):
-    """IMX_COMPRESS_TILE above 32 with the memo fused into the tiled
-    compression: the tile is capped at k_gains_tile's 32 lanes, so the gains
+def test_wide_lane_tiles_with_fused_memo(gpu, tile, monkeypatch):
+    """Lane tiles wider than 32 with the memo fused into the tiled
+    compression: k_gains_tile sums every quad of a tile row, so the gains
     (and everything after them) stay the reference's."""
-    monkeypatch.setenv("IMX_COMPRESS_TILE", tile)
+    monkeypatch.setenv("IMX_TILE_LANES", tile)
     z = load_golden("er_big_1000")
     from test_gpu_golden import build_graph
     g = build_graph(gpu, z)

@@ -179,7 +179,8 @@ int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
 int launch_gains_tile(const uint32_t *T, int64_t n, int64_t tld, int32_t ns_t, int first, int64_t *gains,
                       cudaStream_t st);
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
-                    cudaStream_t st, int *launches = nullptr, int64_t window = 0);
+                    cudaStream_t st, int *launches = nullptr, int64_t window = 0,
+                    const int32_t *rows = nullptr, int64_t nrows = 0);
 
 }  // namespace imx
 

@@ -532,7 +532,7 @@ void graph_free(imx_graph *g) {
     if (!g) return;
     cudaSetDevice(g->dev);
     if (g->thr_pending) graph_settle(g);    // joins the weight upload
-    void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip,
+    void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip, g->nz_rows,
                     g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff, g->lut,
                     g->hv[0].heavy, g->hv[0].hs_v, g->hv[0].hs_a, g->hv[0].hs_len,
                     g->hv[1].heavy, g->hv[1].hs_v, g->hv[1].hs_a, g->hv[1].hs_len};
@@ -913,6 +913,50 @@ int ensure_recip(imx_graph *g) {
         return IMX_EFORMAT;
     }
     g->recip_ready = true;
+    return IMX_OK;
+}
+
+__global__ void k_nz_flags(const int64_t *__restrict__ xadj, int64_t n, uint8_t *__restrict__ flag) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        flag[v] = xadj[v + 1] > xadj[v];
+}
+
+// The rows the compression must stream: vertices with at least one slot.
+// Kept only when at least 1/8 of the vertices are isolated (C4: 44%).
+int ensure_nz_rows(imx_graph *g) {
+    if (g->n_nz >= 0) return IMX_OK;
+    cudaStream_t st = g->stream;
+    const int64_t n = g->n;
+    g->n_nz = n;
+    if (n == 0) return IMX_OK;
+    uint8_t *flag = nullptr;
+    int32_t *rows = nullptr;
+    int64_t *cnt = nullptr;
+    void *tmp = nullptr;
+    size_t tb = 0;
+    IMX_CUDA(pool_alloc((void **)&flag, n, st));
+    IMX_CUDA(pool_alloc((void **)&rows, sizeof(int32_t) * n, st));
+    IMX_CUDA(pool_alloc((void **)&cnt, sizeof(int64_t), st));
+    k_nz_flags<<<grid_for(n), 256, 0, st>>>(g->xadj, n, flag);
+    note_launch();
+    thrust::counting_iterator<int32_t> it(0);
+    IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag, rows, cnt, n, st));
+    IMX_CUDA(pool_alloc(&tmp, tb, st));
+    IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tb, it, flag, rows, cnt, n, st));
+    note_launch(2);
+    int64_t h = n;
+    IMX_CUDA(cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+    IMX_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(flag, st);
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(tmp, st);
+    if (n - h >= n / 8) {
+        g->nz_rows = rows;
+        g->n_nz = h;
+    } else {
+        cudaFreeAsync(rows, st);
+    }
+    IMX_CUDA(cudaStreamSynchronize(st));
     return IMX_OK;
 }
 

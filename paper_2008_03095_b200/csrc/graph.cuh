@@ -55,6 +55,10 @@ struct imx_graph {
     int wthread_rc = 0;
     bool recip_ready = true;
     bool index_ready = false;
+    // non-isolated vertices (built on first use, ensure_nz_rows); NULL when
+    // isolated vertices are too few to be worth skipping
+    int32_t *nz_rows = nullptr;
+    int64_t n_nz = -1;
     struct HeavySlices {
         int T = -1;
         uint8_t *heavy = nullptr;
@@ -76,4 +80,5 @@ int graph_build_from_device_edges(imx_graph *g, const int64_t *dedges, int64_t k
 int graph_settle(imx_graph *g);
 int ensure_recip(imx_graph *g);
 int ensure_index(imx_graph *g);
+int ensure_nz_rows(imx_graph *g);
 }

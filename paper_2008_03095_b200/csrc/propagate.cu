@@ -535,9 +535,12 @@ __device__ __forceinline__ void compress_cell(uint32_t *__restrict__ L, int64_t 
 // the walks (and their dependent loads) run warp-wide instead of diverging.
 constexpr int kCRows = 2;                // label rows per thread per step
 constexpr int kCQ = 32 + 32 * 4 * kCRows;  // drain threshold + one step's worth of appends
+// rows (optional): the rows to stream (the graph's non-isolated vertices --
+// an isolated vertex's row is all roots that nothing points to); n = their count
 __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int64_t n, int64_t ld, int32_t W,
                                                   int64_t nq, int64_t vstep,
-                                                  unsigned long long *__restrict__ nonroot) {
+                                                  unsigned long long *__restrict__ nonroot,
+                                                  const int32_t *__restrict__ rows) {
     __shared__ uint32_t qv[8][kCQ], qw[8][kCQ], qr[8][kCQ];
     __shared__ uint32_t hcs[8][kHot * 128];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -562,7 +565,8 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
 #pragma unroll
     for (int i = 0; i < kCRows; ++i) {
         const int64_t vi = v_first + i * vstep;
-        nxt[i] = vi < n ? *(reinterpret_cast<const uint4 *>(L + vi * ld) + q) : make_uint4(ROOT, ROOT, ROOT, ROOT);
+        nxt[i] = vi < n ? *(reinterpret_cast<const uint4 *>(L + (rows ? (int64_t)rows[vi] : vi) * ld) + q)
+                        : make_uint4(ROOT, ROOT, ROOT, ROOT);
     }
     for (int64_t v = v_first; __any_sync(FULL, v < n); v += kCRows * vstep) {
         uint32_t w[4 * kCRows];
@@ -570,7 +574,8 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
         for (int i = 0; i < kCRows; ++i) {
             w[4 * i] = nxt[i].x; w[4 * i + 1] = nxt[i].y; w[4 * i + 2] = nxt[i].z; w[4 * i + 3] = nxt[i].w;
             const int64_t vi = v + (kCRows + i) * vstep;
-            nxt[i] = vi < n ? *(reinterpret_cast<const uint4 *>(L + vi * ld) + q) : make_uint4(ROOT, ROOT, ROOT, ROOT);
+            nxt[i] = vi < n ? *(reinterpret_cast<const uint4 *>(L + (rows ? (int64_t)rows[vi] : vi) * ld) + q)
+                            : make_uint4(ROOT, ROOT, ROOT, ROOT);
         }
         unsigned m = 0;
 #pragma unroll
@@ -588,7 +593,8 @@ __global__ void __launch_bounds__(256) k_compress(uint32_t *__restrict__ L, int6
 #pragma unroll
         for (int k = 0; k < 4 * kCRows; ++k) {
             if ((m >> k) & 1u) {
-                qv[warp][pos] = (uint32_t)(v + (k >> 2) * vstep);
+                const int64_t vk = v + (k >> 2) * vstep;
+                qv[warp][pos] = (uint32_t)(rows ? (int64_t)rows[vk] : vk);
                 qw[warp][pos] = w[k];
                 qr[warp][pos] = (uint32_t)(r + (k & 3));
                 ++pos;
@@ -1020,7 +1026,8 @@ static int64_t compress_window(int64_t n, int64_t ld) {
 }
 
 int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long long *nonroot,
-                    cudaStream_t st, int *launches, int64_t window) {
+                    cudaStream_t st, int *launches, int64_t window, const int32_t *rows, int64_t nrows) {
+    if (rows) n = nrows;             // stream only these rows
     if (n == 0) return IMX_OK;
     const int64_t win = window > 0 ? window : compress_window(n, ld);
     if (launches) *launches = (int)ceil_div(W, win);
@@ -1036,13 +1043,13 @@ int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long
         const int waves = cw_env && atoi(cw_env) > 0 ? atoi(cw_env)
                           : (quads < ((int64_t)1 << 26) ? 1 : (quads < ((int64_t)1 << 29) ? 8 : 16));
         const int64_t want = std::min<int64_t>(n * nq, (int64_t)148 * 2048 * waves);
-        const int64_t rows = std::max<int64_t>(1, want / nq);
-        const int64_t threads = rows * nq;
+        const int64_t prows = std::max<int64_t>(1, want / nq);
+        const int64_t threads = prows * nq;
         const int blocks = (int)ceil_div(threads, 256);
         // threads beyond rows*nq would break the fixed-quad mapping: size the
         // stride from the launched thread count, rounded down to whole rows
         const int64_t vstep = ((int64_t)blocks * 256) / nq;
-        k_compress<<<blocks, 256, 0, st>>>(L + l0, n, ld, wl, nq, vstep, nonroot);
+        k_compress<<<blocks, 256, 0, st>>>(L + l0, n, ld, wl, nq, vstep, nonroot, rows);
         IMX_CHECK_LAUNCH();
         note_launch();
     }
@@ -1057,9 +1064,12 @@ int launch_compress(uint32_t *L, int64_t n, int64_t ld, int32_t W, unsigned long
 static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
     const int64_t n = c->g->n;
     if (n == 0) return IMX_OK;
+    IMX_TRY(ensure_nz_rows(c->g));
+    const int32_t *rows = c->g->nz_rows;
+    const int64_t nrows = c->g->n_nz;
     if (!c->lay.tiled()) {
         int k = 0;
-        IMX_TRY(launch_compress(c->L, n, c->ld, c->W, nonroot, c->st, &k));
+        IMX_TRY(launch_compress(c->L, n, c->ld, c->W, nonroot, c->st, &k, 0, rows, nrows));
         c->tm.kernel_launches += k;
         return IMX_OK;
     }
@@ -1077,7 +1087,7 @@ static int run_compress(imx_ctx *c, unsigned long long *nonroot) {
             if (l0 >= c->W) break;
             const int32_t wl = (int32_t)std::min<int64_t>(win, c->W - l0);
             int k = 0;
-            IMX_TRY(launch_compress(T + w0, n, tl, wl, nonroot, c->st, &k, win));
+            IMX_TRY(launch_compress(T + w0, n, tl, wl, nonroot, c->st, &k, win, rows, nrows));
             c->tm.kernel_launches += k;
             if (fuse) {
                 // the memo's gains over this window's scored lanes, while it is in L2

@@ -38,10 +38,10 @@ __device__ __forceinline__ uint32_t cell_size(const uint32_t *__restrict__ L, co
     if (ENC) {
         if (is_root(w)) { label = u; return (w & COUNT) + 1u; }
         label = w;
-        return (L[ld.off(w, r)] & COUNT) + 1u;
+        return (L[cell_off(ld, w, r)] & COUNT) + 1u;
     }
     label = w;
-    return C[ld.off(w, r)];
+    return C[cell_off(ld, w, r)];
 }
 
 // marginal_gain (selection.py:63-70): sum over scored lanes of the component
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const int32_t *__restrict
         const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
         unsigned long long acc = 0;
         for (int q = threadIdx.x; q < nqs; q += kEvalThreads) {
-            const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
+            const uint4 l4 = row_quad(rowbase, ld, u, q);
             const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
             uint32_t wd[4], s[4];
             const int r = q << 2;
@@ -100,7 +100,7 @@ __global__ void k_commit(int32_t u, const uint32_t *__restrict__ L, const uint32
     unsigned long long acc = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ns; r += gridDim.x * blockDim.x) {
         uint32_t lab;
-        const uint32_t s = cell_size<ENC>(L, C, ld, (uint32_t)u, L[ld.off(u, r)], r, lab);
+        const uint32_t s = cell_size<ENC>(L, C, ld, (uint32_t)u, L[cell_off(ld, u, r)], r, lab);
         const uint32_t bit = 1u << (r & 31);
         const uint32_t old = atomicOr(cov + (int64_t)lab * cw + (r >> 5), bit);
         if (!(old & bit)) {
@@ -252,7 +252,7 @@ __device__ __forceinline__ int64_t block_eval(const uint32_t *__restrict__ L, co
     const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
     unsigned long long acc = 0;
     for (int q = threadIdx.x; q < nqs; q += blockDim.x) {
-        const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
+        const uint4 l4 = row_quad(rowbase, ld, u, q);
         const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
         uint32_t wd[4], sz[4];
         const int r = q << 2;
@@ -328,7 +328,7 @@ __device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, co
         const int nqs = (ns + 3) >> 2;
         const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
         for (int q = tid; q < nqs; q += gsz) {
-            const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
+            const uint4 l4 = row_quad(rowbase, ld, u, q);
             const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
             uint32_t wd[4], sz[4];
             const int r = q << 2;
@@ -359,7 +359,7 @@ constexpr int64_t kStepPerCta = IMX_CELF_STEP_PER_CTA;
 #endif
 constexpr int64_t kFirstBatchCap = IMX_CELF_FIRST_CAP;
 
-template <bool ENC>
+template <bool ENC, bool XM>
 #ifndef IMX_CELF_MINB
 #define IMX_CELF_MINB 4
 #endif
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
     int32_t bpct, int32_t ngroup, int64_t *__restrict__ xbuf, int64_t xcap) {
     cg::grid_group grid = cg::this_grid();
-    const bool xm = xcap > 0;                  // exchange mode (sharded run)
+    constexpr bool xm = XM;                    // exchange mode (sharded run; xcap > 0)
     // a stop that waits for the host (done, trace full, error, big round)
     if (xm && st->status != 0 && st->status != 5) return;
     __shared__ unsigned long long sback[kSmemBack];
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                         const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
                         unsigned long long acc = 0;
                         for (int q = wl; q < nqs; q += 32) {
-                            const uint4 l4 = *reinterpret_cast<const uint4 *>(rowbase + ld.off(u, q << 2));
+                            const uint4 l4 = row_quad(rowbase, ld, u, q);
                             const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
                             uint32_t wd[4], sz[4];
                             const int r = q << 2;
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
             unsigned long long acc = 0;
             for (int64_t r = gtid; r < ns; r += gthreads) {
                 uint32_t lab;
-                const uint32_t sz = cell_size<ENC>(L, C, ld, (uint32_t)best_v, L[ld.off(best_v, r)], (int)r, lab);
+                const uint32_t sz = cell_size<ENC>(L, C, ld, (uint32_t)best_v, L[cell_off(ld, best_v, r)], (int)r, lab);
                 const uint32_t bit = 1u << (r & 31);
                 const uint32_t old = atomicOr(cov + (int64_t)lab * cw + (r >> 5), bit);
                 if (!(old & bit)) { per_sim[r] += sz; acc += sz; }
@@ -1017,7 +1017,7 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
     int *grid_cache = c->celf_grid;
     const int enc = c->C ? 0 : 1;
-    void *fn = enc ? (void *)k_celf_rounds<true> : (void *)k_celf_rounds<false>;
+    void *fn = enc ? (void *)k_celf_rounds<true, false> : (void *)k_celf_rounds<false, false>;
     if (!grid_cache[enc]) {
         // fewer CTAs make the grid barriers cheaper; the evaluation batches
         // still have one CTA per candidate in flight per SM slot
@@ -1230,14 +1230,16 @@ static int celf_select_xchg(imx_ctx *c, int32_t k, std::vector<int32_t> &seeds, 
     unsigned long long *gain = c->scratch + 7;
     IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
     const int enc = c->C ? 0 : 1;
-    void *fn = enc ? (void *)k_celf_rounds<true> : (void *)k_celf_rounds<false>;
-    if (!c->celf_grid[enc]) {
+    // the exchange-mode kernel may hold fewer CTAs per SM than the single-rank
+    // one (its own grid cache slot)
+    void *fn = enc ? (void *)k_celf_rounds<true, true> : (void *)k_celf_rounds<false, true>;
+    if (!c->celf_grid[2 + enc]) {
         int per_sm = 0, sms = 0;
         IMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
         IMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
         int want = 4;
         if (const char *b = getenv("IMX_CELF_BPSM")) want = std::max(1, atoi(b));
-        c->celf_grid[enc] = std::max(1, std::min(per_sm, want)) * sms;
+        c->celf_grid[2 + enc] = std::max(1, std::min(per_sm, want)) * sms;
     }
     int32_t kk = k, bpct = 150, ngroup = 1;
     if (const char *b = getenv("IMX_CELF_BATCH_PCT")) bpct = std::max(1, atoi(b));
@@ -1275,7 +1277,7 @@ static int celf_select_xchg(imx_ctx *c, int32_t k, std::vector<int32_t> &seeds, 
         int slot = 0, pending = -1;
         for (;;) {
             for (int j = 0; j < kXchgChunk; ++j) {
-                IMX_CUDA(cudaLaunchCooperativeKernel(fn, c->celf_grid[enc], 256, args, 0, c->st));
+                IMX_CUDA(cudaLaunchCooperativeKernel(fn, c->celf_grid[2 + enc], 256, args, 0, c->st));
                 count_launch(c);
                 IMX_TRY(comm_allreduce_i64(c->comm, xbuf, xcap + 1, c->st));
             }

@@ -101,7 +101,7 @@ struct imx_ctx {
     int32_t *dseeds = nullptr;
     int64_t *dsgains = nullptr;
     int32_t dseeds_cap = 0;
-    int celf_grid[2] = {0, 0};        // cooperative grid of k_celf_rounds<ENC> on this context's device
+    int celf_grid[4] = {0, 0, 0, 0};  // cooperative grids of k_celf_rounds<ENC, XM> on this context's device
     // interval-enumeration sampler
     int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;
     int64_t nseg_cap = 0;

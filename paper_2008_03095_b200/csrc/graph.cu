@@ -214,10 +214,11 @@ struct GStats {
     unsigned long long tsum;   // sum of canonical-slot thresholds
     int64_t me;                // canonical slots (DeviceSelect count)
     unsigned long long symsum; // sum of mix(u, v) - mix(v, u) over slots (k_sym_check)
+    int64_t nnz;               // non-isolated vertices (graph_nz_rows_async)
 };
 __global__ void k_stats_init(GStats *gs) {
     gs->flags = 0; gs->tmin = INT32_MAX; gs->tmax = INT32_MIN; gs->pad = 0;
-    gs->maxp = 0; gs->tsum = 0; gs->me = 0; gs->symsum = 0;
+    gs->maxp = 0; gs->tsum = 0; gs->me = 0; gs->symsum = 0; gs->nnz = 0;
 }
 
 // Symmetry of a large host CSR without the reciprocal search (deferred
@@ -643,6 +644,9 @@ done:
 // late_weights (structure pass only): enqueues the weight upload after the
 // weight-free structure kernels and makes the graph stream wait for it; the
 // pairing then runs without thresholds and k_thresholds follows the upload
+static int graph_nz_rows_async(imx_graph *g, GStats *gs);
+static void graph_nz_rows_done(imx_graph *g, int64_t nnz);
+
 static int graph_analyze(imx_graph *g, bool structure, const std::function<int()> &late_weights = nullptr) {
     cudaStream_t st = g->stream;
     const int64_t m2 = g->m2, n = g->n;
@@ -685,6 +689,7 @@ static int graph_analyze(imx_graph *g, bool structure, const std::function<int()
             note_launch(2);
             cudaFreeAsync(tmp, st);
             cudaFreeAsync(flag, st);
+            IMX_TRY(graph_nz_rows_async(g, gs));
         }
     }
     if (late_weights) IMX_TRY(late_weights());
@@ -717,6 +722,7 @@ static int graph_analyze(imx_graph *g, bool structure, const std::function<int()
         g->symmetric = (h.flags & 8u) == 0 && (m2 % 2 == 0);
         g->max_prefix = (int64_t)h.maxp;
         g->me = m2 ? h.me : 0;
+        if (m2) graph_nz_rows_done(g, h.nnz);
         if (g->me >= (int64_t(1) << 31)) {
             cudaFreeAsync(gs, st);
             set_error("%lld undirected edges exceed 2^31 - 1", (long long)g->me);
@@ -777,6 +783,7 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
         cudaFreeAsync(tmp, st);
         cudaFreeAsync(flag, st);
     }
+    IMX_TRY(graph_nz_rows_async(g, gs));
     // the weight stream: upload, then (after the structure) raw thresholds
     cudaEvent_t ev_struct = nullptr;
     IMX_CUDA(cudaEventCreateWithFlags(&ev_struct, cudaEventDisableTiming));
@@ -824,6 +831,7 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
     g->symmetric = (h.flags & 8u) == 0 && h.symsum == 0 && (m2 % 2 == 0);
     g->max_prefix = (int64_t)h.maxp;
     g->me = h.me;
+    graph_nz_rows_done(g, h.nnz);
     if (g->me >= (int64_t(1) << 31)) {
         set_error("%lld undirected edges exceed 2^31 - 1", (long long)g->me);
         return IMX_ECONSTRAINT;
@@ -921,42 +929,53 @@ __global__ void k_nz_flags(const int64_t *__restrict__ xadj, int64_t n, uint8_t 
         flag[v] = xadj[v + 1] > xadj[v];
 }
 
-// The rows the compression must stream: vertices with at least one slot.
-// Kept only when at least 1/8 of the vertices are isolated (C4: 44%).
-int ensure_nz_rows(imx_graph *g) {
-    if (g->n_nz >= 0) return IMX_OK;
+// The rows the compression must stream: vertices with at least one slot,
+// listed on the graph stream while the structure is analysed (the count
+// rides on the analysis' one host sync: graph_nz_rows_done).
+static int graph_nz_rows_async(imx_graph *g, GStats *gs) {
     cudaStream_t st = g->stream;
     const int64_t n = g->n;
-    g->n_nz = n;
     if (n == 0) return IMX_OK;
     uint8_t *flag = nullptr;
-    int32_t *rows = nullptr;
-    int64_t *cnt = nullptr;
     void *tmp = nullptr;
     size_t tb = 0;
+    if (g->nz_rows) { cudaFreeAsync(g->nz_rows, st); g->nz_rows = nullptr; }
     IMX_CUDA(pool_alloc((void **)&flag, n, st));
-    IMX_CUDA(pool_alloc((void **)&rows, sizeof(int32_t) * n, st));
-    IMX_CUDA(pool_alloc((void **)&cnt, sizeof(int64_t), st));
+    IMX_CUDA(pool_alloc((void **)&g->nz_rows, sizeof(int32_t) * n, st));
     k_nz_flags<<<grid_for(n), 256, 0, st>>>(g->xadj, n, flag);
     note_launch();
     thrust::counting_iterator<int32_t> it(0);
-    IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag, rows, cnt, n, st));
+    IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag, g->nz_rows, &gs->nnz, n, st));
     IMX_CUDA(pool_alloc(&tmp, tb, st));
-    IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tb, it, flag, rows, cnt, n, st));
+    IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tb, it, flag, g->nz_rows, &gs->nnz, n, st));
     note_launch(2);
-    int64_t h = n;
-    IMX_CUDA(cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
-    IMX_CUDA(cudaStreamSynchronize(st));
     cudaFreeAsync(flag, st);
-    cudaFreeAsync(cnt, st);
     cudaFreeAsync(tmp, st);
-    if (n - h >= n / 8) {
-        g->nz_rows = rows;
-        g->n_nz = h;
+    return IMX_OK;
+}
+
+// kept only when at least 1/8 of the vertices are isolated (C4: 44%)
+static void graph_nz_rows_done(imx_graph *g, int64_t nnz) {
+    if (g->nz_rows && g->n - nnz >= g->n / 8) {
+        g->n_nz = nnz;
     } else {
-        cudaFreeAsync(rows, st);
+        if (g->nz_rows) cudaFreeAsync(g->nz_rows, g->stream);
+        g->nz_rows = nullptr;
+        g->n_nz = g->n;
     }
-    IMX_CUDA(cudaStreamSynchronize(st));
+}
+
+int ensure_nz_rows(imx_graph *g) {
+    if (g->n_nz >= 0) return IMX_OK;
+    GStats *gs;
+    IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), g->stream));
+    k_stats_init<<<1, 1, 0, g->stream>>>(gs);
+    IMX_TRY(graph_nz_rows_async(g, gs));
+    GStats h;
+    IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, g->stream));
+    IMX_CUDA(cudaStreamSynchronize(g->stream));
+    cudaFreeAsync(gs, g->stream);
+    graph_nz_rows_done(g, h.nnz);
     return IMX_OK;
 }
 

@@ -66,15 +66,14 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int q = q0 + 32 * h;
-                const uint4 l = q < nqs ? __ldg(reinterpret_cast<const uint4 *>(L + y.off(v, 4 * q)))
-                                        : make_uint4(ROOT, ROOT, ROOT, ROOT);
+                const uint4 l = q < nqs ? row_quad(L, y, v, q) : make_uint4(ROOT, ROOT, ROOT, ROOT);
                 w[4 * h] = l.x; w[4 * h + 1] = l.y; w[4 * h + 2] = l.z; w[4 * h + 3] = l.w;
             }
             uint32_t rw[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int r = ((q0 + 32 * (k >> 2)) << 2) + (k & 3);
-                rw[k] = is_root(w[k]) ? w[k] : __ldg(L + y.off(w[k], r));
+                rw[k] = is_root(w[k]) ? w[k] : __ldg(L + cell_off(y, w[k], r));
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {

@@ -39,6 +39,15 @@ struct Lay {
     }
 };
 
+// quad q (lanes 4q..4q+3) of row v; rows keep the plain row-pointer form
+__device__ __forceinline__ uint4 row_quad(const uint32_t *L, const Lay &y, int64_t v, int q) {
+    if (!y.tiled()) return reinterpret_cast<const uint4 *>(L + v * y.ld)[q];
+    return *reinterpret_cast<const uint4 *>(L + y.off(v, q << 2));
+}
+__device__ __forceinline__ int64_t cell_off(const Lay &y, int64_t v, int r) {
+    return y.tiled() ? y.off(v, r) : v * y.ld + r;
+}
+
 __device__ __forceinline__ uint32_t *cell(uint32_t *L, const Lay &y, uint32_t v, int r) {
     return L + y.off(v, r);
 }

@@ -38,6 +38,7 @@ allreduces of the gains and CELF partial sums).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -406,10 +407,11 @@ def run_ours(args, world, rank, local):
     # would keep its graph) ----
     host = imx.Graph(pinned(g.xadj), pinned(g.adj), pinned(g.weights), g.orig_ids)
     e2e_steps = args.e2e_steps or args.steps
-    times, d2h, run = [], 0, None
+    times, d2h, run, phase_ms = [], 0, None, []
     for i in range(args.warmup + e2e_steps):
         gi = imx.Graph(host.xadj, host.adj, host.weights, host.orig_ids)
         run = None
+        gc.collect()          # the previous step's buffers go back to the pools outside the timed region
         barrier(world)
         t0 = time.perf_counter()
         run = imx.run_fused(gi, K, num_simulations=R_total, master_seed=0)
@@ -417,6 +419,7 @@ def run_ours(args, world, rank, local):
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(allreduce_max(dt, world))
+            phase_ms.append({k: round(1e3 * v, 2) for k, v in run.timings.items()})
             d2h = 4 * K + 8 * K + 40 * len(run.selection.trace)
     e2e_s = float(np.mean(times))
     h2d = 8 * (n + 1) + 4 * m2 + 8 * m2 + 4 * len(X)
@@ -431,7 +434,9 @@ def run_ours(args, world, rank, local):
         "roofline": roof,
         "e2e": {"value": units_total / e2e_s, "unit": "edge-sims/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "k_seed_wall_s": e2e_s, "seeds_head": seeds[:5], "spread": spread,
+                "k_seed_wall_s": e2e_s, "step_ms": [round(1e3 * x, 2) for x in times],
+                "step_phase_ms": phase_ms,
+                "seeds_head": seeds[:5], "spread": spread,
                 "timings_last": {k: round(v, 5) for k, v in run.timings.items()}},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

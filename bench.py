@@ -406,6 +406,10 @@ def run_ours(args, world, rank, local):
     # ---- e2e: public API with host buffers (pinned, as a serving caller
     # would keep its graph) ----
     host = imx.Graph(pinned(g.xadj), pinned(g.adj), pinned(g.weights), g.orig_ids)
+    # the e2e runs start from the host graph alone: release the generated one
+    g.drop_device()
+    del table, ctx
+    gc.collect()
     e2e_steps = args.e2e_steps or args.steps
     times, d2h, run, phase_ms = [], 0, None, []
     for i in range(args.warmup + e2e_steps):

@@ -1159,7 +1159,19 @@ static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<in
         count_launch(c);
         const int64_t base = c->trace_n;
         if ((rc = trace_reserve(c, base + 5 * (kr + 1))) != IMX_OK) goto done;
-        GB(cudaMemcpyAsync(c->trace + base, rec, sizeof(int64_t) * 5 * (kr + 1), cudaMemcpyDeviceToHost, st));
+        // the records (C4 round 1: 2.3 M, 91 MB) go to the host on the side
+        // stream while the next rounds run; rec is freed there after the copy
+        if (!c->tst) GB(acquire_stream(c->dev, &c->tst));
+        {
+            cudaEvent_t ev;
+            GB(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            GB(cudaEventRecord(ev, st));
+            GB(cudaStreamWaitEvent(c->tst, ev, 0));
+            cudaEventDestroy(ev);
+        }
+        GB(cudaMemcpyAsync(c->trace + base, rec, sizeof(int64_t) * 5 * (kr + 1), cudaMemcpyDeviceToHost, c->tst));
+        GB(cudaFreeAsync(rec, c->tst));
+        rec = nullptr;
         unsigned long long got = 0;
         GB(cudaMemcpyAsync(&got, gain, sizeof got, cudaMemcpyDeviceToHost, st));
         GB(cudaStreamSynchronize(st));
@@ -1398,6 +1410,7 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     }
     if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
     if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);
+    IMX_TRY(trace_flush(c));
     cudaEventRecord(c->ev[7], c->st);
     cudaEventSynchronize(c->ev[7]);
     cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);
@@ -1455,6 +1468,7 @@ extern "C" int imx_celf_select_comm(imx_ctx *c, int32_t k, int32_t *seeds_out, i
     const char *mode = getenv("IMX_CELF");
     if (coop && !(mode && !strcmp(mode, "host"))) {
         IMX_TRY(celf_select_xchg(c, k, seeds, gains));
+        IMX_TRY(trace_flush(c));
         if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
         if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);
         cudaEventRecord(c->ev[7], c->st);
@@ -1490,6 +1504,7 @@ extern "C" int imx_celf_select_comm(imx_ctx *c, int32_t k, int32_t *seeds_out, i
 extern "C" int imx_celf_trace_take(imx_ctx *c, int64_t **out, int64_t *len) {
     CTX_CHECK(c);
     if (!out || !len) { set_error("NULL argument"); return IMX_EINVAL; }
+    IMX_TRY(trace_flush(c));
     *len = c->trace_n / 5;
     *out = nullptr;
     if (*len == 0) return IMX_OK;
@@ -1503,6 +1518,7 @@ extern "C" int imx_celf_trace_take(imx_ctx *c, int64_t **out, int64_t *len) {
 
 extern "C" int imx_celf_trace(imx_ctx *c, int64_t *out, int64_t cap) {
     CTX_CHECK(c);
+    IMX_TRY(trace_flush(c));
     const int64_t len = c->trace_n / 5;
     const int64_t k = std::min(cap, len);
     if (k > 0 && out) memcpy(out, c->trace, sizeof(int64_t) * 5 * k);

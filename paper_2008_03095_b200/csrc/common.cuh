@@ -73,6 +73,9 @@ void release_stream(int dev, cudaStream_t st);
 // host threads when large (upload.cu)
 cudaError_t upload_h2d(void *dst, const void *src, size_t bytes, cudaStream_t st);
 bool host_pinned_ptr(const void *p);
+// recycled pinned host buffers (ctx.cu)
+cudaError_t pinned_get(void **p, size_t bytes);
+void pinned_put(void *p, size_t bytes);
 // stream-ordered allocation from the device's pool (ctx.cu)
 cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st);
 

@@ -64,11 +64,48 @@ cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st) {
     return cudaMallocAsync(p, bytes, st);
 }
 
+// Label matrices are the only multi-GB buffers (C4 17 GB, C5 33 GB).  Back-
+// to-back runs release one and ask for another of the same size, often on a
+// different recycled stream; the stream-ordered pool then sometimes maps
+// fresh memory (up to ~0.8 s at 33 GB) instead of reusing the block.  A
+// released matrix is kept (one per device) and handed to the next context
+// that fits it.
+static std::mutex g_lbuf_mu;
+struct LBuf { int dev; void *p; size_t bytes; };
+static std::vector<LBuf> g_lbuf;
+
+static cudaError_t label_alloc(int dev, void **p, size_t bytes, cudaStream_t st) {
+    {
+        std::lock_guard<std::mutex> lk(g_lbuf_mu);
+        for (size_t i = 0; i < g_lbuf.size(); ++i)
+            if (g_lbuf[i].dev == dev && g_lbuf[i].bytes >= bytes && g_lbuf[i].bytes <= 2 * bytes + (64 << 20)) {
+                *p = g_lbuf[i].p;
+                g_lbuf.erase(g_lbuf.begin() + i);
+                return cudaSuccess;
+            }
+    }
+    return pool_alloc(p, bytes, st);
+}
+
+static void label_release(int dev, void *p, size_t bytes, cudaStream_t st) {
+    if (!p) return;
+    if (bytes < ((size_t)256 << 20)) { cudaFreeAsync(p, st); return; }
+    cudaStreamSynchronize(st);       // the matrix is idle before anyone else gets it
+    std::lock_guard<std::mutex> lk(g_lbuf_mu);
+    for (size_t i = 0; i < g_lbuf.size(); ++i)
+        if (g_lbuf[i].dev == dev) {   // one kept per device: the newest
+            cudaFreeAsync(g_lbuf[i].p, st);
+            g_lbuf.erase(g_lbuf.begin() + i);
+            break;
+        }
+    g_lbuf.push_back({dev, p, bytes});
+}
+
 void ctx_free(imx_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->dev);
     if (c->st) cudaStreamSynchronize(c->st);
-    if (c->L) cudaFreeAsync(c->L, c->st);
+    if (c->L) label_release(c->dev, c->L, c->L_bytes, c->st);
     if (c->C) cudaFreeAsync(c->C, c->st);
     c->L = c->C = nullptr;
     if (c->st) cudaStreamSynchronize(c->st);
@@ -83,6 +120,7 @@ void ctx_free(imx_ctx *c) {
     pinned_put(c->h_vals, sizeof(int64_t) * c->stage_cap);
     pinned_put(c->trace, sizeof(int64_t) * c->trace_hcap);
     for (auto &e : c->ev) if (e) cudaEventDestroy(e);
+    if (c->tst) { cudaStreamSynchronize(c->tst); release_stream(c->dev, c->tst); }
     release_stream(c->dev, c->st);
     delete c;
 }
@@ -178,9 +216,10 @@ extern "C" int imx_create(imx_graph *g, const int32_t *X, int32_t width, int32_t
     for (auto &e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return fail(IMX_ECUDA);
     const size_t cells = (size_t)(n > 0 ? n : 1) * (size_t)c->ld;
+    c->L_bytes = sizeof(uint32_t) * cells;
     cudaError_t e = cudaSuccess;
     if ((e = pool_alloc((void **)&c->X, sizeof(int32_t) * c->ld, c->st)) != cudaSuccess ||
-        (e = pool_alloc((void **)&c->L, sizeof(uint32_t) * cells, c->st)) != cudaSuccess ||
+        (e = label_alloc(c->dev, (void **)&c->L, sizeof(uint32_t) * cells, c->st)) != cudaSuccess ||
         (e = pool_alloc((void **)&c->gains, sizeof(int64_t) * (n + 1), c->st)) != cudaSuccess ||
         (e = pool_alloc((void **)&c->scratch, sizeof(unsigned long long) * 16, c->st)) != cudaSuccess ||
         (e = cudaMemsetAsync(c->scratch, 0, sizeof(unsigned long long) * 16, c->st)) != cudaSuccess) {
@@ -209,8 +248,15 @@ extern "C" int imx_get_timings(imx_ctx *c, imx_timings *out) {
 
 namespace imx {
 // grow the pinned host trace buffer to hold at least cnt int64 (keeps content)
+// the host trace buffer is complete (an asynchronous big-round copy landed)
+int trace_flush(imx_ctx *c) {
+    if (c->tst) IMX_CUDA(cudaStreamSynchronize(c->tst));
+    return IMX_OK;
+}
+
 int trace_reserve(imx_ctx *c, int64_t cnt) {
     if (cnt <= c->trace_hcap) return IMX_OK;
+    IMX_TRY(trace_flush(c));         // no copy may still be landing in the old buffer
     const int64_t cap = std::max<int64_t>(cnt, std::max<int64_t>(2 * c->trace_hcap, 1 << 16));
     int64_t *p = nullptr;
     IMX_CUDA(pinned_get((void **)&p, sizeof(int64_t) * cap));

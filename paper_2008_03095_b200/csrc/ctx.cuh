@@ -67,6 +67,7 @@ struct imx_ctx {
     int vb = 0;                   // bits for vertex ids in packed CELF keys
     int32_t *X = nullptr;         // [ld]
     uint32_t *L = nullptr;        // [n*ld]
+    size_t L_bytes = 0;
     uint32_t *C = nullptr;        // [n*ld] caller-label mode only
     int64_t *gains = nullptr;     // [n]
     // CELF state
@@ -126,6 +127,9 @@ struct imx_ctx {
     bool fuse_memo = false, gains_fused = false;
     // ranks of a sharded run (comm.cu); NULL = single rank
     imx_comm *comm = nullptr;
+    // a big CELF round's trace records travel to the host on this side stream
+    // while the later rounds run (celf_big_round); trace_flush waits for it
+    cudaStream_t tst = nullptr;
     // the last sampler launch used a deferred graph's speculative threshold
     bool spec_used = false;
     imx_timings tm{};
@@ -162,8 +166,7 @@ inline void count_launch(imx_ctx *c, int k = 1) {
 
 int ensure_celf_buffers(imx_ctx *c);
 int trace_reserve(imx_ctx *c, int64_t cnt);
-cudaError_t pinned_get(void **p, size_t bytes);
-void pinned_put(void *p, size_t bytes);
+int trace_flush(imx_ctx *c);
 void pinned_lend(void *p, size_t bytes);   // handed to the caller; imx_host_free returns it
 int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);

@@ -791,7 +791,7 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
     IMX_CUDA(acquire_stream(g->dev, &g->wst));
     IMX_CUDA(cudaEventCreateWithFlags(&g->wev, cudaEventDisableTiming));
     IMX_CUDA(pool_alloc(&g->wstats_d, sizeof(GStats), st));
-    IMX_CUDA(cudaMallocHost(&g->wstats_h, sizeof(GStats)));
+    IMX_CUDA(pinned_get(&g->wstats_h, sizeof(GStats)));   // recycled: cudaFreeHost synchronises the device
     IMX_CUDA(cudaStreamWaitEvent(g->wst, ev_struct, 0));      // buffers allocated on st
     GStats *wd = static_cast<GStats *>(g->wstats_d);
     GStats *wh = static_cast<GStats *>(g->wstats_h);
@@ -868,7 +868,7 @@ int graph_settle(imx_graph *g) {
     g->wev = nullptr;
     release_stream(g->dev, g->wst);
     g->wst = nullptr;
-    cudaFreeHost(g->wstats_h);
+    pinned_put(g->wstats_h, sizeof(GStats));
     g->wstats_h = nullptr;
     cudaFreeAsync(g->wstats_d, g->stream);
     g->wstats_d = nullptr;

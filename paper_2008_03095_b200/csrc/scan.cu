@@ -55,9 +55,10 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
     // flags, per-warp union queues (pass 2), the chunk's lane tables
     uint8_t *flags_all = reinterpret_cast<uint8_t *>(smem4);                   // [warps][cw]
     uint32_t *queues = reinterpret_cast<uint32_t *>(flags_all + kScanWarps * cw);   // [warps][3][kScanQ]
-    int32_t *sxs = reinterpret_cast<int32_t *>(queues + (PASS == 2 ? kScanWarps * 3 * kScanQ : 0));
-    int32_t *sboff = sxs + cw;                                                   // [nb + 1]
-    uint16_t *sperm = reinterpret_cast<uint16_t *>(sboff + nb + 1);              // [cw]
+    // the chunk's lanes sorted by bucket as (word, lane) pairs, and every
+    // bucket's [lo, hi): one 8-byte shared load each
+    int2 *sx2 = reinterpret_cast<int2 *>(queues + (PASS == 2 ? kScanWarps * 3 * kScanQ : 0));   // [cw]
+    int2 *sbb = sx2 + cw;                                                        // [nb]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t *flag = flags_all + warp * cw;
     uint32_t *qlo = queues + warp * 3 * kScanQ, *qhi = qlo + kScanQ, *qr = qhi + kScanQ;
@@ -71,11 +72,10 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
         // row cells of this chunk; the last chunk also covers the row padding
         const int rwc = (int)(c == nchunks - 1 ? ld - r0 : min((int64_t)cw, ld - r0));
         __syncthreads();
-        for (int i = threadIdx.x; i < cw; i += blockDim.x) {
-            sxs[i] = xs_all[(int64_t)c * cw + i];
-            sperm[i] = perm_all[(int64_t)c * cw + i];
-        }
-        for (int i = threadIdx.x; i <= nb; i += blockDim.x) sboff[i] = boff_all[(int64_t)c * (nb + 1) + i];
+        for (int i = threadIdx.x; i < cw; i += blockDim.x)
+            sx2[i] = make_int2(xs_all[(int64_t)c * cw + i], (int)perm_all[(int64_t)c * cw + i]);
+        for (int i = threadIdx.x; i < nb; i += blockDim.x)
+            sbb[i] = make_int2(boff_all[(int64_t)c * (nb + 1) + i], boff_all[(int64_t)c * (nb + 1) + i + 1]);
         __syncthreads();
         for (;;) {
             // dynamic distribution: rows differ by orders of magnitude in
@@ -157,11 +157,13 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                         const uint32_t u = __shfl_sync(FULL, bu, j);
                         const int32_t h = __shfl_sync(FULL, bh, j);
                         const int bk = (int)((uint32_t)h >> kb);
-                        const int lo = sboff[bk], hi = sboff[bk + 1];
+                        const int2 bb = sbb[bk];
+                        const int lo = bb.x, hi = bb.y;
                         for (int i0 = lo; i0 < hi; i0 += 32) {
                             const int i = i0 + lane;
-                            const bool live = i < hi && (sxs[i] ^ h) < t;
-                            const int p = live ? sperm[i] : 0;
+                            const int2 xp = i < hi ? sx2[i] : make_int2(0x7fffffff, 0);
+                            const bool live = i < hi && (xp.x ^ h) < t;
+                            const int p = live ? xp.y : 0;
                             if (PASS == 1) {
                                 // ascending slots: the first live neighbour is the smallest
                                 if (live && !flag[p]) {
@@ -180,20 +182,22 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                                     }
                                 }
                                 const unsigned b = __ballot_sync(FULL, un);
-                                if (un) {
-                                    const int pos = qn + __popc(b & lt_mask);
-                                    qlo[pos] = u;
-                                    qhi[pos] = (uint32_t)v;
-                                    qr[pos] = (uint32_t)(r0 + p);
-                                }
-                                qn += __popc(b);
-                                __syncwarp();
-                                if (qn >= 32) {
-                                    qn -= 32;
-                                    const uint32_t a2 = qlo[qn + lane], b2 = qhi[qn + lane];
-                                    const int rr = (int)qr[qn + lane];
+                                if (b) {                            // most live pairs are forest edges
+                                    if (un) {
+                                        const int pos = qn + __popc(b & lt_mask);
+                                        qlo[pos] = u;
+                                        qhi[pos] = (uint32_t)v;
+                                        qr[pos] = (uint32_t)(r0 + p);
+                                    }
+                                    qn += __popc(b);
                                     __syncwarp();
-                                    nh += unite(L, y, a2, b2, rr);
+                                    if (qn >= 32) {
+                                        qn -= 32;
+                                        const uint32_t a2 = qlo[qn + lane], b2 = qhi[qn + lane];
+                                        const int rr = (int)qr[qn + lane];
+                                        __syncwarp();
+                                        nh += unite(L, y, a2, b2, rr);
+                                    }
                                 }
                             }
                         }
@@ -298,7 +302,7 @@ int run_scan(imx_ctx *c, int pass, unsigned long long *hooks) {
     const int cw = c->scan_cw, nb = c->scan_nb;
     // cw is a multiple of 16, so every section keeps 16-byte alignment
     const size_t smem = (size_t)kScanWarps * cw + (pass == 2 ? sizeof(uint32_t) * kScanWarps * 3 * kScanQ : 0) +
-                        sizeof(int32_t) * cw + sizeof(int32_t) * (nb + 1) + sizeof(uint16_t) * cw;
+                        sizeof(int2) * cw + sizeof(int2) * nb;
     using KF = void (*)(const int64_t *, const int32_t *, const int32_t *, int32_t, int, int, int, int,
                         const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, Lay, uint32_t *,
                         unsigned long long *, const uint8_t *, const int32_t *, const int64_t *, const int32_t *,

@@ -289,6 +289,7 @@ extern "C" int imx_evaluate_seeds(imx_graph *g, const int32_t *seeds, int32_t k,
     IMX_CUDA(cudaSetDevice(g->dev));
     IMX_TRY(graph_settle(g));          // weights of a deferred graph
     IMX_TRY(ensure_recip(g));          // p = max(w, w[reciprocal]) per canonical edge
+    IMX_TRY(ensure_cslot(g));
     cudaStream_t st = g->stream;
     // worlds per batch: the label matrix stays under ~4 GiB
     int64_t B = std::min<int64_t>(chunk, 4096);
@@ -370,6 +371,7 @@ extern "C" int imx_sampling_cdf(imx_graph *g, const int32_t *X, int32_t scored, 
     if (bins < 1) { set_error("need at least 1 bin, got %d", bins); return IMX_EINVAL; }
     if (scored < 0 || stride < 1) { set_error("bad scored/stride"); return IMX_EINVAL; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(ensure_cslot(g));
     cudaStream_t st = g->stream;
     const int64_t nc = (g->me + stride - 1) / stride, nv = nc * scored;
     int32_t *dX = nullptr, *va = nullptr, *vb = nullptr;

@@ -192,6 +192,12 @@ __global__ void k_recip_check(const int64_t *__restrict__ xadj, const int32_t *_
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 8u);
 }
 
+// k_sym_check and k_slot_hashes in one pass over the slots (deferred path)
+struct GStats;
+__global__ void k_sym_hash(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                           const int32_t *__restrict__ src, int64_t n, int64_t m2, int32_t *__restrict__ hash,
+                           GStats *__restrict__ gs);
+
 __global__ void k_slot_hashes(const int32_t *__restrict__ src, const int32_t *__restrict__ adj,
                               int64_t m2, int32_t *__restrict__ hash) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
@@ -221,6 +227,10 @@ __global__ void k_stats_init(GStats *gs) {
     gs->maxp = 0; gs->tsum = 0; gs->me = 0; gs->symsum = 0; gs->nnz = 0;
 }
 
+__global__ void k_sym_hash(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                           const int32_t *__restrict__ src, int64_t n, int64_t m2, int32_t *__restrict__ hash,
+                           GStats *__restrict__ gs);
+
 // Symmetry of a large host CSR without the reciprocal search (deferred
 // path): rows strictly ascending (no duplicate, no self-loop) and the slot
 // multiset equal to its transpose, tested as sum(mix(u, v) - mix(v, u)) == 0
@@ -240,6 +250,30 @@ __global__ void k_sym_check(const int64_t *__restrict__ xadj, const int32_t *__r
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
          s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t u = src[s], v = adj[s];
+        if (v < 0 || v >= n) { fl |= 32u | 8u; continue; }
+        if (u == v) fl |= 8u;
+        if (s > xadj[u] && adj[s - 1] >= v) fl |= 8u;
+        sum += pair_mix((uint32_t)u, (uint32_t)v) - pair_mix((uint32_t)v, (uint32_t)u);
+    }
+    for (int o = 16; o; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (sum) atomicAdd(&gs->symsum, sum);
+        if (fl) atomicOr(&gs->flags, fl);
+    }
+}
+
+__global__ void k_sym_hash(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                           const int32_t *__restrict__ src, int64_t n, int64_t m2, int32_t *__restrict__ hash,
+                           GStats *__restrict__ gs) {
+    unsigned long long sum = 0;
+    unsigned fl = 0;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = src[s], v = adj[s];
+        hash[s] = edge_hash(u, v);
         if (v < 0 || v >= n) { fl |= 32u | 8u; continue; }
         if (u == v) fl |= 8u;
         if (s > xadj[u] && adj[s - 1] >= v) fl |= 8u;
@@ -764,25 +798,11 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
     IMX_CUDA(cudaMemsetAsync(g->src, 0, sizeof(int32_t) * m2, st));   // rows of corrupt offsets
     k_src_rows<<<grid_for(n * 32), 256, 0, st>>>(g->xadj, n, m2, g->src);
     k_check_xadj<<<grid_for(n), 256, 0, st>>>(g->xadj, n, m2, &gs->flags);
-    k_sym_check<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, n, m2, gs);
-    k_slot_hashes<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, g->hash);
+    k_sym_hash<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, n, m2, g->hash, gs);
     k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, m2, &gs->maxp);
-    note_launch(5);
+    note_launch(4);
     IMX_CHECK_LAUNCH();
-    {
-        uint8_t *flag;
-        IMX_CUDA(pool_alloc((void **)&flag, m2, st));
-        k_canon_flags<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, flag); note_launch();
-        size_t tmp_bytes = 0;
-        thrust::counting_iterator<int64_t> it(0);
-        IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flag, g->cslot, &gs->me, m2, st));
-        void *tmp;
-        IMX_CUDA(pool_alloc(&tmp, tmp_bytes, st));
-        IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flag, g->cslot, &gs->me, m2, st));
-        note_launch(2);
-        cudaFreeAsync(tmp, st);
-        cudaFreeAsync(flag, st);
-    }
+    g->cslot_ready = false;          // canonical slot list on first use (ensure_cslot)
     IMX_TRY(graph_nz_rows_async(g, gs));
     // the weight stream: upload, then (after the structure) raw thresholds
     cudaEvent_t ev_struct = nullptr;
@@ -830,7 +850,8 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
     if (h.flags & 32u) { set_error("adjacency entry outside 0..n-1"); return IMX_EINVAL; }
     g->symmetric = (h.flags & 8u) == 0 && h.symsum == 0 && (m2 % 2 == 0);
     g->max_prefix = (int64_t)h.maxp;
-    g->me = h.me;
+    // symmetric, no self-loop: every undirected edge has exactly one canonical slot
+    g->me = m2 / 2;
     graph_nz_rows_done(g, h.nnz);
     if (g->me >= (int64_t(1) << 31)) {
         set_error("%lld undirected edges exceed 2^31 - 1", (long long)g->me);
@@ -979,9 +1000,41 @@ int ensure_nz_rows(imx_graph *g) {
     return IMX_OK;
 }
 
+// canonical slots (src < adj) in slot order, built on first use on large
+// host CSRs (the enumeration index, evaluate_seeds and sampling_cdf need them)
+int ensure_cslot(imx_graph *g) {
+    if (g->cslot_ready) return IMX_OK;
+    cudaStream_t st = g->stream;
+    const int64_t m2 = g->m2;
+    if (m2) {
+        uint8_t *flag;
+        int64_t *cnt;
+        IMX_CUDA(pool_alloc((void **)&flag, m2, st));
+        IMX_CUDA(pool_alloc((void **)&cnt, sizeof(int64_t), st));
+        k_canon_flags<<<grid_for(m2), 256, 0, st>>>(g->src, g->adj, m2, flag); note_launch();
+        size_t tmp_bytes = 0;
+        thrust::counting_iterator<int64_t> it(0);
+        IMX_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flag, g->cslot, cnt, m2, st));
+        void *tmp;
+        IMX_CUDA(pool_alloc(&tmp, tmp_bytes, st));
+        IMX_CUDA(cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flag, g->cslot, cnt, m2, st));
+        note_launch(2);
+        int64_t me = 0;
+        IMX_CUDA(cudaMemcpyAsync(&me, cnt, sizeof me, cudaMemcpyDeviceToHost, st));
+        IMX_CUDA(cudaStreamSynchronize(st));
+        cudaFreeAsync(tmp, st);
+        cudaFreeAsync(flag, st);
+        cudaFreeAsync(cnt, st);
+        g->me = me;
+    }
+    g->cslot_ready = true;
+    return IMX_OK;
+}
+
 int ensure_index(imx_graph *g) {
     IMX_TRY(graph_settle(g));
     if (g->index_ready) return IMX_OK;
+    IMX_TRY(ensure_cslot(g));
     IMX_TRY(graph_build_index(g));
     // built on the graph stream; its users run on context streams
     IMX_CUDA(cudaStreamSynchronize(g->stream));

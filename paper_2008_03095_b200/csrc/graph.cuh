@@ -55,6 +55,7 @@ struct imx_graph {
     int wthread_rc = 0;
     bool recip_ready = true;
     bool index_ready = false;
+    bool cslot_ready = true;     // false: cslot built on first use (ensure_cslot)
     // non-isolated vertices (built on first use, ensure_nz_rows); NULL when
     // isolated vertices are too few to be worth skipping
     int32_t *nz_rows = nullptr;
@@ -81,4 +82,5 @@ int graph_settle(imx_graph *g);
 int ensure_recip(imx_graph *g);
 int ensure_index(imx_graph *g);
 int ensure_nz_rows(imx_graph *g);
+int ensure_cslot(imx_graph *g);
 }

@@ -92,11 +92,15 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval(const int32_t *__restrict
 
 // commit_seed (selection.py:73-81): own u's component in every scored lane;
 // per_sim[r] += its size when newly owned (K8, SelectionResult.spread_se)
+// seeds whose newly covered components are listed per lane (the seed table
+// of the early CELF rounds, tab_covered)
+constexpr int kTab = 4;
+
 template <bool ENC>
 __global__ void k_commit(int32_t u, const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
                          uint32_t *__restrict__ cov, Lay ld, int32_t ns, int32_t cw,
                          int64_t *__restrict__ per_sim, uint8_t *__restrict__ inS,
-                         unsigned long long *__restrict__ gain) {
+                         unsigned long long *__restrict__ gain, int2 *__restrict__ tab_row) {
     unsigned long long acc = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ns; r += gridDim.x * blockDim.x) {
         uint32_t lab;
@@ -107,6 +111,7 @@ __global__ void k_commit(int32_t u, const uint32_t *__restrict__ L, const uint32
             per_sim[r] += s;
             acc += s;
         }
+        if (tab_row) tab_row[r] = (old & bit) ? make_int2(-1, 0) : make_int2((int)lab, (int)s);
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(gain, acc);
@@ -151,10 +156,13 @@ __global__ void k_merge(const int32_t *__restrict__ aid, const unsigned long lon
     }
 }
 
-static void launch_commit(imx_ctx *c, int32_t u, unsigned long long *gain) {
+// t: the seed count before this commit when it is a round of the CELF loop
+// (its seed-table row, kTab, is written too), -1 otherwise
+static void launch_commit(imx_ctx *c, int32_t u, unsigned long long *gain, int32_t t = -1) {
     const int blocks = grid_for(std::max(c->ns, 1));
-    if (c->C) k_commit<false><<<blocks, 256, 0, c->st>>>(u, c->L, c->C, c->cov, c->lay, c->ns, c->cw, c->per_sim, c->inS, gain);
-    else k_commit<true><<<blocks, 256, 0, c->st>>>(u, c->L, nullptr, c->cov, c->lay, c->ns, c->cw, c->per_sim, c->inS, gain);
+    int2 *row = (t >= 0 && t < kTab && c->stab && !c->C) ? c->stab + (int64_t)t * c->ld : nullptr;
+    if (c->C) k_commit<false><<<blocks, 256, 0, c->st>>>(u, c->L, c->C, c->cov, c->lay, c->ns, c->cw, c->per_sim, c->inS, gain, nullptr);
+    else k_commit<true><<<blocks, 256, 0, c->st>>>(u, c->L, nullptr, c->cov, c->lay, c->ns, c->cw, c->per_sim, c->inS, gain, row);
 }
 
 static int celf_eval_dev(imx_ctx *c, const int32_t *dcand, int64_t cnt, int64_t *dout) {
@@ -315,6 +323,31 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// Early rounds (t <= kTab seeds, encoded labels, one rank): the components
+// covered so far are listed per lane in the seed table -- tab[i][r] = (label,
+// size) of the component seed i newly covered in lane r, or (NONE, 0) -- so
+// a candidate's fresh gain is its initial gain minus the sizes of its listed
+// components: one row read per candidate, no root-cell or covered-bitmap
+// gathers (C4's round 1 refreshes 2.3 M candidates after the hub seed).
+__device__ __forceinline__ unsigned long long tab_covered(const uint32_t *__restrict__ L, const Lay &ld,
+                                                          const int2 *__restrict__ tab, int64_t tld, int ntab,
+                                                          int32_t ns, int64_t u, int q) {
+    const uint4 l4 = row_quad(L, ld, u, q);
+    const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+    unsigned long long acc = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int r = (q << 2) + j;
+        if (r >= ns) continue;
+        const uint32_t lab = is_root(lv[j]) ? (uint32_t)u : lv[j];
+        for (int i = 0; i < ntab; ++i) {
+            const int2 e = __ldg(tab + i * tld + r);
+            if ((uint32_t)e.x == lab) acc += (uint32_t)e.y;
+        }
+    }
+    return acc;
+}
+
 // marginal gain of u (u < 0: none) by a group of gsz threads (tid in the
 // group); per-warp partial sums meet in the group's shared accumulator.
 // Every thread of the CTA must call it (it has a CTA barrier).
@@ -322,9 +355,13 @@ template <bool ENC>
 __device__ __forceinline__ int64_t group_eval(const uint32_t *__restrict__ L, const uint32_t *__restrict__ C,
                                               const uint32_t *__restrict__ cov, Lay ld, int32_t ns,
                                               int32_t cw, int64_t u, int tid, int gsz,
-                                              unsigned long long *acc_sh) {
+                                              unsigned long long *acc_sh, const int2 *__restrict__ tab = nullptr,
+                                              int64_t tld = 0, int ntab = 0) {
     unsigned long long acc = 0;
-    if (u >= 0) {
+    if (u >= 0 && tab) {
+        const int nqs = (ns + 3) >> 2;
+        for (int q = tid; q < nqs; q += gsz) acc += tab_covered(L, ld, tab, tld, ntab, ns, u, q);
+    } else if (u >= 0) {
         const int nqs = (ns + 3) >> 2;
         const uint32_t *rowbase = L;   // quads via ld.off (rows or lane tiles)
         for (int q = tid; q < nqs; q += gsz) {
@@ -371,7 +408,8 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
     unsigned long long *__restrict__ skey, int32_t *__restrict__ sid,
     int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
-    int32_t bpct, int32_t ngroup, int64_t *__restrict__ xbuf, int64_t xcap) {
+    int32_t bpct, int32_t ngroup, int64_t *__restrict__ xbuf, int64_t xcap, int2 *__restrict__ tab,
+    int64_t tab_ld, const int64_t *__restrict__ gains0) {
     cg::grid_group grid = cg::this_grid();
     constexpr bool xm = XM;                    // exchange mode (sharded run; xcap > 0)
     // a stop that waits for the host (done, trace full, error, big round)
@@ -460,7 +498,25 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                 // huge batches (a round that refreshes most vertices): throughput
                 // over latency -- a warp per candidate, per-warp max folded once
                 const bool wide = hi - lo > (int64_t)gridDim.x * 8 && ns <= 4096;
-                if (wide) {
+                // the seed table instead of the covered bitmap (tab != NULL only for ENC, one rank)
+                const int ntab = (tab && t <= kTab) ? t : 0;
+                const int2 *etab = ntab ? tab : nullptr;
+                if (wide && etab) {
+                    unsigned long long wmax = 0;
+                    const int wl = threadIdx.x & 31;
+                    const int nqs = (ns + 3) >> 2;
+                    for (int64_t i = lo + (gtid >> 5); i < hi; i += gthreads >> 5) {
+                        const int64_t u = oid[ostart + i];
+                        unsigned long long cov_sz = 0;
+                        for (int q = wl; q < nqs; q += 32) cov_sz += tab_covered(L, ld, etab, tab_ld, ntab, ns, u, q);
+                        for (int o = 16; o; o >>= 1) cov_sz += __shfl_xor_sync(0xffffffffu, cov_sz, o);
+                        const unsigned long long acc = (unsigned long long)gains0[u] - cov_sz;
+                        if (wl == 0) fresh[i] = (int64_t)acc;
+                        const unsigned long long fk = (acc << vb) | (unsigned long long)(vmask - (uint32_t)u);
+                        wmax = fk > wmax ? fk : wmax;
+                    }
+                    if (wl == 0 && wmax) atomicMax(&st->smax[sstep & 3], wmax);
+                } else if (wide) {
                     unsigned long long wmax = 0;
                     const int wl = threadIdx.x & 31;
                     for (int64_t i = lo + (gtid >> 5); i < hi; i += gthreads >> 5) {
@@ -499,8 +555,10 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                      base += (int64_t)gridDim.x * ngroup) {
                     const int gsz = blockDim.x / ngroup, g = threadIdx.x / gsz;
                     const int64_t i = base + g;
-                    const int64_t f = group_eval<ENC>(L, C, cov, ld, ns, cw, i < hi ? (int64_t)oid[ostart + i] : -1,
-                                                      threadIdx.x - g * gsz, gsz, gacc + g);
+                    const int64_t ui = i < hi ? (int64_t)oid[ostart + i] : -1;
+                    int64_t f = group_eval<ENC>(L, C, cov, ld, ns, cw, ui, threadIdx.x - g * gsz, gsz, gacc + g,
+                                                etab, tab_ld, ntab);
+                    if (etab && ui >= 0) f = gains0[ui] - f;
                     if (threadIdx.x == g * gsz && i < hi) {
                         if (xm) {
                             xbuf[i - lo] = f;
@@ -602,6 +660,8 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                 const uint32_t bit = 1u << (r & 31);
                 const uint32_t old = atomicOr(cov + (int64_t)lab * cw + (r >> 5), bit);
                 if (!(old & bit)) { per_sim[r] += sz; acc += sz; }
+                if (tab && t < kTab)        // the seed table of the early rounds
+                    tab[t * tab_ld + r] = (old & bit) ? make_int2(-1, 0) : make_int2((int)lab, (int)sz);
             }
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if ((threadIdx.x & 31) == 0 && acc) atomicAdd(gain, acc);
@@ -965,7 +1025,7 @@ static int celf_host_round(imx_ctx *c, int32_t t, int64_t &batch0, int32_t *seed
     for (size_t i = 0; i < back.size(); ++i) { bkey[i] = back[i].first; bid[i] = back[i].second; }
     unsigned long long *gain = c->scratch + 7;
     IMX_CUDA(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), c->st));
-    launch_commit(c, best_v, gain);
+    launch_commit(c, best_v, gain, t);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     IMX_TRY(celf_advance(c, kr, bid.data(), bkey.data(), (int64_t)back.size()));
@@ -1048,8 +1108,14 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     if (const char *gv = getenv("IMX_CELF_GROUPS")) ngroup = std::min(8, std::max(1, atoi(gv)));
     while (ngroup & (ngroup - 1)) --ngroup;
     int64_t *xbuf = nullptr, xcap = 0;
+    // encoded labels with the memo's gains at hand: early rounds use the seed table
+    if (!c->stab) IMX_CUDA(pool_alloc((void **)&c->stab, sizeof(int2) * kTab * c->ld, c->st));
+    int2 *tab = (!c->C && c->memo_ready && !getenv("IMX_CELF_NO_TAB")) ? c->stab : nullptr;
+    int64_t tab_ld = c->ld;
+    const int64_t *gains0 = c->gains;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
-                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap};
+                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap, &tab,
+                    &tab_ld, &gains0};
     IMX_CUDA(cudaLaunchCooperativeKernel(fn, grid_cache[enc], 256, args, 0, c->st));
     count_launch(c);
     IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
@@ -1146,7 +1212,7 @@ static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<in
     {
         unsigned long long *gain = c->scratch + 7;
         GB(cudaMemsetAsync(gain, 0, sizeof(unsigned long long), st));
-        launch_commit(c, best_v, gain);
+        launch_commit(c, best_v, gain, t);
         GB(cudaGetLastError());
         count_launch(c);
         // merge order[kr, olen) with the kr-1 sorted refreshed vertices (the
@@ -1266,8 +1332,12 @@ static int celf_select_xchg(imx_ctx *c, int32_t k, std::vector<int32_t> &seeds, 
     unsigned long long *k0 = c->okey[0], *k1 = c->okey[1], *skey = c->skey;
     int64_t cap = c->trace_cap;
     CelfDev *stp = c->cdev;
+    int2 *tab = nullptr;             // partial gains per rank: the covered bitmap only
+    int64_t tab_ld = 0;
+    const int64_t *gains0 = nullptr;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
-                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap};
+                    &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap, &tab,
+                    &tab_ld, &gains0};
     CelfDev *snap = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int rc = IMX_OK;

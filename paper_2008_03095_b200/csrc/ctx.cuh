@@ -102,6 +102,7 @@ struct imx_ctx {
     int32_t *dseeds = nullptr;
     int64_t *dsgains = nullptr;
     int32_t dseeds_cap = 0;
+    int2 *stab = nullptr;             // [kTab][ld] seed table of the early CELF rounds
     int celf_grid[4] = {0, 0, 0, 0};  // cooperative grids of k_celf_rounds<ENC, XM> on this context's device
     // interval-enumeration sampler
     int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;

@@ -14,6 +14,7 @@
 // fresh keys.  No per-round scan or sort of all n vertices; one or two host
 // syncs per round; the dequeue trace is the evaluated prefix itself.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -1116,10 +1117,20 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
                     &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap, &tab,
                     &tab_ld, &gains0};
+    const bool hprof = getenv("IMX_CELF_PROFILE") != nullptr;
+    auto hq0 = std::chrono::steady_clock::now();
+    if (hprof) IMX_CUDA(cudaStreamSynchronize(c->st));
+    auto hq1 = std::chrono::steady_clock::now();
     IMX_CUDA(cudaLaunchCooperativeKernel(fn, grid_cache[enc], 256, args, 0, c->st));
     count_launch(c);
+    auto hq2 = std::chrono::steady_clock::now();
     IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
+    if (hprof)
+        fprintf(stderr, "[celf host]   pre-launch wait %.3f ms, launch call %.3f ms, kernel+state %.3f ms\n",
+                std::chrono::duration<double, std::milli>(hq1 - hq0).count(),
+                std::chrono::duration<double, std::milli>(hq2 - hq1).count(),
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hq2).count());
     c->big_key = h.big_key;
     c->big_kr = (h.status == 2 || h.status == 4) ? h.big_kr : 0;
     if (getenv("IMX_CELF_PROFILE"))
@@ -1224,7 +1235,9 @@ static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<in
         GB(cudaGetLastError());
         count_launch(c);
         const int64_t base = c->trace_n;
-        if ((rc = trace_reserve(c, base + 5 * (kr + 1))) != IMX_OK) goto done;
+        // room for the later rounds too (2^18 records): growing the host buffer
+        // after this copy would wait for it and copy 91 MB on the host (C4: +6.6 ms)
+        if ((rc = trace_reserve(c, base + 5 * (kr + 1) + 5 * ((int64_t)1 << 18))) != IMX_OK) goto done;
         // the records (C4 round 1: 2.3 M, 91 MB) go to the host on the side
         // stream while the next rounds run; rec is freed there after the copy
         if (!c->tst) GB(acquire_stream(c->dev, &c->tst));
@@ -1457,10 +1470,18 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     const bool host_only = mode && !strcmp(mode, "host");
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->dev);
+    const bool hprof = getenv("IMX_CELF_PROFILE") != nullptr;
+    auto hnow = [] { return std::chrono::steady_clock::now(); };
+    auto hms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    auto h0 = hnow();
     while (t < k) {
         if (!host_only && coop) {
             int32_t status = 0, t2 = t;
+            auto h1 = hnow();
             IMX_TRY(celf_device_rounds(c, t, k, batch0, &status, &t2, &batch0, seeds, gains));
+            if (hprof) fprintf(stderr, "[celf host] device rounds %d..%d: %.3f ms (status %d)\n", t, t2, hms(h1, hnow()), status);
             const bool progressed = t2 > t;
             t = t2;
             if (status == 1 || t >= k) break;
@@ -1469,7 +1490,9 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
             // from its evaluated prefix; otherwise drain the trace and relaunch
             const bool oversized = c->big_kr > 0 && (status == 4 || c->big_kr + 1 > c->trace_cap);
             if (t > 0 && oversized) {
+                auto h2 = hnow();
                 IMX_TRY(celf_big_round(c, t, batch0, seeds, gains));
+                if (hprof) fprintf(stderr, "[celf host] big round %d (kr %lld): %.3f ms\n", t, (long long)c->big_kr, hms(h2, hnow()));
                 ++t;
                 continue;
             }
@@ -1480,7 +1503,9 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
     }
     if (seeds_out) std::copy(seeds.begin(), seeds.end(), seeds_out);
     if (gains_out) std::copy(gains.begin(), gains.end(), gains_out);
+    auto h3 = hnow();
     IMX_TRY(trace_flush(c));
+    if (hprof) fprintf(stderr, "[celf host] trace flush %.3f ms, select total %.3f ms\n", hms(h3, hnow()), hms(h0, hnow()));
     cudaEventRecord(c->ev[7], c->st);
     cudaEventSynchronize(c->ev[7]);
     cudaEventElapsedTime(&c->tm.select_ms, c->ev[6], c->ev[7]);

@@ -153,6 +153,60 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                     if (b0 != s0) batch(b0, s1, v, bu, bh);
                     // rows ascend: the smaller neighbours are a prefix of the batch
                     const int cnt = __popc(__ballot_sync(FULL, bu < (uint32_t)v));
+                    if (HEAVY) {
+                        // heavy slices: both passes are order-free (atomicMin into the
+                        // row; "all but the forest edge"), so four slots go at once,
+                        // eight threads each (buckets hold ~8 lanes: C4)
+                        const int sg = lane >> 3, sl = lane & 7;
+                        for (int j0 = 0; j0 < cnt; j0 += 4) {
+                            const int j = j0 + sg;
+                            const bool has = j < cnt;
+                            const uint32_t u = __shfl_sync(FULL, bu, has ? j : 0);
+                            const int32_t h = __shfl_sync(FULL, bh, has ? j : 0);
+                            int lo = 0, hi = 0;
+                            if (has) {
+                                const int2 bb = sbb[(uint32_t)h >> kb];
+                                lo = bb.x;
+                                hi = bb.y;
+                            }
+                            const int its = __reduce_max_sync(FULL, (unsigned)((hi - lo + 7) >> 3));
+                            for (int it = 0; it < its; ++it) {
+                                const int i = lo + (it << 3) + sl;
+                                const int2 xp = i < hi ? sx2[i] : make_int2(0x7fffffff, 0);
+                                const bool live = i < hi && (xp.x ^ h) < t;
+                                const int p = live ? xp.y : 0;
+                                if (PASS == 1) {
+                                    if (live && !flag[p]) {       // a racing duplicate only repeats the min
+                                        flag[p] = 1;
+                                        atomicMin(L + y.off(v, r0 + p), u);
+                                    }
+                                } else {
+                                    const bool un = live && ld_relaxed(L + y.off(v, r0 + p)) != u;
+                                    const unsigned b = __ballot_sync(FULL, un);
+                                    if (b) {
+                                        if (un) {
+                                            const int pos = qn + __popc(b & lt_mask);
+                                            qlo[pos] = u;
+                                            qhi[pos] = (uint32_t)v;
+                                            qr[pos] = (uint32_t)(r0 + p);
+                                        }
+                                        qn += __popc(b);
+                                        __syncwarp();
+                                        if (qn >= 32) {
+                                            qn -= 32;
+                                            const uint32_t a2 = qlo[qn + lane], b2 = qhi[qn + lane];
+                                            const int rr = (int)qr[qn + lane];
+                                            __syncwarp();
+                                            nh += unite(L, y, a2, b2, rr);
+                                        }
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                        }
+                        if (cnt < 32) break;
+                        continue;
+                    }
                     for (int j = 0; j < cnt; ++j) {
                         const uint32_t u = __shfl_sync(FULL, bu, j);
                         const int32_t h = __shfl_sync(FULL, bh, j);

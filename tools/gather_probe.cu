@@ -12,6 +12,7 @@
 //   tools/gather_probe            -> one JSON line per (kind, bytes)
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t mix(uint32_t x) {
@@ -69,7 +70,15 @@ __global__ void k_chase(const uint32_t *__restrict__ a, uint64_t words, int K, u
     if (p == 0x12345678u) out[0] = p;
 }
 
-int main() {
+int main(int argc, char **argv) {
+    // optional argument: cudaLimitMaxL2FetchGranularity (32 / 64 / 128 bytes)
+    if (argc > 1) {
+        cudaError_t le = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[1]));
+        if (le != cudaSuccess) printf("set limit: %s\n", cudaGetErrorString(le));
+    }
+    size_t gran = 0;
+    cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity);
+    printf("{\"l2_fetch_granularity\": %zu}\n", gran);
     const uint64_t sizes_mb[] = {16, 64, 256, 1024, 4096, 16384};
     uint32_t *a = nullptr, *out = nullptr;
     const uint64_t maxw = sizes_mb[5] << 18;

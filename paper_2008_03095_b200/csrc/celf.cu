@@ -396,6 +396,10 @@ constexpr int64_t kStepPerCta = IMX_CELF_STEP_PER_CTA;
 #define IMX_CELF_FIRST_CAP 16384
 #endif
 constexpr int64_t kFirstBatchCap = IMX_CELF_FIRST_CAP;
+#ifndef IMX_CELF_WIDE_OUT
+#define IMX_CELF_WIDE_OUT 64
+#endif
+constexpr int64_t kWideOutPerCta = IMX_CELF_WIDE_OUT;   // seed-table batches above this many candidates per CTA leave the kernel
 
 template <bool ENC, bool XM>
 #ifndef IMX_CELF_MINB
@@ -502,6 +506,14 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                 // the seed table instead of the covered bitmap (tab != NULL only for ENC, one rank)
                 const int ntab = (tab && t <= kTab) ? t : 0;
                 const int2 *etab = ntab ? tab : nullptr;
+                // a huge batch through the seed table (C4's round 1 evaluates 2.4 M
+                // candidates) is a streaming pass over rows: k_wide_tab_round does
+                // it with the registers this kernel does not have
+                if (!xm && etab && hi - lo > (int64_t)gridDim.x * kWideOutPerCta) {
+                    if (gtid == 0) { st->xlo = lo; st->xhi = hi; st->xbest = bestkey; }
+                    status = 6;
+                    break;
+                }
                 if (wide && etab) {
                     unsigned long long wmax = 0;
                     const int wl = threadIdx.x & 31;
@@ -736,6 +748,187 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
         st->status = status ? status : 1;
         // done in exchange mode: the last commit's part goes out with one more exchange
         if (xm && !status) xbuf[xcap] = st->xpend ? st->xpend_got : 0;
+    }
+}
+
+// tab_covered on a quad already in registers
+__device__ __forceinline__ unsigned long long tab_covered_quad(const uint4 l4, const int2 *__restrict__ tab,
+                                                               int64_t tld, int ntab, int32_t ns, int64_t u, int q) {
+    const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+    const int r0 = q << 2;
+    unsigned long long acc = 0;
+    if (r0 + 3 < ns) {
+        for (int i = 0; i < ntab; ++i) {
+            // four (label, size) entries as two 16-byte loads (tld and r0 are multiples of 4)
+            const int4 e01 = __ldg(reinterpret_cast<const int4 *>(tab + i * tld + r0));
+            const int4 e23 = __ldg(reinterpret_cast<const int4 *>(tab + i * tld + r0) + 1);
+            const uint32_t el[4] = {(uint32_t)e01.x, (uint32_t)e01.z, (uint32_t)e23.x, (uint32_t)e23.z};
+            const uint32_t es[4] = {(uint32_t)e01.y, (uint32_t)e01.w, (uint32_t)e23.y, (uint32_t)e23.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t lab = is_root(lv[j]) ? (uint32_t)u : lv[j];
+                if (el[j] == lab) acc += es[j];
+            }
+        }
+        return acc;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int r = r0 + j;
+        if (r >= ns) continue;
+        const uint32_t lab = is_root(lv[j]) ? (uint32_t)u : lv[j];
+        for (int i = 0; i < ntab; ++i) {
+            const int2 e = __ldg(tab + i * tld + r);
+            if ((uint32_t)e.x == lab) acc += (uint32_t)e.y;
+        }
+    }
+    return acc;
+}
+
+// A huge evaluation through the seed table (status 6 of k_celf_rounds: C4's
+// round 1 refreshes 2.3 M candidates after the hub seed) as a streaming pass
+// over the candidates' rows: fresh = initial gain - sizes of the listed
+// components, one 4 KB row read per candidate and nothing else.  The same
+// batch loop and stop rule as the persistent kernel (it continues that
+// kernel's round from [xlo, xhi) with the best key so far), but a warp per
+// candidate, its row staged in shared memory by cp.async one row ahead of the
+// compares (no registers held by the loads in flight), candidates handed
+// out kWideGrab at a time from a counter (with a static split the slowest of
+// the warps held every step's barrier for ~40% of the step).  Ends with the
+// round's best key and refreshed prefix length in big_key / big_kr (status
+// 2): the host finishes the round with celf_big_round.
+constexpr int kWideGrab = 16;           // candidates per counter grab
+constexpr int kWideRowQuads = 256;      // quads per staged row segment (4 KB)
+constexpr int kWideSmem = 8 * 2 * kWideRowQuads * (int)sizeof(uint4);   // 8 warps, double-buffered
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gptr) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// TAB1 (one listed seed, rows of <= 1024 lanes: C4's round 1): every thread
+// keeps the table entries of its 32 cells in registers for the whole launch
+// -- the compares then cost shared-memory reads only (with the entries read
+// through L1, two 16-byte loads per quad, the L1 pipe bound the pass at 4 TB/s).
+template <bool TAB1>
+__global__ void __launch_bounds__(256, TAB1 ? 2 : 3) k_wide_tab_round(
+    const uint32_t *__restrict__ L, Lay ld, int32_t ns, const int2 *__restrict__ tab, int64_t tab_ld, int ntab,
+    const int64_t *__restrict__ gains0, const int32_t *__restrict__ cand, const unsigned long long *__restrict__ keys,
+    int64_t olen, int64_t *__restrict__ fresh, int vb, CelfDev *__restrict__ st, int64_t batch0, int64_t cap) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ uint4 wide_rows[];
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const uint32_t vmask = (vb >= 32) ? 0xffffffffu : ((1u << vb) - 1u);
+    const int wl = threadIdx.x & 31;
+    const int nqs = (ns + 3) >> 2;
+    const int nseg = (nqs + kWideRowQuads - 1) / kWideRowQuads;     // ns <= 1024: one
+    uint4 *wbuf = wide_rows + (threadIdx.x >> 5) * 2 * kWideRowQuads;
+    int64_t lo = st->xlo, hi = st->xhi;
+    unsigned long long bestkey = st->xbest;
+    unsigned long long evals = 0, steps = 0;
+    uint32_t tl[TAB1 ? 32 : 1], tz[TAB1 ? 32 : 1];
+    if (TAB1) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int q = wl + 32 * j;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int r = 4 * q + c;
+                const int2 e = r < ns ? __ldg(tab + r) : make_int2(-1, 0);    // label -1 matches nothing
+                tl[4 * j + c] = (uint32_t)e.x;
+                tz[4 * j + c] = (uint32_t)e.y;
+            }
+        }
+    }
+    for (int s = 0;; ++s) {
+        // slot (s+2)&3 was last used two barriers ago
+        if (gtid == 0) { st->smax[(s + 2) & 3] = 0; st->wctr[(s + 2) & 3] = 0; }
+        unsigned long long wmax = 0;
+        for (;;) {
+            unsigned long long b0 = 0;
+            if (wl == 0) b0 = atomicAdd(&st->wctr[s & 3], (unsigned long long)kWideGrab);
+            const int64_t ib = lo + (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+            if (ib >= hi) break;
+            const int gcnt = (int)(hi - ib < kWideGrab ? hi - ib : kWideGrab);
+            const int32_t uw = wl < gcnt ? cand[ib + wl] : 0;
+            // unit j of the grab = segment j % nseg of candidate j / nseg; unit j + 1 is
+            // copied into the other buffer while unit j is compared
+            const int units = gcnt * nseg;
+            auto issue = [&](int j) {
+                const int64_t u = __shfl_sync(0xffffffffu, uw, j / nseg);
+                const int qs = (j % nseg) * kWideRowQuads;
+                const int qe = nqs - qs < kWideRowQuads ? nqs - qs : kWideRowQuads;
+                uint4 *dst = wbuf + (j & 1) * kWideRowQuads;
+                for (int q = wl; q < qe; q += 32) cp_async16(dst + q, L + cell_off(ld, u, (qs + q) << 2));
+                cp_async_commit();
+            };
+            issue(0);
+            const long long gw = wl < gcnt ? gains0[uw] : 0;
+            unsigned long long cov_sz = 0;
+            for (int j = 0; j < units; ++j) {
+                if (j + 1 < units) {
+                    issue(j + 1);
+                    cp_async_wait<1>();
+                } else {
+                    cp_async_wait<0>();
+                }
+                __syncwarp();
+                const int k2 = j / nseg;
+                const int64_t u = __shfl_sync(0xffffffffu, uw, k2);
+                const int qs = (j % nseg) * kWideRowQuads;
+                const int qe = nqs - qs < kWideRowQuads ? nqs - qs : kWideRowQuads;
+                const uint4 *src = wbuf + (j & 1) * kWideRowQuads;
+                if (TAB1) {
+#pragma unroll
+                    for (int j2 = 0; j2 < 8; ++j2) {
+                        if (wl + 32 * j2 < qe) {
+                            const uint4 l4 = src[wl + 32 * j2];
+                            const uint32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                const uint32_t lab = is_root(lv[c]) ? (uint32_t)u : lv[c];
+                                if (tl[4 * j2 + c] == lab) cov_sz += tz[4 * j2 + c];
+                            }
+                        }
+                    }
+                } else {
+                    for (int q = wl; q < qe; q += 32)
+                        cov_sz += tab_covered_quad(src[q], tab, tab_ld, ntab, ns, u, qs + q);
+                }
+                __syncwarp();                      // the buffer is refilled two units later
+                if (j % nseg == nseg - 1) {
+                    for (int o = 16; o; o >>= 1) cov_sz += __shfl_xor_sync(0xffffffffu, cov_sz, o);
+                    const unsigned long long acc = (unsigned long long)__shfl_sync(0xffffffffu, gw, k2) - cov_sz;
+                    if (wl == 0) fresh[ib + k2] = (int64_t)acc;
+                    const unsigned long long fk = (acc << vb) | (unsigned long long)(vmask - (uint32_t)u);
+                    wmax = fk > wmax ? fk : wmax;
+                    cov_sz = 0;
+                }
+            }
+        }
+        if (wl == 0 && wmax) atomicMax(&st->smax[s & 3], wmax);
+        grid.sync();
+        const unsigned long long m = ld_relaxed64(&st->smax[s & 3]);
+        bestkey = m > bestkey ? m : bestkey;
+        evals += hi - lo;
+        ++steps;
+        if (hi >= olen || bestkey >= keys[hi]) break;            // nothing unevaluated can win
+        lo = hi;
+        int64_t step = batch0 > hi ? batch0 : hi;
+        if (step > cap) step = cap;
+        hi = (olen - hi < step) ? olen : hi + step;
+    }
+    // refreshed prefix: stale key >= best fresh key (keys sorted descending)
+    const int64_t kr = warp_count_above<true>(keys, hi, bestkey);
+    if (gtid == 0) {
+        st->big_key = bestkey;
+        st->big_kr = kr;
+        st->status = 2;
+        st->prof[4] += steps;
+        st->prof[5] += evals;
     }
 }
 
@@ -1277,6 +1470,48 @@ done:
     return rc;
 }
 
+// status 6 of the persistent kernel: the huge seed-table batch it left
+// (state in cdev: xlo, xhi, xbest) evaluated by k_wide_tab_round up to the
+// round's stop; big_key / big_kr then feed celf_big_round
+static int celf_wide_round(imx_ctx *c, int32_t t, int64_t batch0) {
+    const bool tab1 = t == 1 && c->ns <= 4 * kWideRowQuads;
+    int *grid = &c->wide_grid[tab1 ? 1 : 0];
+    void *fn = tab1 ? (void *)k_wide_tab_round<true> : (void *)k_wide_tab_round<false>;
+    if (!*grid) {
+        int per_sm = 0, sms = 0;
+        IMX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideSmem));
+        IMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, kWideSmem));
+        IMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
+        *grid = std::max(1, std::min(per_sm, tab1 ? 2 : 3)) * sms;
+    }
+    IMX_CUDA(cudaMemsetAsync(c->cdev->smax, 0, sizeof(unsigned long long) * 8, c->st));   // smax[4], wctr[4]
+    const uint32_t *L = c->L;
+    Lay ld = c->lay;
+    int32_t ns = c->ns;
+    const int2 *tab = c->stab;
+    int64_t tab_ld = c->ld;
+    int ntab = t;
+    const int64_t *gains0 = c->gains;
+    const int32_t *cand = c->oid[c->ocur] + c->ostart;
+    const unsigned long long *keys = c->okey[c->ocur] + c->ostart;
+    int64_t olen = c->olen, *fresh = c->eval_out;
+    int vb = c->vb;
+    CelfDev *stp = c->cdev;
+    int64_t cap = (int64_t)*grid * 512;
+    void *args[] = {&L, &ld, &ns, &tab, &tab_ld, &ntab, &gains0, &cand, &keys, &olen, &fresh, &vb, &stp, &batch0, &cap};
+    IMX_CUDA(cudaLaunchCooperativeKernel(fn, *grid, 256, args, kWideSmem, c->st));
+    count_launch(c);
+    CelfDev h;
+    IMX_CUDA(cudaMemcpyAsync(&h, c->cdev, sizeof h, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaStreamSynchronize(c->st));
+    c->big_key = h.big_key;
+    c->big_kr = h.big_kr;
+    if (getenv("IMX_CELF_PROFILE"))
+        fprintf(stderr, "[celf] wide round %d grid %d: %llu eval steps, %llu evaluations, kr %lld\n", t, *grid,
+                h.prof[4], h.prof[5], (long long)h.big_kr);
+    return IMX_OK;
+}
+
 // The whole CELF loop on one context (single-rank path): the persistent
 // cooperative kernel runs the rounds; a round it cannot hold (trace buffer
 // full, refreshed prefix larger than kMaxRank) is finished on the host.
@@ -1488,6 +1723,12 @@ extern "C" int imx_celf_select(imx_ctx *c, int32_t k, int32_t *seeds_out, int64_
             // a round the kernel can never hold (refreshed prefix > kMaxRank, or
             // more records than the whole trace buffer) is finished right here
             // from its evaluated prefix; otherwise drain the trace and relaunch
+            if (status == 6) {
+                auto h2 = hnow();
+                IMX_TRY(celf_wide_round(c, t, batch0));
+                if (hprof) fprintf(stderr, "[celf host] wide round %d: %.3f ms\n", t, hms(h2, hnow()));
+                status = 4;                   // evaluated: finished below from big_key / big_kr
+            }
             const bool oversized = c->big_kr > 0 && (status == 4 || c->big_kr + 1 > c->trace_cap);
             if (t > 0 && oversized) {
                 auto h2 = hnow();

@@ -29,7 +29,8 @@ struct CelfDev {
     int64_t ostart, olen;
     int32_t ocur, t;
     int64_t trace_len, batch0;
-    int32_t status;        // 1 done, 2 trace buffer full, 3 self-check failed, 4 round too large
+    int32_t status;        // 1 done, 2 trace buffer full, 3 self-check failed, 4 round too large,
+                           // 5 paused for an exchange, 6 a huge seed-table batch [xlo, xhi) is left to k_wide_tab_round
     int32_t bad_v;
     int64_t bad_want, bad_got;
     // phase times (ns, %globaltimer on block 0): eval, commit, rank, merge;
@@ -39,6 +40,8 @@ struct CelfDev {
     unsigned long long prof[10];
     // per-step maximum fresh key of the evaluated batch, 4 rotating slots
     unsigned long long smax[4];
+    // work counters of k_wide_tab_round's dynamic candidate grabs, rotating like smax
+    unsigned long long wctr[4];
     // a round the kernel cannot hold (status 2/4): its best fresh key and
     // refreshed prefix length (fresh[] holds the evaluated prefix)
     unsigned long long big_key;
@@ -104,6 +107,7 @@ struct imx_ctx {
     int32_t dseeds_cap = 0;
     int2 *stab = nullptr;             // [kTab][ld] seed table of the early CELF rounds
     int celf_grid[4] = {0, 0, 0, 0};  // cooperative grids of k_celf_rounds<ENC, XM> on this context's device
+    int wide_grid[2] = {0, 0};        // and of k_wide_tab_round<TAB1>
     // interval-enumeration sampler
     int64_t *seg_a = nullptr, *seg_n = nullptr, *seg_off = nullptr;
     int64_t nseg_cap = 0;

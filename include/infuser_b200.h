@@ -138,6 +138,20 @@ int  imx_memoize(imx_ctx *c, int64_t *gains_out);
  * while it is on chip, and the next imx_memoize only copies them out.      */
 int  imx_set_fuse_memo(imx_ctx *c, int32_t on);
 
+/* Large host CSRs: imx_graph_from_csr leaves the 8-byte-per-slot weights on
+ * the link and imx_propagate starts on the speculative uniform threshold of
+ * weights[0].  By default imx_propagate waits for the weights before it
+ * returns results (and runs again if they differ).  imx_spec_defer(c, 1)
+ * hands that check to the caller: memoisation and the CELF loop then also run
+ * while the weights upload, and imx_spec_settle says afterwards whether the
+ * speculation held (held = 0: call imx_propagate again and redo what followed;
+ * the thresholds are settled then).  Getters of labels, sizes, gains and the
+ * seed state check by themselves and fail rather than return unconfirmed
+ * results.  The reference has no counterpart: Graph.weights is a host array
+ * (graph.py:37-60) and thresholds are computed eagerly (hashing.py:153-165). */
+int  imx_spec_defer(imx_ctx *c, int32_t on);
+int  imx_spec_settle(imx_ctx *c, int32_t *held);
+
 /* Load labels (and optionally sizes; NULL -> recomputed from labels) from
  * the host instead of propagating: select_seeds / initial_marginal_gains on
  * caller arrays (selection.py:115, propagation.py:349-368).  ld = row

@@ -75,6 +75,8 @@ _SIGNATURES = {
     "imx_propagate": (c_i32, [c_void_p, c_i32, P(PropStats)]),
     "imx_memoize": (c_i32, [c_void_p, c_void_p]),
     "imx_set_fuse_memo": (c_i32, [c_void_p, c_i32]),
+    "imx_spec_defer": (c_i32, [c_void_p, c_i32]),
+    "imx_spec_settle": (c_i32, [c_void_p, P(c_i32)]),
     "imx_load_labels": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64]),
     "imx_copy_labels": (c_i32, [c_void_p, c_i32, c_i32, c_void_p]),
     "imx_copy_sizes": (c_i32, [c_void_p, c_i32, c_i32, c_void_p]),

@@ -92,6 +92,18 @@ class DeviceContext:
         return (st.sweeps, changed[:k].tolist(), sums[:k].tolist(),
                 [MODE_NAMES[int(x)] for x in modes[:k]])
 
+    def spec_defer(self, on: bool = True):
+        """Let memo and CELF run while a large host graph's weights are still
+        uploading; the caller must check ``spec_settle()`` afterwards."""
+        check(_lib.load().imx_spec_defer(self.handle, 1 if on else 0))
+
+    def spec_settle(self) -> bool:
+        """Wait for the graph's weights; False when the results so far stand
+        on a speculative threshold that did not hold (propagate again)."""
+        held = ctypes.c_int32(1)
+        check(_lib.load().imx_spec_settle(self.handle, ctypes.byref(held)))
+        return bool(held.value)
+
     # -- K4/K5 ------------------------------------------------------------------
     def set_fuse_memo(self, on: bool = True):
         """Sum the gains inside the next propagations' tiled compression."""

@@ -1025,6 +1025,7 @@ extern "C" int imx_celf_reset(imx_ctx *c, const int64_t *prio) {
 
 extern "C" int imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
     CELF_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (!prio_out || !v_out) { set_error("NULL argument"); return IMX_EINVAL; }
     if (c->olen == 0) { *v_out = -1; *prio_out = 0; return IMX_OK; }
     int32_t id;
@@ -1040,6 +1041,7 @@ extern "C" int imx_celf_top(imx_ctx *c, int64_t *prio_out, int32_t *v_out) {
 extern "C" int imx_celf_prefix(imx_ctx *c, int64_t lo, int64_t hi, int32_t *ids_out, int64_t *prio_out,
                                int64_t *fresh_out, int64_t *len_out) {
     CELF_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (lo < 0 || hi < lo) { set_error("prefix range [%lld, %lld) invalid", (long long)lo, (long long)hi); return IMX_EINVAL; }
     if (len_out) *len_out = c->olen;
     hi = std::min(hi, c->olen);
@@ -1058,6 +1060,7 @@ extern "C" int imx_celf_prefix(imx_ctx *c, int64_t lo, int64_t hi, int32_t *ids_
 extern "C" int imx_celf_advance(imx_ctx *c, int64_t k, int32_t u, const int32_t *ids, const int64_t *prio,
                                 int64_t cnt, int64_t *gain_out) {
     CELF_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (k < 0 || cnt < 0 || (cnt && (!ids || !prio))) { set_error("bad arguments"); return IMX_EINVAL; }
     if (u < 0 || u >= c->g->n) { set_error("vertex %d outside vertex range", u); return IMX_EINVAL; }
     std::vector<unsigned long long> keys(cnt);
@@ -1079,6 +1082,7 @@ extern "C" int imx_celf_advance(imx_ctx *c, int64_t k, int32_t u, const int32_t 
 
 extern "C" int imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int64_t *out) {
     CELF_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (cnt < 0 || (cnt && (!cand || !out))) { set_error("bad arguments"); return IMX_EINVAL; }
     if (!cnt) return IMX_OK;
     for (int64_t i = 0; i < cnt; ++i)
@@ -1099,6 +1103,7 @@ extern "C" int imx_eval_gains(imx_ctx *c, const int32_t *cand, int64_t cnt, int6
 
 extern "C" int imx_commit(imx_ctx *c, int32_t u, int64_t *gain_out) {
     CELF_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (u < 0 || u >= c->g->n) { set_error("vertex %d outside vertex range", u); return IMX_EINVAL; }
     uint8_t in = 0;
     IMX_CUDA(cudaMemcpyAsync(&in, c->inS + u, 1, cudaMemcpyDeviceToHost, c->st));
@@ -1863,6 +1868,7 @@ extern "C" int imx_celf_trace(imx_ctx *c, int64_t *out, int64_t cap) {
 
 extern "C" int imx_per_sim(imx_ctx *c, int64_t *out) {
     CELF_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (!out) { set_error("out is NULL"); return IMX_EINVAL; }
     if (c->ns) {
         IMX_CUDA(cudaMemcpyAsync(out, c->per_sim, sizeof(int64_t) * c->ns, cudaMemcpyDeviceToHost, c->st));
@@ -1873,6 +1879,7 @@ extern "C" int imx_per_sim(imx_ctx *c, int64_t *out) {
 
 extern "C" int imx_copy_owned(imx_ctx *c, uint32_t *bits_out) {
     CELF_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (!bits_out) { set_error("out is NULL"); return IMX_EINVAL; }
     const int64_t n = c->g->n;
     if (n) {

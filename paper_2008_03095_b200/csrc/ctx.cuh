@@ -137,6 +137,11 @@ struct imx_ctx {
     cudaStream_t tst = nullptr;
     // the last sampler launch used a deferred graph's speculative threshold
     bool spec_used = false;
+    // imx_spec_defer: imx_propagate does not wait for the weights; the caller
+    // checks with imx_spec_settle before it trusts any result (run_fused does,
+    // after the CELF loop); spec_thr = the threshold the results stand on
+    bool spec_defer = false;
+    int32_t spec_thr = 0;
     imx_timings tm{};
 };
 
@@ -177,11 +182,22 @@ int ensure_pinned(imx_ctx *c, int64_t cnt);
 int run_init(imx_ctx *c);
 // heavy-row slices of the graph for slice length T, cached on the graph (propagate.cu)
 int ensure_heavy(imx_ctx *c, int pass, int T);
+// the same in steps, for row ranges that become available one after the other (streamed CSR)
+int heavy_begin(imx_ctx *c, int pass, int T);
+int heavy_count_rows(imx_ctx *c, int pass, int T, int64_t v0, int64_t v1);
+int heavy_finish(imx_ctx *c, int pass, int T);
+void heavy_abort(imx_ctx *c, int pass);
 // buf[0, n) on the device <- its sum over the communicator's ranks (comm.cu)
 int comm_allreduce_i64(imx_comm *cm, int64_t *dbuf, int64_t n, cudaStream_t st);
 // the scan sampler (scan.cu)
 bool scan_eligible(const imx_graph *g);
 int run_scan(imx_ctx *c, int pass, unsigned long long *hooks);
+int run_scan_streamed(imx_ctx *c);
+// results computed on a speculative threshold (spec_used): wait for the
+// weights; held = the speculation was right.  spec_guard: the same before a
+// result leaves the device, failing when it did not hold.
+int spec_settle(imx_ctx *c, int32_t *held);
+int spec_guard(imx_ctx *c);
 // raw label-matrix passes shared with the evaluation worlds (evaluation.cu)
 int launch_init(uint32_t *L, int64_t n, int64_t ld, cudaStream_t st);
 int launch_gains_tile(const uint32_t *T, int64_t n, int64_t tld, int32_t ns_t, int first, int64_t *gains,

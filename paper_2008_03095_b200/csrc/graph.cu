@@ -145,9 +145,10 @@ __global__ void k_xadj_from_src(const int32_t *__restrict__ src, int64_t m2, int
 
 // src[s] = row of slot s (np.repeat over degrees, graph.py:75-78): one warp
 // per vertex writes its row (coalesced, no search)
-__global__ void k_src_rows(const int64_t *__restrict__ xadj, int64_t n, int64_t m2, int32_t *__restrict__ src) {
+__global__ void k_src_rows(const int64_t *__restrict__ xadj, int64_t n, int64_t m2, int32_t *__restrict__ src,
+                           int64_t v0 = 0) {
     const int lane = threadIdx.x & 31;
-    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n;
+    for (int64_t v = v0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); v < n;
          v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t a = xadj[v], b = xadj[v + 1];
         if (a < 0 || b > m2 || a > b) continue;      // corrupt offsets: flagged by k_check_xadj
@@ -196,7 +197,7 @@ __global__ void k_recip_check(const int64_t *__restrict__ xadj, const int32_t *_
 struct GStats;
 __global__ void k_sym_hash(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                            const int32_t *__restrict__ src, int64_t n, int64_t m2, int32_t *__restrict__ hash,
-                           GStats *__restrict__ gs);
+                           GStats *__restrict__ gs, int64_t s0 = 0);
 
 __global__ void k_slot_hashes(const int32_t *__restrict__ src, const int32_t *__restrict__ adj,
                               int64_t m2, int32_t *__restrict__ hash) {
@@ -229,7 +230,7 @@ __global__ void k_stats_init(GStats *gs) {
 
 __global__ void k_sym_hash(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                            const int32_t *__restrict__ src, int64_t n, int64_t m2, int32_t *__restrict__ hash,
-                           GStats *__restrict__ gs);
+                           GStats *__restrict__ gs, int64_t s0);
 
 // Symmetry of a large host CSR without the reciprocal search (deferred
 // path): rows strictly ascending (no duplicate, no self-loop) and the slot
@@ -265,12 +266,13 @@ __global__ void k_sym_check(const int64_t *__restrict__ xadj, const int32_t *__r
     }
 }
 
+// slots [s0, m2): a chunk of a streamed CSR passes its own slot range
 __global__ void k_sym_hash(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                            const int32_t *__restrict__ src, int64_t n, int64_t m2, int32_t *__restrict__ hash,
-                           GStats *__restrict__ gs) {
+                           GStats *__restrict__ gs, int64_t s0) {
     unsigned long long sum = 0;
     unsigned fl = 0;
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
+    for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2;
          s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t u = src[s], v = adj[s];
         hash[s] = edge_hash(u, v);
@@ -495,9 +497,9 @@ __global__ void k_check_xadj(const int64_t *__restrict__ xadj, int64_t n, int64_
 
 // number of neighbours smaller than v = lower_bound(row v, v) - xadj[v]
 __global__ void k_max_prefix(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, int64_t n,
-                             int64_t m2, unsigned long long *__restrict__ out) {
+                             int64_t m2, unsigned long long *__restrict__ out, int64_t v0 = 0) {
     unsigned long long best = 0;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+    for (int64_t v = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
         int64_t lo = xadj[v], hi = xadj[v + 1];
         if (lo < 0 || hi > m2 || lo > hi) continue;     // corrupt offsets: flagged by k_check_xadj
@@ -566,8 +568,15 @@ static int dalloc(imx_graph *g, T **p, int64_t count) {
 void graph_free(imx_graph *g) {
     if (!g) return;
     cudaSetDevice(g->dev);
+    if (g->struct_pending) graph_settle_structure(g);   // waits for the chunk uploads
     if (g->thr_pending) graph_settle(g);    // joins the weight upload
-    void *ptrs[] = {g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip, g->nz_rows,
+    // leftovers of a streamed build that failed half way
+    if (g->ust) { cudaStreamSynchronize(g->ust); release_stream(g->dev, g->ust); g->ust = nullptr; }
+    for (auto &e : g->chunk_ev) if (e) { cudaEventDestroy(e); e = nullptr; }
+    if (g->sev_done) { cudaEventDestroy(g->sev_done); g->sev_done = nullptr; }
+    if (g->sstats_h) { cudaStreamSynchronize(g->stream); pinned_put(g->sstats_h, sizeof(GStats)); g->sstats_h = nullptr; }
+    if (g->sstats_d) { cudaFreeAsync(g->sstats_d, g->stream); g->sstats_d = nullptr; }
+    void *ptrs[] = {g->hv[0].pre, g->hv[0].nsl, g->hv[0].off, g->hv[1].pre, g->hv[1].nsl, g->hv[1].off, g->xadj, g->adj, g->w, g->src, g->hash, g->thr, g->recip, g->nz_rows,
                     g->cslot, g->E, g->EH, g->ET, g->btmax, g->boff, g->lut,
                     g->hv[0].heavy, g->hv[0].hs_v, g->hv[0].hs_a, g->hv[0].hs_len,
                     g->hv[1].heavy, g->hv[1].hs_v, g->hv[1].hs_a, g->hv[1].hs_len};
@@ -780,31 +789,12 @@ static int graph_analyze(imx_graph *g, bool structure, const std::function<int()
     return IMX_OK;
 }
 
-// imx_graph_from_csr for large graphs: the structure (sources, hashes, max
-// prefix, offsets, symmetry, canonical slots) on the graph stream with one
-// host sync; the weights and their raw per-slot thresholds on a second
-// stream, not waited for (graph_settle).  Until then the graph claims the
-// speculative uniform threshold of weights[0].
-static int graph_analyze_deferred(imx_graph *g, const double *weights) {
+// The weight stream of a deferred graph: the upload, then (after everything
+// enqueued on the graph stream so far: the structure) the raw per-slot
+// thresholds and their statistics, not waited for (graph_settle).
+static int deferred_weights_start(imx_graph *g, const double *weights) {
     cudaStream_t st = g->stream;
-    const int64_t m2 = g->m2, n = g->n;
-    GStats *gs = nullptr;
-    IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
-    k_stats_init<<<1, 1, 0, st>>>(gs); note_launch();
-    IMX_TRY(dalloc(g, &g->src, m2));
-    IMX_TRY(dalloc(g, &g->hash, m2));
-    IMX_TRY(dalloc(g, &g->thr, m2));
-    IMX_TRY(dalloc(g, &g->cslot, m2));
-    IMX_CUDA(cudaMemsetAsync(g->src, 0, sizeof(int32_t) * m2, st));   // rows of corrupt offsets
-    k_src_rows<<<grid_for(n * 32), 256, 0, st>>>(g->xadj, n, m2, g->src);
-    k_check_xadj<<<grid_for(n), 256, 0, st>>>(g->xadj, n, m2, &gs->flags);
-    k_sym_hash<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, n, m2, g->hash, gs);
-    k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, m2, &gs->maxp);
-    note_launch(4);
-    IMX_CHECK_LAUNCH();
-    g->cslot_ready = false;          // canonical slot list on first use (ensure_cslot)
-    IMX_TRY(graph_nz_rows_async(g, gs));
-    // the weight stream: upload, then (after the structure) raw thresholds
+    const int64_t m2 = g->m2;
     cudaEvent_t ev_struct = nullptr;
     IMX_CUDA(cudaEventCreateWithFlags(&ev_struct, cudaEventDisableTiming));
     IMX_CUDA(cudaEventRecord(ev_struct, st));
@@ -813,6 +803,7 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
     IMX_CUDA(pool_alloc(&g->wstats_d, sizeof(GStats), st));
     IMX_CUDA(pinned_get(&g->wstats_h, sizeof(GStats)));   // recycled: cudaFreeHost synchronises the device
     IMX_CUDA(cudaStreamWaitEvent(g->wst, ev_struct, 0));      // buffers allocated on st
+    cudaEventDestroy(ev_struct);
     GStats *wd = static_cast<GStats *>(g->wstats_d);
     GStats *wh = static_cast<GStats *>(g->wstats_h);
     auto finish = [g, m2, wd, wh]() -> int {
@@ -840,10 +831,38 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
         });
     }
     g->thr_pending = true;
+    return IMX_OK;
+}
+
+// imx_graph_from_csr for large graphs: the structure (sources, hashes, max
+// prefix, offsets, symmetry, canonical slots) on the graph stream with one
+// host sync; the weights and their raw per-slot thresholds on a second
+// stream, not waited for (graph_settle).  Until then the graph claims the
+// speculative uniform threshold of weights[0].
+static int graph_analyze_deferred(imx_graph *g, const double *weights) {
+    cudaStream_t st = g->stream;
+    const int64_t m2 = g->m2, n = g->n;
+    GStats *gs = nullptr;
+    IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
+    k_stats_init<<<1, 1, 0, st>>>(gs); note_launch();
+    IMX_TRY(dalloc(g, &g->src, m2));
+    IMX_TRY(dalloc(g, &g->hash, m2));
+    IMX_TRY(dalloc(g, &g->thr, m2));
+    IMX_TRY(dalloc(g, &g->cslot, m2));
+    IMX_CUDA(cudaMemsetAsync(g->src, 0, sizeof(int32_t) * m2, st));   // rows of corrupt offsets
+    k_src_rows<<<grid_for(n * 32), 256, 0, st>>>(g->xadj, n, m2, g->src);
+    k_check_xadj<<<grid_for(n), 256, 0, st>>>(g->xadj, n, m2, &gs->flags);
+    k_sym_hash<<<grid_for(m2), 256, 0, st>>>(g->xadj, g->adj, g->src, n, m2, g->hash, gs);
+    k_max_prefix<<<grid_for(n), 256, 0, st>>>(g->xadj, g->adj, n, m2, &gs->maxp);
+    note_launch(4);
+    IMX_CHECK_LAUNCH();
+    g->cslot_ready = false;          // canonical slot list on first use (ensure_cslot)
+    IMX_TRY(graph_nz_rows_async(g, gs));
+    IMX_TRY(deferred_weights_start(g, weights));
+    g->thr_pending = true;
     GStats h;
     IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
     IMX_CUDA(cudaStreamSynchronize(st));
-    cudaEventDestroy(ev_struct);
     cudaFreeAsync(gs, st);
     g_clock.mark("structure (1 sync)", st);
     if (h.flags & 64u) { set_error("corrupt CSR offsets"); return IMX_EINVAL; }
@@ -868,12 +887,145 @@ static int graph_analyze_deferred(imx_graph *g, const double *weights) {
     return IMX_OK;
 }
 
+// imx_graph_from_csr for large PINNED host CSRs: returns after the offsets
+// are up and checked; the adjacency follows in row-aligned chunks on the
+// upload stream, each chunk's structure kernels run on the graph stream as
+// soon as it lands (graph.cuh, struct_pending).  The statistics are read by
+// graph_settle_structure.  Until then the graph claims what a valid CSR has:
+// symmetric, m2 / 2 undirected edges, the speculative uniform threshold.
+static int graph_analyze_streamed(imx_graph *g, const int64_t *xadj_h, const int32_t *adj_h, const double *weights) {
+    cudaStream_t st = g->stream;
+    const int64_t m2 = g->m2, n = g->n;
+    GStats *gs = nullptr;
+    IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), st));
+    g->sstats_d = gs;
+    IMX_CUDA(pinned_get(&g->sstats_h, sizeof(GStats)));
+    k_stats_init<<<1, 1, 0, st>>>(gs); note_launch();
+    IMX_TRY(dalloc(g, &g->src, m2));
+    IMX_TRY(dalloc(g, &g->hash, m2));
+    IMX_TRY(dalloc(g, &g->thr, m2));
+    IMX_TRY(dalloc(g, &g->cslot, m2));
+    IMX_CUDA(acquire_stream(g->dev, &g->ust));
+    cudaEvent_t ev = nullptr;
+    IMX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    IMX_CUDA(cudaEventRecord(ev, st));                       // the buffers were allocated on st
+    IMX_CUDA(cudaStreamWaitEvent(g->ust, ev, 0));
+    // offsets first: everything below indexes with them
+    IMX_CUDA(cudaMemcpyAsync(g->xadj, xadj_h, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, g->ust));
+    IMX_CUDA(cudaEventRecord(ev, g->ust));
+    // chunks of about equal slot counts, cut at row boundaries (host offsets);
+    // the last one in quarters: what follows the final chunk's arrival (its
+    // structure kernels, its share of the sampler's first pass) is not hidden
+    // behind the link any more, and on skewed graphs the highest ids hold the
+    // most rows per slot (C4: the last sixteenth took 1.2 ms of pass 1)
+    int want = 16;
+    if (const char *e = getenv("IMX_STREAM_CHUNKS")) want = std::max(1, std::min((int)imx_graph::kMaxChunks - 3, atoi(e)));
+    g->nchunk = 0;
+    g->chunk_row[0] = 0;
+    auto cut = [&](int64_t slot, bool last) {
+        int64_t v = last ? n : std::upper_bound(xadj_h, xadj_h + n + 1, slot) - xadj_h - 1;
+        v = std::min(std::max(v, g->chunk_row[g->nchunk]), n);
+        if (v > g->chunk_row[g->nchunk] || last) g->chunk_row[++g->nchunk] = v;
+    };
+    for (int c = 1; c < want; ++c) cut(m2 / want * c, false);
+    for (int q = 1; q <= 4; ++q) cut(m2 / want * (want - 1) + (m2 - m2 / want * (want - 1)) * q / 4, q == 4);
+    for (int c = 0; c < g->nchunk; ++c) {
+        const int64_t s0 = xadj_h[g->chunk_row[c]], s1 = xadj_h[g->chunk_row[c + 1]];
+        if (s0 < 0 || s1 > m2 || s0 > s1) { cudaEventDestroy(ev); set_error("corrupt CSR offsets"); return IMX_EINVAL; }
+        if (s1 > s0)
+            IMX_CUDA(cudaMemcpyAsync(g->adj + s0, adj_h + s0, sizeof(int32_t) * (s1 - s0), cudaMemcpyHostToDevice, g->ust));
+        IMX_CUDA(cudaEventCreateWithFlags(&g->chunk_ev[c], cudaEventDisableTiming));
+        IMX_CUDA(cudaEventRecord(g->chunk_ev[c], g->ust));   // re-recorded on st below
+    }
+    // graph stream: offsets check (read back now), then per chunk its structure
+    IMX_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    k_check_xadj<<<grid_for(n), 256, 0, st>>>(g->xadj, n, m2, &gs->flags);
+    note_launch();
+    unsigned xflags = 0;
+    IMX_CUDA(cudaMemcpyAsync(&xflags, &gs->flags, sizeof xflags, cudaMemcpyDeviceToHost, st));
+    IMX_CUDA(cudaStreamSynchronize(st));
+    cudaEventDestroy(ev);
+    g_clock.mark("offsets up + checked", st);
+    if (xflags & 64u) { set_error("corrupt CSR offsets"); return IMX_EINVAL; }
+    IMX_TRY(graph_nz_rows_async(g, gs));
+    for (int c = 0; c < g->nchunk; ++c) {
+        const int64_t v0 = g->chunk_row[c], v1 = g->chunk_row[c + 1];
+        const int64_t s0 = xadj_h[v0], s1 = xadj_h[v1];
+        IMX_CUDA(cudaStreamWaitEvent(st, g->chunk_ev[c], 0));
+        if (s1 > s0) {
+            k_src_rows<<<grid_for((v1 - v0) * 32), 256, 0, st>>>(g->xadj, v1, m2, g->src, v0);
+            k_sym_hash<<<grid_for(s1 - s0), 256, 0, st>>>(g->xadj, g->adj, g->src, n, s1, g->hash, gs, s0);
+            k_max_prefix<<<grid_for(v1 - v0), 256, 0, st>>>(g->xadj, g->adj, v1, m2, &gs->maxp, v0);
+            note_launch(3);
+            IMX_CHECK_LAUNCH();
+        }
+        IMX_CUDA(cudaEventRecord(g->chunk_ev[c], st));       // chunk c: adjacency, sources and hashes ready
+    }
+    IMX_CUDA(cudaMemcpyAsync(g->sstats_h, gs, sizeof(GStats), cudaMemcpyDeviceToHost, st));
+    IMX_CUDA(cudaEventCreateWithFlags(&g->sev_done, cudaEventDisableTiming));
+    IMX_CUDA(cudaEventRecord(g->sev_done, st));
+    g->cslot_ready = false;
+    // the weights follow the adjacency on the link (their stream waits for the graph stream)
+    IMX_TRY(deferred_weights_start(g, weights));
+    g->struct_pending = true;
+    g->struct_rc = IMX_OK;
+    g->symmetric = 1;
+    g->max_prefix = -1;                  // unknown until settled
+    g->me = m2 / 2;
+    g->n_nz = -1;
+    g->recip_ready = false;
+    g->index_ready = false;
+    g->hash_neg = 0;
+    const int32_t t0 = (int32_t)(int64_t)(weights[0] * 2147483647.0);
+    g->uniform = 1;
+    g->thr_u = t0;
+    g->thr_mean = (double)t0 / 2147483647.0;
+    g_clock.mark("chunks enqueued", st);
+    return IMX_OK;
+}
+
 }  // namespace imx
 
 namespace imx {
 
+int graph_settle_structure(imx_graph *g) {
+    if (!g->struct_pending) return g->struct_rc;
+    g->struct_pending = false;
+    cudaError_t e = cudaEventSynchronize(g->sev_done);
+    const GStats h = *static_cast<GStats *>(g->sstats_h);
+    cudaEventDestroy(g->sev_done);
+    g->sev_done = nullptr;
+    for (int c = 0; c < g->nchunk; ++c) {
+        if (g->chunk_ev[c]) cudaEventDestroy(g->chunk_ev[c]);
+        g->chunk_ev[c] = nullptr;
+    }
+    g->nchunk = 0;
+    release_stream(g->dev, g->ust);
+    g->ust = nullptr;
+    pinned_put(g->sstats_h, sizeof(GStats));
+    g->sstats_h = nullptr;
+    cudaFreeAsync(g->sstats_d, g->stream);
+    g->sstats_d = nullptr;
+    int rc = IMX_OK;
+    if (e != cudaSuccess) rc = cuda_fail(e, "streamed CSR", __FILE__, __LINE__);
+    else if (h.flags & 64u) { set_error("corrupt CSR offsets"); rc = IMX_EINVAL; }
+    else if (h.flags & 32u) { set_error("adjacency entry outside 0..n-1"); rc = IMX_EINVAL; }
+    g->symmetric = (h.flags & 8u) == 0 && h.symsum == 0 && (g->m2 % 2 == 0);
+    g->max_prefix = (int64_t)h.maxp;
+    g->me = g->m2 / 2;
+    if (rc == IMX_OK) graph_nz_rows_done(g, h.nnz);
+    if (rc == IMX_OK && !g->symmetric) { set_error("adjacency is not symmetric"); rc = IMX_EFORMAT; }
+    if (rc == IMX_OK && g->me >= (int64_t(1) << 31)) {
+        set_error("%lld undirected edges exceed 2^31 - 1", (long long)g->me);
+        rc = IMX_ECONSTRAINT;
+    }
+    g->struct_rc = rc;
+    return rc;
+}
+
 int graph_settle(imx_graph *g) {
-    if (!g->thr_pending) return IMX_OK;
+    const int struct_rc = graph_settle_structure(g);
+    if (!g->thr_pending) return struct_rc;
     g->thr_pending = false;
     if (g->wthread) {
         auto *t = static_cast<std::thread *>(g->wthread);
@@ -893,6 +1045,7 @@ int graph_settle(imx_graph *g) {
     g->wstats_h = nullptr;
     cudaFreeAsync(g->wstats_d, g->stream);
     g->wstats_d = nullptr;
+    if (struct_rc != IMX_OK) return struct_rc;
     if (rc != IMX_OK) return rc;
     if (g->m2 && h.tmin != h.tmax && g->symmetric) {
         // per-slot thresholds: symmetrized through the reciprocal slots
@@ -1188,13 +1341,29 @@ extern "C" int imx_graph_from_csr(int32_t device, int64_t n, int64_t m2, const i
     g_clock.mark("validate+stream", st);
     auto fail = [&](int code) { graph_free(g); return code; };
     if (dalloc(g, &g->xadj, n + 1) || dalloc(g, &g->adj, m2) || dalloc(g, &g->w, m2)) return fail(IMX_ENOMEM);
+    // large graphs: the weights (8 bytes per slot, the biggest array) go up on
+    // a second stream and are not waited for (graph_analyze_deferred); very
+    // large pinned ones also stream the adjacency (graph_analyze_streamed)
+    const char *lw = getenv("IMX_LATE_WEIGHTS");
+    const bool late = m2 > 0 && (lw ? atoi(lw) != 0 : m2 >= ((int64_t)1 << 22));
+    const char *sc = getenv("IMX_STREAM_CSR");
+    const bool streamed = late && n > 0 && (sc ? atoi(sc) != 0 : (m2 >= ((int64_t)1 << 24) && host_pinned_ptr(xadj) &&
+                                                                   host_pinned_ptr(adj) && host_pinned_ptr(weights)));
+    if (streamed) {
+        const int rc = graph_analyze_streamed(g, xadj, adj, weights);
+        if (rc != IMX_OK) {
+            // chunk copies may still read the caller's arrays
+            if (g->ust) cudaStreamSynchronize(g->ust);
+            cudaStreamSynchronize(st);
+            g->struct_pending = false;
+            return fail(rc);
+        }
+        *out = g;
+        return IMX_OK;
+    }
     if (upload_h2d(g->xadj, xadj, sizeof(int64_t) * (n + 1), st) != cudaSuccess ||
         (m2 && upload_h2d(g->adj, adj, sizeof(int32_t) * m2, st) != cudaSuccess))
         return fail(cuda_fail(cudaGetLastError(), "upload csr", __FILE__, __LINE__));
-    // large graphs: the weights (8 bytes per slot, the biggest array) go up on
-    // a second stream and are not waited for (graph_analyze_deferred)
-    const char *lw = getenv("IMX_LATE_WEIGHTS");
-    const bool late = m2 > 0 && (lw ? atoi(lw) != 0 : m2 >= ((int64_t)1 << 22));
     if (late) {
         g_clock.mark("upload csr", st);
         const int rc = graph_analyze_deferred(g, weights);
@@ -1278,6 +1447,7 @@ extern "C" int imx_graph_set_weights(imx_graph *g, const double *weights) {
 extern "C" int imx_graph_hashes(imx_graph *g, int32_t *out) {
     if (!g || (!out && g->m2)) { set_error("NULL argument"); return IMX_EINVAL; }
     IMX_CUDA(cudaSetDevice(g->dev));
+    IMX_TRY(graph_settle_structure(g));
     if (g->m2) {
         IMX_CUDA(cudaMemcpyAsync(out, g->hash, sizeof(int32_t) * g->m2, cudaMemcpyDeviceToHost, g->stream));
         IMX_CUDA(cudaStreamSynchronize(g->stream));

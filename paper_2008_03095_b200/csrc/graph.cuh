@@ -53,6 +53,24 @@ struct imx_graph {
     void *wstats_d = nullptr, *wstats_h = nullptr;   // GStats (device, pinned host)
     void *wthread = nullptr;                           // std::thread of a pageable upload
     int wthread_rc = 0;
+    // Streamed structure (imx_graph_from_csr on large pinned host CSRs): the
+    // adjacency goes up in row-aligned chunks on its own stream `ust`, the
+    // per-slot structure (sources, hashes, symmetry sums, prefix maxima) of a
+    // chunk is computed on `stream` as soon as it lands (chunk_ev[c] marks
+    // it), and imx_graph_from_csr returns once the offsets are checked --
+    // before the adjacency is up.  The scan sampler's first pass starts on the
+    // chunks as they arrive (scan.cu, run_scan_streamed); everything else waits
+    // in graph_settle_structure(), which reads the statistics and reports
+    // what imx_graph_from_csr would have (bad entries, asymmetry).
+    bool struct_pending = false;
+    int struct_rc = 0;                  // sticky result of the settled structure
+    cudaStream_t ust = nullptr;
+    static constexpr int kMaxChunks = 32;
+    int nchunk = 0;
+    int64_t chunk_row[kMaxChunks + 1] = {0};
+    cudaEvent_t chunk_ev[kMaxChunks] = {nullptr};
+    cudaEvent_t sev_done = nullptr;
+    void *sstats_d = nullptr, *sstats_h = nullptr;   // GStats (device, pinned host)
     bool recip_ready = true;
     bool index_ready = false;
     bool cslot_ready = true;     // false: cslot built on first use (ensure_cslot)
@@ -67,6 +85,9 @@ struct imx_graph {
         int64_t *hs_a = nullptr;
         int32_t *hs_len = nullptr;
         int64_t nhs = 0;
+        // scratch of a table under construction (heavy_begin .. heavy_finish)
+        int32_t *pre = nullptr;
+        int64_t *nsl = nullptr, *off = nullptr;
     } hv[2];
 };
 
@@ -79,6 +100,8 @@ int graph_build_from_device_edges(imx_graph *g, const int64_t *dedges, int64_t k
 // the deferred weights/thresholds are in (waits for them); the lazily built
 // reciprocal slots and sampler index
 int graph_settle(imx_graph *g);
+// the streamed structure is complete and valid (waits for the chunk uploads)
+int graph_settle_structure(imx_graph *g);
 int ensure_recip(imx_graph *g);
 int ensure_index(imx_graph *g);
 int ensure_nz_rows(imx_graph *g);

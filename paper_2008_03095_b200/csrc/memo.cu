@@ -232,6 +232,7 @@ using namespace imx;
 
 extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
     CTX_CHECK(c);
+    if (gains_out) IMX_TRY(spec_guard(c));
     if (!c->labels_ready) { set_error("labels not computed (call imx_propagate first)"); return IMX_EINVAL; }
     const int64_t n = c->g->n;
     IMX_CUDA(cudaEventRecord(c->ev[4], c->st));
@@ -308,6 +309,7 @@ extern "C" int imx_load_labels(imx_ctx *c, const int32_t *labels, const int32_t 
 
 extern "C" int imx_copy_labels(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out) {
     CTX_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (r0 < 0 || r1 > c->W || r0 > r1) { set_error("lane window [%d, %d) invalid", r0, r1); return IMX_EINVAL; }
     if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
     if (c->g->n == 0 || r1 == r0) return IMX_OK;
@@ -320,6 +322,7 @@ extern "C" int imx_copy_labels(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out)
 
 extern "C" int imx_copy_sizes(imx_ctx *c, int32_t r0, int32_t r1, int32_t *out) {
     CTX_CHECK(c);
+    IMX_TRY(spec_guard(c));
     if (r0 < 0 || r1 > c->W || r0 > r1) { set_error("lane window [%d, %d) invalid", r0, r1); return IMX_EINVAL; }
     if (!c->labels_ready) { set_error("labels not computed"); return IMX_EINVAL; }
     if (c->g->n == 0 || r1 == r0) return IMX_OK;

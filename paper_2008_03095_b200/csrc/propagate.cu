@@ -804,9 +804,11 @@ static int run_hook_enum(imx_ctx *c, unsigned long long *hooks, bool skip_forest
 }
 
 // ---- heavy rows of the pull sampler ---------------------------------------
+// rows [v0, v1); nsl[n] = 0 closes the exclusive scan
 __global__ void k_heavy_count(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, int64_t n, int T,
-                              uint8_t *__restrict__ heavy, int32_t *__restrict__ pre, int64_t *__restrict__ nsl) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+                              uint8_t *__restrict__ heavy, int32_t *__restrict__ pre, int64_t *__restrict__ nsl,
+                              int64_t v0, int64_t v1) {
+    for (int64_t v = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < v1; v += (int64_t)gridDim.x * blockDim.x) {
         int64_t lo = xadj[v], hi = xadj[v + 1];
         const int64_t s0 = lo;
         while (lo < hi) {                     // first slot with adj >= v (rows ascend)
@@ -853,48 +855,91 @@ static int pull_heavy_T(const imx_graph *g) {
     return prefix_balanced(g) ? 0 : 10;
 }
 
-// the heavy-row slices of the graph for slice length T, cached on the graph
-int ensure_heavy(imx_ctx *c, int pass, int T) {
-    imx_graph *g = c->g;
-    auto &H = g->hv[pass - 1];
-    if (H.T == T) return IMX_OK;
-    for (void **p : {(void **)&H.heavy, (void **)&H.hs_v, (void **)&H.hs_a, (void **)&H.hs_len}) {
+static void heavy_drop(imx_ctx *c, imx_graph::HeavySlices &H) {
+    for (void **p : {(void **)&H.heavy, (void **)&H.hs_v, (void **)&H.hs_a, (void **)&H.hs_len, (void **)&H.pre,
+                     (void **)&H.nsl, (void **)&H.off}) {
         if (*p) cudaFreeAsync(*p, c->st);
         *p = nullptr;
     }
     H.nhs = 0;
     H.T = -1;
-    if (T <= 0 || g->max_prefix <= T) { H.T = T; return IMX_OK; }
+}
+
+// start a table for slice length T (T > 0): flags and per-row counts to be
+// filled by heavy_count_rows over every row, then heavy_finish
+int heavy_begin(imx_ctx *c, int pass, int T) {
+    imx_graph *g = c->g;
+    auto &H = g->hv[pass - 1];
+    heavy_drop(c, H);
+    if (T <= 0) return IMX_OK;
     const int64_t n = g->n;
-    int32_t *pre = nullptr;
-    int64_t *nsl = nullptr, *off = nullptr;
     IMX_CUDA(pool_alloc((void **)&H.heavy, n, c->st));
-    IMX_CUDA(pool_alloc((void **)&pre, sizeof(int32_t) * n, c->st));
-    IMX_CUDA(pool_alloc((void **)&nsl, sizeof(int64_t) * (n + 1), c->st));
-    IMX_CUDA(pool_alloc((void **)&off, sizeof(int64_t) * (n + 1), c->st));
-    k_heavy_count<<<grid_for(n), 256, 0, c->st>>>(g->xadj, g->adj, n, T, H.heavy, pre, nsl);
+    IMX_CUDA(pool_alloc((void **)&H.pre, sizeof(int32_t) * n, c->st));
+    IMX_CUDA(pool_alloc((void **)&H.nsl, sizeof(int64_t) * (n + 1), c->st));
+    IMX_CUDA(pool_alloc((void **)&H.off, sizeof(int64_t) * (n + 1), c->st));
+    return IMX_OK;
+}
+
+int heavy_count_rows(imx_ctx *c, int pass, int T, int64_t v0, int64_t v1) {
+    imx_graph *g = c->g;
+    auto &H = g->hv[pass - 1];
+    if (T <= 0 || v1 <= v0) return IMX_OK;
+    k_heavy_count<<<grid_for(v1 - v0), 256, 0, c->st>>>(g->xadj, g->adj, g->n, T, H.heavy, H.pre, H.nsl, v0, v1);
     IMX_CHECK_LAUNCH();
+    note_launch(1);
+    return IMX_OK;
+}
+
+// every row counted: the slices (one host sync for their number); a table
+// without heavy rows keeps nothing
+int heavy_finish(imx_ctx *c, int pass, int T) {
+    imx_graph *g = c->g;
+    auto &H = g->hv[pass - 1];
+    if (T <= 0 || g->max_prefix <= T) {
+        heavy_drop(c, H);
+        H.T = T;
+        return IMX_OK;
+    }
+    const int64_t n = g->n;
     size_t tb = 0;
-    IMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nsl, off, n + 1, c->st));
+    IMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, H.nsl, H.off, n + 1, c->st));
     void *tmp = nullptr;
     IMX_CUDA(pool_alloc(&tmp, tb, c->st));
-    IMX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nsl, off, n + 1, c->st));
+    IMX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, H.nsl, H.off, n + 1, c->st));
     int64_t total = 0;
-    IMX_CUDA(cudaMemcpyAsync(&total, off + n, sizeof total, cudaMemcpyDeviceToHost, c->st));
+    IMX_CUDA(cudaMemcpyAsync(&total, H.off + n, sizeof total, cudaMemcpyDeviceToHost, c->st));
     IMX_CUDA(cudaStreamSynchronize(c->st));
     if (total > 0) {
         IMX_CUDA(pool_alloc((void **)&H.hs_v, sizeof(int32_t) * total, c->st));
         IMX_CUDA(pool_alloc((void **)&H.hs_a, sizeof(int64_t) * total, c->st));
         IMX_CUDA(pool_alloc((void **)&H.hs_len, sizeof(int32_t) * total, c->st));
-        k_heavy_fill<<<grid_for(n), 256, 0, c->st>>>(g->xadj, n, T, pre, nsl, off, H.hs_v, H.hs_a, H.hs_len);
+        k_heavy_fill<<<grid_for(n), 256, 0, c->st>>>(g->xadj, n, T, H.pre, H.nsl, H.off, H.hs_v, H.hs_a, H.hs_len);
         IMX_CHECK_LAUNCH();
     }
-    note_launch(total > 0 ? 4 : 3);
-    for (void *p : {(void *)pre, (void *)nsl, (void *)off, tmp}) cudaFreeAsync(p, c->st);
+    note_launch(total > 0 ? 3 : 2);
+    for (void **p : {(void **)&H.pre, (void **)&H.nsl, (void **)&H.off}) { cudaFreeAsync(*p, c->st); *p = nullptr; }
+    cudaFreeAsync(tmp, c->st);
     IMX_CUDA(cudaStreamSynchronize(c->st));   // the slices are shared by every context of the graph
     H.nhs = total;
     H.T = T;
     return IMX_OK;
+}
+
+void heavy_abort(imx_ctx *c, int pass) { heavy_drop(c, c->g->hv[pass - 1]); }
+
+// the heavy-row slices of the graph for slice length T, cached on the graph
+int ensure_heavy(imx_ctx *c, int pass, int T) {
+    imx_graph *g = c->g;
+    auto &H = g->hv[pass - 1];
+    if (H.T == T) return IMX_OK;
+    if (T <= 0 || g->max_prefix <= T) {
+        heavy_drop(c, H);
+        H.T = T;
+        return IMX_OK;
+    }
+    IMX_TRY(heavy_begin(c, pass, T));
+    IMX_TRY(heavy_count_rows(c, pass, T, 0, g->n));
+    return heavy_finish(c, pass, T);
 }
 
 // blocks per SM of the pull grids (IMX_PULL_BPSM, default 16): about three
@@ -993,10 +1038,17 @@ static int run_sample_cc(imx_ctx *c, unsigned long long *hooks, cudaEvent_t e_in
         mode = hook_mode(g, c->W);
         if (needs_index(mode)) IMX_TRY(ensure_index(g));
     }
+    // a streamed CSR: only the scan's first pass can start on the chunks
+    // that are up; everything else needs the settled structure
+    if (g->struct_pending && mode != HOOK_SCAN) {
+        IMX_TRY(graph_settle_structure(g));
+        mode = g->me ? hook_mode(g, c->W) : HOOK_ENUM;
+    }
     // scan / pull with a deferred graph run on the speculative threshold
     c->spec_used = g->thr_pending;
     if (mode == HOOK_SCAN) {
-        IMX_TRY(run_scan(c, 1, nullptr));
+        if (g->struct_pending) IMX_TRY(run_scan_streamed(c));
+        else IMX_TRY(run_scan(c, 1, nullptr));
         if (e_init) IMX_CUDA(cudaEventRecord(e_init, c->st));
         IMX_TRY(run_scan(c, 2, hooks));
     } else if (mode == HOOK_PULL || mode == HOOK_HYBRID) {
@@ -1130,6 +1182,47 @@ static void push_stat(imx_prop_stats *st, int mode, int64_t changed, int64_t lsu
 
 using namespace imx;
 
+namespace imx {
+int spec_settle(imx_ctx *c, int32_t *held) {
+    *held = 1;
+    if (!c->spec_used) return IMX_OK;
+    imx_graph *g = c->g;
+    IMX_TRY(graph_settle(g));
+    c->spec_used = false;
+    if (!g->uniform || g->thr_u != c->spec_thr || g->hash_neg) {
+        *held = 0;
+        c->labels_ready = false;
+        c->memo_ready = false;
+        c->celf_ready = false;
+        c->gains_fused = false;
+    }
+    return IMX_OK;
+}
+
+int spec_guard(imx_ctx *c) {
+    if (!c->spec_used) return IMX_OK;
+    int32_t held = 1;
+    IMX_TRY(spec_settle(c, &held));
+    if (!held) {
+        set_error("results stand on a speculative threshold that the uploaded weights do not confirm: propagate again");
+        return IMX_EINVAL;
+    }
+    return IMX_OK;
+}
+}  // namespace imx
+
+extern "C" int imx_spec_defer(imx_ctx *c, int32_t on) {
+    CTX_CHECK(c);
+    c->spec_defer = on != 0;
+    return IMX_OK;
+}
+
+extern "C" int imx_spec_settle(imx_ctx *c, int32_t *held) {
+    CTX_CHECK(c);
+    if (!held) { set_error("NULL argument"); return IMX_EINVAL; }
+    return spec_settle(c, held);
+}
+
 extern "C" int imx_set_fuse_memo(imx_ctx *c, int32_t on) {
     CTX_CHECK(c);
     c->fuse_memo = on != 0;
@@ -1151,7 +1244,9 @@ extern "C" int imx_propagate(imx_ctx *c, int32_t verify, imx_prop_stats *st) {
         const int32_t t_spec = g->thr_u;
         IMX_TRY(run_sample_cc(c, st ? sc : nullptr, c->ev[1], c->ev[2]));
         IMX_TRY(run_compress(c, st ? sc + 1 : nullptr));
-        if (c->spec_used) {
+        if (c->spec_used && c->spec_defer) {
+            c->spec_thr = t_spec;            // checked by imx_spec_settle / spec_guard
+        } else if (c->spec_used) {
             // the propagate ran on the speculative uniform threshold while the
             // weights were still uploading: wait for them (the device is busy
             // meanwhile) and run again if the thresholds are not that one

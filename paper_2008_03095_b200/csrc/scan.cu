@@ -49,7 +49,8 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
        const uint16_t *__restrict__ perm_all, const int32_t *__restrict__ boff_all, int64_t n, int32_t W,
        int64_t ld, Lay y, uint32_t *__restrict__ L, unsigned long long *__restrict__ hooks,
        const uint8_t *__restrict__ heavy, const int32_t *__restrict__ hs_v, const int64_t *__restrict__ hs_a,
-       const int32_t *__restrict__ hs_len, int64_t nhs, unsigned long long *__restrict__ ctr, int grab) {
+       const int32_t *__restrict__ hs_len, int64_t nhs, unsigned long long *__restrict__ ctr, int grab,
+       int64_t row0) {
     extern __shared__ int4 smem4[];
     // 16-byte aligned sections (run_scan sizes them): per-warp first-live
     // flags, per-warp union queues (pass 2), the chunk's lane tables
@@ -66,6 +67,7 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
     const unsigned lt_mask = (1u << lane) - 1u;
     int qn = 0;
     unsigned long long nh = 0;
+    // light rows: [row0, row0 + n) (a chunk of a streamed CSR; otherwise row0 = 0)
     const int64_t items = HEAVY ? nhs : n;
     for (int c = 0; c < nchunks; ++c) {
         const int r0 = c * cw;
@@ -90,8 +92,8 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
             int64_t xa = 0;
             bool hv_l = false;
             if (!HEAVY) {
-                if (lane <= cntv) xa = __ldg(xadj + base + lane);
-                if (heavy && lane < cntv) hv_l = heavy[base + lane] != 0;
+                if (lane <= cntv) xa = __ldg(xadj + row0 + base + lane);
+                if (heavy && lane < cntv) hv_l = heavy[row0 + base + lane] != 0;
             }
             const unsigned hmask = __ballot_sync(FULL, hv_l);
             auto bounds = [&](int k, int64_t &v, int64_t &s0, int64_t &s1) {
@@ -100,7 +102,7 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                     s0 = hs_a[base + k];
                     s1 = s0 + hs_len[base + k];
                 } else {
-                    v = (int64_t)base + k;
+                    v = row0 + (int64_t)base + k;
                     s0 = __shfl_sync(FULL, xa, k);
                     s1 = __shfl_sync(FULL, xa, k + 1);
                     if ((hmask >> k) & 1u) s1 = s0;        // heavy row: ROOT here, slices below
@@ -346,42 +348,75 @@ static int scan_bpsm() {
     return e && atoi(e) > 0 ? atoi(e) : 8;
 }
 
+using ScanKernel = void (*)(const int64_t *, const int32_t *, const int32_t *, int32_t, int, int, int, int,
+                            const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, Lay, uint32_t *,
+                            unsigned long long *, const uint8_t *, const int32_t *, const int64_t *, const int32_t *,
+                            int64_t, unsigned long long *, int, int64_t);
+static const ScanKernel kScanKernels[2][2] = {{k_scan<1, false>, k_scan<1, true>}, {k_scan<2, false>, k_scan<2, true>}};
+
+// one launch: the light rows [row0, row0 + rows) (heavy = false), or all heavy slices
+static int launch_scan(imx_ctx *c, int pass, bool heavy, int64_t row0, int64_t rows, unsigned long long *hooks) {
+    imx_graph *g = c->g;
+    const auto &H = g->hv[0];            // both passes cut heavy rows alike: one table
+    const int cw = c->scan_cw, nb = c->scan_nb;
+    // cw is a multiple of 16, so every section keeps 16-byte alignment
+    const size_t smem = (size_t)kScanWarps * cw + (pass == 2 ? sizeof(uint32_t) * kScanWarps * 3 * kScanQ : 0) +
+                        sizeof(int2) * cw + sizeof(int2) * nb;
+    ScanKernel kern = kScanKernels[pass - 1][heavy ? 1 : 0];
+    IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t items = heavy ? H.nhs : rows;
+    if (items <= 0) return IMX_OK;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, kScanWarps), 148 * scan_bpsm()));
+    // items per counter grab: up to 16 rows, fewer when that would leave
+    // warps idle (C2: 37k rows over ~9.5k warps)
+    const int64_t warps = (int64_t)blocks * kScanWarps;
+    const int grab = heavy ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, items / (warps * 8)));
+    IMX_CUDA(cudaMemsetAsync(c->scan_ctr, 0, sizeof(unsigned long long) * c->scan_nchunks, c->st));
+    kern<<<blocks, kScanWarps * 32, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr_u, c->scan_kb, nb, cw,
+                                                   c->scan_nchunks, c->scan_xs, c->scan_perm, c->scan_boff, rows,
+                                                   c->W, c->ld, c->lay, c->L, pass == 2 ? hooks : nullptr,
+                                                   H.heavy, H.hs_v, H.hs_a, H.hs_len, H.nhs, c->scan_ctr, grab, row0);
+    IMX_CHECK_LAUNCH();
+    count_launch(c);
+    return IMX_OK;
+}
+
 int run_scan(imx_ctx *c, int pass, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (n == 0) return IMX_OK;
     IMX_TRY(ensure_scan_tables(c));
     const int T = scan_heavy_T();
-    IMX_TRY(ensure_heavy(c, pass, T));
-    const auto &H = g->hv[pass - 1];
-    const int cw = c->scan_cw, nb = c->scan_nb;
-    // cw is a multiple of 16, so every section keeps 16-byte alignment
-    const size_t smem = (size_t)kScanWarps * cw + (pass == 2 ? sizeof(uint32_t) * kScanWarps * 3 * kScanQ : 0) +
-                        sizeof(int2) * cw + sizeof(int2) * nb;
-    using KF = void (*)(const int64_t *, const int32_t *, const int32_t *, int32_t, int, int, int, int,
-                        const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, Lay, uint32_t *,
-                        unsigned long long *, const uint8_t *, const int32_t *, const int64_t *, const int32_t *,
-                        int64_t, unsigned long long *, int);
-    static const KF kerns[2][2] = {{k_scan<1, false>, k_scan<1, true>}, {k_scan<2, false>, k_scan<2, true>}};
-    const int hv = H.nhs > 0 ? 2 : 1;
-    for (int h = 0; h < hv; ++h) {
-        KF kern = kerns[pass - 1][h];
-        IMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int64_t items = h ? H.nhs : n;
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, kScanWarps), 148 * scan_bpsm()));
-        // items per counter grab: up to 16 rows, fewer when that would leave
-        // warps idle (C2: 37k rows over ~9.5k warps)
-        const int64_t warps = (int64_t)blocks * kScanWarps;
-        const int grab = h ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, items / (warps * 8)));
-        IMX_CUDA(cudaMemsetAsync(c->scan_ctr, 0, sizeof(unsigned long long) * c->scan_nchunks, c->st));
-        kern<<<blocks, kScanWarps * 32, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr_u, c->scan_kb, nb, cw,
-                                                       c->scan_nchunks, c->scan_xs, c->scan_perm, c->scan_boff, n,
-                                                       c->W, c->ld, c->lay, c->L, pass == 2 ? hooks : nullptr,
-                                                       H.nhs > 0 ? H.heavy : nullptr, H.hs_v, H.hs_a, H.hs_len,
-                                                       H.nhs, c->scan_ctr, grab);
-        IMX_CHECK_LAUNCH();
-        count_launch(c);
+    IMX_TRY(ensure_heavy(c, 1, T));
+    IMX_TRY(launch_scan(c, pass, false, 0, n, hooks));
+    if (g->hv[0].nhs > 0) IMX_TRY(launch_scan(c, pass, true, 0, n, hooks));
+    return IMX_OK;
+}
+
+// Pass 1 on a streamed CSR (graph.cuh, struct_pending): the light rows of
+// every chunk as soon as its adjacency, sources and hashes are on the device
+// (the chunk's event), while the later chunks are still on the link; the
+// heavy flags of a chunk's rows are computed right before.  Then the
+// structure is settled (the host waits for the last chunk here; its
+// statistics can fail the call) and the heavy slices follow as usual.
+int run_scan_streamed(imx_ctx *c) {
+    imx_graph *g = c->g;
+    const int64_t n = g->n;
+    IMX_TRY(ensure_scan_tables(c));
+    const int T = scan_heavy_T();
+    IMX_TRY(heavy_begin(c, 1, T));
+    for (int ch = 0; ch < g->nchunk; ++ch) {
+        const int64_t v0 = g->chunk_row[ch], v1 = g->chunk_row[ch + 1];
+        IMX_CUDA(cudaStreamWaitEvent(c->st, g->chunk_ev[ch], 0));
+        if (v1 <= v0) continue;
+        IMX_TRY(heavy_count_rows(c, 1, T, v0, v1));
+        IMX_TRY(launch_scan(c, 1, false, v0, v1 - v0, nullptr));
     }
+    const int rc = graph_settle_structure(g);
+    if (rc != IMX_OK) { heavy_abort(c, 1); return rc; }
+    IMX_TRY(heavy_finish(c, 1, T));
+    if (g->hv[0].nhs > 0) IMX_TRY(launch_scan(c, 1, true, 0, n, nullptr));
+    (void)n;
     return IMX_OK;
 }
 

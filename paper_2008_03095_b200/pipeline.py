@@ -118,37 +118,51 @@ def run_fused(g: Graph, k: int, num_simulations: int = 256, master_seed: int = 0
 
     t = time.perf_counter()
     a, b, scored = lane_window(randoms.padded, randoms.num_scored, comm.rank, comm.size)
-    ctx, _ = propagated_context(g, table, randoms.values[a:b], scored, lane0=a, fuse_memo=True)
+    # a large host graph's weights may still be on the link: everything up to
+    # the seeds runs on the speculative threshold and is checked afterwards
+    native = native_comm(comm) if comm.size > 1 else None
+    ctx, _ = propagated_context(g, table, randoms.values[a:b], scored, lane0=a, fuse_memo=True,
+                                defer_spec=comm.size == 1 or native is not None)
     timings["propagate"] = time.perf_counter() - t
 
-    native = native_comm(comm) if comm.size > 1 else None
-    t = time.perf_counter()
-    if comm.size == 1:
-        ctx.memoize(want_gains=False)
-    elif native is not None:
+    if native is not None:
         ctx.attach_comm(native)           # gains summed over the ranks on the device
-        ctx.memoize(want_gains=False)
-    else:
-        gains = comm.allreduce(ctx.memoize(want_gains=True))
-    timings["memoize"] = time.perf_counter() - t
 
+    def score():
+        t = time.perf_counter()
+        if comm.size == 1 or native is not None:
+            ctx.memoize(want_gains=False)
+        else:
+            gains = comm.allreduce(ctx.memoize(want_gains=True))
+        timings["memoize"] = timings.get("memoize", 0.0) + time.perf_counter() - t
+        t = time.perf_counter()
+        if comm.size == 1:
+            ctx.celf_reset(None)
+            out = ctx.celf_select(k)
+        elif native is not None:
+            ctx.celf_reset(None)
+            out = ctx.celf_select_comm(k)
+        else:
+            ctx.celf_reset(gains)
+            # the select_rounds loop, driven from native code with comm's allreduce
+            out = ctx.celf_select_sharded(k, comm)
+        timings["select"] = timings.get("select", 0.0) + time.perf_counter() - t
+        return out
+
+    seeds, gains_k, trace = score()
+    if not ctx.spec_settle():
+        # the weights were not uniform at weights[0]'s threshold: again, on the settled thresholds
+        t = time.perf_counter()
+        ctx.propagate()
+        timings["propagate"] += time.perf_counter() - t
+        seeds, gains_k, trace = score()
     t = time.perf_counter()
-    if comm.size == 1:
-        ctx.celf_reset(None)
-        seeds, gains_k, trace = ctx.celf_select(k)
-    elif native is not None:
-        ctx.celf_reset(None)
-        seeds, gains_k, trace = ctx.celf_select_comm(k)
-    else:
-        ctx.celf_reset(gains)
-        # the select_rounds loop, driven from native code with comm's allreduce
-        seeds, gains_k, trace = ctx.celf_select_sharded(k, comm)
     selection = result_from_context(ctx, seeds, gains_k, trace, randoms.num_scored)
     if comm.size > 1:
         per_sim = np.concatenate(comm.allgather(ctx.per_sim()))
         selection.state._per_sim = per_sim
         selection.state._ctx = None
         selection.state._shard = (ctx, comm)
-    timings["select"] = time.perf_counter() - t
+    timings["select"] += time.perf_counter() - t
     timings["total"] = sum(timings.values())
     return FusedRun(g, selection, ctx, table, randoms, timings, comm)

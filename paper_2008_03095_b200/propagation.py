@@ -48,7 +48,7 @@ def _width(randoms, num_simulations) -> int:
 
 def propagated_context(g: Graph, table: EdgeHashTable | None, X: np.ndarray, num_scored: int,
                        verify: bool = False, stats: bool = False, lane0: int = 0,
-                       fuse_memo: bool = False):
+                       fuse_memo: bool = False, defer_spec: bool = False):
     """Create a context for lanes X on g, bind the hash table, propagate
     (with the memo fused into a tiled compression when ``fuse_memo``)."""
     if table is not None:
@@ -56,6 +56,8 @@ def propagated_context(g: Graph, table: EdgeHashTable | None, X: np.ndarray, num
     ctx = DeviceContext(g, X, num_scored, lane0)
     if fuse_memo:
         ctx.set_fuse_memo(True)
+    if defer_spec:          # the caller checks ctx.spec_settle() before trusting results
+        ctx.spec_defer(True)
     st = ctx.propagate(verify=verify, stats=stats)
     return ctx, st
 

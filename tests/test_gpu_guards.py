@@ -184,3 +184,84 @@ def test_deferred_weights_evaluate_and_reciprocal(gpu, orc, monkeypatch):
     got = evaluate_counts(g, np.array([1, 5, 9]), 300, 4)
     want = orc.evaluate_counts(xadj, adj, z["weights"], np.array([1, 5, 9]), 300, 4, nthreads=2)
     assert np.array_equal(got, want)
+
+
+# ---- streamed CSR (very large pinned host CSRs; forced on small ones) ---------
+
+def _stream_env(monkeypatch, hook, chunks="5", heavy=None):
+    monkeypatch.setenv("IMX_LATE_WEIGHTS", "1")
+    monkeypatch.setenv("IMX_STREAM_CSR", "1")
+    monkeypatch.setenv("IMX_STREAM_CHUNKS", chunks)
+    if hook:
+        monkeypatch.setenv("IMX_HOOK", hook)
+    if heavy:
+        monkeypatch.setenv("IMX_SCAN_HEAVY", heavy)
+
+
+@pytest.mark.parametrize("hook,heavy", [(None, None), ("scan", None), ("scan", "4"), ("pull", None), ("enum", None)])
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("case", ["uniform", "last_differs"])
+def test_streamed_csr_matches_oracle(gpu, orc, case, pinned, hook, heavy, monkeypatch):
+    """imx_graph_from_csr returns before the adjacency is up; the scan's first
+    pass runs on the chunks as they land (with and without heavy-row slices),
+    every other sampler settles the structure first.  Results are the
+    oracle's, also when the weight speculation fails afterwards."""
+    _stream_env(monkeypatch, hook, heavy=heavy)
+    z = load_golden("er_big_1000")
+    xadj, adj, _ = orc.csr_from_edges(int(z["n"]), z["edges"].astype(np.int64))
+    w = np.full(len(adj), 0.05)
+    if case == "last_differs":
+        rec = orc.reciprocal(xadj, adj)
+        w[[-1, rec[-1]]] = 0.6
+    g = _deferred_graph(gpu, xadj, adj, w, pinned)
+    run = gpu.run_fused(g, 5, num_simulations=40, master_seed=2)
+    want = orc.run_fused(xadj, adj, w, 5, 40, 2, nthreads=4)
+    assert np.array_equal(run.labels, want["labels"])
+    assert np.array_equal(run.sizes, want["sizes"])
+    assert run.seeds == want["seeds"].tolist()
+    assert np.array_equal(run.selection.trace.array, want["trace"])
+    assert np.array_equal(gpu.slot_thresholds(g), want["thr"])
+
+
+@pytest.mark.parametrize("chunks", ["1", "3", "16", "32"])
+@pytest.mark.parametrize("name", ["cfg_c1", "cfg_c2"])
+def test_streamed_csr_golden_configs(gpu, name, chunks, monkeypatch):
+    """The benchmark graphs through the streamed build (C2 takes the scan
+    sampler by rule, with isolated vertices and chunk cuts inside hub rows'
+    neighbourhoods) against the reference's own outputs."""
+    _stream_env(monkeypatch, None, chunks=chunks)
+    z = load_golden(name)
+    from test_gpu_golden import build_graph, check_array
+    g0 = build_graph(gpu, z)
+    g = _deferred_graph(gpu, np.asarray(g0.xadj), np.asarray(g0.adj), np.asarray(g0.weights), pinned=True)
+    run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))
+    check_array(z, "labels", run.labels)
+    check_array(z, "sizes", run.sizes)
+    assert run.seeds == z["seeds"].tolist()
+    assert np.array_equal(run.selection.trace.array, z["trace"])
+    # the graph's lazily built parts after a streamed build
+    assert np.array_equal(g.reciprocal_slots, g0.reciprocal_slots)
+    assert np.array_equal(gpu.build_hash_table(g).hashes, gpu.build_hash_table(g0).hashes)
+
+
+@pytest.mark.parametrize("hook", [None, "scan"])
+@pytest.mark.parametrize("bad,match", [
+    ("asymmetric", "symmetric"), ("unsorted", "symmetric"), ("range", "outside"), ("offsets", "offsets")])
+def test_streamed_csr_refuses_bad_input(gpu, bad, match, hook, monkeypatch):
+    """What imx_graph_from_csr reports for a bad CSR surfaces from the
+    streamed build too (at the latest when the structure is settled inside
+    the propagate), and nothing is read out of bounds before."""
+    _stream_env(monkeypatch, hook, chunks="2")
+    xadj = np.array([0, 2, 3, 4], np.int64)
+    adj = np.array([1, 2, 0, 0], np.int32)
+    if bad == "asymmetric":
+        adj = np.array([1, 2, 0, 1], np.int32)          # 0-2 has no 2-0
+    elif bad == "unsorted":
+        adj = np.array([2, 1, 0, 0], np.int32)
+    elif bad == "range":
+        adj = np.array([1, 7, 0, 0], np.int32)
+    elif bad == "offsets":
+        xadj = np.array([0, 3, 2, 4], np.int64)
+    g = gpu.Graph(xadj, adj, np.full(4, 0.5), np.arange(3, dtype=np.int64))
+    with pytest.raises(Exception, match=match):
+        gpu.run_fused(g, 1, num_simulations=8)

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
     int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
     int32_t bpct, int32_t ngroup, int64_t *__restrict__ xbuf, int64_t xcap, int2 *__restrict__ tab,
-    int64_t tab_ld, const int64_t *__restrict__ gains0) {
+    int64_t tab_ld, const int64_t *__restrict__ gains0, int64_t wide_out) {
     cg::grid_group grid = cg::this_grid();
     constexpr bool xm = XM;                    // exchange mode (sharded run; xcap > 0)
     // a stop that waits for the host (done, trace full, error, big round)
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                 // a huge batch through the seed table (C4's round 1 evaluates 2.4 M
                 // candidates) is a streaming pass over rows: k_wide_tab_round does
                 // it with the registers this kernel does not have
-                if (!xm && etab && hi - lo > (int64_t)gridDim.x * kWideOutPerCta) {
+                if (!xm && etab && hi - lo > (int64_t)gridDim.x * wide_out) {
                     if (gtid == 0) { st->xlo = lo; st->xhi = hi; st->xbest = bestkey; }
                     status = 6;
                     break;
@@ -1312,9 +1312,12 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     int2 *tab = (!c->C && c->memo_ready && !getenv("IMX_CELF_NO_TAB")) ? c->stab : nullptr;
     int64_t tab_ld = c->ld;
     const int64_t *gains0 = c->gains;
+    // seed-table batches above this many candidates per CTA leave the kernel (k_wide_tab_round)
+    int64_t wide_out = kWideOutPerCta;
+    if (const char *wo = getenv("IMX_CELF_WIDE_OUT")) wide_out = std::max<int64_t>(0, atoll(wo));
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
                     &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap, &tab,
-                    &tab_ld, &gains0};
+                    &tab_ld, &gains0, &wide_out};
     const bool hprof = getenv("IMX_CELF_PROFILE") != nullptr;
     auto hq0 = std::chrono::steady_clock::now();
     if (hprof) IMX_CUDA(cudaStreamSynchronize(c->st));
@@ -1586,11 +1589,11 @@ static int celf_select_xchg(imx_ctx *c, int32_t k, std::vector<int32_t> &seeds, 
     int64_t cap = c->trace_cap;
     CelfDev *stp = c->cdev;
     int2 *tab = nullptr;             // partial gains per rank: the covered bitmap only
-    int64_t tab_ld = 0;
+    int64_t tab_ld = 0, wide_out = 0;
     const int64_t *gains0 = nullptr;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
                     &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap, &tab,
-                    &tab_ld, &gains0};
+                    &tab_ld, &gains0, &wide_out};
     CelfDev *snap = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int rc = IMX_OK;

@@ -265,3 +265,24 @@ def test_streamed_csr_refuses_bad_input(gpu, bad, match, hook, monkeypatch):
     g = gpu.Graph(xadj, adj, np.full(4, 0.5), np.arange(3, dtype=np.int64))
     with pytest.raises(Exception, match=match):
         gpu.run_fused(g, 1, num_simulations=8)
+
+
+# ---- CELF: seed-table batches evaluated by k_wide_tab_round --------------------
+
+@pytest.mark.parametrize("name", ["er_mid_300", "er_big_1000", "er_pad20", "er_wc_r40", "cfg_c1", "cfg_c2"])
+def test_wide_tab_round_forced(gpu, name, monkeypatch):
+    """Every seed-table batch (rounds 1-4) leaves the persistent CELF kernel
+    for the streaming kernel and the device-wide round finish (at scale only
+    rounds that evaluate > 37 k candidates at once do): one listed seed with
+    the table in registers, 2-4 listed seeds through L1, row quads that end
+    inside a quad (R = 20).  Seeds, gains and the full trace stay the
+    reference's."""
+    monkeypatch.setenv("IMX_CELF_WIDE_OUT", "0")
+    from test_gpu_golden import build_graph
+    z = load_golden(name)
+    g = build_graph(gpu, z)
+    run = gpu.run_fused(g, int(z["k"]), num_simulations=int(z["R"]), master_seed=int(z["master_seed"]))
+    assert run.seeds == z["seeds"].tolist()
+    assert run.selection.gains == z["seed_gains"].tolist()
+    assert np.array_equal(run.selection.trace.array, z["trace"])
+    assert run.spread_se == pytest.approx(float(z["spread_se"]), rel=1e-12, abs=1e-15)

@@ -414,7 +414,8 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
     int64_t *__restrict__ trace, int64_t trace_cap, int32_t *__restrict__ seeds,
     int64_t *__restrict__ sgains, unsigned long long *__restrict__ gain, CelfDev *__restrict__ st,
     int32_t bpct, int32_t ngroup, int64_t *__restrict__ xbuf, int64_t xcap, int2 *__restrict__ tab,
-    int64_t tab_ld, const int64_t *__restrict__ gains0, int64_t wide_out) {
+    int64_t tab_ld, const int64_t *__restrict__ gains0, int64_t wide_out, const int64_t *__restrict__ g1,
+    const unsigned long long *__restrict__ hub) {
     cg::grid_group grid = cg::this_grid();
     constexpr bool xm = XM;                    // exchange mode (sharded run; xcap > 0)
     // a stop that waits for the host (done, trace full, error, big round)
@@ -506,15 +507,36 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                 // the seed table instead of the covered bitmap (tab != NULL only for ENC, one rank)
                 const int ntab = (tab && t <= kTab) ? t : 0;
                 const int2 *etab = ntab ? tab : nullptr;
+                // round 1 after the speculated first seed (memo.cu: the max-degree
+                // vertex): the memo pass left every vertex's exact gain after that
+                // seed in g1 -- one word per candidate, no row read
+                const bool spec1 = !xm && g1 && ntab == 1 &&
+                                   (unsigned long long)(uint32_t)(*(volatile int32_t *)seeds) == *hub;
+                if (spec1) {
+                    unsigned long long lmax = 0;
+                    for (int64_t i = lo + gtid; i < hi; i += gthreads) {
+                        const uint32_t u = (uint32_t)oid[ostart + i];
+                        const int64_t f = g1[u];
+                        fresh[i] = f;
+                        const unsigned long long fk = ((unsigned long long)f << vb) | (unsigned long long)(vmask - u);
+                        lmax = fk > lmax ? fk : lmax;
+                    }
+                    for (int o = 16; o; o >>= 1) {
+                        const unsigned long long x = __shfl_xor_sync(0xffffffffu, lmax, o);
+                        lmax = x > lmax ? x : lmax;
+                    }
+                    if ((threadIdx.x & 31) == 0 && lmax) atomicMax(&st->smax[sstep & 3], lmax);
+                }
                 // a huge batch through the seed table (C4's round 1 evaluates 2.4 M
                 // candidates) is a streaming pass over rows: k_wide_tab_round does
                 // it with the registers this kernel does not have
-                if (!xm && etab && hi - lo > (int64_t)gridDim.x * wide_out) {
+                if (!spec1 && !xm && etab && hi - lo > (int64_t)gridDim.x * wide_out) {
                     if (gtid == 0) { st->xlo = lo; st->xhi = hi; st->xbest = bestkey; }
                     status = 6;
                     break;
                 }
-                if (wide && etab) {
+                if (spec1) {
+                } else if (wide && etab) {
                     unsigned long long wmax = 0;
                     const int wl = threadIdx.x & 31;
                     const int nqs = (ns + 3) >> 2;
@@ -564,7 +586,7 @@ __global__ void __launch_bounds__(256, IMX_CELF_MINB) k_celf_rounds(
                     if (!xm && wl == 0 && wmax) atomicMax(&st->smax[sstep & 3], wmax);
                 }
                 // otherwise ngroup candidates per CTA at a time, 256/ngroup threads each
-                for (int64_t base = lo + (int64_t)blockIdx.x * ngroup; !wide && base < hi;
+                for (int64_t base = lo + (int64_t)blockIdx.x * ngroup; !wide && !spec1 && base < hi;
                      base += (int64_t)gridDim.x * ngroup) {
                     const int gsz = blockDim.x / ngroup, g = threadIdx.x / gsz;
                     const int64_t i = base + g;
@@ -1315,9 +1337,12 @@ static int celf_device_rounds(imx_ctx *c, int32_t t, int32_t k, int64_t batch0, 
     // seed-table batches above this many candidates per CTA leave the kernel (k_wide_tab_round)
     int64_t wide_out = kWideOutPerCta;
     if (const char *wo = getenv("IMX_CELF_WIDE_OUT")) wide_out = std::max<int64_t>(0, atoll(wo));
+    // the memo's first-seed speculation (round 1 from g1 when seed 0 is the max-degree vertex)
+    const int64_t *g1 = (tab && c->g1_ready) ? c->g1 : nullptr;
+    const unsigned long long *hubp = c->scratch + 15;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
                     &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap, &tab,
-                    &tab_ld, &gains0, &wide_out};
+                    &tab_ld, &gains0, &wide_out, &g1, &hubp};
     const bool hprof = getenv("IMX_CELF_PROFILE") != nullptr;
     auto hq0 = std::chrono::steady_clock::now();
     if (hprof) IMX_CUDA(cudaStreamSynchronize(c->st));
@@ -1590,10 +1615,11 @@ static int celf_select_xchg(imx_ctx *c, int32_t k, std::vector<int32_t> &seeds, 
     CelfDev *stp = c->cdev;
     int2 *tab = nullptr;             // partial gains per rank: the covered bitmap only
     int64_t tab_ld = 0, wide_out = 0;
-    const int64_t *gains0 = nullptr;
+    const int64_t *gains0 = nullptr, *g1 = nullptr;
+    const unsigned long long *hubp = c->scratch + 15;
     void *args[] = {&kk, &vb, &L, &C, &cov, &ld, &ns, &cw, &per_sim, &inS, &o0, &o1, &k0, &k1, &fresh,
                     &skey, &sid, &trace, &cap, &sd, &sg, &gain, &stp, &bpct, &ngroup, &xbuf, &xcap, &tab,
-                    &tab_ld, &gains0, &wide_out};
+                    &tab_ld, &gains0, &wide_out, &g1, &hubp};
     CelfDev *snap = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int rc = IMX_OK;

@@ -113,7 +113,7 @@ void ctx_free(imx_ctx *c) {
                     c->okey[0], c->okey[1], c->scratch, c->eval_out, c->d_one,
                     c->sort_tmp, c->d_ids, c->d_vals, c->seg_a, c->seg_n, c->seg_off, c->scan_tmp,
                     c->scan_xs, c->scan_perm, c->scan_boff, c->scan_ctr,
-                    c->cdev, c->skey, c->sid, c->dtrace, c->dseeds, c->dsgains, c->stab};
+                    c->cdev, c->skey, c->sid, c->dtrace, c->dseeds, c->dsgains, c->stab, c->hublab, c->g1};
     for (void *p : ptrs) if (p) cudaFreeAsync(p, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     pinned_put(c->h_ids, sizeof(int32_t) * c->stage_cap);

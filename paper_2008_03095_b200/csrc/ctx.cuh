@@ -106,6 +106,11 @@ struct imx_ctx {
     int64_t *dsgains = nullptr;
     int32_t dseeds_cap = 0;
     int2 *stab = nullptr;             // [kTab][ld] seed table of the early CELF rounds
+    // first-seed speculation (memo.cu): labels of the max-degree vertex's components per lane and
+    // g1[v] = gain of v once that vertex is the first seed; scratch[15] = that vertex
+    int32_t *hublab = nullptr;        // [ld]
+    int64_t *g1 = nullptr;            // [n]
+    bool g1_ready = false;
     int celf_grid[4] = {0, 0, 0, 0};  // cooperative grids of k_celf_rounds<ENC, XM> on this context's device
     int wide_grid[2] = {0, 0};        // and of k_wide_tab_round<TAB1>
     // interval-enumeration sampler
@@ -121,8 +126,9 @@ struct imx_ctx {
     int32_t *scan_boff = nullptr;
     unsigned long long *scan_ctr = nullptr;   // [scan_nchunks] work counters of one launch
     int scan_kb = -1, scan_nb = 0, scan_cw = 0, scan_nchunks = 0;
+    int scan_iso_pass = 2;            // the pass of the current propagate that writes the isolated rows
     // misc
-    unsigned long long *scratch = nullptr;  // [16]: per-call counters (4 label sum, 6 bad labels, 7 commit gain, 9 max prio, 13 bad prio)
+    unsigned long long *scratch = nullptr;  // [16]: per-call counters (4 label sum, 6 bad labels, 7 commit gain, 9 max prio, 13 bad prio, 14 hub degree key, 15 hub)
     bool labels_ready = false, memo_ready = false, celf_ready = false;
     cudaEvent_t ev[8];
     // phase timings not read back yet: 1 = propagate (ev 0-3), 2 = memo (ev 4-5)

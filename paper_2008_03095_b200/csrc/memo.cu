@@ -47,19 +47,32 @@ __global__ void __launch_bounds__(256) k_gains_caller(const uint32_t *__restrict
 // L1/texture cache instead of hammering one L2 line).
 // An isolated vertex (no slot in xadj) is its own component in every lane:
 // its gain is ns without reading its row (C4: 44% of the rows).
-__global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ L, int64_t n, Lay y,
+//
+// First-seed speculation (hublab != NULL): CELF's round 0 commits the vertex
+// with the largest gain, and on skewed graphs that is the vertex with the
+// most neighbours.  While v's row is here anyway, g1[v] = gains[v] - (sizes of
+// v's components that contain that vertex) is v's exact marginal gain after
+// that first seed, so round 1 -- which re-evaluates most candidates (C4:
+// 2.3 M rows, 9.5 GB) -- reads one word per candidate instead of its row.  If
+// the first seed turns out to be another vertex, g1 is not used.
+template <bool G1>
+__global__ void __launch_bounds__(256, G1 ? 5 : 1) k_gains_enc(const uint32_t *__restrict__ L, int64_t n, Lay y,
                                                    int32_t ns, int64_t *__restrict__ gains,
-                                                   const int64_t *__restrict__ xadj) {
+                                                   const int64_t *__restrict__ xadj,
+                                                   const int32_t *__restrict__ hublab, int64_t *__restrict__ g1) {
     const int lane = threadIdx.x & 31;
     const int nqs = (ns + 3) >> 2;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = wg; v < n; v += nw) {
         if (xadj && xadj[v + 1] == xadj[v]) {
-            if (lane == 0) gains[v] = ns;
+            if (lane == 0) {
+                gains[v] = ns;
+                if (G1) g1[v] = ns;
+            }
             continue;
         }
-        unsigned long long acc = 0;
+        unsigned long long acc = 0, acc1 = 0;
         // two quads per step, all eight root gathers issued before any is used
         for (int q0 = lane; q0 < nqs; q0 += 64) {
             uint32_t w[8];
@@ -75,6 +88,23 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
                 const int r = ((q0 + 32 * (k >> 2)) << 2) + (k & 3);
                 rw[k] = is_root(w[k]) ? w[k] : __ldg(L + cell_off(y, w[k], r));
             }
+            if (G1) {
+                // the lanes' labels as 16-byte quads like the row (hublab has ld entries)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int q = q0 + 32 * h;
+                    if (q < nqs) {
+                        const int4 hq = __ldg(reinterpret_cast<const int4 *>(hublab) + q);
+                        const uint32_t hl[4] = {(uint32_t)hq.x, (uint32_t)hq.y, (uint32_t)hq.z, (uint32_t)hq.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int k = 4 * h + j;
+                            const uint32_t lab = is_root(w[k]) ? (uint32_t)v : w[k];
+                            if (4 * q + j < ns && hl[j] == lab) acc1 += (rw[k] & COUNT) + 1u;
+                        }
+                    }
+                }
+            }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int r = ((q0 + 32 * (k >> 2)) << 2) + (k & 3);
@@ -82,8 +112,37 @@ __global__ void __launch_bounds__(256) k_gains_enc(const uint32_t *__restrict__ 
             }
         }
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) gains[v] = (int64_t)acc;
+        if (G1)
+            for (int o = 16; o; o >>= 1) acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
+        if (lane == 0) {
+            gains[v] = (int64_t)acc;
+            if (G1) g1[v] = (int64_t)(acc - acc1);
+        }
     }
+}
+
+// the vertex with the most slots (ties: the smallest id) as a packed key
+__global__ void k_hub_degree(const int64_t *__restrict__ xadj, int64_t n, unsigned long long *__restrict__ key) {
+    unsigned long long best = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = ((unsigned long long)(xadj[v + 1] - xadj[v]) << 32) | (0xffffffffull - (uint32_t)v);
+        best = k > best ? k : best;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+        best = x > best ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(key, best);
+}
+// its label in every lane (compressed matrix), the vertex itself in hub_out
+__global__ void k_hub_labels(const uint32_t *__restrict__ L, Lay y, int64_t ld, const unsigned long long *__restrict__ key,
+                             int32_t *__restrict__ hublab, unsigned long long *__restrict__ hub_out) {
+    const uint32_t hub = 0xffffffffu - (uint32_t)(*key & 0xffffffffull);
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < ld; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t w = L[y.off(hub, (int)r)];
+        hublab[r] = (int32_t)(is_root(w) ? hub : w);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *hub_out = hub;
 }
 
 // Gains of one compressed lane tile T[n][tld] (lanes l0.. of the matrix, the
@@ -235,6 +294,7 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
     if (gains_out) IMX_TRY(spec_guard(c));
     if (!c->labels_ready) { set_error("labels not computed (call imx_propagate first)"); return IMX_EINVAL; }
     const int64_t n = c->g->n;
+    c->g1_ready = false;
     IMX_CUDA(cudaEventRecord(c->ev[4], c->st));
     if (n && c->gains_fused && !c->C) {
         // already summed by the tiled compression of the last propagate
@@ -247,7 +307,25 @@ extern "C" int imx_memoize(imx_ctx *c, int64_t *gains_out) {
                 // against 16; C3 0.443 -> 0.430 ms)
                 const char *mg = getenv("IMX_MEMO_BPSM");
                 const int gb = (int)std::min<int64_t>(ceil_div(n * 32, 256), 148 * (mg && atoi(mg) > 0 ? atoi(mg) : 64));
-                k_gains_enc<<<gb, 256, 0, c->st>>>(c->L, n, c->lay, c->ns, c->gains, c->g->m2 ? c->g->xadj : nullptr);
+                // first-seed speculation for the CELF loop of this rank alone
+                const bool spec1 = c->g->m2 > 0 && !c->comm && !getenv("IMX_MEMO_NO_G1");
+                if (spec1) {
+                    if (!c->g1) {
+                        IMX_CUDA(pool_alloc((void **)&c->g1, sizeof(int64_t) * n, c->st));
+                        IMX_CUDA(pool_alloc((void **)&c->hublab, sizeof(int32_t) * c->ld, c->st));
+                    }
+                    IMX_CUDA(cudaMemsetAsync(c->scratch + 14, 0, sizeof(unsigned long long), c->st));
+                    k_hub_degree<<<grid_for(n), 256, 0, c->st>>>(c->g->xadj, n, c->scratch + 14);
+                    k_hub_labels<<<grid_for(c->ld), 256, 0, c->st>>>(c->L, c->lay, c->ld, c->scratch + 14, c->hublab,
+                                                                   c->scratch + 15);
+                    count_launch(c, 2);
+                }
+                if (spec1)
+                    k_gains_enc<true><<<gb, 256, 0, c->st>>>(c->L, n, c->lay, c->ns, c->gains, c->g->xadj, c->hublab, c->g1);
+                else
+                    k_gains_enc<false><<<gb, 256, 0, c->st>>>(c->L, n, c->lay, c->ns, c->gains,
+                                                              c->g->m2 ? c->g->xadj : nullptr, nullptr, nullptr);
+                c->g1_ready = spec1;
             }
         }
         IMX_CHECK_LAUNCH();

@@ -50,7 +50,7 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
        int64_t ld, Lay y, uint32_t *__restrict__ L, unsigned long long *__restrict__ hooks,
        const uint8_t *__restrict__ heavy, const int32_t *__restrict__ hs_v, const int64_t *__restrict__ hs_a,
        const int32_t *__restrict__ hs_len, int64_t nhs, unsigned long long *__restrict__ ctr, int grab,
-       int64_t row0) {
+       int64_t row0, int iso_pass) {
     extern __shared__ int4 smem4[];
     // 16-byte aligned sections (run_scan sizes them): per-warp first-live
     // flags, per-warp union queues (pass 2), the chunk's lane tables
@@ -96,6 +96,14 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                 if (heavy && lane < cntv) hv_l = heavy[row0 + base + lane] != 0;
             }
             const unsigned hmask = __ballot_sync(FULL, hv_l);
+            // isolated rows (no slot at all: 44% of C4's) are all ROOT and nothing
+            // reads them before the compression, so either pass can write them
+            // (iso_pass): pass 2's light launch is latency-bound with HBM bandwidth
+            // to spare while pass 1 is bound by its row stores (C4: 19.5 GB, of which
+            // 7.5 GB isolated) -- unless pass 1 runs hidden behind the upload of a
+            // streamed CSR, where the stores cost nothing
+            const int64_t xa_next = __shfl_down_sync(FULL, xa, 1);      // every lane takes part
+            const unsigned imask = HEAVY ? 0u : __ballot_sync(FULL, lane < cntv && xa == xa_next);
             auto bounds = [&](int k, int64_t &v, int64_t &s0, int64_t &s1) {
                 if (HEAVY) {
                     v = hs_v[base + k];
@@ -137,7 +145,8 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                     bounds(k, v, s0, s1);
                     batch(s0, s1, v, bu0, bh0);
                 }
-                if (PASS == 1 && !HEAVY) {                 // the row starts as all roots
+                // the row starts as all roots (an isolated one: in pass 2)
+                if (!HEAVY && (((imask >> k) & 1u) ? PASS == iso_pass : PASS == 1)) {
                     for (int q = lane; q < (rwc >> 2); q += 32)
                         *reinterpret_cast<uint4 *>(L + y.off(v, r0 + 4 * q)) = make_uint4(ROOT, ROOT, ROOT, ROOT);
                 }
@@ -343,6 +352,12 @@ static int scan_heavy_T() {
     return e ? std::max(0, atoi(e)) : 256;
 }
 
+// the pass that writes the isolated rows of a resident graph (IMX_SCAN_ISO_PASS, default 2)
+static int scan_iso_pass() {
+    const char *e = getenv("IMX_SCAN_ISO_PASS");
+    return e && atoi(e) == 1 ? 1 : 2;
+}
+
 static int scan_bpsm() {
     const char *e = getenv("IMX_SCAN_BPSM");
     return e && atoi(e) > 0 ? atoi(e) : 8;
@@ -351,7 +366,7 @@ static int scan_bpsm() {
 using ScanKernel = void (*)(const int64_t *, const int32_t *, const int32_t *, int32_t, int, int, int, int,
                             const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, Lay, uint32_t *,
                             unsigned long long *, const uint8_t *, const int32_t *, const int64_t *, const int32_t *,
-                            int64_t, unsigned long long *, int, int64_t);
+                            int64_t, unsigned long long *, int, int64_t, int);
 static const ScanKernel kScanKernels[2][2] = {{k_scan<1, false>, k_scan<1, true>}, {k_scan<2, false>, k_scan<2, true>}};
 
 // one launch: the light rows [row0, row0 + rows) (heavy = false), or all heavy slices
@@ -375,7 +390,8 @@ static int launch_scan(imx_ctx *c, int pass, bool heavy, int64_t row0, int64_t r
     kern<<<blocks, kScanWarps * 32, smem, c->st>>>(g->xadj, g->adj, g->hash, g->thr_u, c->scan_kb, nb, cw,
                                                    c->scan_nchunks, c->scan_xs, c->scan_perm, c->scan_boff, rows,
                                                    c->W, c->ld, c->lay, c->L, pass == 2 ? hooks : nullptr,
-                                                   H.heavy, H.hs_v, H.hs_a, H.hs_len, H.nhs, c->scan_ctr, grab, row0);
+                                                   H.heavy, H.hs_v, H.hs_a, H.hs_len, H.nhs, c->scan_ctr, grab, row0,
+                                                   c->scan_iso_pass);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;
@@ -388,6 +404,7 @@ int run_scan(imx_ctx *c, int pass, unsigned long long *hooks) {
     IMX_TRY(ensure_scan_tables(c));
     const int T = scan_heavy_T();
     IMX_TRY(ensure_heavy(c, 1, T));
+    if (pass == 1) c->scan_iso_pass = scan_iso_pass();
     IMX_TRY(launch_scan(c, pass, false, 0, n, hooks));
     if (g->hv[0].nhs > 0) IMX_TRY(launch_scan(c, pass, true, 0, n, hooks));
     return IMX_OK;
@@ -404,6 +421,7 @@ int run_scan_streamed(imx_ctx *c) {
     const int64_t n = g->n;
     IMX_TRY(ensure_scan_tables(c));
     const int T = scan_heavy_T();
+    c->scan_iso_pass = 1;            // hidden behind the upload
     IMX_TRY(heavy_begin(c, 1, T));
     for (int ch = 0; ch < g->nchunk; ++ch) {
         const int64_t v0 = g->chunk_row[ch], v1 = g->chunk_row[ch + 1];

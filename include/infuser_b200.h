@@ -62,7 +62,15 @@ int64_t imx_launch_count(void);
 int  imx_graph_from_edges(int32_t device, int64_t n, const int64_t *edges,
                           int64_t k, const double *w_edge, double w_scalar,
                           imx_graph **out);
-/* Upload an existing CSR (Graph(xadj, adj, weights, orig_ids), graph.py:37). */
+/* Upload an existing CSR (Graph(xadj, adj, weights, orig_ids), graph.py:37).
+ * Large graphs (>= 4 M slots) leave the weights on the link when the call
+ * returns, very large ones in pinned host memory (>= 16 M slots) also the
+ * adjacency: the caller's arrays must stay valid and unchanged until the
+ * first result of the graph has been read back (or the graph is destroyed).
+ * What the eager build reports for a bad CSR ("corrupt CSR offsets",
+ * "adjacency entry outside 0..n-1", "adjacency is not symmetric") then
+ * surfaces from the first call that needs the structure (imx_propagate,
+ * imx_graph_get_csr, ...); the offsets are always checked before return.    */
 int  imx_graph_from_csr(int32_t device, int64_t n, int64_t m2,
                         const int64_t *xadj, const int32_t *adj,
                         const double *weights, imx_graph **out);

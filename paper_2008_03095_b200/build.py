@@ -21,15 +21,26 @@ NVCC_FLAGS = [
 ]
 
 
+def _code_only(text: str) -> str:
+    """C/C++ source without comments and with whitespace runs collapsed, so
+    that documentation edits do not change the stamp (string literals are kept
+    as they are)."""
+    import re
+    pat = re.compile(r'"(?:\\.|[^"\\])*"|\'(?:\\.|[^\'\\])*\'|//[^\n]*|/\*.*?\*/', re.S)
+    text = pat.sub(lambda m: m.group(0) if m.group(0)[0] in "\"'" else " ", text)
+    return " ".join(text.split())
+
+
 def source_hash() -> str:
-    """sha256 (16 hex) over the library's sources, headers and flags: stamps
-    the ncu summaries under profiles/ so bench.py can refuse a stale one
-    (the GPU box has no git history)."""
+    """sha256 (16 hex) over the library's sources and headers (code only:
+    comments and layout do not count) and the compiler flags: stamps the ncu
+    summaries under profiles/ so bench.py can refuse a stale one (the GPU box
+    has no git history)."""
     import hashlib
     h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
     for p in sorted(SOURCES + HEADERS, key=lambda q: q.name):
         h.update(p.name.encode())
-        h.update(p.read_bytes())
+        h.update(_code_only(p.read_text()).encode())
     return h.hexdigest()[:16]
 
 

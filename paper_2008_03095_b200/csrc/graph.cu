@@ -913,24 +913,33 @@ static int graph_analyze_streamed(imx_graph *g, const int64_t *xadj_h, const int
     // offsets first: everything below indexes with them
     IMX_CUDA(cudaMemcpyAsync(g->xadj, xadj_h, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, g->ust));
     IMX_CUDA(cudaEventRecord(ev, g->ust));
-    // chunks of about equal slot counts, cut at row boundaries (host offsets);
-    // the last one in quarters: what follows the final chunk's arrival (its
-    // structure kernels, its share of the sampler's first pass) is not hidden
-    // behind the link any more, and on skewed graphs the highest ids hold the
-    // most rows per slot (C4: the last sixteenth took 1.2 ms of pass 1)
+    // chunks of about equal slot counts, cut at row boundaries (host offsets)
     int want = 16;
-    if (const char *e = getenv("IMX_STREAM_CHUNKS")) want = std::max(1, std::min((int)imx_graph::kMaxChunks - 3, atoi(e)));
+    if (const char *e = getenv("IMX_STREAM_CHUNKS")) want = std::max(1, std::min((int)imx_graph::kMaxChunks, atoi(e)));
     g->nchunk = 0;
     g->chunk_row[0] = 0;
-    auto cut = [&](int64_t slot, bool last) {
-        int64_t v = last ? n : std::upper_bound(xadj_h, xadj_h + n + 1, slot) - xadj_h - 1;
+    for (int c = 1; c <= want; ++c) {
+        int64_t v = c == want ? n : std::upper_bound(xadj_h, xadj_h + n + 1, m2 / want * c) - xadj_h - 1;
         v = std::min(std::max(v, g->chunk_row[g->nchunk]), n);
-        if (v > g->chunk_row[g->nchunk] || last) g->chunk_row[++g->nchunk] = v;
-    };
-    for (int c = 1; c < want; ++c) cut(m2 / want * c, false);
-    for (int q = 1; q <= 4; ++q) cut(m2 / want * (want - 1) + (m2 - m2 / want * (want - 1)) * q / 4, q == 4);
+        if (v > g->chunk_row[g->nchunk] || c == want) g->chunk_row[++g->nchunk] = v;
+    }
+    // Upload order: the chunks of the highest ids first.  Pass 1 of a chunk
+    // writes only that chunk's rows, so any order is valid, and on skewed
+    // graphs the high ids hold many low-degree rows -- row stores that outlast
+    // their slots' upload (C4: the last sixteenth of the slots took 1.5 ms of
+    // pass 1 against 0.6 ms on the link) -- while the hub chunks are all slots
+    // and few rows: with the hubs last, almost nothing is left when the link
+    // goes quiet.  chunk_row[] / chunk_ev[] are kept in upload order.
+    {
+        int64_t rows[imx_graph::kMaxChunks + 1];
+        for (int c = 0; c <= g->nchunk; ++c) rows[c] = g->chunk_row[c];
+        for (int c = 0; c < g->nchunk; ++c) {
+            g->chunk_lo[c] = rows[g->nchunk - 1 - c];
+            g->chunk_hi[c] = rows[g->nchunk - c];
+        }
+    }
     for (int c = 0; c < g->nchunk; ++c) {
-        const int64_t s0 = xadj_h[g->chunk_row[c]], s1 = xadj_h[g->chunk_row[c + 1]];
+        const int64_t s0 = xadj_h[g->chunk_lo[c]], s1 = xadj_h[g->chunk_hi[c]];
         if (s0 < 0 || s1 > m2 || s0 > s1) { cudaEventDestroy(ev); set_error("corrupt CSR offsets"); return IMX_EINVAL; }
         if (s1 > s0)
             IMX_CUDA(cudaMemcpyAsync(g->adj + s0, adj_h + s0, sizeof(int32_t) * (s1 - s0), cudaMemcpyHostToDevice, g->ust));
@@ -949,7 +958,7 @@ static int graph_analyze_streamed(imx_graph *g, const int64_t *xadj_h, const int
     if (xflags & 64u) { set_error("corrupt CSR offsets"); return IMX_EINVAL; }
     IMX_TRY(graph_nz_rows_async(g, gs));
     for (int c = 0; c < g->nchunk; ++c) {
-        const int64_t v0 = g->chunk_row[c], v1 = g->chunk_row[c + 1];
+        const int64_t v0 = g->chunk_lo[c], v1 = g->chunk_hi[c];
         const int64_t s0 = xadj_h[v0], s1 = xadj_h[v1];
         IMX_CUDA(cudaStreamWaitEvent(st, g->chunk_ev[c], 0));
         if (s1 > s0) {

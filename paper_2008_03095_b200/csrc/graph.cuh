@@ -67,7 +67,8 @@ struct imx_graph {
     cudaStream_t ust = nullptr;
     static constexpr int kMaxChunks = 32;
     int nchunk = 0;
-    int64_t chunk_row[kMaxChunks + 1] = {0};
+    int64_t chunk_row[kMaxChunks + 1] = {0};       // row cuts, ascending
+    int64_t chunk_lo[kMaxChunks] = {0}, chunk_hi[kMaxChunks] = {0};   // rows of chunk c in upload order
     cudaEvent_t chunk_ev[kMaxChunks] = {nullptr};
     cudaEvent_t sev_done = nullptr;
     void *sstats_d = nullptr, *sstats_h = nullptr;   // GStats (device, pinned host)

@@ -424,7 +424,7 @@ int run_scan_streamed(imx_ctx *c) {
     c->scan_iso_pass = 1;            // hidden behind the upload
     IMX_TRY(heavy_begin(c, 1, T));
     for (int ch = 0; ch < g->nchunk; ++ch) {
-        const int64_t v0 = g->chunk_row[ch], v1 = g->chunk_row[ch + 1];
+        const int64_t v0 = g->chunk_lo[ch], v1 = g->chunk_hi[ch];
         IMX_CUDA(cudaStreamWaitEvent(c->st, g->chunk_ev[ch], 0));
         if (v1 <= v0) continue;
         IMX_TRY(heavy_count_rows(c, 1, T, v0, v1));

@@ -126,6 +126,7 @@ struct imx_ctx {
     int32_t *scan_boff = nullptr;
     unsigned long long *scan_ctr = nullptr;   // [scan_nchunks] work counters of one launch
     int scan_kb = -1, scan_nb = 0, scan_cw = 0, scan_nchunks = 0;
+    int scan_heavy_forest = 1;        // heavy rows got their forest edge in pass 1 (pass 2 skips it)
     int scan_iso_pass = 2;            // the pass of the current propagate that writes the isolated rows
     // misc
     unsigned long long *scratch = nullptr;  // [16]: per-call counters (4 label sum, 6 bad labels, 7 commit gain, 9 max prio, 13 bad prio, 14 hub degree key, 15 hub)

@@ -22,9 +22,10 @@
 // neighbour (the forest edge) is united through a per-warp shared-memory
 // queue (uf.cuh unite), 32 unions at a time.
 // Heavy rows (prefix > T slots) are cut into slices of T slots, one warp
-// each: pass 1 folds the slice's first live neighbours into the row with
-// atomicMin (the light pass wrote the row as ROOT), pass 2 unites every live
-// neighbour except the one the row points at.
+// each.  Pass 1 leaves them all ROOT (the light pass writes the row) and pass 2
+// unites every live neighbour; optionally (IMX_SCAN_HEAVY_P1) pass 1 folds the
+// slices' first live neighbours into the row with atomicMin and pass 2 skips
+// the neighbour the row points at.
 //
 // Correctness does not depend on the buckets: a bucket is a superset of the
 // live lanes and every candidate is re-tested exactly.
@@ -50,7 +51,7 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
        int64_t ld, Lay y, uint32_t *__restrict__ L, unsigned long long *__restrict__ hooks,
        const uint8_t *__restrict__ heavy, const int32_t *__restrict__ hs_v, const int64_t *__restrict__ hs_a,
        const int32_t *__restrict__ hs_len, int64_t nhs, unsigned long long *__restrict__ ctr, int grab,
-       int64_t row0, int iso_pass) {
+       int64_t row0, int iso_pass, int heavy_forest) {
     extern __shared__ int4 smem4[];
     // 16-byte aligned sections (run_scan sizes them): per-warp first-live
     // flags, per-warp union queues (pass 2), the chunk's lane tables
@@ -192,7 +193,8 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                                         atomicMin(L + y.off(v, r0 + p), u);
                                     }
                                 } else {
-                                    const bool un = live && ld_relaxed(L + y.off(v, r0 + p)) != u;
+                                    // all but the forest edge of heavy pass 1 -- or all, when that pass was skipped
+                                    const bool un = live && (!heavy_forest || ld_relaxed(L + y.off(v, r0 + p)) != u);
                                     const unsigned b = __ballot_sync(FULL, un);
                                     if (b) {
                                         if (un) {
@@ -240,7 +242,7 @@ k_scan(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj, const 
                                 bool un = false;
                                 if (live) {
                                     if (HEAVY) {
-                                        un = ld_relaxed(L + y.off(v, r0 + p)) != u;   // all but the forest edge
+                                        un = !heavy_forest || ld_relaxed(L + y.off(v, r0 + p)) != u;   // all but the forest edge
                                     } else {
                                         un = flag[p] != 0;              // all but the first live neighbour
                                         flag[p] = 1;
@@ -358,6 +360,18 @@ static int scan_iso_pass() {
     return e && atoi(e) == 1 ? 1 : 2;
 }
 
+// Heavy rows' pass 1 (the slices' first live neighbours folded into the row
+// by atomicMin, so that pass 2 can skip one union per row and lane) is off by
+// default: a heavy row has many live neighbours per lane (C4's hubs: ~250),
+// so the forest edge spares pass 2 well under 1% of its unions while the
+// slices' pass 1 costs a full walk of every heavy prefix (C4: 0.92 ms;
+// propagate 17.3 -> 16.25 ms without it).  Pass 2 then unites every live pair
+// of a heavy row.  IMX_SCAN_HEAVY_P1=1 brings it back.
+static int scan_heavy_forest() {
+    const char *e = getenv("IMX_SCAN_HEAVY_P1");
+    return e ? (atoi(e) != 0) : 0;
+}
+
 static int scan_bpsm() {
     const char *e = getenv("IMX_SCAN_BPSM");
     return e && atoi(e) > 0 ? atoi(e) : 8;
@@ -366,7 +380,7 @@ static int scan_bpsm() {
 using ScanKernel = void (*)(const int64_t *, const int32_t *, const int32_t *, int32_t, int, int, int, int,
                             const int32_t *, const uint16_t *, const int32_t *, int64_t, int32_t, int64_t, Lay, uint32_t *,
                             unsigned long long *, const uint8_t *, const int32_t *, const int64_t *, const int32_t *,
-                            int64_t, unsigned long long *, int, int64_t, int);
+                            int64_t, unsigned long long *, int, int64_t, int, int);
 static const ScanKernel kScanKernels[2][2] = {{k_scan<1, false>, k_scan<1, true>}, {k_scan<2, false>, k_scan<2, true>}};
 
 // one launch: the light rows [row0, row0 + rows) (heavy = false), or all heavy slices
@@ -391,7 +405,7 @@ static int launch_scan(imx_ctx *c, int pass, bool heavy, int64_t row0, int64_t r
                                                    c->scan_nchunks, c->scan_xs, c->scan_perm, c->scan_boff, rows,
                                                    c->W, c->ld, c->lay, c->L, pass == 2 ? hooks : nullptr,
                                                    H.heavy, H.hs_v, H.hs_a, H.hs_len, H.nhs, c->scan_ctr, grab, row0,
-                                                   c->scan_iso_pass);
+                                                   c->scan_iso_pass, c->scan_heavy_forest);
     IMX_CHECK_LAUNCH();
     count_launch(c);
     return IMX_OK;
@@ -404,9 +418,12 @@ int run_scan(imx_ctx *c, int pass, unsigned long long *hooks) {
     IMX_TRY(ensure_scan_tables(c));
     const int T = scan_heavy_T();
     IMX_TRY(ensure_heavy(c, 1, T));
-    if (pass == 1) c->scan_iso_pass = scan_iso_pass();
+    if (pass == 1) {
+        c->scan_iso_pass = scan_iso_pass();
+        c->scan_heavy_forest = scan_heavy_forest();
+    }
     IMX_TRY(launch_scan(c, pass, false, 0, n, hooks));
-    if (g->hv[0].nhs > 0) IMX_TRY(launch_scan(c, pass, true, 0, n, hooks));
+    if (g->hv[0].nhs > 0 && (pass == 2 || c->scan_heavy_forest)) IMX_TRY(launch_scan(c, pass, true, 0, n, hooks));
     return IMX_OK;
 }
 
@@ -422,6 +439,7 @@ int run_scan_streamed(imx_ctx *c) {
     IMX_TRY(ensure_scan_tables(c));
     const int T = scan_heavy_T();
     c->scan_iso_pass = 1;            // hidden behind the upload
+    c->scan_heavy_forest = scan_heavy_forest();
     IMX_TRY(heavy_begin(c, 1, T));
     for (int ch = 0; ch < g->nchunk; ++ch) {
         const int64_t v0 = g->chunk_lo[ch], v1 = g->chunk_hi[ch];
@@ -433,7 +451,7 @@ int run_scan_streamed(imx_ctx *c) {
     const int rc = graph_settle_structure(g);
     if (rc != IMX_OK) { heavy_abort(c, 1); return rc; }
     IMX_TRY(heavy_finish(c, 1, T));
-    if (g->hv[0].nhs > 0) IMX_TRY(launch_scan(c, 1, true, 0, n, nullptr));
+    if (g->hv[0].nhs > 0 && c->scan_heavy_forest) IMX_TRY(launch_scan(c, 1, true, 0, n, nullptr));
     (void)n;
     return IMX_OK;
 }

@@ -346,12 +346,16 @@ static int ensure_scan_tables(imx_ctx *c) {
     return IMX_OK;
 }
 
-// slice length of heavy rows (IMX_SCAN_HEAVY, default 256 slots): C4 18.7 /
-// 18.0 / 18.7 / 21.7 ms at 128 / 256 / 512 / 1024 (four slots per warp step
-// make slices cheap; shorter ones add per-slice flag and atomic work)
+// slice length of heavy rows (IMX_SCAN_HEAVY, default 64 slots).  With the
+// forest edge of heavy rows (pass 1 over the slices): C4 18.7 / 18.0 / 18.7 /
+// 21.7 ms at 128 / 256 / 512 / 1024.  Without it (the default now) shorter
+// slices win -- the order-free slice walk (four slots per warp step) beats the
+// light rows' slot-by-slot walk with its first-live flags: C4 21.0 / 17.0 /
+// 15.9 / 15.5 / 15.7 / 16.3 / 17.6 ms at 16 / 32 / 48 / 64 / 128 / 256 / 512;
+// C2 0.221 / 0.181 ms at 32 / 64 (no heavy row at 64); C5 unchanged.
 static int scan_heavy_T() {
     const char *e = getenv("IMX_SCAN_HEAVY");
-    return e ? std::max(0, atoi(e)) : 256;
+    return e ? std::max(0, atoi(e)) : 64;
 }
 
 // the pass that writes the isolated rows of a resident graph (IMX_SCAN_ISO_PASS, default 2)

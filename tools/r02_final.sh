@@ -26,9 +26,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
     python bench.py --steps 2 --warmup 1 --parity off --no-cpu-baseline --e2e-steps 1 > $O/launches_c4_bench.log 2>&1
 echo "launch list rc=$?"
 # 4. --set full of the two longest C4 kernels (R = 256 lanes so that kernel replay can save the matrix);
-#    ncu matches the function name without template arguments: k_scan<2, true> is the 8th k_scan launch
-#    of the driver (warm-up propagate + one measured: <1,false> <1,true> <2,false> <2,true> each)
-for spec in "k_compress 1 k_compress" "k_scan 7 k_scan2true"; do
+#    ncu matches the function name without template arguments: k_scan<2, true> is the 6th k_scan launch
+#    of the driver (warm-up propagate + one measured: <1,false> <2,false> <2,true> each; the heavy pass 1 is off)
+for spec in "k_compress 1 k_compress" "k_scan 5 k_scan2true"; do
   set -- $spec
   timeout 900 ncu --set full --clock-control none --import-source on -k $1 --launch-skip $2 --launch-count 1 \
       -o $O/full_c4_$3 -f python tools/ncu_driver.py c4 1 256 > $O/full_c4_$3.log 2>&1

@@ -325,6 +325,22 @@ __global__ void k_thresholds(const double *__restrict__ w, const int64_t *__rest
     }
 }
 
+// flag 256: some weight's bit pattern differs from w0's (the deferred graph's
+// whole check when the weights are uniform: 8 bytes read per slot instead of
+// the 28 read and written by k_thresholds)
+__global__ void k_weights_same(const double *__restrict__ w, int64_t m2, unsigned long long w0,
+                               unsigned *__restrict__ flags) {
+    bool diff = false;
+    const unsigned long long *wb = reinterpret_cast<const unsigned long long *>(w);
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m2; s += (int64_t)gridDim.x * blockDim.x)
+        diff |= wb[s] != w0;
+    if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) atomicOr(flags, 256u);
+}
+__global__ void k_fill_i32(int32_t *__restrict__ a, int64_t cnt, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = v;
+}
+
 __global__ void k_reciprocal(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                              const int32_t *__restrict__ src, const double *__restrict__ w, int64_t n,
                              int64_t m2, int64_t *__restrict__ recip, int32_t *__restrict__ thr,
@@ -590,6 +606,7 @@ void graph_free(imx_graph *g) {
 // (the reference's index sweep, propagation.py:104-163, on the device).
 // Stream-ordered, no host synchronisation.
 static int graph_build_index(imx_graph *g) {
+    IMX_TRY(ensure_thr(g));
     cudaStream_t st = g->stream;
     const int64_t me = g->me;
     const int nb = g->uniform ? 1 : (int)std::min<int64_t>(64, std::max<int64_t>(1, me));
@@ -786,6 +803,7 @@ static int graph_analyze(imx_graph *g, bool structure, const std::function<int()
     g->thr_u = m2 ? h.tmin : 0;
     g->thr_mean = g->me ? (double)h.tsum / (double)g->me / 2147483647.0 : 0.0;
     g->index_ready = false;          // built on first use (ensure_index)
+    g->thr_ready = true;
     return IMX_OK;
 }
 
@@ -806,10 +824,14 @@ static int deferred_weights_start(imx_graph *g, const double *weights) {
     cudaEventDestroy(ev_struct);
     GStats *wd = static_cast<GStats *>(g->wstats_d);
     GStats *wh = static_cast<GStats *>(g->wstats_h);
-    auto finish = [g, m2, wd, wh]() -> int {
+    unsigned long long w0_bits;
+    memcpy(&w0_bits, weights, sizeof w0_bits);
+    auto finish = [g, m2, wd, wh, w0_bits]() -> int {
         cudaStream_t ws = g->wst;
         k_stats_init<<<1, 1, 0, ws>>>(wd);
-        k_thresholds<<<grid_for(m2), 256, 0, ws>>>(g->w, nullptr, g->src, g->adj, g->hash, m2, g->thr, wd);
+        // uniform weights (the speculation) need no per-slot pass: only the proof that
+        // every weight is weights[0]; anything else is settled by graph_settle
+        k_weights_same<<<grid_for(m2), 256, 0, ws>>>(g->w, m2, w0_bits, &wd->flags);
         note_launch(2);
         IMX_CHECK_LAUNCH();
         IMX_CUDA(cudaMemcpyAsync(wh, wd, sizeof(GStats), cudaMemcpyDeviceToHost, ws));
@@ -1056,14 +1078,21 @@ int graph_settle(imx_graph *g) {
     g->wstats_d = nullptr;
     if (struct_rc != IMX_OK) return struct_rc;
     if (rc != IMX_OK) return rc;
-    if (g->m2 && h.tmin != h.tmax && g->symmetric) {
+    if (g->m2 && !(h.flags & 256u)) {
+        // every weight is weights[0]: the speculative threshold is the threshold
+        // of every slot; the per-slot array is filled when something reads it
+        h.flags = 0;
+        h.tmin = h.tmax = g->thr_u;
+        h.tsum = (unsigned long long)(uint32_t)g->thr_u * (unsigned long long)g->me;
+        g->thr_ready = false;
+    } else if (g->m2) {
         // per-slot thresholds: symmetrized through the reciprocal slots
-        IMX_TRY(ensure_recip(g));
+        if (g->symmetric) IMX_TRY(ensure_recip(g));
         GStats *gs;
         IMX_CUDA(pool_alloc((void **)&gs, sizeof(GStats), g->stream));
         k_stats_init<<<1, 1, 0, g->stream>>>(gs);
-        k_thresholds<<<grid_for(g->m2), 256, 0, g->stream>>>(g->w, g->recip, g->src, g->adj, g->hash, g->m2,
-                                                             g->thr, gs);
+        k_thresholds<<<grid_for(g->m2), 256, 0, g->stream>>>(g->w, g->symmetric ? g->recip : nullptr, g->src, g->adj,
+                                                             g->hash, g->m2, g->thr, gs);
         note_launch(2);
         IMX_CHECK_LAUNCH();
         IMX_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, g->stream));
@@ -1075,6 +1104,18 @@ int graph_settle(imx_graph *g) {
     g->thr_u = g->m2 ? h.tmin : 0;
     g->thr_mean = g->me ? (double)h.tsum / (double)g->me / 2147483647.0 : 0.0;
     g->index_ready = false;
+    return IMX_OK;
+}
+
+int ensure_thr(imx_graph *g) {
+    if (g->thr_ready) return IMX_OK;
+    if (g->m2) {
+        k_fill_i32<<<grid_for(g->m2), 256, 0, g->stream>>>(g->thr, g->m2, g->thr_u);
+        note_launch();
+        IMX_CHECK_LAUNCH();
+        IMX_CUDA(cudaStreamSynchronize(g->stream));   // its readers run on other streams
+    }
+    g->thr_ready = true;
     return IMX_OK;
 }
 
@@ -1489,6 +1530,7 @@ extern "C" int imx_graph_thresholds(imx_graph *g, int32_t symmetrize, int32_t *t
     if (symmetrize && !g->symmetric) { set_error("adjacency is not symmetric"); return IMX_EFORMAT; }
     if (g->m2) {
         if (symmetrize) {
+            IMX_TRY(ensure_thr(g));
             IMX_CUDA(cudaMemcpyAsync(thr_out, g->thr, sizeof(int32_t) * g->m2, cudaMemcpyDeviceToHost, st));
         } else {
             int32_t *tmp;

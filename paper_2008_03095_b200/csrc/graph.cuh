@@ -74,6 +74,9 @@ struct imx_graph {
     void *sstats_d = nullptr, *sstats_h = nullptr;   // GStats (device, pinned host)
     bool recip_ready = true;
     bool index_ready = false;
+    // false: the thresholds are uniform (thr_u) and the per-slot array is filled on first use
+    // (ensure_thr): a deferred graph only checks that every weight equals weights[0]
+    bool thr_ready = true;
     bool cslot_ready = true;     // false: cslot built on first use (ensure_cslot)
     // non-isolated vertices (built on first use, ensure_nz_rows); NULL when
     // isolated vertices are too few to be worth skipping
@@ -104,6 +107,7 @@ int graph_settle(imx_graph *g);
 // the streamed structure is complete and valid (waits for the chunk uploads)
 int graph_settle_structure(imx_graph *g);
 int ensure_recip(imx_graph *g);
+int ensure_thr(imx_graph *g);
 int ensure_index(imx_graph *g);
 int ensure_nz_rows(imx_graph *g);
 int ensure_cslot(imx_graph *g);

@@ -955,6 +955,7 @@ static int run_pull(imx_ctx *c, int pass, unsigned long long *hooks) {
     imx_graph *g = c->g;
     const int64_t n = g->n;
     if (n == 0) return IMX_OK;
+    IMX_TRY(ensure_thr(g));
     // pass 1 (atomicMin per slice and lane) prefers longer slices than
     // pass 2 (unions per slice): its table uses IMX_PULL_HEAVY1 (3) x T slots
     // (C3 pass 1 0.94 -> 0.83 ms)

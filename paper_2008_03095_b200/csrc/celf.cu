@@ -1467,6 +1467,12 @@ static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<in
         // the records (C4 round 1: 2.3 M, 91 MB) go to the host on the side
         // stream while the next rounds run; rec is freed there after the copy
         if (!c->tst) GB(acquire_stream(c->dev, &c->tst));
+        // the commit's gain is read back BEFORE the side stream is released: both copies
+        // become ready behind k_merge, and when the 91 MB of records reached the one
+        // device-to-host copy engine first, these 8 bytes (and the host) waited 1.7 ms
+        // for them -- two runs in three on C4
+        unsigned long long got = 0;
+        GB(cudaMemcpyAsync(&got, gain, sizeof got, cudaMemcpyDeviceToHost, st));
         {
             cudaEvent_t ev;
             GB(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1477,8 +1483,6 @@ static int celf_big_round(imx_ctx *c, int32_t t, int64_t &batch0, std::vector<in
         GB(cudaMemcpyAsync(c->trace + base, rec, sizeof(int64_t) * 5 * (kr + 1), cudaMemcpyDeviceToHost, c->tst));
         GB(cudaFreeAsync(rec, c->tst));
         rec = nullptr;
-        unsigned long long got = 0;
-        GB(cudaMemcpyAsync(&got, gain, sizeof got, cudaMemcpyDeviceToHost, st));
         GB(cudaStreamSynchronize(st));
         if (partial_gain) {
             *partial_gain = (int64_t)got;       // one rank's part: checked after the next exchange

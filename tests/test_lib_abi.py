@@ -75,3 +75,19 @@ def test_header_is_plain_c(tmp_path):
                           "-o", str(tmp_path / "abi"), str(lib), f"-Wl,-rpath,{lib.parent}"],
                          capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
+
+
+def test_source_stamp_ignores_comments_and_layout():
+    """The stamp that ties the ncu summaries under profiles/ to the library
+    code (build.source_hash) hashes code only: comments and whitespace do not
+    invalidate a measurement, string literals and code do."""
+    from paper_2008_03095_b200 import build
+    a = 'int f(int x) { // add\n  return x + 1; /* one\n more */ }\nconst char *s = "// kept /* too */";\n'
+    b = 'int f(int x) {\n\n   return x + 1;   }\n  const char *s = "// kept /* too */";'
+    c = b.replace("x + 1", "x + 2")
+    d = b.replace("// kept", "// changed")
+    assert build._code_only(a) == build._code_only(b)
+    assert build._code_only(c) != build._code_only(b)
+    assert build._code_only(d) != build._code_only(b)
+    h = build.source_hash()
+    assert len(h) == 16 and int(h, 16) >= 0

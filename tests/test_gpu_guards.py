@@ -286,3 +286,39 @@ def test_wide_tab_round_forced(gpu, name, monkeypatch):
     assert run.selection.gains == z["seed_gains"].tolist()
     assert np.array_equal(run.selection.trace.array, z["trace"])
     assert run.spread_se == pytest.approx(float(z["spread_se"]), rel=1e-12, abs=1e-15)
+
+
+def test_deferred_speculation_guard_refuses_unconfirmed_results(gpu, orc, monkeypatch):
+    """imx_spec_defer hands the check of the speculative threshold to the
+    caller; a caller that forgets it still cannot read unconfirmed results:
+    the getters settle the weights themselves and fail when the speculation
+    did not hold, and a second propagate (on the settled thresholds) gives
+    the oracle's labels."""
+    monkeypatch.setenv("IMX_LATE_WEIGHTS", "1")
+    z = load_golden("er_big_1000")
+    xadj, adj, _ = orc.csr_from_edges(int(z["n"]), z["edges"].astype(np.int64))
+    w = np.full(len(adj), 0.05)
+    rec = orc.reciprocal(xadj, adj)
+    w[[-1, rec[-1]]] = 0.6                       # weights[0]'s threshold is not every slot's
+    g = _deferred_graph(gpu, xadj, adj, w, pinned=True)
+    from paper_2008_03095_b200.context import DeviceContext
+    X = gpu.SimulationRandoms(40, 2).values
+    ctx = DeviceContext(g, X, 40)
+    ctx.spec_defer(True)
+    ctx.propagate()
+    with pytest.raises(ValueError, match="speculative"):      # IMX_EINVAL, like "labels not computed"
+        ctx.labels()
+    assert ctx.spec_settle() is True             # settled by the guard; nothing pending any more
+    ctx.propagate()
+    want = orc.run_fused(xadj, adj, w, 5, 40, 2, nthreads=4)
+    assert np.array_equal(ctx.labels()[:, :40], want["labels"][:, :40])
+    # and the explicit protocol: settle says no, propagate again
+    g2 = _deferred_graph(gpu, xadj, adj, w, pinned=True)
+    ctx2 = DeviceContext(g2, X, 40)
+    ctx2.spec_defer(True)
+    ctx2.propagate()
+    assert ctx2.spec_settle() is False
+    ctx2.propagate()
+    assert np.array_equal(ctx2.labels()[:, :40], want["labels"][:, :40])
+    ctx.close()
+    ctx2.close()
